@@ -1,0 +1,134 @@
+/*
+ * stable_b200.h — C ABI of the B200 (sm_100a) hot path of STABLE's AUTO metric:
+ * exhaustive AUTO top-k, HELP graph construction and Dynamic Heterogeneity Routing.
+ *
+ * The reference (hybridann 0.1.0, pure Python + Numba) reaches its hot path only through
+ * module-attribute calls `_kernels.<fn>(...)` on C-contiguous NumPy buffers
+ * (graph.py:13, router.py:15).  Each entry point below replaces one of those functions, or a
+ * Python loop around them, with the same argument meaning; the binding a maintainer adds on
+ * the reference side is a ctypes stub.
+ *
+ * Conventions
+ *   - plain pointers + sizes, no C++ or torch types; host buffers unless the name ends in
+ *     _dev (device pointers, asynchronous on the handle's stream).
+ *   - every call returns SB_OK or an error code and never throws; sb_last_error() gives a
+ *     thread-local message.  Codes map onto the reference's exception taxonomy
+ *     (errors.py:8-31, exit codes cli.py:353-361):
+ *       SB_EARG -> ValueError, SB_EFORMAT -> FormatError, SB_ECONSTRAINT -> ConstraintError,
+ *       SB_ECUDA -> a device failure (no reference counterpart; raised as RuntimeError).
+ *   - layouts as the reference passes them (_kernels.py:1-6, graph.py:64-72):
+ *       features f32[n*m], attrs i32[n*l], nbr_ids i32[n*gamma], nbr_dists f32[n*gamma],
+ *       nbr_flags u8[n*gamma], nbr_counts i32[n].
+ *   - one CUDA stream per handle: calls on one handle serialise; distinct handles may run
+ *     concurrently.
+ */
+#ifndef STABLE_B200_H
+#define STABLE_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum { SB_OK = 0, SB_EARG = 1, SB_EFORMAT = 2, SB_ECONSTRAINT = 3, SB_ECUDA = 4 };
+
+typedef struct sb_index sb_index;
+
+const char* sb_last_error(void);
+int sb_version(void);                 /* (major << 16) | minor */
+int sb_device_count(int* count);
+
+/* ---- handle ----------------------------------------------------------------------
+ * Uploads the dataset (RelationGraph.features / .attrs, graph.py:64-65) and reserves an
+ * adjacency of capacity gamma (graph.py:69-72).  Replaces nothing by itself: the reference
+ * keeps these arrays on the Python object and re-passes them to every kernel. */
+int sb_index_create(const float* features, const int32_t* attrs, int64_t n, int32_t m,
+                    int32_t l, int32_t gamma, sb_index** out);
+int sb_index_destroy(sb_index* idx);
+int sb_set_stream(sb_index* idx, void* cuda_stream);   /* NULL: the handle's own stream */
+int sb_synchronize(sb_index* idx);
+/* nbr_flags may be NULL (frozen graphs carry none, graph.py:231) */
+int sb_adj_upload(sb_index* idx, const int32_t* nbr_ids, const float* nbr_dists,
+                  const int32_t* nbr_counts, const uint8_t* nbr_flags);
+int sb_adj_download(sb_index* idx, int32_t* nbr_ids, float* nbr_dists, int32_t* nbr_counts,
+                    uint8_t* nbr_flags);
+
+/* ---- HELP construction ----------------------------------------------------------- */
+
+/* compute_row_distances (_kernels.py:71-78) + the per-row lexsort((ids, dists))
+ * (graph.py:132-136) of init_random_graph: ids are the host-drawn random neighbours
+ * (graph.py:120-129); afterwards the device adjacency is sorted, counts = gamma, flags = 1. */
+int sb_init_graph(sb_index* idx, const int32_t* ids, double inv_alpha);
+
+/* build_candidates (_kernels.py:81-135) on the device adjacency; the new/old lists stay on
+ * the device for sb_local_join.  Output pointers may be NULL (download skipped). */
+int sb_build_candidates(sb_index* idx, int32_t gamma_new, int32_t* new_cand,
+                        int32_t* new_counts, int32_t* old_cand, int32_t* old_counts);
+
+/* local_join (_kernels.py:138-173).  *inserted > 0 iff some row changed (the reference's
+ * return value is only compared with 0, graph.py:256); *pairs = distance evaluations. */
+int sb_local_join(sb_index* idx, double inv_alpha, int64_t* inserted, int64_t* pairs);
+
+/* descent_iteration (graph.py:151-176) = sb_build_candidates + sb_local_join */
+int sb_descent_iteration(sb_index* idx, int32_t gamma_new, double inv_alpha, int64_t* inserted,
+                         int64_t* pairs);
+
+/* count_in_degrees (_kernels.py:256-263) */
+int sb_count_in_degrees(sb_index* idx, int64_t* in_deg);
+
+/* rows ids[s*gamma], counts[s] of the given nodes (the inputs graph_quality reads,
+ * _kernels.py:207-224; psi itself is summed on the host in the reference's order). */
+int sb_get_rows(sb_index* idx, const int64_t* rows, int64_t s, int32_t* ids, int32_t* counts);
+
+/* prune_pass (_kernels.py:266-303) with in_deg = count_in_degrees (graph.py:212-216).
+ * *rounds = Jacobi guard rounds used. */
+int sb_prune(sb_index* idx, double sigma, int32_t* rounds);
+
+/* reinforce_pass (_kernels.py:398-409) and the <= 10 reconnect_islands sweeps
+ * (graph.py:217-230), continuing from sb_prune's in-degrees.  *overflow_rows = rows that would
+ * exceed capacity (0: symmetrisation fast path), *sweeps = reconnect sweeps run. */
+int sb_reinforce(sb_index* idx, double sigma, int64_t* overflow_rows, int32_t* sweeps);
+
+/* ---- exhaustive AUTO top-k ------------------------------------------------------ */
+
+/* brute_force_topk (_kernels.py:176-204): exact top-k over all v != u, ids padded -1. */
+int sb_bf_topk_nodes(sb_index* idx, const int64_t* sample_ids, int64_t s, int32_t k,
+                     double inv_alpha, int32_t* out_ids);
+
+/* oracle_auto_topk (evaluate.py:32-55) for q queries at once: qf f64[q*m], qa i64[q*l],
+ * qmask i64[q*l] or NULL; fused = sqrt(s_v) * (1 + s_a / alpha), ties by id.
+ * *uncertain counts queries whose exact re-rank could not be certified (0 expected). */
+int sb_bf_topk_queries(sb_index* idx, const double* qf, const int64_t* qa, const int64_t* qmask,
+                       int64_t q, int32_t k, double alpha, int64_t* out_ids, double* out_dists,
+                       int32_t* uncertain);
+
+/* ---- Dynamic Heterogeneity Routing --------------------------------------------- */
+
+/* entry_points (router.py:42-45) for query indices qi0 .. qi0+q-1, host computation:
+ * default_rng(SeedSequence((seed, qi))).choice(n, k, replace=False). out i64[q*k]. */
+int sb_entry_points(int64_t n, int32_t k, uint64_t seed, int64_t qi0, int64_t q, int64_t* out);
+
+/* search_batch (router.py:98-124) as one device call: route (_kernels.py:504-610) for q
+ * queries with query_index = qi0 + row.  qf f64[q*m], qa f64[q*l], qmask f64[q*l] or NULL
+ * (router.py:62-73 widens to f64); entries i64[q*k] or NULL (drawn on the device with the
+ * reference's stream).  out_stats i64[q*5] or NULL: dist_evals, phase1_evals,
+ * phase1_expansions, hops (SearchStats, router.py:34-39) + neighbours scanned. */
+int sb_route_batch(sb_index* idx, const double* qf, const double* qa, const double* qmask,
+                   int64_t q, int32_t k, int32_t pioneer, int32_t use_coarse,
+                   const int64_t* entries, uint64_t seed, int64_t qi0, double inv_alpha,
+                   int64_t* out_ids, double* out_dists, int64_t* out_stats);
+
+/* same, all pointers on the device, asynchronous on the handle's stream */
+int sb_route_batch_dev(sb_index* idx, const double* qf, const double* qa, const double* qmask,
+                       int64_t q, int32_t k, int32_t pioneer, int32_t use_coarse,
+                       const int64_t* entries, uint64_t seed, int64_t qi0, double inv_alpha,
+                       int64_t* out_ids, double* out_dists, int64_t* out_stats);
+
+/* number of kernel launches this handle issued since creation (instrumentation) */
+int64_t sb_launch_count(sb_index* idx);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* STABLE_B200_H */

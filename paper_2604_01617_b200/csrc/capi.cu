@@ -1,0 +1,704 @@
+// capi.cu — the C ABI (include/stable_b200.h): index handle, device buffers, orchestration
+// of the kernels of one reference call, host<->device copies, error mapping.
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <stdio.h>
+#include <string.h>
+
+#include <algorithm>
+#include <string>
+#include <vector>
+
+#include "../../include/stable_b200.h"
+#include "common.cuh"
+#include "rng.cuh"
+#include "sb_internal.h"
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const std::string& msg) {
+  g_err = msg;
+  return code;
+}
+
+int cuda_fail(cudaError_t e, const char* what) {
+  g_err = std::string(what) + ": " + cudaGetErrorString(e);
+  return SB_ECUDA;
+}
+
+#define CK(expr)                                              \
+  do {                                                        \
+    cudaError_t e_ = (expr);                                  \
+    if (e_ != cudaSuccess) return cuda_fail(e_, #expr);       \
+  } while (0)
+
+#define CKL(expr)                                                          \
+  do {                                                                     \
+    int r_ = (expr);                                                       \
+    if (r_ != 0) return cuda_fail((cudaError_t)r_, #expr);                 \
+  } while (0)
+
+// grow-only device buffer
+struct DBuf {
+  void* p = nullptr;
+  size_t bytes = 0;
+  cudaError_t ensure(size_t b) {
+    if (b <= bytes) return cudaSuccess;
+    if (p) cudaFree(p);
+    p = nullptr;
+    bytes = 0;
+    size_t want = b < 256 ? 256 : b;
+    cudaError_t e = cudaMalloc(&p, want);
+    if (e == cudaSuccess) bytes = want;
+    return e;
+  }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    bytes = 0;
+  }
+  template <typename T>
+  T* as() const { return reinterpret_cast<T*>(p); }
+};
+
+}  // namespace
+
+struct sb_index {
+  int64_t n = 0;
+  int m = 0, l = 0, g = 0;
+  int sms = 148;
+  cudaStream_t own = nullptr, st = nullptr;
+  int64_t launches = 0;
+  // dataset + adjacency
+  DBuf F, A, ids, dists, flags, counts;
+  // candidates
+  int gn = 0;
+  bool have_cand = false;
+  DBuf new_cand, new_cnt, old_cand, old_cnt;
+  DBuf fwd_new, fwd_old, rev_cnt, rev_off, rev_cur, rev, scan_tmp;
+  // join
+  DBuf thr, row_cnt, row_off, row_cur, push_tgt, push_key, seg, small;
+  // prune / reinforce
+  DBuf rbits, smax, indeg0, guard, drop_other, keep, in_deg, seqtmp;
+  bool have_indeg = false;
+  // routing / brute force
+  DBuf qf, qa, qm, entries, ent_scratch, out_ids, out_dists, stats, visited, vlog, counter;
+  DBuf bf_part_d, bf_part_i, bf_self, bf_qa, bf_qm, bf_out32;
+  ~sb_index() {
+    DBuf* all[] = {&F, &A, &ids, &dists, &flags, &counts, &new_cand, &new_cnt, &old_cand,
+                   &old_cnt, &fwd_new, &fwd_old, &rev_cnt, &rev_off, &rev_cur, &rev, &scan_tmp,
+                   &thr, &row_cnt, &row_off, &row_cur, &push_tgt, &push_key, &seg, &small,
+                   &rbits, &smax, &indeg0, &guard, &drop_other, &keep, &in_deg, &seqtmp, &qf,
+                   &qa, &qm, &entries, &ent_scratch, &out_ids, &out_dists, &stats, &visited,
+                   &vlog, &counter, &bf_part_d, &bf_part_i, &bf_self, &bf_qa, &bf_qm,
+                   &bf_out32};
+    for (DBuf* b : all) b->release();
+    if (own) cudaStreamDestroy(own);
+  }
+};
+
+using sb::next_pow2;
+
+extern "C" {
+
+const char* sb_last_error(void) { return g_err.c_str(); }
+int sb_version(void) { return (0 << 16) | 1; }
+
+int sb_device_count(int* count) {
+  if (!count) return fail(SB_EARG, "count is NULL");
+  cudaError_t e = cudaGetDeviceCount(count);
+  if (e != cudaSuccess) {
+    *count = 0;
+    return cuda_fail(e, "cudaGetDeviceCount");
+  }
+  return SB_OK;
+}
+
+int sb_index_create(const float* features, const int32_t* attrs, int64_t n, int32_t m, int32_t l,
+                    int32_t gamma, sb_index** out) {
+  if (!out) return fail(SB_EARG, "out is NULL");
+  *out = nullptr;
+  if (!features || !attrs) return fail(SB_EARG, "features/attrs are NULL");
+  if (n < 1 || m < 1 || l < 1) return fail(SB_EARG, "n, m and l must be >= 1");
+  if (gamma < 2 || gamma > 256) return fail(SB_EARG, "gamma must be in [2, 256]");
+  if (n >= (int64_t)1 << 30) return fail(SB_EARG, "n must be < 2^30");
+  sb_index* x = new sb_index();
+  x->n = n; x->m = m; x->l = l; x->g = gamma;
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e == cudaSuccess) e = cudaDeviceGetAttribute(&x->sms, cudaDevAttrMultiProcessorCount, dev);
+  if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&x->own, cudaStreamNonBlocking);
+  if (e != cudaSuccess) { delete x; return cuda_fail(e, "device/stream setup"); }
+  x->st = x->own;
+  size_t fb = sizeof(float) * (size_t)n * m, ab = sizeof(int32_t) * (size_t)n * l;
+  size_t adj = (size_t)n * gamma;
+  if ((e = x->F.ensure(fb)) != cudaSuccess || (e = x->A.ensure(ab)) != cudaSuccess ||
+      (e = x->ids.ensure(adj * 4)) != cudaSuccess || (e = x->dists.ensure(adj * 4)) != cudaSuccess ||
+      (e = x->flags.ensure(adj)) != cudaSuccess || (e = x->counts.ensure((size_t)n * 4)) != cudaSuccess) {
+    delete x;
+    return cuda_fail(e, "cudaMalloc(index)");
+  }
+  e = cudaMemcpyAsync(x->F.p, features, fb, cudaMemcpyHostToDevice, x->st);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(x->A.p, attrs, ab, cudaMemcpyHostToDevice, x->st);
+  if (e == cudaSuccess) e = cudaMemsetAsync(x->counts.p, 0, (size_t)n * 4, x->st);
+  if (e == cudaSuccess) e = cudaMemsetAsync(x->flags.p, 0, adj, x->st);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(x->st);
+  if (e != cudaSuccess) { delete x; return cuda_fail(e, "upload(index)"); }
+  *out = x;
+  return SB_OK;
+}
+
+int sb_index_destroy(sb_index* idx) {
+  delete idx;
+  return SB_OK;
+}
+
+int sb_set_stream(sb_index* idx, void* s) {
+  if (!idx) return fail(SB_EARG, "idx is NULL");
+  idx->st = s ? reinterpret_cast<cudaStream_t>(s) : idx->own;
+  return SB_OK;
+}
+
+int sb_synchronize(sb_index* idx) {
+  if (!idx) return fail(SB_EARG, "idx is NULL");
+  CK(cudaStreamSynchronize(idx->st));
+  return SB_OK;
+}
+
+int64_t sb_launch_count(sb_index* idx) { return idx ? idx->launches : 0; }
+
+int sb_adj_upload(sb_index* idx, const int32_t* ids, const float* dists, const int32_t* counts,
+                  const uint8_t* flags) {
+  if (!idx || !ids || !dists || !counts) return fail(SB_EARG, "NULL argument");
+  size_t adj = (size_t)idx->n * idx->g;
+  CK(cudaMemcpyAsync(idx->ids.p, ids, adj * 4, cudaMemcpyHostToDevice, idx->st));
+  CK(cudaMemcpyAsync(idx->dists.p, dists, adj * 4, cudaMemcpyHostToDevice, idx->st));
+  CK(cudaMemcpyAsync(idx->counts.p, counts, (size_t)idx->n * 4, cudaMemcpyHostToDevice, idx->st));
+  if (flags) CK(cudaMemcpyAsync(idx->flags.p, flags, adj, cudaMemcpyHostToDevice, idx->st));
+  idx->have_cand = false;
+  idx->have_indeg = false;
+  CK(cudaStreamSynchronize(idx->st));
+  return SB_OK;
+}
+
+int sb_adj_download(sb_index* idx, int32_t* ids, float* dists, int32_t* counts, uint8_t* flags) {
+  if (!idx) return fail(SB_EARG, "idx is NULL");
+  size_t adj = (size_t)idx->n * idx->g;
+  if (ids) CK(cudaMemcpyAsync(ids, idx->ids.p, adj * 4, cudaMemcpyDeviceToHost, idx->st));
+  if (dists) CK(cudaMemcpyAsync(dists, idx->dists.p, adj * 4, cudaMemcpyDeviceToHost, idx->st));
+  if (counts) CK(cudaMemcpyAsync(counts, idx->counts.p, (size_t)idx->n * 4, cudaMemcpyDeviceToHost, idx->st));
+  if (flags) CK(cudaMemcpyAsync(flags, idx->flags.p, adj, cudaMemcpyDeviceToHost, idx->st));
+  CK(cudaStreamSynchronize(idx->st));
+  return SB_OK;
+}
+
+// ---------------------------------------------------------------------------
+__global__ void sb_fill_i32(int32_t* p, int64_t n, int32_t v) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) p[i] = v;
+}
+
+int sb_init_graph(sb_index* idx, const int32_t* ids, double inv_alpha) {
+  if (!idx || !ids) return fail(SB_EARG, "NULL argument");
+  if (idx->n <= idx->g) return fail(SB_EARG, "dataset size must exceed gamma");
+  size_t adj = (size_t)idx->n * idx->g;
+  CK(cudaMemcpyAsync(idx->ids.p, ids, adj * 4, cudaMemcpyHostToDevice, idx->st));
+  CKL(sb::launch_init_dists(idx->F.as<float>(), idx->A.as<int32_t>(), idx->n, idx->m, idx->l,
+                            idx->g, inv_alpha, idx->ids.as<int32_t>(), idx->dists.as<float>(),
+                            idx->st));
+  sb_fill_i32<<<(unsigned)((idx->n + 255) / 256), 256, 0, idx->st>>>(idx->counts.as<int32_t>(),
+                                                                      idx->n, idx->g);
+  CK(cudaMemsetAsync(idx->flags.p, 1, adj, idx->st));
+  idx->launches += 2;
+  idx->have_cand = false;
+  CK(cudaStreamSynchronize(idx->st));
+  return SB_OK;
+}
+
+int sb_build_candidates(sb_index* idx, int32_t gamma_new, int32_t* new_cand, int32_t* new_counts,
+                        int32_t* old_cand, int32_t* old_counts) {
+  if (!idx) return fail(SB_EARG, "idx is NULL");
+  if (gamma_new < 1 || gamma_new > 256) return fail(SB_EARG, "gamma_new must be in [1, 256]");
+  const int64_t n = idx->n;
+  const int g = idx->g;
+  idx->gn = gamma_new;
+  CK(idx->new_cand.ensure(sizeof(int32_t) * n * gamma_new));
+  CK(idx->old_cand.ensure(sizeof(int32_t) * n * g));
+  CK(idx->new_cnt.ensure(sizeof(int32_t) * n));
+  CK(idx->old_cnt.ensure(sizeof(int32_t) * n));
+  CK(idx->fwd_new.ensure(sizeof(int32_t) * n));
+  CK(idx->fwd_old.ensure(sizeof(int32_t) * n));
+  CK(idx->rev_cnt.ensure(sizeof(int64_t) * n));
+  CK(idx->rev_off.ensure(sizeof(int64_t) * n));
+  CK(idx->rev_cur.ensure(sizeof(int64_t) * n));
+  CK(idx->rev.ensure(sizeof(int32_t) * n * std::max(gamma_new, g)));
+  CK(idx->scan_tmp.ensure(sizeof(int64_t) * sb::scan_tmp_slots(n)));
+  sb::BuildScratch s;
+  s.fwd_new = idx->fwd_new.as<int32_t>();
+  s.fwd_old = idx->fwd_old.as<int32_t>();
+  s.rev_cnt = idx->rev_cnt.as<int64_t>();
+  s.rev_off = idx->rev_off.as<int64_t>();
+  s.rev_cur = idx->rev_cur.as<int64_t>();
+  s.rev = idx->rev.as<int32_t>();
+  s.scan_tmp = idx->scan_tmp.as<int64_t>();
+  CKL(sb::launch_build_candidates(idx->ids.as<int32_t>(), idx->flags.as<uint8_t>(), n, g,
+                                  gamma_new, idx->new_cand.as<int32_t>(),
+                                  idx->new_cnt.as<int32_t>(), idx->old_cand.as<int32_t>(),
+                                  idx->old_cnt.as<int32_t>(), s, idx->st));
+  idx->launches += 9;
+  idx->have_cand = true;
+  if (new_cand) CK(cudaMemcpyAsync(new_cand, idx->new_cand.p, sizeof(int32_t) * n * gamma_new, cudaMemcpyDeviceToHost, idx->st));
+  if (new_counts) CK(cudaMemcpyAsync(new_counts, idx->new_cnt.p, sizeof(int32_t) * n, cudaMemcpyDeviceToHost, idx->st));
+  if (old_cand) CK(cudaMemcpyAsync(old_cand, idx->old_cand.p, sizeof(int32_t) * n * g, cudaMemcpyDeviceToHost, idx->st));
+  if (old_counts) CK(cudaMemcpyAsync(old_counts, idx->old_cnt.p, sizeof(int32_t) * n, cudaMemcpyDeviceToHost, idx->st));
+  CK(cudaStreamSynchronize(idx->st));
+  return SB_OK;
+}
+
+int sb_local_join(sb_index* idx, double inv_alpha, int64_t* inserted_out, int64_t* pairs_out) {
+  if (!idx) return fail(SB_EARG, "idx is NULL");
+  if (!idx->have_cand) return fail(SB_EARG, "sb_build_candidates must run first");
+  const int64_t n = idx->n;
+  const int g = idx->g, gn = idx->gn;
+  // per-node worst-case pushes (2 per pair) to plan chunks
+  std::vector<int32_t> nc(n), oc(n);
+  CK(cudaMemcpyAsync(nc.data(), idx->new_cnt.p, sizeof(int32_t) * n, cudaMemcpyDeviceToHost, idx->st));
+  CK(cudaMemcpyAsync(oc.data(), idx->old_cnt.p, sizeof(int32_t) * n, cudaMemcpyDeviceToHost, idx->st));
+  CK(cudaStreamSynchronize(idx->st));
+  std::vector<uint64_t> worst(n);
+  uint64_t total_pairs = 0, total_worst = 0;
+  int max_ns = 1, max_na = 1;
+  for (int64_t i = 0; i < n; ++i) {
+    uint64_t na = (uint64_t)nc[i], nb = (uint64_t)oc[i];
+    uint64_t pairs = na * (na > 0 ? na - 1 : 0) / 2 + na * nb;
+    total_pairs += pairs;
+    worst[i] = 2 * pairs;
+    total_worst += worst[i];
+    max_ns = std::max(max_ns, (int)(na + nb));
+    max_na = std::max(max_na, (int)na);
+  }
+  if (pairs_out) *pairs_out = (int64_t)total_pairs;
+  CK(idx->thr.ensure(sizeof(uint64_t) * n));
+  CK(idx->row_cnt.ensure(sizeof(int64_t) * n));
+  CK(idx->row_off.ensure(sizeof(int64_t) * n));
+  CK(idx->row_cur.ensure(sizeof(int64_t) * n));
+  CK(idx->small.ensure(64));
+  CK(idx->scan_tmp.ensure(sizeof(int64_t) * sb::scan_tmp_slots(n)));
+  CKL(sb::launch_thr_init(idx->ids.as<int32_t>(), idx->dists.as<float>(), n, g,
+                          idx->thr.as<uint64_t>(), idx->st));
+  // emit kernel geometry
+  const int spad = (max_ns + 3) & ~3;
+  const int ntiles_max = ((max_na + 3) / 4) * ((max_ns + 3) / 4);
+  const size_t stage_budget = 96 * 1024;
+  int dc = (int)std::min<int64_t>(idx->m, (int64_t)(stage_budget / (sizeof(float) * spad)));
+  if (dc < idx->m) dc = std::max(4, dc & ~3);
+  size_t smem = sb::join_emit_smem(spad, dc, idx->l, ntiles_max);
+  int per_sm = 0;
+  CKL(sb::join_emit_occupancy(smem, &per_sm));
+  if (per_sm < 1) return fail(SB_ECUDA, "join kernel does not fit on an SM");
+  const int ctas = idx->sms * per_sm;
+  const uint64_t slack = (uint64_t)ctas * (256 / 32) * 128 * 2;  // reservation padding
+  // push buffer: 4 + 8 (emit) + 8 (segments) bytes per slot
+  size_t free_b = 0, tot_b = 0;
+  CK(cudaMemGetInfo(&free_b, &tot_b));
+  uint64_t budget_slots = (uint64_t)(free_b * 0.6) / 20;
+  uint64_t cap = std::min<uint64_t>(total_worst + slack, budget_slots);
+  if (cap < slack * 2) return fail(SB_ECUDA, "not enough device memory for the join buffers");
+  CK(idx->push_tgt.ensure(sizeof(uint32_t) * cap));
+  CK(idx->push_key.ensure(sizeof(uint64_t) * cap));
+  CK(idx->seg.ensure(sizeof(uint64_t) * cap));
+  unsigned long long* d_count = idx->small.as<unsigned long long>();
+  unsigned long long* d_inserted = d_count + 1;
+  int* d_nodectr = reinterpret_cast<int*>(d_count + 2);
+  int* d_overflow = d_nodectr + 1;
+  CK(cudaMemsetAsync(d_inserted, 0, sizeof(unsigned long long), idx->st));
+  int64_t begin = 0;
+  while (begin < n) {
+    uint64_t acc = slack;
+    int64_t end = begin;
+    while (end < n && acc + worst[end] <= cap) acc += worst[end++];
+    if (end == begin) return fail(SB_ECUDA, "join buffer too small for one node");
+    CK(cudaMemsetAsync(d_count, 0, sizeof(unsigned long long), idx->st));
+    CK(cudaMemsetAsync(d_nodectr, 0, sizeof(int) * 2, idx->st));
+    CK(cudaMemsetAsync(idx->row_cnt.p, 0, sizeof(int64_t) * n, idx->st));
+    sb::JoinArgs a;
+    a.F = idx->F.as<float>(); a.A = idx->A.as<int32_t>(); a.n = n; a.m = idx->m; a.l = idx->l;
+    a.g = g; a.gn = gn; a.inv_alpha = inv_alpha;
+    a.new_cand = idx->new_cand.as<int32_t>(); a.new_cnt = idx->new_cnt.as<int32_t>();
+    a.old_cand = idx->old_cand.as<int32_t>(); a.old_cnt = idx->old_cnt.as<int32_t>();
+    a.thr = idx->thr.as<uint64_t>(); a.node_begin = begin; a.node_end = end;
+    a.node_counter = d_nodectr; a.push_tgt = idx->push_tgt.as<uint32_t>();
+    a.push_key = idx->push_key.as<uint64_t>(); a.push_cap = cap; a.push_count = d_count;
+    a.row_cnt = idx->row_cnt.as<int64_t>(); a.overflow = d_overflow; a.spad = spad; a.dc = dc;
+    int nctas = (int)std::min<int64_t>(ctas, end - begin);
+    CKL(sb::launch_join_emit(a, nctas, smem, idx->st));
+    unsigned long long used = 0;
+    int over = 0;
+    CK(cudaMemcpyAsync(&used, d_count, sizeof(used), cudaMemcpyDeviceToHost, idx->st));
+    CK(cudaMemcpyAsync(&over, d_overflow, sizeof(int), cudaMemcpyDeviceToHost, idx->st));
+    CK(cudaStreamSynchronize(idx->st));
+    if (over) return fail(SB_ECUDA, "join push buffer overflow (planning bug)");
+    uint64_t total = std::min<uint64_t>(used, cap);
+    CKL(sb::exclusive_scan(idx->row_cnt.as<int64_t>(), idx->row_off.as<int64_t>(), n,
+                           idx->scan_tmp.as<int64_t>(), idx->st));
+    CK(cudaMemsetAsync(idx->row_cur.p, 0, sizeof(int64_t) * n, idx->st));
+    CKL(sb::launch_push_scatter(idx->push_tgt.as<uint32_t>(), idx->push_key.as<uint64_t>(), total,
+                                idx->row_off.as<int64_t>(), idx->row_cur.as<int64_t>(),
+                                idx->seg.as<uint64_t>(), idx->st));
+    CKL(sb::launch_row_merge(idx->ids.as<int32_t>(), idx->dists.as<float>(),
+                             idx->flags.as<uint8_t>(), idx->thr.as<uint64_t>(), n, g,
+                             idx->row_off.as<int64_t>(), idx->row_cnt.as<int64_t>(),
+                             idx->seg.as<uint64_t>(), d_inserted, idx->st));
+    idx->launches += 5;
+    begin = end;
+  }
+  unsigned long long ins = 0;
+  CK(cudaMemcpyAsync(&ins, d_inserted, sizeof(ins), cudaMemcpyDeviceToHost, idx->st));
+  CK(cudaStreamSynchronize(idx->st));
+  if (inserted_out) *inserted_out = (int64_t)ins;
+  idx->have_cand = false;
+  return SB_OK;
+}
+
+int sb_descent_iteration(sb_index* idx, int32_t gamma_new, double inv_alpha, int64_t* inserted,
+                         int64_t* pairs) {
+  int r = sb_build_candidates(idx, gamma_new, nullptr, nullptr, nullptr, nullptr);
+  if (r) return r;
+  return sb_local_join(idx, inv_alpha, inserted, pairs);
+}
+
+int sb_count_in_degrees(sb_index* idx, int64_t* in_deg) {
+  if (!idx || !in_deg) return fail(SB_EARG, "NULL argument");
+  const int64_t n = idx->n;
+  CK(idx->in_deg.ensure(sizeof(int32_t) * n));
+  CKL(sb::launch_count_in_degrees(idx->ids.as<int32_t>(), idx->counts.as<int32_t>(), n, idx->g,
+                                  idx->in_deg.as<int32_t>(), nullptr, idx->st));
+  idx->launches += 1;
+  std::vector<int32_t> h(n);
+  CK(cudaMemcpyAsync(h.data(), idx->in_deg.p, sizeof(int32_t) * n, cudaMemcpyDeviceToHost, idx->st));
+  CK(cudaStreamSynchronize(idx->st));
+  for (int64_t i = 0; i < n; ++i) in_deg[i] = h[i];
+  return SB_OK;
+}
+
+__global__ void sb_gather_rows(const int32_t* ids, const int32_t* counts, int g, const int64_t* rows,
+                               int64_t s, int32_t* out_ids, int32_t* out_counts) {
+  int64_t r = blockIdx.x;
+  if (r >= s) return;
+  int64_t row = rows[r];
+  for (int t = threadIdx.x; t < g; t += blockDim.x) out_ids[r * g + t] = ids[row * g + t];
+  if (threadIdx.x == 0) out_counts[r] = counts[row];
+}
+
+int sb_get_rows(sb_index* idx, const int64_t* rows, int64_t s, int32_t* ids, int32_t* counts) {
+  if (!idx || !rows || !ids || !counts) return fail(SB_EARG, "NULL argument");
+  if (s <= 0) return SB_OK;
+  const int g = idx->g;
+  size_t need = sizeof(int64_t) * s + sizeof(int32_t) * s * (g + 1);
+  CK(idx->bf_self.ensure(need));
+  int64_t* d_rows = idx->bf_self.as<int64_t>();
+  int32_t* d_ids = reinterpret_cast<int32_t*>(d_rows + s);
+  int32_t* d_cnt = d_ids + s * g;
+  CK(cudaMemcpyAsync(d_rows, rows, sizeof(int64_t) * s, cudaMemcpyHostToDevice, idx->st));
+  sb_gather_rows<<<(unsigned)s, 128, 0, idx->st>>>(idx->ids.as<int32_t>(), idx->counts.as<int32_t>(),
+                                                    g, d_rows, s, d_ids, d_cnt);
+  idx->launches += 1;
+  CK(cudaMemcpyAsync(ids, d_ids, sizeof(int32_t) * s * g, cudaMemcpyDeviceToHost, idx->st));
+  CK(cudaMemcpyAsync(counts, d_cnt, sizeof(int32_t) * s, cudaMemcpyDeviceToHost, idx->st));
+  CK(cudaStreamSynchronize(idx->st));
+  return SB_OK;
+}
+
+int sb_prune(sb_index* idx, double sigma, int32_t* rounds_out) {
+  if (!idx) return fail(SB_EARG, "idx is NULL");
+  const int64_t n = idx->n;
+  const int g = idx->g, W = (g + 31) / 32;
+  CK(idx->smax.ensure(sizeof(int32_t) * n));
+  CK(idx->indeg0.ensure(sizeof(int32_t) * n));
+  CK(idx->in_deg.ensure(sizeof(int32_t) * n));
+  CK(idx->guard.ensure(n));
+  CK(idx->drop_other.ensure(sizeof(int32_t) * n));
+  CK(idx->keep.ensure(sizeof(uint32_t) * n * W));
+  CK(idx->rbits.ensure(sizeof(uint32_t) * n * g * W));
+  CK(idx->small.ensure(64));
+  CKL(sb::launch_count_in_degrees(idx->ids.as<int32_t>(), idx->counts.as<int32_t>(), n, g,
+                                  idx->indeg0.as<int32_t>(), idx->smax.as<int32_t>(), idx->st));
+  CK(cudaMemsetAsync(idx->guard.p, 0, n, idx->st));
+  sb::PruneArgs a;
+  a.F = idx->F.as<float>(); a.A = idx->A.as<int32_t>(); a.n = n; a.m = idx->m; a.l = idx->l;
+  a.g = g; a.W = W; a.ids = idx->ids.as<int32_t>(); a.dists = idx->dists.as<float>();
+  a.counts = idx->counts.as<int32_t>(); a.sigma = sigma; a.rbits = idx->rbits.as<uint32_t>();
+  a.smax = idx->smax.as<int32_t>(); a.indeg0 = idx->indeg0.as<int32_t>();
+  a.guard = idx->guard.as<uint8_t>(); a.drop_other = idx->drop_other.as<int32_t>();
+  a.keep = idx->keep.as<uint32_t>(); a.in_deg = idx->in_deg.as<int32_t>();
+  a.cpad = (g + 3) & ~3;
+  const size_t stage_budget = 96 * 1024;
+  a.dc = (int)std::min<int64_t>(idx->m, (int64_t)(stage_budget / (sizeof(float) * a.cpad)));
+  size_t smem = sb::prune_bits_smem(a.cpad, a.dc, idx->m, idx->l, W);
+  CKL(sb::launch_prune_bits(a, smem, idx->st));
+  int* d_changed = reinterpret_cast<int*>(idx->small.p);
+  int rounds = 0;
+  for (;;) {
+    CK(cudaMemsetAsync(idx->drop_other.p, 0, sizeof(int32_t) * n, idx->st));
+    CK(cudaMemsetAsync(d_changed, 0, sizeof(int), idx->st));
+    CKL(sb::launch_prune_scan(a, idx->st));
+    CKL(sb::launch_prune_guard(a, d_changed, idx->st));
+    idx->launches += 2;
+    int changed = 0;
+    CK(cudaMemcpyAsync(&changed, d_changed, sizeof(int), cudaMemcpyDeviceToHost, idx->st));
+    CK(cudaStreamSynchronize(idx->st));
+    ++rounds;
+    if (!changed) break;
+    if (rounds > 100000) return fail(SB_ECUDA, "prune guard iteration did not converge");
+  }
+  CK(cudaMemcpyAsync(idx->in_deg.p, idx->indeg0.p, sizeof(int32_t) * n, cudaMemcpyDeviceToDevice, idx->st));
+  CKL(sb::launch_prune_compact(a, idx->st));
+  idx->launches += 3;
+  idx->have_indeg = true;
+  CK(cudaStreamSynchronize(idx->st));
+  if (rounds_out) *rounds_out = rounds;
+  return SB_OK;
+}
+
+int sb_reinforce(sb_index* idx, double sigma, int64_t* overflow_rows, int32_t* sweeps_out) {
+  if (!idx) return fail(SB_EARG, "idx is NULL");
+  if (!idx->have_indeg) return fail(SB_EARG, "sb_prune must run first");
+  const int64_t n = idx->n;
+  const int g = idx->g;
+  CK(idx->rev_cnt.ensure(sizeof(int64_t) * n));
+  CK(idx->rev_off.ensure(sizeof(int64_t) * n));
+  CK(idx->rev_cur.ensure(sizeof(int64_t) * n));
+  CK(idx->scan_tmp.ensure(sizeof(int64_t) * sb::scan_tmp_slots(n)));
+  CK(idx->small.ensure(64));
+  unsigned long long* d_over = idx->small.as<unsigned long long>() + 4;
+  CKL(sb::launch_reinforce_check(idx->ids.as<int32_t>(), idx->dists.as<float>(),
+                                 idx->counts.as<int32_t>(), n, g, idx->rev_cnt.as<int64_t>(),
+                                 d_over, idx->st));
+  unsigned long long over = 0;
+  CK(cudaMemcpyAsync(&over, d_over, sizeof(over), cudaMemcpyDeviceToHost, idx->st));
+  CK(cudaStreamSynchronize(idx->st));
+  if (overflow_rows) *overflow_rows = (int64_t)over;
+  CK(idx->seqtmp.ensure((sizeof(int64_t) + sizeof(double) + 1) * (g + 1) + 64));
+  if (over == 0) {
+    CK(idx->seg.ensure(sizeof(uint64_t) * n * g));
+    CKL(sb::launch_symmetrize(idx->ids.as<int32_t>(), idx->dists.as<float>(),
+                              idx->counts.as<int32_t>(), n, g, idx->rev_cnt.as<int64_t>(),
+                              idx->rev_off.as<int64_t>(), idx->rev_cur.as<int64_t>(),
+                              idx->seg.as<uint64_t>(), idx->scan_tmp.as<int64_t>(), idx->st));
+    idx->launches += 6;
+  } else {
+    CKL(sb::launch_seq_reinforce(idx->F.as<float>(), idx->A.as<int32_t>(), idx->m, idx->l, g,
+                                 idx->ids.as<int32_t>(), idx->dists.as<float>(),
+                                 idx->counts.as<int32_t>(), idx->in_deg.as<int32_t>(), sigma, n,
+                                 idx->seqtmp.p, 0, idx->st));
+    idx->launches += 3;
+  }
+  // reconnect sweeps (graph.py:221-230)
+  int sweeps = 0;
+  int* d_min = reinterpret_cast<int*>(idx->small.as<unsigned long long>() + 5);
+  for (int it = 0; it < 10; ++it) {
+    CKL(sb::launch_count_in_degrees(idx->ids.as<int32_t>(), idx->counts.as<int32_t>(), n, g,
+                                    idx->in_deg.as<int32_t>(), nullptr, idx->st));
+    int big = 0x7FFFFFFF;
+    CK(cudaMemcpyAsync(d_min, &big, sizeof(int), cudaMemcpyHostToDevice, idx->st));
+    CKL(sb::launch_min_i32(idx->in_deg.as<int32_t>(), n, d_min, idx->st));
+    int mn = 0;
+    CK(cudaMemcpyAsync(&mn, d_min, sizeof(int), cudaMemcpyDeviceToHost, idx->st));
+    CK(cudaStreamSynchronize(idx->st));
+    idx->launches += 2;
+    if (mn >= 1) break;
+    CKL(sb::launch_seq_reinforce(idx->F.as<float>(), idx->A.as<int32_t>(), idx->m, idx->l, g,
+                                 idx->ids.as<int32_t>(), idx->dists.as<float>(),
+                                 idx->counts.as<int32_t>(), idx->in_deg.as<int32_t>(), sigma, n,
+                                 idx->seqtmp.p, 1, idx->st));
+    idx->launches += 1;
+    ++sweeps;
+  }
+  CK(cudaStreamSynchronize(idx->st));
+  if (sweeps_out) *sweeps_out = sweeps;
+  idx->have_indeg = false;
+  return SB_OK;
+}
+
+// ---------------------------------------------------------------------------
+static int bf_run(sb_index* idx, sb::BfArgs& a, int kout, int64_t* out64, int32_t* out32,
+                  double* outd, int* uncertain_host) {
+  const int64_t q = a.q;
+  const int groups = (int)((q + sb::bf_group_size() - 1) / sb::bf_group_size());
+  // enough CTAs to fill the GPU twice over
+  int splits = std::max(1, (2 * idx->sms + groups - 1) / groups);
+  splits = (int)std::min<int64_t>(splits, std::max<int64_t>(1, idx->n / 256));
+  a.splits = splits;
+  CK(idx->bf_part_d.ensure(sizeof(double) * q * splits * a.k));
+  CK(idx->bf_part_i.ensure(sizeof(uint32_t) * q * splits * a.k));
+  a.part_d = idx->bf_part_d.as<double>();
+  a.part_i = idx->bf_part_i.as<uint32_t>();
+  CK(idx->small.ensure(64));
+  int* d_unc = reinterpret_cast<int*>(idx->small.as<unsigned long long>() + 6);
+  CK(cudaMemsetAsync(d_unc, 0, sizeof(int), idx->st));
+  CKL(sb::launch_bf_partial(a, idx->st));
+  CKL(sb::launch_bf_merge_k(a, kout, out64, out32, outd, d_unc, idx->st));
+  idx->launches += 2;
+  if (uncertain_host) CK(cudaMemcpyAsync(uncertain_host, d_unc, sizeof(int), cudaMemcpyDeviceToHost, idx->st));
+  return SB_OK;
+}
+
+int sb_bf_topk_nodes(sb_index* idx, const int64_t* sample_ids, int64_t s, int32_t k,
+                     double inv_alpha, int32_t* out_ids) {
+  if (!idx || !sample_ids || !out_ids) return fail(SB_EARG, "NULL argument");
+  if (k < 1 || k > 1024) return fail(SB_EARG, "k must be in [1, 1024]");
+  if (s <= 0) return SB_OK;
+  CK(idx->bf_self.ensure(sizeof(int64_t) * s));
+  CK(idx->bf_out32.ensure(sizeof(int32_t) * s * k));
+  CK(cudaMemcpyAsync(idx->bf_self.p, sample_ids, sizeof(int64_t) * s, cudaMemcpyHostToDevice, idx->st));
+  sb::BfArgs a{};
+  a.F = idx->F.as<float>(); a.A = idx->A.as<int32_t>(); a.n = idx->n; a.m = idx->m; a.l = idx->l;
+  a.self_ids = idx->bf_self.as<int64_t>(); a.q = s; a.k = k; a.inv_alpha = inv_alpha;
+  int r = bf_run(idx, a, k, nullptr, idx->bf_out32.as<int32_t>(), nullptr, nullptr);
+  if (r) return r;
+  CK(cudaMemcpyAsync(out_ids, idx->bf_out32.p, sizeof(int32_t) * s * k, cudaMemcpyDeviceToHost, idx->st));
+  CK(cudaStreamSynchronize(idx->st));
+  return SB_OK;
+}
+
+int sb_bf_topk_queries(sb_index* idx, const double* qf, const int64_t* qa, const int64_t* qmask,
+                       int64_t q, int32_t k, double alpha, int64_t* out_ids, double* out_dists,
+                       int32_t* uncertain) {
+  if (!idx || !qf || !qa || !out_ids) return fail(SB_EARG, "NULL argument");
+  if (k < 1 || k > idx->n) return fail(SB_EARG, "k must be in [1, n]");
+  if (k > 1000) return fail(SB_EARG, "k must be <= 1000");
+  if (q <= 0) return SB_OK;
+  const int extra = 16;
+  const int kk = (int)std::min<int64_t>(idx->n, k + extra);
+  CK(idx->qf.ensure(sizeof(double) * q * idx->m));
+  CK(idx->bf_qa.ensure(sizeof(int64_t) * q * idx->l));
+  CK(idx->bf_qm.ensure(sizeof(int64_t) * q * idx->l));
+  CK(idx->out_ids.ensure(sizeof(int64_t) * q * k));
+  CK(idx->out_dists.ensure(sizeof(double) * q * k));
+  CK(cudaMemcpyAsync(idx->qf.p, qf, sizeof(double) * q * idx->m, cudaMemcpyHostToDevice, idx->st));
+  CK(cudaMemcpyAsync(idx->bf_qa.p, qa, sizeof(int64_t) * q * idx->l, cudaMemcpyHostToDevice, idx->st));
+  if (qmask) CK(cudaMemcpyAsync(idx->bf_qm.p, qmask, sizeof(int64_t) * q * idx->l, cudaMemcpyHostToDevice, idx->st));
+  sb::BfArgs a{};
+  a.F = idx->F.as<float>(); a.A = idx->A.as<int32_t>(); a.n = idx->n; a.m = idx->m; a.l = idx->l;
+  a.qf = idx->qf.as<double>(); a.qa = idx->bf_qa.as<int64_t>();
+  a.qmask = qmask ? idx->bf_qm.as<int64_t>() : nullptr; a.q = q; a.k = kk; a.alpha = alpha;
+  int unc = 0;
+  int r = bf_run(idx, a, k, idx->out_ids.as<int64_t>(), nullptr, idx->out_dists.as<double>(), &unc);
+  if (r) return r;
+  CK(cudaMemcpyAsync(out_ids, idx->out_ids.p, sizeof(int64_t) * q * k, cudaMemcpyDeviceToHost, idx->st));
+  if (out_dists) CK(cudaMemcpyAsync(out_dists, idx->out_dists.p, sizeof(double) * q * k, cudaMemcpyDeviceToHost, idx->st));
+  CK(cudaStreamSynchronize(idx->st));
+  if (uncertain) *uncertain = unc;
+  return SB_OK;
+}
+
+// ---------------------------------------------------------------------------
+int sb_entry_points(int64_t n, int32_t k, uint64_t seed, int64_t qi0, int64_t q, int64_t* out) {
+  if (!out) return fail(SB_EARG, "out is NULL");
+  if (k < 1 || k > n) return fail(SB_EARG, "k must be in [1, n]");
+  std::vector<int64_t> scratch(sbrng::choice_scratch_slots(n, k));
+  for (int64_t i = 0; i < q; ++i)
+    sbrng::entry_points(n, k, seed, (uint64_t)(qi0 + i), out + i * k, scratch.data());
+  return SB_OK;
+}
+
+static int route_dev(sb_index* idx, const double* qf, const double* qa, const double* qm, int64_t q,
+                     int32_t k, int32_t p, int32_t use_coarse, const int64_t* entries,
+                     uint64_t seed, int64_t qi0, double inv_alpha, int64_t* out_ids,
+                     double* out_dists, int64_t* out_stats) {
+  if (k < 1 || k > idx->n) return fail(SB_EARG, "k must be in [1, n]");
+  if (p < 1 || p > k) return fail(SB_EARG, "pioneer_size must be in [1, k]");
+  if (k > 16384) return fail(SB_EARG, "k must be <= 16384");
+  if (q <= 0) return SB_OK;
+  const int64_t n = idx->n;
+  if (!entries) {
+    uint64_t slots = sbrng::choice_scratch_slots(n, k);
+    CK(idx->entries.ensure(sizeof(int64_t) * q * k));
+    // bound the RNG scratch: draw in slices
+    int64_t slice = std::max<int64_t>(1, std::min<int64_t>(q, (int64_t)((1ull << 30) / (slots * 8))));
+    CK(idx->ent_scratch.ensure(sizeof(int64_t) * slots * slice));
+    for (int64_t b = 0; b < q; b += slice) {
+      int64_t c = std::min(slice, q - b);
+      CKL(sb::launch_entry_points(n, k, seed, qi0 + b, c, idx->entries.as<int64_t>() + b * k,
+                                  idx->ent_scratch.as<int64_t>(), slots, idx->st));
+      idx->launches += 1;
+    }
+    entries = idx->entries.as<int64_t>();
+  }
+  sb::RouteArgs a;
+  a.F = idx->F.as<float>(); a.A = idx->A.as<int32_t>(); a.nbr_ids = idx->ids.as<int32_t>();
+  a.nbr_counts = idx->counts.as<int32_t>(); a.n = n; a.m = idx->m; a.l = idx->l; a.g = idx->g;
+  a.qf = qf; a.qa = qa; a.qm = qm; a.entries = entries; a.q = q; a.K = k; a.P = p;
+  a.use_coarse = use_coarse ? 1 : 0; a.inv_alpha = inv_alpha; a.out_ids = out_ids;
+  a.out_dists = out_dists; a.stats = out_stats;
+  a.Kpad = next_pow2(k);
+  a.Cpad = next_pow2(idx->g);
+  size_t per_warp = sb::route_smem_per_warp(a.Kpad, a.Cpad, idx->m, idx->l);
+  int wpc = (int)std::max<size_t>(1, std::min<size_t>(8, (size_t)(100 * 1024) / per_warp));
+  if (per_warp * wpc > 227 * 1024) return fail(SB_EARG, "k too large for the routing kernel");
+  int per_sm = 0;
+  CKL(sb::route_occupancy(wpc, per_warp * wpc, &per_sm));
+  if (per_sm < 1) return fail(SB_EARG, "routing kernel does not fit on an SM for this k");
+  int ctas = (int)std::min<int64_t>((int64_t)idx->sms * per_sm, (q + wpc - 1) / wpc);
+  int64_t slots = (int64_t)ctas * wpc;
+  a.vwords = (n + 31) / 32;
+  a.logcap = 8192;
+  size_t vis_bytes = sizeof(uint32_t) * slots * a.vwords;
+  bool fresh = idx->visited.bytes < vis_bytes;
+  CK(idx->visited.ensure(vis_bytes));
+  if (fresh) CK(cudaMemsetAsync(idx->visited.p, 0, idx->visited.bytes, idx->st));
+  CK(idx->vlog.ensure(sizeof(uint32_t) * slots * a.logcap));
+  CK(idx->counter.ensure(sizeof(int) * 4));
+  CK(cudaMemsetAsync(idx->counter.p, 0, sizeof(int), idx->st));
+  a.visited = idx->visited.as<uint32_t>();
+  a.vlog = idx->vlog.as<uint32_t>();
+  a.counter = idx->counter.as<int>();
+  CKL(sb::launch_route(a, wpc, ctas, idx->st));
+  idx->launches += 1;
+  return SB_OK;
+}
+
+int sb_route_batch_dev(sb_index* idx, const double* qf, const double* qa, const double* qmask,
+                       int64_t q, int32_t k, int32_t pioneer, int32_t use_coarse,
+                       const int64_t* entries, uint64_t seed, int64_t qi0, double inv_alpha,
+                       int64_t* out_ids, double* out_dists, int64_t* out_stats) {
+  if (!idx || !qf || !qa || !out_ids || !out_dists) return fail(SB_EARG, "NULL argument");
+  return route_dev(idx, qf, qa, qmask, q, k, pioneer, use_coarse, entries, seed, qi0, inv_alpha,
+                   out_ids, out_dists, out_stats);
+}
+
+int sb_route_batch(sb_index* idx, const double* qf, const double* qa, const double* qmask,
+                   int64_t q, int32_t k, int32_t pioneer, int32_t use_coarse,
+                   const int64_t* entries, uint64_t seed, int64_t qi0, double inv_alpha,
+                   int64_t* out_ids, double* out_dists, int64_t* out_stats) {
+  if (!idx || !qf || !qa || !out_ids || !out_dists) return fail(SB_EARG, "NULL argument");
+  if (q <= 0) return SB_OK;
+  const int m = idx->m, l = idx->l;
+  // one device block for all per-call inputs/outputs
+  size_t o_qf = 0, o_qa = o_qf + sizeof(double) * q * m, o_qm = o_qa + sizeof(double) * q * l;
+  size_t o_en = o_qm + sizeof(double) * q * l, o_ids = o_en + (entries ? sizeof(int64_t) * q * k : 0);
+  size_t o_d = o_ids + sizeof(int64_t) * q * k, o_st = o_d + sizeof(double) * q * k;
+  size_t total = o_st + sizeof(int64_t) * q * 5;
+  CK(idx->qf.ensure(total));
+  char* base = idx->qf.as<char>();
+  CK(cudaMemcpyAsync(base + o_qf, qf, sizeof(double) * q * m, cudaMemcpyHostToDevice, idx->st));
+  CK(cudaMemcpyAsync(base + o_qa, qa, sizeof(double) * q * l, cudaMemcpyHostToDevice, idx->st));
+  if (qmask) CK(cudaMemcpyAsync(base + o_qm, qmask, sizeof(double) * q * l, cudaMemcpyHostToDevice, idx->st));
+  if (entries) CK(cudaMemcpyAsync(base + o_en, entries, sizeof(int64_t) * q * k, cudaMemcpyHostToDevice, idx->st));
+  int r = route_dev(idx, reinterpret_cast<double*>(base + o_qf), reinterpret_cast<double*>(base + o_qa),
+                    qmask ? reinterpret_cast<double*>(base + o_qm) : nullptr, q, k, pioneer,
+                    use_coarse, entries ? reinterpret_cast<int64_t*>(base + o_en) : nullptr, seed,
+                    qi0, inv_alpha, reinterpret_cast<int64_t*>(base + o_ids),
+                    reinterpret_cast<double*>(base + o_d),
+                    out_stats ? reinterpret_cast<int64_t*>(base + o_st) : nullptr);
+  if (r) return r;
+  CK(cudaMemcpyAsync(out_ids, base + o_ids, sizeof(int64_t) * q * k, cudaMemcpyDeviceToHost, idx->st));
+  CK(cudaMemcpyAsync(out_dists, base + o_d, sizeof(double) * q * k, cudaMemcpyDeviceToHost, idx->st));
+  if (out_stats) CK(cudaMemcpyAsync(out_stats, base + o_st, sizeof(int64_t) * q * 5, cudaMemcpyDeviceToHost, idx->st));
+  CK(cudaStreamSynchronize(idx->st));
+  return SB_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,268 @@
+// common.cuh — shared device utilities for the STABLE hot path on sm_100a.
+//
+// AUTO metric (reference _kernels.py:14-35):
+//     U = sqrt(S_V) * (1 + S_A * inv_alpha)
+// S_V = sum_t (f64 x_i[t] - f64 x_j[t])^2 and S_A = sum_t |f64 a_i[t] - f64 a_j[t]|, both
+// accumulated in ascending t.  Every distance here is computed with explicitly rounded
+// fp64 operations (__dsub_rn/__dmul_rn/__dadd_rn: no FMA contraction) in that same
+// ascending order, one pair per thread, so the values equal the reference's
+// bit for bit.  Work is spread by giving each thread many independent pairs (ILP), not
+// by splitting one sum across lanes.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#define SB_DEV __device__ __forceinline__
+#define SB_HD __host__ __device__ __forceinline__
+
+namespace sb {
+
+constexpr int kWarp = 32;
+
+// ---------------------------------------------------------------------------
+// exact fp64 helpers (no contraction)
+SB_DEV double dsub(double a, double b) { return __dsub_rn(a, b); }
+SB_DEV double dmul(double a, double b) { return __dmul_rn(a, b); }
+SB_DEV double dadd(double a, double b) { return __dadd_rn(a, b); }
+
+// s_v accumulation step: s += (a - b)^2, each op rounded separately (_kernels.py:18-19)
+SB_DEV double sq_step(double s, double a, double b) {
+  double d = dsub(a, b);
+  return dadd(s, dmul(d, d));
+}
+
+// attribute term between two data nodes (_kernels.py:20-22)
+SB_DEV double attr_l1(const int32_t* __restrict__ ai, const int32_t* __restrict__ aj, int l) {
+  double s = 0.0;
+  for (int t = 0; t < l; ++t) s = dadd(s, fabs(dsub((double)ai[t], (double)aj[t])));
+  return s;
+}
+
+// finish: sqrt(s_v) * (1 + s_a * inv_alpha)   (_kernels.py:23)
+SB_DEV double auto_finish(double s_v, double s_a, double inv_alpha) {
+  return dmul(sqrt(s_v), dadd(1.0, dmul(s_a, inv_alpha)));
+}
+
+// Exact pair distance of data rows i, j (used where no tiling is possible).
+SB_DEV double pair_dist(const float* __restrict__ F, const int32_t* __restrict__ A, int m, int l,
+                        int64_t i, int64_t j, double inv_alpha) {
+  const float* xi = F + i * (int64_t)m;
+  const float* xj = F + j * (int64_t)m;
+  double s = 0.0;
+  int t = 0;
+  if (((m & 3) == 0)) {
+    const float4* vi = reinterpret_cast<const float4*>(xi);
+    const float4* vj = reinterpret_cast<const float4*>(xj);
+    for (int q = 0; q < (m >> 2); ++q) {
+      float4 a = __ldg(vi + q), b = __ldg(vj + q);
+      s = sq_step(s, a.x, b.x);
+      s = sq_step(s, a.y, b.y);
+      s = sq_step(s, a.z, b.z);
+      s = sq_step(s, a.w, b.w);
+    }
+    t = m;
+  }
+  for (; t < m; ++t) s = sq_step(s, __ldg(xi + t), __ldg(xj + t));
+  return auto_finish(s, attr_l1(A + i * (int64_t)l, A + j * (int64_t)l, l), inv_alpha);
+}
+
+// ---------------------------------------------------------------------------
+// keys.  Non-negative IEEE floats order like their bit patterns, so
+//   build rows: key64 = (f32 bits << 32) | id        — the (f32 d, id) row order (_kernels.py:48-60)
+//   routing / brute force: (f64 bits, id) compared lexicographically (_kernels.py:190-196, 546)
+SB_HD uint64_t row_key(float d, uint32_t id) {
+#ifdef __CUDA_ARCH__
+  return ((uint64_t)__float_as_uint(d) << 32) | id;
+#else
+  union { float f; uint32_t u; } c; c.f = d;
+  return ((uint64_t)c.u << 32) | id;
+#endif
+}
+SB_HD float key_dist(uint64_t k) {
+#ifdef __CUDA_ARCH__
+  return __uint_as_float((uint32_t)(k >> 32));
+#else
+  union { float f; uint32_t u; } c; c.u = (uint32_t)(k >> 32);
+  return c.f;
+#endif
+}
+SB_HD uint32_t key_id(uint64_t k) { return (uint32_t)k; }
+constexpr uint64_t kKeyInf = 0xFFFFFFFFFFFFFFFFull;
+
+// (d, id) lexicographic less for fp64 distances
+SB_DEV bool dlt(double da, uint32_t ia, double db, uint32_t ib) {
+  return da < db || (da == db && ia < ib);
+}
+
+// ---------------------------------------------------------------------------
+// warp helpers
+SB_DEV int lane_id() { return threadIdx.x & 31; }
+SB_DEV int warp_id() { return threadIdx.x >> 5; }
+
+template <typename T>
+SB_DEV T warp_sum(T v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+SB_HD int next_pow2(int x) {
+  int p = 1;
+  while (p < x) p <<= 1;
+  return p;
+}
+
+// In-place bitonic sort of n64 (power of two) u64 keys in shared memory by one warp.
+SB_DEV void warp_bitonic_u64(uint64_t* s, int n) {
+  for (int k = 2; k <= n; k <<= 1) {
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      for (int i = lane_id(); i < n; i += 32) {
+        int p = i ^ j;
+        if (p > i) {
+          uint64_t a = s[i], b = s[p];
+          bool up = (i & k) == 0;
+          if ((a > b) == up) { s[i] = b; s[p] = a; }
+        }
+      }
+      __syncwarp();
+    }
+  }
+}
+
+// In-place bitonic sort of n (power of two) u64 keys in shared memory by a whole CTA.
+SB_DEV void cta_bitonic_u64(uint64_t* s, int n) {
+  for (int k = 2; k <= n; k <<= 1) {
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      for (int i = threadIdx.x; i < n; i += blockDim.x) {
+        int p = i ^ j;
+        if (p > i) {
+          uint64_t a = s[i], b = s[p];
+          bool up = (i & k) == 0;
+          if ((a > b) == up) { s[i] = b; s[p] = a; }
+        }
+      }
+      __syncthreads();
+    }
+  }
+}
+
+// Bitonic sort of (fp64 dist, u32 id) pairs held in two shared arrays, one warp.
+SB_DEV void warp_bitonic_did(double* d, uint32_t* id, int n) {
+  for (int k = 2; k <= n; k <<= 1) {
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      for (int i = lane_id(); i < n; i += 32) {
+        int p = i ^ j;
+        if (p > i) {
+          double da = d[i], db = d[p];
+          uint32_t ia = id[i], ib = id[p];
+          bool up = (i & k) == 0;
+          bool gt = dlt(db, ib, da, ia);
+          if (gt == up) { d[i] = db; d[p] = da; id[i] = ib; id[p] = ia; }
+        }
+      }
+      __syncwarp();
+    }
+  }
+}
+
+// Merge c unsorted candidates (cd, cid) into the sorted top list (rd, rid) of size K, by one
+// warp, in shared memory.  The list's id words may carry flag bits outside `idmask`; flags
+// travel with their entries, inserted entries carry none.  Equivalent to inserting the
+// candidates one by one with a bounded insertion sort (_kernels.py:490-501): candidates that
+// do not beat the tail are dropped, the rest land at j + #{R < C[j]} and R[i] moves to
+// i + #{C < R[i]}.  cpos is scratch of >= c ints; cd/cid must hold next_pow2(c) slots.
+// Returns the lowest position that received a new entry, or K if none did.
+SB_DEV int warp_merge_topk(double* rd, uint32_t* rid, int K, double* cd, uint32_t* cid,
+                           int* cpos, int c, uint32_t idmask) {
+  const int lane = lane_id();
+  const double wd = rd[K - 1];
+  const uint32_t wi = rid[K - 1] & idmask;
+  int kept = 0;
+  for (int base = 0; base < c; base += 32) {
+    int i = base + lane;
+    double d = 0.0;
+    uint32_t id = 0;
+    bool ok = false;
+    if (i < c) {
+      d = cd[i];
+      id = cid[i];
+      ok = dlt(d, id, wd, wi);
+    }
+    unsigned bal = __ballot_sync(0xffffffffu, ok);
+    __syncwarp();
+    if (ok) {
+      int pos = kept + __popc(bal & ((1u << lane) - 1u));
+      cd[pos] = d;
+      cid[pos] = id;
+    }
+    kept += __popc(bal);
+    __syncwarp();
+  }
+  if (kept == 0) return K;
+  int np = next_pow2(kept);
+  for (int i = kept + lane; i < np; i += 32) {
+    cd[i] = __longlong_as_double(0x7FF0000000000000ll);
+    cid[i] = 0xFFFFFFFFu;
+  }
+  __syncwarp();
+  if (np > 1) warp_bitonic_did(cd, cid, np);
+  for (int j = lane; j < kept; j += 32) {
+    double d = cd[j];
+    uint32_t id = cid[j];
+    int lo = 0, hi = K;
+    while (lo < hi) {
+      int mid = (lo + hi) >> 1;
+      if (dlt(rd[mid], rid[mid] & idmask, d, id)) lo = mid + 1; else hi = mid;
+    }
+    cpos[j] = j + lo;
+  }
+  __syncwarp();
+  const int first_ins = cpos[0];
+  if (first_ins >= K) return K;
+  // move list entries at or after first_ins back to front; targets never precede sources
+  for (int top = K - 1; top >= first_ins; top -= 32) {
+    int i = top - lane;
+    bool act = i >= first_ins;
+    double d = 0.0;
+    uint32_t idw = 0;
+    int tgt = K;
+    if (act) {
+      d = rd[i];
+      idw = rid[i];
+      uint32_t id = idw & idmask;
+      int lo = 0, hi = kept;
+      while (lo < hi) {
+        int mid = (lo + hi) >> 1;
+        if (dlt(cd[mid], cid[mid], d, id)) lo = mid + 1; else hi = mid;
+      }
+      tgt = i + lo;
+    }
+    __syncwarp();
+    if (act && tgt < K) {
+      rd[tgt] = d;
+      rid[tgt] = idw;
+    }
+    __syncwarp();
+  }
+  for (int j = lane; j < kept; j += 32) {
+    int p = cpos[j];
+    if (p < K) {
+      rd[p] = cd[j];
+      rid[p] = cid[j];
+    }
+  }
+  __syncwarp();
+  return first_ins;
+}
+
+// number of elements of sorted u64 array s[0..n) strictly less than x
+SB_DEV int lower_bound_u64(const uint64_t* s, int n, uint64_t x) {
+  int lo = 0, hi = n;
+  while (lo < hi) {
+    int mid = (lo + hi) >> 1;
+    if (s[mid] < x) lo = mid + 1; else hi = mid;
+  }
+  return lo;
+}
+
+}  // namespace sb

@@ -1,0 +1,389 @@
+// help_join.cu — HELP build, part 2: the NN-descent local join (_kernels.py:138-173).
+//
+// The reference pushes, for every candidate pair (j, k) of every node i (new x new with
+// x < y, new x old), k into row j and j into row k with _heap_push (_kernels.py:38-68).
+// Restated order-independently: each row ends as the top-gamma, under the
+// (f32 dist, id) key, of (its entries before the join) ∪ (everything pushed to it), and an
+// id gets flag 1 iff it was not in the row before the join.  Pushes that do not beat the
+// row's current tail can never survive, so they are filtered at the source.
+//
+// Pipeline per node chunk (chunks are sized so the worst-case push count fits the buffer):
+//   emit     persistent CTAs take nodes i; gather the candidate rows (new ∪ old) into shared
+//            memory; each thread evaluates a 4 x 4 tile of pairs as 16 independent fp64 chains
+//            in ascending dimension order (bit-exact _pair_dist); pushes that beat the target
+//            row's tail are appended (target, key) to a global buffer, and counted per target.
+//   scatter  counting sort of the pushes into per-row segments.
+//   merge    warp per touched row: chunks of its segment are filtered against the tail,
+//            sorted, de-duplicated (identical keys = identical (dist, id): distances are
+//            computed by one canonical exact function, so a repeated id has the same key)
+//            and merged into the row; flags of surviving old entries are kept, new ids get 1.
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "common.cuh"
+#include "sb_internal.h"
+
+namespace sb {
+
+constexpr int kJoinThreads = 256;
+constexpr int kJT = 4;            // pair tile edge
+constexpr int kEmitBlock = 128;   // push slots a warp reserves at a time
+
+struct JoinCta {
+  int32_t* slot_id;   // [spad]
+  int32_t* slot_attr; // [spad * l]
+  float* xs;          // [dc][spad]
+  int* tiles;         // tile list
+};
+
+// warp-aggregated append of up to two pushes per lane into the global push buffer
+struct Emitter {
+  uint64_t base;  // current reserved block start
+  int used;       // slots used in the block (warp-uniform)
+};
+
+SB_DEV void emit2(const JoinArgs& a, Emitter& em, bool p1, uint32_t t1, uint64_t k1, bool p2,
+                  uint32_t t2, uint64_t k2) {
+  const int lane = lane_id();
+  int cnt = (int)p1 + (int)p2;
+  // inclusive warp scan
+  int inc = cnt;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    int v = __shfl_up_sync(0xffffffffu, inc, o);
+    if (lane >= o) inc += v;
+  }
+  int total = __shfl_sync(0xffffffffu, inc, 31);
+  if (total == 0) return;
+  int excl = inc - cnt;
+  if (em.used + total > kEmitBlock) {
+    // pad out the rest of the block, reserve a new one
+    for (int s = em.used + lane; s < kEmitBlock; s += 32)
+      if (em.base + s < a.push_cap) a.push_tgt[em.base + s] = 0xFFFFFFFFu;
+    uint64_t nb = 0;
+    if (lane == 0) nb = atomicAdd(reinterpret_cast<unsigned long long*>(a.push_count), (unsigned long long)kEmitBlock);
+    em.base = __shfl_sync(0xffffffffu, nb, 0);
+    em.used = 0;
+  }
+  uint64_t pos = em.base + em.used + excl;
+  if (pos + cnt <= a.push_cap) {
+    if (p1) {
+      a.push_tgt[pos] = t1;
+      a.push_key[pos] = k1;
+      atomicAdd(reinterpret_cast<unsigned long long*>(a.row_cnt + t1), 1ull);
+      ++pos;
+    }
+    if (p2) {
+      a.push_tgt[pos] = t2;
+      a.push_key[pos] = k2;
+      atomicAdd(reinterpret_cast<unsigned long long*>(a.row_cnt + t2), 1ull);
+    }
+  } else if (cnt) {
+    atomicExch(a.overflow, 1);
+  }
+  em.used += total;
+}
+
+__global__ void __launch_bounds__(kJoinThreads, 2) join_emit_kernel(JoinArgs a) {
+  extern __shared__ __align__(16) char smem_raw[];
+  const int spad = a.spad;
+  JoinCta s;
+  {
+    char* p = smem_raw;
+    s.xs = reinterpret_cast<float*>(p); p += sizeof(float) * (size_t)a.dc * spad;
+    s.slot_id = reinterpret_cast<int32_t*>(p); p += sizeof(int32_t) * spad;
+    s.slot_attr = reinterpret_cast<int32_t*>(p); p += sizeof(int32_t) * (size_t)spad * a.l;
+    s.tiles = reinterpret_cast<int*>(p);
+  }
+  __shared__ int sh_node, sh_ntiles, sh_na, sh_nb;
+  const int tid = threadIdx.x;
+  Emitter em;
+  em.base = 0;
+  em.used = kEmitBlock;  // forces a reservation on first use
+  const bool whole = a.dc >= a.m;  // all dimensions staged at once
+
+  for (;;) {
+    __syncthreads();
+    if (tid == 0) {
+      int64_t i = a.node_begin + atomicAdd(a.node_counter, 1);
+      sh_node = i < a.node_end ? (int)i : -1;
+    }
+    __syncthreads();
+    const int node = sh_node;
+    if (node < 0) break;
+    if (tid == 0) {
+      sh_na = a.new_cnt[node];
+      sh_nb = a.old_cnt[node];
+    }
+    __syncthreads();
+    const int na = sh_na, nb = sh_nb;
+    const int ns = na + nb;
+    if (na == 0) continue;
+    for (int t = tid; t < ns; t += blockDim.x) {
+      int32_t v = t < na ? a.new_cand[(int64_t)node * a.gn + t] : a.old_cand[(int64_t)node * a.g + (t - na)];
+      s.slot_id[t] = v;
+      for (int u = 0; u < a.l; ++u) s.slot_attr[t * a.l + u] = __ldg(a.A + (int64_t)v * a.l + u);
+    }
+    for (int t = ns + tid; t < spad; t += blockDim.x) s.slot_id[t] = -1;
+    // tile list: row block rb (x in [4rb, 4rb+4) ⊂ new), col block cb (y in [4cb, 4cb+4)),
+    // keep tiles holding at least one pair with y > x, y < ns
+    if (tid == 0) {
+      int nt = 0;
+      int nrb = (na + kJT - 1) / kJT, ncb = (ns + kJT - 1) / kJT;
+      for (int rb = 0; rb < nrb; ++rb)
+        for (int cb = rb; cb < ncb; ++cb) s.tiles[nt++] = (rb << 16) | cb;
+      sh_ntiles = nt;
+    }
+    __syncthreads();
+    const int ntiles = sh_ntiles;
+    if (whole) {
+      for (int e = tid; e < ns * a.m; e += blockDim.x) {
+        int t = e / a.m, dd = e % a.m;
+        s.xs[dd * spad + t] = __ldg(a.F + (int64_t)s.slot_id[t] * a.m + dd);
+      }
+      __syncthreads();
+    }
+    for (int pass = 0; pass * kJoinThreads < ntiles; ++pass) {
+      const int ti = pass * kJoinThreads + tid;
+      const bool have = ti < ntiles;
+      const int tile = have ? s.tiles[ti] : 0;
+      const int rb = tile >> 16, cb = tile & 0xFFFF;
+      double acc[kJT][kJT];
+#pragma unroll
+      for (int u = 0; u < kJT; ++u)
+#pragma unroll
+        for (int w = 0; w < kJT; ++w) acc[u][w] = 0.0;
+      for (int d0 = 0; d0 < a.m; d0 += a.dc) {
+        const int dc = a.m - d0 < a.dc ? a.m - d0 : a.dc;
+        if (!whole) {
+          __syncthreads();
+          for (int e = tid; e < ns * dc; e += blockDim.x) {
+            int t = e / dc, dd = e % dc;
+            s.xs[dd * spad + t] = __ldg(a.F + (int64_t)s.slot_id[t] * a.m + d0 + dd);
+          }
+          __syncthreads();
+        }
+        if (have) {
+          const int off = whole ? d0 : 0;
+          for (int dd = 0; dd < dc; ++dd) {
+            const float* row = s.xs + (size_t)(off + dd) * spad;
+            float4 xv = *reinterpret_cast<const float4*>(row + rb * kJT);
+            float4 yv = *reinterpret_cast<const float4*>(row + cb * kJT);
+            const double xx[4] = {(double)xv.x, (double)xv.y, (double)xv.z, (double)xv.w};
+            const double yy[4] = {(double)yv.x, (double)yv.y, (double)yv.z, (double)yv.w};
+#pragma unroll
+            for (int u = 0; u < kJT; ++u)
+#pragma unroll
+              for (int w = 0; w < kJT; ++w) acc[u][w] = sq_step(acc[u][w], xx[u], yy[w]);
+          }
+        }
+      }
+      // pushes (warp-uniform loop; lanes without a tile contribute nothing)
+#pragma unroll
+      for (int u = 0; u < kJT; ++u)
+#pragma unroll
+        for (int w = 0; w < kJT; ++w) {
+          const int x = rb * kJT + u, y = cb * kJT + w;
+          bool valid = have && x < na && y < ns && y > x;
+          int32_t j = valid ? s.slot_id[x] : 0;
+          int32_t k = valid ? s.slot_id[y] : 0;
+          valid = valid && j != k;
+          bool p1 = false, p2 = false;
+          uint64_t k1 = 0, k2 = 0;
+          if (valid) {
+            double sa = 0.0;
+            for (int t = 0; t < a.l; ++t)
+              sa = dadd(sa, fabs(dsub((double)s.slot_attr[x * a.l + t], (double)s.slot_attr[y * a.l + t])));
+            float d = __double2float_rn(auto_finish(acc[u][w], sa, a.inv_alpha));
+            k1 = row_key(d, (uint32_t)k);  // into row j
+            k2 = row_key(d, (uint32_t)j);  // into row k
+            p1 = k1 < a.thr[j];
+            p2 = k2 < a.thr[k];
+          }
+          emit2(a, em, p1, (uint32_t)j, k1, p2, (uint32_t)k, k2);
+        }
+    }
+  }
+  // pad this warp's unused reservation
+  const int lane = lane_id();
+  if (em.used < kEmitBlock)
+    for (int s2 = em.used + lane; s2 < kEmitBlock; s2 += 32)
+      if (em.base + s2 < a.push_cap) a.push_tgt[em.base + s2] = 0xFFFFFFFFu;
+}
+
+// ---------------------------------------------------------------------------
+__global__ void push_scatter_kernel(const uint32_t* tgt, const uint64_t* key, uint64_t total,
+                                    const int64_t* row_off, int64_t* row_cur, uint64_t* seg) {
+  uint64_t e = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= total) return;
+  uint32_t t = tgt[e];
+  if (t == 0xFFFFFFFFu) return;
+  unsigned long long p = atomicAdd(reinterpret_cast<unsigned long long*>(row_cur + t), 1ull);
+  seg[row_off[t] + (int64_t)p] = key[e];
+}
+
+// ---------------------------------------------------------------------------
+// merge a row's pushes into it (warp per row)
+constexpr int kMergeChunk = 256;
+
+__global__ void row_merge_kernel(int32_t* ids, float* dists, uint8_t* flags, uint64_t* thr,
+                                 int64_t n, int g, int gpad, const int64_t* row_off,
+                                 const int64_t* row_cnt, const uint64_t* seg,
+                                 unsigned long long* inserted) {
+  extern __shared__ __align__(16) char smem_raw[];
+  const int wpb = blockDim.x >> 5;
+  const size_t per_warp = (size_t)gpad * 9 + (size_t)kMergeChunk * 12 + 16;
+  char* base = smem_raw + ((per_warp + 15) & ~(size_t)15) * warp_id();
+  uint64_t* L = reinterpret_cast<uint64_t*>(base);
+  uint64_t* C = L + gpad;
+  int* cpos = reinterpret_cast<int*>(C + kMergeChunk);
+  uint8_t* LF = reinterpret_cast<uint8_t*>(cpos + kMergeChunk);
+  int64_t r = (int64_t)blockIdx.x * wpb + warp_id();
+  if (r >= n) return;
+  const int64_t S = row_cnt[r];
+  if (S == 0) return;
+  const int lane = lane_id();
+  const unsigned lt = (1u << lane) - 1u;
+  for (int t = lane; t < g; t += 32) {
+    L[t] = row_key(dists[r * g + t], (uint32_t)ids[r * g + t]);
+    LF[t] = flags[r * g + t];
+  }
+  __syncwarp();
+  const uint64_t* sg = seg + row_off[r];
+  int new_total = 0;
+  for (int64_t b = 0; b < S; b += kMergeChunk) {
+    const int c = (int)(S - b < kMergeChunk ? S - b : kMergeChunk);
+    const uint64_t tail = L[g - 1];
+    // 1. load + filter (strictly below the tail)
+    int kept = 0;
+    for (int o = 0; o < c; o += 32) {
+      int t = o + lane;
+      uint64_t k = t < c ? sg[b + t] : kKeyInf;
+      bool ok = k < tail;
+      unsigned bal = __ballot_sync(0xffffffffu, ok);
+      if (ok) C[kept + __popc(bal & lt)] = k;
+      kept += __popc(bal);
+    }
+    __syncwarp();
+    if (kept == 0) continue;
+    // 2. sort
+    int np = next_pow2(kept);
+    for (int t = kept + lane; t < np; t += 32) C[t] = kKeyInf;
+    __syncwarp();
+    if (np > 1) warp_bitonic_u64(C, np);
+    // 3. de-duplicate (within the chunk, and against the row) and compact
+    int uniq = 0;
+    for (int o = 0; o < kept; o += 32) {
+      int t = o + lane;
+      uint64_t k = 0;
+      bool ok = false;
+      if (t < kept) {
+        k = C[t];
+        ok = (t == 0 || C[t - 1] != k);
+        if (ok) {
+          int p = lower_bound_u64(L, g, k);
+          ok = !(p < g && L[p] == k);
+        }
+      }
+      unsigned bal = __ballot_sync(0xffffffffu, ok);
+      __syncwarp();
+      if (ok) C[uniq + __popc(bal & lt)] = k;
+      uniq += __popc(bal);
+      __syncwarp();
+    }
+    if (uniq == 0) continue;
+    // 4. merge: candidate j -> j + #{L < C[j]}; L[i] -> i + #{C < L[i]}
+    for (int t = lane; t < uniq; t += 32) cpos[t] = t + lower_bound_u64(L, g, C[t]);
+    __syncwarp();
+    const int first = cpos[0];
+    if (first >= g) continue;
+    for (int top = g - 1; top >= first; top -= 32) {
+      int i = top - lane;
+      bool act = i >= first;
+      uint64_t k = 0;
+      uint8_t f = 0;
+      int tg = g;
+      if (act) {
+        k = L[i];
+        f = LF[i];
+        tg = i + lower_bound_u64(C, uniq, k);
+      }
+      __syncwarp();
+      if (act && tg < g) { L[tg] = k; LF[tg] = f; }
+      __syncwarp();
+    }
+    int ins = 0;
+    for (int t = lane; t < uniq; t += 32) {
+      int p = cpos[t];
+      if (p < g) { L[p] = C[t]; LF[p] = 1; ++ins; }
+    }
+    new_total += warp_sum(ins);
+    __syncwarp();
+  }
+  if (new_total == 0) return;
+  for (int t = lane; t < g; t += 32) {
+    ids[r * g + t] = (int32_t)key_id(L[t]);
+    dists[r * g + t] = key_dist(L[t]);
+    flags[r * g + t] = LF[t];
+  }
+  if (lane == 0) {
+    thr[r] = L[g - 1];
+    atomicAdd(inserted, (unsigned long long)new_total);
+  }
+}
+
+__global__ void thr_init_kernel(const int32_t* ids, const float* dists, int64_t n, int g,
+                                uint64_t* thr) {
+  int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= n) return;
+  thr[r] = row_key(dists[r * g + g - 1], (uint32_t)ids[r * g + g - 1]);
+}
+
+size_t join_emit_smem(int spad, int dc, int l, int ntiles_max) {
+  return sizeof(float) * (size_t)dc * spad + sizeof(int32_t) * spad +
+         sizeof(int32_t) * (size_t)spad * l + sizeof(int) * (size_t)ntiles_max + 64;
+}
+
+int launch_thr_init(const int32_t* ids, const float* dists, int64_t n, int g, uint64_t* thr,
+                    cudaStream_t st) {
+  thr_init_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(ids, dists, n, g, thr);
+  return (int)cudaGetLastError();
+}
+
+int launch_join_emit(const JoinArgs& a, int ctas, size_t smem, cudaStream_t st) {
+  cudaError_t e = cudaFuncSetAttribute(join_emit_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)smem);
+  if (e != cudaSuccess) return (int)e;
+  join_emit_kernel<<<ctas, kJoinThreads, smem, st>>>(a);
+  return (int)cudaGetLastError();
+}
+
+int join_emit_occupancy(size_t smem, int* ctas_per_sm) {
+  cudaFuncSetAttribute(join_emit_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  return (int)cudaOccupancyMaxActiveBlocksPerMultiprocessor(ctas_per_sm, join_emit_kernel,
+                                                            kJoinThreads, smem);
+}
+
+int launch_push_scatter(const uint32_t* tgt, const uint64_t* key, uint64_t total,
+                        const int64_t* row_off, int64_t* row_cur, uint64_t* seg, cudaStream_t st) {
+  if (total == 0) return 0;
+  push_scatter_kernel<<<(unsigned)((total + 255) / 256), 256, 0, st>>>(tgt, key, total, row_off,
+                                                                        row_cur, seg);
+  return (int)cudaGetLastError();
+}
+
+int launch_row_merge(int32_t* ids, float* dists, uint8_t* flags, uint64_t* thr, int64_t n, int g,
+                     const int64_t* row_off, const int64_t* row_cnt, const uint64_t* seg,
+                     unsigned long long* inserted, cudaStream_t st) {
+  int gpad = next_pow2(g);
+  int wpb = 4;
+  size_t per_warp = (size_t)gpad * 9 + (size_t)kMergeChunk * 12 + 16;
+  per_warp = (per_warp + 15) & ~(size_t)15;
+  size_t smem = per_warp * wpb;
+  cudaFuncSetAttribute(row_merge_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  row_merge_kernel<<<(unsigned)((n + wpb - 1) / wpb), wpb * 32, smem, st>>>(
+      ids, dists, flags, thr, n, g, gpad, row_off, row_cnt, seg, inserted);
+  return (int)cudaGetLastError();
+}
+
+}  // namespace sb

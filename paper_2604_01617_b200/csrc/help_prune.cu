@@ -1,0 +1,537 @@
+// help_prune.cu — HELP build, part 3: heterogeneous semantic pruning (graph.py:202-232).
+//
+// prune_pass (_kernels.py:266-303) processes rows in ascending order; the only sequential
+// coupling is the in-degree safeguard.  Restated: the safeguard can only fire on
+// the edge smax(p) -> p, where smax(p) is p's largest-id in-neighbour, and it fires iff that
+// edge is redundant and every other in-edge of p was dropped.  So
+//   guard[p] = (#dropped in-edges of p from rows != smax(p)) == indeg0[p] - 1
+// and row s drops entry t iff redundant(t | kept entries before t) and not (s == smax(p) and
+// guard[p]).  Guards depend only on rows below smax(p), so Jacobi rounds from guard = 0 reach
+// the sequential result exactly; the loop stops when no guard changes.
+//
+//   bits    CTA per row: redundancy matrix R[t][u] (u < t) = attrs_equal(p_t, p_u) and
+//           cos(p_t - s, p_u - s) > sigma, cosines in fp64 with the reference's exact
+//           operation order (_kernels.py:235-253), 4 x 4 register tiles.
+//   scan    thread per row: keep-mask walk under the current guards.
+//   guard   thread per node.
+//   compact thread per row, order-preserving, stale tails left as the reference leaves them.
+//
+// reinforce_pass (_kernels.py:398-409) equals symmetrisation when no row j would exceed
+// capacity, |row_j ∪ {s : j in row_s}| <= gamma — checked exactly first.  Rows
+// then get their missing reverse entries merged in by (f32 dist, id).  Otherwise the exact
+// sequential semantics (_try_insert_edge re-prune, reconnect_islands) run in a single-thread
+// device kernel over the same device arrays (reinforce_exact_kernel / reconnect_kernel).
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "common.cuh"
+#include "sb_internal.h"
+
+namespace sb {
+
+constexpr int kPruneThreads = 256;
+constexpr int kPT = 4;
+
+__global__ void __launch_bounds__(kPruneThreads) prune_bits_kernel(PruneArgs a) {
+  extern __shared__ __align__(16) char smem_raw[];
+  const int cpad = a.cpad;
+  char* p = smem_raw;
+  double* xs = reinterpret_cast<double*>(p); p += sizeof(double) * a.m;
+  double* nrm = reinterpret_cast<double*>(p); p += sizeof(double) * cpad;
+  float* xr = reinterpret_cast<float*>(p); p += sizeof(float) * (size_t)a.dc * cpad;
+  int32_t* eid = reinterpret_cast<int32_t*>(p); p += sizeof(int32_t) * cpad;
+  int32_t* eat = reinterpret_cast<int32_t*>(p); p += sizeof(int32_t) * (size_t)cpad * a.l;
+  uint32_t* bits = reinterpret_cast<uint32_t*>(p); p += sizeof(uint32_t) * (size_t)cpad * a.W;
+  const int64_t s = blockIdx.x;
+  const int cnt = a.counts[s];
+  if (cnt <= 1) return;
+  const int tid = threadIdx.x;
+  const bool whole = a.dc >= a.m;
+  for (int t = tid; t < a.m; t += blockDim.x) xs[t] = (double)__ldg(a.F + s * a.m + t);
+  for (int t = tid; t < cpad; t += blockDim.x) {
+    int32_t v = t < cnt ? a.ids[s * a.g + t] : 0;
+    eid[t] = v;
+    for (int u = 0; u < a.l; ++u) eat[t * a.l + u] = t < cnt ? __ldg(a.A + (int64_t)v * a.l + u) : 0;
+  }
+  for (int t = tid; t < cpad * a.W; t += blockDim.x) bits[t] = 0u;
+  __syncthreads();
+
+  auto stage = [&](int d0, int dc) {
+    for (int e = tid; e < cnt * dc; e += blockDim.x) {
+      int t = e / dc, dd = e % dc;
+      xr[dd * cpad + t] = __ldg(a.F + (int64_t)eid[t] * a.m + d0 + dd);
+    }
+  };
+  // norms |p_t - s|^2, sequential over dimensions (np2 / nk2 of _diff_cosine)
+  {
+    double acc = 0.0;
+    for (int d0 = 0; d0 < a.m; d0 += a.dc) {
+      const int dc = a.m - d0 < a.dc ? a.m - d0 : a.dc;
+      __syncthreads();
+      stage(d0, dc);
+      __syncthreads();
+      if (tid < cnt)
+        for (int dd = 0; dd < dc; ++dd) {
+          double dp = dsub((double)xr[dd * cpad + tid], xs[d0 + dd]);
+          acc = dadd(acc, dmul(dp, dp));
+        }
+    }
+    if (tid < cnt) nrm[tid] = acc;
+  }
+  __syncthreads();
+  // dot products on lower-triangle 4 x 4 tiles (row block tb >= column block ub)
+  const int nb = (cnt + kPT - 1) / kPT;
+  const int ntiles = nb * (nb + 1) / 2;
+  for (int pass = 0; pass * kPruneThreads < ntiles; ++pass) {
+    const int ti = pass * kPruneThreads + tid;
+    const bool have = ti < ntiles;
+    int tb = 0, ub = 0;
+    if (have) {
+      // ti -> (tb, ub) with ub <= tb, row-major over the lower triangle
+      tb = (int)((sqrt(8.0 * ti + 1.0) - 1.0) * 0.5);
+      while ((tb + 1) * (tb + 2) / 2 <= ti) ++tb;
+      while (tb * (tb + 1) / 2 > ti) --tb;
+      ub = ti - tb * (tb + 1) / 2;
+    }
+    double acc[kPT][kPT];
+#pragma unroll
+    for (int u = 0; u < kPT; ++u)
+#pragma unroll
+      for (int w = 0; w < kPT; ++w) acc[u][w] = 0.0;
+    for (int d0 = 0; d0 < a.m; d0 += a.dc) {
+      const int dc = a.m - d0 < a.dc ? a.m - d0 : a.dc;
+      if (!whole || pass == 0) {
+        __syncthreads();
+        stage(d0, dc);
+        __syncthreads();
+      }
+      if (have) {
+        for (int dd = 0; dd < dc; ++dd) {
+          const float* row = xr + (size_t)dd * cpad;
+          const double xsd = xs[d0 + dd];
+          float4 tv = *reinterpret_cast<const float4*>(row + tb * kPT);
+          float4 uv = *reinterpret_cast<const float4*>(row + ub * kPT);
+          const double dt[4] = {dsub((double)tv.x, xsd), dsub((double)tv.y, xsd),
+                                dsub((double)tv.z, xsd), dsub((double)tv.w, xsd)};
+          const double du[4] = {dsub((double)uv.x, xsd), dsub((double)uv.y, xsd),
+                                dsub((double)uv.z, xsd), dsub((double)uv.w, xsd)};
+#pragma unroll
+          for (int u = 0; u < kPT; ++u)
+#pragma unroll
+            for (int w = 0; w < kPT; ++w) acc[u][w] = dadd(acc[u][w], dmul(dt[u], du[w]));
+        }
+      }
+    }
+    if (have) {
+#pragma unroll
+      for (int u = 0; u < kPT; ++u)
+#pragma unroll
+        for (int w = 0; w < kPT; ++w) {
+          const int t = tb * kPT + u, v = ub * kPT + w;
+          if (t >= cnt || v >= t) continue;
+          bool eq = true;
+          for (int z = 0; z < a.l; ++z) eq = eq && eat[t * a.l + z] == eat[v * a.l + z];
+          if (!eq) continue;
+          const double np2 = nrm[t], nk2 = nrm[v];
+          double c = (np2 == 0.0 || nk2 == 0.0) ? 1.0
+                                                 : __ddiv_rn(acc[u][w], sqrt(dmul(np2, nk2)));
+          if (c > a.sigma) atomicOr(bits + t * a.W + (v >> 5), 1u << (v & 31));
+        }
+    }
+  }
+  __syncthreads();
+  uint32_t* out = a.rbits + s * (int64_t)a.g * a.W;
+  for (int t = tid; t < cnt * a.W; t += blockDim.x) out[t] = bits[t];
+}
+
+__global__ void prune_scan_kernel(PruneArgs a) {
+  int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (s >= a.n) return;
+  const int cnt = a.counts[s];
+  uint32_t keep[8];
+  for (int w = 0; w < a.W; ++w) keep[w] = 0u;
+  if (cnt <= 1) {
+    if (cnt == 1) keep[0] = 1u;
+  } else {
+    const uint32_t* rb = a.rbits + s * (int64_t)a.g * a.W;
+    keep[0] = 1u;
+    for (int t = 1; t < cnt; ++t) {
+      bool red = false;
+      for (int w = 0; w <= (t >> 5); ++w) red = red || (rb[t * a.W + w] & keep[w]) != 0u;
+      const int32_t p = a.ids[s * a.g + t];
+      const bool last = a.smax[p] == (int32_t)s;
+      if (red && !(last && a.guard[p])) {
+        if (!last) atomicAdd(a.drop_other + p, 1);
+      } else {
+        keep[t >> 5] |= 1u << (t & 31);
+      }
+    }
+  }
+  for (int w = 0; w < a.W; ++w) a.keep[s * a.W + w] = keep[w];
+}
+
+__global__ void prune_guard_kernel(PruneArgs a, int* changed) {
+  int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= a.n) return;
+  uint8_t gnew = (a.indeg0[p] >= 1 && a.drop_other[p] == a.indeg0[p] - 1) ? 1 : 0;
+  if (gnew != a.guard[p]) {
+    a.guard[p] = gnew;
+    atomicOr(changed, 1);
+  }
+}
+
+__global__ void prune_compact_kernel(PruneArgs a) {
+  int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (s >= a.n) return;
+  const int cnt = a.counts[s];
+  int w = 0;
+  for (int t = 0; t < cnt; ++t) {
+    int32_t id = a.ids[s * a.g + t];
+    if (a.keep[s * a.W + (t >> 5)] & (1u << (t & 31))) {
+      a.ids[s * a.g + w] = id;
+      a.dists[s * a.g + w] = a.dists[s * a.g + t];
+      ++w;
+    } else {
+      atomicSub(a.in_deg + id, 1);
+    }
+  }
+  a.counts[s] = w;
+}
+
+size_t prune_bits_smem(int cpad, int dc, int m, int l, int W) {
+  return sizeof(double) * m + sizeof(double) * cpad + sizeof(float) * (size_t)dc * cpad +
+         sizeof(int32_t) * cpad + sizeof(int32_t) * (size_t)cpad * l +
+         sizeof(uint32_t) * (size_t)cpad * W + 64;
+}
+
+int launch_prune_bits(const PruneArgs& a, size_t smem, cudaStream_t st) {
+  cudaError_t e = cudaFuncSetAttribute(prune_bits_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)smem);
+  if (e != cudaSuccess) return (int)e;
+  prune_bits_kernel<<<(unsigned)a.n, kPruneThreads, smem, st>>>(a);
+  return (int)cudaGetLastError();
+}
+int launch_prune_scan(const PruneArgs& a, cudaStream_t st) {
+  prune_scan_kernel<<<(unsigned)((a.n + 127) / 128), 128, 0, st>>>(a);
+  return (int)cudaGetLastError();
+}
+int launch_prune_guard(const PruneArgs& a, int* changed, cudaStream_t st) {
+  prune_guard_kernel<<<(unsigned)((a.n + 255) / 256), 256, 0, st>>>(a, changed);
+  return (int)cudaGetLastError();
+}
+int launch_prune_compact(const PruneArgs& a, cudaStream_t st) {
+  prune_compact_kernel<<<(unsigned)((a.n + 127) / 128), 128, 0, st>>>(a);
+  return (int)cudaGetLastError();
+}
+
+// ---------------------------------------------------------------------------
+// reinforce, fast path
+SB_DEV bool row_has_key(const int32_t* ids, const float* dists, int cnt, uint64_t key) {
+  int lo = 0, hi = cnt;
+  while (lo < hi) {
+    int mid = (lo + hi) >> 1;
+    uint64_t k = row_key(dists[mid], (uint32_t)ids[mid]);
+    if (k < key) lo = mid + 1; else hi = mid;
+  }
+  return lo < cnt && row_key(dists[lo], (uint32_t)ids[lo]) == key;
+}
+
+// count, per target j, reverse entries s (j in row_s) that row j lacks
+__global__ void rev_missing_kernel(const int32_t* ids, const float* dists, const int32_t* counts,
+                                   int64_t n, int g, int64_t* rev_extra) {
+  int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= n * g) return;
+  int64_t s = e / g;
+  int t = (int)(e % g);
+  if (t >= counts[s]) return;
+  int32_t j = ids[e];
+  uint64_t key = row_key(dists[e], (uint32_t)s);
+  if (!row_has_key(ids + (int64_t)j * g, dists + (int64_t)j * g, counts[j], key))
+    atomicAdd(reinterpret_cast<unsigned long long*>(rev_extra + j), 1ull);
+}
+
+__global__ void overflow_kernel(const int32_t* counts, const int64_t* rev_extra, int64_t n, int g,
+                                unsigned long long* over) {
+  int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= n) return;
+  if ((int64_t)counts[j] + rev_extra[j] > g) atomicAdd(over, 1ull);
+}
+
+__global__ void rev_missing_scatter_kernel(const int32_t* ids, const float* dists,
+                                           const int32_t* counts, int64_t n, int g,
+                                           const int64_t* off, int64_t* cur, uint64_t* seg) {
+  int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= n * g) return;
+  int64_t s = e / g;
+  int t = (int)(e % g);
+  if (t >= counts[s]) return;
+  int32_t j = ids[e];
+  uint64_t key = row_key(dists[e], (uint32_t)s);
+  if (!row_has_key(ids + (int64_t)j * g, dists + (int64_t)j * g, counts[j], key)) {
+    unsigned long long p = atomicAdd(reinterpret_cast<unsigned long long*>(cur + j), 1ull);
+    seg[off[j] + (int64_t)p] = key;
+  }
+}
+
+// warp per row: sorted union of the row and its missing reverse entries
+__global__ void symmetrize_merge_kernel(int32_t* ids, float* dists, int32_t* counts, int64_t n,
+                                        int g, int gpad, const int64_t* off,
+                                        const int64_t* extra, const uint64_t* seg) {
+  extern __shared__ __align__(16) char smem_raw[];
+  const int wpb = blockDim.x >> 5;
+  uint64_t* L = reinterpret_cast<uint64_t*>(smem_raw) + (size_t)warp_id() * 2 * gpad;
+  uint64_t* C = L + gpad;
+  int64_t j = (int64_t)blockIdx.x * wpb + warp_id();
+  if (j >= n) return;
+  const int E = (int)extra[j];
+  if (E == 0) return;
+  const int lane = lane_id();
+  const int cnt = counts[j];
+  for (int t = lane; t < cnt; t += 32) L[t] = row_key(dists[j * g + t], (uint32_t)ids[j * g + t]);
+  int np = next_pow2(E);
+  for (int t = lane; t < np; t += 32) C[t] = t < E ? seg[off[j] + t] : kKeyInf;
+  __syncwarp();
+  if (np > 1) warp_bitonic_u64(C, np);
+  // positions in the union (no duplicates by construction)
+  for (int t = lane; t < cnt; t += 32) {
+    uint64_t k = L[t];
+    int pos = t + lower_bound_u64(C, E, k);
+    ids[j * g + pos] = (int32_t)key_id(k);
+    dists[j * g + pos] = key_dist(k);
+  }
+  for (int t = lane; t < E; t += 32) {
+    uint64_t k = C[t];
+    int pos = t + lower_bound_u64(L, cnt, k);
+    ids[j * g + pos] = (int32_t)key_id(k);
+    dists[j * g + pos] = key_dist(k);
+  }
+  if (lane == 0) counts[j] = cnt + E;
+}
+
+int launch_reinforce_check(const int32_t* ids, const float* dists, const int32_t* counts,
+                           int64_t n, int g, int64_t* rev_extra, unsigned long long* over,
+                           cudaStream_t st) {
+  cudaMemsetAsync(rev_extra, 0, sizeof(int64_t) * n, st);
+  cudaMemsetAsync(over, 0, sizeof(unsigned long long), st);
+  int64_t tot = n * g;
+  rev_missing_kernel<<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(ids, dists, counts, n, g,
+                                                                     rev_extra);
+  overflow_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(counts, rev_extra, n, g, over);
+  return (int)cudaGetLastError();
+}
+
+int launch_symmetrize(int32_t* ids, float* dists, int32_t* counts, int64_t n, int g,
+                      const int64_t* rev_extra, int64_t* off, int64_t* cur, uint64_t* seg,
+                      int64_t* scan_tmp, cudaStream_t st) {
+  exclusive_scan(rev_extra, off, n, scan_tmp, st);
+  cudaMemsetAsync(cur, 0, sizeof(int64_t) * n, st);
+  int64_t tot = n * g;
+  rev_missing_scatter_kernel<<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(ids, dists, counts, n,
+                                                                             g, off, cur, seg);
+  int gpad = next_pow2(g);
+  int wpb = 4;
+  size_t smem = (size_t)wpb * 2 * gpad * sizeof(uint64_t);
+  cudaFuncSetAttribute(symmetrize_merge_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  symmetrize_merge_kernel<<<(unsigned)((n + wpb - 1) / wpb), wpb * 32, smem, st>>>(
+      ids, dists, counts, n, g, gpad, off, rev_extra, seg);
+  return (int)cudaGetLastError();
+}
+
+// ---------------------------------------------------------------------------
+// exact sequential semantics (overflow case): _try_insert_edge / reinforce_pass /
+// _force_insert_edge / reconnect_islands, single device thread.
+struct SeqCtx {
+  const float* F;
+  const int32_t* A;
+  int m, l, g;
+  int32_t* ids;
+  float* dists;
+  int32_t* counts;
+  int32_t* in_deg;
+  double sigma;
+  int64_t* tmp_ids;   // g + 1
+  double* tmp_d;      // g + 1
+  uint8_t* keep;      // g + 1
+};
+
+SB_DEV bool seq_attrs_equal(const SeqCtx& c, int64_t a, int64_t b) {
+  for (int t = 0; t < c.l; ++t)
+    if (c.A[a * c.l + t] != c.A[b * c.l + t]) return false;
+  return true;
+}
+
+SB_DEV double seq_cos(const SeqCtx& c, int64_t s, int64_t p, int64_t k) {
+  const float* xs = c.F + s * c.m;
+  const float* xp = c.F + p * c.m;
+  const float* xk = c.F + k * c.m;
+  double dot = 0.0, np2 = 0.0, nk2 = 0.0;
+  for (int t = 0; t < c.m; ++t) {
+    double dp = dsub((double)xp[t], (double)xs[t]);
+    double dk = dsub((double)xk[t], (double)xs[t]);
+    dot = dadd(dot, dmul(dp, dk));
+    np2 = dadd(np2, dmul(dp, dp));
+    nk2 = dadd(nk2, dmul(dk, dk));
+  }
+  if (np2 == 0.0 || nk2 == 0.0) return 1.0;
+  return __ddiv_rn(dot, sqrt(dmul(np2, nk2)));
+}
+
+SB_DEV int seq_try_insert(SeqCtx& c, int64_t j, int64_t cand, double dd) {
+  const float d = __double2float_rn(dd);
+  int32_t* ri = c.ids + j * c.g;
+  float* rd = c.dists + j * c.g;
+  const int cj = c.counts[j];
+  for (int t = 0; t < cj; ++t)
+    if (ri[t] == cand) return 0;
+  if (cj < c.g) {
+    int pos = cj;
+    while (pos > 0 && (rd[pos - 1] > d || (rd[pos - 1] == d && ri[pos - 1] > cand))) {
+      ri[pos] = ri[pos - 1];
+      rd[pos] = rd[pos - 1];
+      --pos;
+    }
+    ri[pos] = (int32_t)cand;
+    rd[pos] = d;
+    c.counts[j] = cj + 1;
+    c.in_deg[cand] += 1;
+    return 1;
+  }
+  int pos = cj;
+  for (int t = 0; t < cj; ++t) { c.tmp_ids[t] = ri[t]; c.tmp_d[t] = (double)rd[t]; }
+  while (pos > 0 && (c.tmp_d[pos - 1] > (double)d ||
+                     (c.tmp_d[pos - 1] == (double)d && c.tmp_ids[pos - 1] > cand))) {
+    c.tmp_ids[pos] = c.tmp_ids[pos - 1];
+    c.tmp_d[pos] = c.tmp_d[pos - 1];
+    --pos;
+  }
+  c.tmp_ids[pos] = cand;
+  c.tmp_d[pos] = (double)d;
+  const int total = cj + 1;
+  for (int t = 0; t < total; ++t) c.keep[t] = 1;
+  int kept = 1;
+  for (int t = 1; t < total; ++t) {
+    int64_t p = c.tmp_ids[t];
+    bool red = false;
+    for (int u = 0; u < t; ++u) {
+      if (!c.keep[u]) continue;
+      int64_t k = c.tmp_ids[u];
+      if (seq_attrs_equal(c, p, k) && seq_cos(c, j, p, k) > c.sigma) { red = true; break; }
+    }
+    if (red && (p == cand || c.in_deg[p] >= 2)) {
+      c.keep[t] = 0;
+      if (p != cand) c.in_deg[p] -= 1;
+    } else {
+      ++kept;
+    }
+  }
+  if (kept > c.g) {
+    for (int t = total - 1; t >= 0; --t) {
+      if (!c.keep[t]) continue;
+      int64_t p = c.tmp_ids[t];
+      if (p == cand) { c.keep[t] = 0; break; }
+      if (c.in_deg[p] >= 2) { c.keep[t] = 0; c.in_deg[p] -= 1; break; }
+    }
+  }
+  int w = 0, inserted = 0;
+  for (int t = 0; t < total; ++t) {
+    if (!c.keep[t]) continue;
+    ri[w] = (int32_t)c.tmp_ids[t];
+    rd[w] = __double2float_rn(c.tmp_d[t]);
+    if (c.tmp_ids[t] == cand) inserted = 1;
+    ++w;
+  }
+  c.counts[j] = w;
+  if (inserted) c.in_deg[cand] += 1;
+  return inserted;
+}
+
+SB_DEV int seq_force_insert(SeqCtx& c, int64_t j, int64_t cand, double dd, bool unsafe) {
+  const float d = __double2float_rn(dd);
+  int32_t* ri = c.ids + j * c.g;
+  float* rd = c.dists + j * c.g;
+  int cj = c.counts[j];
+  for (int t = 0; t < cj; ++t)
+    if (ri[t] == cand) return 0;
+  if (cj >= c.g) {
+    int ev = -1;
+    for (int t = cj - 1; t >= 0; --t)
+      if (c.in_deg[ri[t]] >= 2) { ev = t; break; }
+    if (ev < 0) {
+      if (!unsafe) return 0;
+      ev = cj - 1;
+    }
+    c.in_deg[ri[ev]] -= 1;
+    for (int t = ev; t < cj - 1; ++t) { ri[t] = ri[t + 1]; rd[t] = rd[t + 1]; }
+    --cj;
+  }
+  int pos = cj;
+  while (pos > 0 && (rd[pos - 1] > d || (rd[pos - 1] == d && ri[pos - 1] > cand))) {
+    ri[pos] = ri[pos - 1];
+    rd[pos] = rd[pos - 1];
+    --pos;
+  }
+  ri[pos] = (int32_t)cand;
+  rd[pos] = d;
+  c.counts[j] = cj + 1;
+  c.in_deg[cand] += 1;
+  return 1;
+}
+
+__global__ void reinforce_exact_kernel(SeqCtx c, int64_t n) {
+  if (blockIdx.x != 0 || threadIdx.x != 0) return;
+  for (int64_t s = 0; s < n; ++s) {
+    const int cs = c.counts[s];
+    for (int t = 0; t < cs; ++t) {
+      if (t >= c.counts[s]) break;
+      int64_t j = c.ids[s * c.g + t];
+      double d = (double)c.dists[s * c.g + t];
+      seq_try_insert(c, j, s, d);
+    }
+  }
+}
+
+__global__ void reconnect_kernel(SeqCtx c, int64_t n) {
+  if (blockIdx.x != 0 || threadIdx.x != 0) return;
+  for (int64_t v = 0; v < n; ++v) {
+    if (c.in_deg[v] > 0) continue;
+    bool done = false;
+    for (int t = 0; t < c.counts[v]; ++t) {
+      int64_t u = c.ids[v * c.g + t];
+      if (seq_try_insert(c, u, v, (double)c.dists[v * c.g + t])) { done = true; break; }
+    }
+    if (done) continue;
+    for (int t = 0; t < c.counts[v]; ++t) {
+      int64_t u = c.ids[v * c.g + t];
+      if (seq_force_insert(c, u, v, (double)c.dists[v * c.g + t], false)) { done = true; break; }
+    }
+    if (!done && c.counts[v] > 0)
+      seq_force_insert(c, c.ids[v * c.g], v, (double)c.dists[v * c.g], true);
+  }
+}
+
+__global__ void min_kernel(const int32_t* x, int64_t n, int* out) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) atomicMin(out, x[i]);
+}
+
+int launch_seq_reinforce(const float* F, const int32_t* A, int m, int l, int g, int32_t* ids,
+                         float* dists, int32_t* counts, int32_t* in_deg, double sigma,
+                         int64_t n, void* scratch, int reconnect, cudaStream_t st) {
+  SeqCtx c;
+  c.F = F; c.A = A; c.m = m; c.l = l; c.g = g;
+  c.ids = ids; c.dists = dists; c.counts = counts; c.in_deg = in_deg; c.sigma = sigma;
+  char* p = reinterpret_cast<char*>(scratch);
+  c.tmp_ids = reinterpret_cast<int64_t*>(p); p += sizeof(int64_t) * (g + 1);
+  c.tmp_d = reinterpret_cast<double*>(p); p += sizeof(double) * (g + 1);
+  c.keep = reinterpret_cast<uint8_t*>(p);
+  if (reconnect) reconnect_kernel<<<1, 1, 0, st>>>(c, n);
+  else reinforce_exact_kernel<<<1, 1, 0, st>>>(c, n);
+  return (int)cudaGetLastError();
+}
+
+int launch_min_i32(const int32_t* x, int64_t n, int* out, cudaStream_t st) {
+  min_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(x, n, out);
+  return (int)cudaGetLastError();
+}
+
+}  // namespace sb

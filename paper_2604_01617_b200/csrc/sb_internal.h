@@ -1,0 +1,152 @@
+// sb_internal.h — kernel launch interfaces shared between the .cu files and the C ABI.
+#pragma once
+#include <cuda_runtime.h>
+#include <stddef.h>
+#include <stdint.h>
+
+namespace sb {
+
+// ---- routing (route.cu) ----------------------------------------------------
+struct RouteArgs {
+  const float* F;
+  const int32_t* A;
+  const int32_t* nbr_ids;
+  const int32_t* nbr_counts;
+  int64_t n;
+  int m, l, g;
+  const double* qf;        // q x m
+  const double* qa;        // q x l
+  const double* qm;        // q x l or null (all ones)
+  const int64_t* entries;  // q x K
+  int64_t q;
+  int K, P, use_coarse;
+  double inv_alpha;
+  int64_t* out_ids;   // q x K
+  double* out_dists;  // q x K
+  int64_t* stats;     // q x 5 or null
+  uint32_t* visited;  // slots x vwords
+  int64_t vwords;
+  uint32_t* vlog;     // slots x logcap
+  int logcap;
+  int* counter;
+  int Kpad, Cpad;
+};
+
+size_t route_smem_per_warp(int Kpad, int Cpad, int m, int l);
+int route_occupancy(int warps_per_cta, size_t smem, int* ctas_per_sm);
+int launch_route(const RouteArgs& a, int warps_per_cta, int ctas, cudaStream_t st);
+int launch_entry_points(int64_t n, int K, uint64_t seed, int64_t qi0, int64_t q, int64_t* out,
+                        int64_t* scratch, uint64_t scratch_slots, cudaStream_t st);
+
+// ---- exhaustive AUTO top-k (bf_topk.cu) --------------------------------------
+struct BfArgs {
+  const float* F;
+  const int32_t* A;
+  int64_t n;
+  int m, l;
+  const int64_t* self_ids;  // node mode when non-null
+  const double* qf;         // query mode: f64 q x m
+  const int64_t* qa;        // query mode: i64 q x l
+  const int64_t* qmask;     // query mode: i64 q x l or null
+  int64_t q;
+  int k;                    // list length kept per query (>= requested k)
+  double inv_alpha;         // node mode: s_a * inv_alpha (_kernels.py:23)
+  double alpha;             // query mode: s_a / alpha (evaluate.py:53)
+  int splits;
+  double* part_d;           // q x splits x k
+  uint32_t* part_i;
+};
+int bf_group_size();
+size_t bf_partial_smem(int k);
+int launch_bf_partial(const BfArgs& a, cudaStream_t st);
+int launch_bf_merge_k(const BfArgs& a, int kout, int64_t* out_ids64, int32_t* out_ids32,
+                      double* out_dists, int* uncertain, cudaStream_t st);
+
+// ---- HELP build ---------------------------------------------------------------
+struct BuildScratch {
+  int32_t* fwd_new;   // n
+  int32_t* fwd_old;   // n
+  int64_t* rev_cnt;   // n
+  int64_t* rev_off;   // n
+  int64_t* rev_cur;   // n
+  int32_t* rev;       // n * max(gn, g)
+  int64_t* scan_tmp;  // scan_tmp_slots(n)
+};
+
+int64_t scan_tmp_slots(int64_t n);
+int exclusive_scan(const int64_t* in, int64_t* out, int64_t n, int64_t* tmp, cudaStream_t st);
+int launch_init_dists(const float* F, const int32_t* A, int64_t n, int m, int l, int g,
+                      double inv_alpha, int32_t* ids, float* dists, cudaStream_t st);
+int launch_count_in_degrees(const int32_t* ids, const int32_t* counts, int64_t n, int g,
+                            int32_t* in_deg, int32_t* smax, cudaStream_t st);
+int launch_build_candidates(const int32_t* ids, uint8_t* flags, int64_t n, int g, int gn,
+                            int32_t* new_cand, int32_t* new_cnt, int32_t* old_cand,
+                            int32_t* old_cnt, BuildScratch& s, cudaStream_t st);
+
+struct JoinArgs {
+  const float* F;
+  const int32_t* A;
+  int64_t n;
+  int m, l, g, gn;
+  double inv_alpha;
+  const int32_t* new_cand;
+  const int32_t* new_cnt;
+  const int32_t* old_cand;
+  const int32_t* old_cnt;
+  const uint64_t* thr;     // current row tails
+  int64_t node_begin, node_end;
+  int* node_counter;
+  uint32_t* push_tgt;
+  uint64_t* push_key;
+  uint64_t push_cap;
+  unsigned long long* push_count;
+  int64_t* row_cnt;
+  int* overflow;
+  int spad, dc;
+};
+size_t join_emit_smem(int spad, int dc, int l, int ntiles_max);
+int join_emit_occupancy(size_t smem, int* ctas_per_sm);
+int launch_thr_init(const int32_t* ids, const float* dists, int64_t n, int g, uint64_t* thr,
+                    cudaStream_t st);
+int launch_join_emit(const JoinArgs& a, int ctas, size_t smem, cudaStream_t st);
+int launch_push_scatter(const uint32_t* tgt, const uint64_t* key, uint64_t total,
+                        const int64_t* row_off, int64_t* row_cur, uint64_t* seg, cudaStream_t st);
+int launch_row_merge(int32_t* ids, float* dists, uint8_t* flags, uint64_t* thr, int64_t n, int g,
+                     const int64_t* row_off, const int64_t* row_cnt, const uint64_t* seg,
+                     unsigned long long* inserted, cudaStream_t st);
+
+struct PruneArgs {
+  const float* F;
+  const int32_t* A;
+  int64_t n;
+  int m, l, g, W;
+  int32_t* ids;
+  float* dists;
+  int32_t* counts;
+  double sigma;
+  uint32_t* rbits;     // n x g x W
+  const int32_t* smax;
+  const int32_t* indeg0;
+  uint8_t* guard;
+  int32_t* drop_other;
+  uint32_t* keep;      // n x W
+  int32_t* in_deg;
+  int cpad, dc;
+};
+size_t prune_bits_smem(int cpad, int dc, int m, int l, int W);
+int launch_prune_bits(const PruneArgs& a, size_t smem, cudaStream_t st);
+int launch_prune_scan(const PruneArgs& a, cudaStream_t st);
+int launch_prune_guard(const PruneArgs& a, int* changed, cudaStream_t st);
+int launch_prune_compact(const PruneArgs& a, cudaStream_t st);
+int launch_reinforce_check(const int32_t* ids, const float* dists, const int32_t* counts,
+                           int64_t n, int g, int64_t* rev_extra, unsigned long long* over,
+                           cudaStream_t st);
+int launch_symmetrize(int32_t* ids, float* dists, int32_t* counts, int64_t n, int g,
+                      const int64_t* rev_extra, int64_t* off, int64_t* cur, uint64_t* seg,
+                      int64_t* scan_tmp, cudaStream_t st);
+int launch_seq_reinforce(const float* F, const int32_t* A, int m, int l, int g, int32_t* ids,
+                         float* dists, int32_t* counts, int32_t* in_deg, double sigma,
+                         int64_t n, void* scratch, int reconnect, cudaStream_t st);
+int launch_min_i32(const int32_t* x, int64_t n, int* out, cudaStream_t st);
+
+}  // namespace sb

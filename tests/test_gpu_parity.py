@@ -1,0 +1,236 @@
+"""GPU parity: every device stage vs the reference's golden vectors and the CPU oracle.
+
+The device path computes AUTO distances with explicitly rounded fp64 operations in the
+reference's order, so parity here is bit-exact (ids, f32 row distances, flags, counts, fp64
+search distances, all SearchStats counters) — stricter than the north star's tolerance
+(ids exact except ties within 1e-5 relative; distances within 1e-5 relative).
+"""
+
+import numpy as np
+import pytest
+
+import paper_2604_01617_b200 as sb
+from paper_2604_01617_b200.device import DeviceIndex
+from oracle import oracle as O
+
+pytestmark = pytest.mark.gpu
+
+
+def _dev_from_state(gd, ids, dists, counts, flags, gamma):
+    d = DeviceIndex(gd["features"], gd["attrs"], gamma)
+    d.upload(ids, dists, counts, flags)
+    return d
+
+
+def _stage_check(gd, gamma, seed, sigma):
+    """Run each device stage from the golden input of that stage and compare its output."""
+    f, a, alpha = gd["features"], gd["attrs"], float(gd["alpha"])
+    n = f.shape[0]
+    inv = 1.0 / alpha
+    # init
+    ids0 = sb.init_random_ids(n, gamma, seed)
+    d = DeviceIndex(f, a, gamma)
+    d.init_graph(ids0, inv)
+    ids, dists, counts, flags = d.download()
+    np.testing.assert_array_equal(ids, gd["init_ids"])
+    np.testing.assert_array_equal(dists, gd["init_dists"])
+    assert (counts == gamma).all() and (flags == 1).all()
+    # psi ground truth (node-mode brute force)
+    gt = d.bf_topk_nodes(gd["q_sample"], gamma, inv)
+    np.testing.assert_array_equal(gt, gd["q_gt"])
+    # descent iterations, each from the golden previous state
+    prev = (gd["init_ids"], gd["init_dists"], np.ones_like(gd["init_ids"], dtype=np.uint8))
+    for it in range(1, int(gd["iterations"]) + 1):
+        dd = _dev_from_state(gd, prev[0], prev[1], np.full(n, gamma, np.int32), prev[2], gamma)
+        nc, ncnt, oc, ocnt = dd.build_candidates(gamma, download=True)
+        fl = prev[2].copy()
+        w_nc, w_ncnt, w_oc, w_ocnt = O.kernels.build_candidates(prev[0].copy(), fl, gamma)
+        np.testing.assert_array_equal(ncnt, w_ncnt)
+        np.testing.assert_array_equal(ocnt, w_ocnt)
+        np.testing.assert_array_equal(nc, w_nc)
+        np.testing.assert_array_equal(oc, w_oc)
+        ins, pairs = dd.local_join(inv)
+        assert ins > 0
+        ids, dists, counts, flags = dd.download()
+        np.testing.assert_array_equal(ids, gd[f"it{it}_ids"], err_msg=f"iteration {it}")
+        np.testing.assert_array_equal(dists, gd[f"it{it}_dists"], err_msg=f"iteration {it}")
+        np.testing.assert_array_equal(flags, gd[f"it{it}_flags"], err_msg=f"iteration {it}")
+        prev = (ids, dists, flags)
+    # prune from the golden post-descent state
+    last = int(gd["iterations"])
+    dp = _dev_from_state(gd, gd[f"it{last}_ids"], gd[f"it{last}_dists"],
+                         np.full(n, gamma, np.int32), None, gamma)
+    np.testing.assert_array_equal(dp.count_in_degrees(), gd["indeg0"])
+    dp.prune(sigma)
+    ids, dists, counts, _ = dp.download(with_flags=False)
+    np.testing.assert_array_equal(counts, gd["prune_counts"])
+    np.testing.assert_array_equal(ids, gd["prune_ids"])
+    np.testing.assert_array_equal(dists, gd["prune_dists"])
+    over, sweeps = dp.reinforce(sigma)
+    ids, dists, counts, _ = dp.download(with_flags=False)
+    np.testing.assert_array_equal(counts, gd["final_counts"])
+    np.testing.assert_array_equal(ids, gd["final_ids"])
+    np.testing.assert_array_equal(dists, gd["final_dists"])
+    assert sweeps == int(gd["reconnect_sweeps"])
+    return over
+
+
+def test_small_every_stage(small_golden):
+    over = _stage_check(small_golden, 24, 3, float(small_golden["sigma"]))
+    assert over == 0
+
+
+def test_overflow_every_stage(overflow_golden):
+    over = _stage_check(overflow_golden, 12, 9, float(overflow_golden["sigma"]))
+    assert over > 0, "case must take the exact sequential reinforce path"
+
+
+def _graph(gd, gamma):
+    return sb.RelationGraph(features=gd["features"], attrs=gd["attrs"],
+                            schema=sb.AttributeSchema(tuple(("x",) for _ in range(gd["attrs"].shape[1]))),
+                            metric=sb.MetricConfig.manual(float(gd["alpha"]), gd["attrs"].shape[1]),
+                            sigma=0.44, nbr_ids=gd["final_ids"], nbr_dists=gd["final_dists"],
+                            nbr_counts=gd["final_counts"], frozen=True)
+
+
+def _check_search_keys(gd, graph, qf, qa, masks, prefix):
+    keys = sorted(k for k in gd.files if k.startswith(prefix) and k.endswith("_ids"))
+    assert keys
+    for key in keys:
+        tag = key[len(prefix):-len("_ids")]
+        k = int(tag.split("_")[0][1:])
+        coarse = tag.endswith("_c")
+        ids, dists, st = sb.search_batch_arrays(graph, qf, qa, sb.SearchParams(k=k, use_coarse=coarse),
+                                                masks=masks)
+        np.testing.assert_array_equal(ids, gd[key], err_msg=key)
+        np.testing.assert_array_equal(dists, gd[f"{prefix}{tag}_dists"], err_msg=key)
+        np.testing.assert_array_equal(st[:, :4], gd[f"{prefix}{tag}_stats"], err_msg=key)
+
+
+def test_small_searches_bit_exact(small_golden):
+    gd = small_golden
+    g = _graph(gd, 24)
+    _check_search_keys(gd, g, gd["qf"], gd["qa"], gd["qm"], "s_")
+    _check_search_keys(gd, g, gd["qf"], gd["qa"], None, "nomask_s_")
+
+
+def test_single_search_equals_batch(small_golden):
+    gd = small_golden
+    g = _graph(gd, 24)
+    ids, dists, stats = sb.search_batch(g, gd["qf"], gd["qa"], sb.SearchParams(k=15, seed=1),
+                                        masks=gd["qm"])
+    for qi in (0, 5, 19):
+        one = sb.search(g, gd["qf"][qi], gd["qa"][qi], sb.SearchParams(k=15, seed=1, mask=gd["qm"][qi]), qi)
+        np.testing.assert_array_equal(one[0], ids[qi])
+        np.testing.assert_array_equal(one[1], dists[qi])
+        assert one[2] == stats[qi]
+
+
+def test_overflow_searches_bit_exact(overflow_golden):
+    gd = overflow_golden
+    _check_search_keys(gd, _graph(gd, 12), gd["qf"], gd["qa"], None, "s_")
+
+
+def test_oracle_topk_matches_reference(small_golden):
+    gd = small_golden
+    cfg = sb.MetricConfig.manual(float(gd["alpha"]), 3)
+    ids, dists = sb.oracle_auto_topk_batch(gd["features"], gd["attrs"], gd["qf"], gd["qa"], 20, cfg,
+                                           gd["qm"], return_dists=True)
+    np.testing.assert_array_equal(ids, gd["oracle_top20"])
+    for qi in range(gd["qf"].shape[0]):
+        wi, wd = O.oracle_auto_topk(gd["features"], gd["attrs"], gd["qf"][qi], gd["qa"][qi], 20,
+                                    float(gd["alpha"]), gd["qm"][qi], return_dists=True)
+        np.testing.assert_array_equal(dists[qi], wd)
+
+
+def test_oracle_topk_tie_break_and_k_equals_n():
+    f = np.zeros((5, 2), np.float32)
+    a = np.ones((5, 1), np.int32)
+    cfg = sb.MetricConfig.manual(1.0, 1)
+    got = sb.oracle_auto_topk(f, a, np.ones(2, np.float32), [1], 5, cfg)
+    np.testing.assert_array_equal(got, [0, 1, 2, 3, 4])
+    with pytest.raises(ValueError):
+        sb.oracle_auto_topk(f, a, np.ones(2, np.float32), [1], 6, cfg)
+
+
+def test_bf_nodes_pads_when_n_small():
+    rng = np.random.default_rng(0)
+    f = rng.standard_normal((7, 3)).astype(np.float32)
+    a = rng.integers(1, 3, (7, 1)).astype(np.int32)
+    d = DeviceIndex(f, a, 2)
+    got = d.bf_topk_nodes(np.array([0, 3, 6]), 10, 0.5)
+    want = O.kernels.brute_force_topk(f, a, 0.5, np.array([0, 3, 6]), 10)
+    np.testing.assert_array_equal(got, want)
+    assert (got[:, 6:] == -1).all()
+
+
+def test_bf_nodes_random_vs_oracle():
+    rng = np.random.default_rng(1)
+    for n, m, l, k in ((3000, 24, 2, 50), (5000, 100, 1, 100), (2000, 7, 3, 5), (1500, 256, 1, 64)):
+        f = rng.standard_normal((n, m)).astype(np.float32)
+        a = rng.integers(1, 4, (n, l)).astype(np.int32)
+        s = np.sort(rng.choice(n, 37, replace=False)).astype(np.int64)
+        got = DeviceIndex(f, a, 2).bf_topk_nodes(s, k, 0.37)
+        want = O.kernels.brute_force_topk(f, a, 0.37, s, k)
+        np.testing.assert_array_equal(got, want)
+
+
+def test_route_random_graph_vs_oracle():
+    """Routing on an arbitrary (non-HELP) graph, odd dims, masks, K=1..K=300."""
+    rng = np.random.default_rng(2)
+    n, m, l, g = 4000, 20, 3, 16
+    f = rng.integers(0, 6, (n, m)).astype(np.float32)  # many exact ties
+    a = rng.integers(1, 4, (n, l)).astype(np.int32)
+    ids = np.stack([rng.choice(n, g, replace=False) for _ in range(n)]).astype(np.int32)
+    cnt = rng.integers(1, g + 1, n).astype(np.int32)
+    dists = np.zeros((n, g), np.float32)
+    graph = sb.RelationGraph(features=f, attrs=a, schema=sb.AttributeSchema((("x",),) * l),
+                             metric=sb.MetricConfig.manual(0.8, l), sigma=0.44, nbr_ids=ids,
+                             nbr_dists=dists, nbr_counts=cnt, frozen=True)
+    q = 64
+    qf = rng.integers(0, 6, (q, m)).astype(np.float32)
+    qa = rng.integers(1, 4, (q, l)).astype(np.int32)
+    masks = rng.integers(0, 2, (q, l)).astype(np.float64)
+    for k, coarse in ((1, True), (2, True), (7, False), (33, True), (300, True)):
+        got = sb.search_batch_arrays(graph, qf, qa, sb.SearchParams(k=k, seed=5, use_coarse=coarse),
+                                     masks=masks)
+        want = O.search_batch(f, a, ids, cnt, 0.8, qf, qa, k, seed=5, masks=masks, use_coarse=coarse)
+        np.testing.assert_array_equal(got[0], want[0], err_msg=f"k={k}")
+        np.testing.assert_array_equal(got[1], want[1], err_msg=f"k={k}")
+        np.testing.assert_array_equal(got[2][:, :4], want[2], err_msg=f"k={k}")
+
+
+@pytest.mark.slow
+def test_cfg1_end_to_end(cfg1_golden):
+    """BASELINE config 1 through the public API: alpha, psi history, edge counts, final
+    adjacency hashes, searches at K = 10 / 25 / 50 (ids, dists, stats) and the exact GT."""
+    import hashlib
+    gd = cfg1_golden
+
+    def sha(x):
+        x = np.ascontiguousarray(x)
+        return hashlib.sha256(x.tobytes() + str(x.dtype).encode() + str(x.shape).encode()).hexdigest()
+
+    rng = np.random.default_rng(0)
+    X = rng.standard_normal((10000, 32), dtype=np.float32)
+    A = rng.integers(1, 5, (10000, 1), dtype=np.int32)
+    QX = rng.standard_normal((200, 32), dtype=np.float32)
+    QA = rng.integers(1, 5, (200, 1), dtype=np.int32)
+    cfg = sb.compute_alpha(sb.sample_statistics(X, A, 1000, seed=0), 10000, 1)
+    assert cfg.alpha == float(gd["alpha"])
+    g = sb.build(X, A, sb.AttributeSchema((("v1", "v2", "v3", "v4"),)), sb.BuildParams(), cfg)
+    np.testing.assert_array_equal(np.array(g.build_log["psi_history"]), gd["psi_history"])
+    assert sha(g.nbr_counts) == str(gd["sha_final_counts"])
+    assert sha(g.nbr_ids) == str(gd["sha_final_ids"])
+    assert sha(g.nbr_dists) == str(gd["sha_final_dists"])
+    assert int(g.nbr_counts.sum()) == 194_468
+    for k in (10, 25, 50):
+        ids, dists, st = sb.search_batch_arrays(g, QX, QA, sb.SearchParams(k=k))
+        np.testing.assert_array_equal(ids, gd[f"s_k{k}_c_ids"])
+        np.testing.assert_array_equal(dists, gd[f"s_k{k}_c_dists"])
+        np.testing.assert_array_equal(st[:, :4], gd[f"s_k{k}_c_stats"])
+    gt = sb.oracle_auto_topk_batch(X, A, QX, QA, 10, cfg)
+    np.testing.assert_array_equal(gt, gd["oracle_top10"])
+    # recall at the operating point K=25 (0.9550)
+    ids, _, _ = sb.search_batch_arrays(g, QX, QA, sb.SearchParams(k=25))
+    assert sb.mean_recall(ids, gt, 10) == pytest.approx(0.955, abs=1e-9)
