@@ -299,13 +299,19 @@ int sb_local_join(sb_index* idx, double inv_alpha, int64_t* inserted_out, int64_
   CKL(sb::join_emit_occupancy(smem, &per_sm));
   if (per_sm < 1) return fail(SB_ECUDA, "join kernel does not fit on an SM");
   const int ctas = idx->sms * per_sm;
-  const uint64_t slack = (uint64_t)ctas * (256 / 32) * 128 * 2;  // reservation padding
+  // reservation padding: each warp may leave < 1024 slots of its last block unused, and a
+  // block renewal pads at most 63 slots (<= 64 pushes per warp step) — plan with 7% headroom
+  const uint64_t slack = (uint64_t)ctas * (256 / 32) * 1024;
+  for (int64_t i = 0; i < n; ++i) worst[i] += worst[i] / 14 + 64;
+  total_worst += total_worst / 14 + 64 * (uint64_t)n;
   // push buffer: 4 + 8 (emit) + 8 (segments) bytes per slot
   size_t free_b = 0, tot_b = 0;
   CK(cudaMemGetInfo(&free_b, &tot_b));
   uint64_t budget_slots = (uint64_t)(free_b * 0.6) / 20;
+  uint64_t max_worst = 0;
+  for (int64_t i = 0; i < n; ++i) max_worst = std::max(max_worst, worst[i]);
   uint64_t cap = std::min<uint64_t>(total_worst + slack, budget_slots);
-  if (cap < slack * 2) return fail(SB_ECUDA, "not enough device memory for the join buffers");
+  if (cap < slack + max_worst) return fail(SB_ECUDA, "not enough device memory for the join buffers");
   CK(idx->push_tgt.ensure(sizeof(uint32_t) * cap));
   CK(idx->push_key.ensure(sizeof(uint64_t) * cap));
   CK(idx->seg.ensure(sizeof(uint64_t) * cap));

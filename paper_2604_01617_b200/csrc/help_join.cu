@@ -27,7 +27,7 @@ namespace sb {
 
 constexpr int kJoinThreads = 256;
 constexpr int kJT = 4;            // pair tile edge
-constexpr int kEmitBlock = 128;   // push slots a warp reserves at a time
+constexpr int kEmitBlock = 1024;  // push slots a warp reserves at a time (<= 6% padding)
 
 struct JoinCta {
   int32_t* slot_id;   // [spad]
