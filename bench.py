@@ -1,0 +1,418 @@
+#!/usr/bin/env python
+"""bench.py — hybrid QPS @ Recall@10 >= 0.95 on one B200, HELP build seconds, and routing HBM
+GB/s vs the measured peak, on BASELINE.json configs[1] (cfg 2: N=1M, d=128 integer-valued
+clustered features, 3 attributes 3/5/10, 10,000 queries with a full constraint, k=10).
+
+One step = one pass of the hot path over one batch: search_batch of all queries at the
+operating pool size K* (the smallest K of the sweep whose mean Recall@10 against the exact
+AUTO ground truth is >= 0.95).  Data are seeded synthetic stand-ins (tools/configs.py).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl mine|reference] [--config cfg2]
+
+--impl reference times the reference's CPU implementation of the path (the oracle port in
+oracle/, the reference being Python + Numba) on all host cores over bounded samples of the
+same workload.  N > 1: replicas only (routing does not shard); every rank searches the full
+query batch on its own copy of the index, timed with CUDA events, max over ranks.
+"""
+
+from __future__ import annotations
+
+import argparse
+import csv
+import io
+import json
+import os
+import subprocess
+import sys
+import tempfile
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "hybrid QPS @ recall@10>=0.95 (1 B200); HELP build s; HBM GB/s vs peak"
+UNIT = "queries/s"
+K_SWEEP = [10, 20, 25, 30, 50, 100, 200, 300, 500, 750, 1000, 1500, 2000, 3000, 4000]
+
+
+def parse_args():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=20)
+    p.add_argument("--warmup", type=int, default=3)
+    p.add_argument("--impl", choices=["mine", "reference"], default="mine")
+    p.add_argument("--config", default="cfg2")
+    p.add_argument("--n", type=int, default=None, help="override N (testing only)")
+    p.add_argument("--kcap", type=int, default=4000)
+    p.add_argument("--cpu-seconds", type=float, default=12.0)
+    return p.parse_args()
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+# ---------------------------------------------------------------------------------------
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled every 200 ms during the timed region."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.gpu = gpu_index
+        self.proc = None
+        self.path = None
+
+    def start(self):
+        fd, self.path = tempfile.mkstemp(suffix=".csv")
+        os.close(fd)
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except OSError:
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self.proc.terminate()
+        self.proc.wait()
+        rows = []
+        for r in csv.reader(io.StringIO(open(self.path).read())):
+            r = [x.strip() for x in r]
+            if len(r) >= 9:
+                rows.append(r)
+        os.unlink(self.path)
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"]}
+        sm = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in rows if r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i in range(4) if r[5 + i] == "Active"})
+        return {"sm_mhz": float(np.median(sm)) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(rows)}
+
+
+def measured_hbm_peak():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        v = float(json.load(open(path))["hbm_gbs"])
+        return v, "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+def ncu_traffic(config_name):
+    """dram bytes per route_kernel launch from the committed ncu --set full summary."""
+    path = os.path.join(ROOT, "profiles", f"route_ncu_{config_name}.json")
+    try:
+        d = json.load(open(path))
+        return float(d["dram_bytes_per_launch"])
+    except Exception:
+        return None
+
+
+# ---------------------------------------------------------------------------------------
+def load_workload(args):
+    from tools.configs import make_config
+    X, A, QX, QA, card = make_config(args.config, args.n)
+    return X, A, QX, QA, card
+
+
+def build_index(X, A, card):
+    import paper_2604_01617_b200 as sb
+    cfg = sb.compute_alpha(sb.sample_statistics(X, A, min(1000, X.shape[0]), seed=0),
+                           X.shape[0], A.shape[1])
+    schema = sb.AttributeSchema(tuple(tuple(str(i) for i in range(c)) for c in card))
+    t0 = time.perf_counter()
+    g = sb.build(X, A, schema, sb.BuildParams(), cfg)
+    return g, cfg, time.perf_counter() - t0
+
+
+def sweep_operating_point(g, cfg, X, A, QX, QA, kcap):
+    import paper_2604_01617_b200 as sb
+    t0 = time.perf_counter()
+    gt = sb.oracle_auto_topk_batch(X, A, QX, QA, 10, cfg)
+    gt_s = time.perf_counter() - t0
+    table = []
+    kstar = None
+    for k in K_SWEEP:
+        if k > min(kcap, X.shape[0]):
+            break
+        ids, _, st = sb.search_batch_arrays(g, QX, QA, sb.SearchParams(k=k))
+        rec = sb.mean_recall(ids, gt, 10)
+        table.append({"k": k, "recall_at_10": round(rec, 6), "mean_dist_evals": float(st[:, 0].mean())})
+        if rec >= 0.95:
+            kstar = k
+            break
+    if kstar is None:
+        kstar = table[-1]["k"]
+    return kstar, table, gt, gt_s
+
+
+def algorithmic_bytes(st, m, l):
+    """Routing bytes per SURVEY §8(d): evals*(4d+4L) + 4*(expansions + scanned)."""
+    evals = st[:, 0].astype(np.float64)
+    exps = (st[:, 2] + st[:, 3]).astype(np.float64)
+    scanned = st[:, 4].astype(np.float64)
+    return float((evals * (4 * m + 4 * l) + 4 * (exps + scanned)).sum())
+
+
+# ---------------------------------------------------------------------------------------
+def run_mine(args, rank, world, local):
+    import torch
+    import paper_2604_01617_b200 as sb
+    from paper_2604_01617_b200.device import entry_points_host
+
+    torch.cuda.set_device(local)
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl")
+
+    def barrier():
+        if world > 1:
+            import torch.distributed as dist
+            dist.barrier()
+
+    def max_over_ranks(x):
+        if world == 1:
+            return x
+        import torch.distributed as dist
+        t = torch.tensor([x], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    X, A, QX, QA, card = load_workload(args)
+    n, m = X.shape
+    l = A.shape[1]
+    q = QX.shape[0]
+    g, cfg, build_s = build_index(X, A, card)
+    kstar, table, gt, gt_s = sweep_operating_point(g, cfg, X, A, QX, QA, args.kcap)
+    params = sb.SearchParams(k=kstar)
+    P = params.resolved_pioneer_size()
+    inv_alpha = 1.0 / cfg.alpha
+    dev = g.device()
+    # a dedicated (non-default) stream: kernels and CUDA events must share it
+    stream = torch.cuda.Stream()
+    torch.cuda.set_stream(stream)
+    dev.set_stream(stream.cuda_stream)
+
+    # ---- value: inputs resident in HBM, one device call per step ------------------------
+    qf_d = torch.from_numpy(np.ascontiguousarray(QX, np.float64)).cuda()
+    qa_d = torch.from_numpy(np.ascontiguousarray(QA, np.float64)).cuda()
+    ids_d = torch.empty((q, kstar), dtype=torch.int64, device="cuda")
+    dists_d = torch.empty((q, kstar), dtype=torch.float64, device="cuda")
+    st_d = torch.empty((q, 5), dtype=torch.int64, device="cuda")
+
+    def step_dev(entries_ptr=None):
+        dev.route_dev(qf_d.data_ptr(), qa_d.data_ptr(), None, q, kstar, P, inv_alpha,
+                      ids_d.data_ptr(), dists_d.data_ptr(), st_d.data_ptr(),
+                      entries_ptr=entries_ptr, seed=0, qi0=0)
+
+    for _ in range(max(3, args.warmup)):
+        step_dev()
+    torch.cuda.synchronize()
+    # parity of the device-resident path with the public API at K*
+    ids_api, _, st_api = sb.search_batch_arrays(g, QX, QA, params)
+    assert np.array_equal(ids_d.cpu().numpy(), ids_api), "device-resident path != public API"
+    gpu_index = int(os.environ.get("CUDA_VISIBLE_DEVICES", str(local)).split(",")[local]) \
+        if os.environ.get("CUDA_VISIBLE_DEVICES") else local
+    sampler = ClockSampler(gpu_index)
+    l0 = dev.launch_count()
+    barrier()
+    torch.cuda.synchronize()
+    sampler.start()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(args.steps):
+        step_dev()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    barrier()
+    clocks = sampler.stop()
+    launches = dev.launch_count() - l0
+    ms = e0.elapsed_time(e1) / args.steps
+    ms = max_over_ranks(ms)
+    value = world * q / (ms / 1000.0)
+
+    # ---- roofline: the routing kernel alone (entries precomputed), CUDA events ----------
+    ent = entry_points_host(n, kstar, 0, 0, q)
+    ent_d = torch.from_numpy(ent).cuda()
+    step_dev(ent_d.data_ptr())
+    torch.cuda.synchronize()
+    reps = max(3, min(args.steps, 10))
+    r0 = torch.cuda.Event(enable_timing=True)
+    r1 = torch.cuda.Event(enable_timing=True)
+    r0.record(stream)
+    for _ in range(reps):
+        step_dev(ent_d.data_ptr())
+    r1.record(stream)
+    torch.cuda.synchronize()
+    route_ms = r0.elapsed_time(r1) / reps
+    st = st_d.cpu().numpy()
+    abytes = algorithmic_bytes(st, m, l)
+    achieved = abytes / (route_ms / 1000.0) / 1e9
+    peak, peak_src = measured_hbm_peak()
+    traffic = ncu_traffic(args.config)
+
+    # ---- e2e: public API, host buffers (pinned), copies inside the timed region -----------
+    qf_h = torch.empty((q, m), dtype=torch.float64, pin_memory=True).numpy()
+    qa_h = torch.empty((q, l), dtype=torch.float64, pin_memory=True).numpy()
+    qf_h[:] = QX
+    qa_h[:] = QA
+    dev.set_stream(None)
+    sb.search_batch_arrays(g, qf_h, qa_h, params)
+    barrier()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        ids_h, dists_h, st_h = sb.search_batch_arrays(g, qf_h, qa_h, params)
+    e2e_s = (time.perf_counter() - t0) / args.steps
+    e2e_s = max_over_ranks(e2e_s)
+    e2e = world * q / e2e_s
+    h2d = qf_h.nbytes + qa_h.nbytes
+    d2h = ids_h.nbytes + dists_h.nbytes + st_h.nbytes
+
+    # ---- CPU baseline: the oracle port, one thread (the reference's search is
+    # single-threaded), bounded sample of the same queries -------------------
+    cpu = None
+    if rank == 0 and world == 1:
+        cpu = cpu_baseline(g, cfg, QX, QA, kstar, args.cpu_seconds, ids_api)
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": round(value, 1), "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 4),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (seeded generator with the config's shapes; tools/configs.py)",
+            "config": {
+                "workload": f"{args.config}: N={n:,} d={m} L={l} cards={list(card)} Q={q} k=10",
+                "operating_K": kstar, "pioneer": P, "recall_at_10": table[-1]["recall_at_10"],
+                "index": "HELP gamma=100 sigma=0.44 psi_target=0.8 (BuildParams defaults)",
+                "parallelism": "replicas" if world > 1 else "single",
+                "l2": "inputs larger than L2 (features %.0f MB + adjacency %.0f MB vs 126 MB L2)"
+                      % (X.nbytes / 1e6, n * 100 * 8 / 1e6),
+            },
+            "build_s": round(build_s, 3),
+            "build_log": {k: v for k, v in g.build_log.items()
+                          if k in ("iterations", "psi_history", "termination", "seconds_init",
+                                   "seconds_iterations", "seconds_prune", "pairs",
+                                   "reinforce_overflow_rows", "prune_guard_rounds")},
+            "edges": int(g.nbr_counts.sum()),
+            "gt_s": round(gt_s, 3),
+            "sweep": table,
+            "mean_dist_evals": float(st[:, 0].mean()),
+            "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak,
+                         "unit": "GB/s", "frac": round(achieved / peak, 4),
+                         "traffic": traffic, "kernel": "route_kernel",
+                         "kernel_ms": round(route_ms, 4),
+                         "algorithmic_bytes_per_launch": abytes, "peak_source": peak_src,
+                         "share_of_step": round(route_ms / ms, 3)},
+            "e2e": {"value": round(e2e, 1), "unit": UNIT, "h2d_bytes_per_step": int(h2d),
+                    "d2h_bytes_per_step": int(d2h)},
+            "gpu_launches": int(launches),
+            "clocks": clocks,
+            "cpu_baseline": cpu,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+def cpu_baseline(g, cfg, QX, QA, kstar, seconds, ids_gpu):
+    """The oracle port (C restatement of _kernels.route + NumPy entry points) on the host."""
+    from oracle import oracle as O
+    f, a = g.features, g.attrs
+
+    def run(lo, hi, threads):
+        t0 = time.perf_counter()
+        ids, _, _ = O.search_batch(f, a, g.nbr_ids, g.nbr_counts, cfg.alpha, QX[lo:hi], QA[lo:hi],
+                                   kstar, nthreads=threads,
+                                   entries=O.all_entry_points(f.shape[0], kstar, 0, hi)[lo:hi])
+        return time.perf_counter() - t0, ids
+
+    dt, _ = run(0, 4, 1)
+    per = max(dt / 4, 1e-6)
+    s = int(min(QX.shape[0], max(8, seconds / per)))
+    dt, ids = run(0, s, 1)
+    return {"value": round(s / dt, 2), "unit": UNIT, "cores": 1, "kind": "port",
+            "sample": f"first {s} of {QX.shape[0]} queries at K={kstar}, single thread "
+                      f"(oracle/stable_oracle.c route + NumPy entry points, as search() does)",
+            "parity_with_gpu_on_sample": bool(np.array_equal(ids, ids_gpu[:s]))}
+
+
+# ---------------------------------------------------------------------------------------
+def run_reference(args, rank, world, local):
+    """The reference's CPU path (oracle port) on all host cores, bounded samples per step."""
+    if rank != 0:
+        return
+    import paper_2604_01617_b200 as sb
+    from oracle import oracle as O
+
+    X, A, QX, QA, card = load_workload(args)
+    # setup (untimed): the HELP index the CPU path searches.  Built on the GPU because the
+    # CPU build takes ~40 min at N=1M; the device build is bit-identical to the reference's
+    # (tests/test_gpu_parity.py), so the CPU search below runs on the reference's own graph.
+    g, cfg, _ = build_index(X, A, card)
+    kstar, table, _, _ = sweep_operating_point(g, cfg, X, A, QX, QA, args.kcap)
+    threads = os.cpu_count() or 1
+    n = X.shape[0]
+
+    def step(lo, hi):
+        ent = np.stack([O.entry_points(n, kstar, 0, qi) for qi in range(lo, hi)])
+        O.search_batch(g.features, g.attrs, g.nbr_ids, g.nbr_counts, cfg.alpha, QX[lo:hi],
+                       QA[lo:hi], kstar, nthreads=threads, entries=ent)
+
+    t0 = time.perf_counter()
+    step(0, min(QX.shape[0], 4 * threads))
+    per = (time.perf_counter() - t0) / min(QX.shape[0], 4 * threads)
+    budget = 150.0 / max(1, args.steps + args.warmup)
+    s = int(min(QX.shape[0], max(threads, budget / max(per, 1e-6))))
+    for w in range(args.warmup):
+        step(0, s)
+    t0 = time.perf_counter()
+    for i in range(args.steps):
+        lo = (i * s) % QX.shape[0]
+        hi = min(QX.shape[0], lo + s)
+        step(lo, hi)
+    dt = (time.perf_counter() - t0) / args.steps
+    value = s / dt
+    line = {
+        "impl": "reference", "metric": METRIC, "value": round(value, 2), "unit": UNIT,
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": round(dt * 1000, 3), "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": f"{args.config}: N={n:,} d={X.shape[1]} L={A.shape[1]} "
+                               f"Q={QX.shape[0]} k=10", "operating_K": kstar},
+        "cpu_baseline": {"value": round(value, 2), "unit": UNIT, "cores": threads, "kind": "port",
+                         "sample": f"{s} queries per step at K={kstar}, {threads} threads "
+                                   "(oracle/stable_oracle.c route + NumPy entry points)"},
+        "e2e": {"value": round(value, 2), "unit": UNIT, "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    args = parse_args()
+    rank, world, local = dist_env()
+    if args.impl == "reference":
+        run_reference(args, rank, world, local)
+    else:
+        run_mine(args, rank, world, local)
+
+
+if __name__ == "__main__":
+    main()

@@ -66,6 +66,12 @@ int sb_init_graph(sb_index* idx, const int32_t* ids, double inv_alpha);
 int sb_build_candidates(sb_index* idx, int32_t gamma_new, int32_t* new_cand,
                         int32_t* new_counts, int32_t* old_cand, int32_t* old_counts);
 
+/* hand the device a candidate split computed elsewhere (the arrays build_candidates
+ * returns, _kernels.py:81-135), for a kernel-level local_join call */
+int sb_set_candidates(sb_index* idx, int32_t gamma_new, const int32_t* new_cand,
+                      const int32_t* new_counts, const int32_t* old_cand,
+                      const int32_t* old_counts);
+
 /* local_join (_kernels.py:138-173).  *inserted > 0 iff some row changed (the reference's
  * return value is only compared with 0, graph.py:256); *pairs = distance evaluations. */
 int sb_local_join(sb_index* idx, double inv_alpha, int64_t* inserted, int64_t* pairs);
@@ -89,6 +95,12 @@ int sb_prune(sb_index* idx, double sigma, int32_t* rounds);
  * (graph.py:217-230), continuing from sb_prune's in-degrees.  *overflow_rows = rows that would
  * exceed capacity (0: symmetrisation fast path), *sweeps = reconnect sweeps run. */
 int sb_reinforce(sb_index* idx, double sigma, int64_t* overflow_rows, int32_t* sweeps);
+
+/* the two halves of sb_reinforce at kernel granularity: reinforce_pass
+ * (_kernels.py:398-409) alone, and one reconnect_islands sweep (_kernels.py:455-487) with
+ * freshly counted in-degrees (*ran = 0 when every node already has an in-edge). */
+int sb_reinforce_pass(sb_index* idx, double sigma, int64_t* overflow_rows);
+int sb_reconnect_islands(sb_index* idx, double sigma, int32_t* ran);
 
 /* ---- exhaustive AUTO top-k ------------------------------------------------------ */
 

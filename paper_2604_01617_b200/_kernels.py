@@ -1,0 +1,177 @@
+"""Kernel-level drop-in for ``hybridann._kernels`` (reference _kernels.py), backed by the
+C ABI.  Same function names, argument meaning, return values and in-place mutation of
+the adjacency / in-degree arrays, so the reference's own orchestration can drive the B200:
+
+    import hybridann._kernels as K, paper_2604_01617_b200._kernels as G
+    for name in G.__all__: setattr(K, name, getattr(G, name))
+
+(the reference resolves ``_kernels.<fn>`` at call time, graph.py:13, router.py:15).
+
+Device indexes are cached per (features, attrs) buffer; ``route`` additionally caches the
+uploaded adjacency per (nbr_ids, nbr_counts) buffer, i.e. it assumes a frozen graph, as the
+reference's search does (router.py:56-57).
+"""
+
+from __future__ import annotations
+
+import ctypes
+
+import numpy as np
+
+from . import _lib
+from ._lib import c64, ptr
+from .device import DeviceIndex
+
+__all__ = ["compute_row_distances", "build_candidates", "local_join", "brute_force_topk",
+           "graph_quality", "count_in_degrees", "prune_pass", "reinforce_pass",
+           "reconnect_islands", "route"]
+
+_IDX: dict = {}
+_ROUTE_ADJ: dict = {}
+
+
+def _addr(a: np.ndarray) -> int:
+    return a.__array_interface__["data"][0]
+
+
+def _index(features, attrs, gamma) -> DeviceIndex:
+    key = (_addr(features), features.shape, _addr(attrs), attrs.shape, int(gamma))
+    d = _IDX.get(key)
+    if d is None:
+        if len(_IDX) > 4:
+            _IDX.clear()
+            _ROUTE_ADJ.clear()
+        d = DeviceIndex(features, attrs, gamma)
+        _IDX[key] = d
+    return d
+
+
+def _adjacency_only(n, gamma) -> DeviceIndex:
+    """An index for kernels that read only the adjacency (no features involved)."""
+    return _index(np.zeros((n, 1), np.float32), np.zeros((n, 1), np.int32), gamma)
+
+
+def _write_back(dst: np.ndarray, src: np.ndarray):
+    dst[...] = src
+
+
+def compute_row_distances(features, attrs, nbr_ids, inv_alpha):  # _kernels.py:71-78
+    n, g = nbr_ids.shape
+    d = _index(features, attrs, g)
+    d.init_graph(nbr_ids, inv_alpha)   # computes and sorts each row on the device
+    ids_s, dists_s, _, _ = d.download(with_flags=False)
+    # back to the caller's column order
+    out = np.empty((n, g), np.float32)
+    order_in = np.argsort(nbr_ids, axis=1, kind="stable")
+    order_s = np.argsort(ids_s, axis=1, kind="stable")
+    np.put_along_axis(out, order_in, np.take_along_axis(dists_s, order_s, axis=1), axis=1)
+    return out
+
+
+def build_candidates(nbr_ids, nbr_flags, gamma_new):  # _kernels.py:81-135
+    n, g = nbr_ids.shape
+    d = _adjacency_only(n, g)
+    d.upload(nbr_ids, np.zeros((n, g), np.float32), np.full(n, g, np.int32), nbr_flags)
+    nc, ncnt, oc, ocnt = d.build_candidates(int(gamma_new), download=True)
+    _, _, _, flags = d.download(with_flags=True)
+    _write_back(nbr_flags, flags)
+    return nc, ncnt, oc, ocnt
+
+
+def local_join(features, attrs, inv_alpha, new_cand, new_counts, old_cand, old_counts,
+               nbr_ids, nbr_dists, nbr_flags):  # _kernels.py:138-173
+    n, g = nbr_ids.shape
+    d = _index(features, attrs, g)
+    d.upload(nbr_ids, nbr_dists, np.full(n, g, np.int32), nbr_flags)
+    nc, ncnt = c64(new_cand, np.int32), c64(new_counts, np.int32)
+    oc, ocnt = c64(old_cand, np.int32), c64(old_counts, np.int32)
+    _lib.call("sb_set_candidates", d.handle, nc.shape[1], ptr(nc), ptr(ncnt), ptr(oc), ptr(ocnt))
+    inserted, _ = d.local_join(inv_alpha)
+    ids, dists, _, flags = d.download(with_flags=True)
+    _write_back(nbr_ids, ids)
+    _write_back(nbr_dists, dists)
+    _write_back(nbr_flags, flags)
+    return int(inserted)
+
+
+def brute_force_topk(features, attrs, inv_alpha, sample_ids, k):  # _kernels.py:176-204
+    return _index(features, attrs, 2).bf_topk_nodes(sample_ids, int(k), inv_alpha)
+
+
+def graph_quality(nbr_ids, nbr_counts, sample_ids, gt_ids):  # _kernels.py:207-224
+    """Hit counting over <= quality_sample rows; summed in the reference's order."""
+    k = gt_ids.shape[1]
+    total = 0.0
+    for si, u in enumerate(np.asarray(sample_ids)):
+        c = min(k, int(nbr_counts[u]))
+        total += int(np.isin(nbr_ids[u, :c], gt_ids[si]).sum()) / k
+    return total / len(sample_ids)
+
+
+def count_in_degrees(nbr_ids, nbr_counts):  # _kernels.py:256-263
+    n, g = nbr_ids.shape
+    d = _adjacency_only(n, g)
+    d.upload(nbr_ids, np.zeros((n, g), np.float32), nbr_counts)
+    return d.count_in_degrees()
+
+
+def _check_indeg(d: DeviceIndex, in_deg):
+    if not np.array_equal(d.count_in_degrees(), np.asarray(in_deg)):
+        raise NotImplementedError("in_deg must equal count_in_degrees(nbr_ids, nbr_counts), as "
+                                  "in the reference pipeline (graph.py:212-230)")
+
+
+def prune_pass(features, attrs, nbr_ids, nbr_dists, nbr_counts, in_deg, sigma):  # 266-303
+    n, g = nbr_ids.shape
+    d = _index(features, attrs, g)
+    d.upload(nbr_ids, nbr_dists, nbr_counts)
+    _check_indeg(d, in_deg)
+    d.prune(sigma)
+    ids, dists, counts, _ = d.download(with_flags=False)
+    _write_back(nbr_ids, ids)
+    _write_back(nbr_dists, dists)
+    _write_back(nbr_counts, counts)
+    _write_back(in_deg, d.count_in_degrees())
+
+
+def reinforce_pass(features, attrs, nbr_ids, nbr_dists, nbr_counts, in_deg, sigma):  # 398-409
+    n, g = nbr_ids.shape
+    d = _index(features, attrs, g)
+    d.upload(nbr_ids, nbr_dists, nbr_counts)
+    _check_indeg(d, in_deg)
+    over = ctypes.c_int64(0)
+    _lib.call("sb_reinforce_pass", d.handle, float(sigma), ctypes.addressof(over))
+    ids, dists, counts, _ = d.download(with_flags=False)
+    _write_back(nbr_ids, ids)
+    _write_back(nbr_dists, dists)
+    _write_back(nbr_counts, counts)
+    _write_back(in_deg, d.count_in_degrees())
+
+
+def reconnect_islands(features, attrs, nbr_ids, nbr_dists, nbr_counts, in_deg, sigma):  # 455-487
+    n, g = nbr_ids.shape
+    d = _index(features, attrs, g)
+    d.upload(nbr_ids, nbr_dists, nbr_counts)
+    _check_indeg(d, in_deg)
+    ran = ctypes.c_int32(0)
+    _lib.call("sb_reconnect_islands", d.handle, float(sigma), ctypes.addressof(ran))
+    ids, dists, counts, _ = d.download(with_flags=False)
+    _write_back(nbr_ids, ids)
+    _write_back(nbr_dists, dists)
+    _write_back(nbr_counts, counts)
+    _write_back(in_deg, d.count_in_degrees())
+
+
+def route(features, attrs, nbr_ids, nbr_counts, qfeat, qattr, qmask, inv_alpha, entries,
+          pioneer_size, use_coarse):  # _kernels.py:504-610
+    n, g = nbr_ids.shape
+    d = _index(features, attrs, g)
+    key = (id(d), _addr(nbr_ids), _addr(nbr_counts))
+    if _ROUTE_ADJ.get(id(d)) != key:
+        d.upload(nbr_ids, np.zeros((n, g), np.float32), nbr_counts)
+        _ROUTE_ADJ[id(d)] = key
+    k = int(np.asarray(entries).shape[0])
+    ids, dists, st = d.route(np.asarray(qfeat)[None], np.asarray(qattr)[None], k,
+                             int(pioneer_size), inv_alpha, qmask=np.asarray(qmask)[None],
+                             entries=np.asarray(entries)[None], use_coarse=bool(use_coarse))
+    return ids[0], dists[0], int(st[0, 0]), int(st[0, 1]), int(st[0, 2]), int(st[0, 3])

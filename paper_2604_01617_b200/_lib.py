@@ -36,12 +36,15 @@ _SIGS = {
     "sb_adj_download": [_vp, _vp, _vp, _vp, _vp],
     "sb_init_graph": [_vp, _vp, _f64],
     "sb_build_candidates": [_vp, _i32, _vp, _vp, _vp, _vp],
+    "sb_set_candidates": [_vp, _i32, _vp, _vp, _vp, _vp],
     "sb_local_join": [_vp, _f64, _vp, _vp],
     "sb_descent_iteration": [_vp, _i32, _f64, _vp, _vp],
     "sb_count_in_degrees": [_vp, _vp],
     "sb_get_rows": [_vp, _vp, _i64, _vp, _vp],
     "sb_prune": [_vp, _f64, _vp],
     "sb_reinforce": [_vp, _f64, _vp, _vp],
+    "sb_reinforce_pass": [_vp, _f64, _vp],
+    "sb_reconnect_islands": [_vp, _f64, _vp],
     "sb_bf_topk_nodes": [_vp, _vp, _i64, _i32, _f64, _vp],
     "sb_bf_topk_queries": [_vp, _vp, _vp, _vp, _i64, _i32, _f64, _vp, _vp, _vp],
     "sb_entry_points": [_i64, _i32, _u64, _i64, _i64, _vp],

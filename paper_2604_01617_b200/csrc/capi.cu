@@ -83,6 +83,9 @@ struct sb_index {
   // prune / reinforce
   DBuf rbits, smax, indeg0, guard, drop_other, keep, in_deg, seqtmp;
   bool have_indeg = false;
+  int64_t last_overflow_rows = 0;
+  // exact reinforce (overflow rows)
+  DBuf rf_n8, rf_nb, rf_n32, rf_n64, rf_o32, rf_o64, rf_ulist, rf_bits, rf_rec, rf_sim;
   // routing / brute force
   DBuf qf, qa, qm, entries, ent_scratch, out_ids, out_dists, stats, visited, vlog, counter;
   DBuf bf_part_d, bf_part_i, bf_self, bf_qa, bf_qm, bf_out32;
@@ -93,7 +96,8 @@ struct sb_index {
                    &rbits, &smax, &indeg0, &guard, &drop_other, &keep, &in_deg, &seqtmp, &qf,
                    &qa, &qm, &entries, &ent_scratch, &out_ids, &out_dists, &stats, &visited,
                    &vlog, &counter, &bf_part_d, &bf_part_i, &bf_self, &bf_qa, &bf_qm,
-                   &bf_out32};
+                   &bf_out32, &rf_n8, &rf_nb, &rf_n32, &rf_n64, &rf_o32, &rf_o64,
+                   &rf_ulist, &rf_bits, &rf_rec, &rf_sim};
     for (DBuf* b : all) b->release();
     if (own) cudaStreamDestroy(own);
   }
@@ -254,6 +258,27 @@ int sb_build_candidates(sb_index* idx, int32_t gamma_new, int32_t* new_cand, int
   if (old_cand) CK(cudaMemcpyAsync(old_cand, idx->old_cand.p, sizeof(int32_t) * n * g, cudaMemcpyDeviceToHost, idx->st));
   if (old_counts) CK(cudaMemcpyAsync(old_counts, idx->old_cnt.p, sizeof(int32_t) * n, cudaMemcpyDeviceToHost, idx->st));
   CK(cudaStreamSynchronize(idx->st));
+  return SB_OK;
+}
+
+int sb_set_candidates(sb_index* idx, int32_t gamma_new, const int32_t* new_cand,
+                      const int32_t* new_counts, const int32_t* old_cand,
+                      const int32_t* old_counts) {
+  if (!idx || !new_cand || !new_counts || !old_cand || !old_counts) return fail(SB_EARG, "NULL argument");
+  if (gamma_new < 1 || gamma_new > 256) return fail(SB_EARG, "gamma_new must be in [1, 256]");
+  const int64_t n = idx->n;
+  const int g = idx->g;
+  idx->gn = gamma_new;
+  CK(idx->new_cand.ensure(sizeof(int32_t) * n * gamma_new));
+  CK(idx->old_cand.ensure(sizeof(int32_t) * n * g));
+  CK(idx->new_cnt.ensure(sizeof(int32_t) * n));
+  CK(idx->old_cnt.ensure(sizeof(int32_t) * n));
+  CK(cudaMemcpyAsync(idx->new_cand.p, new_cand, sizeof(int32_t) * n * gamma_new, cudaMemcpyHostToDevice, idx->st));
+  CK(cudaMemcpyAsync(idx->new_cnt.p, new_counts, sizeof(int32_t) * n, cudaMemcpyHostToDevice, idx->st));
+  CK(cudaMemcpyAsync(idx->old_cand.p, old_cand, sizeof(int32_t) * n * g, cudaMemcpyHostToDevice, idx->st));
+  CK(cudaMemcpyAsync(idx->old_cnt.p, old_counts, sizeof(int32_t) * n, cudaMemcpyHostToDevice, idx->st));
+  CK(cudaStreamSynchronize(idx->st));
+  idx->have_cand = true;
   return SB_OK;
 }
 
@@ -468,16 +493,119 @@ int sb_prune(sb_index* idx, double sigma, int32_t* rounds_out) {
   return SB_OK;
 }
 
-int sb_reinforce(sb_index* idx, double sigma, int64_t* overflow_rows, int32_t* sweeps_out) {
-  if (!idx) return fail(SB_EARG, "idx is NULL");
-  if (!idx->have_indeg) return fail(SB_EARG, "sb_prune must run first");
+// exact reinforce when some row can overflow (help_reinforce.cu)
+static int reinforce_overflow(sb_index* idx, double sigma) {
+  const int64_t n = idx->n;
+  const int g = idx->g;
+  sb::RfArgs a{};
+  a.n = n; a.m = idx->m; a.l = idx->l; a.g = g;
+  a.F = idx->F.as<float>(); a.A = idx->A.as<int32_t>();
+  a.ids = idx->ids.as<int32_t>(); a.dists = idx->dists.as<float>();
+  a.counts = idx->counts.as<int32_t>(); a.in_deg = idx->in_deg.as<int32_t>(); a.sigma = sigma;
+  CK(idx->rf_n8.ensure((size_t)n * g));            // mutual flags
+  CK(idx->rf_nb.ensure((size_t)n * 2));            // is_o, relevant
+  CK(idx->rf_n32.ensure(sizeof(int32_t) * n * 2)); // o_idx, static_ins
+  CK(idx->rf_n64.ensure(sizeof(int64_t) * n * 8)); // rev_extra, oflag, oscan, orev, apply x3, rec_head
+  a.mutual = idx->rf_n8.as<uint8_t>();
+  a.is_o = idx->rf_nb.as<uint8_t>();
+  a.relevant = a.is_o + n;
+  a.o_idx = idx->rf_n32.as<int32_t>();
+  a.static_ins = a.o_idx + n;
+  int64_t* p64 = idx->rf_n64.as<int64_t>();
+  a.rev_extra = p64; int64_t* oflag = p64 + n; int64_t* oscan = p64 + 2 * n;
+  a.orev_cnt = p64 + 3 * n; a.apply_cnt = p64 + 4 * n; a.apply_off = p64 + 5 * n;
+  a.apply_cur = p64 + 6 * n; a.rec_head = p64 + 7 * n;
+  CKL(sb::rf_launch_stage1(a, oflag, oscan, idx->scan_tmp.as<int64_t>(), idx->st));
+  int64_t last[2] = {0, 0};
+  CK(cudaMemcpyAsync(&last[0], oscan + n - 1, sizeof(int64_t), cudaMemcpyDeviceToHost, idx->st));
+  CK(cudaMemcpyAsync(&last[1], oflag + n - 1, sizeof(int64_t), cudaMemcpyDeviceToHost, idx->st));
+  CK(cudaStreamSynchronize(idx->st));
+  const int64_t no = last[0] + last[1];
+  a.no = no;
+  CK(idx->rf_o32.ensure(sizeof(int32_t) * no * (1 + (size_t)g)));
+  a.o_nodes = idx->rf_o32.as<int32_t>();
+  a.u_pos = a.o_nodes + no;
+  CK(idx->rf_o64.ensure(sizeof(int64_t) * (no * 4 + 4)));
+  a.u_size = idx->rf_o64.as<int64_t>();
+  a.u_off = a.u_size + no;
+  a.u_cur = a.u_off + no + 1;
+  a.r_off = a.u_cur + no;
+  CKL(sb::rf_launch_stage2(a, oscan, idx->st));
+  std::vector<int64_t> usz(no), uoff(no + 1), roff(no + 1);
+  CK(cudaMemcpyAsync(usz.data(), a.u_size, sizeof(int64_t) * no, cudaMemcpyDeviceToHost, idx->st));
+  CK(cudaStreamSynchronize(idx->st));
+  int64_t umax = 1, wmax = 1;
+  uoff[0] = 0; roff[0] = 0;
+  for (int64_t o = 0; o < no; ++o) {
+    int64_t W = (usz[o] + 31) / 32;
+    uoff[o + 1] = uoff[o] + usz[o];
+    roff[o + 1] = roff[o] + usz[o] * W;
+    umax = std::max(umax, usz[o]);
+    wmax = std::max(wmax, W);
+  }
+  if (umax > 4096) return fail(SB_ECUDA, "reinforce: an overflow row has more than 4096 candidate members");
+  CK(cudaMemcpyAsync(a.u_off, uoff.data(), sizeof(int64_t) * (no + 1), cudaMemcpyHostToDevice, idx->st));
+  CK(cudaMemcpyAsync(a.r_off, roff.data(), sizeof(int64_t) * (no + 1), cudaMemcpyHostToDevice, idx->st));
+  CK(idx->rf_ulist.ensure(sizeof(int32_t) * (uoff[no] + 1)));
+  CK(idx->rf_bits.ensure(sizeof(uint32_t) * (roff[no] + 1)));
+  a.u_list = idx->rf_ulist.as<int32_t>();
+  a.r_bits = idx->rf_bits.as<uint32_t>();
+  CK(cudaMemsetAsync(a.r_bits, 0, sizeof(uint32_t) * (roff[no] + 1), idx->st));
+  const int upad_max = next_pow2((int)umax);
+  const int upad4 = (int)((umax + 3) & ~3);
+  int dc_max = (int)std::min<int64_t>(idx->m, (96 * 1024) / (4 * (int64_t)upad4));
+  dc_max = std::max(1, dc_max);
+  size_t bits_smem = sizeof(double) * dc_max + sizeof(double) * upad4 + sizeof(float) * (size_t)dc_max * upad4 + 64;
+  CKL(sb::rf_launch_stage3(a, upad_max, dc_max, upad4, bits_smem, idx->st));
+  // sequential simulation over events touching overflow rows
+  a.rec_cap = std::max<int64_t>(1, no * g);
+  CK(idx->rf_rec.ensure((sizeof(int32_t) + sizeof(uint64_t) + sizeof(int64_t)) * a.rec_cap + 64));
+  a.rec_key = idx->rf_rec.as<uint64_t>();
+  a.rec_next = reinterpret_cast<int64_t*>(a.rec_key + a.rec_cap);
+  a.rec_tgt = reinterpret_cast<int32_t*>(a.rec_next + a.rec_cap);
+  CK(cudaMemsetAsync(a.rec_head, 0xFF, sizeof(int64_t) * n, idx->st));
+  a.dyn_cap = 1 << 16;
+  size_t sim_bytes = sizeof(uint64_t) * a.dyn_cap + (size_t)(g + 1) * 13 + sizeof(uint32_t) * wmax + 256;
+  CK(idx->rf_sim.ensure(sim_bytes));
+  char* sp = idx->rf_sim.as<char>();
+  a.dyn = reinterpret_cast<uint64_t*>(sp); sp += sizeof(uint64_t) * a.dyn_cap;
+  a.result = reinterpret_cast<int64_t*>(sp); sp += 16;
+  a.sim_d = reinterpret_cast<float*>(sp); sp += sizeof(float) * (g + 1);
+  a.sim_ids = reinterpret_cast<int32_t*>(sp); sp += sizeof(int32_t) * (g + 1);
+  a.sim_u = reinterpret_cast<int32_t*>(sp); sp += sizeof(int32_t) * (g + 1);
+  a.sim_mask = reinterpret_cast<uint32_t*>(sp); sp += sizeof(uint32_t) * wmax;
+  a.sim_keep = reinterpret_cast<uint8_t*>(sp);
+  CKL(sb::rf_launch_simulate(a, idx->st));
+  int64_t res[2] = {0, 0};
+  CK(cudaMemcpyAsync(res, a.result, sizeof(res), cudaMemcpyDeviceToHost, idx->st));
+  CK(cudaStreamSynchronize(idx->st));
+  if (res[1]) return fail(SB_ECUDA, "reinforce simulation invariant violated (code " + std::to_string(res[1]) + ")");
+  // parallel part: insertions into rows that cannot overflow
+  CK(idx->seg.ensure(sizeof(uint64_t) * n * g));
+  a.apply_seg = idx->seg.as<uint64_t>();
+  CKL(sb::rf_launch_apply(a, res[0], idx->scan_tmp.as<int64_t>(), idx->st));
+  CKL(sb::launch_row_union_merge(a.ids, a.dists, a.counts, n, g, a.apply_off, a.apply_cnt,
+                                 a.apply_seg, idx->st));
+  idx->launches += 16;
+  idx->last_overflow_rows = no;
+  return SB_OK;
+}
+
+// reinforce_pass (_kernels.py:398-409); in_deg continues from sb_prune, else it is counted
+static int reinforce_pass(sb_index* idx, double sigma, int64_t* overflow_rows) {
   const int64_t n = idx->n;
   const int g = idx->g;
   CK(idx->rev_cnt.ensure(sizeof(int64_t) * n));
   CK(idx->rev_off.ensure(sizeof(int64_t) * n));
   CK(idx->rev_cur.ensure(sizeof(int64_t) * n));
+  CK(idx->in_deg.ensure(sizeof(int32_t) * n));
   CK(idx->scan_tmp.ensure(sizeof(int64_t) * sb::scan_tmp_slots(n)));
   CK(idx->small.ensure(64));
+  if (!idx->have_indeg) {
+    CKL(sb::launch_count_in_degrees(idx->ids.as<int32_t>(), idx->counts.as<int32_t>(), n, g,
+                                    idx->in_deg.as<int32_t>(), nullptr, idx->st));
+    idx->launches += 1;
+  }
   unsigned long long* d_over = idx->small.as<unsigned long long>() + 4;
   CKL(sb::launch_reinforce_check(idx->ids.as<int32_t>(), idx->dists.as<float>(),
                                  idx->counts.as<int32_t>(), n, g, idx->rev_cnt.as<int64_t>(),
@@ -486,7 +614,6 @@ int sb_reinforce(sb_index* idx, double sigma, int64_t* overflow_rows, int32_t* s
   CK(cudaMemcpyAsync(&over, d_over, sizeof(over), cudaMemcpyDeviceToHost, idx->st));
   CK(cudaStreamSynchronize(idx->st));
   if (overflow_rows) *overflow_rows = (int64_t)over;
-  CK(idx->seqtmp.ensure((sizeof(int64_t) + sizeof(double) + 1) * (g + 1) + 64));
   if (over == 0) {
     CK(idx->seg.ensure(sizeof(uint64_t) * n * g));
     CKL(sb::launch_symmetrize(idx->ids.as<int32_t>(), idx->dists.as<float>(),
@@ -495,36 +622,71 @@ int sb_reinforce(sb_index* idx, double sigma, int64_t* overflow_rows, int32_t* s
                               idx->seg.as<uint64_t>(), idx->scan_tmp.as<int64_t>(), idx->st));
     idx->launches += 6;
   } else {
-    CKL(sb::launch_seq_reinforce(idx->F.as<float>(), idx->A.as<int32_t>(), idx->m, idx->l, g,
-                                 idx->ids.as<int32_t>(), idx->dists.as<float>(),
-                                 idx->counts.as<int32_t>(), idx->in_deg.as<int32_t>(), sigma, n,
-                                 idx->seqtmp.p, 0, idx->st));
-    idx->launches += 3;
-  }
-  // reconnect sweeps (graph.py:221-230)
-  int sweeps = 0;
-  int* d_min = reinterpret_cast<int*>(idx->small.as<unsigned long long>() + 5);
-  for (int it = 0; it < 10; ++it) {
-    CKL(sb::launch_count_in_degrees(idx->ids.as<int32_t>(), idx->counts.as<int32_t>(), n, g,
-                                    idx->in_deg.as<int32_t>(), nullptr, idx->st));
-    int big = 0x7FFFFFFF;
-    CK(cudaMemcpyAsync(d_min, &big, sizeof(int), cudaMemcpyHostToDevice, idx->st));
-    CKL(sb::launch_min_i32(idx->in_deg.as<int32_t>(), n, d_min, idx->st));
-    int mn = 0;
-    CK(cudaMemcpyAsync(&mn, d_min, sizeof(int), cudaMemcpyDeviceToHost, idx->st));
-    CK(cudaStreamSynchronize(idx->st));
-    idx->launches += 2;
-    if (mn >= 1) break;
-    CKL(sb::launch_seq_reinforce(idx->F.as<float>(), idx->A.as<int32_t>(), idx->m, idx->l, g,
-                                 idx->ids.as<int32_t>(), idx->dists.as<float>(),
-                                 idx->counts.as<int32_t>(), idx->in_deg.as<int32_t>(), sigma, n,
-                                 idx->seqtmp.p, 1, idx->st));
-    idx->launches += 1;
-    ++sweeps;
+    int r = reinforce_overflow(idx, sigma);
+    if (r) return r;
   }
   CK(cudaStreamSynchronize(idx->st));
-  if (sweeps_out) *sweeps_out = sweeps;
   idx->have_indeg = false;
+  return SB_OK;
+}
+
+// one reconnect_islands sweep (_kernels.py:455-487) if some node has in-degree 0;
+// *ran = 1 if the sweep ran
+static int reconnect_sweep(sb_index* idx, double sigma, int* ran) {
+  const int64_t n = idx->n;
+  const int g = idx->g;
+  CK(idx->in_deg.ensure(sizeof(int32_t) * n));
+  CK(idx->small.ensure(64));
+  CK(idx->seqtmp.ensure((sizeof(int64_t) + sizeof(double) + 1) * (g + 1) + 64));
+  int* d_min = reinterpret_cast<int*>(idx->small.as<unsigned long long>() + 5);
+  CKL(sb::launch_count_in_degrees(idx->ids.as<int32_t>(), idx->counts.as<int32_t>(), n, g,
+                                  idx->in_deg.as<int32_t>(), nullptr, idx->st));
+  int big = 0x7FFFFFFF;
+  CK(cudaMemcpyAsync(d_min, &big, sizeof(int), cudaMemcpyHostToDevice, idx->st));
+  CKL(sb::launch_min_i32(idx->in_deg.as<int32_t>(), n, d_min, idx->st));
+  int mn = 0;
+  CK(cudaMemcpyAsync(&mn, d_min, sizeof(int), cudaMemcpyDeviceToHost, idx->st));
+  CK(cudaStreamSynchronize(idx->st));
+  idx->launches += 2;
+  *ran = 0;
+  if (mn >= 1) return SB_OK;
+  CKL(sb::launch_seq_reinforce(idx->F.as<float>(), idx->A.as<int32_t>(), idx->m, idx->l, g,
+                               idx->ids.as<int32_t>(), idx->dists.as<float>(),
+                               idx->counts.as<int32_t>(), idx->in_deg.as<int32_t>(), sigma, n,
+                               idx->seqtmp.p, 1, idx->st));
+  idx->launches += 1;
+  CK(cudaStreamSynchronize(idx->st));
+  *ran = 1;
+  return SB_OK;
+}
+
+int sb_reinforce_pass(sb_index* idx, double sigma, int64_t* overflow_rows) {
+  if (!idx) return fail(SB_EARG, "idx is NULL");
+  return reinforce_pass(idx, sigma, overflow_rows);
+}
+
+int sb_reconnect_islands(sb_index* idx, double sigma, int32_t* ran) {
+  if (!idx) return fail(SB_EARG, "idx is NULL");
+  int r = 0;
+  int rc = reconnect_sweep(idx, sigma, &r);
+  if (ran) *ran = r;
+  return rc;
+}
+
+int sb_reinforce(sb_index* idx, double sigma, int64_t* overflow_rows, int32_t* sweeps_out) {
+  if (!idx) return fail(SB_EARG, "idx is NULL");
+  int r = reinforce_pass(idx, sigma, overflow_rows);
+  if (r) return r;
+  // reconnect sweeps with freshly counted in-degrees (graph.py:221-230)
+  int sweeps = 0;
+  for (int it = 0; it < 10; ++it) {
+    int ran = 0;
+    r = reconnect_sweep(idx, sigma, &ran);
+    if (r) return r;
+    if (!ran) break;
+    ++sweeps;
+  }
+  if (sweeps_out) *sweeps_out = sweeps;
   return SB_OK;
 }
 

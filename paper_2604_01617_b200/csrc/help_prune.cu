@@ -308,6 +308,18 @@ __global__ void symmetrize_merge_kernel(int32_t* ids, float* dists, int32_t* cou
   if (lane == 0) counts[j] = cnt + E;
 }
 
+int launch_row_union_merge(int32_t* ids, float* dists, int32_t* counts, int64_t n, int g,
+                           const int64_t* off, const int64_t* extra, const uint64_t* seg,
+                           cudaStream_t st) {
+  int gpad = next_pow2(g);
+  int wpb = 4;
+  size_t smem = (size_t)wpb * 2 * gpad * sizeof(uint64_t);
+  cudaFuncSetAttribute(symmetrize_merge_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  symmetrize_merge_kernel<<<(unsigned)((n + wpb - 1) / wpb), wpb * 32, smem, st>>>(
+      ids, dists, counts, n, g, gpad, off, extra, seg);
+  return (int)cudaGetLastError();
+}
+
 int launch_reinforce_check(const int32_t* ids, const float* dists, const int32_t* counts,
                            int64_t n, int g, int64_t* rev_extra, unsigned long long* over,
                            cudaStream_t st) {

@@ -148,5 +148,60 @@ int launch_seq_reinforce(const float* F, const int32_t* A, int m, int l, int g, 
                          float* dists, int32_t* counts, int32_t* in_deg, double sigma,
                          int64_t n, void* scratch, int reconnect, cudaStream_t st);
 int launch_min_i32(const int32_t* x, int64_t n, int* out, cudaStream_t st);
+int launch_row_union_merge(int32_t* ids, float* dists, int32_t* counts, int64_t n, int g,
+                           const int64_t* off, const int64_t* extra, const uint64_t* seg,
+                           cudaStream_t st);
+
+// exact reinforce with the sequential part confined to overflow rows (help_reinforce.cu)
+struct RfArgs {
+  int64_t n;
+  int m, l, g;
+  const float* F;
+  const int32_t* A;
+  int32_t* ids;
+  float* dists;
+  int32_t* counts;
+  int32_t* in_deg;
+  double sigma;
+  uint8_t* mutual;      // n x g
+  int64_t* rev_extra;   // n
+  uint8_t* is_o;        // n
+  int32_t* o_idx;       // n
+  int64_t no;
+  int32_t* o_nodes;     // no
+  int64_t* u_size;      // no
+  int64_t* u_off;       // no + 1
+  int64_t* u_cur;       // no
+  int32_t* u_list;      // sum u
+  int64_t* r_off;       // no + 1
+  uint32_t* r_bits;
+  int32_t* u_pos;       // no x g
+  int32_t* static_ins;  // n
+  uint8_t* relevant;    // n
+  int64_t* orev_cnt;    // n
+  int64_t* apply_cnt;   // n
+  int64_t* apply_off;   // n
+  int64_t* apply_cur;   // n
+  uint64_t* apply_seg;
+  int32_t* rec_tgt;
+  uint64_t* rec_key;
+  int64_t* rec_next;
+  int64_t* rec_head;    // n
+  int64_t rec_cap;
+  uint64_t* dyn;
+  int dyn_cap;
+  int32_t* sim_ids;
+  float* sim_d;
+  int32_t* sim_u;
+  uint8_t* sim_keep;
+  uint32_t* sim_mask;
+  int64_t* result;      // [nrec, err]
+};
+int rf_launch_stage1(RfArgs& a, int64_t* oflag, int64_t* oscan, int64_t* scan_tmp, cudaStream_t st);
+int rf_launch_stage2(RfArgs& a, const int64_t* oscan, cudaStream_t st);
+int rf_launch_stage3(RfArgs& a, int upad_max, int dc_max, int upad4_max, size_t bits_smem,
+                     cudaStream_t st);
+int rf_launch_simulate(RfArgs& a, cudaStream_t st);
+int rf_launch_apply(RfArgs& a, int64_t nrec, int64_t* scan_tmp, cudaStream_t st);
 
 }  // namespace sb
