@@ -35,10 +35,11 @@ constexpr int kPT = 4;
 __global__ void __launch_bounds__(kPruneThreads) prune_bits_kernel(PruneArgs a) {
   extern __shared__ __align__(16) char smem_raw[];
   const int cpad = a.cpad;
+  // the float tile goes first: its float4 reads need 16-byte alignment
   char* p = smem_raw;
+  float* xr = reinterpret_cast<float*>(p); p += sizeof(float) * (size_t)a.dc * cpad;
   double* xs = reinterpret_cast<double*>(p); p += sizeof(double) * a.m;
   double* nrm = reinterpret_cast<double*>(p); p += sizeof(double) * cpad;
-  float* xr = reinterpret_cast<float*>(p); p += sizeof(float) * (size_t)a.dc * cpad;
   int32_t* eid = reinterpret_cast<int32_t*>(p); p += sizeof(int32_t) * cpad;
   int32_t* eat = reinterpret_cast<int32_t*>(p); p += sizeof(int32_t) * (size_t)cpad * a.l;
   uint32_t* bits = reinterpret_cast<uint32_t*>(p); p += sizeof(uint32_t) * (size_t)cpad * a.W;

@@ -139,10 +139,11 @@ __global__ void __launch_bounds__(kRfThreads) rf_bits_kernel(RfArgs a, int dc_ma
   const int32_t* U = a.u_list + a.u_off[o];
   const int W = (u + 31) >> 5;
   uint32_t* bits = a.r_bits + a.r_off[o];
+  // the float tile goes first: its float4 reads need 16-byte alignment
   char* p = smem_raw;
+  float* xr = reinterpret_cast<float*>(p); p += sizeof(float) * (size_t)dc_max * upad4;
   double* xs = reinterpret_cast<double*>(p); p += sizeof(double) * dc_max;
-  double* nrm = reinterpret_cast<double*>(p); p += sizeof(double) * upad4;
-  float* xr = reinterpret_cast<float*>(p);
+  double* nrm = reinterpret_cast<double*>(p);
   const int tid = threadIdx.x;
   const int up4 = (u + 3) & ~3;
   // norms |p - j|^2 in ascending dimension order; thread tid owns entries tid + 256 r
