@@ -69,6 +69,9 @@ struct sb_index {
   int64_t n = 0;
   int m = 0, l = 0, g = 0;
   int sms = 148;
+  bool int_exact = false;  // all features integral (order-free exact distances possible)
+  double fmax = 0.0;
+  bool force_sequential = false;  // testing: always use the sequential-order distance path
   cudaStream_t own = nullptr, st = nullptr;
   int64_t launches = 0;
   // dataset + adjacency
@@ -148,7 +151,19 @@ int sb_index_create(const float* features, const int32_t* attrs, int64_t n, int3
   if (e == cudaSuccess) e = cudaMemcpyAsync(x->A.p, attrs, ab, cudaMemcpyHostToDevice, x->st);
   if (e == cudaSuccess) e = cudaMemsetAsync(x->counts.p, 0, (size_t)n * 4, x->st);
   if (e == cudaSuccess) e = cudaMemsetAsync(x->flags.p, 0, adj, x->st);
-  if (e == cudaSuccess) e = cudaStreamSynchronize(x->st);
+  if (e == cudaSuccess) e = x->small.ensure(64);
+  if (e == cudaSuccess) {
+    unsigned* flags2 = x->small.as<unsigned>() + 14;
+    int r = sb::launch_feature_scan(x->F.as<float>(), (int64_t)n * m, flags2, flags2 + 1, x->st);
+    if (r) e = (cudaError_t)r;
+    unsigned h[2] = {1, 0};
+    if (e == cudaSuccess) e = cudaMemcpyAsync(h, flags2, sizeof(h), cudaMemcpyDeviceToHost, x->st);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(x->st);
+    float fmax = 0.f;
+    memcpy(&fmax, &h[1], sizeof(float));
+    x->int_exact = (h[0] == 0) && (m % 4 == 0);
+    x->fmax = (double)fmax;
+  }
   if (e != cudaSuccess) { delete x; return cuda_fail(e, "upload(index)"); }
   *out = x;
   return SB_OK;
@@ -172,6 +187,20 @@ int sb_synchronize(sb_index* idx) {
 }
 
 int64_t sb_launch_count(sb_index* idx) { return idx ? idx->launches : 0; }
+
+int sb_index_info(sb_index* idx, int32_t* int_exact, double* fmax_abs) {
+  if (!idx) return fail(SB_EARG, "idx is NULL");
+  if (int_exact) *int_exact = idx->int_exact ? 1 : 0;
+  if (fmax_abs) *fmax_abs = idx->fmax;
+  return SB_OK;
+}
+
+int sb_set_distance_mode(sb_index* idx, int32_t mode) {
+  if (!idx) return fail(SB_EARG, "idx is NULL");
+  if (mode != 0 && mode != 1) return fail(SB_EARG, "mode must be 0 (auto) or 1 (sequential)");
+  idx->force_sequential = mode == 1;
+  return SB_OK;
+}
 
 int sb_adj_upload(sb_index* idx, const int32_t* ids, const float* dists, const int32_t* counts,
                   const uint8_t* flags) {
@@ -803,6 +832,9 @@ static int route_dev(sb_index* idx, const double* qf, const double* qa, const do
   a.out_dists = out_dists; a.stats = out_stats;
   a.Kpad = next_pow2(k);
   a.Cpad = next_pow2(idx->g);
+  a.int_exact = idx->int_exact && !idx->force_sequential ? 1 : 0;
+  a.fmax = idx->fmax;
+  a.lpr = std::min(32, next_pow2(std::max(1, idx->m / 4)));
   size_t per_warp = sb::route_smem_per_warp(a.Kpad, a.Cpad, idx->m, idx->l);
   int wpc = (int)std::max<size_t>(1, std::min<size_t>(8, (size_t)(100 * 1024) / per_warp));
   if (per_warp * wpc > 227 * 1024) return fail(SB_EARG, "k too large for the routing kernel");

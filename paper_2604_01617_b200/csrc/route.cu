@@ -72,6 +72,61 @@ SB_DEV double query_dist(const RouteArgs& a, int64_t v, const double* qs, const 
   return auto_finish(s, sa, a.inv_alpha);
 }
 
+// Order-free exact distances for a batch of rows (ids in cid[0..c) -> cd).  Valid only when
+// every (x - q)^2 term and every partial sum is an integer below 2^53, so fp64 addition is
+// exact in any order and the result equals the sequential one bit for bit.  lpr lanes share
+// a row (128-bit loads, coalesced), kRows rows per lane group in flight, xor-shuffle reduce.
+constexpr int kRows = 8;
+SB_DEV void batch_dist_warp(const RouteArgs& a, const uint32_t* cid, double* cd, int c,
+                            const double* qs, const double* qas, const double* qms) {
+  const int lane = lane_id();
+  const int lpr = a.lpr;
+  const int rpp = 32 / lpr;
+  const int sub = lane & (lpr - 1);
+  const int grp = lane / lpr;
+  const int nq = a.m >> 2;
+  for (int base = 0; base < c; base += rpp * kRows) {
+    double part[kRows];
+    const float4* rows[kRows];
+#pragma unroll
+    for (int g = 0; g < kRows; ++g) {
+      int r = base + grp + rpp * g;
+      rows[g] = r < c ? reinterpret_cast<const float4*>(a.F + (int64_t)cid[r] * a.m) : nullptr;
+      part[g] = 0.0;
+    }
+    for (int k = sub; k < nq; k += lpr) {
+      float4 x[kRows];
+#pragma unroll
+      for (int g = 0; g < kRows; ++g)
+        if (rows[g]) x[g] = __ldg(rows[g] + k);
+      const double* qv = qs + 4 * k;
+#pragma unroll
+      for (int g = 0; g < kRows; ++g)
+        if (rows[g]) {
+          double d0 = dsub(x[g].x, qv[0]), d1 = dsub(x[g].y, qv[1]);
+          double d2 = dsub(x[g].z, qv[2]), d3 = dsub(x[g].w, qv[3]);
+          part[g] = dadd(part[g], dadd(dadd(dmul(d0, d0), dmul(d1, d1)), dadd(dmul(d2, d2), dmul(d3, d3))));
+        }
+    }
+#pragma unroll
+    for (int g = 0; g < kRows; ++g)
+      for (int o = lpr >> 1; o > 0; o >>= 1) part[g] = dadd(part[g], __shfl_xor_sync(0xffffffffu, part[g], o));
+    if (sub == 0) {
+#pragma unroll
+      for (int g = 0; g < kRows; ++g) {
+        int r = base + grp + rpp * g;
+        if (r < c) {
+          const int32_t* av = a.A + (int64_t)cid[r] * a.l;
+          double sa = 0.0;
+          for (int u = 0; u < a.l; ++u)
+            sa = dadd(sa, dmul(qms[u], fabs(dsub((double)__ldg(av + u), qas[u]))));
+          cd[r] = auto_finish(part[g], sa, a.inv_alpha);
+        }
+      }
+    }
+  }
+}
+
 struct WarpSmem {
   double* rd;     // Kpad
   uint32_t* rid;  // Kpad
@@ -127,7 +182,7 @@ struct Counters {
 // Expand `node` over its first `cnt` stored neighbours: test-and-set the visited bits,
 // evaluate the unvisited ones, merge into R.  Returns min insert position (or K).
 SB_DEV int expand(const RouteArgs& a, WarpSmem& w, int64_t node, int cnt, uint32_t* vis,
-                  uint32_t* vlog, int& logn, int64_t& evals_out) {
+                  uint32_t* vlog, int& logn, int64_t& evals_out, bool fast) {
   const int lane = lane_id();
   const int32_t* nb = a.nbr_ids + node * (int64_t)a.g;
   // gather unvisited neighbours into the candidate buffer (ids only)
@@ -154,8 +209,12 @@ SB_DEV int expand(const RouteArgs& a, WarpSmem& w, int64_t node, int cnt, uint32
   logn += c;
   evals_out += c;
   __syncwarp();
-  // evaluate (one row per lane)
-  for (int j = lane; j < c; j += 32) w.cd[j] = query_dist(a, w.cid[j], w.qs, w.qas, w.qms);
+  // evaluate: warp-split rows (order-free exact mode) or one row per lane, sequential order
+  if (fast) {
+    batch_dist_warp(a, w.cid, w.cd, c, w.qs, w.qas, w.qms);
+  } else {
+    for (int j = lane; j < c; j += 32) w.cd[j] = query_dist(a, w.cid[j], w.qs, w.qas, w.qms);
+  }
   __syncwarp();
   if (c == 0) return a.K;
   return merge_into_r(w, a.K, c);
@@ -185,6 +244,21 @@ __global__ void __launch_bounds__(256) route_kernel(RouteArgs a) {
       w.qms[t] = a.qm ? a.qm[(int64_t)qi * a.l + t] : 1.0;
     }
     __syncwarp();
+    // order-free exact mode for this query: integral coordinates, sums below 2^53
+    bool fast = false;
+    if (a.int_exact) {
+      bool integral = true;
+      double qmax = 0.0;
+      for (int t = lane; t < a.m; t += 32) {
+        double v = w.qs[t];
+        integral = integral && v == rint(v);
+        qmax = fmax(qmax, fabs(v));
+      }
+      for (int o = 16; o > 0; o >>= 1) qmax = fmax(qmax, __shfl_xor_sync(0xffffffffu, qmax, o));
+      integral = __all_sync(0xffffffffu, integral);
+      double lim = (a.fmax + qmax) * (a.fmax + qmax) * (double)a.m;
+      fast = integral && lim < 9007199254740992.0;  // 2^53
+    }
 
     Counters ct = {0, 0, 0, 0, 0};
     int logn = 0;
@@ -197,7 +271,12 @@ __global__ void __launch_bounds__(256) route_kernel(RouteArgs a) {
       w.rid[t] = v;
     }
     __syncwarp();
-    for (int t = lane; t < K; t += 32) w.rd[t] = query_dist(a, w.rid[t], w.qs, w.qas, w.qms);
+    if (fast) {
+      batch_dist_warp(a, w.rid, w.rd, K, w.qs, w.qas, w.qms);
+    } else {
+      for (int t = lane; t < K; t += 32) w.rd[t] = query_dist(a, w.rid[t], w.qs, w.qas, w.qms);
+    }
+    __syncwarp();
     for (int t = K + lane; t < a.Kpad; t += 32) {
       w.rd[t] = __longlong_as_double(0x7FF0000000000000ll);
       w.rid[t] = 0xFFFFFFFFu;
@@ -222,7 +301,7 @@ __global__ void __launch_bounds__(256) route_kernel(RouteArgs a) {
         int half = (deg + 1) >> 1;
         ct.scanned += half;
         int64_t before = ct.evals;
-        int ins = expand(a, w, node, half, vis, vlog, logn, ct.evals);
+        int ins = expand(a, w, node, half, vis, vlog, logn, ct.evals, fast);
         ct.p1_evals += ct.evals - before;
         lb = sel + 1;
         if (ins < lb) lb = ins;
@@ -243,7 +322,7 @@ __global__ void __launch_bounds__(256) route_kernel(RouteArgs a) {
         ct.hops += 1;
         int deg = __ldg(a.nbr_counts + node);
         ct.scanned += deg;
-        int ins = expand(a, w, node, deg, vis, vlog, logn, ct.evals);
+        int ins = expand(a, w, node, deg, vis, vlog, logn, ct.evals, fast);
         lb = sel + 1;
         if (ins < lb) lb = ins;
       }
@@ -307,6 +386,35 @@ int route_occupancy(int warps_per_cta, size_t smem, int* ctas_per_sm) {
   if (e != cudaSuccess) return (int)e;
   return (int)cudaOccupancyMaxActiveBlocksPerMultiprocessor(ctas_per_sm, route_kernel,
                                                             warps_per_cta * 32, smem);
+}
+
+}  // namespace sb
+
+namespace sb {
+
+// index property for the order-free exact mode: are all features integral, and max |x|
+__global__ void feature_scan_kernel(const float* F, int64_t count, unsigned* nonint,
+                                    unsigned* maxbits) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  bool bad = false;
+  float mx = 0.f;
+  for (; i < count; i += stride) {
+    float v = F[i];
+    bad = bad || v != rintf(v) || !isfinite(v);
+    mx = fmaxf(mx, fabsf(v));
+  }
+  if (__any_sync(0xffffffffu, bad) && lane_id() == 0) atomicOr(nonint, 1u);
+  for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  if (lane_id() == 0) atomicMax(maxbits, __float_as_uint(mx));
+}
+
+int launch_feature_scan(const float* F, int64_t count, unsigned* nonint, unsigned* maxbits,
+                        cudaStream_t st) {
+  cudaMemsetAsync(nonint, 0, sizeof(unsigned), st);
+  cudaMemsetAsync(maxbits, 0, sizeof(unsigned), st);
+  feature_scan_kernel<<<1184, 256, 0, st>>>(F, count, nonint, maxbits);
+  return (int)cudaGetLastError();
 }
 
 }  // namespace sb

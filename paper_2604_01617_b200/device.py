@@ -71,6 +71,15 @@ class DeviceIndex:
     def launch_count(self) -> int:
         return int(_lib.load().sb_launch_count(self._h))
 
+    def info(self) -> dict:
+        ie = ctypes.c_int32(0)
+        fm = ctypes.c_double(0.0)
+        _lib.call("sb_index_info", self._h, ctypes.addressof(ie), ctypes.addressof(fm))
+        return {"int_exact": bool(ie.value), "fmax_abs": fm.value}
+
+    def set_distance_mode(self, sequential: bool):
+        _lib.call("sb_set_distance_mode", self._h, 1 if sequential else 0)
+
     # ---- HELP build ------------------------------------------------------------------
     def init_graph(self, ids: np.ndarray, inv_alpha: float):
         ids = c64(ids, np.int32)

@@ -199,6 +199,46 @@ def test_route_random_graph_vs_oracle():
         np.testing.assert_array_equal(got[2][:, :4], want[2], err_msg=f"k={k}")
 
 
+def test_order_free_mode_is_bit_exact():
+    """Integer-valued data routes through the warp-split distance path; it must equal both
+    the sequential path and the oracle bit for bit (ids, fp64 dists, all stats)."""
+    rng = np.random.default_rng(3)
+    n, m, l, g = 6000, 128, 3, 24
+    f = np.clip(np.rint(rng.normal(128, 40, (n, m))), 0, 255).astype(np.float32)
+    a = rng.integers(1, 6, (n, l)).astype(np.int32)
+    ids = np.stack([rng.choice(n, g, replace=False) for _ in range(n)]).astype(np.int32)
+    cnt = rng.integers(1, g + 1, n).astype(np.int32)
+    graph = sb.RelationGraph(features=f, attrs=a, schema=sb.AttributeSchema((("x",),) * l),
+                             metric=sb.MetricConfig.manual(1.03, l), sigma=0.44, nbr_ids=ids,
+                             nbr_dists=np.zeros((n, g), np.float32), nbr_counts=cnt, frozen=True)
+    dev = graph.device()
+    assert dev.info()["int_exact"]
+    qf = np.clip(np.rint(rng.normal(128, 40, (48, m))), 0, 255).astype(np.float32)
+    qa = rng.integers(1, 6, (48, l)).astype(np.int32)
+    for k in (5, 64, 257):
+        p = sb.SearchParams(k=k, seed=2)
+        fast = sb.search_batch_arrays(graph, qf, qa, p)
+        dev.set_distance_mode(sequential=True)
+        seq = sb.search_batch_arrays(graph, qf, qa, p)
+        dev.set_distance_mode(sequential=False)
+        want = O.search_batch(f, a, ids, cnt, 1.03, qf, qa, k, seed=2)
+        for got in (fast, seq):
+            np.testing.assert_array_equal(got[0], want[0])
+            np.testing.assert_array_equal(got[1], want[1])
+            np.testing.assert_array_equal(got[2][:, :4], want[2])
+    # a non-integral query falls back to the sequential path, still exact
+    qf2 = qf + 0.25
+    got = sb.search_batch_arrays(graph, qf2, qa, sb.SearchParams(k=33))
+    want = O.search_batch(f, a, ids, cnt, 1.03, qf2, qa, 33)
+    np.testing.assert_array_equal(got[0], want[0])
+    np.testing.assert_array_equal(got[1], want[1])
+    # real-valued features never take the order-free path
+    fr = f + np.float32(0.5)
+    assert not sb.RelationGraph(features=fr, attrs=a, schema=graph.schema, metric=graph.metric,
+                                sigma=0.44, nbr_ids=ids, nbr_dists=graph.nbr_dists,
+                                nbr_counts=cnt, frozen=True).device().info()["int_exact"]
+
+
 @pytest.mark.slow
 def test_cfg1_end_to_end(cfg1_golden):
     """BASELINE config 1 through the public API: alpha, psi history, edge counts, final
