@@ -15,7 +15,7 @@ import numpy as np
 from .errors import ConstraintError, FormatError
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libstable_b200.so")
+LIB_PATH = os.environ.get("STABLE_B200_LIB") or os.path.join(_HERE, "libstable_b200.so")
 
 SB_OK, SB_EARG, SB_EFORMAT, SB_ECONSTRAINT, SB_ECUDA = 0, 1, 2, 3, 4
 

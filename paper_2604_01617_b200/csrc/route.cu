@@ -32,7 +32,7 @@ constexpr uint32_t kChkP = 0x40000000u;   // phase-1 (pioneer) checked
 constexpr uint32_t kIdMask = 0x3FFFFFFFu;
 
 // exact fp64 AUTO distance of node v against the query held in shared memory
-SB_DEV double query_dist(const RouteArgs& a, int64_t v, const double* qs, const double* qas,
+__device__ __noinline__ double query_dist(const RouteArgs& a, int64_t v, const double* qs, const double* qas,
                          const double* qms) {
   const float* x = a.F + v * (int64_t)a.m;
   double s = 0.0;
@@ -76,8 +76,8 @@ SB_DEV double query_dist(const RouteArgs& a, int64_t v, const double* qs, const 
 // every (x - q)^2 term and every partial sum is an integer below 2^53, so fp64 addition is
 // exact in any order and the result equals the sequential one bit for bit.  lpr lanes share
 // a row (128-bit loads, coalesced), kRows rows per lane group in flight, xor-shuffle reduce.
-constexpr int kRows = 8;
-SB_DEV void batch_dist_warp(const RouteArgs& a, const uint32_t* cid, double* cd, int c,
+constexpr int kRows = 4;
+__device__ __noinline__ void batch_dist_warp(const RouteArgs& a, const uint32_t* cid, double* cd, int c,
                             const double* qs, const double* qas, const double* qms) {
   const int lane = lane_id();
   const int lpr = a.lpr;
@@ -85,26 +85,28 @@ SB_DEV void batch_dist_warp(const RouteArgs& a, const uint32_t* cid, double* cd,
   const int sub = lane & (lpr - 1);
   const int grp = lane / lpr;
   const int nq = a.m >> 2;
+  const float4* F4 = reinterpret_cast<const float4*>(a.F);
   for (int base = 0; base < c; base += rpp * kRows) {
     double part[kRows];
-    const float4* rows[kRows];
+    uint32_t rid[kRows];
 #pragma unroll
     for (int g = 0; g < kRows; ++g) {
       int r = base + grp + rpp * g;
-      rows[g] = r < c ? reinterpret_cast<const float4*>(a.F + (int64_t)cid[r] * a.m) : nullptr;
+      rid[g] = r < c ? cid[r] : 0xFFFFFFFFu;
       part[g] = 0.0;
     }
     for (int k = sub; k < nq; k += lpr) {
       float4 x[kRows];
 #pragma unroll
       for (int g = 0; g < kRows; ++g)
-        if (rows[g]) x[g] = __ldg(rows[g] + k);
+        if (rid[g] != 0xFFFFFFFFu) x[g] = __ldg(F4 + (int64_t)rid[g] * nq + k);
       const double* qv = qs + 4 * k;
+      const double q0 = qv[0], q1 = qv[1], q2 = qv[2], q3 = qv[3];
 #pragma unroll
       for (int g = 0; g < kRows; ++g)
-        if (rows[g]) {
-          double d0 = dsub(x[g].x, qv[0]), d1 = dsub(x[g].y, qv[1]);
-          double d2 = dsub(x[g].z, qv[2]), d3 = dsub(x[g].w, qv[3]);
+        if (rid[g] != 0xFFFFFFFFu) {
+          double d0 = dsub(x[g].x, q0), d1 = dsub(x[g].y, q1);
+          double d2 = dsub(x[g].z, q2), d3 = dsub(x[g].w, q3);
           part[g] = dadd(part[g], dadd(dadd(dmul(d0, d0), dmul(d1, d1)), dadd(dmul(d2, d2), dmul(d3, d3))));
         }
     }
@@ -181,7 +183,7 @@ struct Counters {
 
 // Expand `node` over its first `cnt` stored neighbours: test-and-set the visited bits,
 // evaluate the unvisited ones, merge into R.  Returns min insert position (or K).
-SB_DEV int expand(const RouteArgs& a, WarpSmem& w, int64_t node, int cnt, uint32_t* vis,
+__device__ __noinline__ int expand(const RouteArgs& a, WarpSmem& w, int64_t node, int cnt, uint32_t* vis,
                   uint32_t* vlog, int& logn, int64_t& evals_out, bool fast) {
   const int lane = lane_id();
   const int32_t* nb = a.nbr_ids + node * (int64_t)a.g;
@@ -220,7 +222,8 @@ SB_DEV int expand(const RouteArgs& a, WarpSmem& w, int64_t node, int cnt, uint32
   return merge_into_r(w, a.K, c);
 }
 
-__global__ void __launch_bounds__(256) route_kernel(RouteArgs a) {
+// 256 threads x 3 CTAs per SM (<= 85 registers per thread, 24 warps resident)
+__global__ void __launch_bounds__(256, 3) route_kernel(RouteArgs a) {
   extern __shared__ __align__(16) char smem_raw[];
   const int lane = lane_id();
   const int wid = warp_id();

@@ -1,0 +1,44 @@
+"""Route-kernel micro-benchmark: build the cfg index once (cached to /tmp), then time the
+routing launch at K with device-resident inputs and precomputed entries (CUDA events)."""
+import os, sys, time
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np
+import torch
+import paper_2604_01617_b200 as sb
+from paper_2604_01617_b200.device import DeviceIndex, entry_points_host
+from tools.configs import make_config
+
+cfgname = os.environ.get("CFG", "cfg2")
+K = int(os.environ.get("K", "200"))
+X, A, QX, QA, card = make_config(cfgname)
+cache = f"/tmp/sb_graph_{cfgname}.npz"
+if os.path.exists(cache):
+    z = np.load(cache); ids, dists, counts, alpha = z["ids"], z["dists"], z["counts"], float(z["alpha"])
+else:
+    cfg = sb.compute_alpha(sb.sample_statistics(X, A, 1000, seed=0), X.shape[0], A.shape[1])
+    g = sb.build(X, A, sb.AttributeSchema(tuple(tuple(str(i) for i in range(c)) for c in card)), sb.BuildParams(), cfg)
+    ids, dists, counts, alpha = g.nbr_ids, g.nbr_dists, g.nbr_counts, cfg.alpha
+    np.savez(cache, ids=ids, dists=dists, counts=counts, alpha=alpha)
+dev = DeviceIndex(X, A, ids.shape[1])
+dev.upload(ids, dists, counts)
+if os.environ.get("SEQ"): dev.set_distance_mode(True)
+q, m = QX.shape
+P = max(1, K // 2)
+s = torch.cuda.Stream(); torch.cuda.set_stream(s); dev.set_stream(s.cuda_stream)
+qf = torch.from_numpy(QX.astype(np.float64)).cuda(); qa = torch.from_numpy(QA.astype(np.float64)).cuda()
+ent = torch.from_numpy(entry_points_host(X.shape[0], K, 0, 0, q)).cuda()
+out_i = torch.empty((q, K), dtype=torch.int64, device="cuda"); out_d = torch.empty((q, K), dtype=torch.float64, device="cuda")
+st = torch.empty((q, 5), dtype=torch.int64, device="cuda")
+def run():
+    dev.route_dev(qf.data_ptr(), qa.data_ptr(), None, q, K, P, 1.0 / alpha, out_i.data_ptr(), out_d.data_ptr(), st.data_ptr(), entries_ptr=ent.data_ptr())
+for _ in range(3): run()
+torch.cuda.synchronize()
+e0 = torch.cuda.Event(enable_timing=True); e1 = torch.cuda.Event(enable_timing=True)
+e0.record(s)
+for _ in range(5): run()
+e1.record(s); torch.cuda.synchronize()
+ms = e0.elapsed_time(e1) / 5
+stn = st.cpu().numpy().astype(np.float64)
+byt = (stn[:, 0] * (4 * m + 4 * A.shape[1]) + 4 * (stn[:, 2] + stn[:, 3] + stn[:, 4])).sum()
+print(f"lib={os.path.basename(os.environ.get('STABLE_B200_LIB','default'))} K={K} route {ms:.3f} ms  {q/ms*1e3:,.0f} QPS  {byt/ms/1e6:,.1f} GB/s  "
+      f"evals={stn[:,0].mean():.0f} p1_exp={stn[:,2].mean():.1f} hops={stn[:,3].mean():.1f} scanned={stn[:,4].mean():.0f}  ids_sum={int(out_i.sum())}", flush=True)
