@@ -140,11 +140,11 @@ int sb_route_batch_dev(sb_index* idx, const double* qf, const double* qa, const 
 /* number of kernel launches this handle issued since creation (instrumentation) */
 int64_t sb_launch_count(sb_index* idx);
 
-/* *int_exact = 1 when every feature is an integer (|x| <= *fmax_abs): then a query whose
- * coordinates are integers with (fmax + max|q|)^2 * m < 2^53 is routed with warp-split
- * distance sums, which are exact in any order and bit-identical to the sequential ones. */
+/* *int_exact = 1 when every feature is an integer (|x| <= *fmax_abs); such data admits exact
+ * reduced-precision / reordered distance sums. */
 int sb_index_info(sb_index* idx, int32_t* int_exact, double* fmax_abs);
-/* 0 = auto (default), 1 = always the sequential one-row-per-lane distance path */
+/* routing row loads: 0 = staged through shared memory with cp.async (default),
+ * 1 = each lane reads its row from global memory directly; both bit-exact */
 int sb_set_distance_mode(sb_index* idx, int32_t mode);
 
 #ifdef __cplusplus

@@ -3,6 +3,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 #include <stdio.h>
+#include <stdlib.h>
 #include <string.h>
 
 #include <algorithm>
@@ -832,11 +833,18 @@ static int route_dev(sb_index* idx, const double* qf, const double* qa, const do
   a.out_dists = out_dists; a.stats = out_stats;
   a.Kpad = next_pow2(k);
   a.Cpad = next_pow2(idx->g);
-  a.int_exact = idx->int_exact && !idx->force_sequential ? 1 : 0;
-  a.fmax = idx->fmax;
-  a.lpr = std::min(32, next_pow2(std::max(1, idx->m / 4)));
-  size_t per_warp = sb::route_smem_per_warp(a.Kpad, a.Cpad, idx->m, idx->l);
-  int wpc = (int)std::max<size_t>(1, std::min<size_t>(8, (size_t)(100 * 1024) / per_warp));
+  // row stage: rows 16-byte aligned (m % 4 == 0) -> stage ~8 KB of rows per warp
+  a.stride = idx->m + 4;
+  a.stage_rows = 0;
+  if (idx->m % 4 == 0 && !idx->force_sequential) {
+    int want = (int)std::max<int64_t>(1, (8 * 1024) / (4 * (int64_t)a.stride));
+    if (const char* e = getenv("SB_ROUTE_STAGE_ROWS")) want = std::max(1, atoi(e));
+    a.stage_rows = std::min(32, want);
+  }
+  size_t per_warp = sb::route_smem_per_warp(a);
+  int wpc_max = 8;
+  if (const char* e = getenv("SB_ROUTE_WPC")) wpc_max = std::max(1, std::min(8, atoi(e)));
+  int wpc = (int)std::max<size_t>(1, std::min<size_t>(wpc_max, (size_t)(110 * 1024) / per_warp));
   if (per_warp * wpc > 227 * 1024) return fail(SB_EARG, "k too large for the routing kernel");
   int per_sm = 0;
   CKL(sb::route_occupancy(wpc, per_warp * wpc, &per_sm));

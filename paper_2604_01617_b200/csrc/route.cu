@@ -12,9 +12,12 @@
 //   into R.  Sequential bounded insertion into a strictly ordered list equals top-K of the
 //   union (evicted entries can never return), so ids, distances and all four SearchStats
 //   counters equal the reference's.
-// * Distances: one neighbour row per lane, fp64, ascending dimension order, explicitly
-//   rounded ops — bit-identical to _query_dist (_kernels.py:26-35).  Rows are gathered
-//   with 128-bit loads, 8 in flight per lane.
+// * Memory round trips per expansion are the bound (each query is a serial walk), so each
+//   step issues everything it can at once: the neighbour count and the whole id row load
+//   together; all visited test-and-sets go out together; all unvisited rows are copied
+//   into a per-warp shared-memory stage with cp.async (16 B per copy, no registers held).
+// * Distances: one staged row per lane, fp64, ascending dimension order, explicitly rounded
+//   operations — bit-identical to _query_dist (_kernels.py:26-35) for any data.
 // * Visited set: exact, one bitset of ceil(n/32) words per warp slot in HBM, set with
 //   atomicOr (test-and-set); cleared after each query from a per-slot log of visited ids
 //   (a full clear when the log overflows).
@@ -31,40 +34,12 @@ constexpr uint32_t kChkR = 0x80000000u;   // phase-2 checked
 constexpr uint32_t kChkP = 0x40000000u;   // phase-1 (pioneer) checked
 constexpr uint32_t kIdMask = 0x3FFFFFFFu;
 
-// exact fp64 AUTO distance of node v against the query held in shared memory
-__device__ __noinline__ double query_dist(const RouteArgs& a, int64_t v, const double* qs, const double* qas,
-                         const double* qms) {
+// ---- fallback when rows are not 16-byte aligned (m % 4 != 0): lane-owned global reads ---
+__device__ __noinline__ double query_dist_global(const RouteArgs& a, int64_t v, const double* qs,
+                                                 const double* qas, const double* qms) {
   const float* x = a.F + v * (int64_t)a.m;
   double s = 0.0;
-  int t = 0;
-  if ((a.m & 3) == 0) {
-    const float4* vx = reinterpret_cast<const float4*>(x);
-    int nq = a.m >> 2;
-    int qq = 0;
-    for (; qq + 8 <= nq; qq += 8) {
-      float4 r[8];
-#pragma unroll
-      for (int u = 0; u < 8; ++u) r[u] = __ldg(vx + qq + u);
-#pragma unroll
-      for (int u = 0; u < 8; ++u) {
-        const double* qv = qs + 4 * (qq + u);
-        s = sq_step(s, r[u].x, qv[0]);
-        s = sq_step(s, r[u].y, qv[1]);
-        s = sq_step(s, r[u].z, qv[2]);
-        s = sq_step(s, r[u].w, qv[3]);
-      }
-    }
-    for (; qq < nq; ++qq) {
-      float4 r = __ldg(vx + qq);
-      const double* qv = qs + 4 * qq;
-      s = sq_step(s, r.x, qv[0]);
-      s = sq_step(s, r.y, qv[1]);
-      s = sq_step(s, r.z, qv[2]);
-      s = sq_step(s, r.w, qv[3]);
-    }
-    t = a.m;
-  }
-  for (; t < a.m; ++t) s = sq_step(s, __ldg(x + t), qs[t]);
+  for (int t = 0; t < a.m; ++t) s = sq_step(s, __ldg(x + t), qs[t]);
   const int32_t* av = a.A + v * (int64_t)a.l;
   double sa = 0.0;
   for (int u = 0; u < a.l; ++u)
@@ -72,164 +47,181 @@ __device__ __noinline__ double query_dist(const RouteArgs& a, int64_t v, const d
   return auto_finish(s, sa, a.inv_alpha);
 }
 
-// Order-free exact distances for a batch of rows (ids in cid[0..c) -> cd).  Valid only when
-// every (x - q)^2 term and every partial sum is an integer below 2^53, so fp64 addition is
-// exact in any order and the result equals the sequential one bit for bit.  lpr lanes share
-// a row (128-bit loads, coalesced), kRows rows per lane group in flight, xor-shuffle reduce.
-constexpr int kRows = 4;
-__device__ __noinline__ void batch_dist_warp(const RouteArgs& a, const uint32_t* cid, double* cd, int c,
-                            const double* qs, const double* qas, const double* qms) {
-  const int lane = lane_id();
-  const int lpr = a.lpr;
-  const int rpp = 32 / lpr;
-  const int sub = lane & (lpr - 1);
-  const int grp = lane / lpr;
-  const int nq = a.m >> 2;
-  const float4* F4 = reinterpret_cast<const float4*>(a.F);
-  for (int base = 0; base < c; base += rpp * kRows) {
-    double part[kRows];
-    uint32_t rid[kRows];
-#pragma unroll
-    for (int g = 0; g < kRows; ++g) {
-      int r = base + grp + rpp * g;
-      rid[g] = r < c ? cid[r] : 0xFFFFFFFFu;
-      part[g] = 0.0;
-    }
-    for (int k = sub; k < nq; k += lpr) {
-      float4 x[kRows];
-#pragma unroll
-      for (int g = 0; g < kRows; ++g)
-        if (rid[g] != 0xFFFFFFFFu) x[g] = __ldg(F4 + (int64_t)rid[g] * nq + k);
-      const double* qv = qs + 4 * k;
-      const double q0 = qv[0], q1 = qv[1], q2 = qv[2], q3 = qv[3];
-#pragma unroll
-      for (int g = 0; g < kRows; ++g)
-        if (rid[g] != 0xFFFFFFFFu) {
-          double d0 = dsub(x[g].x, q0), d1 = dsub(x[g].y, q1);
-          double d2 = dsub(x[g].z, q2), d3 = dsub(x[g].w, q3);
-          part[g] = dadd(part[g], dadd(dadd(dmul(d0, d0), dmul(d1, d1)), dadd(dmul(d2, d2), dmul(d3, d3))));
-        }
-    }
-#pragma unroll
-    for (int g = 0; g < kRows; ++g)
-      for (int o = lpr >> 1; o > 0; o >>= 1) part[g] = dadd(part[g], __shfl_xor_sync(0xffffffffu, part[g], o));
-    if (sub == 0) {
-#pragma unroll
-      for (int g = 0; g < kRows; ++g) {
-        int r = base + grp + rpp * g;
-        if (r < c) {
-          const int32_t* av = a.A + (int64_t)cid[r] * a.l;
-          double sa = 0.0;
-          for (int u = 0; u < a.l; ++u)
-            sa = dadd(sa, dmul(qms[u], fabs(dsub((double)__ldg(av + u), qas[u]))));
-          cd[r] = auto_finish(part[g], sa, a.inv_alpha);
-        }
-      }
-    }
-  }
+SB_DEV void cp_async16(void* smem_dst, const void* gsrc) {
+  unsigned d = (unsigned)__cvta_generic_to_shared(smem_dst);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(d), "l"(gsrc) : "memory");
+}
+SB_DEV void cp_async_wait_all() {
+  asm volatile("cp.async.commit_group;\n" ::: "memory");
+  asm volatile("cp.async.wait_group 0;\n" ::: "memory");
 }
 
 struct WarpSmem {
+  float* stage;   // stage_rows x stride (16-byte aligned, first in the warp's slice)
   double* rd;     // Kpad
-  uint32_t* rid;  // Kpad
   double* cd;     // Cpad
-  uint32_t* cid;  // Cpad
-  int* cpos;      // Cpad
   double* qs;     // m
   double* qas;    // l
   double* qms;    // l
+  uint32_t* rid;  // Kpad
+  uint32_t* cid;  // Cpad
+  int* cpos;      // Cpad
 };
 
-SB_HD size_t route_warp_smem_bytes(int Kpad, int Cpad, int m, int l) {
-  size_t b = (size_t)Kpad * 8 + (size_t)Cpad * 8 + (size_t)m * 8 + (size_t)l * 16;  // doubles
-  b += (size_t)Kpad * 4 + (size_t)Cpad * 8;                                          // u32/int
+SB_HD size_t route_warp_smem_bytes_full(int Kpad, int Cpad, int m, int l, int stage_rows,
+                                        int stride) {
+  size_t b = (size_t)stage_rows * stride * 4;
+  b += (size_t)Kpad * 8 + (size_t)Cpad * 8 + (size_t)m * 8 + (size_t)l * 16;
+  b += (size_t)Kpad * 4 + (size_t)Cpad * 8;
   return (b + 15) & ~(size_t)15;
 }
 
-SB_DEV WarpSmem carve(char* base, int Kpad, int Cpad, int m, int l) {
+SB_DEV WarpSmem carve(char* base, const RouteArgs& a) {
   WarpSmem w;
-  double* dp = reinterpret_cast<double*>(base);
-  w.rd = dp; dp += Kpad;
-  w.cd = dp; dp += Cpad;
-  w.qs = dp; dp += m;
-  w.qas = dp; dp += l;
-  w.qms = dp; dp += l;
+  w.stage = reinterpret_cast<float*>(base);
+  double* dp = reinterpret_cast<double*>(base + (size_t)a.stage_rows * a.stride * 4);
+  w.rd = dp; dp += a.Kpad;
+  w.cd = dp; dp += a.Cpad;
+  w.qs = dp; dp += a.m;
+  w.qas = dp; dp += a.l;
+  w.qms = dp; dp += a.l;
   uint32_t* up = reinterpret_cast<uint32_t*>(dp);
-  w.rid = up; up += Kpad;
-  w.cid = up; up += Cpad;
+  w.rid = up; up += a.Kpad;
+  w.cid = up; up += a.Cpad;
   w.cpos = reinterpret_cast<int*>(up);
   return w;
 }
 
-// first position in [lb, hi) whose id word lacks `bit`; -1 if none
-SB_DEV int first_unchecked(const uint32_t* rid, int lb, int hi, uint32_t bit) {
+// Exact distances of rows ids[0..c) -> out[0..c): copy up to stage_rows rows at once into the
+// warp's stage (all copies in flight together), then one row per lane, sequential order.
+SB_DEV void eval_rows(const RouteArgs& a, WarpSmem& w, const uint32_t* ids, double* out, int c) {
+  const int lane = lane_id();
+  if (a.stage_rows == 0) {
+    for (int j = lane; j < c; j += 32) out[j] = query_dist_global(a, ids[j], w.qs, w.qas, w.qms);
+    __syncwarp();
+    return;
+  }
+  const int nq = a.m >> 2;
+  for (int ch = 0; ch < c; ch += a.stage_rows) {
+    const int cc = c - ch < a.stage_rows ? c - ch : a.stage_rows;
+    const int items = cc * nq;
+    for (int it = lane; it < items; it += 32) {
+      const int r = it / nq, p = it - r * nq;
+      cp_async16(w.stage + r * a.stride + 4 * p, a.F + (int64_t)ids[ch + r] * a.m + 4 * p);
+    }
+    cp_async_wait_all();
+    __syncwarp();
+    if (lane < cc) {
+      const float4* row = reinterpret_cast<const float4*>(w.stage + lane * a.stride);
+      double s = 0.0;
+      for (int p = 0; p < nq; ++p) {
+        float4 v = row[p];
+        const double* q = w.qs + 4 * p;
+        s = sq_step(s, v.x, q[0]);
+        s = sq_step(s, v.y, q[1]);
+        s = sq_step(s, v.z, q[2]);
+        s = sq_step(s, v.w, q[3]);
+      }
+      const int32_t* av = a.A + (int64_t)ids[ch + lane] * a.l;
+      double sa = 0.0;
+      for (int u = 0; u < a.l; ++u)
+        sa = dadd(sa, dmul(w.qms[u], fabs(dsub((double)__ldg(av + u), w.qas[u]))));
+      out[ch + lane] = auto_finish(s, sa, a.inv_alpha);
+    }
+    __syncwarp();
+  }
+}
+
+// first (and second) position in [lb, hi) whose id word lacks `bit`; -1 if none
+SB_DEV int first_unchecked(const uint32_t* rid, int lb, int hi, uint32_t bit, int* second) {
+  *second = -1;
   for (int base = lb; base < hi; base += 32) {
     int i = base + lane_id();
     bool un = i < hi && !(rid[i] & bit);
     unsigned bal = __ballot_sync(0xffffffffu, un);
-    if (bal) return base + __ffs(bal) - 1;
+    if (bal) {
+      int f = __ffs(bal) - 1;
+      unsigned rest = bal & (bal - 1u);
+      if (rest) *second = base + __ffs(rest) - 1;
+      return base + f;
+    }
   }
   return -1;
-}
-
-// Merge the c candidates in (cd, cid) into R (size K); see warp_merge_topk.
-SB_DEV int merge_into_r(WarpSmem& w, int K, int c) {
-  return warp_merge_topk(w.rd, w.rid, K, w.cd, w.cid, w.cpos, c, kIdMask);
 }
 
 struct Counters {
   int64_t evals, p1_evals, p1_exp, hops, scanned;
 };
 
-// Expand `node` over its first `cnt` stored neighbours: test-and-set the visited bits,
-// evaluate the unvisited ones, merge into R.  Returns min insert position (or K).
-__device__ __noinline__ int expand(const RouteArgs& a, WarpSmem& w, int64_t node, int cnt, uint32_t* vis,
-                  uint32_t* vlog, int& logn, int64_t& evals_out, bool fast) {
+// warm L2 with the neighbour row of a node we will probably expand next
+SB_DEV void prefetch_row(const RouteArgs& a, uint32_t node) {
   const int lane = lane_id();
-  const int32_t* nb = a.nbr_ids + node * (int64_t)a.g;
-  // gather unvisited neighbours into the candidate buffer (ids only)
-  int c = 0;
-  for (int base = 0; base < cnt; base += 32) {
-    int t = base + lane;
-    bool fresh = false;
-    uint32_t v = 0;
-    if (t < cnt) {
-      v = (uint32_t)__ldg(nb + t);
-      uint32_t bit = 1u << (v & 31);
-      uint32_t old = atomicOr(vis + (v >> 5), bit);
-      fresh = !(old & bit);
-    }
-    unsigned bal = __ballot_sync(0xffffffffu, fresh);
-    if (fresh) {
-      int pos = c + __popc(bal & ((1u << lane) - 1u));
-      w.cid[pos] = v;
-      int lp = logn + pos;
-      if (lp < a.logcap) vlog[lp] = v;
-    }
-    c += __popc(bal);
-  }
-  logn += c;
-  evals_out += c;
-  __syncwarp();
-  // evaluate: warp-split rows (order-free exact mode) or one row per lane, sequential order
-  if (fast) {
-    batch_dist_warp(a, w.cid, w.cd, c, w.qs, w.qas, w.qms);
-  } else {
-    for (int j = lane; j < c; j += 32) w.cd[j] = query_dist(a, w.cid[j], w.qs, w.qas, w.qms);
-  }
-  __syncwarp();
-  if (c == 0) return a.K;
-  return merge_into_r(w, a.K, c);
+  const char* p = reinterpret_cast<const char*>(a.nbr_ids + (int64_t)node * a.g);
+  const int bytes = a.g * 4;
+  if (lane * 128 < bytes) asm volatile("prefetch.global.L2 [%0];" ::"l"(p + lane * 128));
 }
 
-// 256 threads x 3 CTAs per SM (<= 85 registers per thread, 24 warps resident)
+// Expand `node`: read its count and id row together, test-and-set the visited bits of the
+// first cnt neighbours (cnt = ceil(deg/2) in phase 1), evaluate the unvisited ones, merge
+// into R.  Returns the lowest position that received an entry (or K).
+__device__ __noinline__ int expand(const RouteArgs& a, WarpSmem& w, uint32_t node, bool half,
+                                   uint32_t* vis, uint32_t* vlog, int& logn, Counters& ct) {
+  const int lane = lane_id();
+  const int32_t* nb = a.nbr_ids + (int64_t)node * a.g;
+  const int deg = __ldg(a.nbr_counts + node);
+  int c = 0;
+  for (int base = 0; base < a.g; base += 128) {
+    // up to 4 ids per lane per pass, loaded before the count is known
+    uint32_t v[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      int t = base + lane + 32 * k;
+      v[k] = t < a.g ? (uint32_t)__ldg(nb + t) : 0u;
+    }
+    const int cnt = half ? (deg + 1) >> 1 : deg;
+    if (base >= cnt) break;
+    bool fresh[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      int t = base + lane + 32 * k;
+      fresh[k] = false;
+      if (t < cnt) {
+        uint32_t bit = 1u << (v[k] & 31);
+        uint32_t old = atomicOr(vis + (v[k] >> 5), bit);
+        fresh[k] = !(old & bit);
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      unsigned bal = __ballot_sync(0xffffffffu, fresh[k]);
+      if (fresh[k]) {
+        int pos = c + __popc(bal & ((1u << lane) - 1u));
+        w.cid[pos] = v[k];
+        int lp = logn + pos;
+        if (lp < a.logcap) vlog[lp] = v[k];
+      }
+      c += __popc(bal);
+    }
+  }
+  const int cnt = half ? (deg + 1) >> 1 : deg;
+  ct.scanned += cnt;
+  logn += c;
+  ct.evals += c;
+  if (half) ct.p1_evals += c;
+  __syncwarp();
+  if (c == 0) return a.K;
+  eval_rows(a, w, w.cid, w.cd, c);
+  return warp_merge_topk(w.rd, w.rid, a.K, w.cd, w.cid, w.cpos, c, kIdMask);
+}
+
+// 256 threads x 3 CTAs per SM (<= 85 registers per thread)
 __global__ void __launch_bounds__(256, 3) route_kernel(RouteArgs a) {
   extern __shared__ __align__(16) char smem_raw[];
   const int lane = lane_id();
   const int wid = warp_id();
   const int nw = blockDim.x >> 5;
-  const size_t wbytes = route_warp_smem_bytes(a.Kpad, a.Cpad, a.m, a.l);
-  WarpSmem w = carve(smem_raw + wbytes * wid, a.Kpad, a.Cpad, a.m, a.l);
+  const size_t wbytes = route_warp_smem_bytes_full(a.Kpad, a.Cpad, a.m, a.l, a.stage_rows, a.stride);
+  WarpSmem w = carve(smem_raw + wbytes * wid, a);
   const int64_t slot = (int64_t)blockIdx.x * nw + wid;
   uint32_t* vis = a.visited + slot * a.vwords;
   uint32_t* vlog = a.vlog + slot * (int64_t)a.logcap;
@@ -247,21 +239,6 @@ __global__ void __launch_bounds__(256, 3) route_kernel(RouteArgs a) {
       w.qms[t] = a.qm ? a.qm[(int64_t)qi * a.l + t] : 1.0;
     }
     __syncwarp();
-    // order-free exact mode for this query: integral coordinates, sums below 2^53
-    bool fast = false;
-    if (a.int_exact) {
-      bool integral = true;
-      double qmax = 0.0;
-      for (int t = lane; t < a.m; t += 32) {
-        double v = w.qs[t];
-        integral = integral && v == rint(v);
-        qmax = fmax(qmax, fabs(v));
-      }
-      for (int o = 16; o > 0; o >>= 1) qmax = fmax(qmax, __shfl_xor_sync(0xffffffffu, qmax, o));
-      integral = __all_sync(0xffffffffu, integral);
-      double lim = (a.fmax + qmax) * (a.fmax + qmax) * (double)a.m;
-      fast = integral && lim < 9007199254740992.0;  // 2^53
-    }
 
     Counters ct = {0, 0, 0, 0, 0};
     int logn = 0;
@@ -274,12 +251,7 @@ __global__ void __launch_bounds__(256, 3) route_kernel(RouteArgs a) {
       w.rid[t] = v;
     }
     __syncwarp();
-    if (fast) {
-      batch_dist_warp(a, w.rid, w.rd, K, w.qs, w.qas, w.qms);
-    } else {
-      for (int t = lane; t < K; t += 32) w.rd[t] = query_dist(a, w.rid[t], w.qs, w.qas, w.qms);
-    }
-    __syncwarp();
+    eval_rows(a, w, w.rid, w.rd, K);
     for (int t = K + lane; t < a.Kpad; t += 32) {
       w.rd[t] = __longlong_as_double(0x7FF0000000000000ll);
       w.rid[t] = 0xFFFFFFFFu;
@@ -293,19 +265,16 @@ __global__ void __launch_bounds__(256, 3) route_kernel(RouteArgs a) {
     if (a.use_coarse) {
       int lb = 0;
       for (;;) {
-        int sel = first_unchecked(w.rid, lb, a.P, kChkP);
+        int nxt;
+        int sel = first_unchecked(w.rid, lb, a.P, kChkP, &nxt);
         if (sel < 0) break;
         uint32_t node = w.rid[sel] & kIdMask;
+        if (nxt >= 0) prefetch_row(a, w.rid[nxt] & kIdMask);
         __syncwarp();
         if (lane == 0) w.rid[sel] |= kChkP;
         __syncwarp();
         ct.p1_exp += 1;
-        int deg = __ldg(a.nbr_counts + node);
-        int half = (deg + 1) >> 1;
-        ct.scanned += half;
-        int64_t before = ct.evals;
-        int ins = expand(a, w, node, half, vis, vlog, logn, ct.evals, fast);
-        ct.p1_evals += ct.evals - before;
+        int ins = expand(a, w, node, true, vis, vlog, logn, ct);
         lb = sel + 1;
         if (ins < lb) lb = ins;
       }
@@ -316,16 +285,16 @@ __global__ void __launch_bounds__(256, 3) route_kernel(RouteArgs a) {
     {
       int lb = 0;
       for (;;) {
-        int sel = first_unchecked(w.rid, lb, K, kChkR);
+        int nxt;
+        int sel = first_unchecked(w.rid, lb, K, kChkR, &nxt);
         if (sel < 0) break;
         uint32_t node = w.rid[sel] & kIdMask;
+        if (nxt >= 0) prefetch_row(a, w.rid[nxt] & kIdMask);
         __syncwarp();
         if (lane == 0) w.rid[sel] |= kChkR;
         __syncwarp();
         ct.hops += 1;
-        int deg = __ldg(a.nbr_counts + node);
-        ct.scanned += deg;
-        int ins = expand(a, w, node, deg, vis, vlog, logn, ct.evals, fast);
+        int ins = expand(a, w, node, false, vis, vlog, logn, ct);
         lb = sel + 1;
         if (ins < lb) lb = ins;
       }
@@ -370,12 +339,12 @@ int launch_entry_points(int64_t n, int K, uint64_t seed, int64_t qi0, int64_t q,
   return (int)cudaGetLastError();
 }
 
-size_t route_smem_per_warp(int Kpad, int Cpad, int m, int l) {
-  return route_warp_smem_bytes(Kpad, Cpad, m, l);
+size_t route_smem_per_warp(const RouteArgs& a) {
+  return route_warp_smem_bytes_full(a.Kpad, a.Cpad, a.m, a.l, a.stage_rows, a.stride);
 }
 
 int launch_route(const RouteArgs& a, int warps_per_cta, int ctas, cudaStream_t st) {
-  size_t smem = route_warp_smem_bytes(a.Kpad, a.Cpad, a.m, a.l) * warps_per_cta;
+  size_t smem = route_smem_per_warp(a) * warps_per_cta;
   cudaError_t e = cudaFuncSetAttribute(route_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)smem);
   if (e != cudaSuccess) return (int)e;
@@ -391,11 +360,8 @@ int route_occupancy(int warps_per_cta, size_t smem, int* ctas_per_sm) {
                                                             warps_per_cta * 32, smem);
 }
 
-}  // namespace sb
-
-namespace sb {
-
-// index property for the order-free exact mode: are all features integral, and max |x|
+// index property: are all features integral, and max |x| (used by the exhaustive top-k
+// filter to pick an exact low-precision path)
 __global__ void feature_scan_kernel(const float* F, int64_t count, unsigned* nonint,
                                     unsigned* maxbits) {
   int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;

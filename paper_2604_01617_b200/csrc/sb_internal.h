@@ -30,14 +30,11 @@ struct RouteArgs {
   int logcap;
   int* counter;
   int Kpad, Cpad;
-  // order-free exact mode: all features integral with |x| <= fmax (index property); a query
-  // that is integral too with (fmax + max|q|)^2 * m < 2^53 gets warp-split distances
-  int int_exact;
-  double fmax;
-  int lpr;  // lanes per row in the warp-split layout (power of two, <= 32)
+  // per-warp shared-memory row stage: stage_rows rows of `stride` floats (0: no staging)
+  int stage_rows, stride;
 };
 
-size_t route_smem_per_warp(int Kpad, int Cpad, int m, int l);
+size_t route_smem_per_warp(const RouteArgs& a);
 int launch_feature_scan(const float* F, int64_t count, unsigned* nonint, unsigned* maxbits,
                         cudaStream_t st);
 int route_occupancy(int warps_per_cta, size_t smem, int* ctas_per_sm);
