@@ -833,13 +833,13 @@ static int route_dev(sb_index* idx, const double* qf, const double* qa, const do
   a.out_dists = out_dists; a.stats = out_stats;
   a.Kpad = next_pow2(k);
   a.Cpad = next_pow2(idx->g);
-  // row stage: rows 16-byte aligned (m % 4 == 0) -> stage ~8 KB of rows per warp
-  a.stride = idx->m + 4;
-  a.stage_rows = 0;
+  // lanes per row: the fewest that keep a whole row in flight with <= 8 float4 per lane
+  a.lpr = 0;
   if (idx->m % 4 == 0 && !idx->force_sequential) {
-    int want = (int)std::max<int64_t>(1, (8 * 1024) / (4 * (int64_t)a.stride));
-    if (const char* e = getenv("SB_ROUTE_STAGE_ROWS")) want = std::max(1, atoi(e));
-    a.stage_rows = std::min(32, want);
+    int nq = idx->m / 4, lpr = 1;
+    while (lpr < 32 && (nq + lpr - 1) / lpr > 8) lpr <<= 1;
+    if (const char* e = getenv("SB_ROUTE_LPR")) lpr = std::max(1, std::min(32, atoi(e)));
+    a.lpr = lpr;
   }
   size_t per_warp = sb::route_smem_per_warp(a);
   int wpc_max = 8;

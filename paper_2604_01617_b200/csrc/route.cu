@@ -14,10 +14,10 @@
 //   counters equal the reference's.
 // * Memory round trips per expansion are the bound (each query is a serial walk), so each
 //   step issues everything it can at once: the neighbour count and the whole id row load
-//   together; all visited test-and-sets go out together; all unvisited rows are copied
-//   into a per-warp shared-memory stage with cp.async (16 B per copy, no registers held).
-// * Distances: one staged row per lane, fp64, ascending dimension order, explicitly rounded
-//   operations — bit-identical to _query_dist (_kernels.py:26-35) for any data.
+//   together; all visited test-and-sets go out together; a few lanes share each unvisited
+//   row so that the whole row is in flight at once (eval_rows).
+// * Distances: fp64, ascending dimension order, explicitly rounded operations, the running
+//   sum handed lane to lane — bit-identical to _query_dist (_kernels.py:26-35) for any data.
 // * Visited set: exact, one bitset of ceil(n/32) words per warp slot in HBM, set with
 //   atomicOr (test-and-set); cleared after each query from a per-slot log of visited ids
 //   (a full clear when the log overflows).
@@ -47,17 +47,7 @@ __device__ __noinline__ double query_dist_global(const RouteArgs& a, int64_t v, 
   return auto_finish(s, sa, a.inv_alpha);
 }
 
-SB_DEV void cp_async16(void* smem_dst, const void* gsrc) {
-  unsigned d = (unsigned)__cvta_generic_to_shared(smem_dst);
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(d), "l"(gsrc) : "memory");
-}
-SB_DEV void cp_async_wait_all() {
-  asm volatile("cp.async.commit_group;\n" ::: "memory");
-  asm volatile("cp.async.wait_group 0;\n" ::: "memory");
-}
-
 struct WarpSmem {
-  float* stage;   // stage_rows x stride (16-byte aligned, first in the warp's slice)
   double* rd;     // Kpad
   double* cd;     // Cpad
   double* qs;     // m
@@ -68,18 +58,15 @@ struct WarpSmem {
   int* cpos;      // Cpad
 };
 
-SB_HD size_t route_warp_smem_bytes_full(int Kpad, int Cpad, int m, int l, int stage_rows,
-                                        int stride) {
-  size_t b = (size_t)stage_rows * stride * 4;
-  b += (size_t)Kpad * 8 + (size_t)Cpad * 8 + (size_t)m * 8 + (size_t)l * 16;
+SB_HD size_t route_warp_smem_bytes_full(int Kpad, int Cpad, int m, int l) {
+  size_t b = (size_t)Kpad * 8 + (size_t)Cpad * 8 + (size_t)m * 8 + (size_t)l * 16;
   b += (size_t)Kpad * 4 + (size_t)Cpad * 8;
   return (b + 15) & ~(size_t)15;
 }
 
 SB_DEV WarpSmem carve(char* base, const RouteArgs& a) {
   WarpSmem w;
-  w.stage = reinterpret_cast<float*>(base);
-  double* dp = reinterpret_cast<double*>(base + (size_t)a.stage_rows * a.stride * 4);
+  double* dp = reinterpret_cast<double*>(base);
   w.rd = dp; dp += a.Kpad;
   w.cd = dp; dp += a.Cpad;
   w.qs = dp; dp += a.m;
@@ -92,44 +79,74 @@ SB_DEV WarpSmem carve(char* base, const RouteArgs& a) {
   return w;
 }
 
-// Exact distances of rows ids[0..c) -> out[0..c): copy up to stage_rows rows at once into the
-// warp's stage (all copies in flight together), then one row per lane, sequential order.
+// Exact distances of rows ids[0..c) -> out[0..c).  `lpr` lanes share a row: lane q of the
+// group loads float4s [q*per, (q+1)*per) of the row up front (so a 128-d row arrives in one
+// memory round trip), then the groups' lanes take turns extending the fp64 sum in ascending
+// dimension order, handing the running sum on with a shuffle — the sequential order of
+// _query_dist (_kernels.py:26-35), bit for bit.
+constexpr int kVec = 8;  // float4s a lane keeps in flight
 SB_DEV void eval_rows(const RouteArgs& a, WarpSmem& w, const uint32_t* ids, double* out, int c) {
   const int lane = lane_id();
-  if (a.stage_rows == 0) {
+  if (a.lpr == 0) {
     for (int j = lane; j < c; j += 32) out[j] = query_dist_global(a, ids[j], w.qs, w.qas, w.qms);
     __syncwarp();
     return;
   }
+  const int lpr = a.lpr;
+  const int q = lane & (lpr - 1);
+  const int gbase = lane & ~(lpr - 1);
+  const int rows_pp = 32 / lpr;
   const int nq = a.m >> 2;
-  for (int ch = 0; ch < c; ch += a.stage_rows) {
-    const int cc = c - ch < a.stage_rows ? c - ch : a.stage_rows;
-    const int items = cc * nq;
-    for (int it = lane; it < items; it += 32) {
-      const int r = it / nq, p = it - r * nq;
-      cp_async16(w.stage + r * a.stride + 4 * p, a.F + (int64_t)ids[ch + r] * a.m + 4 * p);
-    }
-    cp_async_wait_all();
-    __syncwarp();
-    if (lane < cc) {
-      const float4* row = reinterpret_cast<const float4*>(w.stage + lane * a.stride);
-      double s = 0.0;
-      for (int p = 0; p < nq; ++p) {
-        float4 v = row[p];
-        const double* q = w.qs + 4 * p;
-        s = sq_step(s, v.x, q[0]);
-        s = sq_step(s, v.y, q[1]);
-        s = sq_step(s, v.z, q[2]);
-        s = sq_step(s, v.w, q[3]);
+  const int per = (nq + lpr - 1) / lpr;
+  const int f0 = q * per;
+  const int f1 = f0 + per < nq ? f0 + per : nq;
+  const float4* F4 = reinterpret_cast<const float4*>(a.F);
+  for (int base = 0; base < c; base += rows_pp) {
+    const int r = base + lane / lpr;
+    const bool valid = r < c;
+    const float4* row = F4 + (int64_t)(valid ? ids[r] : 0) * nq;
+    float4 x[kVec];
+#pragma unroll
+    for (int k = 0; k < kVec; ++k)
+      if (valid && f0 + k < f1) x[k] = __ldg(row + f0 + k);
+    double s = 0.0;
+    for (int step = 0; step < lpr; ++step) {
+      if (q == step && valid) {
+#pragma unroll
+        for (int k = 0; k < kVec; ++k)
+          if (f0 + k < f1) {
+            const double* qv = w.qs + 4 * (f0 + k);
+            s = sq_step(s, x[k].x, qv[0]);
+            s = sq_step(s, x[k].y, qv[1]);
+            s = sq_step(s, x[k].z, qv[2]);
+            s = sq_step(s, x[k].w, qv[3]);
+          }
+        for (int f = f0 + kVec; f < f1; f += kVec) {
+#pragma unroll
+          for (int k = 0; k < kVec; ++k)
+            if (f + k < f1) x[k] = __ldg(row + f + k);
+#pragma unroll
+          for (int k = 0; k < kVec; ++k)
+            if (f + k < f1) {
+              const double* qv = w.qs + 4 * (f + k);
+              s = sq_step(s, x[k].x, qv[0]);
+              s = sq_step(s, x[k].y, qv[1]);
+              s = sq_step(s, x[k].z, qv[2]);
+              s = sq_step(s, x[k].w, qv[3]);
+            }
+        }
       }
-      const int32_t* av = a.A + (int64_t)ids[ch + lane] * a.l;
+      if (lpr > 1) s = __shfl_sync(0xffffffffu, s, gbase | step);
+    }
+    if (q == 0 && valid) {
+      const int32_t* av = a.A + (int64_t)ids[r] * a.l;
       double sa = 0.0;
       for (int u = 0; u < a.l; ++u)
         sa = dadd(sa, dmul(w.qms[u], fabs(dsub((double)__ldg(av + u), w.qas[u]))));
-      out[ch + lane] = auto_finish(s, sa, a.inv_alpha);
+      out[r] = auto_finish(s, sa, a.inv_alpha);
     }
-    __syncwarp();
   }
+  __syncwarp();
 }
 
 // first (and second) position in [lb, hi) whose id word lacks `bit`; -1 if none
@@ -214,13 +231,13 @@ __device__ __noinline__ int expand(const RouteArgs& a, WarpSmem& w, uint32_t nod
   return warp_merge_topk(w.rd, w.rid, a.K, w.cd, w.cid, w.cpos, c, kIdMask);
 }
 
-// 256 threads x 3 CTAs per SM (<= 85 registers per thread)
-__global__ void __launch_bounds__(256, 3) route_kernel(RouteArgs a) {
+// 256 threads x 4 CTAs per SM: <= 64 registers per thread, 32 warps resident
+__global__ void __launch_bounds__(256, 4) route_kernel(RouteArgs a) {
   extern __shared__ __align__(16) char smem_raw[];
   const int lane = lane_id();
   const int wid = warp_id();
   const int nw = blockDim.x >> 5;
-  const size_t wbytes = route_warp_smem_bytes_full(a.Kpad, a.Cpad, a.m, a.l, a.stage_rows, a.stride);
+  const size_t wbytes = route_warp_smem_bytes_full(a.Kpad, a.Cpad, a.m, a.l);
   WarpSmem w = carve(smem_raw + wbytes * wid, a);
   const int64_t slot = (int64_t)blockIdx.x * nw + wid;
   uint32_t* vis = a.visited + slot * a.vwords;
@@ -340,7 +357,7 @@ int launch_entry_points(int64_t n, int K, uint64_t seed, int64_t qi0, int64_t q,
 }
 
 size_t route_smem_per_warp(const RouteArgs& a) {
-  return route_warp_smem_bytes_full(a.Kpad, a.Cpad, a.m, a.l, a.stage_rows, a.stride);
+  return route_warp_smem_bytes_full(a.Kpad, a.Cpad, a.m, a.l);
 }
 
 int launch_route(const RouteArgs& a, int warps_per_cta, int ctas, cudaStream_t st) {

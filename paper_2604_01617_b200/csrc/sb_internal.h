@@ -30,8 +30,8 @@ struct RouteArgs {
   int logcap;
   int* counter;
   int Kpad, Cpad;
-  // per-warp shared-memory row stage: stage_rows rows of `stride` floats (0: no staging)
-  int stage_rows, stride;
+  // lanes sharing one row in eval_rows (power of two <= 32; 0: one lane per row, scalar)
+  int lpr;
 };
 
 size_t route_smem_per_warp(const RouteArgs& a);
