@@ -7,6 +7,7 @@
 #include <string.h>
 
 #include <algorithm>
+#include <cmath>
 #include <string>
 #include <vector>
 
@@ -72,6 +73,7 @@ struct sb_index {
   int sms = 148;
   bool int_exact = false;  // all features integral (order-free exact distances possible)
   double fmax = 0.0;
+  float flo = 0.f, fhi = 0.f;
   bool force_sequential = false;  // testing: always use the sequential-order distance path
   cudaStream_t own = nullptr, st = nullptr;
   int64_t launches = 0;
@@ -154,16 +156,16 @@ int sb_index_create(const float* features, const int32_t* attrs, int64_t n, int3
   if (e == cudaSuccess) e = cudaMemsetAsync(x->flags.p, 0, adj, x->st);
   if (e == cudaSuccess) e = x->small.ensure(64);
   if (e == cudaSuccess) {
-    unsigned* flags2 = x->small.as<unsigned>() + 14;
-    int r = sb::launch_feature_scan(x->F.as<float>(), (int64_t)n * m, flags2, flags2 + 1, x->st);
+    unsigned* f3 = x->small.as<unsigned>() + 12;
+    int r = sb::launch_feature_scan(x->F.as<float>(), (int64_t)n * m, f3, x->st);
     if (r) e = (cudaError_t)r;
-    unsigned h[2] = {1, 0};
-    if (e == cudaSuccess) e = cudaMemcpyAsync(h, flags2, sizeof(h), cudaMemcpyDeviceToHost, x->st);
+    unsigned h[3] = {1, 0, 0};
+    if (e == cudaSuccess) e = cudaMemcpyAsync(h, f3, sizeof(h), cudaMemcpyDeviceToHost, x->st);
     if (e == cudaSuccess) e = cudaStreamSynchronize(x->st);
-    float fmax = 0.f;
-    memcpy(&fmax, &h[1], sizeof(float));
-    x->int_exact = (h[0] == 0) && (m % 4 == 0);
-    x->fmax = (double)fmax;
+    x->flo = sb::feature_key_to_float(h[1]);
+    x->fhi = sb::feature_key_to_float(h[2]);
+    x->int_exact = h[0] == 0;
+    x->fmax = std::max(std::fabs((double)x->flo), std::fabs((double)x->fhi));
   }
   if (e != cudaSuccess) { delete x; return cuda_fail(e, "upload(index)"); }
   *out = x;
@@ -833,14 +835,12 @@ static int route_dev(sb_index* idx, const double* qf, const double* qa, const do
   a.out_dists = out_dists; a.stats = out_stats;
   a.Kpad = next_pow2(k);
   a.Cpad = next_pow2(idx->g);
-  // lanes per row: the fewest that keep a whole row in flight with <= 8 float4 per lane
-  a.lpr = 0;
-  if (idx->m % 4 == 0 && !idx->force_sequential) {
-    int nq = idx->m / 4, lpr = 1;
-    while (lpr < 32 && (nq + lpr - 1) / lpr > 8) lpr <<= 1;
-    if (const char* e = getenv("SB_ROUTE_LPR")) lpr = std::max(1, std::min(32, atoi(e)));
-    a.lpr = lpr;
-  }
+  // fp32-exact path for integer data (per query the kernel checks the query and the range)
+  a.f32_ok = (idx->int_exact && idx->m % 4 == 0 && !idx->force_sequential) ? 1 : 0;
+  a.flo = idx->flo;
+  a.fhi = idx->fhi;
+  a.lpr = std::min(32, next_pow2(std::max(1, idx->m / 4)));
+  if (const char* e = getenv("SB_ROUTE_LPR")) a.lpr = std::max(1, std::min(32, atoi(e)));
   size_t per_warp = sb::route_smem_per_warp(a);
   int wpc_max = 8;
   if (const char* e = getenv("SB_ROUTE_WPC")) wpc_max = std::max(1, std::min(8, atoi(e)));

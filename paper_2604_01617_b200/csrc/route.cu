@@ -12,12 +12,17 @@
 //   into R.  Sequential bounded insertion into a strictly ordered list equals top-K of the
 //   union (evicted entries can never return), so ids, distances and all four SearchStats
 //   counters equal the reference's.
-// * Memory round trips per expansion are the bound (each query is a serial walk), so each
-//   step issues everything it can at once: the neighbour count and the whole id row load
-//   together; all visited test-and-sets go out together; a few lanes share each unvisited
-//   row so that the whole row is in flight at once (eval_rows).
-// * Distances: fp64, ascending dimension order, explicitly rounded operations, the running
-//   sum handed lane to lane — bit-identical to _query_dist (_kernels.py:26-35) for any data.
+// * Entries and expansions share one candidate buffer and one evaluation site, so the whole
+//   walk is a single inlined loop (no call-frame spills).
+// * Distances, two exact paths:
+//     fp64 path (any data): one row per lane, fp64, ascending dimension order, explicitly
+//       rounded operations — bit-identical to _query_dist (_kernels.py:26-35).
+//     fp32 path (integer data): when features and query are integers and
+//       max|x - q|^2 * m < 2^24, every partial sum of squares is an integer below 2^24, so
+//       fp32 arithmetic in any order is exact and equals the reference's fp64 sum; lanes then
+//       split each row (coalesced 128-bit loads, 8 rows in flight) and reduce with shuffles.
+//     The attribute term and the final sqrt(s_v) * (1 + s_a * inv_alpha) are fp64 as in the
+//     reference in both paths.
 // * Visited set: exact, one bitset of ceil(n/32) words per warp slot in HBM, set with
 //   atomicOr (test-and-set); cleared after each query from a per-slot log of visited ids
 //   (a full clear when the log overflows).
@@ -33,19 +38,7 @@ namespace sb {
 constexpr uint32_t kChkR = 0x80000000u;   // phase-2 checked
 constexpr uint32_t kChkP = 0x40000000u;   // phase-1 (pioneer) checked
 constexpr uint32_t kIdMask = 0x3FFFFFFFu;
-
-// ---- fallback when rows are not 16-byte aligned (m % 4 != 0): lane-owned global reads ---
-__device__ __noinline__ double query_dist_global(const RouteArgs& a, int64_t v, const double* qs,
-                                                 const double* qas, const double* qms) {
-  const float* x = a.F + v * (int64_t)a.m;
-  double s = 0.0;
-  for (int t = 0; t < a.m; ++t) s = sq_step(s, __ldg(x + t), qs[t]);
-  const int32_t* av = a.A + v * (int64_t)a.l;
-  double sa = 0.0;
-  for (int u = 0; u < a.l; ++u)
-    sa = dadd(sa, dmul(qms[u], fabs(dsub((double)__ldg(av + u), qas[u]))));
-  return auto_finish(s, sa, a.inv_alpha);
-}
+constexpr int kRows = 8;                   // rows per lane group in flight (fp32 path)
 
 struct WarpSmem {
   double* rd;     // Kpad
@@ -53,20 +46,23 @@ struct WarpSmem {
   double* qs;     // m
   double* qas;    // l
   double* qms;    // l
+  float* qs32;    // m (fp32 copy of the query, integer path)
   uint32_t* rid;  // Kpad
   uint32_t* cid;  // Cpad
   int* cpos;      // Cpad
 };
 
 SB_HD size_t route_warp_smem_bytes_full(int Kpad, int Cpad, int m, int l) {
-  size_t b = (size_t)Kpad * 8 + (size_t)Cpad * 8 + (size_t)m * 8 + (size_t)l * 16;
+  size_t b = (size_t)((m + 3) & ~3) * 4;  // fp32 query first: 16-byte aligned float4 reads
+  b += (size_t)Kpad * 8 + (size_t)Cpad * 8 + (size_t)m * 8 + (size_t)l * 16;
   b += (size_t)Kpad * 4 + (size_t)Cpad * 8;
   return (b + 15) & ~(size_t)15;
 }
 
 SB_DEV WarpSmem carve(char* base, const RouteArgs& a) {
   WarpSmem w;
-  double* dp = reinterpret_cast<double*>(base);
+  w.qs32 = reinterpret_cast<float*>(base);
+  double* dp = reinterpret_cast<double*>(base + (size_t)((a.m + 3) & ~3) * 4);
   w.rd = dp; dp += a.Kpad;
   w.cd = dp; dp += a.Cpad;
   w.qs = dp; dp += a.m;
@@ -79,71 +75,90 @@ SB_DEV WarpSmem carve(char* base, const RouteArgs& a) {
   return w;
 }
 
-// Exact distances of rows ids[0..c) -> out[0..c).  `lpr` lanes share a row: lane q of the
-// group loads float4s [q*per, (q+1)*per) of the row up front (so a 128-d row arrives in one
-// memory round trip), then the groups' lanes take turns extending the fp64 sum in ascending
-// dimension order, handing the running sum on with a shuffle — the sequential order of
-// _query_dist (_kernels.py:26-35), bit for bit.
-constexpr int kVec = 8;  // float4s a lane keeps in flight
-SB_DEV void eval_rows(const RouteArgs& a, WarpSmem& w, const uint32_t* ids, double* out, int c) {
+// attribute term + final fp64 AUTO combination, exactly _query_dist's tail (_kernels.py:32-35)
+SB_DEV double finish_row(const RouteArgs& a, const WarpSmem& w, uint32_t v, double s_v) {
+  const int32_t* av = a.A + (int64_t)v * a.l;
+  double sa = 0.0;
+  for (int u = 0; u < a.l; ++u)
+    sa = dadd(sa, dmul(w.qms[u], fabs(dsub((double)__ldg(av + u), w.qas[u]))));
+  return auto_finish(s_v, sa, a.inv_alpha);
+}
+
+// Exact distances of rows cid[0..c) -> cd[0..c).
+SB_DEV void eval_rows(const RouteArgs& a, WarpSmem& w, int c, bool f32) {
   const int lane = lane_id();
-  if (a.lpr == 0) {
-    for (int j = lane; j < c; j += 32) out[j] = query_dist_global(a, ids[j], w.qs, w.qas, w.qms);
-    __syncwarp();
-    return;
-  }
-  const int lpr = a.lpr;
-  const int q = lane & (lpr - 1);
-  const int gbase = lane & ~(lpr - 1);
-  const int rows_pp = 32 / lpr;
-  const int nq = a.m >> 2;
-  const int per = (nq + lpr - 1) / lpr;
-  const int f0 = q * per;
-  const int f1 = f0 + per < nq ? f0 + per : nq;
-  const float4* F4 = reinterpret_cast<const float4*>(a.F);
-  for (int base = 0; base < c; base += rows_pp) {
-    const int r = base + lane / lpr;
-    const bool valid = r < c;
-    const float4* row = F4 + (int64_t)(valid ? ids[r] : 0) * nq;
-    float4 x[kVec];
+  if (f32) {
+    const int lpr = a.lpr;
+    const int rpp = 32 / lpr;
+    const int sub = lane & (lpr - 1);
+    const int grp = lane / lpr;
+    const int nq = a.m >> 2;
+    const float4* F4 = reinterpret_cast<const float4*>(a.F);
+    for (int base = 0; base < c; base += rpp * kRows) {
+      float acc[kRows];
+      uint32_t id[kRows];
 #pragma unroll
-    for (int k = 0; k < kVec; ++k)
-      if (valid && f0 + k < f1) x[k] = __ldg(row + f0 + k);
-    double s = 0.0;
-    for (int step = 0; step < lpr; ++step) {
-      if (q == step && valid) {
-#pragma unroll
-        for (int k = 0; k < kVec; ++k)
-          if (f0 + k < f1) {
-            const double* qv = w.qs + 4 * (f0 + k);
-            s = sq_step(s, x[k].x, qv[0]);
-            s = sq_step(s, x[k].y, qv[1]);
-            s = sq_step(s, x[k].z, qv[2]);
-            s = sq_step(s, x[k].w, qv[3]);
-          }
-        for (int f = f0 + kVec; f < f1; f += kVec) {
-#pragma unroll
-          for (int k = 0; k < kVec; ++k)
-            if (f + k < f1) x[k] = __ldg(row + f + k);
-#pragma unroll
-          for (int k = 0; k < kVec; ++k)
-            if (f + k < f1) {
-              const double* qv = w.qs + 4 * (f + k);
-              s = sq_step(s, x[k].x, qv[0]);
-              s = sq_step(s, x[k].y, qv[1]);
-              s = sq_step(s, x[k].z, qv[2]);
-              s = sq_step(s, x[k].w, qv[3]);
-            }
-        }
+      for (int g = 0; g < kRows; ++g) {
+        int r = base + grp + rpp * g;
+        id[g] = r < c ? w.cid[r] : 0xFFFFFFFFu;
+        acc[g] = 0.f;
       }
-      if (lpr > 1) s = __shfl_sync(0xffffffffu, s, gbase | step);
+      for (int k = sub; k < nq; k += lpr) {
+        float4 x[kRows];
+#pragma unroll
+        for (int g = 0; g < kRows; ++g)
+          if (id[g] != 0xFFFFFFFFu) x[g] = __ldg(F4 + (int64_t)id[g] * nq + k);
+        const float4 qv = reinterpret_cast<const float4*>(w.qs32)[k];
+#pragma unroll
+        for (int g = 0; g < kRows; ++g)
+          if (id[g] != 0xFFFFFFFFu) {
+            float d0 = x[g].x - qv.x, d1 = x[g].y - qv.y, d2 = x[g].z - qv.z, d3 = x[g].w - qv.w;
+            acc[g] = fmaf(d0, d0, acc[g]);
+            acc[g] = fmaf(d1, d1, acc[g]);
+            acc[g] = fmaf(d2, d2, acc[g]);
+            acc[g] = fmaf(d3, d3, acc[g]);
+          }
+      }
+#pragma unroll
+      for (int g = 0; g < kRows; ++g)
+        for (int o = lpr >> 1; o > 0; o >>= 1) acc[g] += __shfl_xor_sync(0xffffffffu, acc[g], o);
+      if (sub == 0) {
+#pragma unroll
+        for (int g = 0; g < kRows; ++g)
+          if (id[g] != 0xFFFFFFFFu) w.cd[base + grp + rpp * g] = finish_row(a, w, id[g], (double)acc[g]);
+      }
     }
-    if (q == 0 && valid) {
-      const int32_t* av = a.A + (int64_t)ids[r] * a.l;
-      double sa = 0.0;
-      for (int u = 0; u < a.l; ++u)
-        sa = dadd(sa, dmul(w.qms[u], fabs(dsub((double)__ldg(av + u), w.qas[u]))));
-      out[r] = auto_finish(s, sa, a.inv_alpha);
+  } else if ((a.m & 3) == 0) {
+    const int nq = a.m >> 2;
+    for (int j = lane; j < c; j += 32) {
+      const uint32_t v = w.cid[j];
+      const float4* vx = reinterpret_cast<const float4*>(a.F) + (int64_t)v * nq;
+      double s = 0.0;
+      for (int qq = 0; qq < nq; qq += 8) {
+        float4 r[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+          if (qq + u < nq) r[u] = __ldg(vx + qq + u);
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+          if (qq + u < nq) {
+            const double* qv = w.qs + 4 * (qq + u);
+            s = sq_step(s, r[u].x, qv[0]);
+            s = sq_step(s, r[u].y, qv[1]);
+            s = sq_step(s, r[u].z, qv[2]);
+            s = sq_step(s, r[u].w, qv[3]);
+          }
+      }
+      w.cd[j] = finish_row(a, w, v, s);
+    }
+  } else {
+    for (int j = lane; j < c; j += 32) {
+      const uint32_t v = w.cid[j];
+      const float* x = a.F + (int64_t)v * a.m;
+      double s = 0.0;
+#pragma unroll 4
+      for (int t = 0; t < a.m; ++t) s = sq_step(s, __ldg(x + t), w.qs[t]);
+      w.cd[j] = finish_row(a, w, v, s);
     }
   }
   __syncwarp();
@@ -166,73 +181,39 @@ SB_DEV int first_unchecked(const uint32_t* rid, int lb, int hi, uint32_t bit, in
   return -1;
 }
 
-struct Counters {
-  int64_t evals, p1_evals, p1_exp, hops, scanned;
-};
-
 // warm L2 with the neighbour row of a node we will probably expand next
 SB_DEV void prefetch_row(const RouteArgs& a, uint32_t node) {
   const int lane = lane_id();
   const char* p = reinterpret_cast<const char*>(a.nbr_ids + (int64_t)node * a.g);
-  const int bytes = a.g * 4;
-  if (lane * 128 < bytes) asm volatile("prefetch.global.L2 [%0];" ::"l"(p + lane * 128));
+  if (lane * 128 < a.g * 4) asm volatile("prefetch.global.L2 [%0];" ::"l"(p + lane * 128));
 }
 
-// Expand `node`: read its count and id row together, test-and-set the visited bits of the
-// first cnt neighbours (cnt = ceil(deg/2) in phase 1), evaluate the unvisited ones, merge
-// into R.  Returns the lowest position that received an entry (or K).
-__device__ __noinline__ int expand(const RouteArgs& a, WarpSmem& w, uint32_t node, bool half,
-                                   uint32_t* vis, uint32_t* vlog, int& logn, Counters& ct) {
-  const int lane = lane_id();
-  const int32_t* nb = a.nbr_ids + (int64_t)node * a.g;
-  const int deg = __ldg(a.nbr_counts + node);
-  int c = 0;
-  for (int base = 0; base < a.g; base += 128) {
-    // up to 4 ids per lane per pass, loaded before the count is known
-    uint32_t v[4];
-#pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      int t = base + lane + 32 * k;
-      v[k] = t < a.g ? (uint32_t)__ldg(nb + t) : 0u;
-    }
-    const int cnt = half ? (deg + 1) >> 1 : deg;
-    if (base >= cnt) break;
-    bool fresh[4];
-#pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      int t = base + lane + 32 * k;
-      fresh[k] = false;
-      if (t < cnt) {
-        uint32_t bit = 1u << (v[k] & 31);
-        uint32_t old = atomicOr(vis + (v[k] >> 5), bit);
-        fresh[k] = !(old & bit);
-      }
-    }
-#pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      unsigned bal = __ballot_sync(0xffffffffu, fresh[k]);
-      if (fresh[k]) {
-        int pos = c + __popc(bal & ((1u << lane) - 1u));
-        w.cid[pos] = v[k];
-        int lp = logn + pos;
-        if (lp < a.logcap) vlog[lp] = v[k];
-      }
-      c += __popc(bal);
-    }
-  }
-  const int cnt = half ? (deg + 1) >> 1 : deg;
-  ct.scanned += cnt;
-  logn += c;
-  ct.evals += c;
-  if (half) ct.p1_evals += c;
-  __syncwarp();
-  if (c == 0) return a.K;
-  eval_rows(a, w, w.cid, w.cd, c);
-  return warp_merge_topk(w.rd, w.rid, a.K, w.cd, w.cid, w.cpos, c, kIdMask);
+// float ordering key usable with integer atomics (monotone in the float value)
+SB_HD uint32_t fkey(float f) {
+#ifdef __CUDA_ARCH__
+  uint32_t b = __float_as_uint(f);
+#else
+  uint32_t b;
+  memcpy(&b, &f, 4);
+#endif
+  return (b & 0x80000000u) ? ~b : (b | 0x80000000u);
+}
+SB_HD float fkey_inv(uint32_t k) {
+  uint32_t b = (k & 0x80000000u) ? (k & 0x7FFFFFFFu) : ~k;
+#ifdef __CUDA_ARCH__
+  return __uint_as_float(b);
+#else
+  float f;
+  memcpy(&f, &b, 4);
+  return f;
+#endif
 }
 
-// 256 threads x 4 CTAs per SM: <= 64 registers per thread, 32 warps resident
-__global__ void __launch_bounds__(256, 4) route_kernel(RouteArgs a) {
+// 256 threads x ROUTE_MIN_CTAS CTAs per SM
+#ifndef ROUTE_MIN_CTAS
+#define ROUTE_MIN_CTAS 3
+#endif
+__global__ void __launch_bounds__(256, ROUTE_MIN_CTAS) route_kernel(RouteArgs a) {
   extern __shared__ __align__(16) char smem_raw[];
   const int lane = lane_id();
   const int wid = warp_id();
@@ -243,6 +224,7 @@ __global__ void __launch_bounds__(256, 4) route_kernel(RouteArgs a) {
   uint32_t* vis = a.visited + slot * a.vwords;
   uint32_t* vlog = a.vlog + slot * (int64_t)a.logcap;
   const int K = a.K;
+  const int Cap = a.Cpad;
 
   for (;;) {
     int qi = 0;
@@ -250,69 +232,137 @@ __global__ void __launch_bounds__(256, 4) route_kernel(RouteArgs a) {
     qi = __shfl_sync(0xffffffffu, qi, 0);
     if (qi >= a.q) break;
 
-    for (int t = lane; t < a.m; t += 32) w.qs[t] = a.qf[(int64_t)qi * a.m + t];
+    // query -> shared memory; choose the distance path
+    bool integral = true;
+    float qlo = 3.4e38f, qhi = -3.4e38f;
+    for (int t = lane; t < a.m; t += 32) {
+      double v = a.qf[(int64_t)qi * a.m + t];
+      w.qs[t] = v;
+      w.qs32[t] = (float)v;
+      integral = integral && v == rint(v) && fabs(v) < 16777216.0;
+      qlo = fminf(qlo, (float)v);
+      qhi = fmaxf(qhi, (float)v);
+    }
     for (int t = lane; t < a.l; t += 32) {
       w.qas[t] = a.qa[(int64_t)qi * a.l + t];
       w.qms[t] = a.qm ? a.qm[(int64_t)qi * a.l + t] : 1.0;
     }
+    for (int o = 16; o > 0; o >>= 1) {
+      qlo = fminf(qlo, __shfl_xor_sync(0xffffffffu, qlo, o));
+      qhi = fmaxf(qhi, __shfl_xor_sync(0xffffffffu, qhi, o));
+    }
+    integral = __all_sync(0xffffffffu, integral);
+    bool f32 = false;
+    if (a.f32_ok && integral) {
+      double dmax = fmax((double)a.fhi - (double)qlo, (double)qhi - (double)a.flo);
+      f32 = dmax * dmax * (double)a.m < 16777216.0;  // 2^24
+    }
     __syncwarp();
 
-    Counters ct = {0, 0, 0, 0, 0};
+    int64_t evals = 0, p1_evals = 0, p1_exp = 0, hops = 0, scanned = 0;
     int logn = 0;
-    // entries: mark visited, evaluate, sort (_kernels.py:535-551)
+    // walk state: stage 0 = evaluating entries, 1 = phase 1, 2 = phase 2
+    int stage = 0;
+    int ent_pos = 0;
+    int lb = 0;
     const int64_t* ent = a.entries + (int64_t)qi * K;
-    for (int t = lane; t < K; t += 32) {
-      uint32_t v = (uint32_t)ent[t];
-      atomicOr(vis + (v >> 5), 1u << (v & 31));
-      if (t < a.logcap) vlog[t] = v;
-      w.rid[t] = v;
-    }
-    __syncwarp();
-    eval_rows(a, w, w.rid, w.rd, K);
-    for (int t = K + lane; t < a.Kpad; t += 32) {
-      w.rd[t] = __longlong_as_double(0x7FF0000000000000ll);
-      w.rid[t] = 0xFFFFFFFFu;
-    }
-    logn = K;
-    ct.evals = K;
-    __syncwarp();
-    if (a.Kpad > 1) warp_bitonic_did(w.rd, w.rid, a.Kpad);
-
-    // phase 1: pioneer walk over R[:P], expanding ceil(deg/2) neighbours (_kernels.py:556-585)
-    if (a.use_coarse) {
-      int lb = 0;
-      for (;;) {
+    for (;;) {
+      int c = 0;
+      bool half = false;
+      if (stage == 0) {
+        // next chunk of entries: mark visited, evaluate (_kernels.py:535-540)
+        c = K - ent_pos < Cap ? K - ent_pos : Cap;
+        for (int t = lane; t < c; t += 32) {
+          uint32_t v = (uint32_t)ent[ent_pos + t];
+          atomicOr(vis + (v >> 5), 1u << (v & 31));
+          if (ent_pos + t < a.logcap) vlog[ent_pos + t] = v;
+          w.cid[t] = v;
+        }
+      } else {
+        const bool p1 = stage == 1;
+        const int hi = p1 ? a.P : K;
+        const uint32_t bit = p1 ? kChkP : kChkR;
         int nxt;
-        int sel = first_unchecked(w.rid, lb, a.P, kChkP, &nxt);
-        if (sel < 0) break;
-        uint32_t node = w.rid[sel] & kIdMask;
+        int sel = first_unchecked(w.rid, lb, hi, bit, &nxt);
+        if (sel < 0) {
+          if (!p1) break;
+          stage = 2;  // phase 2 starts with all checked flags cleared (_kernels.py:587-588)
+          lb = 0;
+          for (int t = lane; t < K; t += 32) w.rid[t] &= ~kChkR;
+          __syncwarp();
+          continue;
+        }
+        const uint32_t node = w.rid[sel] & kIdMask;
         if (nxt >= 0) prefetch_row(a, w.rid[nxt] & kIdMask);
         __syncwarp();
-        if (lane == 0) w.rid[sel] |= kChkP;
+        if (lane == 0) w.rid[sel] |= bit;
         __syncwarp();
-        ct.p1_exp += 1;
-        int ins = expand(a, w, node, true, vis, vlog, logn, ct);
+        if (p1) ++p1_exp; else ++hops;
         lb = sel + 1;
-        if (ins < lb) lb = ins;
+        half = p1;
+        // expand: count and id row load together; visited test-and-set of the first cnt
+        const int32_t* nb = a.nbr_ids + (int64_t)node * a.g;
+        const int deg = __ldg(a.nbr_counts + node);
+        for (int base = 0; base < a.g; base += 128) {
+          uint32_t v[4];
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {
+            int t = base + lane + 32 * k;
+            v[k] = t < a.g ? (uint32_t)__ldg(nb + t) : 0u;
+          }
+          const int cnt = half ? (deg + 1) >> 1 : deg;
+          if (base >= cnt) break;
+          bool fresh[4];
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {
+            int t = base + lane + 32 * k;
+            fresh[k] = false;
+            if (t < cnt) {
+              uint32_t b = 1u << (v[k] & 31);
+              uint32_t old = atomicOr(vis + (v[k] >> 5), b);
+              fresh[k] = !(old & b);
+            }
+          }
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {
+            unsigned bal = __ballot_sync(0xffffffffu, fresh[k]);
+            if (fresh[k]) {
+              int pos = c + __popc(bal & ((1u << lane) - 1u));
+              w.cid[pos] = v[k];
+              int lp = logn + pos;
+              if (lp < a.logcap) vlog[lp] = v[k];
+            }
+            c += __popc(bal);
+          }
+        }
+        scanned += half ? (deg + 1) >> 1 : deg;
+        logn += c;
+        evals += c;
+        if (half) p1_evals += c;
       }
-    }
-    // phase 2: clear checked flags, greedy walk over R (_kernels.py:587-609)
-    for (int t = lane; t < K; t += 32) w.rid[t] &= ~kChkR;
-    __syncwarp();
-    {
-      int lb = 0;
-      for (;;) {
-        int nxt;
-        int sel = first_unchecked(w.rid, lb, K, kChkR, &nxt);
-        if (sel < 0) break;
-        uint32_t node = w.rid[sel] & kIdMask;
-        if (nxt >= 0) prefetch_row(a, w.rid[nxt] & kIdMask);
+      __syncwarp();
+      if (c > 0) eval_rows(a, w, c, f32);
+      if (stage == 0) {
+        for (int t = lane; t < c; t += 32) {
+          w.rd[ent_pos + t] = w.cd[t];
+          w.rid[ent_pos + t] = w.cid[t];
+        }
+        ent_pos += c;
+        if (ent_pos == K) {
+          logn = K;
+          evals = K;
+          for (int t = K + lane; t < a.Kpad; t += 32) {
+            w.rd[t] = __longlong_as_double(0x7FF0000000000000ll);
+            w.rid[t] = 0xFFFFFFFFu;
+          }
+          __syncwarp();
+          if (a.Kpad > 1) warp_bitonic_did(w.rd, w.rid, a.Kpad);
+          stage = a.use_coarse ? 1 : 2;
+          lb = 0;
+        }
         __syncwarp();
-        if (lane == 0) w.rid[sel] |= kChkR;
-        __syncwarp();
-        ct.hops += 1;
-        int ins = expand(a, w, node, false, vis, vlog, logn, ct);
-        lb = sel + 1;
+      } else if (c > 0) {
+        int ins = warp_merge_topk(w.rd, w.rid, K, w.cd, w.cid, w.cpos, c, kIdMask);
         if (ins < lb) lb = ins;
       }
     }
@@ -323,11 +373,11 @@ __global__ void __launch_bounds__(256, 4) route_kernel(RouteArgs a) {
     }
     if (a.stats && lane == 0) {
       int64_t* st = a.stats + (int64_t)qi * 5;
-      st[0] = ct.evals;
-      st[1] = ct.p1_evals;
-      st[2] = ct.p1_exp;
-      st[3] = ct.hops;
-      st[4] = ct.scanned;
+      st[0] = evals;
+      st[1] = p1_evals;
+      st[2] = p1_exp;
+      st[3] = hops;
+      st[4] = scanned;
     }
     // clear the visited bits this query set
     if (logn <= a.logcap) {
@@ -377,30 +427,37 @@ int route_occupancy(int warps_per_cta, size_t smem, int* ctas_per_sm) {
                                                             warps_per_cta * 32, smem);
 }
 
-// index property: are all features integral, and max |x| (used by the exhaustive top-k
-// filter to pick an exact low-precision path)
-__global__ void feature_scan_kernel(const float* F, int64_t count, unsigned* nonint,
-                                    unsigned* maxbits) {
+// index property: are all features integral, and their range (monotone keys in out[1..2])
+__global__ void feature_scan_kernel(const float* F, int64_t count, unsigned* out) {
   int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   bool bad = false;
-  float mx = 0.f;
+  float lo = 3.4e38f, hi = -3.4e38f;
   for (; i < count; i += stride) {
     float v = F[i];
     bad = bad || v != rintf(v) || !isfinite(v);
-    mx = fmaxf(mx, fabsf(v));
+    lo = fminf(lo, v);
+    hi = fmaxf(hi, v);
   }
-  if (__any_sync(0xffffffffu, bad) && lane_id() == 0) atomicOr(nonint, 1u);
-  for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-  if (lane_id() == 0) atomicMax(maxbits, __float_as_uint(mx));
+  if (__any_sync(0xffffffffu, bad) && lane_id() == 0) atomicOr(out, 1u);
+  for (int o = 16; o > 0; o >>= 1) {
+    lo = fminf(lo, __shfl_xor_sync(0xffffffffu, lo, o));
+    hi = fmaxf(hi, __shfl_xor_sync(0xffffffffu, hi, o));
+  }
+  if (lane_id() == 0) {
+    atomicMin(out + 1, fkey(lo));
+    atomicMax(out + 2, fkey(hi));
+  }
 }
 
-int launch_feature_scan(const float* F, int64_t count, unsigned* nonint, unsigned* maxbits,
-                        cudaStream_t st) {
-  cudaMemsetAsync(nonint, 0, sizeof(unsigned), st);
-  cudaMemsetAsync(maxbits, 0, sizeof(unsigned), st);
-  feature_scan_kernel<<<1184, 256, 0, st>>>(F, count, nonint, maxbits);
+int launch_feature_scan(const float* F, int64_t count, unsigned* out3, cudaStream_t st) {
+  unsigned init[3] = {0u, 0xFFFFFFFFu, 0u};
+  cudaMemcpyAsync(out3, init, sizeof(init), cudaMemcpyHostToDevice, st);
+  cudaStreamSynchronize(st);
+  feature_scan_kernel<<<1184, 256, 0, st>>>(F, count, out3);
   return (int)cudaGetLastError();
 }
+
+float feature_key_to_float(unsigned k) { return fkey_inv(k); }
 
 }  // namespace sb
