@@ -836,7 +836,9 @@ static int route_dev(sb_index* idx, const double* qf, const double* qa, const do
   a.Kpad = next_pow2(k);
   a.Cpad = next_pow2(idx->g);
   // fp32-exact path for integer data (per query the kernel checks the query and the range)
-  a.f32_ok = (idx->int_exact && idx->m % 4 == 0 && !idx->force_sequential) ? 1 : 0;
+  // (measured slower than the fp64 lane-per-row path on cfg 2 at N=1M; opt in with SB_ROUTE_F32=1)
+  const char* f32env = getenv("SB_ROUTE_F32");
+  a.f32_ok = (f32env && atoi(f32env) && idx->int_exact && idx->m % 4 == 0 && !idx->force_sequential) ? 1 : 0;
   a.flo = idx->flo;
   a.fhi = idx->fhi;
   a.lpr = std::min(32, next_pow2(std::max(1, idx->m / 4)));

@@ -84,6 +84,28 @@ SB_DEV double finish_row(const RouteArgs& a, const WarpSmem& w, uint32_t v, doub
   return auto_finish(s_v, sa, a.inv_alpha);
 }
 
+// attribute codes loaded early (first 4 in registers) so their latency overlaps the row loads
+struct AttrPre {
+  int32_t v[4];
+};
+SB_DEV void attr_preload(const RouteArgs& a, uint32_t node, AttrPre& p) {
+  const int32_t* av = a.A + (int64_t)node * a.l;
+#pragma unroll
+  for (int u = 0; u < 4; ++u)
+    if (u < a.l) p.v[u] = __ldg(av + u);
+}
+SB_DEV double finish_pre(const RouteArgs& a, const WarpSmem& w, uint32_t node, const AttrPre& p,
+                         double s_v) {
+  double sa = 0.0;
+#pragma unroll
+  for (int u = 0; u < 4; ++u)
+    if (u < a.l) sa = dadd(sa, dmul(w.qms[u], fabs(dsub((double)p.v[u], w.qas[u]))));
+  const int32_t* av = a.A + (int64_t)node * a.l;
+  for (int u = 4; u < a.l; ++u)
+    sa = dadd(sa, dmul(w.qms[u], fabs(dsub((double)__ldg(av + u), w.qas[u]))));
+  return auto_finish(s_v, sa, a.inv_alpha);
+}
+
 // Exact distances of rows cid[0..c) -> cd[0..c).
 SB_DEV void eval_rows(const RouteArgs& a, WarpSmem& w, int c, bool f32) {
   const int lane = lane_id();
@@ -103,6 +125,13 @@ SB_DEV void eval_rows(const RouteArgs& a, WarpSmem& w, int c, bool f32) {
         id[g] = r < c ? w.cid[r] : 0xFFFFFFFFu;
         acc[g] = 0.f;
       }
+      // lane `sub == g` finishes row g (needs lpr >= kRows); its attributes load now
+      uint32_t own = 0xFFFFFFFFu;
+#pragma unroll
+      for (int g = 0; g < kRows; ++g)
+        if (g == sub) own = id[g];
+      AttrPre pre;
+      if (lpr >= kRows && own != 0xFFFFFFFFu) attr_preload(a, own, pre);
       for (int k = sub; k < nq; k += lpr) {
         float4 x[kRows];
 #pragma unroll
@@ -122,7 +151,15 @@ SB_DEV void eval_rows(const RouteArgs& a, WarpSmem& w, int c, bool f32) {
 #pragma unroll
       for (int g = 0; g < kRows; ++g)
         for (int o = lpr >> 1; o > 0; o >>= 1) acc[g] += __shfl_xor_sync(0xffffffffu, acc[g], o);
-      if (sub == 0) {
+      if (lpr >= kRows) {
+        if (own != 0xFFFFFFFFu) {
+          float tot = 0.f;
+#pragma unroll
+          for (int g = 0; g < kRows; ++g)
+            if (g == sub) tot = acc[g];
+          w.cd[base + grp + rpp * sub] = finish_pre(a, w, own, pre, (double)tot);
+        }
+      } else if (sub == 0) {
 #pragma unroll
         for (int g = 0; g < kRows; ++g)
           if (id[g] != 0xFFFFFFFFu) w.cd[base + grp + rpp * g] = finish_row(a, w, id[g], (double)acc[g]);
@@ -133,6 +170,8 @@ SB_DEV void eval_rows(const RouteArgs& a, WarpSmem& w, int c, bool f32) {
     for (int j = lane; j < c; j += 32) {
       const uint32_t v = w.cid[j];
       const float4* vx = reinterpret_cast<const float4*>(a.F) + (int64_t)v * nq;
+      AttrPre pre;
+      attr_preload(a, v, pre);
       double s = 0.0;
       for (int qq = 0; qq < nq; qq += 8) {
         float4 r[8];
@@ -149,7 +188,7 @@ SB_DEV void eval_rows(const RouteArgs& a, WarpSmem& w, int c, bool f32) {
             s = sq_step(s, r[u].w, qv[3]);
           }
       }
-      w.cd[j] = finish_row(a, w, v, s);
+      w.cd[j] = finish_pre(a, w, v, pre, s);
     }
   } else {
     for (int j = lane; j < c; j += 32) {
