@@ -215,9 +215,14 @@ def test_order_free_mode_is_bit_exact():
     assert dev.info()["int_exact"]
     qf = np.clip(np.rint(rng.normal(128, 40, (48, m))), 0, 255).astype(np.float32)
     qa = rng.integers(1, 6, (48, l)).astype(np.int32)
+    import os
     for k in (5, 64, 257):
         p = sb.SearchParams(k=k, seed=2)
-        fast = sb.search_batch_arrays(graph, qf, qa, p)
+        os.environ["SB_ROUTE_F32"] = "1"   # fp32-exact integer path (opt-in)
+        try:
+            fast = sb.search_batch_arrays(graph, qf, qa, p)
+        finally:
+            del os.environ["SB_ROUTE_F32"]
         dev.set_distance_mode(sequential=True)
         seq = sb.search_batch_arrays(graph, qf, qa, p)
         dev.set_distance_mode(sequential=False)
