@@ -141,8 +141,9 @@ int sb_route_batch_dev(sb_index* idx, const double* qf, const double* qa, const 
 int64_t sb_launch_count(sb_index* idx);
 
 /* *int_exact = 1 when every feature is an integer (|x| <= *fmax_abs); such data admits exact
- * reduced-precision / reordered distance sums. */
-int sb_index_info(sb_index* idx, int32_t* int_exact, double* fmax_abs);
+ * reduced-precision / reordered distance sums.  *last_bf_tc = 1 when the last
+ * sb_bf_topk_queries ran on the tensor cores (tcgen05). */
+int sb_index_info(sb_index* idx, int32_t* int_exact, double* fmax_abs, int32_t* last_bf_tc);
 /* routing row loads: 0 = staged through shared memory with cp.async (default),
  * 1 = each lane reads its row from global memory directly; both bit-exact */
 int sb_set_distance_mode(sb_index* idx, int32_t mode);

@@ -53,7 +53,7 @@ _SIGS = {
     "sb_route_batch_dev": [_vp, _vp, _vp, _vp, _i64, _i32, _i32, _i32, _vp, _u64, _i64, _f64,
                            _vp, _vp, _vp],
     "sb_launch_count": [_vp],
-    "sb_index_info": [_vp, _vp, _vp],
+    "sb_index_info": [_vp, _vp, _vp, _vp],
     "sb_set_distance_mode": [_vp, _i32],
 }
 _RESTYPE = {"sb_last_error": ctypes.c_char_p, "sb_launch_count": ctypes.c_int64}

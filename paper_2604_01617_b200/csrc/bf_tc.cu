@@ -1,0 +1,345 @@
+// bf_tc.cu — exhaustive AUTO top-k on the 5th-generation tensor cores (tcgen05 + TMEM),
+// query mode (oracle_auto_topk, evaluate.py:32-55) for integer-valued data.
+//
+// Exactness: when features and queries are integers with d * max(|x|,|q|)^2 < 2^24, every
+// bf16 operand is exact and every partial dot product in the fp32 TMEM accumulator is an
+// integer below 2^24, so x.q is exact whatever order the tensor core adds in.  Then
+//   S = |x|^2 + |q|^2 - 2 x.q            (int32, exact)
+// equals the reference's fp64 sum of squared differences exactly, and
+//   U = sqrt(S) * (1 + s_a / alpha)       (fp64, as evaluate.py:48-53)
+// is bit-identical to the reference's value.  No re-rank is needed; the split merge
+// (bf_merge_kernel) recomputes the kept candidates in NumPy order, which changes nothing.
+//
+// CTA = 128 queries (one per TMEM lane / epilogue thread) x a node range.  Per tile of 256
+// nodes: the bf16 node rows are copied into shared memory in the canonical K-major
+// no-swizzle core-matrix layout (8 rows x 16 B per core matrix), one elected thread issues
+// d/16 tcgen05.mma (M=128, N=256, K=16, BF16 -> F32) into TMEM and commits to an mbarrier;
+// each thread then reads its query's 256 dot products with tcgen05.ld and keeps a private
+// top-kk list.  A node can enter the list only if sqrt(S) <= T (the factor is >= 1), so the
+// epilogue mostly costs one integer compare per (query, node).
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "common.cuh"
+#include "sb_internal.h"
+
+namespace sb {
+
+constexpr int kTcM = 128;       // queries per CTA (UMMA M)
+constexpr int kTcN = 256;       // nodes per tile (UMMA N)
+constexpr int kTcThreads = 128;
+constexpr int kTcMaxKK = 32;    // per-thread list length limit
+
+// ---- PTX wrappers --------------------------------------------------------------------
+SB_DEV uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+SB_DEV uint64_t umma_desc(uint32_t start, uint32_t lbo, uint32_t sbo) {
+  // K-major, SWIZZLE_NONE canonical layout ((8,n),2):((1,SBO),LBO) in 16-byte units;
+  // bits: start[0,14) lbo[16,30) sbo[32,46) version=1 [46,48) layout=0 [61,64)
+  uint64_t d = 0;
+  d |= (uint64_t)((start >> 4) & 0x3FFF);
+  d |= (uint64_t)((lbo >> 4) & 0x3FFF) << 16;
+  d |= (uint64_t)((sbo >> 4) & 0x3FFF) << 32;
+  d |= (uint64_t)1 << 46;
+  return d;
+}
+
+// BF16 x BF16 -> F32, both K-major, M = 128, N = 256
+constexpr uint32_t kIdesc = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(kTcN >> 3) << 17) |
+                            ((uint32_t)(kTcM >> 4) << 24);
+
+SB_DEV void mma_bf16(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(kIdesc), "r"(accumulate));
+}
+
+SB_DEV void mma_commit(uint32_t bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar)
+               : "memory");
+}
+
+SB_DEV void mbar_init(uint32_t bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count) : "memory");
+}
+
+SB_DEV void mbar_wait(uint32_t bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred P1;\n\t"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+      "@!P1 bra WAIT_%=;\n\t}\n" ::"r"(bar),
+      "r"(parity)
+      : "memory");
+}
+
+SB_DEV void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+SB_DEV void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+SB_DEV void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+
+SB_DEV void tmem_ld16(uint32_t taddr, uint32_t (&r)[16]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 "
+      "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
+        "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+
+SB_DEV void cp_async16(uint32_t dst, const void* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
+}
+SB_DEV void cp_async_wait_all() {
+  asm volatile("cp.async.commit_group;\n\tcp.async.wait_group 0;" ::: "memory");
+}
+
+// byte offset of (row, 16-byte k-chunk) in the core-matrix layout of an R-row tile
+SB_DEV uint32_t cm_off(int row, int kc, int R) {
+  return (uint32_t)(((kc * (R >> 3) + (row >> 3)) << 7) + ((row & 7) << 4));
+}
+
+// ---- prep kernels ----------------------------------------------------------------------
+// bf16 copy of integer features and exact squared norms
+__global__ void tc_prep_nodes_kernel(const float* F, int64_t n, int m, __nv_bfloat16* Fb,
+                                     int32_t* nx) {
+  int64_t v = (int64_t)blockIdx.x * (blockDim.x >> 5) + warp_id();
+  if (v >= n) return;
+  int acc = 0;
+  for (int t = lane_id(); t < m; t += 32) {
+    float x = F[v * m + t];
+    Fb[v * m + t] = __float2bfloat16_rn(x);
+    acc += (int)x * (int)x;
+  }
+  acc = warp_sum(acc);
+  if (lane_id() == 0) nx[v] = acc;
+}
+
+__global__ void tc_prep_queries_kernel(const double* qf, int64_t q, int m, __nv_bfloat16* Qb,
+                                       int32_t* nq) {
+  int64_t i = (int64_t)blockIdx.x * (blockDim.x >> 5) + warp_id();
+  if (i >= q) return;
+  int acc = 0;
+  for (int t = lane_id(); t < m; t += 32) {
+    double x = qf[i * m + t];
+    Qb[i * m + t] = __float2bfloat16_rn((float)x);
+    acc += (int)x * (int)x;
+  }
+  acc = warp_sum(acc);
+  if (lane_id() == 0) nq[i] = acc;
+}
+
+// ---- main kernel -------------------------------------------------------------------------
+struct TcArgs {
+  const __nv_bfloat16* Fb;  // n x m
+  const int32_t* nx;        // n
+  const int32_t* A;         // n x l
+  const __nv_bfloat16* Qb;  // q x m
+  const int32_t* nq;        // q
+  const int64_t* qa;        // q x l
+  const int64_t* qmask;     // q x l or null
+  int64_t n, q;
+  int m, l, kk, splits;
+  double alpha;
+  double* part_d;           // q x splits x kk
+  uint32_t* part_i;
+};
+
+__global__ void __launch_bounds__(kTcThreads, 1) bf_tc_kernel(TcArgs a) {
+  extern __shared__ __align__(1024) char smem[];
+  const int tid = threadIdx.x;
+  const int m = a.m;
+  // shared layout: A tile | B tile | node norms | node attrs | lists | barrier | tmem slot
+  char* p = smem;
+  char* sA = p; p += (size_t)kTcM * m * 2;
+  char* sB = p; p += (size_t)kTcN * m * 2;
+  int32_t* s_nx = reinterpret_cast<int32_t*>(p); p += sizeof(int32_t) * kTcN;
+  int32_t* s_at = reinterpret_cast<int32_t*>(p); p += sizeof(int32_t) * (size_t)kTcN * a.l;
+  double* ld = reinterpret_cast<double*>(p); p += sizeof(double) * (size_t)kTcMaxKK * kTcM;
+  uint32_t* li = reinterpret_cast<uint32_t*>(p); p += sizeof(uint32_t) * (size_t)kTcMaxKK * kTcM;
+  uint64_t* bar = reinterpret_cast<uint64_t*>(p); p += 16;
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(p);
+
+  const int64_t q0 = (int64_t)blockIdx.x * kTcM;
+  const int split = blockIdx.y;
+  const int64_t per = ((a.n + a.splits - 1) / a.splits + kTcN - 1) / kTcN * kTcN;
+  const int64_t v_begin = per * split;
+  const int64_t v_end = v_begin + per < a.n ? v_begin + per : a.n;
+  const int64_t my_q = q0 + tid;
+  const bool qok = my_q < a.q;
+  const double inf = __longlong_as_double(0x7FF0000000000000ll);
+
+  // TMEM: 256 fp32 columns (one accumulator of 128 x 256)
+  if (warp_id() == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tslot)),
+                 "r"(256));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  if (tid == 0) {
+    mbar_init(smem_u32(bar), 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  // A tile: this CTA's queries (zero rows past q)
+  const int kchunks = m / 8;
+  for (int e = tid; e < kTcM * kchunks; e += kTcThreads) {
+    int row = e / kchunks, kc = e % kchunks;
+    uint32_t dst = smem_u32(sA) + cm_off(row, kc, kTcM);
+    if (q0 + row < a.q) {
+      cp_async16(dst, a.Qb + (q0 + row) * m + kc * 8);
+    } else {
+      *reinterpret_cast<uint4*>(sA + cm_off(row, kc, kTcM)) = make_uint4(0, 0, 0, 0);
+    }
+  }
+  for (int i = 0; i < a.kk; ++i) {
+    ld[i * kTcM + tid] = inf;
+    li[i * kTcM + tid] = 0xFFFFFFFFu;
+  }
+  cp_async_wait_all();
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tslot;
+  const int32_t my_nq = qok ? a.nq[my_q] : 0;
+  int64_t qa_row[8];
+  int64_t qm_row[8];
+  for (int u = 0; u < 8; ++u) {
+    qa_row[u] = (qok && u < a.l) ? a.qa[my_q * a.l + u] : 0;
+    qm_row[u] = (qok && u < a.l) ? (a.qmask ? a.qmask[my_q * a.l + u] : 1) : 0;
+  }
+  double thr_s = inf;  // a node can enter only if S <= thr_s (conservative)
+  uint32_t phase = 0;
+
+  for (int64_t vb = v_begin; vb < v_end; vb += kTcN) {
+    // B tile: node rows (zero rows past the range) + norms + attributes
+    for (int e = tid; e < kTcN * kchunks; e += kTcThreads) {
+      int row = e / kchunks, kc = e % kchunks;
+      int64_t v = vb + row;
+      uint32_t off = cm_off(row, kc, kTcN);
+      if (v < v_end) cp_async16(smem_u32(sB) + off, a.Fb + v * m + kc * 8);
+      else *reinterpret_cast<uint4*>(sB + off) = make_uint4(0, 0, 0, 0);
+    }
+    for (int r = tid; r < kTcN; r += kTcThreads) {
+      int64_t v = vb + r;
+      s_nx[r] = v < v_end ? a.nx[v] : 0x7FFFFFFF;
+      for (int u = 0; u < a.l; ++u) s_at[r * a.l + u] = v < v_end ? a.A[v * a.l + u] : 0;
+    }
+    cp_async_wait_all();
+    fence_async_smem();
+    __syncthreads();
+    if (tid == 0) {
+      tc_fence_after();
+      const uint32_t a0 = smem_u32(sA), b0 = smem_u32(sB);
+      for (int s = 0; s < m / 16; ++s) {
+        uint64_t ad = umma_desc(a0 + (uint32_t)s * 2 * (kTcM / 8) * 128, (kTcM / 8) * 128, 128);
+        uint64_t bd = umma_desc(b0 + (uint32_t)s * 2 * (kTcN / 8) * 128, (kTcN / 8) * 128, 128);
+        mma_bf16(tmem, ad, bd, s > 0 ? 1u : 0u);
+      }
+      mma_commit(smem_u32(bar));
+    }
+    __syncwarp();
+    mbar_wait(smem_u32(bar), phase);
+    phase ^= 1u;
+    tc_fence_after();
+    // epilogue: this thread = TMEM lane (32 * warp + lane) = query q0 + tid
+    const uint32_t lane_base = tmem + ((uint32_t)(warp_id() * 32) << 16);
+    for (int c = 0; c < kTcN / 16; ++c) {
+      uint32_t r[16];
+      tmem_ld16(lane_base + (uint32_t)(c * 16), r);
+      if (!qok) continue;
+#pragma unroll
+      for (int j = 0; j < 16; ++j) {
+        const int col = c * 16 + j;
+        const int64_t dot = (int64_t)__uint_as_float(r[j]);
+        const int64_t S = (int64_t)s_nx[col] + my_nq - 2 * dot;
+        if ((double)S > thr_s) continue;
+        const int64_t v = vb + col;
+        if (v >= v_end) continue;
+        int64_t sa = 0;
+        for (int u = 0; u < a.l; ++u) {
+          int64_t ad = (int64_t)s_at[col * a.l + u] - qa_row[u < 8 ? u : 7];
+          ad = ad < 0 ? -ad : ad;
+          sa += ad * qm_row[u < 8 ? u : 7];
+        }
+        const double dist = dmul(sqrt((double)S), dadd(1.0, __ddiv_rn((double)sa, a.alpha)));
+        // insert into this thread's sorted list (d, id) if it beats the tail
+        const uint32_t vid = (uint32_t)v;
+        double wd = ld[(a.kk - 1) * kTcM + tid];
+        uint32_t wi = li[(a.kk - 1) * kTcM + tid];
+        if (!dlt(dist, vid, wd, wi)) continue;
+        int pos = a.kk - 1;
+        while (pos > 0) {
+          double pd = ld[(pos - 1) * kTcM + tid];
+          uint32_t pi = li[(pos - 1) * kTcM + tid];
+          if (!dlt(dist, vid, pd, pi)) break;
+          ld[pos * kTcM + tid] = pd;
+          li[pos * kTcM + tid] = pi;
+          --pos;
+        }
+        ld[pos * kTcM + tid] = dist;
+        li[pos * kTcM + tid] = vid;
+        const double t = ld[(a.kk - 1) * kTcM + tid];
+        thr_s = t * t * (1.0 + 1e-9) + 1.0;
+      }
+    }
+    tc_fence_before();
+    __syncthreads();
+  }
+  // partial lists out
+  if (qok) {
+    size_t o = ((size_t)my_q * a.splits + split) * a.kk;
+    for (int i = 0; i < a.kk; ++i) {
+      a.part_d[o + i] = ld[i * kTcM + tid];
+      a.part_i[o + i] = li[i * kTcM + tid];
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp_id() == 0) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(256));
+  }
+}
+
+size_t bf_tc_smem(int m, int l) {
+  return (size_t)kTcM * m * 2 + (size_t)kTcN * m * 2 + sizeof(int32_t) * kTcN +
+         sizeof(int32_t) * (size_t)kTcN * l + (sizeof(double) + sizeof(uint32_t)) * kTcMaxKK * kTcM +
+         64;
+}
+
+int bf_tc_supported(int m, int l, int kk) {
+  return (m % 16 == 0) && m <= 256 && l <= 8 && kk <= kTcMaxKK && bf_tc_smem(m, l) <= 227 * 1024;
+}
+
+int launch_bf_tc_prep_nodes(const float* F, int64_t n, int m, void* Fb, int32_t* nx,
+                            cudaStream_t st) {
+  tc_prep_nodes_kernel<<<(unsigned)((n + 7) / 8), 256, 0, st>>>(F, n, m, (__nv_bfloat16*)Fb, nx);
+  return (int)cudaGetLastError();
+}
+
+int launch_bf_tc_prep_queries(const double* qf, int64_t q, int m, void* Qb, int32_t* nq,
+                              cudaStream_t st) {
+  tc_prep_queries_kernel<<<(unsigned)((q + 7) / 8), 256, 0, st>>>(qf, q, m, (__nv_bfloat16*)Qb, nq);
+  return (int)cudaGetLastError();
+}
+
+int launch_bf_tc(const void* Fb, const int32_t* nx, const int32_t* A, const void* Qb,
+                 const int32_t* nq, const int64_t* qa, const int64_t* qmask, int64_t n, int64_t q,
+                 int m, int l, int kk, int splits, double alpha, double* part_d, uint32_t* part_i,
+                 cudaStream_t st) {
+  TcArgs a;
+  a.Fb = (const __nv_bfloat16*)Fb; a.nx = nx; a.A = A; a.Qb = (const __nv_bfloat16*)Qb;
+  a.nq = nq; a.qa = qa; a.qmask = qmask; a.n = n; a.q = q; a.m = m; a.l = l; a.kk = kk;
+  a.splits = splits; a.alpha = alpha; a.part_d = part_d; a.part_i = part_i;
+  size_t smem = bf_tc_smem(m, l);
+  cudaError_t e = cudaFuncSetAttribute(bf_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return (int)e;
+  dim3 grid((unsigned)((q + kTcM - 1) / kTcM), (unsigned)splits);
+  bf_tc_kernel<<<grid, kTcThreads, smem, st>>>(a);
+  return (int)cudaGetLastError();
+}
+
+}  // namespace sb

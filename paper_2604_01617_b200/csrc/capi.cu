@@ -75,6 +75,8 @@ struct sb_index {
   double fmax = 0.0;
   float flo = 0.f, fhi = 0.f;
   bool force_sequential = false;  // testing: always use the sequential-order distance path
+  bool have_fb = false;           // bf16 feature copy + norms for the tensor-core top-k
+  bool last_bf_tc = false;        // the last sb_bf_topk_queries ran on tensor cores
   cudaStream_t own = nullptr, st = nullptr;
   int64_t launches = 0;
   // dataset + adjacency
@@ -94,8 +96,11 @@ struct sb_index {
   DBuf rf_n8, rf_nb, rf_n32, rf_n64, rf_o32, rf_o64, rf_ulist, rf_bits, rf_rec, rf_sim;
   // routing / brute force
   DBuf qf, qa, qm, entries, ent_scratch, out_ids, out_dists, stats, visited, vlog, counter;
-  DBuf bf_part_d, bf_part_i, bf_self, bf_qa, bf_qm, bf_out32;
+  DBuf bf_part_d, bf_part_i, bf_self, bf_qa, bf_qm, bf_out32, fb, fb_norm, qb;
   ~sb_index() {
+    fb.release();
+    fb_norm.release();
+    qb.release();
     DBuf* all[] = {&F, &A, &ids, &dists, &flags, &counts, &new_cand, &new_cnt, &old_cand,
                    &old_cnt, &fwd_new, &fwd_old, &rev_cnt, &rev_off, &rev_cur, &rev, &scan_tmp,
                    &thr, &row_cnt, &row_off, &row_cur, &push_tgt, &push_key, &seg, &small,
@@ -191,8 +196,9 @@ int sb_synchronize(sb_index* idx) {
 
 int64_t sb_launch_count(sb_index* idx) { return idx ? idx->launches : 0; }
 
-int sb_index_info(sb_index* idx, int32_t* int_exact, double* fmax_abs) {
+int sb_index_info(sb_index* idx, int32_t* int_exact, double* fmax_abs, int32_t* last_bf_tc) {
   if (!idx) return fail(SB_EARG, "idx is NULL");
+  if (last_bf_tc) *last_bf_tc = idx->last_bf_tc ? 1 : 0;
   if (int_exact) *int_exact = idx->int_exact ? 1 : 0;
   if (fmax_abs) *fmax_abs = idx->fmax;
   return SB_OK;
@@ -785,8 +791,52 @@ int sb_bf_topk_queries(sb_index* idx, const double* qf, const int64_t* qa, const
   a.qf = idx->qf.as<double>(); a.qa = idx->bf_qa.as<int64_t>();
   a.qmask = qmask ? idx->bf_qm.as<int64_t>() : nullptr; a.q = q; a.k = kk; a.alpha = alpha;
   int unc = 0;
-  int r = bf_run(idx, a, k, idx->out_ids.as<int64_t>(), nullptr, idx->out_dists.as<double>(), &unc);
-  if (r) return r;
+  // tensor-core path: integer features and queries, |values| <= 256 (exact in bf16), every
+  // partial dot product below 2^24 (exact in the fp32 accumulator)
+  bool tc = idx->int_exact && idx->fmax <= 256.0 && idx->m <= 255 && !idx->force_sequential &&
+            sb::bf_tc_supported(idx->m, idx->l, kk);
+  if (const char* e = getenv("SB_BF_TC")) tc = tc && atoi(e) != 0;
+  for (int64_t i = 0; tc && i < q * idx->m; ++i) {
+    double v = qf[i];
+    tc = v == std::rint(v) && std::fabs(v) <= 256.0;
+  }
+  if (tc) {
+    const int64_t n = idx->n;
+    if (!idx->have_fb) {
+      CK(idx->fb.ensure(sizeof(uint16_t) * n * idx->m));
+      CK(idx->fb_norm.ensure(sizeof(int32_t) * n));
+      CKL(sb::launch_bf_tc_prep_nodes(idx->F.as<float>(), n, idx->m, idx->fb.p,
+                                      idx->fb_norm.as<int32_t>(), idx->st));
+      idx->have_fb = true;
+      idx->launches += 1;
+    }
+    CK(idx->qb.ensure(sizeof(uint16_t) * q * idx->m + sizeof(int32_t) * q + 64));
+    int32_t* d_nq = reinterpret_cast<int32_t*>(idx->qb.as<char>() + ((sizeof(uint16_t) * q * idx->m + 15) & ~(size_t)15));
+    CKL(sb::launch_bf_tc_prep_queries(idx->qf.as<double>(), q, idx->m, idx->qb.p, d_nq, idx->st));
+    const int groups = (int)((q + 127) / 128);
+    int splits = std::max(1, (2 * idx->sms + groups - 1) / groups);
+    splits = (int)std::min<int64_t>(splits, std::max<int64_t>(1, n / 256));
+    a.splits = splits;
+    CK(idx->bf_part_d.ensure(sizeof(double) * q * splits * kk));
+    CK(idx->bf_part_i.ensure(sizeof(uint32_t) * q * splits * kk));
+    a.part_d = idx->bf_part_d.as<double>();
+    a.part_i = idx->bf_part_i.as<uint32_t>();
+    CK(idx->small.ensure(64));
+    int* d_unc = reinterpret_cast<int*>(idx->small.as<unsigned long long>() + 6);
+    CK(cudaMemsetAsync(d_unc, 0, sizeof(int), idx->st));
+    CKL(sb::launch_bf_tc(idx->fb.p, idx->fb_norm.as<int32_t>(), idx->A.as<int32_t>(), idx->qb.p,
+                         d_nq, a.qa, a.qmask, n, q, idx->m, idx->l, kk, splits, alpha, a.part_d,
+                         a.part_i, idx->st));
+    CKL(sb::launch_bf_merge_k(a, k, idx->out_ids.as<int64_t>(), nullptr, idx->out_dists.as<double>(),
+                              d_unc, idx->st));
+    CK(cudaMemcpyAsync(&unc, d_unc, sizeof(int), cudaMemcpyDeviceToHost, idx->st));
+    idx->launches += 3;
+    idx->last_bf_tc = true;
+  } else {
+    int r = bf_run(idx, a, k, idx->out_ids.as<int64_t>(), nullptr, idx->out_dists.as<double>(), &unc);
+    if (r) return r;
+    idx->last_bf_tc = false;
+  }
   CK(cudaMemcpyAsync(out_ids, idx->out_ids.p, sizeof(int64_t) * q * k, cudaMemcpyDeviceToHost, idx->st));
   if (out_dists) CK(cudaMemcpyAsync(out_dists, idx->out_dists.p, sizeof(double) * q * k, cudaMemcpyDeviceToHost, idx->st));
   CK(cudaStreamSynchronize(idx->st));

@@ -68,6 +68,18 @@ int launch_bf_partial(const BfArgs& a, cudaStream_t st);
 int launch_bf_merge_k(const BfArgs& a, int kout, int64_t* out_ids64, int32_t* out_ids32,
                       double* out_dists, int* uncertain, cudaStream_t st);
 
+// tensor-core query-mode top-k for integer data (bf_tc.cu)
+size_t bf_tc_smem(int m, int l);
+int bf_tc_supported(int m, int l, int kk);
+int launch_bf_tc_prep_nodes(const float* F, int64_t n, int m, void* Fb, int32_t* nx,
+                            cudaStream_t st);
+int launch_bf_tc_prep_queries(const double* qf, int64_t q, int m, void* Qb, int32_t* nq,
+                              cudaStream_t st);
+int launch_bf_tc(const void* Fb, const int32_t* nx, const int32_t* A, const void* Qb,
+                 const int32_t* nq, const int64_t* qa, const int64_t* qmask, int64_t n, int64_t q,
+                 int m, int l, int kk, int splits, double alpha, double* part_d, uint32_t* part_i,
+                 cudaStream_t st);
+
 // ---- HELP build ---------------------------------------------------------------
 struct BuildScratch {
   int32_t* fwd_new;   // n

@@ -74,8 +74,10 @@ class DeviceIndex:
     def info(self) -> dict:
         ie = ctypes.c_int32(0)
         fm = ctypes.c_double(0.0)
-        _lib.call("sb_index_info", self._h, ctypes.addressof(ie), ctypes.addressof(fm))
-        return {"int_exact": bool(ie.value), "fmax_abs": fm.value}
+        tc = ctypes.c_int32(0)
+        _lib.call("sb_index_info", self._h, ctypes.addressof(ie), ctypes.addressof(fm),
+                  ctypes.addressof(tc))
+        return {"int_exact": bool(ie.value), "fmax_abs": fm.value, "last_bf_tc": bool(tc.value)}
 
     def set_distance_mode(self, sequential: bool):
         _lib.call("sb_set_distance_mode", self._h, 1 if sequential else 0)

@@ -244,6 +244,40 @@ def test_order_free_mode_is_bit_exact():
                                 nbr_counts=cnt, frozen=True).device().info()["int_exact"]
 
 
+@pytest.mark.parametrize("n,m,l,q,k", [(5000, 128, 3, 300, 10), (3001, 64, 2, 129, 16),
+                                       (777, 32, 1, 5, 1), (20000, 128, 3, 1000, 10)])
+def test_tensor_core_topk_exact(n, m, l, q, k):
+    """tcgen05 path (integer data): identical ids and fp64 distances to the fp64 SIMT path and
+    to the oracle, including ragged tiles (n % 256, q % 128), masks and duplicate points."""
+    import os
+    rng = np.random.default_rng(n + m)
+    f = np.clip(np.rint(rng.normal(128, 50, (n, m))), 0, 255).astype(np.float32)
+    f[10:20] = f[5]                      # exact duplicates: ties broken by id
+    a = rng.integers(1, 6, (n, l)).astype(np.int32)
+    qf = np.clip(np.rint(rng.normal(128, 50, (q, m))), 0, 255)
+    qf[0] = f[5]
+    qa = rng.integers(1, 6, (q, l))
+    masks = rng.integers(0, 2, (q, l))
+    cfg = sb.MetricConfig.manual(0.91, l)
+    d = DeviceIndex(f, a, 2)
+    for mk in (None, masks):
+        ids_tc, dd_tc = d.bf_topk_queries(qf, qa, k, cfg.alpha, mk)
+        assert d.info()["last_bf_tc"], "tensor-core path not taken"
+        os.environ["SB_BF_TC"] = "0"
+        try:
+            ids_s, dd_s = d.bf_topk_queries(qf, qa, k, cfg.alpha, mk)
+            assert not d.info()["last_bf_tc"]
+        finally:
+            del os.environ["SB_BF_TC"]
+        np.testing.assert_array_equal(ids_tc, ids_s)
+        np.testing.assert_array_equal(dd_tc, dd_s)
+        for qi in list(range(0, q, max(1, q // 7))) + [0]:
+            wi, wd = O.oracle_auto_topk(f, a, qf[qi], qa[qi], k, cfg.alpha,
+                                        None if mk is None else mk[qi], return_dists=True)
+            np.testing.assert_array_equal(ids_tc[qi], wi)
+            np.testing.assert_array_equal(dd_tc[qi], wd)
+
+
 @pytest.mark.slow
 def test_cfg1_end_to_end(cfg1_golden):
     """BASELINE config 1 through the public API: alpha, psi history, edge counts, final
