@@ -28,7 +28,7 @@ namespace sb {
 
 constexpr int kTcM = 128;       // queries per CTA (UMMA M)
 constexpr int kTcN = 256;       // nodes per tile (UMMA N)
-constexpr int kTcThreads = 128;
+constexpr int kTcThreads = 256;  // two threads per query row, each owning half the columns
 constexpr int kTcMaxKK = 32;    // per-thread list length limit
 
 // ---- PTX wrappers --------------------------------------------------------------------
@@ -159,8 +159,8 @@ __global__ void __launch_bounds__(kTcThreads, 1) bf_tc_kernel(TcArgs a) {
   char* sB = p; p += (size_t)kTcN * m * 2;
   int32_t* s_nx = reinterpret_cast<int32_t*>(p); p += sizeof(int32_t) * kTcN;
   int32_t* s_at = reinterpret_cast<int32_t*>(p); p += sizeof(int32_t) * (size_t)kTcN * a.l;
-  double* ld = reinterpret_cast<double*>(p); p += sizeof(double) * (size_t)kTcMaxKK * kTcM;
-  uint32_t* li = reinterpret_cast<uint32_t*>(p); p += sizeof(uint32_t) * (size_t)kTcMaxKK * kTcM;
+  double* ld = reinterpret_cast<double*>(p); p += sizeof(double) * (size_t)kTcMaxKK * kTcThreads;
+  uint32_t* li = reinterpret_cast<uint32_t*>(p); p += sizeof(uint32_t) * (size_t)kTcMaxKK * kTcThreads;
   uint64_t* bar = reinterpret_cast<uint64_t*>(p); p += 16;
   uint32_t* tslot = reinterpret_cast<uint32_t*>(p);
 
@@ -169,7 +169,9 @@ __global__ void __launch_bounds__(kTcThreads, 1) bf_tc_kernel(TcArgs a) {
   const int64_t per = ((a.n + a.splits - 1) / a.splits + kTcN - 1) / kTcN * kTcN;
   const int64_t v_begin = per * split;
   const int64_t v_end = v_begin + per < a.n ? v_begin + per : a.n;
-  const int64_t my_q = q0 + tid;
+  const int row = tid & (kTcM - 1);   // query row = TMEM lane
+  const int half = tid >> 7;          // which 128 columns of each tile this thread owns
+  const int64_t my_q = q0 + row;
   const bool qok = my_q < a.q;
   const double inf = __longlong_as_double(0x7FF0000000000000ll);
 
@@ -186,17 +188,14 @@ __global__ void __launch_bounds__(kTcThreads, 1) bf_tc_kernel(TcArgs a) {
   // A tile: this CTA's queries (zero rows past q)
   const int kchunks = m / 8;
   for (int e = tid; e < kTcM * kchunks; e += kTcThreads) {
-    int row = e / kchunks, kc = e % kchunks;
-    uint32_t dst = smem_u32(sA) + cm_off(row, kc, kTcM);
-    if (q0 + row < a.q) {
-      cp_async16(dst, a.Qb + (q0 + row) * m + kc * 8);
-    } else {
-      *reinterpret_cast<uint4*>(sA + cm_off(row, kc, kTcM)) = make_uint4(0, 0, 0, 0);
-    }
+    int r = e / kchunks, kc = e % kchunks;
+    uint32_t dst = smem_u32(sA) + cm_off(r, kc, kTcM);
+    if (q0 + r < a.q) cp_async16(dst, a.Qb + (q0 + r) * m + kc * 8);
+    else *reinterpret_cast<uint4*>(sA + cm_off(r, kc, kTcM)) = make_uint4(0, 0, 0, 0);
   }
   for (int i = 0; i < a.kk; ++i) {
-    ld[i * kTcM + tid] = inf;
-    li[i * kTcM + tid] = 0xFFFFFFFFu;
+    ld[i * kTcThreads + tid] = inf;
+    li[i * kTcThreads + tid] = 0xFFFFFFFFu;
   }
   cp_async_wait_all();
   tc_fence_before();
@@ -204,27 +203,33 @@ __global__ void __launch_bounds__(kTcThreads, 1) bf_tc_kernel(TcArgs a) {
   tc_fence_after();
   const uint32_t tmem = *tslot;
   const int32_t my_nq = qok ? a.nq[my_q] : 0;
-  int64_t qa_row[8];
-  int64_t qm_row[8];
+  int32_t qa_row[8];
+  int32_t qm_row[8];
+#pragma unroll
   for (int u = 0; u < 8; ++u) {
-    qa_row[u] = (qok && u < a.l) ? a.qa[my_q * a.l + u] : 0;
-    qm_row[u] = (qok && u < a.l) ? (a.qmask ? a.qmask[my_q * a.l + u] : 1) : 0;
+    qa_row[u] = (qok && u < a.l) ? (int32_t)a.qa[my_q * a.l + u] : 0;
+    qm_row[u] = (qok && u < a.l) ? (int32_t)(a.qmask ? a.qmask[my_q * a.l + u] : 1) : 0;
   }
-  double thr_s = inf;  // a node can enter only if S <= thr_s (conservative)
+  // Conservative fp32 filter: the exact distance is d = sqrt(S) * (1 + sa/alpha), so a node
+  // can beat the list tail T only if S * f^2 <= T^2 with f = 1 + sa * ia, ia <= 1/alpha.
+  // fp32 rounding (< 1e-6 relative) is covered by the 1e-5 slack; survivors are decided in
+  // exact fp64 below.
+  const float ia = __double2float_rd(1.0 / a.alpha);
+  float t2 = 3.4e38f;
   uint32_t phase = 0;
 
   for (int64_t vb = v_begin; vb < v_end; vb += kTcN) {
     // B tile: node rows (zero rows past the range) + norms + attributes
     for (int e = tid; e < kTcN * kchunks; e += kTcThreads) {
-      int row = e / kchunks, kc = e % kchunks;
-      int64_t v = vb + row;
-      uint32_t off = cm_off(row, kc, kTcN);
+      int r = e / kchunks, kc = e % kchunks;
+      int64_t v = vb + r;
+      uint32_t off = cm_off(r, kc, kTcN);
       if (v < v_end) cp_async16(smem_u32(sB) + off, a.Fb + v * m + kc * 8);
       else *reinterpret_cast<uint4*>(sB + off) = make_uint4(0, 0, 0, 0);
     }
     for (int r = tid; r < kTcN; r += kTcThreads) {
       int64_t v = vb + r;
-      s_nx[r] = v < v_end ? a.nx[v] : 0x7FFFFFFF;
+      s_nx[r] = v < v_end ? a.nx[v] : 0;
       for (int u = 0; u < a.l; ++u) s_at[r * a.l + u] = v < v_end ? a.A[v * a.l + u] : 0;
     }
     cp_async_wait_all();
@@ -244,56 +249,54 @@ __global__ void __launch_bounds__(kTcThreads, 1) bf_tc_kernel(TcArgs a) {
     mbar_wait(smem_u32(bar), phase);
     phase ^= 1u;
     tc_fence_after();
-    // epilogue: this thread = TMEM lane (32 * warp + lane) = query q0 + tid
-    const uint32_t lane_base = tmem + ((uint32_t)(warp_id() * 32) << 16);
-    for (int c = 0; c < kTcN / 16; ++c) {
+    // epilogue: TMEM lanes 32 * (warp % 4) .. + 31, columns [half * 128, half * 128 + 128)
+    const uint32_t lane_base = tmem + ((uint32_t)((warp_id() & 3) * 32) << 16) + (uint32_t)(half * 128);
+    const int nvalid = (int)(v_end - vb < kTcN ? v_end - vb : kTcN);
+    for (int c = 0; c < 8; ++c) {
       uint32_t r[16];
       tmem_ld16(lane_base + (uint32_t)(c * 16), r);
       if (!qok) continue;
 #pragma unroll
       for (int j = 0; j < 16; ++j) {
-        const int col = c * 16 + j;
-        const int64_t dot = (int64_t)__uint_as_float(r[j]);
-        const int64_t S = (int64_t)s_nx[col] + my_nq - 2 * dot;
-        if ((double)S > thr_s) continue;
-        const int64_t v = vb + col;
-        if (v >= v_end) continue;
-        int64_t sa = 0;
-        for (int u = 0; u < a.l; ++u) {
-          int64_t ad = (int64_t)s_at[col * a.l + u] - qa_row[u < 8 ? u : 7];
-          ad = ad < 0 ? -ad : ad;
-          sa += ad * qm_row[u < 8 ? u : 7];
-        }
+        const int col = half * 128 + c * 16 + j;
+        const int S = s_nx[col] + my_nq - 2 * (int)__uint_as_float(r[j]);
+        int sa = 0;
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+          if (u < a.l) sa += abs(s_at[col * a.l + u] - qa_row[u]) * qm_row[u];
+        const float f = fmaf((float)sa, ia, 1.0f);
+        if ((float)S * f * f > t2 || col >= nvalid) continue;
+        // exact fp64 decision (evaluate.py:48-53), ties by id
         const double dist = dmul(sqrt((double)S), dadd(1.0, __ddiv_rn((double)sa, a.alpha)));
-        // insert into this thread's sorted list (d, id) if it beats the tail
-        const uint32_t vid = (uint32_t)v;
-        double wd = ld[(a.kk - 1) * kTcM + tid];
-        uint32_t wi = li[(a.kk - 1) * kTcM + tid];
+        const uint32_t vid = (uint32_t)(vb + col);
+        double wd = ld[(a.kk - 1) * kTcThreads + tid];
+        uint32_t wi = li[(a.kk - 1) * kTcThreads + tid];
         if (!dlt(dist, vid, wd, wi)) continue;
         int pos = a.kk - 1;
         while (pos > 0) {
-          double pd = ld[(pos - 1) * kTcM + tid];
-          uint32_t pi = li[(pos - 1) * kTcM + tid];
+          double pd = ld[(pos - 1) * kTcThreads + tid];
+          uint32_t pi = li[(pos - 1) * kTcThreads + tid];
           if (!dlt(dist, vid, pd, pi)) break;
-          ld[pos * kTcM + tid] = pd;
-          li[pos * kTcM + tid] = pi;
+          ld[pos * kTcThreads + tid] = pd;
+          li[pos * kTcThreads + tid] = pi;
           --pos;
         }
-        ld[pos * kTcM + tid] = dist;
-        li[pos * kTcM + tid] = vid;
-        const double t = ld[(a.kk - 1) * kTcM + tid];
-        thr_s = t * t * (1.0 + 1e-9) + 1.0;
+        ld[pos * kTcThreads + tid] = dist;
+        li[pos * kTcThreads + tid] = vid;
+        const double t = ld[(a.kk - 1) * kTcThreads + tid];
+        if (t < inf) t2 = (float)(t * t * (1.0 + 1e-5));
       }
     }
     tc_fence_before();
     __syncthreads();
   }
-  // partial lists out
+  // partial lists out: split index 2 * split + half
   if (qok) {
-    size_t o = ((size_t)my_q * a.splits + split) * a.kk;
+    const int sp = 2 * split + half;
+    size_t o = ((size_t)my_q * (2 * a.splits) + sp) * a.kk;
     for (int i = 0; i < a.kk; ++i) {
-      a.part_d[o + i] = ld[i * kTcM + tid];
-      a.part_i[o + i] = li[i * kTcM + tid];
+      a.part_d[o + i] = ld[i * kTcThreads + tid];
+      a.part_i[o + i] = li[i * kTcThreads + tid];
     }
   }
   tc_fence_before();
@@ -306,7 +309,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) bf_tc_kernel(TcArgs a) {
 
 size_t bf_tc_smem(int m, int l) {
   return (size_t)kTcM * m * 2 + (size_t)kTcN * m * 2 + sizeof(int32_t) * kTcN +
-         sizeof(int32_t) * (size_t)kTcN * l + (sizeof(double) + sizeof(uint32_t)) * kTcMaxKK * kTcM +
+         sizeof(int32_t) * (size_t)kTcN * l + (sizeof(double) + sizeof(uint32_t)) * kTcMaxKK * kTcThreads +
          64;
 }
 

@@ -816,9 +816,9 @@ int sb_bf_topk_queries(sb_index* idx, const double* qf, const int64_t* qa, const
     const int groups = (int)((q + 127) / 128);
     int splits = std::max(1, (2 * idx->sms + groups - 1) / groups);
     splits = (int)std::min<int64_t>(splits, std::max<int64_t>(1, n / 256));
-    a.splits = splits;
-    CK(idx->bf_part_d.ensure(sizeof(double) * q * splits * kk));
-    CK(idx->bf_part_i.ensure(sizeof(uint32_t) * q * splits * kk));
+    a.splits = 2 * splits;  // each CTA emits two partial lists per query (column halves)
+    CK(idx->bf_part_d.ensure(sizeof(double) * q * a.splits * kk));
+    CK(idx->bf_part_i.ensure(sizeof(uint32_t) * q * a.splits * kk));
     a.part_d = idx->bf_part_d.as<double>();
     a.part_i = idx->bf_part_i.as<uint32_t>();
     CK(idx->small.ensure(64));
