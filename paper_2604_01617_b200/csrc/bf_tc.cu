@@ -104,21 +104,6 @@ SB_DEV uint32_t cm_off(int row, int kc, int R) {
 }
 
 // ---- prep kernels ----------------------------------------------------------------------
-// bf16 copy of integer features and exact squared norms
-__global__ void tc_prep_nodes_kernel(const float* F, int64_t n, int m, __nv_bfloat16* Fb,
-                                     int32_t* nx) {
-  int64_t v = (int64_t)blockIdx.x * (blockDim.x >> 5) + warp_id();
-  if (v >= n) return;
-  int acc = 0;
-  for (int t = lane_id(); t < m; t += 32) {
-    float x = F[v * m + t];
-    Fb[v * m + t] = __float2bfloat16_rn(x);
-    acc += (int)x * (int)x;
-  }
-  acc = warp_sum(acc);
-  if (lane_id() == 0) nx[v] = acc;
-}
-
 __global__ void tc_prep_queries_kernel(const double* qf, int64_t q, int m, __nv_bfloat16* Qb,
                                        int32_t* nq) {
   int64_t i = (int64_t)blockIdx.x * (blockDim.x >> 5) + warp_id();
@@ -135,9 +120,13 @@ __global__ void tc_prep_queries_kernel(const double* qf, int64_t q, int m, __nv_
 
 // ---- main kernel -------------------------------------------------------------------------
 struct TcArgs {
+  // node arrays in attribute-grouped order (tc_prepare): nodes with one attribute tuple are
+  // contiguous, so the epilogue recomputes the attribute factor only when the tuple changes
   const __nv_bfloat16* Fb;  // n x m
   const int32_t* nx;        // n
   const int32_t* A;         // n x l
+  const int32_t* code;      // n: attribute-tuple code (equal codes <=> equal tuples)
+  const int32_t* orig;      // n: original node id
   const __nv_bfloat16* Qb;  // q x m
   const int32_t* nq;        // q
   const int64_t* qa;        // q x l
@@ -159,6 +148,8 @@ __global__ void __launch_bounds__(kTcThreads, 1) bf_tc_kernel(TcArgs a) {
   char* sB = p; p += (size_t)kTcN * m * 2;
   int32_t* s_nx = reinterpret_cast<int32_t*>(p); p += sizeof(int32_t) * kTcN;
   int32_t* s_at = reinterpret_cast<int32_t*>(p); p += sizeof(int32_t) * (size_t)kTcN * a.l;
+  int32_t* s_code = reinterpret_cast<int32_t*>(p); p += sizeof(int32_t) * kTcN;
+  int32_t* s_orig = reinterpret_cast<int32_t*>(p); p += sizeof(int32_t) * kTcN;
   double* ld = reinterpret_cast<double*>(p); p += sizeof(double) * (size_t)kTcMaxKK * kTcThreads;
   uint32_t* li = reinterpret_cast<uint32_t*>(p); p += sizeof(uint32_t) * (size_t)kTcMaxKK * kTcThreads;
   uint64_t* bar = reinterpret_cast<uint64_t*>(p); p += 16;
@@ -217,6 +208,8 @@ __global__ void __launch_bounds__(kTcThreads, 1) bf_tc_kernel(TcArgs a) {
   const float ia = __double2float_rd(1.0 / a.alpha);
   float t2 = 3.4e38f;
   uint32_t phase = 0;
+  int last_code = -2, sa = 0;
+  float f2 = 1.0f;
 
   for (int64_t vb = v_begin; vb < v_end; vb += kTcN) {
     // B tile: node rows (zero rows past the range) + norms + attributes
@@ -230,6 +223,8 @@ __global__ void __launch_bounds__(kTcThreads, 1) bf_tc_kernel(TcArgs a) {
     for (int r = tid; r < kTcN; r += kTcThreads) {
       int64_t v = vb + r;
       s_nx[r] = v < v_end ? a.nx[v] : 0;
+      s_code[r] = v < v_end ? a.code[v] : -1;
+      s_orig[r] = v < v_end ? a.orig[v] : 0;
       for (int u = 0; u < a.l; ++u) s_at[r * a.l + u] = v < v_end ? a.A[v * a.l + u] : 0;
     }
     cp_async_wait_all();
@@ -259,16 +254,24 @@ __global__ void __launch_bounds__(kTcThreads, 1) bf_tc_kernel(TcArgs a) {
 #pragma unroll
       for (int j = 0; j < 16; ++j) {
         const int col = half * 128 + c * 16 + j;
-        const int S = s_nx[col] + my_nq - 2 * (int)__uint_as_float(r[j]);
-        int sa = 0;
+        // S = |x|^2 + |q|^2 - 2 x.q, exact in fp32 (an integer below 2^24)
+        const float Sf = fmaf(-2.0f, __uint_as_float(r[j]), (float)(s_nx[col] + my_nq));
+        const int code = s_code[col];
+        if (code != last_code) {  // new attribute tuple: recompute its factor for this query
+          last_code = code;
+          int s2 = 0;
 #pragma unroll
-        for (int u = 0; u < 8; ++u)
-          if (u < a.l) sa += abs(s_at[col * a.l + u] - qa_row[u]) * qm_row[u];
-        const float f = fmaf((float)sa, ia, 1.0f);
-        if ((float)S * f * f > t2 || col >= nvalid) continue;
-        // exact fp64 decision (evaluate.py:48-53), ties by id
+          for (int u = 0; u < 8; ++u)
+            if (u < a.l) s2 += abs(s_at[col * a.l + u] - qa_row[u]) * qm_row[u];
+          sa = s2;
+          const float f = fmaf((float)sa, ia, 1.0f);
+          f2 = f * f;
+        }
+        if (Sf * f2 > t2 || col >= nvalid) continue;
+        // exact fp64 decision (evaluate.py:48-53), ties by original id
+        const int S = (int)Sf;
         const double dist = dmul(sqrt((double)S), dadd(1.0, __ddiv_rn((double)sa, a.alpha)));
-        const uint32_t vid = (uint32_t)(vb + col);
+        const uint32_t vid = (uint32_t)s_orig[col];
         double wd = ld[(a.kk - 1) * kTcThreads + tid];
         uint32_t wi = li[(a.kk - 1) * kTcThreads + tid];
         if (!dlt(dist, vid, wd, wi)) continue;
@@ -308,7 +311,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) bf_tc_kernel(TcArgs a) {
 }
 
 size_t bf_tc_smem(int m, int l) {
-  return (size_t)kTcM * m * 2 + (size_t)kTcN * m * 2 + sizeof(int32_t) * kTcN +
+  return (size_t)kTcM * m * 2 + (size_t)kTcN * m * 2 + sizeof(int32_t) * kTcN * 3 +
          sizeof(int32_t) * (size_t)kTcN * l + (sizeof(double) + sizeof(uint32_t)) * kTcMaxKK * kTcThreads +
          64;
 }
@@ -317,9 +320,82 @@ int bf_tc_supported(int m, int l, int kk) {
   return (m % 16 == 0) && m <= 256 && l <= 8 && kk <= kTcMaxKK && bf_tc_smem(m, l) <= 227 * 1024;
 }
 
-int launch_bf_tc_prep_nodes(const float* F, int64_t n, int m, void* Fb, int32_t* nx,
-                            cudaStream_t st) {
-  tc_prep_nodes_kernel<<<(unsigned)((n + 7) / 8), 256, 0, st>>>(F, n, m, (__nv_bfloat16*)Fb, nx);
+// ---- attribute-grouped node order ---------------------------------------------------
+__global__ void tc_attr_range_kernel(const int32_t* A, int64_t n, int l, int32_t* lo, int32_t* hi) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  for (int u = 0; u < l; ++u) {
+    atomicMin(lo + u, A[i * l + u]);
+    atomicMax(hi + u, A[i * l + u]);
+  }
+}
+
+// code = mixed-radix attribute tuple (or the node id when tuples are too many to group)
+__global__ void tc_code_kernel(const int32_t* A, int64_t n, int l, const int32_t* lo,
+                               const int64_t* stride, int grouped, int32_t* code,
+                               unsigned long long* hist) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  int64_t c = 0;
+  if (grouped) {
+    for (int u = 0; u < l; ++u) c += (int64_t)(A[i * l + u] - lo[u]) * stride[u];
+  } else {
+    c = i;
+  }
+  code[i] = (int32_t)c;
+  atomicAdd(hist + c, 1ull);
+}
+
+__global__ void tc_scatter_kernel(const int32_t* code, int64_t n, const int64_t* off,
+                                  unsigned long long* cur, int32_t* orig) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  int32_t c = code[i];
+  unsigned long long p = atomicAdd(cur + c, 1ull);
+  orig[off[c] + (int64_t)p] = (int32_t)i;
+}
+
+// sorted copies: bf16 rows, exact squared norms, codes, attributes (warp per node)
+__global__ void tc_gather_kernel(const float* F, const int32_t* A, const int32_t* code_in,
+                                 const int32_t* orig, int64_t n, int m, int l,
+                                 __nv_bfloat16* Fb, int32_t* nx, int32_t* code, int32_t* As) {
+  int64_t p = (int64_t)blockIdx.x * (blockDim.x >> 5) + warp_id();
+  if (p >= n) return;
+  const int64_t v = orig[p];
+  int acc = 0;
+  for (int t = lane_id(); t < m; t += 32) {
+    float x = F[v * m + t];
+    Fb[p * m + t] = __float2bfloat16_rn(x);
+    acc += (int)x * (int)x;
+  }
+  acc = warp_sum(acc);
+  if (lane_id() == 0) {
+    nx[p] = acc;
+    code[p] = code_in[v];
+  }
+  for (int u = lane_id(); u < l; u += 32) As[p * l + u] = A[v * l + u];
+}
+
+int launch_tc_attr_range(const int32_t* A, int64_t n, int l, int32_t* lo, int32_t* hi,
+                         cudaStream_t st) {
+  tc_attr_range_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(A, n, l, lo, hi);
+  return (int)cudaGetLastError();
+}
+int launch_tc_code(const int32_t* A, int64_t n, int l, const int32_t* lo, const int64_t* stride,
+                   int grouped, int32_t* code, unsigned long long* hist, cudaStream_t st) {
+  tc_code_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(A, n, l, lo, stride, grouped, code, hist);
+  return (int)cudaGetLastError();
+}
+int launch_tc_scatter(const int32_t* code, int64_t n, const int64_t* off, unsigned long long* cur,
+                      int32_t* orig, cudaStream_t st) {
+  tc_scatter_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(code, n, off, cur, orig);
+  return (int)cudaGetLastError();
+}
+int launch_tc_gather(const float* F, const int32_t* A, const int32_t* code_in, const int32_t* orig,
+                     int64_t n, int m, int l, void* Fb, int32_t* nx, int32_t* code, int32_t* As,
+                     cudaStream_t st) {
+  tc_gather_kernel<<<(unsigned)((n + 7) / 8), 256, 0, st>>>(F, A, code_in, orig, n, m, l,
+                                                             (__nv_bfloat16*)Fb, nx, code, As);
   return (int)cudaGetLastError();
 }
 
@@ -329,12 +405,13 @@ int launch_bf_tc_prep_queries(const double* qf, int64_t q, int m, void* Qb, int3
   return (int)cudaGetLastError();
 }
 
-int launch_bf_tc(const void* Fb, const int32_t* nx, const int32_t* A, const void* Qb,
-                 const int32_t* nq, const int64_t* qa, const int64_t* qmask, int64_t n, int64_t q,
-                 int m, int l, int kk, int splits, double alpha, double* part_d, uint32_t* part_i,
-                 cudaStream_t st) {
+int launch_bf_tc(const void* Fb, const int32_t* nx, const int32_t* A, const int32_t* code,
+                 const int32_t* orig, const void* Qb, const int32_t* nq, const int64_t* qa,
+                 const int64_t* qmask, int64_t n, int64_t q, int m, int l, int kk, int splits,
+                 double alpha, double* part_d, uint32_t* part_i, cudaStream_t st) {
   TcArgs a;
-  a.Fb = (const __nv_bfloat16*)Fb; a.nx = nx; a.A = A; a.Qb = (const __nv_bfloat16*)Qb;
+  a.Fb = (const __nv_bfloat16*)Fb; a.nx = nx; a.A = A; a.code = code; a.orig = orig;
+  a.Qb = (const __nv_bfloat16*)Qb;
   a.nq = nq; a.qa = qa; a.qmask = qmask; a.n = n; a.q = q; a.m = m; a.l = l; a.kk = kk;
   a.splits = splits; a.alpha = alpha; a.part_d = part_d; a.part_i = part_i;
   size_t smem = bf_tc_smem(m, l);

@@ -96,9 +96,10 @@ struct sb_index {
   DBuf rf_n8, rf_nb, rf_n32, rf_n64, rf_o32, rf_o64, rf_ulist, rf_bits, rf_rec, rf_sim;
   // routing / brute force
   DBuf qf, qa, qm, entries, ent_scratch, out_ids, out_dists, stats, visited, vlog, counter;
-  DBuf bf_part_d, bf_part_i, bf_self, bf_qa, bf_qm, bf_out32, fb, fb_norm, qb;
+  DBuf bf_part_d, bf_part_i, bf_self, bf_qa, bf_qm, bf_out32, fb, fb_norm, fb_tmp, qb;
   ~sb_index() {
     fb.release();
+    fb_tmp.release();
     fb_norm.release();
     qb.release();
     DBuf* all[] = {&F, &A, &ids, &dists, &flags, &counts, &new_cand, &new_cnt, &old_cand,
@@ -803,12 +804,54 @@ int sb_bf_topk_queries(sb_index* idx, const double* qf, const int64_t* qa, const
   if (tc) {
     const int64_t n = idx->n;
     if (!idx->have_fb) {
+      // attribute-grouped node order: counting sort by the attribute tuple
+      const int l = idx->l;
       CK(idx->fb.ensure(sizeof(uint16_t) * n * idx->m));
-      CK(idx->fb_norm.ensure(sizeof(int32_t) * n));
-      CKL(sb::launch_bf_tc_prep_nodes(idx->F.as<float>(), n, idx->m, idx->fb.p,
-                                      idx->fb_norm.as<int32_t>(), idx->st));
+      CK(idx->fb_norm.ensure(sizeof(int32_t) * n * (3 + l)));  // nx | code | orig | attrs
+      int32_t* s_nx = idx->fb_norm.as<int32_t>();
+      int32_t* s_code = s_nx + n;
+      int32_t* s_orig = s_code + n;
+      int32_t* s_attr = s_orig + n;
+      CK(idx->small.ensure(64));
+      CK(idx->fb_tmp.ensure(sizeof(int32_t) * (2 * 8 + n + 2) + sizeof(int64_t) * 8));
+      int32_t* d_lo = idx->fb_tmp.as<int32_t>();
+      int32_t* d_hi = d_lo + 8;
+      int32_t* d_code = d_hi + 8;
+      int64_t* d_stride = reinterpret_cast<int64_t*>(d_code + n + (n & 1));
+      std::vector<int32_t> hlo(8, 0x7FFFFFFF), hhi(8, (int32_t)0x80000000);
+      CK(cudaMemcpyAsync(d_lo, hlo.data(), sizeof(int32_t) * 8, cudaMemcpyHostToDevice, idx->st));
+      CK(cudaMemcpyAsync(d_hi, hhi.data(), sizeof(int32_t) * 8, cudaMemcpyHostToDevice, idx->st));
+      CKL(sb::launch_tc_attr_range(idx->A.as<int32_t>(), n, l, d_lo, d_hi, idx->st));
+      CK(cudaMemcpyAsync(hlo.data(), d_lo, sizeof(int32_t) * 8, cudaMemcpyDeviceToHost, idx->st));
+      CK(cudaMemcpyAsync(hhi.data(), d_hi, sizeof(int32_t) * 8, cudaMemcpyDeviceToHost, idx->st));
+      CK(cudaStreamSynchronize(idx->st));
+      std::vector<int64_t> stride(8, 0);
+      int64_t combos = 1;
+      for (int u = l - 1; u >= 0; --u) {
+        stride[u] = combos;
+        combos *= (int64_t)hhi[u] - hlo[u] + 1;
+        if (combos > ((int64_t)1 << 24)) break;
+      }
+      const int grouped = combos <= ((int64_t)1 << 24) ? 1 : 0;
+      const int64_t bins = grouped ? combos : n;
+      CK(cudaMemcpyAsync(d_stride, stride.data(), sizeof(int64_t) * 8, cudaMemcpyHostToDevice, idx->st));
+      CK(idx->rev_cnt.ensure(sizeof(int64_t) * std::max<int64_t>(bins, n)));
+      CK(idx->rev_off.ensure(sizeof(int64_t) * std::max<int64_t>(bins, n)));
+      CK(idx->rev_cur.ensure(sizeof(int64_t) * std::max<int64_t>(bins, n)));
+      CK(idx->scan_tmp.ensure(sizeof(int64_t) * sb::scan_tmp_slots(std::max<int64_t>(bins, n))));
+      CK(cudaMemsetAsync(idx->rev_cnt.p, 0, sizeof(int64_t) * bins, idx->st));
+      CK(cudaMemsetAsync(idx->rev_cur.p, 0, sizeof(int64_t) * bins, idx->st));
+      CKL(sb::launch_tc_code(idx->A.as<int32_t>(), n, l, d_lo, d_stride, grouped, d_code,
+                             idx->rev_cnt.as<unsigned long long>(), idx->st));
+      CKL(sb::exclusive_scan(idx->rev_cnt.as<int64_t>(), idx->rev_off.as<int64_t>(), bins,
+                             idx->scan_tmp.as<int64_t>(), idx->st));
+      CKL(sb::launch_tc_scatter(d_code, n, idx->rev_off.as<int64_t>(),
+                                idx->rev_cur.as<unsigned long long>(), s_orig, idx->st));
+      CKL(sb::launch_tc_gather(idx->F.as<float>(), idx->A.as<int32_t>(), d_code, s_orig, n,
+                               idx->m, l, idx->fb.p, s_nx, s_code, s_attr, idx->st));
       idx->have_fb = true;
-      idx->launches += 1;
+      idx->have_cand = false;  // rev_* scratch was reused
+      idx->launches += 6;
     }
     CK(idx->qb.ensure(sizeof(uint16_t) * q * idx->m + sizeof(int32_t) * q + 64));
     int32_t* d_nq = reinterpret_cast<int32_t*>(idx->qb.as<char>() + ((sizeof(uint16_t) * q * idx->m + 15) & ~(size_t)15));
@@ -824,9 +867,12 @@ int sb_bf_topk_queries(sb_index* idx, const double* qf, const int64_t* qa, const
     CK(idx->small.ensure(64));
     int* d_unc = reinterpret_cast<int*>(idx->small.as<unsigned long long>() + 6);
     CK(cudaMemsetAsync(d_unc, 0, sizeof(int), idx->st));
-    CKL(sb::launch_bf_tc(idx->fb.p, idx->fb_norm.as<int32_t>(), idx->A.as<int32_t>(), idx->qb.p,
-                         d_nq, a.qa, a.qmask, n, q, idx->m, idx->l, kk, splits, alpha, a.part_d,
-                         a.part_i, idx->st));
+    {
+      int32_t* s_nx = idx->fb_norm.as<int32_t>();
+      CKL(sb::launch_bf_tc(idx->fb.p, s_nx, s_nx + 3 * n, s_nx + n, s_nx + 2 * n, idx->qb.p,
+                           d_nq, a.qa, a.qmask, n, q, idx->m, idx->l, kk, splits, alpha, a.part_d,
+                           a.part_i, idx->st));
+    }
     CKL(sb::launch_bf_merge_k(a, k, idx->out_ids.as<int64_t>(), nullptr, idx->out_dists.as<double>(),
                               d_unc, idx->st));
     CK(cudaMemcpyAsync(&unc, d_unc, sizeof(int), cudaMemcpyDeviceToHost, idx->st));

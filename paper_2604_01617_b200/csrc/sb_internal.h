@@ -71,14 +71,21 @@ int launch_bf_merge_k(const BfArgs& a, int kout, int64_t* out_ids64, int32_t* ou
 // tensor-core query-mode top-k for integer data (bf_tc.cu)
 size_t bf_tc_smem(int m, int l);
 int bf_tc_supported(int m, int l, int kk);
-int launch_bf_tc_prep_nodes(const float* F, int64_t n, int m, void* Fb, int32_t* nx,
-                            cudaStream_t st);
+int launch_tc_attr_range(const int32_t* A, int64_t n, int l, int32_t* lo, int32_t* hi,
+                         cudaStream_t st);
+int launch_tc_code(const int32_t* A, int64_t n, int l, const int32_t* lo, const int64_t* stride,
+                   int grouped, int32_t* code, unsigned long long* hist, cudaStream_t st);
+int launch_tc_scatter(const int32_t* code, int64_t n, const int64_t* off, unsigned long long* cur,
+                      int32_t* orig, cudaStream_t st);
+int launch_tc_gather(const float* F, const int32_t* A, const int32_t* code_in, const int32_t* orig,
+                     int64_t n, int m, int l, void* Fb, int32_t* nx, int32_t* code, int32_t* As,
+                     cudaStream_t st);
 int launch_bf_tc_prep_queries(const double* qf, int64_t q, int m, void* Qb, int32_t* nq,
                               cudaStream_t st);
-int launch_bf_tc(const void* Fb, const int32_t* nx, const int32_t* A, const void* Qb,
-                 const int32_t* nq, const int64_t* qa, const int64_t* qmask, int64_t n, int64_t q,
-                 int m, int l, int kk, int splits, double alpha, double* part_d, uint32_t* part_i,
-                 cudaStream_t st);
+int launch_bf_tc(const void* Fb, const int32_t* nx, const int32_t* A, const int32_t* code,
+                 const int32_t* orig, const void* Qb, const int32_t* nq, const int64_t* qa,
+                 const int64_t* qmask, int64_t n, int64_t q, int m, int l, int kk, int splits,
+                 double alpha, double* part_d, uint32_t* part_i, cudaStream_t st);
 
 // ---- HELP build ---------------------------------------------------------------
 struct BuildScratch {
