@@ -152,6 +152,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) bf_tc_kernel(TcArgs a) {
   int32_t* s_orig = reinterpret_cast<int32_t*>(p); p += sizeof(int32_t) * kTcN;
   double* ld = reinterpret_cast<double*>(p); p += sizeof(double) * (size_t)kTcMaxKK * kTcThreads;
   uint32_t* li = reinterpret_cast<uint32_t*>(p); p += sizeof(uint32_t) * (size_t)kTcMaxKK * kTcThreads;
+  float* s_t2 = reinterpret_cast<float*>(p); p += sizeof(float) * kTcThreads;
   uint64_t* bar = reinterpret_cast<uint64_t*>(p); p += 16;
   uint32_t* tslot = reinterpret_cast<uint32_t*>(p);
 
@@ -206,7 +207,8 @@ __global__ void __launch_bounds__(kTcThreads, 1) bf_tc_kernel(TcArgs a) {
   // fp32 rounding (< 1e-6 relative) is covered by the 1e-5 slack; survivors are decided in
   // exact fp64 below.
   const float ia = __double2float_rd(1.0 / a.alpha);
-  float t2 = 3.4e38f;
+  float t2 = 3.4e38f;      // own list tail bound
+  float t2_eff = 3.4e38f;  // min over both halves of this query
   uint32_t phase = 0;
   int last_code = -2, sa = 0;
   float f2 = 1.0f;
@@ -251,13 +253,27 @@ __global__ void __launch_bounds__(kTcThreads, 1) bf_tc_kernel(TcArgs a) {
       uint32_t r[16];
       tmem_ld16(lane_base + (uint32_t)(c * 16), r);
       if (!qok) continue;
+      const int c0 = half * 128 + c * 16;
+      // columns are in attribute-grouped order: if both ends of the chunk carry the current
+      // tuple, the whole chunk does, and the factor f2 holds for all 16 columns
+      unsigned cand = 0;
+      if (s_code[c0] == last_code && s_code[c0 + 15] == last_code) {
 #pragma unroll
-      for (int j = 0; j < 16; ++j) {
-        const int col = half * 128 + c * 16 + j;
-        // S = |x|^2 + |q|^2 - 2 x.q, exact in fp32 (an integer below 2^24)
-        const float Sf = fmaf(-2.0f, __uint_as_float(r[j]), (float)(s_nx[col] + my_nq));
+        for (int j = 0; j < 16; ++j) {
+          // S = |x|^2 + |q|^2 - 2 x.q, exact in fp32 (an integer below 2^24)
+          const float Sf = fmaf(-2.0f, __uint_as_float(r[j]), (float)(s_nx[c0 + j] + my_nq));
+          cand |= (Sf * f2 <= t2_eff ? 1u : 0u) << j;
+        }
+      } else {
+        cand = 0xFFFFu;  // mixed chunk: decide column by column below
+      }
+      if (c0 + 16 > nvalid) cand &= (nvalid > c0) ? ((1u << (nvalid - c0)) - 1u) : 0u;
+      while (cand) {
+        const int j = __ffs(cand) - 1;
+        cand &= cand - 1u;
+        const int col = c0 + j;
         const int code = s_code[col];
-        if (code != last_code) {  // new attribute tuple: recompute its factor for this query
+        if (code != last_code) {  // new attribute tuple: its factor for this query
           last_code = code;
           int s2 = 0;
 #pragma unroll
@@ -267,7 +283,12 @@ __global__ void __launch_bounds__(kTcThreads, 1) bf_tc_kernel(TcArgs a) {
           const float f = fmaf((float)sa, ia, 1.0f);
           f2 = f * f;
         }
-        if (Sf * f2 > t2 || col >= nvalid) continue;
+        float rj = 0.f;
+#pragma unroll
+        for (int jj = 0; jj < 16; ++jj)
+          if (jj == j) rj = __uint_as_float(r[jj]);
+        const float Sf = fmaf(-2.0f, rj, (float)(s_nx[col] + my_nq));
+        if (Sf * f2 > t2_eff) continue;
         // exact fp64 decision (evaluate.py:48-53), ties by original id
         const int S = (int)Sf;
         const double dist = dmul(sqrt((double)S), dadd(1.0, __ddiv_rn((double)sa, a.alpha)));
@@ -287,11 +308,18 @@ __global__ void __launch_bounds__(kTcThreads, 1) bf_tc_kernel(TcArgs a) {
         ld[pos * kTcThreads + tid] = dist;
         li[pos * kTcThreads + tid] = vid;
         const double t = ld[(a.kk - 1) * kTcThreads + tid];
-        if (t < inf) t2 = (float)(t * t * (1.0 + 1e-5));
+        if (t < inf) {
+          t2 = (float)(t * t * (1.0 + 1e-5));
+          t2_eff = fminf(t2_eff, t2);
+        }
       }
     }
+    // share list tails between the two threads of a query: a node beyond the other half's
+    // kk-th cannot enter the merged top-kk either, so the tighter bound filters both
+    s_t2[tid] = t2;
     tc_fence_before();
     __syncthreads();
+    t2_eff = fminf(t2, s_t2[tid ^ kTcM]);
   }
   // partial lists out: split index 2 * split + half
   if (qok) {
@@ -313,7 +341,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) bf_tc_kernel(TcArgs a) {
 size_t bf_tc_smem(int m, int l) {
   return (size_t)kTcM * m * 2 + (size_t)kTcN * m * 2 + sizeof(int32_t) * kTcN * 3 +
          sizeof(int32_t) * (size_t)kTcN * l + (sizeof(double) + sizeof(uint32_t)) * kTcMaxKK * kTcThreads +
-         64;
+         sizeof(float) * kTcThreads + 64;
 }
 
 int bf_tc_supported(int m, int l, int kk) {

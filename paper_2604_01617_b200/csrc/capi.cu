@@ -856,9 +856,15 @@ int sb_bf_topk_queries(sb_index* idx, const double* qf, const int64_t* qa, const
     CK(idx->qb.ensure(sizeof(uint16_t) * q * idx->m + sizeof(int32_t) * q + 64));
     int32_t* d_nq = reinterpret_cast<int32_t*>(idx->qb.as<char>() + ((sizeof(uint16_t) * q * idx->m + 15) & ~(size_t)15));
     CKL(sb::launch_bf_tc_prep_queries(idx->qf.as<double>(), q, idx->m, idx->qb.p, d_nq, idx->st));
+    // split the node range so that whole waves of CTAs are busy: minimise waves / splits
     const int groups = (int)((q + 127) / 128);
-    int splits = std::max(1, (2 * idx->sms + groups - 1) / groups);
-    splits = (int)std::min<int64_t>(splits, std::max<int64_t>(1, n / 256));
+    int splits = 1;
+    double best = 1e30;
+    for (int s2 = 1; s2 <= 8 && (int64_t)s2 * 256 <= n; ++s2) {
+      double waves = (double)((groups * s2 + idx->sms - 1) / idx->sms);
+      double cost = waves / s2;
+      if (cost < best - 1e-9) { best = cost; splits = s2; }
+    }
     a.splits = 2 * splits;  // each CTA emits two partial lists per query (column halves)
     CK(idx->bf_part_d.ensure(sizeof(double) * q * a.splits * kk));
     CK(idx->bf_part_i.ensure(sizeof(uint32_t) * q * a.splits * kk));
