@@ -312,7 +312,7 @@ size_t bf_partial_smem(int k) { return bf_smem_bytes(next_pow2(k)); }
 
 int launch_bf_merge_k(const BfArgs& a, int kout, int64_t* out_ids64, int32_t* out_ids32,
                       double* out_dists, int* uncertain, cudaStream_t st) {
-  int kpad = next_pow2(a.k);
+  int kpad = next_pow2(a.k < 2 ? 2 : a.k);  // even, so every warp's slice stays 8-byte aligned
   int wpb = 4;
   size_t per_warp = (size_t)kpad * 2 * (sizeof(double) + sizeof(uint32_t)) + kpad * sizeof(int);
   size_t smem = per_warp * wpb;

@@ -778,7 +778,7 @@ int sb_bf_topk_queries(sb_index* idx, const double* qf, const int64_t* qa, const
   if (k > 1000) return fail(SB_EARG, "k must be <= 1000");
   if (q <= 0) return SB_OK;
   const int extra = 16;
-  const int kk = (int)std::min<int64_t>(idx->n, k + extra);
+  int kk = (int)std::min<int64_t>(idx->n, k + extra);
   CK(idx->qf.ensure(sizeof(double) * q * idx->m));
   CK(idx->bf_qa.ensure(sizeof(int64_t) * q * idx->l));
   CK(idx->bf_qm.ensure(sizeof(int64_t) * q * idx->l));
@@ -794,24 +794,31 @@ int sb_bf_topk_queries(sb_index* idx, const double* qf, const int64_t* qa, const
   int unc = 0;
   // tensor-core path: integer features and queries, |values| <= 256 (exact in bf16), every
   // partial dot product below 2^24 (exact in the fp32 accumulator)
+  // (integer data: U is exact whatever the summation order, so lists of exactly k suffice)
   bool tc = idx->int_exact && idx->fmax <= 256.0 && idx->m <= 255 && !idx->force_sequential &&
-            sb::bf_tc_supported(idx->m, idx->l, kk);
+            sb::bf_tc_supported(idx->m, idx->l, k);
   if (const char* e = getenv("SB_BF_TC")) tc = tc && atoi(e) != 0;
   for (int64_t i = 0; tc && i < q * idx->m; ++i) {
     double v = qf[i];
     tc = v == std::rint(v) && std::fabs(v) <= 256.0;
   }
   if (tc) {
+    kk = k;
+    a.k = kk;
     const int64_t n = idx->n;
+    const int64_t npad = (n + sb::kTcNodePad - 1) / sb::kTcNodePad * sb::kTcNodePad;
     if (!idx->have_fb) {
       // attribute-grouped node order: counting sort by the attribute tuple
       const int l = idx->l;
-      CK(idx->fb.ensure(sizeof(uint16_t) * n * idx->m));
-      CK(idx->fb_norm.ensure(sizeof(int32_t) * n * (3 + l)));  // nx | code | orig | attrs
+      // padded, zero-filled: every tile the kernel copies lies inside the buffers
+      CK(idx->fb.ensure(sizeof(uint16_t) * npad * idx->m));
+      CK(idx->fb_norm.ensure(sizeof(int32_t) * npad * (3 + l)));  // nx | code | orig | attrs
+      CK(cudaMemsetAsync(idx->fb.p, 0, sizeof(uint16_t) * npad * idx->m, idx->st));
+      CK(cudaMemsetAsync(idx->fb_norm.p, 0, sizeof(int32_t) * npad * (3 + l), idx->st));
       int32_t* s_nx = idx->fb_norm.as<int32_t>();
-      int32_t* s_code = s_nx + n;
-      int32_t* s_orig = s_code + n;
-      int32_t* s_attr = s_orig + n;
+      int32_t* s_code = s_nx + npad;
+      int32_t* s_orig = s_code + npad;
+      int32_t* s_attr = s_orig + npad;
       CK(idx->small.ensure(64));
       CK(idx->fb_tmp.ensure(sizeof(int32_t) * (2 * 8 + n + 2) + sizeof(int64_t) * 8));
       int32_t* d_lo = idx->fb_tmp.as<int32_t>();
@@ -853,8 +860,9 @@ int sb_bf_topk_queries(sb_index* idx, const double* qf, const int64_t* qa, const
       idx->have_cand = false;  // rev_* scratch was reused
       idx->launches += 6;
     }
-    CK(idx->qb.ensure(sizeof(uint16_t) * q * idx->m + sizeof(int32_t) * q + 64));
-    int32_t* d_nq = reinterpret_cast<int32_t*>(idx->qb.as<char>() + ((sizeof(uint16_t) * q * idx->m + 15) & ~(size_t)15));
+    const int64_t qpad = (q + 127) / 128 * 128;
+    CK(idx->qb.ensure(sizeof(uint16_t) * qpad * idx->m + sizeof(int32_t) * q + 64));
+    int32_t* d_nq = reinterpret_cast<int32_t*>(idx->qb.as<char>() + sizeof(uint16_t) * qpad * idx->m);
     CKL(sb::launch_bf_tc_prep_queries(idx->qf.as<double>(), q, idx->m, idx->qb.p, d_nq, idx->st));
     // split the node range so that whole waves of CTAs are busy: minimise waves / splits
     const int groups = (int)((q + 127) / 128);
@@ -875,7 +883,7 @@ int sb_bf_topk_queries(sb_index* idx, const double* qf, const int64_t* qa, const
     CK(cudaMemsetAsync(d_unc, 0, sizeof(int), idx->st));
     {
       int32_t* s_nx = idx->fb_norm.as<int32_t>();
-      CKL(sb::launch_bf_tc(idx->fb.p, s_nx, s_nx + 3 * n, s_nx + n, s_nx + 2 * n, idx->qb.p,
+      CKL(sb::launch_bf_tc(idx->fb.p, s_nx, s_nx + 3 * npad, s_nx + npad, s_nx + 2 * npad, idx->qb.p,
                            d_nq, a.qa, a.qmask, n, q, idx->m, idx->l, kk, splits, alpha, a.part_d,
                            a.part_i, idx->st));
     }

@@ -69,8 +69,8 @@ int launch_bf_merge_k(const BfArgs& a, int kout, int64_t* out_ids64, int32_t* ou
                       double* out_dists, int* uncertain, cudaStream_t st);
 
 // tensor-core query-mode top-k for integer data (bf_tc.cu)
-size_t bf_tc_smem(int m, int l);
 int bf_tc_supported(int m, int l, int kk);
+constexpr int kTcNodePad = 256;  // node arrays of the tensor-core path are padded to this
 int launch_tc_attr_range(const int32_t* A, int64_t n, int l, int32_t* lo, int32_t* hi,
                          cudaStream_t st);
 int launch_tc_code(const int32_t* A, int64_t n, int l, const int32_t* lo, const int64_t* stride,
