@@ -125,7 +125,7 @@ struct TcArgs {
   // contiguous, so the epilogue recomputes the attribute factor only when the tuple changes.
   // All node arrays are padded with zeros to a multiple of kTcPad nodes.
   const char* Fb;           // bf16 rows, row-group layout
-  const int32_t* nx;        // |x|^2
+  const int32_t* nx;        // |x|^2 as fp32 bits
   const int32_t* A;         // attributes, n x l
   const int32_t* code;      // attribute-tuple code (equal codes <=> equal tuples)
   const int32_t* orig;      // original node id
@@ -143,28 +143,33 @@ struct TcArgs {
 // One CTA = 128 queries x one node range, 9 warps:
 //   warps 0..7  epilogue: thread (row = tid % 128, half = tid / 128) reads its query's dot
 //               products for half of each tile's columns from TMEM and keeps a top-kk list;
-//   warp 8      producer: one thread bulk-copies tile i (bf16 rows + norms/codes/ids/attrs)
-//               into stage i % 2 and issues the tile's MMAs into accumulator i % 2.
-// Stage i % 2 (shared memory and TMEM columns) is refilled only after all 256 epilogue threads
-// released tile i - 2, so loading and MMA of tile i + 1 overlap the epilogue of tile i.
+//   warp 8      producer: one thread bulk-copies tile i's bf16 rows into B stage i % 2 and its
+//               per-node metadata into meta stage i % 2, and issues the tile's MMAs into TMEM
+//               accumulator i % 2.
+// Barriers per stage s: fullB (rows landed), fullM (metadata landed), done (MMAs complete:
+// accumulator ready and B stage free again), empty (all 256 epilogue threads finished the
+// tile: accumulator and metadata free).  Rows for tile i + 1 load while MMA i runs; MMA i + 1
+// starts as soon as the epilogue leaves tile i - 1.
 __global__ void __launch_bounds__(kTcThreads + 32, 1) bf_tc_kernel(TcArgs a) {
   extern __shared__ __align__(1024) char smem[];
   const int tid = threadIdx.x;
   const int m = a.m, N = a.N, l = a.l;
   const size_t b_bytes = (size_t)N * m * 2;
   const size_t meta_bytes = (size_t)N * (3 + l) * 4;
-  // shared layout: A tile | 2 x (B tile | nx | code | orig | attrs) | lists | t2 | barriers
+  // shared layout: A tile | 2 x B tile | 2 x (nx | code | orig | attrs) | lists | t2 | barriers
   char* p = smem;
   char* sA = p; p += (size_t)kTcM * m * 2;
-  char* stage0 = p; p += 2 * (b_bytes + meta_bytes);
+  char* sB = p; p += 2 * b_bytes;
+  char* sM = p; p += 2 * meta_bytes;
   double* ld = reinterpret_cast<double*>(p); p += sizeof(double) * (size_t)a.kk * kTcThreads;
   uint32_t* li = reinterpret_cast<uint32_t*>(p); p += sizeof(uint32_t) * (size_t)a.kk * kTcThreads;
   volatile float* s_t2 = reinterpret_cast<float*>(p); p += sizeof(float) * kTcThreads;
   p = reinterpret_cast<char*>(((uintptr_t)p + 7) & ~(uintptr_t)7);
-  uint64_t* bars = reinterpret_cast<uint64_t*>(p); p += 8 * 8;  // full[2] done[2] empty[2] a
+  uint64_t* bars = reinterpret_cast<uint64_t*>(p); p += 8 * 10;
   uint32_t* tslot = reinterpret_cast<uint32_t*>(p);
-  const uint32_t bar_full = smem_u32(bars), bar_done = smem_u32(bars + 2),
-                 bar_empty = smem_u32(bars + 4), bar_a = smem_u32(bars + 6);
+  const uint32_t bar_fullB = smem_u32(bars), bar_fullM = smem_u32(bars + 2),
+                 bar_done = smem_u32(bars + 4), bar_empty = smem_u32(bars + 6),
+                 bar_a = smem_u32(bars + 8);
 
   const int64_t q0 = (int64_t)blockIdx.x * kTcM;
   const int64_t tiles = (a.n + N - 1) / N;
@@ -180,19 +185,21 @@ __global__ void __launch_bounds__(kTcThreads + 32, 1) bf_tc_kernel(TcArgs a) {
   }
   if (tid == kTcThreads) {
     for (int s = 0; s < 2; ++s) {
-      mbar_init(bar_full + 8 * s, 1);
+      mbar_init(bar_fullB + 8 * s, 1);
+      mbar_init(bar_fullM + 8 * s, 1);
       mbar_init(bar_done + 8 * s, 1);
       mbar_init(bar_empty + 8 * s, kTcThreads);
     }
     mbar_init(bar_a, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  if (tid < kTcThreads)
+  if (tid < kTcThreads) {
     for (int i = 0; i < a.kk; ++i) {
       ld[i * kTcThreads + tid] = __longlong_as_double(0x7FF0000000000000ll);
       li[i * kTcThreads + tid] = 0xFFFFFFFFu;
     }
-  if (tid < kTcThreads) s_t2[tid] = 3.4e38f;
+    s_t2[tid] = 3.4e38f;
+  }
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -204,26 +211,34 @@ __global__ void __launch_bounds__(kTcThreads + 32, 1) bf_tc_kernel(TcArgs a) {
       const uint32_t a_bytes = (uint32_t)(kTcM * m * 2);
       mbar_expect_tx(bar_a, a_bytes);
       bulk_g2s(smem_u32(sA), a.Qb + (size_t)q0 * m * 2, a_bytes, bar_a);
+      auto load_rows = [&](int i) {
+        const int s = i & 1;
+        const int64_t v0 = (t_begin + i) * (int64_t)N;
+        mbar_expect_tx(bar_fullB + 8 * s, (uint32_t)b_bytes);
+        bulk_g2s(smem_u32(sB + s * b_bytes), a.Fb + (size_t)v0 * m * 2, (uint32_t)b_bytes,
+                 bar_fullB + 8 * s);
+      };
+      if (ntl > 0) load_rows(0);
       mbar_wait(bar_a, 0);
       const uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(N >> 3) << 17) |
                              ((uint32_t)(kTcM >> 4) << 24);
       const uint32_t sbo = (uint32_t)(m / 8) * 128;
       for (int i = 0; i < ntl; ++i) {
         const int s = i & 1;
-        if (i >= 2) mbar_wait(bar_empty + 8 * s, (uint32_t)(((i >> 1) - 1) & 1));
+        const uint32_t ph = (uint32_t)((i >> 1) & 1);
+        // accumulator s and meta stage s: free once the epilogue has left tile i - 2
+        if (i >= 2) mbar_wait(bar_empty + 8 * s, ph ^ 1u);
         const int64_t v0 = (t_begin + i) * (int64_t)N;
-        char* st = stage0 + (size_t)s * (b_bytes + meta_bytes);
-        const uint32_t full = bar_full + 8 * s;
-        mbar_expect_tx(full, (uint32_t)(b_bytes + meta_bytes));
-        bulk_g2s(smem_u32(st), a.Fb + (size_t)v0 * m * 2, (uint32_t)b_bytes, full);
-        char* meta = st + b_bytes;
-        bulk_g2s(smem_u32(meta), a.nx + v0, (uint32_t)(N * 4), full);
-        bulk_g2s(smem_u32(meta + N * 4), a.code + v0, (uint32_t)(N * 4), full);
-        bulk_g2s(smem_u32(meta + N * 8), a.orig + v0, (uint32_t)(N * 4), full);
-        bulk_g2s(smem_u32(meta + N * 12), a.A + v0 * l, (uint32_t)(N * l * 4), full);
-        mbar_wait(full, (uint32_t)((i >> 1) & 1));
+        char* meta = sM + s * meta_bytes;
+        const uint32_t fm = bar_fullM + 8 * s;
+        mbar_expect_tx(fm, (uint32_t)meta_bytes);
+        bulk_g2s(smem_u32(meta), a.nx + v0, (uint32_t)(N * 4), fm);
+        bulk_g2s(smem_u32(meta + N * 4), a.code + v0, (uint32_t)(N * 4), fm);
+        bulk_g2s(smem_u32(meta + N * 8), a.orig + v0, (uint32_t)(N * 4), fm);
+        bulk_g2s(smem_u32(meta + N * 12), a.A + v0 * l, (uint32_t)(N * l * 4), fm);
+        mbar_wait(bar_fullB + 8 * s, ph);
         tc_fence_after();
-        const uint32_t a0 = smem_u32(sA), b0 = smem_u32(st);
+        const uint32_t a0 = smem_u32(sA), b0 = smem_u32(sB + s * b_bytes);
         for (int k = 0; k < m / 16; ++k) {
           uint64_t ad = umma_desc(a0 + (uint32_t)k * 256, 128, sbo);
           uint64_t bd = umma_desc(b0 + (uint32_t)k * 256, 128, sbo);
@@ -234,6 +249,11 @@ __global__ void __launch_bounds__(kTcThreads + 32, 1) bf_tc_kernel(TcArgs a) {
               "l"(ad), "l"(bd), "r"(idesc), "r"(k > 0 ? 1u : 0u));
         }
         mma_commit(bar_done + 8 * s);
+        // rows of tile i + 1 go to B stage s ^ 1, free once MMA i - 1 has completed
+        if (i + 1 < ntl) {
+          if (i >= 1) mbar_wait(bar_done + 8 * (s ^ 1), (uint32_t)(((i - 1) >> 1) & 1));
+          load_rows(i + 1);
+        }
       }
     }
     __syncwarp();
@@ -245,6 +265,7 @@ __global__ void __launch_bounds__(kTcThreads + 32, 1) bf_tc_kernel(TcArgs a) {
     const bool qok = my_q < a.q;
     const double inf = __longlong_as_double(0x7FF0000000000000ll);
     const int32_t my_nq = qok ? a.nq[my_q] : 0;
+    const float nqf = (float)my_nq;
     int32_t qa_row[8];
     int32_t qm_row[8];
 #pragma unroll
@@ -252,43 +273,57 @@ __global__ void __launch_bounds__(kTcThreads + 32, 1) bf_tc_kernel(TcArgs a) {
       qa_row[u] = (qok && u < l) ? (int32_t)a.qa[my_q * l + u] : 0;
       qm_row[u] = (qok && u < l) ? (int32_t)(a.qmask ? a.qmask[my_q * l + u] : 1) : 0;
     }
-    // Conservative fp32 filter: the exact distance is d = sqrt(S) * (1 + sa/alpha), so a node
-    // can beat the list tail T only if S * f^2 <= T^2 with f = 1 + sa * ia, ia <= 1/alpha.
-    // fp32 rounding (< 1e-6 relative) is covered by the 1e-5 slack; survivors are decided in
-    // exact fp64 below.
+    // Conservative fp32 filter.  The exact distance is d = sqrt(S) * (1 + sa/alpha) with
+    // S = |x|^2 + |q|^2 - 2 x.q, so a node can beat the list tail T only if S * f^2 <= T^2
+    // (f = 1 + sa * ia, ia <= 1/alpha), i.e. only if  y = 2 x.q - |x|^2 >= |q|^2 - T^2 / f^2.
+    // t2 = T^2 (1 + 1e-5) and the 8-unit margin cover every fp32 rounding; survivors are
+    // decided in exact integer / fp64 arithmetic below.
     const float ia = __double2float_rd(1.0 / a.alpha);
     float t2 = 3.4e38f;      // own list tail bound
     float t2_eff = 3.4e38f;  // min over both halves of this query
     int last_code = -2, sa = 0;
-    float f2 = 1.0f;
+    float f2 = 1.0f, inv_f2 = 1.0f;
+    float thr = -3.4e38f;    // y threshold for the current tuple and t2_eff
     const int cols = N >> 1;
     const uint32_t lane_base = tmem + ((uint32_t)((warp_id() & 3) * 32) << 16) + (uint32_t)(half * cols);
     for (int i = 0; i < ntl; ++i) {
       const int s = i & 1;
-      const char* meta = stage0 + (size_t)s * (b_bytes + meta_bytes) + b_bytes;
-      const int32_t* s_nx = reinterpret_cast<const int32_t*>(meta);
-      const int32_t* s_code = s_nx + N;
-      const int32_t* s_orig = s_nx + 2 * N;
-      const int32_t* s_at = s_nx + 3 * N;
+      const uint32_t ph = (uint32_t)((i >> 1) & 1);
+      const char* meta = sM + s * meta_bytes;
+      const float* s_nx = reinterpret_cast<const float*>(meta);
+      const int32_t* s_code = reinterpret_cast<const int32_t*>(meta) + N;
+      const int32_t* s_orig = reinterpret_cast<const int32_t*>(meta) + 2 * N;
+      const int32_t* s_at = reinterpret_cast<const int32_t*>(meta) + 3 * N;
       const int64_t vb = (t_begin + i) * (int64_t)N;
       const int nvalid = (int)(a.n - vb < N ? a.n - vb : N);
-      mbar_wait(bar_done + 8 * s, (uint32_t)((i >> 1) & 1));
+      mbar_wait(bar_fullM + 8 * s, ph);
+      mbar_wait(bar_done + 8 * s, ph);
       tc_fence_after();
       for (int c = 0; c < cols / 16; ++c) {
         uint32_t r[16];
         tmem_ld16(lane_base + (uint32_t)(s * N + c * 16), r);
         if (!qok) continue;
         const int c0 = half * cols + c * 16;
-        // columns are in attribute-grouped order: if both ends of the chunk carry the current
-        // tuple, the whole chunk does, and the factor f2 holds for all 16 columns
-        unsigned cand = 0;
-        if (s_code[c0] == last_code && s_code[c0 + 15] == last_code) {
+        float y[16];
+        float mx = -3.4e38f;
 #pragma unroll
-          for (int j = 0; j < 16; ++j) {
-            // S = |x|^2 + |q|^2 - 2 x.q, exact in fp32 (an integer below 2^24)
-            const float Sf = fmaf(-2.0f, __uint_as_float(r[j]), (float)(s_nx[c0 + j] + my_nq));
-            cand |= (Sf * f2 <= t2_eff ? 1u : 0u) << j;
-          }
+        for (int q4 = 0; q4 < 4; ++q4) {
+          const float4 v = *reinterpret_cast<const float4*>(s_nx + c0 + 4 * q4);
+          y[4 * q4 + 0] = fmaf(2.0f, __uint_as_float(r[4 * q4 + 0]), -v.x);
+          y[4 * q4 + 1] = fmaf(2.0f, __uint_as_float(r[4 * q4 + 1]), -v.y);
+          y[4 * q4 + 2] = fmaf(2.0f, __uint_as_float(r[4 * q4 + 2]), -v.z);
+          y[4 * q4 + 3] = fmaf(2.0f, __uint_as_float(r[4 * q4 + 3]), -v.w);
+        }
+#pragma unroll
+        for (int j = 0; j < 16; ++j) mx = fmaxf(mx, y[j]);
+        // columns are in attribute-grouped order: if both ends of the chunk carry the current
+        // tuple, the whole chunk does, and one threshold covers all 16 columns
+        const bool uniform = s_code[c0] == last_code && s_code[c0 + 15] == last_code;
+        if (uniform && mx < thr) continue;
+        unsigned cand = 0;
+        if (uniform) {
+#pragma unroll
+          for (int j = 0; j < 16; ++j) cand |= (y[j] >= thr ? 1u : 0u) << j;
         } else {
           cand = 0xFFFFu;  // mixed chunk: decide column by column below
         }
@@ -307,15 +342,17 @@ __global__ void __launch_bounds__(kTcThreads + 32, 1) bf_tc_kernel(TcArgs a) {
             sa = s2;
             const float f = fmaf((float)sa, ia, 1.0f);
             f2 = f * f;
+            inv_f2 = __frcp_ru(f2);
+            thr = nqf - t2_eff * inv_f2 - 8.0f;
           }
           float rj = 0.f;
 #pragma unroll
           for (int jj = 0; jj < 16; ++jj)
             if (jj == j) rj = __uint_as_float(r[jj]);
-          const float Sf = fmaf(-2.0f, rj, (float)(s_nx[col] + my_nq));
-          if (Sf * f2 > t2_eff) continue;
+          // exact: x.q is an integer below 2^24 held exactly by the fp32 accumulator
+          const int S = (int)s_nx[col] + my_nq - 2 * (int)rj;
+          if ((float)S * f2 > t2_eff) continue;
           // exact fp64 decision (evaluate.py:48-53), ties by original id
-          const int S = (int)Sf;
           const double dist = dmul(sqrt((double)S), dadd(1.0, __ddiv_rn((double)sa, a.alpha)));
           const uint32_t vid = (uint32_t)s_orig[col];
           double wd = ld[(a.kk - 1) * kTcThreads + tid];
@@ -336,17 +373,22 @@ __global__ void __launch_bounds__(kTcThreads + 32, 1) bf_tc_kernel(TcArgs a) {
           if (t < inf) {
             t2 = (float)(t * t * (1.0 + 1e-5));
             t2_eff = fminf(t2_eff, t2);
+            thr = nqf - t2_eff * inv_f2 - 8.0f;
           }
         }
       }
-      // release the stage (shared memory and accumulator) to the producer
+      // release accumulator s and meta stage s to the producer
       tc_fence_before();
       mbar_arrive(bar_empty + 8 * s);
       // share list tails between the two threads of a query: a node beyond the other half's
       // kk-th cannot enter the merged top-kk either, so the tighter bound filters both.  The
       // partner's value may be stale (larger), which only weakens the filter.
       s_t2[tid] = t2;
-      t2_eff = fminf(t2_eff, s_t2[tid ^ kTcM]);
+      const float pt = s_t2[tid ^ kTcM];
+      if (pt < t2_eff) {
+        t2_eff = pt;
+        thr = nqf - t2_eff * inv_f2 - 8.0f;
+      }
     }
     // partial lists out: split index 2 * split + half
     if (qok) {
@@ -369,7 +411,7 @@ __global__ void __launch_bounds__(kTcThreads + 32, 1) bf_tc_kernel(TcArgs a) {
 size_t bf_tc_smem_n(int m, int l, int kk, int N) {
   return (size_t)kTcM * m * 2 + 2 * ((size_t)N * m * 2 + (size_t)N * (3 + l) * 4) +
          (sizeof(double) + sizeof(uint32_t)) * (size_t)kk * kTcThreads + sizeof(float) * kTcThreads +
-         8 + 64 + 16;
+         8 + 80 + 16;
 }
 
 // widest tile (N = 256 or 128 nodes) whose double-buffered stages fit in shared memory; 0 if none
@@ -433,7 +475,7 @@ __global__ void tc_gather_kernel(const float* F, const int32_t* A, const int32_t
   }
   acc = warp_sum(acc);
   if (lane_id() == 0) {
-    nx[p] = acc;
+    nx[p] = __float_as_int((float)acc);  // |x|^2 as fp32 (exact: below 2^24)
     code[p] = code_in[v];
   }
   for (int u = lane_id(); u < l; u += 32) As[p * l + u] = A[v * l + u];
