@@ -138,6 +138,7 @@ struct TcArgs {
   double alpha;
   double* part_d;           // q x (2 splits) x kk
   uint32_t* part_i;
+  int* gthr;                // q: best list-tail bound of the query over all CTAs (fp32 bits)
 };
 
 // One CTA = 128 queries x one node range, 9 warps:
@@ -296,6 +297,8 @@ __global__ void __launch_bounds__(kTcThreads + 32, 1) bf_tc_kernel(TcArgs a) {
       const int32_t* s_at = reinterpret_cast<const int32_t*>(meta) + 3 * N;
       const int64_t vb = (t_begin + i) * (int64_t)N;
       const int nvalid = (int)(a.n - vb < N ? a.n - vb : N);
+      // the query's tightest bound published by any CTA (read now, used after the tile)
+      const float gpre = qok ? __int_as_float(*reinterpret_cast<volatile int*>(a.gthr + my_q)) : 3.4e38f;
       mbar_wait(bar_fullM + 8 * s, ph);
       mbar_wait(bar_done + 8 * s, ph);
       tc_fence_after();
@@ -372,19 +375,23 @@ __global__ void __launch_bounds__(kTcThreads + 32, 1) bf_tc_kernel(TcArgs a) {
           const double t = ld[(a.kk - 1) * kTcThreads + tid];
           if (t < inf) {
             t2 = (float)(t * t * (1.0 + 1e-5));
-            t2_eff = fminf(t2_eff, t2);
-            thr = nqf - t2_eff * inv_f2 - 8.0f;
+            if (t2 < t2_eff) {
+              t2_eff = t2;
+              thr = nqf - t2_eff * inv_f2 - 8.0f;
+              atomicMin(a.gthr + my_q, __float_as_int(t2));  // positive floats order as ints
+            }
           }
         }
       }
       // release accumulator s and meta stage s to the producer
       tc_fence_before();
       mbar_arrive(bar_empty + 8 * s);
-      // share list tails between the two threads of a query: a node beyond the other half's
-      // kk-th cannot enter the merged top-kk either, so the tighter bound filters both.  The
-      // partner's value may be stale (larger), which only weakens the filter.
-      s_t2[tid] = t2;
-      const float pt = s_t2[tid ^ kTcM];
+      // Share list tails between all partial lists of a query (the other column half in
+      // this CTA, the other node ranges in other CTAs): a node beyond any list's kk-th
+      // cannot enter the merged top-kk either, so the tightest bound filters every list.
+      // Stale (larger) values only weaken the filter.
+      s_t2[tid] = t2_eff;
+      const float pt = fminf(s_t2[tid ^ kTcM], gpre);
       if (pt < t2_eff) {
         t2_eff = pt;
         thr = nqf - t2_eff * inv_f2 - 8.0f;
@@ -514,8 +521,9 @@ int launch_bf_tc_prep_queries(const double* qf, int64_t q, int m, void* Qb, int3
 int launch_bf_tc(const void* Fb, const int32_t* nx, const int32_t* A, const int32_t* code,
                  const int32_t* orig, const void* Qb, const int32_t* nq, const int64_t* qa,
                  const int64_t* qmask, int64_t n, int64_t q, int m, int l, int kk, int splits,
-                 double alpha, double* part_d, uint32_t* part_i, cudaStream_t st) {
+                 double alpha, double* part_d, uint32_t* part_i, int* gthr, cudaStream_t st) {
   TcArgs a;
+  a.gthr = gthr;
   a.Fb = (const char*)Fb; a.nx = nx; a.A = A; a.code = code; a.orig = orig;
   a.Qb = (const char*)Qb;
   a.nq = nq; a.qa = qa; a.qmask = qmask; a.n = n; a.q = q; a.m = m; a.l = l; a.kk = kk;

@@ -861,8 +861,10 @@ int sb_bf_topk_queries(sb_index* idx, const double* qf, const int64_t* qa, const
       idx->launches += 6;
     }
     const int64_t qpad = (q + 127) / 128 * 128;
-    CK(idx->qb.ensure(sizeof(uint16_t) * qpad * idx->m + sizeof(int32_t) * q + 64));
+    CK(idx->qb.ensure(sizeof(uint16_t) * qpad * idx->m + 2 * sizeof(int32_t) * q + 64));
     int32_t* d_nq = reinterpret_cast<int32_t*>(idx->qb.as<char>() + sizeof(uint16_t) * qpad * idx->m);
+    int32_t* d_gthr = d_nq + q;  // per-query shared bound, 0x7F7F7F7F = 3.39e38f
+    CK(cudaMemsetAsync(d_gthr, 0x7F, sizeof(int32_t) * q, idx->st));
     CKL(sb::launch_bf_tc_prep_queries(idx->qf.as<double>(), q, idx->m, idx->qb.p, d_nq, idx->st));
     // split the node range so that whole waves of CTAs are busy: minimise waves / splits
     const int groups = (int)((q + 127) / 128);
@@ -885,7 +887,7 @@ int sb_bf_topk_queries(sb_index* idx, const double* qf, const int64_t* qa, const
       int32_t* s_nx = idx->fb_norm.as<int32_t>();
       CKL(sb::launch_bf_tc(idx->fb.p, s_nx, s_nx + 3 * npad, s_nx + npad, s_nx + 2 * npad, idx->qb.p,
                            d_nq, a.qa, a.qmask, n, q, idx->m, idx->l, kk, splits, alpha, a.part_d,
-                           a.part_i, idx->st));
+                           a.part_i, d_gthr, idx->st));
     }
     CKL(sb::launch_bf_merge_k(a, k, idx->out_ids.as<int64_t>(), nullptr, idx->out_dists.as<double>(),
                               d_unc, idx->st));

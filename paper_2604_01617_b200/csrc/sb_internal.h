@@ -85,7 +85,7 @@ int launch_bf_tc_prep_queries(const double* qf, int64_t q, int m, void* Qb, int3
 int launch_bf_tc(const void* Fb, const int32_t* nx, const int32_t* A, const int32_t* code,
                  const int32_t* orig, const void* Qb, const int32_t* nq, const int64_t* qa,
                  const int64_t* qmask, int64_t n, int64_t q, int m, int l, int kk, int splits,
-                 double alpha, double* part_d, uint32_t* part_i, cudaStream_t st);
+                 double alpha, double* part_d, uint32_t* part_i, int* gthr, cudaStream_t st);
 
 // ---- HELP build ---------------------------------------------------------------
 struct BuildScratch {
