@@ -947,21 +947,25 @@ static int route_dev(sb_index* idx, const double* qf, const double* qa, const do
   a.out_dists = out_dists; a.stats = out_stats;
   a.Kpad = next_pow2(k);
   a.Cpad = next_pow2(idx->g);
-  // fp32-exact path for integer data (per query the kernel checks the query and the range)
-  // (measured slower than the fp64 lane-per-row path on cfg 2 at N=1M; opt in with SB_ROUTE_F32=1)
+  // fp32-exact path for integer data (per query the kernel checks the query and the range,
+  // and falls back to the sequential fp64 path): one row per lane by default (SB_ROUTE_LPR > 1
+  // selects the lane-group variant; SB_ROUTE_F32=0 forces fp64)
   const char* f32env = getenv("SB_ROUTE_F32");
-  a.f32_ok = (f32env && atoi(f32env) && idx->int_exact && idx->m % 4 == 0 && !idx->force_sequential) ? 1 : 0;
+  const bool f32_want = f32env ? atoi(f32env) != 0 : true;
+  a.f32_ok = (f32_want && idx->int_exact && idx->m % 4 == 0 && !idx->force_sequential) ? 1 : 0;
   a.flo = idx->flo;
   a.fhi = idx->fhi;
-  a.lpr = std::min(32, next_pow2(std::max(1, idx->m / 4)));
-  if (const char* e = getenv("SB_ROUTE_LPR")) a.lpr = std::max(1, std::min(32, atoi(e)));
+  a.lpr = 1;
+  if (const char* e = getenv("SB_ROUTE_LPR")) a.lpr = std::max(1, std::min(32, next_pow2(atoi(e))));
+  a.pf_rows = 1;
+  if (const char* e = getenv("SB_ROUTE_PF")) a.pf_rows = atoi(e);
   size_t per_warp = sb::route_smem_per_warp(a);
   int wpc_max = 8;
   if (const char* e = getenv("SB_ROUTE_WPC")) wpc_max = std::max(1, std::min(8, atoi(e)));
   int wpc = (int)std::max<size_t>(1, std::min<size_t>(wpc_max, (size_t)(110 * 1024) / per_warp));
   if (per_warp * wpc > 227 * 1024) return fail(SB_EARG, "k too large for the routing kernel");
   int per_sm = 0;
-  CKL(sb::route_occupancy(wpc, per_warp * wpc, &per_sm));
+  CKL(sb::route_occupancy(a, wpc, per_warp * wpc, &per_sm));
   if (per_sm < 1) return fail(SB_EARG, "routing kernel does not fit on an SM for this k");
   int ctas = (int)std::min<int64_t>((int64_t)idx->sms * per_sm, (q + wpc - 1) / wpc);
   int64_t slots = (int64_t)ctas * wpc;

@@ -106,10 +106,44 @@ SB_DEV double finish_pre(const RouteArgs& a, const WarpSmem& w, uint32_t node, c
   return auto_finish(s_v, sa, a.inv_alpha);
 }
 
+// distance path of a route_kernel instance (each instance carries only its own path, plus the
+// generic fp64 path as the per-query fallback of the integer paths)
+enum RouteMode { kModeF64x4 = 0, kModeF32Lane = 1, kModeF32Split = 2, kModeGeneric = 3 };
+
 // Exact distances of rows cid[0..c) -> cd[0..c).
+template <int MODE>
 SB_DEV void eval_rows(const RouteArgs& a, WarpSmem& w, int c, bool f32) {
   const int lane = lane_id();
-  if (f32) {
+  if (MODE == kModeF32Lane && f32) {
+    // integer data, one row per lane: fp32 with four independent accumulators (every
+    // partial sum is an integer below 2^24, so the order is free and the result exact)
+    const int nq = a.m >> 2;
+    const float4* Q4 = reinterpret_cast<const float4*>(w.qs32);
+    for (int j = lane; j < c; j += 32) {
+      const uint32_t v = w.cid[j];
+      const float4* vx = reinterpret_cast<const float4*>(a.F) + (int64_t)v * nq;
+      AttrPre pre;
+      attr_preload(a, v, pre);
+      float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
+      for (int qq = 0; qq < nq; qq += 8) {
+        float4 r[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+          if (qq + u < nq) r[u] = __ldg(vx + qq + u);
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+          if (qq + u < nq) {
+            const float4 qv = Q4[qq + u];
+            const float d0 = r[u].x - qv.x, d1 = r[u].y - qv.y, d2 = r[u].z - qv.z, d3 = r[u].w - qv.w;
+            s0 = fmaf(d0, d0, s0);
+            s1 = fmaf(d1, d1, s1);
+            s2 = fmaf(d2, d2, s2);
+            s3 = fmaf(d3, d3, s3);
+          }
+      }
+      w.cd[j] = finish_pre(a, w, v, pre, (double)((s0 + s1) + (s2 + s3)));
+    }
+  } else if (MODE == kModeF32Split && f32) {
     const int lpr = a.lpr;
     const int rpp = 32 / lpr;
     const int sub = lane & (lpr - 1);
@@ -165,7 +199,7 @@ SB_DEV void eval_rows(const RouteArgs& a, WarpSmem& w, int c, bool f32) {
           if (id[g] != 0xFFFFFFFFu) w.cd[base + grp + rpp * g] = finish_row(a, w, id[g], (double)acc[g]);
       }
     }
-  } else if ((a.m & 3) == 0) {
+  } else if (MODE == kModeF64x4) {
     const int nq = a.m >> 2;
     for (int j = lane; j < c; j += 32) {
       const uint32_t v = w.cid[j];
@@ -252,6 +286,7 @@ SB_HD float fkey_inv(uint32_t k) {
 #ifndef ROUTE_MIN_CTAS
 #define ROUTE_MIN_CTAS 3
 #endif
+template <int MODE>
 __global__ void __launch_bounds__(256, ROUTE_MIN_CTAS) route_kernel(RouteArgs a) {
   extern __shared__ __align__(16) char smem_raw[];
   const int lane = lane_id();
@@ -292,7 +327,7 @@ __global__ void __launch_bounds__(256, ROUTE_MIN_CTAS) route_kernel(RouteArgs a)
     }
     integral = __all_sync(0xffffffffu, integral);
     bool f32 = false;
-    if (a.f32_ok && integral) {
+    if ((MODE == kModeF32Lane || MODE == kModeF32Split) && integral) {
       double dmax = fmax((double)a.fhi - (double)qlo, (double)qhi - (double)a.flo);
       f32 = dmax * dmax * (double)a.m < 16777216.0;  // 2^24
     }
@@ -380,7 +415,17 @@ __global__ void __launch_bounds__(256, ROUTE_MIN_CTAS) route_kernel(RouteArgs a)
         if (half) p1_evals += c;
       }
       __syncwarp();
-      if (c > 0) eval_rows(a, w, c, f32);
+      if (c > 0 && a.pf_rows) {
+        // request every line of the batch's rows at once (L2), so the per-lane row loads
+        // below wait for one memory latency instead of one per 128-byte chunk
+        const int lines = (a.m * 4 + 127) >> 7;
+        for (int t = lane; t < c * lines; t += 32) {
+          const uint32_t v = w.cid[t / lines];
+          const char* p = reinterpret_cast<const char*>(a.F + (int64_t)v * a.m) + (t % lines) * 128;
+          asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
+        }
+      }
+      if (c > 0) eval_rows<MODE>(a, w, c, f32);
       if (stage == 0) {
         for (int t = lane; t < c; t += 32) {
           w.rd[ent_pos + t] = w.cd[t];
@@ -449,21 +494,47 @@ size_t route_smem_per_warp(const RouteArgs& a) {
   return route_warp_smem_bytes_full(a.Kpad, a.Cpad, a.m, a.l);
 }
 
-int launch_route(const RouteArgs& a, int warps_per_cta, int ctas, cudaStream_t st) {
-  size_t smem = route_smem_per_warp(a) * warps_per_cta;
-  cudaError_t e = cudaFuncSetAttribute(route_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       (int)smem);
+template <int MODE>
+static int launch_route_t(const RouteArgs& a, int warps_per_cta, int ctas, size_t smem,
+                          cudaStream_t st) {
+  cudaError_t e = cudaFuncSetAttribute(route_kernel<MODE>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return (int)e;
-  route_kernel<<<ctas, warps_per_cta * 32, smem, st>>>(a);
+  route_kernel<MODE><<<ctas, warps_per_cta * 32, smem, st>>>(a);
   return (int)cudaGetLastError();
 }
 
-int route_occupancy(int warps_per_cta, size_t smem, int* ctas_per_sm) {
-  cudaError_t e = cudaFuncSetAttribute(route_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       (int)smem);
+static int route_mode(const RouteArgs& a) {
+  if (a.f32_ok) return a.lpr == 1 ? kModeF32Lane : kModeF32Split;
+  return (a.m & 3) == 0 ? kModeF64x4 : kModeGeneric;
+}
+
+int launch_route(const RouteArgs& a, int warps_per_cta, int ctas, cudaStream_t st) {
+  size_t smem = route_smem_per_warp(a) * warps_per_cta;
+  switch (route_mode(a)) {
+    case kModeF64x4: return launch_route_t<kModeF64x4>(a, warps_per_cta, ctas, smem, st);
+    case kModeF32Lane: return launch_route_t<kModeF32Lane>(a, warps_per_cta, ctas, smem, st);
+    case kModeF32Split: return launch_route_t<kModeF32Split>(a, warps_per_cta, ctas, smem, st);
+    default: return launch_route_t<kModeGeneric>(a, warps_per_cta, ctas, smem, st);
+  }
+}
+
+template <int MODE>
+static int route_occupancy_t(int warps_per_cta, size_t smem, int* ctas_per_sm) {
+  cudaError_t e = cudaFuncSetAttribute(route_kernel<MODE>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return (int)e;
-  return (int)cudaOccupancyMaxActiveBlocksPerMultiprocessor(ctas_per_sm, route_kernel,
+  return (int)cudaOccupancyMaxActiveBlocksPerMultiprocessor(ctas_per_sm, route_kernel<MODE>,
                                                             warps_per_cta * 32, smem);
+}
+
+int route_occupancy(const RouteArgs& a, int warps_per_cta, size_t smem, int* ctas_per_sm) {
+  switch (route_mode(a)) {
+    case kModeF64x4: return route_occupancy_t<kModeF64x4>(warps_per_cta, smem, ctas_per_sm);
+    case kModeF32Lane: return route_occupancy_t<kModeF32Lane>(warps_per_cta, smem, ctas_per_sm);
+    case kModeF32Split: return route_occupancy_t<kModeF32Split>(warps_per_cta, smem, ctas_per_sm);
+    default: return route_occupancy_t<kModeGeneric>(warps_per_cta, smem, ctas_per_sm);
+  }
 }
 
 // index property: are all features integral, and their range (monotone keys in out[1..2])

@@ -34,12 +34,13 @@ struct RouteArgs {
   int f32_ok;
   float flo, fhi;
   int lpr;
+  int pf_rows;  // prefetch each batch's rows into L2 before evaluating
 };
 
 size_t route_smem_per_warp(const RouteArgs& a);
 int launch_feature_scan(const float* F, int64_t count, unsigned* out3, cudaStream_t st);
 float feature_key_to_float(unsigned k);
-int route_occupancy(int warps_per_cta, size_t smem, int* ctas_per_sm);
+int route_occupancy(const RouteArgs& a, int warps_per_cta, size_t smem, int* ctas_per_sm);
 int launch_route(const RouteArgs& a, int warps_per_cta, int ctas, cudaStream_t st);
 int launch_entry_points(int64_t n, int K, uint64_t seed, int64_t qi0, int64_t q, int64_t* out,
                         int64_t* scratch, uint64_t scratch_slots, cudaStream_t st);

@@ -200,8 +200,10 @@ def test_route_random_graph_vs_oracle():
 
 
 def test_order_free_mode_is_bit_exact():
-    """Integer-valued data routes through the warp-split distance path; it must equal both
-    the sequential path and the oracle bit for bit (ids, fp64 dists, all stats)."""
+    """Integer-valued data routes through the fp32 order-free distance paths (one row per
+    lane by default, lane groups with SB_ROUTE_LPR=8); both, the fp64 lane path
+    (SB_ROUTE_F32=0) and the sequential path must equal the oracle bit for bit (ids, fp64
+    dists, all stats)."""
     rng = np.random.default_rng(3)
     n, m, l, g = 6000, 128, 3, 24
     f = np.clip(np.rint(rng.normal(128, 40, (n, m))), 0, 255).astype(np.float32)
@@ -216,18 +218,28 @@ def test_order_free_mode_is_bit_exact():
     qf = np.clip(np.rint(rng.normal(128, 40, (48, m))), 0, 255).astype(np.float32)
     qa = rng.integers(1, 6, (48, l)).astype(np.int32)
     import os
+    def with_env(env, fn):
+        old = {k: os.environ.get(k) for k in env}
+        os.environ.update(env)
+        try:
+            return fn()
+        finally:
+            for k, v in old.items():
+                if v is None:
+                    del os.environ[k]
+                else:
+                    os.environ[k] = v
     for k in (5, 64, 257):
         p = sb.SearchParams(k=k, seed=2)
-        os.environ["SB_ROUTE_F32"] = "1"   # fp32-exact integer path (opt-in)
-        try:
-            fast = sb.search_batch_arrays(graph, qf, qa, p)
-        finally:
-            del os.environ["SB_ROUTE_F32"]
+        run = lambda: sb.search_batch_arrays(graph, qf, qa, p)
+        lane = run()
+        split = with_env({"SB_ROUTE_LPR": "8"}, run)
+        f64 = with_env({"SB_ROUTE_F32": "0"}, run)
         dev.set_distance_mode(sequential=True)
         seq = sb.search_batch_arrays(graph, qf, qa, p)
         dev.set_distance_mode(sequential=False)
         want = O.search_batch(f, a, ids, cnt, 1.03, qf, qa, k, seed=2)
-        for got in (fast, seq):
+        for got in (lane, split, f64, seq):
             np.testing.assert_array_equal(got[0], want[0])
             np.testing.assert_array_equal(got[1], want[1])
             np.testing.assert_array_equal(got[2][:, :4], want[2])
