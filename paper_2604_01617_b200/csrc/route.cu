@@ -125,22 +125,22 @@ SB_DEV void eval_rows(const RouteArgs& a, WarpSmem& w, int c, bool f32) {
       AttrPre pre;
       attr_preload(a, v, pre);
       float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
-      for (int qq = 0; qq < nq; qq += 8) {
+      auto step = [&](const float4 x, const float4 qv) {
+        const float d0 = x.x - qv.x, d1 = x.y - qv.y, d2 = x.z - qv.z, d3 = x.w - qv.w;
+        s0 = fmaf(d0, d0, s0);
+        s1 = fmaf(d1, d1, s1);
+        s2 = fmaf(d2, d2, s2);
+        s3 = fmaf(d3, d3, s3);
+      };
+      int qq = 0;
+      for (; qq + 8 <= nq; qq += 8) {
         float4 r[8];
 #pragma unroll
-        for (int u = 0; u < 8; ++u)
-          if (qq + u < nq) r[u] = __ldg(vx + qq + u);
+        for (int u = 0; u < 8; ++u) r[u] = __ldg(vx + qq + u);
 #pragma unroll
-        for (int u = 0; u < 8; ++u)
-          if (qq + u < nq) {
-            const float4 qv = Q4[qq + u];
-            const float d0 = r[u].x - qv.x, d1 = r[u].y - qv.y, d2 = r[u].z - qv.z, d3 = r[u].w - qv.w;
-            s0 = fmaf(d0, d0, s0);
-            s1 = fmaf(d1, d1, s1);
-            s2 = fmaf(d2, d2, s2);
-            s3 = fmaf(d3, d3, s3);
-          }
+        for (int u = 0; u < 8; ++u) step(r[u], Q4[qq + u]);
       }
+      for (; qq < nq; ++qq) step(__ldg(vx + qq), Q4[qq]);
       w.cd[j] = finish_pre(a, w, v, pre, (double)((s0 + s1) + (s2 + s3)));
     }
   } else if (MODE == kModeF32Split && f32) {
@@ -207,21 +207,21 @@ SB_DEV void eval_rows(const RouteArgs& a, WarpSmem& w, int c, bool f32) {
       AttrPre pre;
       attr_preload(a, v, pre);
       double s = 0.0;
-      for (int qq = 0; qq < nq; qq += 8) {
+      auto step = [&](const float4 x, const double* qv) {
+        s = sq_step(s, x.x, qv[0]);
+        s = sq_step(s, x.y, qv[1]);
+        s = sq_step(s, x.z, qv[2]);
+        s = sq_step(s, x.w, qv[3]);
+      };
+      int qq = 0;
+      for (; qq + 8 <= nq; qq += 8) {
         float4 r[8];
 #pragma unroll
-        for (int u = 0; u < 8; ++u)
-          if (qq + u < nq) r[u] = __ldg(vx + qq + u);
+        for (int u = 0; u < 8; ++u) r[u] = __ldg(vx + qq + u);
 #pragma unroll
-        for (int u = 0; u < 8; ++u)
-          if (qq + u < nq) {
-            const double* qv = w.qs + 4 * (qq + u);
-            s = sq_step(s, r[u].x, qv[0]);
-            s = sq_step(s, r[u].y, qv[1]);
-            s = sq_step(s, r[u].z, qv[2]);
-            s = sq_step(s, r[u].w, qv[3]);
-          }
+        for (int u = 0; u < 8; ++u) step(r[u], w.qs + 4 * (qq + u));
       }
+      for (; qq < nq; ++qq) step(__ldg(vx + qq), w.qs + 4 * qq);
       w.cd[j] = finish_pre(a, w, v, pre, s);
     }
   } else {
