@@ -604,16 +604,15 @@ static int reinforce_overflow(sb_index* idx, double sigma) {
   a.rec_tgt = reinterpret_cast<int32_t*>(a.rec_next + a.rec_cap);
   CK(cudaMemsetAsync(a.rec_head, 0xFF, sizeof(int64_t) * n, idx->st));
   a.dyn_cap = 1 << 16;
-  size_t sim_bytes = sizeof(uint64_t) * a.dyn_cap + (size_t)(g + 1) * 13 + sizeof(uint32_t) * wmax + 256;
+  a.sim_wmax = (int)wmax;
+  if (g > 255) return fail(SB_EARG, "reinforce: gamma must be below 256");
+  if (sb::rf_simulate_smem(g, (int)wmax) > 227 * 1024)
+    return fail(SB_ECUDA, "reinforce: simulation scratch exceeds shared memory");
+  size_t sim_bytes = sizeof(uint64_t) * a.dyn_cap + 64;
   CK(idx->rf_sim.ensure(sim_bytes));
   char* sp = idx->rf_sim.as<char>();
   a.dyn = reinterpret_cast<uint64_t*>(sp); sp += sizeof(uint64_t) * a.dyn_cap;
-  a.result = reinterpret_cast<int64_t*>(sp); sp += 16;
-  a.sim_d = reinterpret_cast<float*>(sp); sp += sizeof(float) * (g + 1);
-  a.sim_ids = reinterpret_cast<int32_t*>(sp); sp += sizeof(int32_t) * (g + 1);
-  a.sim_u = reinterpret_cast<int32_t*>(sp); sp += sizeof(int32_t) * (g + 1);
-  a.sim_mask = reinterpret_cast<uint32_t*>(sp); sp += sizeof(uint32_t) * wmax;
-  a.sim_keep = reinterpret_cast<uint8_t*>(sp);
+  a.result = reinterpret_cast<int64_t*>(sp);
   CKL(sb::rf_launch_simulate(a, idx->st));
   int64_t res[2] = {0, 0};
   CK(cudaMemcpyAsync(res, a.result, sizeof(res), cudaMemcpyDeviceToHost, idx->st));

@@ -18,6 +18,8 @@
 // in ascending order, and performs exact try_insert semantics on O rows with bit lookups.
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <stdio.h>
+#include <stdlib.h>
 
 #include "common.cuh"
 #include "sb_internal.h"
@@ -241,11 +243,11 @@ __global__ void __launch_bounds__(kRfThreads) rf_bits_kernel(RfArgs a, int dc_ma
 }
 
 // ---------------------------------------------------------------------------------------
-// K7: the sequential simulation (one thread)
-struct Sim {
-  RfArgs a;
-  int err;
-};
+// K7: the sequential simulation, run by one warp.  Events are processed strictly in the
+// reference's order; the warp parallelises the work inside each event (row scans, the
+// merged-list build, in-degree and redundancy-row loads) and keeps the greedy re-prune
+// sequential over list positions.
+constexpr unsigned kFull = 0xFFFFFFFFu;
 
 SB_DEV int u_index(const RfArgs& a, int o, int32_t node) {
   const int32_t* U = a.u_list + a.u_off[o];
@@ -257,85 +259,205 @@ SB_DEV int u_index(const RfArgs& a, int o, int32_t node) {
   return (lo < (int)a.u_size[o] && U[lo] == node) ? lo : -1;
 }
 
+// u_index by 32-way search over U (sorted, u entries): each round probes 32 positions
+SB_DEV int warp_u_index(const int32_t* U, int u, int32_t node) {
+  const int lane = lane_id();
+  int lo = 0, hi = u;  // first position with U[pos] >= node lies in [lo, hi]
+  while (hi - lo > 32) {
+    const int step = (hi - lo + 31) >> 5;
+    const int pk = lo + lane * step;
+    const bool less = pk < hi && U[pk] < node;
+    const int c = __popc(__ballot_sync(kFull, less));
+    if (c == 0) {
+      hi = lo;
+    } else {
+      const int last = lo + (c - 1) * step;
+      const int nxt = lo + c * step;
+      lo = last + 1;
+      if (c < 32 && nxt < hi) hi = nxt;
+    }
+  }
+  const bool less = lo + lane < hi && U[lo + lane] < node;
+  lo += __popc(__ballot_sync(kFull, less));
+  const bool found = lo < u && U[lo] == node;
+  return found ? lo : -1;
+}
+
 SB_DEV int32_t indeg_read(const RfArgs& a, int32_t p, int64_t s) {
   int32_t v = a.in_deg[p];
   if (p < s && !a.is_o[p]) v += a.static_ins[p];
   return v;
 }
 
+// shared scratch of the simulating warp: the merged list of a full row (g + 1 entries) with
+// in-degrees, keep flags and redundancy rows
+struct SimSmem {
+  int32_t* mi;
+  float* md;
+  int32_t* mu;
+  int32_t* midg;
+  uint8_t* mkeep;
+  uint32_t* Rs;
+};
+
+size_t rf_simulate_smem(int g, int wmax) {
+  return (size_t)(g + 1) * (4 * 4 + 1) + 16 + sizeof(uint32_t) * (size_t)(g + 1) * wmax + 64;
+}
+
 // exact _try_insert_edge on O row j (_kernels.py:306-395); returns 1 if inserted
-SB_DEV int sim_try_insert(RfArgs& a, int32_t j, int32_t cand, float d, int64_t s, int* err) {
+// cycle counters of the simulation (build with -DSB_RF_PROF=1, print with env SB_RF_PROF)
+#ifndef SB_RF_PROF
+#define SB_RF_PROF 0
+#endif
+constexpr bool kRfProf = SB_RF_PROF != 0;
+__device__ unsigned long long g_rf_prof[8];
+
+SB_DEV int warp_try_insert(RfArgs& a, const SimSmem& S, int32_t j, int o, int32_t cand,
+                           float d, int64_t s, int& err) {
+  const int lane = lane_id();
+  const long long t_start = clock64();
   const int g = a.g;
-  const int o = a.o_idx[j];
   int32_t* ri = a.ids + (int64_t)j * g;
   float* rd = a.dists + (int64_t)j * g;
   int32_t* ru = a.u_pos + (int64_t)o * g;
+  // one round of independent loads: the row's count, U bounds and the whole row (rows are
+  // allocated gamma wide, so entries past the count are read and masked)
   const int cj = a.counts[j];
-  for (int t = 0; t < cj; ++t)
-    if (ri[t] == cand) return 0;
-  const int cu = u_index(a, o, cand);
-  if (cu < 0) { *err = 1; return 0; }
-  if (cj < g) {
-    int pos = cj;
-    while (pos > 0 && (rd[pos - 1] > d || (rd[pos - 1] == d && ri[pos - 1] > cand))) {
-      ri[pos] = ri[pos - 1]; rd[pos] = rd[pos - 1]; ru[pos] = ru[pos - 1];
-      --pos;
+  const int64_t uoff = a.u_off[o];
+  const int usz = (int)a.u_size[o];
+  int32_t vi[8], vu[8];
+  float vd[8];
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    const int t = lane + 32 * k;
+    if (t < g) { vi[k] = ri[t]; vd[k] = rd[t]; vu[k] = ru[t]; }
+  }
+  // already present?  and the insertion position: entries ordered before (d, cand)
+  bool dup = false;
+  int pos = 0;
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    const int t = lane + 32 * k;
+    bool lt = false;
+    if (t < cj) {
+      dup = dup || vi[k] == cand;
+      lt = vd[k] < d || (vd[k] == d && vi[k] < cand);
     }
-    ri[pos] = cand; rd[pos] = d; ru[pos] = cu;
-    a.counts[j] = cj + 1;
-    a.in_deg[cand] += 1;
+    if (32 * k < g) pos += __popc(__ballot_sync(kFull, lt));
+  }
+  if (__any_sync(kFull, dup)) {
+    if (kRfProf && lane == 0) { atomicAdd(&g_rf_prof[4], (unsigned long long)(clock64() - t_start)); atomicAdd(&g_rf_prof[5], 1ull); }
+    return 0;
+  }
+  const int cu = warp_u_index(a.u_list + uoff, usz, cand);
+  if (cu < 0) {
+    err = 1;
+    return 0;
+  }
+  if (cj < g) {
+    // shift [pos, cj) one slot right from the registers, then place
+    __syncwarp();
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const int t = lane + 32 * k;
+      if (t >= pos && t < cj) { ri[t + 1] = vi[k]; rd[t + 1] = vd[k]; ru[t + 1] = vu[k]; }
+    }
+    if (lane == 0) {
+      ri[pos] = cand; rd[pos] = d; ru[pos] = cu;
+      a.counts[j] = cj + 1;
+      a.in_deg[cand] += 1;
+      if (kRfProf) { atomicAdd(&g_rf_prof[0], (unsigned long long)(clock64() - t_start)); atomicAdd(&g_rf_prof[1], 1ull); }
+    }
+    __syncwarp();
     return 1;
   }
-  // full: merged list of g + 1 in scratch, re-prune under the safeguard
-  int32_t* ti = a.sim_ids;
-  float* td = a.sim_d;
-  int32_t* tu = a.sim_u;
-  uint8_t* keep = a.sim_keep;
-  int pos = cj;
-  for (int t = 0; t < cj; ++t) { ti[t] = ri[t]; td[t] = rd[t]; tu[t] = ru[t]; }
-  while (pos > 0 && (td[pos - 1] > d || (td[pos - 1] == d && ti[pos - 1] > cand))) {
-    ti[pos] = ti[pos - 1]; td[pos] = td[pos - 1]; tu[pos] = tu[pos - 1];
-    --pos;
-  }
-  ti[pos] = cand; td[pos] = d; tu[pos] = cu;
+  // full: merged list of g + 1, re-prune under the safeguard
   const int total = cj + 1;
   const int W = ((int)a.u_size[o] + 31) >> 5;
   const uint32_t* R = a.r_bits + a.r_off[o];
-  uint32_t* km = a.sim_mask;
-  for (int w = 0; w < W; ++w) km[w] = 0u;
-  for (int t = 0; t < total; ++t) keep[t] = 1;
-  km[tu[0] >> 5] |= 1u << (tu[0] & 31);
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    const int t = lane + 32 * k;
+    if (t < cj) {
+      const int dst = t < pos ? t : t + 1;
+      S.mi[dst] = vi[k]; S.md[dst] = vd[k]; S.mu[dst] = vu[k];
+    }
+  }
+  if (lane == 0) { S.mi[pos] = cand; S.md[pos] = d; S.mu[pos] = cu; }
+  __syncwarp();
+  // in-degrees: an entry's in-degree changes in this call only when that entry is dropped,
+  // after which it is never read again, so loading them all up front is exact
+  for (int t = lane; t < total; t += 32) {
+    const int32_t p = S.mi[t];
+    S.midg[t] = p == cand ? 0 : indeg_read(a, p, s);
+    S.mkeep[t] = 1;
+  }
+  for (int e = lane; e < total * W; e += 32) {
+    const int t = e / W, w = e - t * W;
+    S.Rs[e] = R[(int64_t)S.mu[t] * W + w];
+  }
+  __syncwarp();
+  // greedy re-prune in list order; the kept-U mask lives in registers (word lane + 32 k)
+  uint32_t km[4] = {0u, 0u, 0u, 0u};
+  {
+    const int u0 = S.mu[0];
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+      if ((u0 >> 5) == lane + 32 * k) km[k] |= 1u << (u0 & 31);
+  }
   int kept = 1;
   for (int t = 1; t < total; ++t) {
-    const int32_t p = ti[t];
-    const uint32_t* rr = R + (int64_t)tu[t] * W;
-    bool red = false;
-    for (int w = 0; w < W && !red; ++w) red = (rr[w] & km[w]) != 0u;
-    if (red && (p == cand || indeg_read(a, p, s) >= 2)) {
-      keep[t] = 0;
-      if (p != cand) a.in_deg[p] -= 1;
+    const uint32_t* rr = S.Rs + t * W;
+    bool hit = false;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const int w = lane + 32 * k;
+      if (w < W) hit = hit || (rr[w] & km[k]) != 0u;
+    }
+    const bool red = __any_sync(kFull, hit);
+    const int32_t p = S.mi[t];
+    if (red && (p == cand || S.midg[t] >= 2)) {
+      if (lane == 0) S.mkeep[t] = 0;
     } else {
       ++kept;
-      km[tu[t] >> 5] |= 1u << (tu[t] & 31);
+      const int ut = S.mu[t];
+#pragma unroll
+      for (int k = 0; k < 4; ++k)
+        if ((ut >> 5) == lane + 32 * k) km[k] |= 1u << (ut & 31);
     }
   }
-  if (kept > g) {
+  __syncwarp();
+  if (kept > g && lane == 0) {
     for (int t = total - 1; t >= 0; --t) {
-      if (!keep[t]) continue;
-      const int32_t p = ti[t];
-      if (p == cand) { keep[t] = 0; break; }
-      if (indeg_read(a, p, s) >= 2) { keep[t] = 0; a.in_deg[p] -= 1; break; }
+      if (!S.mkeep[t]) continue;
+      const int32_t p = S.mi[t];
+      if (p == cand) { S.mkeep[t] = 0; break; }
+      if (S.midg[t] >= 2) { S.mkeep[t] = 0; break; }
     }
   }
-  int w = 0, inserted = 0;
-  for (int t = 0; t < total; ++t) {
-    if (!keep[t]) continue;
-    ri[w] = ti[t]; rd[w] = td[t]; ru[w] = tu[t];
-    if (ti[t] == cand) inserted = 1;
-    ++w;
+  __syncwarp();
+  // every dropped entry other than the candidate loses one in-degree
+  for (int t = lane; t < total; t += 32)
+    if (!S.mkeep[t] && S.mi[t] != cand) a.in_deg[S.mi[t]] -= 1;
+  int w0 = 0, inserted = 0;
+  for (int t0 = 0; t0 < total; t0 += 32) {
+    const int t = t0 + lane;
+    const bool k = t < total && S.mkeep[t];
+    const unsigned b = __ballot_sync(kFull, k);
+    if (k) {
+      const int dst = w0 + __popc(b & ((1u << lane) - 1u));
+      ri[dst] = S.mi[t]; rd[dst] = S.md[t]; ru[dst] = S.mu[t];
+      if (S.mi[t] == cand) inserted = 1;
+    }
+    w0 += __popc(b);
   }
-  a.counts[j] = w;
-  if (inserted) a.in_deg[cand] += 1;
+  inserted = __any_sync(kFull, inserted) ? 1 : 0;
+  if (lane == 0) {
+    a.counts[j] = w0;
+    if (inserted) a.in_deg[cand] += 1;
+    if (kRfProf) { atomicAdd(&g_rf_prof[2], (unsigned long long)(clock64() - t_start)); atomicAdd(&g_rf_prof[3], 1ull); }
+  }
+  __syncwarp();
   return inserted;
 }
 
@@ -350,73 +472,140 @@ __global__ void rf_init_upos_kernel(RfArgs a) {
 }
 
 __global__ void rf_simulate_kernel(RfArgs a) {
-  if (blockIdx.x != 0 || threadIdx.x != 0) return;
+  extern __shared__ __align__(16) char smem_raw[];
+  if (blockIdx.x != 0) return;
+  const int lane = lane_id();
+  const int g = a.g;
+  SimSmem S;
+  {
+    char* p = smem_raw;
+    S.Rs = reinterpret_cast<uint32_t*>(p); p += sizeof(uint32_t) * (size_t)(g + 1) * a.sim_wmax;
+    S.mi = reinterpret_cast<int32_t*>(p); p += sizeof(int32_t) * (g + 1);
+    S.mu = reinterpret_cast<int32_t*>(p); p += sizeof(int32_t) * (g + 1);
+    S.midg = reinterpret_cast<int32_t*>(p); p += sizeof(int32_t) * (g + 1);
+    S.md = reinterpret_cast<float*>(p); p += sizeof(float) * (g + 1);
+    S.mkeep = reinterpret_cast<uint8_t*>(p);
+  }
   int err = 0;
   int64_t nrec = 0;
-  const int g = a.g;
-  for (int64_t s = 0; s < a.n; ++s) {
-    if (!a.relevant[s]) continue;
-    if (a.is_o[s]) {
+  const long long t_kernel = clock64();
+  const volatile uint8_t* relevant = a.relevant;
+  auto dyn_insert = [&](uint64_t kd, int64_t s) {
+    const int32_t jd = (int32_t)key_id(kd);
+    warp_try_insert(a, S, jd, a.o_idx[jd], (int32_t)s, key_dist(kd), s, err);
+  };
+  for (int64_t base = 0; base < a.n; base += 32) {
+    const int64_t idx = base + lane;
+    unsigned bal = __ballot_sync(kFull, idx < a.n && relevant[idx]);
+    while (bal) {
+      const int64_t s = base + __ffs(bal) - 1;
+      bal &= bal - 1u;
+      if (kRfProf && lane == 0) atomicAdd(&g_rf_prof[7], 1ull);
+      // one round of loads for the source: count, O index, the row (gamma wide, masked by
+      // the count), the head of its recorded mirrors; then the targets' O indices
       const int cs = a.counts[s];
-      for (int t = 0; t < cs; ++t) {
-        if (t >= a.counts[s]) break;
-        const int32_t j = a.ids[s * g + t];
-        const float d = a.dists[s * g + t];
-        if (a.is_o[j]) {
-          sim_try_insert(a, j, (int32_t)s, d, s, &err);
-        } else {
-          uint64_t key = row_key(d, (uint32_t)s);
-          if (row_find_key(a.ids + (int64_t)j * g, a.dists + (int64_t)j * g, a.counts[j], key) < 0) {
-            if (nrec >= a.rec_cap) { err = 2; continue; }
-            a.rec_tgt[nrec] = j;
-            a.rec_key[nrec] = key;
-            a.rec_next[nrec] = a.rec_head[j];
-            a.rec_head[j] = nrec;
-            ++nrec;
-            a.in_deg[s] += 1;
-            if (j > s) a.relevant[j] = 1;
+      const int osrc = a.o_idx[s];
+      int32_t vi[8];
+      float vd[8];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        const int t = lane + 32 * k;
+        if (t < g) { vi[k] = a.ids[s * g + t]; vd[k] = a.dists[s * g + t]; }
+      }
+      const int64_t rh = a.rec_head[s];
+      int oj[8];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        const int t = lane + 32 * k;
+        oj[k] = t < cs ? a.o_idx[vi[k]] : -2;
+      }
+      if (osrc >= 0) {
+        // mirrors into rows that cannot overflow: record each one not already present
+        // (record order = row order); then the O-target events in row order
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          if (32 * k >= cs) break;
+          const bool rec = oj[k] == -1 &&
+                           row_find_key(a.ids + (int64_t)vi[k] * g, a.dists + (int64_t)vi[k] * g,
+                                        a.counts[vi[k]], row_key(vd[k], (uint32_t)s)) < 0;
+          const unsigned rb = __ballot_sync(kFull, rec);
+          if (rec) {
+            const int64_t r = nrec + __popc(rb & ((1u << lane) - 1u));
+            if (r < a.rec_cap) {
+              const int32_t j = vi[k];
+              a.rec_tgt[r] = j;
+              a.rec_key[r] = row_key(vd[k], (uint32_t)s);
+              a.rec_next[r] = a.rec_head[j];
+              a.rec_head[j] = r;
+              if (j > s) a.relevant[j] = 1;
+            } else {
+              err = 2;
+            }
+          }
+          const int64_t room = a.rec_cap - nrec;
+          const int64_t ok = (int64_t)__popc(rb) < room ? (int64_t)__popc(rb) : (room > 0 ? room : 0);
+          nrec += ok;
+          if (lane == 0) a.in_deg[s] += (int32_t)ok;
+        }
+        __syncwarp();
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          if (32 * k >= cs) break;
+          unsigned ob = __ballot_sync(kFull, oj[k] >= 0);
+          while (ob) {
+            const int src = __ffs(ob) - 1;
+            ob &= ob - 1u;
+            warp_try_insert(a, S, __shfl_sync(kFull, vi[k], src), __shfl_sync(kFull, oj[k], src),
+                            (int32_t)s, __shfl_sync(kFull, vd[k], src), s, err);
           }
         }
-      }
-    } else {
-      // O-target events of a non-O row in key order: static entries j in O, plus entries
-      // mirrored in by O sources processed earlier (linked list)
-      int nd = 0;
-      for (int64_t r = a.rec_head[s]; r >= 0; r = a.rec_next[r]) {
-        if (nd < a.dyn_cap) {
-          uint64_t k = row_key(key_dist(a.rec_key[r]), key_id(a.rec_key[r]));
-          int pos = nd;
-          while (pos > 0 && a.dyn[pos - 1] > k) { a.dyn[pos] = a.dyn[pos - 1]; --pos; }
-          a.dyn[pos] = k;
-          ++nd;
-        } else {
-          err = 3;
+        // recorded mirrors may have made later sources of this chunk relevant
+        bal = __ballot_sync(kFull, idx > s && idx < a.n && relevant[idx]);
+      } else {
+        // O-target events of a non-O row in key order: static entries j in O, plus entries
+        // mirrored in by O sources processed earlier (linked list, sorted here)
+        int nd = 0;
+        if (lane == 0) {
+          for (int64_t r = rh; r >= 0; r = a.rec_next[r]) {
+            if (nd < a.dyn_cap) {
+              uint64_t kk = row_key(key_dist(a.rec_key[r]), key_id(a.rec_key[r]));
+              int pos = nd;
+              while (pos > 0 && a.dyn[pos - 1] > kk) { a.dyn[pos] = a.dyn[pos - 1]; --pos; }
+              a.dyn[pos] = kk;
+              ++nd;
+            } else {
+              err = 3;
+            }
+          }
         }
-      }
-      const int cs = a.counts[s];
-      int t = 0, q = 0;
-      while (t < cs || q < nd) {
-        uint64_t ks = kKeyInf;
-        int32_t js = -1;
-        while (t < cs) {
-          js = a.ids[s * g + t];
-          if (a.is_o[js]) { ks = row_key(a.dists[s * g + t], (uint32_t)js); break; }
-          ++t;
+        nd = __shfl_sync(kFull, nd, 0);
+        __syncwarp();
+        int q = 0;
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          if (32 * k >= cs) break;
+          unsigned ob = __ballot_sync(kFull, oj[k] >= 0);
+          while (ob) {
+            const int src = __ffs(ob) - 1;
+            ob &= ob - 1u;
+            const int32_t jj = __shfl_sync(kFull, vi[k], src);
+            const float dd = __shfl_sync(kFull, vd[k], src);
+            const int oo = __shfl_sync(kFull, oj[k], src);
+            const uint64_t ks = row_key(dd, (uint32_t)jj);
+            while (q < nd && a.dyn[q] < ks) dyn_insert(a.dyn[q++], s);
+            warp_try_insert(a, S, jj, oo, (int32_t)s, dd, s, err);
+          }
         }
-        uint64_t kd = q < nd ? a.dyn[q] : kKeyInf;
-        if (ks == kKeyInf && kd == kKeyInf) break;
-        if (ks <= kd) {
-          sim_try_insert(a, js, (int32_t)s, key_dist(ks), s, &err);
-          ++t;
-        } else {
-          sim_try_insert(a, (int32_t)key_id(kd), (int32_t)s, key_dist(kd), s, &err);
-          ++q;
-        }
+        while (q < nd) dyn_insert(a.dyn[q++], s);
       }
     }
   }
-  a.result[0] = nrec;
-  a.result[1] = err;
+  err = __reduce_max_sync(kFull, err);
+  if (lane == 0) {
+    a.result[0] = nrec;
+    a.result[1] = err;
+    if (kRfProf) g_rf_prof[6] = clock64() - t_kernel;
+  }
 }
 
 // K8: per non-O target, merge static (non-O sources, non-mutual) + recorded insertions
@@ -479,7 +668,22 @@ int rf_launch_stage3(RfArgs& a, int upad_max, int dc_max, int upad4_max, size_t 
 }
 
 int rf_launch_simulate(RfArgs& a, cudaStream_t st) {
-  rf_simulate_kernel<<<1, 1, 0, st>>>(a);
+  const size_t smem = rf_simulate_smem(a.g, a.sim_wmax);
+  cudaError_t e = cudaFuncSetAttribute(rf_simulate_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return (int)e;
+  static const bool prof = kRfProf && getenv("SB_RF_PROF") != nullptr;
+  if (prof) {
+    unsigned long long z[8] = {0};
+    cudaMemcpyToSymbol(g_rf_prof, z, sizeof(z));
+  }
+  rf_simulate_kernel<<<1, 32, smem, st>>>(a);
+  if (prof) {
+    unsigned long long z[8];
+    cudaDeviceSynchronize();
+    cudaMemcpyFromSymbol(z, g_rf_prof, sizeof(z));
+    fprintf(stderr, "rf_sim cycles: total %llu | nonfull %llu x%llu | full %llu x%llu | dup %llu x%llu | sources %llu\n",
+            z[6], z[0], z[1], z[2], z[3], z[4], z[5], z[7]);
+  }
   return (int)cudaGetLastError();
 }
 

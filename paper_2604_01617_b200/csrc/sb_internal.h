@@ -216,13 +216,10 @@ struct RfArgs {
   int64_t rec_cap;
   uint64_t* dyn;
   int dyn_cap;
-  int32_t* sim_ids;
-  float* sim_d;
-  int32_t* sim_u;
-  uint8_t* sim_keep;
-  uint32_t* sim_mask;
+  int sim_wmax;         // max redundancy-row words over O rows (simulation scratch size)
   int64_t* result;      // [nrec, err]
 };
+size_t rf_simulate_smem(int g, int wmax);
 int rf_launch_stage1(RfArgs& a, int64_t* oflag, int64_t* oscan, int64_t* scan_tmp, cudaStream_t st);
 int rf_launch_stage2(RfArgs& a, const int64_t* oscan, cudaStream_t st);
 int rf_launch_stage3(RfArgs& a, int upad_max, int dc_max, int upad4_max, size_t bits_smem,
