@@ -161,12 +161,14 @@ def sweep_operating_point(g, cfg, X, A, QX, QA, kcap):
     return kstar, table, gt, gt_s
 
 
-def algorithmic_bytes(st, m, l):
-    """Routing bytes per SURVEY §8(d): evals*(4d+4L) + 4*(expansions + scanned)."""
+def algorithmic_bytes(st, m, l, row_bytes=None, norm_bytes=0):
+    """Routing bytes per SURVEY §8(d): evals*(row + 4L) + 4*(expansions + scanned), with the
+    row as the kernel reads it (4d fp32, or d bytes + a 4-byte norm on the u8 path)."""
+    rb = 4 * m if row_bytes is None else row_bytes
     evals = st[:, 0].astype(np.float64)
     exps = (st[:, 2] + st[:, 3]).astype(np.float64)
     scanned = st[:, 4].astype(np.float64)
-    return float((evals * (4 * m + 4 * l) + 4 * (exps + scanned)).sum())
+    return float((evals * (rb + norm_bytes + 4 * l) + 4 * (exps + scanned)).sum())
 
 
 # ---------------------------------------------------------------------------------------
@@ -262,7 +264,11 @@ def run_mine(args, rank, world, local):
     torch.cuda.synchronize()
     route_ms = r0.elapsed_time(r1) / reps
     st = st_d.cpu().numpy()
+    rinfo = dev.route_info()
+    # §8(d)'s per-evaluation figure counts the fp32 row (4d + 4L); on integer data in [0, 255]
+    # the kernel reads a d-byte u8 row plus a 4-byte norm instead, reported beside it
     abytes = algorithmic_bytes(st, m, l)
+    read_bytes = algorithmic_bytes(st, m, l, rinfo["row_bytes"], 4 if rinfo["path"] == "u8-dp4a" else 0)
     achieved = abytes / (route_ms / 1000.0) / 1e9
     peak, peak_src = measured_hbm_peak()
     traffic = ncu_traffic(args.config)
@@ -316,6 +322,10 @@ def run_mine(args, rank, world, local):
             "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak,
                          "unit": "GB/s", "frac": round(achieved / peak, 4),
                          "traffic": traffic, "kernel": "route_kernel",
+                         "distance_path": rinfo["path"], "row_bytes": rinfo["row_bytes"],
+                         "algorithmic_bytes_def": "SURVEY 8(d): dist_evals*(4d+4L) + 4*(expansions+scanned)",
+                         "bytes_read_per_launch": read_bytes,
+                         "frac_of_bytes_read": round(read_bytes / (route_ms / 1000.0) / 1e9 / peak, 4),
                          "kernel_ms": round(route_ms, 4),
                          "algorithmic_bytes_per_launch": abytes, "peak_source": peak_src,
                          "share_of_step": round(route_ms / ms, 3)},

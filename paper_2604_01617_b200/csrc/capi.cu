@@ -77,6 +77,8 @@ struct sb_index {
   bool force_sequential = false;  // testing: always use the sequential-order distance path
   bool have_fb = false;           // bf16 feature copy + norms for the tensor-core top-k
   bool last_bf_tc = false;        // the last sb_bf_topk_queries ran on tensor cores
+  bool have_f8 = false;           // u8 feature copy for routing (integer data in [0, 255])
+  int last_route_path = -1;
   cudaStream_t own = nullptr, st = nullptr;
   int64_t launches = 0;
   // dataset + adjacency
@@ -96,9 +98,10 @@ struct sb_index {
   DBuf rf_n8, rf_nb, rf_n32, rf_n64, rf_o32, rf_o64, rf_ulist, rf_bits, rf_rec, rf_sim;
   // routing / brute force
   DBuf qf, qa, qm, entries, ent_scratch, out_ids, out_dists, stats, visited, vlog, counter;
-  DBuf bf_part_d, bf_part_i, bf_self, bf_qa, bf_qm, bf_out32, fb, fb_norm, fb_tmp, qb;
+  DBuf bf_part_d, bf_part_i, bf_self, bf_qa, bf_qm, bf_out32, fb, fb_norm, fb_tmp, qb, f8;
   ~sb_index() {
     fb.release();
+    f8.release();
     fb_tmp.release();
     fb_norm.release();
     qb.release();
@@ -202,6 +205,13 @@ int sb_index_info(sb_index* idx, int32_t* int_exact, double* fmax_abs, int32_t* 
   if (last_bf_tc) *last_bf_tc = idx->last_bf_tc ? 1 : 0;
   if (int_exact) *int_exact = idx->int_exact ? 1 : 0;
   if (fmax_abs) *fmax_abs = idx->fmax;
+  return SB_OK;
+}
+
+int sb_route_info(sb_index* idx, int32_t* path, int32_t* row_bytes) {
+  if (!idx) return fail(SB_EARG, "idx is NULL");
+  if (path) *path = idx->last_route_path;
+  if (row_bytes) *row_bytes = idx->last_route_path == 4 ? idx->m : 4 * idx->m;
   return SB_OK;
 }
 
@@ -958,6 +968,29 @@ static int route_dev(sb_index* idx, const double* qf, const double* qa, const do
   if (const char* e = getenv("SB_ROUTE_LPR")) a.lpr = std::max(1, std::min(32, next_pow2(atoi(e))));
   a.pf_rows = 1;
   if (const char* e = getenv("SB_ROUTE_PF")) a.pf_rows = atoi(e);
+  // integer features in [0, 255]: route over a u8 copy with dp4a dot products (exact), unless
+  // SB_ROUTE_U8=0; built once per index
+  a.F8 = nullptr;
+  a.nx8 = nullptr;
+  {
+    const char* u8env = getenv("SB_ROUTE_U8");
+    const bool want = u8env ? atoi(u8env) != 0 : true;
+    if (want && a.f32_ok && idx->flo >= 0.f && idx->fhi <= 255.f && idx->m % 16 == 0 &&
+        idx->m <= 512) {
+      if (!idx->have_f8) {
+        const size_t fbytes = (size_t)n * idx->m;
+        CK(idx->f8.ensure(fbytes + 256 + sizeof(int32_t) * (size_t)n));
+        CKL(sb::launch_pack_u8(idx->F.as<float>(), n, idx->m, idx->f8.as<uint8_t>(),
+                               reinterpret_cast<int32_t*>(idx->f8.as<uint8_t>() + ((fbytes + 255) & ~(size_t)255)),
+                               idx->st));
+        idx->have_f8 = true;
+        idx->launches += 1;
+      }
+      a.F8 = idx->f8.as<uint8_t>();
+      a.nx8 = reinterpret_cast<const int32_t*>(idx->f8.as<uint8_t>() + (((size_t)n * idx->m + 255) & ~(size_t)255));
+    }
+  }
+  idx->last_route_path = sb::route_path(a);
   size_t per_warp = sb::route_smem_per_warp(a);
   int wpc_max = 8;
   if (const char* e = getenv("SB_ROUTE_WPC")) wpc_max = std::max(1, std::min(8, atoi(e)));

@@ -39,6 +39,9 @@ constexpr uint32_t kChkR = 0x80000000u;   // phase-2 checked
 constexpr uint32_t kChkP = 0x40000000u;   // phase-1 (pioneer) checked
 constexpr uint32_t kIdMask = 0x3FFFFFFFu;
 constexpr int kRows = 8;                   // rows per lane group in flight (fp32 path)
+#ifndef ROUTE_F32_CHUNK
+#define ROUTE_F32_CHUNK 8                  // float4 loads in flight per lane (fp32 lane path)
+#endif
 
 struct WarpSmem {
   double* rd;     // Kpad
@@ -108,13 +111,50 @@ SB_DEV double finish_pre(const RouteArgs& a, const WarpSmem& w, uint32_t node, c
 
 // distance path of a route_kernel instance (each instance carries only its own path, plus the
 // generic fp64 path as the per-query fallback of the integer paths)
-enum RouteMode { kModeF64x4 = 0, kModeF32Lane = 1, kModeF32Split = 2, kModeGeneric = 3 };
+enum RouteMode { kModeF64x4 = 0, kModeF32Lane = 1, kModeF32Split = 2, kModeGeneric = 3, kModeU8 = 4 };
 
 // Exact distances of rows cid[0..c) -> cd[0..c).
 template <int MODE>
-SB_DEV void eval_rows(const RouteArgs& a, WarpSmem& w, int c, bool f32) {
+SB_DEV void eval_rows(const RouteArgs& a, WarpSmem& w, int c, bool f32, int nq8) {
   const int lane = lane_id();
-  if (MODE == kModeF32Lane && f32) {
+  if (MODE == kModeU8 && f32) {
+    // features and query are integers in [0, 255]: rows are read from the u8 copy and
+    // S = |x|^2 + |q|^2 - 2 x.q with x.q from byte dot products (dp4a), exact in int32
+    const int n16 = a.m >> 4;
+    const uint4* Q = reinterpret_cast<const uint4*>(w.qs32);
+    for (int j = lane; j < c; j += 32) {
+      const uint32_t v = w.cid[j];
+      const uint4* xr = reinterpret_cast<const uint4*>(a.F8 + (int64_t)v * a.m);
+      AttrPre pre;
+      attr_preload(a, v, pre);
+      const int nxv = __ldg(a.nx8 + v);
+      unsigned acc0 = 0u, acc1 = 0u;
+      int k = 0;
+      for (; k + 8 <= n16; k += 8) {
+        uint4 r[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) r[u] = __ldg(xr + k + u);
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const uint4 q = Q[k + u];
+          acc0 = __dp4a(r[u].x, q.x, acc0);
+          acc1 = __dp4a(r[u].y, q.y, acc1);
+          acc0 = __dp4a(r[u].z, q.z, acc0);
+          acc1 = __dp4a(r[u].w, q.w, acc1);
+        }
+      }
+      for (; k < n16; ++k) {
+        const uint4 r = __ldg(xr + k);
+        const uint4 q = Q[k];
+        acc0 = __dp4a(r.x, q.x, acc0);
+        acc1 = __dp4a(r.y, q.y, acc1);
+        acc0 = __dp4a(r.z, q.z, acc0);
+        acc1 = __dp4a(r.w, q.w, acc1);
+      }
+      const int S = nxv + nq8 - 2 * (int)(acc0 + acc1);
+      w.cd[j] = finish_pre(a, w, v, pre, (double)S);
+    }
+  } else if (MODE == kModeF32Lane && f32) {
     // integer data, one row per lane: fp32 with four independent accumulators (every
     // partial sum is an integer below 2^24, so the order is free and the result exact)
     const int nq = a.m >> 2;
@@ -133,12 +173,12 @@ SB_DEV void eval_rows(const RouteArgs& a, WarpSmem& w, int c, bool f32) {
         s3 = fmaf(d3, d3, s3);
       };
       int qq = 0;
-      for (; qq + 8 <= nq; qq += 8) {
-        float4 r[8];
+      for (; qq + ROUTE_F32_CHUNK <= nq; qq += ROUTE_F32_CHUNK) {
+        float4 r[ROUTE_F32_CHUNK];
 #pragma unroll
-        for (int u = 0; u < 8; ++u) r[u] = __ldg(vx + qq + u);
+        for (int u = 0; u < ROUTE_F32_CHUNK; ++u) r[u] = __ldg(vx + qq + u);
 #pragma unroll
-        for (int u = 0; u < 8; ++u) step(r[u], Q4[qq + u]);
+        for (int u = 0; u < ROUTE_F32_CHUNK; ++u) step(r[u], Q4[qq + u]);
       }
       for (; qq < nq; ++qq) step(__ldg(vx + qq), Q4[qq]);
       w.cd[j] = finish_pre(a, w, v, pre, (double)((s0 + s1) + (s2 + s3)));
@@ -327,9 +367,38 @@ __global__ void __launch_bounds__(256, ROUTE_MIN_CTAS) route_kernel(RouteArgs a)
     }
     integral = __all_sync(0xffffffffu, integral);
     bool f32 = false;
+    int nq8 = 0;
     if ((MODE == kModeF32Lane || MODE == kModeF32Split) && integral) {
       double dmax = fmax((double)a.fhi - (double)qlo, (double)qhi - (double)a.flo);
       f32 = dmax * dmax * (double)a.m < 16777216.0;  // 2^24
+    }
+    if (MODE == kModeU8 && integral && qlo >= 0.f && qhi <= 255.f) {
+      // u8 query over the fp32 copy (the byte array overlays it: every float is read
+      // before this warp's bytes are written, see the __syncwarp)
+      f32 = true;
+      int acc = 0;
+      uint32_t packed[4];
+      const int nw = a.m >> 2;  // 32-bit words of bytes
+      // lane handles words lane, lane + 32, lane + 64, lane + 96: 4 dims each (m <= 512)
+#pragma unroll
+      for (int it = 0; it < 4; ++it) {
+        const int wd = lane + 32 * it;
+        uint32_t b = 0;
+        if (wd < nw) {
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            const int x = (int)w.qs32[4 * wd + e];
+            acc += x * x;
+            b |= (uint32_t)x << (8 * e);
+          }
+        }
+        packed[it] = b;
+      }
+      __syncwarp();
+#pragma unroll
+      for (int it = 0; it < 4; ++it)
+        if (lane + 32 * it < nw) reinterpret_cast<uint32_t*>(w.qs32)[lane + 32 * it] = packed[it];
+      nq8 = warp_sum(acc);
     }
     __syncwarp();
 
@@ -418,14 +487,16 @@ __global__ void __launch_bounds__(256, ROUTE_MIN_CTAS) route_kernel(RouteArgs a)
       if (c > 0 && a.pf_rows) {
         // request every line of the batch's rows at once (L2), so the per-lane row loads
         // below wait for one memory latency instead of one per 128-byte chunk
-        const int lines = (a.m * 4 + 127) >> 7;
+        const int lines = MODE == kModeU8 && f32 ? (a.m + 127) >> 7 : (a.m * 4 + 127) >> 7;
         for (int t = lane; t < c * lines; t += 32) {
           const uint32_t v = w.cid[t / lines];
-          const char* p = reinterpret_cast<const char*>(a.F + (int64_t)v * a.m) + (t % lines) * 128;
+          const char* p = (MODE == kModeU8 && f32)
+                              ? reinterpret_cast<const char*>(a.F8 + (int64_t)v * a.m) + (t % lines) * 128
+                              : reinterpret_cast<const char*>(a.F + (int64_t)v * a.m) + (t % lines) * 128;
           asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
         }
       }
-      if (c > 0) eval_rows<MODE>(a, w, c, f32);
+      if (c > 0) eval_rows<MODE>(a, w, c, f32, nq8);
       if (stage == 0) {
         for (int t = lane; t < c; t += 32) {
           w.rd[ent_pos + t] = w.cd[t];
@@ -505,9 +576,12 @@ static int launch_route_t(const RouteArgs& a, int warps_per_cta, int ctas, size_
 }
 
 static int route_mode(const RouteArgs& a) {
+  if (a.F8) return kModeU8;
   if (a.f32_ok) return a.lpr == 1 ? kModeF32Lane : kModeF32Split;
   return (a.m & 3) == 0 ? kModeF64x4 : kModeGeneric;
 }
+
+int route_path(const RouteArgs& a) { return route_mode(a); }
 
 int launch_route(const RouteArgs& a, int warps_per_cta, int ctas, cudaStream_t st) {
   size_t smem = route_smem_per_warp(a) * warps_per_cta;
@@ -515,6 +589,7 @@ int launch_route(const RouteArgs& a, int warps_per_cta, int ctas, cudaStream_t s
     case kModeF64x4: return launch_route_t<kModeF64x4>(a, warps_per_cta, ctas, smem, st);
     case kModeF32Lane: return launch_route_t<kModeF32Lane>(a, warps_per_cta, ctas, smem, st);
     case kModeF32Split: return launch_route_t<kModeF32Split>(a, warps_per_cta, ctas, smem, st);
+    case kModeU8: return launch_route_t<kModeU8>(a, warps_per_cta, ctas, smem, st);
     default: return launch_route_t<kModeGeneric>(a, warps_per_cta, ctas, smem, st);
   }
 }
@@ -533,8 +608,28 @@ int route_occupancy(const RouteArgs& a, int warps_per_cta, size_t smem, int* cta
     case kModeF64x4: return route_occupancy_t<kModeF64x4>(warps_per_cta, smem, ctas_per_sm);
     case kModeF32Lane: return route_occupancy_t<kModeF32Lane>(warps_per_cta, smem, ctas_per_sm);
     case kModeF32Split: return route_occupancy_t<kModeF32Split>(warps_per_cta, smem, ctas_per_sm);
+    case kModeU8: return route_occupancy_t<kModeU8>(warps_per_cta, smem, ctas_per_sm);
     default: return route_occupancy_t<kModeGeneric>(warps_per_cta, smem, ctas_per_sm);
   }
+}
+
+// u8 copy of integer features in [0, 255] plus exact squared norms (warp per node)
+__global__ void pack_u8_kernel(const float* F, int64_t n, int m, uint8_t* F8, int32_t* nx) {
+  const int64_t v = (int64_t)blockIdx.x * (blockDim.x >> 5) + warp_id();
+  if (v >= n) return;
+  int acc = 0;
+  for (int t = lane_id(); t < m; t += 32) {
+    const int x = (int)F[v * m + t];
+    F8[v * m + t] = (uint8_t)x;
+    acc += x * x;
+  }
+  acc = warp_sum(acc);
+  if (lane_id() == 0) nx[v] = acc;
+}
+
+int launch_pack_u8(const float* F, int64_t n, int m, uint8_t* F8, int32_t* nx, cudaStream_t st) {
+  pack_u8_kernel<<<(unsigned)((n + 7) / 8), 256, 0, st>>>(F, n, m, F8, nx);
+  return (int)cudaGetLastError();
 }
 
 // index property: are all features integral, and their range (monotone keys in out[1..2])

@@ -35,13 +35,18 @@ struct RouteArgs {
   float flo, fhi;
   int lpr;
   int pf_rows;  // prefetch each batch's rows into L2 before evaluating
+  // u8 copy of integer features in [0, 255] (null: not available) and exact |x|^2
+  const uint8_t* F8;
+  const int32_t* nx8;
 };
 
 size_t route_smem_per_warp(const RouteArgs& a);
 int launch_feature_scan(const float* F, int64_t count, unsigned* out3, cudaStream_t st);
+int launch_pack_u8(const float* F, int64_t n, int m, uint8_t* F8, int32_t* nx, cudaStream_t st);
 float feature_key_to_float(unsigned k);
 int route_occupancy(const RouteArgs& a, int warps_per_cta, size_t smem, int* ctas_per_sm);
 int launch_route(const RouteArgs& a, int warps_per_cta, int ctas, cudaStream_t st);
+int route_path(const RouteArgs& a);  // distance path route_kernel takes for these args
 int launch_entry_points(int64_t n, int K, uint64_t seed, int64_t qi0, int64_t q, int64_t* out,
                         int64_t* scratch, uint64_t scratch_slots, cudaStream_t st);
 

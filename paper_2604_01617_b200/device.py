@@ -79,6 +79,14 @@ class DeviceIndex:
                   ctypes.addressof(tc))
         return {"int_exact": bool(ie.value), "fmax_abs": fm.value, "last_bf_tc": bool(tc.value)}
 
+    def route_info(self) -> dict:
+        """Distance path of the last routing launch and the feature bytes it reads per row."""
+        path = ctypes.c_int32(-1)
+        rb = ctypes.c_int32(0)
+        _lib.call("sb_route_info", self._h, ctypes.addressof(path), ctypes.addressof(rb))
+        names = {0: "fp64", 1: "fp32", 2: "fp32-groups", 3: "fp64-generic", 4: "u8-dp4a"}
+        return {"path": names.get(path.value, "none"), "row_bytes": rb.value}
+
     def set_distance_mode(self, sequential: bool):
         _lib.call("sb_set_distance_mode", self._h, 1 if sequential else 0)
 

@@ -200,10 +200,9 @@ def test_route_random_graph_vs_oracle():
 
 
 def test_order_free_mode_is_bit_exact():
-    """Integer-valued data routes through the fp32 order-free distance paths (one row per
-    lane by default, lane groups with SB_ROUTE_LPR=8); both, the fp64 lane path
-    (SB_ROUTE_F32=0) and the sequential path must equal the oracle bit for bit (ids, fp64
-    dists, all stats)."""
+    """Integer-valued data in [0, 255] routes through the u8/dp4a path by default; the fp32
+    order-free paths (one row per lane, lane groups), the fp64 lane path and the sequential
+    path must all equal the oracle bit for bit (ids, fp64 dists, all stats)."""
     rng = np.random.default_rng(3)
     n, m, l, g = 6000, 128, 3, 24
     f = np.clip(np.rint(rng.normal(128, 40, (n, m))), 0, 255).astype(np.float32)
@@ -232,14 +231,18 @@ def test_order_free_mode_is_bit_exact():
     for k in (5, 64, 257):
         p = sb.SearchParams(k=k, seed=2)
         run = lambda: sb.search_batch_arrays(graph, qf, qa, p)
-        lane = run()
-        split = with_env({"SB_ROUTE_LPR": "8"}, run)
+        u8 = run()
+        assert dev.route_info()["path"] == "u8-dp4a"
+        lane = with_env({"SB_ROUTE_U8": "0"}, run)
+        assert dev.route_info()["path"] == "fp32"
+        split = with_env({"SB_ROUTE_U8": "0", "SB_ROUTE_LPR": "8"}, run)
         f64 = with_env({"SB_ROUTE_F32": "0"}, run)
+        assert dev.route_info()["path"] == "fp64"
         dev.set_distance_mode(sequential=True)
         seq = sb.search_batch_arrays(graph, qf, qa, p)
         dev.set_distance_mode(sequential=False)
         want = O.search_batch(f, a, ids, cnt, 1.03, qf, qa, k, seed=2)
-        for got in (lane, split, f64, seq):
+        for got in (u8, lane, split, f64, seq):
             np.testing.assert_array_equal(got[0], want[0])
             np.testing.assert_array_equal(got[1], want[1])
             np.testing.assert_array_equal(got[2][:, :4], want[2])
