@@ -327,3 +327,35 @@ def test_cfg1_end_to_end(cfg1_golden):
     # recall at the operating point K=25 (0.9550)
     ids, _, _ = sb.search_batch_arrays(g, QX, QA, sb.SearchParams(k=25))
     assert sb.mean_recall(ids, gt, 10) == pytest.approx(0.955, abs=1e-9)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("cfg,n,q", [("cfg2", 3000, 40), ("cfg3", 3000, 40), ("cfg4", 1200, 20),
+                                     ("cfg5c10", 3000, 40), ("cfg5c1", 2000, 30)])
+def test_config_recipes_end_to_end(cfg, n, q):
+    """Every BASELINE config recipe (tools/configs.py) at reduced N: the GPU HELP build equals
+    the oracle's graph bit for bit, and GPU routing / exact top-k equal the oracle's."""
+    from tools.configs import make_config
+    X, A, QX, QA, card = make_config(cfg, n)
+    QX, QA = QX[:q], QA[:q]
+    cfg_m = sb.compute_alpha(sb.sample_statistics(X, A, min(1000, n), seed=0), n, A.shape[1])
+    schema = sb.AttributeSchema(tuple(tuple(str(i) for i in range(c)) for c in card))
+    p = sb.BuildParams(gamma=32, gamma_new=32)
+    g = sb.build(X, A, schema, p, cfg_m)
+    og = O.build(X, A, cfg_m.alpha, sigma=p.sigma, gamma=p.gamma, gamma_new=p.gamma_new)
+    np.testing.assert_array_equal(g.nbr_counts, og.nbr_counts)
+    for i in range(n):
+        c = og.nbr_counts[i]
+        np.testing.assert_array_equal(g.nbr_ids[i, :c], og.nbr_ids[i, :c])
+        np.testing.assert_array_equal(g.nbr_dists[i, :c], og.nbr_dists[i, :c])
+    for k in (10, 50):
+        got = sb.search_batch_arrays(g, QX, QA, sb.SearchParams(k=k))
+        want = O.search_batch(X, A, og.nbr_ids, og.nbr_counts, cfg_m.alpha, QX, QA, k)
+        np.testing.assert_array_equal(got[0], want[0])
+        np.testing.assert_array_equal(got[1], want[1])
+        np.testing.assert_array_equal(got[2][:, :4], want[2])
+    ti, td = sb.oracle_auto_topk_batch(X, A, QX, QA, 10, cfg_m, return_dists=True)
+    for i in range(q):
+        wi, wd = O.oracle_auto_topk(X, A, QX[i], QA[i], 10, cfg_m.alpha, return_dists=True)
+        np.testing.assert_array_equal(ti[i], wi)
+        np.testing.assert_array_equal(td[i], wd)

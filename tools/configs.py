@@ -33,4 +33,65 @@ def make_config(name: str, n_override=None):
         QX = draw(q)
         QA = np.stack([rng.integers(1, c + 1, q) for c in (3, 5, 10)], 1).astype(np.int32)
         return X, A, QX, QA, (3, 5, 10)
+    if name == "cfg3":
+        # N=1M, d=96 unit vectors: 512 directions mu_c, x = normalise(kappa mu_c + N(0, I)),
+        # kappa = 8; 1 attribute, code = popularity rank r in 1..1000 with P(r) ~ r^-1.1 (Zipf);
+        # 10k queries drawn the same way.  Euclidean AUTO on unit vectors orders like cosine.
+        rng = np.random.default_rng(0)
+        n = n_override or 1_000_000
+        q = 10_000
+        mu = rng.standard_normal((512, 96))
+        mu /= np.linalg.norm(mu, axis=1, keepdims=True)
+        p = np.arange(1, 1001, dtype=np.float64) ** -1.1
+        p /= p.sum()
+        def draw(cnt):
+            lab = rng.integers(0, 512, cnt)
+            out = np.empty((cnt, 96), np.float32)
+            for b in range(0, cnt, 65536):
+                e = min(cnt, b + 65536)
+                x = 8.0 * mu[lab[b:e]] + rng.standard_normal((e - b, 96))
+                out[b:e] = x / np.linalg.norm(x, axis=1, keepdims=True)
+            return out
+        X = draw(n)
+        A = (rng.choice(1000, size=n, p=p) + 1).astype(np.int32)[:, None]
+        QX = draw(q)
+        QA = (rng.choice(1000, size=q, p=p) + 1).astype(np.int32)[:, None]
+        return X, A, QX, QA, (1000,)
+    if name == "cfg4":
+        # N=1M, d=960 non-negative: Gamma(2, 1) per entry times a per-dimension scale
+        # s_j = exp(U[-1, 1]); 2 attributes uniform over {1, 2} and {1..50}; 1,000 queries.
+        rng = np.random.default_rng(0)
+        n = n_override or 1_000_000
+        q = 1_000
+        s = np.exp(rng.uniform(-1.0, 1.0, 960))
+        def draw(cnt):
+            out = np.empty((cnt, 960), np.float32)
+            for b in range(0, cnt, 16384):
+                e = min(cnt, b + 16384)
+                out[b:e] = rng.gamma(2.0, 1.0, (e - b, 960)) * s
+            return out
+        X = draw(n)
+        A = np.stack([rng.integers(1, c + 1, n) for c in (2, 50)], 1).astype(np.int32)
+        QX = draw(q)
+        QA = np.stack([rng.integers(1, c + 1, q) for c in (2, 50)], 1).astype(np.int32)
+        return X, A, QX, QA, (2, 50)
+    if name.startswith("cfg5"):
+        # N=2M, d=100: N(0, I)_100 @ W with W ~ N(0, 1)^{100x100} (Euclidean AUTO, labelled);
+        # 1 attribute uniform with cardinality from the name (cfg5 = 1000, cfg5c10 = 10, ...)
+        card = int(name[5:].lstrip("c") or 1000) if len(name) > 4 else 1000
+        rng = np.random.default_rng(0)
+        n = n_override or 2_000_000
+        q = 10_000
+        W = rng.standard_normal((100, 100))
+        def draw(cnt):
+            out = np.empty((cnt, 100), np.float32)
+            for b in range(0, cnt, 65536):
+                e = min(cnt, b + 65536)
+                out[b:e] = rng.standard_normal((e - b, 100)) @ W
+            return out
+        X = draw(n)
+        A = rng.integers(1, card + 1, (n, 1)).astype(np.int32)
+        QX = draw(q)
+        QA = rng.integers(1, card + 1, (q, 1)).astype(np.int32)
+        return X, A, QX, QA, (card,)
     raise ValueError(name)
