@@ -60,6 +60,18 @@ int sb_adj_download(sb_index* idx, int32_t* nbr_ids, float* nbr_dists, int32_t* 
  * (graph.py:132-136) of init_random_graph: ids are the host-drawn random neighbours
  * (graph.py:120-129); afterwards the device adjacency is sorted, counts = gamma, flags = 1. */
 int sb_init_graph(sb_index* idx, const int32_t* ids, double inv_alpha);
+/* The random initial rows of graph.py:120-129 drawn on the device: fills the handle's ids with
+ *   rng = default_rng(seed); ids = rng.integers(0, n - 1, (n, gamma)); ids += ids >= arange(n)
+ * bit-exactly.  Reports the 32-bit draws consumed (*consumed32; the 64-bit PCG64 outputs are
+ * ceil(consumed32 / 2), and when consumed32 is odd NumPy keeps the unused high half,
+ * *buffered, in the generator) and the ascending rows that hold a repeated id (*nbad of them,
+ * written to bad_rows when non-NULL and bad_cap suffices).  The host redraws those rows
+ * (graph.py:124-128) from the generator so restored and writes them with sb_set_rows.  Pass
+ * ids = NULL to sb_init_graph to keep the device rows. */
+int sb_init_random_ids(sb_index* idx, uint64_t seed, int64_t* consumed32, uint32_t* buffered,
+                       int64_t* bad_rows, int64_t bad_cap, int64_t* nbad);
+/* overwrite the ids of rows[0..s) (s x gamma, row-major) on the device */
+int sb_set_rows(sb_index* idx, const int64_t* rows, int64_t s, const int32_t* ids);
 
 /* build_candidates (_kernels.py:81-135) on the device adjacency; the new/old lists stay on
  * the device for sb_local_join.  Output pointers may be NULL (download skipped). */

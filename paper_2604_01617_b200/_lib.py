@@ -35,6 +35,8 @@ _SIGS = {
     "sb_adj_upload": [_vp, _vp, _vp, _vp, _vp],
     "sb_adj_download": [_vp, _vp, _vp, _vp, _vp],
     "sb_init_graph": [_vp, _vp, _f64],
+    "sb_init_random_ids": [_vp, _u64, _vp, _vp, _vp, _i64, _vp],
+    "sb_set_rows": [_vp, _vp, _i64, _vp],
     "sb_build_candidates": [_vp, _i32, _vp, _vp, _vp, _vp],
     "sb_set_candidates": [_vp, _i32, _vp, _vp, _vp, _vp],
     "sb_local_join": [_vp, _f64, _vp, _vp],

@@ -253,11 +253,61 @@ __global__ void sb_fill_i32(int32_t* p, int64_t n, int32_t v) {
   if (i < n) p[i] = v;
 }
 
+int sb_init_random_ids(sb_index* idx, uint64_t seed, int64_t* consumed32, uint32_t* buffered,
+                       int64_t* bad_rows, int64_t bad_cap, int64_t* nbad) {
+  if (!idx || !consumed32 || !nbad) return fail(SB_EARG, "NULL argument");
+  const int64_t n = idx->n;
+  const int g = idx->g;
+  if (n <= g) return fail(SB_EARG, "dataset size must exceed gamma");
+  if (n - 1 > (int64_t)0xFFFFFFFF) return fail(SB_EARG, "n too large for the 32-bit draw path");
+  const int64_t slots = sb::init_random_ids_scratch_slots(n, g);
+  CK(idx->seg.ensure(sizeof(int64_t) * (size_t)std::max<int64_t>(slots, n + 4)));
+  int64_t* scratch = idx->seg.as<int64_t>();
+  CK(idx->small.ensure(64));
+  int64_t* d_consumed = reinterpret_cast<int64_t*>(idx->small.as<unsigned long long>() + 2);
+  unsigned long long* d_nbad = idx->small.as<unsigned long long>() + 4;
+  CK(idx->rev_cnt.ensure(sizeof(int64_t) * n));
+  int64_t* d_bad = idx->rev_cnt.as<int64_t>();
+  CKL(sb::launch_init_random_ids(seed, n, g, idx->ids.as<int32_t>(), scratch, slots, d_consumed,
+                                 d_bad, d_nbad, idx->st));
+  int64_t consumed[2] = {-1, 0};
+  unsigned long long nb = 0;
+  CK(cudaMemcpyAsync(consumed, d_consumed, sizeof(consumed), cudaMemcpyDeviceToHost, idx->st));
+  CK(cudaMemcpyAsync(&nb, d_nbad, sizeof(nb), cudaMemcpyDeviceToHost, idx->st));
+  CK(cudaStreamSynchronize(idx->st));
+  if (consumed[0] < 0) return fail(SB_ECUDA, "random init: rejection margin exhausted");
+  *consumed32 = consumed[0];
+  if (buffered) *buffered = (uint32_t)consumed[1];
+  *nbad = (int64_t)nb;
+  if (bad_rows && nb > 0) {
+    if ((int64_t)nb > bad_cap) return fail(SB_EARG, "bad_rows capacity too small");
+    CK(cudaMemcpyAsync(bad_rows, d_bad, sizeof(int64_t) * nb, cudaMemcpyDeviceToHost, idx->st));
+    CK(cudaStreamSynchronize(idx->st));
+    std::sort(bad_rows, bad_rows + nb);
+  }
+  idx->launches += 4;
+  idx->have_cand = false;
+  return SB_OK;
+}
+
+int sb_set_rows(sb_index* idx, const int64_t* rows, int64_t s, const int32_t* ids) {
+  if (!idx || (s > 0 && (!rows || !ids))) return fail(SB_EARG, "NULL argument");
+  const int g = idx->g;
+  for (int64_t i = 0; i < s; ++i) {
+    if (rows[i] < 0 || rows[i] >= idx->n) return fail(SB_EARG, "row out of range");
+    CK(cudaMemcpyAsync(idx->ids.as<int32_t>() + rows[i] * g, ids + i * g, sizeof(int32_t) * g,
+                       cudaMemcpyHostToDevice, idx->st));
+  }
+  CK(cudaStreamSynchronize(idx->st));
+  idx->have_cand = false;
+  return SB_OK;
+}
+
 int sb_init_graph(sb_index* idx, const int32_t* ids, double inv_alpha) {
-  if (!idx || !ids) return fail(SB_EARG, "NULL argument");
+  if (!idx) return fail(SB_EARG, "NULL argument");
   if (idx->n <= idx->g) return fail(SB_EARG, "dataset size must exceed gamma");
   size_t adj = (size_t)idx->n * idx->g;
-  CK(cudaMemcpyAsync(idx->ids.p, ids, adj * 4, cudaMemcpyHostToDevice, idx->st));
+  if (ids) CK(cudaMemcpyAsync(idx->ids.p, ids, adj * 4, cudaMemcpyHostToDevice, idx->st));
   CKL(sb::launch_init_dists(idx->F.as<float>(), idx->A.as<int32_t>(), idx->n, idx->m, idx->l,
                             idx->g, inv_alpha, idx->ids.as<int32_t>(), idx->dists.as<float>(),
                             idx->st));

@@ -94,6 +94,12 @@ int launch_bf_tc(const void* Fb, const int32_t* nx, const int32_t* A, const int3
                  double alpha, double* part_d, uint32_t* part_i, int* gthr, cudaStream_t st);
 
 // ---- HELP build ---------------------------------------------------------------
+// random initial rows (help_init.cu): device ids, consumed PCG64 outputs, rows with repeats
+int launch_init_random_ids(uint64_t seed, int64_t n, int g, int32_t* ids, int64_t* scratch,
+                           int64_t scratch_slots, int64_t* consumed, int64_t* bad,
+                           unsigned long long* nbad, cudaStream_t st);
+int64_t init_random_ids_scratch_slots(int64_t n, int g);
+
 struct BuildScratch {
   int32_t* fwd_new;   // n
   int32_t* fwd_old;   // n

@@ -91,9 +91,31 @@ class DeviceIndex:
         _lib.call("sb_set_distance_mode", self._h, 1 if sequential else 0)
 
     # ---- HELP build ------------------------------------------------------------------
-    def init_graph(self, ids: np.ndarray, inv_alpha: float):
-        ids = c64(ids, np.int32)
+    def init_graph(self, ids, inv_alpha: float):
+        """Initial distances/flags/counts; ids = None keeps the rows already on the device."""
+        ids = None if ids is None else c64(ids, np.int32)
         _lib.call("sb_init_graph", self._h, ptr(ids), float(inv_alpha))
+
+    def init_random_ids(self, seed: int):
+        """graph.py:120-123 on the device; returns (32-bit draws consumed, the buffered high
+        half NumPy keeps when that count is odd, rows to redraw)."""
+        consumed = ctypes.c_int64(0)
+        buf = ctypes.c_uint32(0)
+        nbad = ctypes.c_int64(0)
+        _lib.call("sb_init_random_ids", self._h, int(seed), ctypes.addressof(consumed),
+                  ctypes.addressof(buf), None, 0, ctypes.addressof(nbad))
+        bad = np.empty(max(1, nbad.value), np.int64)
+        if nbad.value:
+            _lib.call("sb_init_random_ids", self._h, int(seed), ctypes.addressof(consumed),
+                      ctypes.addressof(buf), ptr(bad), bad.shape[0], ctypes.addressof(nbad))
+        return consumed.value, buf.value, bad[: nbad.value]
+
+    def set_rows(self, rows: np.ndarray, ids: np.ndarray):
+        rows = c64(rows, np.int64)
+        ids = c64(ids, np.int32)
+        if ids.shape != (rows.shape[0], self.gamma):
+            raise ValueError("ids must be len(rows) x gamma")
+        _lib.call("sb_set_rows", self._h, ptr(rows), rows.shape[0], ptr(ids))
 
     def build_candidates(self, gamma_new: int, download=False):
         if not download:

@@ -145,6 +145,34 @@ def init_random_ids(n: int, gamma: int, seed: int) -> np.ndarray:
     return ids.astype(np.int32)
 
 
+def restored_generator(seed: int, consumed32: int, buffered: int) -> np.random.Generator:
+    """default_rng(seed) after `consumed32` 32-bit draws: PCG64 advanced past ceil(c / 2)
+    outputs, with the unused high half of the last one buffered when c is odd (NumPy's
+    has_uint32 / uinteger)."""
+    rng = np.random.default_rng(seed)
+    rng.bit_generator.advance((consumed32 + 1) // 2)
+    if consumed32 % 2:
+        st = rng.bit_generator.state
+        st["has_uint32"] = 1
+        st["uinteger"] = int(buffered)
+        rng.bit_generator.state = st
+    return rng
+
+
+def init_random_rows_device(dev: DeviceIndex, n: int, gamma: int, seed: int) -> None:
+    """init_random_ids with the bulk draw on the device (bit-identical): the device fills the
+    rows and reports how many PCG64 outputs it consumed; rows with a repeated id are redrawn
+    here from the same generator advanced past those outputs, in ascending row order."""
+    consumed32, buffered, bad = dev.init_random_ids(seed)
+    if bad.size:
+        rng = restored_generator(seed, consumed32, buffered)
+        rows = np.empty((bad.size, gamma), np.int32)
+        for j, i in enumerate(bad):
+            pick = rng.choice(n - 1, size=gamma, replace=False)
+            rows[j] = pick + (pick >= i)
+        dev.set_rows(bad, rows)
+
+
 def _quality_sample(n: int, params: BuildParams) -> np.ndarray:
     rng = np.random.default_rng(params.seed + 1)
     size = min(params.quality_sample, n)
@@ -172,9 +200,10 @@ def init_random_graph(features, attrs, schema, params: BuildParams, metric: Metr
     g = params.gamma
     if n <= g:
         raise ValueError(f"dataset size {n} must exceed gamma {g}; use a smaller gamma")
-    ids = init_random_ids(n, g, params.seed)
     dev = DeviceIndex(features, attrs, g)
-    dev.init_graph(ids, 1.0 / metric.alpha)
+    init_random_rows_device(dev, n, g, params.seed)
+    dev.init_graph(None, 1.0 / metric.alpha)
+    ids = np.empty((n, g), np.int32)  # filled by _pull
     graph = RelationGraph(features=features, attrs=attrs, schema=schema, metric=metric,
                           sigma=params.sigma, nbr_ids=ids, nbr_dists=np.empty((n, g), np.float32),
                           nbr_counts=np.full(n, g, np.int32), nbr_flags=np.ones((n, g), np.uint8),

@@ -8,6 +8,7 @@ import pytest
 
 from paper_2604_01617_b200 import _kernels as G
 from oracle import oracle as O
+from paper_2604_01617_b200.device import DeviceIndex
 
 pytestmark = pytest.mark.gpu
 
@@ -130,3 +131,35 @@ def test_bf_and_route_shim(small_golden):
             np.testing.assert_array_equal(got[0], want[0])
             np.testing.assert_array_equal(got[1], want[1])
             assert got[2:] == want[2:]
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("n,g,seed", [(150, 100, 0), (2000, 64, 3), (50000, 100, 7), (300, 256, 1)])
+def test_device_random_init_equals_numpy(n, g, seed):
+    """sb_init_random_ids + host redraw of repeated rows == init_random_ids (graph.py:120-129),
+    and the reported consumption leaves the generator exactly where NumPy's draw does."""
+    from paper_2604_01617_b200.graph import init_random_ids, init_random_rows_device
+    rng = np.random.default_rng(seed)
+    f = rng.standard_normal((n, 4)).astype(np.float32)
+    a = np.ones((n, 1), np.int32)
+    dev = DeviceIndex(f, a, g)
+    from paper_2604_01617_b200.graph import restored_generator
+    consumed32, buffered, bad = dev.init_random_ids(seed)
+    ref = np.random.default_rng(seed)
+    ref.integers(0, n - 1, size=(n, g), dtype=np.int64)
+    mine = restored_generator(seed, consumed32, buffered)
+    rs, ms = ref.bit_generator.state, mine.bit_generator.state
+    assert rs["state"] == ms["state"] and rs["has_uint32"] == ms["has_uint32"]
+    if rs["has_uint32"]:
+        assert rs["uinteger"] == ms["uinteger"]
+    np.testing.assert_array_equal(ref.integers(0, 1 << 40, 64), mine.integers(0, 1 << 40, 64))
+    np.testing.assert_array_equal(ref.choice(n - 1, 7, replace=False), mine.choice(n - 1, 7, replace=False))
+    init_random_rows_device(dev, n, g, seed)
+    host = init_random_ids(n, g, seed)
+    np.testing.assert_array_equal(dev.download(with_flags=False)[0], host)
+    # the initial rows built from the device ids equal those built from the host ids
+    dev.init_graph(None, 1.0)
+    ref_dev = DeviceIndex(f, a, g)
+    ref_dev.init_graph(host, 1.0)
+    for x, y in zip(dev.download(), ref_dev.download()):
+        np.testing.assert_array_equal(x, y)
