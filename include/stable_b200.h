@@ -164,6 +164,11 @@ int sb_set_distance_mode(sb_index* idx, int32_t mode);
  * 1 fp32 rows (integer data), 2 fp32 lane groups, 3 fp64 generic, 4 u8 rows with dp4a (integer
  * data in [0, 255]); *row_bytes = bytes read per feature row evaluated */
 int sb_route_info(sb_index* idx, int32_t* path, int32_t* row_bytes);
+/* Prepare the routing layout now instead of at the first routing call: the nodes renumbered
+ * along a locality order (features, attributes and adjacency permuted; results, entries and
+ * distance ties still use the original ids, so routing output is unchanged) and, for
+ * integer data in [0, 255], the u8 feature copy.  SB_ROUTE_RELABEL=0 disables the layout. */
+int sb_route_prepare(sb_index* idx);
 
 #ifdef __cplusplus
 }

@@ -58,6 +58,7 @@ _SIGS = {
     "sb_index_info": [_vp, _vp, _vp, _vp],
     "sb_set_distance_mode": [_vp, _i32],
     "sb_route_info": [_vp, _vp, _vp],
+    "sb_route_prepare": [_vp],
 }
 _RESTYPE = {"sb_last_error": ctypes.c_char_p, "sb_launch_count": ctypes.c_int64}
 

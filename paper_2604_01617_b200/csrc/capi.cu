@@ -78,6 +78,10 @@ struct sb_index {
   bool have_fb = false;           // bf16 feature copy + norms for the tensor-core top-k
   bool last_bf_tc = false;        // the last sb_bf_topk_queries ran on tensor cores
   bool have_f8 = false;           // u8 feature copy for routing (integer data in [0, 255])
+  // routing layout: nodes renumbered in a locality order (route_layout); valid while
+  // rl_version == graph_version (every call that changes the adjacency bumps graph_version)
+  int64_t graph_version = 0, rl_version = -1;
+  bool rl_have_f8 = false;
   int last_route_path = -1;
   cudaStream_t own = nullptr, st = nullptr;
   int64_t launches = 0;
@@ -99,9 +103,12 @@ struct sb_index {
   // routing / brute force
   DBuf qf, qa, qm, entries, ent_scratch, out_ids, out_dists, stats, visited, vlog, counter;
   DBuf bf_part_d, bf_part_i, bf_self, bf_qa, bf_qm, bf_out32, fb, fb_norm, fb_tmp, qb, f8;
+  DBuf rl_F, rl_A, rl_ids, rl_counts, rl_perm, rl_f8, rl_tmp;
   ~sb_index() {
     fb.release();
     f8.release();
+    DBuf* rl[] = {&rl_F, &rl_A, &rl_ids, &rl_counts, &rl_perm, &rl_f8, &rl_tmp};
+    for (DBuf* b : rl) b->release();
     fb_tmp.release();
     fb_norm.release();
     qb.release();
@@ -224,6 +231,7 @@ int sb_set_distance_mode(sb_index* idx, int32_t mode) {
 
 int sb_adj_upload(sb_index* idx, const int32_t* ids, const float* dists, const int32_t* counts,
                   const uint8_t* flags) {
+  if (idx) idx->graph_version++;
   if (!idx || !ids || !dists || !counts) return fail(SB_EARG, "NULL argument");
   size_t adj = (size_t)idx->n * idx->g;
   CK(cudaMemcpyAsync(idx->ids.p, ids, adj * 4, cudaMemcpyHostToDevice, idx->st));
@@ -255,6 +263,7 @@ __global__ void sb_fill_i32(int32_t* p, int64_t n, int32_t v) {
 
 int sb_init_random_ids(sb_index* idx, uint64_t seed, int64_t* consumed32, uint32_t* buffered,
                        int64_t* bad_rows, int64_t bad_cap, int64_t* nbad) {
+  if (idx) idx->graph_version++;
   if (!idx || !consumed32 || !nbad) return fail(SB_EARG, "NULL argument");
   const int64_t n = idx->n;
   const int g = idx->g;
@@ -291,6 +300,7 @@ int sb_init_random_ids(sb_index* idx, uint64_t seed, int64_t* consumed32, uint32
 }
 
 int sb_set_rows(sb_index* idx, const int64_t* rows, int64_t s, const int32_t* ids) {
+  if (idx) idx->graph_version++;
   if (!idx || (s > 0 && (!rows || !ids))) return fail(SB_EARG, "NULL argument");
   const int g = idx->g;
   for (int64_t i = 0; i < s; ++i) {
@@ -304,6 +314,7 @@ int sb_set_rows(sb_index* idx, const int64_t* rows, int64_t s, const int32_t* id
 }
 
 int sb_init_graph(sb_index* idx, const int32_t* ids, double inv_alpha) {
+  if (idx) idx->graph_version++;
   if (!idx) return fail(SB_EARG, "NULL argument");
   if (idx->n <= idx->g) return fail(SB_EARG, "dataset size must exceed gamma");
   size_t adj = (size_t)idx->n * idx->g;
@@ -382,6 +393,7 @@ int sb_set_candidates(sb_index* idx, int32_t gamma_new, const int32_t* new_cand,
 }
 
 int sb_local_join(sb_index* idx, double inv_alpha, int64_t* inserted_out, int64_t* pairs_out) {
+  if (idx) idx->graph_version++;
   if (!idx) return fail(SB_EARG, "idx is NULL");
   if (!idx->have_cand) return fail(SB_EARG, "sb_build_candidates must run first");
   const int64_t n = idx->n;
@@ -542,6 +554,7 @@ int sb_get_rows(sb_index* idx, const int64_t* rows, int64_t s, int32_t* ids, int
 }
 
 int sb_prune(sb_index* idx, double sigma, int32_t* rounds_out) {
+  if (idx) idx->graph_version++;
   if (!idx) return fail(SB_EARG, "idx is NULL");
   const int64_t n = idx->n;
   const int g = idx->g, W = (g + 31) / 32;
@@ -759,11 +772,13 @@ static int reconnect_sweep(sb_index* idx, double sigma, int* ran) {
 }
 
 int sb_reinforce_pass(sb_index* idx, double sigma, int64_t* overflow_rows) {
+  if (idx) idx->graph_version++;
   if (!idx) return fail(SB_EARG, "idx is NULL");
   return reinforce_pass(idx, sigma, overflow_rows);
 }
 
 int sb_reconnect_islands(sb_index* idx, double sigma, int32_t* ran) {
+  if (idx) idx->graph_version++;
   if (!idx) return fail(SB_EARG, "idx is NULL");
   int r = 0;
   int rc = reconnect_sweep(idx, sigma, &r);
@@ -772,6 +787,7 @@ int sb_reconnect_islands(sb_index* idx, double sigma, int32_t* ran) {
 }
 
 int sb_reinforce(sb_index* idx, double sigma, int64_t* overflow_rows, int32_t* sweeps_out) {
+  if (idx) idx->graph_version++;
   if (!idx) return fail(SB_EARG, "idx is NULL");
   int r = reinforce_pass(idx, sigma, overflow_rows);
   if (r) return r;
@@ -975,6 +991,79 @@ int sb_entry_points(int64_t n, int32_t k, uint64_t seed, int64_t qi0, int64_t q,
   return SB_OK;
 }
 
+// The routing layout (route.cu "routing layout"): a locality order of the nodes and the
+// features, attributes and adjacency renumbered into it.  Rebuilt when the adjacency changed.
+static bool relabel_enabled() {
+  const char* e = getenv("SB_ROUTE_RELABEL");
+  return e ? atoi(e) != 0 : true;
+}
+
+static int route_layout(sb_index* idx) {
+  if (idx->rl_version == idx->graph_version) return SB_OK;
+  const int64_t n = idx->n;
+  const int m = idx->m, l = idx->l, g = idx->g;
+  CK(idx->rl_perm.ensure(sizeof(int32_t) * 2 * (size_t)n));
+  int32_t* perm = idx->rl_perm.as<int32_t>();
+  int32_t* inv = perm + n;
+  const size_t sb_bytes = sb::route_order_scratch_bytes(n);
+  CK(idx->rl_tmp.ensure(sb_bytes));
+  CKL(sb::launch_route_order(idx->F.as<float>(), n, m, perm, inv, idx->rl_tmp.p, sb_bytes, idx->st));
+  CK(idx->rl_F.ensure(sizeof(float) * (size_t)n * m));
+  CK(idx->rl_A.ensure(sizeof(int32_t) * (size_t)n * l));
+  CK(idx->rl_ids.ensure(sizeof(int32_t) * (size_t)n * g));
+  CK(idx->rl_counts.ensure(sizeof(int32_t) * (size_t)n));
+  CKL(sb::launch_permute_rows_f32(idx->F.as<float>(), n, m, perm, idx->rl_F.as<float>(), idx->st));
+  CKL(sb::launch_permute_rows_i32(idx->A.as<int32_t>(), n, l, perm, idx->rl_A.as<int32_t>(), idx->st));
+  CKL(sb::launch_relabel_adjacency(idx->ids.as<int32_t>(), idx->counts.as<int32_t>(), n, g, perm, inv,
+                                   idx->rl_ids.as<int32_t>(), idx->rl_counts.as<int32_t>(), idx->st));
+  idx->rl_tmp.release();
+  idx->rl_have_f8 = false;
+  idx->rl_version = idx->graph_version;
+  idx->launches += 7;
+  return SB_OK;
+}
+
+// u8 copy (+ exact norms) of `F` into `buf` once; returns the norms pointer
+static int ensure_u8(sb_index* idx, const float* F, DBuf& buf, bool& have) {
+  const int64_t n = idx->n;
+  const size_t fbytes = (size_t)n * idx->m;
+  if (!have) {
+    CK(buf.ensure(fbytes + 256 + sizeof(int32_t) * (size_t)n));
+    CKL(sb::launch_pack_u8(F, n, idx->m, buf.as<uint8_t>(),
+                           reinterpret_cast<int32_t*>(buf.as<uint8_t>() + ((fbytes + 255) & ~(size_t)255)),
+                           idx->st));
+    have = true;
+    idx->launches += 1;
+  }
+  return SB_OK;
+}
+
+static bool u8_eligible(const sb_index* idx) {
+  const char* f32env = getenv("SB_ROUTE_F32");
+  const bool f32_want = f32env ? atoi(f32env) != 0 : true;
+  const char* u8env = getenv("SB_ROUTE_U8");
+  const bool want = u8env ? atoi(u8env) != 0 : true;
+  return want && f32_want && idx->int_exact && !idx->force_sequential && idx->flo >= 0.f &&
+         idx->fhi <= 255.f && idx->m % 16 == 0 && idx->m <= 512;
+}
+
+int sb_route_prepare(sb_index* idx) {
+  if (!idx) return fail(SB_EARG, "idx is NULL");
+  if (relabel_enabled()) {
+    int r = route_layout(idx);
+    if (r) return r;
+    if (u8_eligible(idx)) {
+      r = ensure_u8(idx, idx->rl_F.as<float>(), idx->rl_f8, idx->rl_have_f8);
+      if (r) return r;
+    }
+  } else if (u8_eligible(idx)) {
+    int r = ensure_u8(idx, idx->F.as<float>(), idx->f8, idx->have_f8);
+    if (r) return r;
+  }
+  CK(cudaStreamSynchronize(idx->st));
+  return SB_OK;
+}
+
 static int route_dev(sb_index* idx, const double* qf, const double* qa, const double* qm, int64_t q,
                      int32_t k, int32_t p, int32_t use_coarse, const int64_t* entries,
                      uint64_t seed, int64_t qi0, double inv_alpha, int64_t* out_ids,
@@ -999,8 +1088,21 @@ static int route_dev(sb_index* idx, const double* qf, const double* qa, const do
     entries = idx->entries.as<int64_t>();
   }
   sb::RouteArgs a;
-  a.F = idx->F.as<float>(); a.A = idx->A.as<int32_t>(); a.nbr_ids = idx->ids.as<int32_t>();
-  a.nbr_counts = idx->counts.as<int32_t>(); a.n = n; a.m = idx->m; a.l = idx->l; a.g = idx->g;
+  const bool relabel = relabel_enabled();
+  if (relabel) {
+    int r = route_layout(idx);
+    if (r) return r;
+    a.F = idx->rl_F.as<float>(); a.A = idx->rl_A.as<int32_t>(); a.nbr_ids = idx->rl_ids.as<int32_t>();
+    a.nbr_counts = idx->rl_counts.as<int32_t>();
+    a.perm = idx->rl_perm.as<int32_t>();
+    a.inv = a.perm + n;
+  } else {
+    a.F = idx->F.as<float>(); a.A = idx->A.as<int32_t>(); a.nbr_ids = idx->ids.as<int32_t>();
+    a.nbr_counts = idx->counts.as<int32_t>();
+    a.perm = nullptr;
+    a.inv = nullptr;
+  }
+  a.n = n; a.m = idx->m; a.l = idx->l; a.g = idx->g;
   a.qf = qf; a.qa = qa; a.qm = qm; a.entries = entries; a.q = q; a.K = k; a.P = p;
   a.use_coarse = use_coarse ? 1 : 0; a.inv_alpha = inv_alpha; a.out_ids = out_ids;
   a.out_dists = out_dists; a.stats = out_stats;
@@ -1019,26 +1121,16 @@ static int route_dev(sb_index* idx, const double* qf, const double* qa, const do
   a.pf_rows = 1;
   if (const char* e = getenv("SB_ROUTE_PF")) a.pf_rows = atoi(e);
   // integer features in [0, 255]: route over a u8 copy with dp4a dot products (exact), unless
-  // SB_ROUTE_U8=0; built once per index
+  // SB_ROUTE_U8=0; built once per layout
   a.F8 = nullptr;
   a.nx8 = nullptr;
-  {
-    const char* u8env = getenv("SB_ROUTE_U8");
-    const bool want = u8env ? atoi(u8env) != 0 : true;
-    if (want && a.f32_ok && idx->flo >= 0.f && idx->fhi <= 255.f && idx->m % 16 == 0 &&
-        idx->m <= 512) {
-      if (!idx->have_f8) {
-        const size_t fbytes = (size_t)n * idx->m;
-        CK(idx->f8.ensure(fbytes + 256 + sizeof(int32_t) * (size_t)n));
-        CKL(sb::launch_pack_u8(idx->F.as<float>(), n, idx->m, idx->f8.as<uint8_t>(),
-                               reinterpret_cast<int32_t*>(idx->f8.as<uint8_t>() + ((fbytes + 255) & ~(size_t)255)),
-                               idx->st));
-        idx->have_f8 = true;
-        idx->launches += 1;
-      }
-      a.F8 = idx->f8.as<uint8_t>();
-      a.nx8 = reinterpret_cast<const int32_t*>(idx->f8.as<uint8_t>() + (((size_t)n * idx->m + 255) & ~(size_t)255));
-    }
+  if (a.f32_ok && u8_eligible(idx)) {
+    DBuf& buf = relabel ? idx->rl_f8 : idx->f8;
+    int r = relabel ? ensure_u8(idx, a.F, idx->rl_f8, idx->rl_have_f8)
+                    : ensure_u8(idx, a.F, idx->f8, idx->have_f8);
+    if (r) return r;
+    a.F8 = buf.as<uint8_t>();
+    a.nx8 = reinterpret_cast<const int32_t*>(buf.as<uint8_t>() + (((size_t)n * idx->m + 255) & ~(size_t)255));
   }
   idx->last_route_path = sb::route_path(a);
   size_t per_warp = sb::route_smem_per_warp(a);

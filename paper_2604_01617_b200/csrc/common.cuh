@@ -94,6 +94,23 @@ SB_DEV bool dlt(double da, uint32_t ia, double db, uint32_t ib) {
   return da < db || (da == db && ia < ib);
 }
 
+// (d, id) order for ids of a relabeled layout: ties compare the ORIGINAL ids perm[id]
+// (perm == null: identity; ids >= n are padding and keep their value).  The lookup runs
+// only on exact distance ties.
+struct IdOrder {
+  const int32_t* perm;
+  uint32_t n;
+  SB_DEV uint32_t key(uint32_t i) const { return (perm && i < n) ? (uint32_t)__ldg(perm + i) : i; }
+  SB_DEV bool operator()(double da, uint32_t ia, double db, uint32_t ib) const {
+    return da < db || (da == db && key(ia) < key(ib));
+  }
+};
+struct PlainOrder {
+  SB_DEV bool operator()(double da, uint32_t ia, double db, uint32_t ib) const {
+    return dlt(da, ia, db, ib);
+  }
+};
+
 // ---------------------------------------------------------------------------
 // warp helpers
 SB_DEV int lane_id() { return threadIdx.x & 31; }
@@ -147,7 +164,8 @@ SB_DEV void cta_bitonic_u64(uint64_t* s, int n) {
 }
 
 // Bitonic sort of (fp64 dist, u32 id) pairs held in two shared arrays, one warp.
-SB_DEV void warp_bitonic_did(double* d, uint32_t* id, int n) {
+template <class Less = PlainOrder>
+SB_DEV void warp_bitonic_did(double* d, uint32_t* id, int n, Less lt = Less()) {
   for (int k = 2; k <= n; k <<= 1) {
     for (int j = k >> 1; j > 0; j >>= 1) {
       for (int i = lane_id(); i < n; i += 32) {
@@ -156,7 +174,7 @@ SB_DEV void warp_bitonic_did(double* d, uint32_t* id, int n) {
           double da = d[i], db = d[p];
           uint32_t ia = id[i], ib = id[p];
           bool up = (i & k) == 0;
-          bool gt = dlt(db, ib, da, ia);
+          bool gt = lt(db, ib, da, ia);
           if (gt == up) { d[i] = db; d[p] = da; id[i] = ib; id[p] = ia; }
         }
       }
@@ -172,8 +190,9 @@ SB_DEV void warp_bitonic_did(double* d, uint32_t* id, int n) {
 // do not beat the tail are dropped, the rest land at j + #{R < C[j]} and R[i] moves to
 // i + #{C < R[i]}.  cpos is scratch of >= c ints; cd/cid must hold next_pow2(c) slots.
 // Returns the lowest position that received a new entry, or K if none did.
+template <class Less = PlainOrder>
 SB_DEV int warp_merge_topk(double* rd, uint32_t* rid, int K, double* cd, uint32_t* cid,
-                           int* cpos, int c, uint32_t idmask) {
+                           int* cpos, int c, uint32_t idmask, Less lt = Less()) {
   const int lane = lane_id();
   const double wd = rd[K - 1];
   const uint32_t wi = rid[K - 1] & idmask;
@@ -186,7 +205,7 @@ SB_DEV int warp_merge_topk(double* rd, uint32_t* rid, int K, double* cd, uint32_
     if (i < c) {
       d = cd[i];
       id = cid[i];
-      ok = dlt(d, id, wd, wi);
+      ok = lt(d, id, wd, wi);
     }
     unsigned bal = __ballot_sync(0xffffffffu, ok);
     __syncwarp();
@@ -205,14 +224,14 @@ SB_DEV int warp_merge_topk(double* rd, uint32_t* rid, int K, double* cd, uint32_
     cid[i] = 0xFFFFFFFFu;
   }
   __syncwarp();
-  if (np > 1) warp_bitonic_did(cd, cid, np);
+  if (np > 1) warp_bitonic_did(cd, cid, np, lt);
   for (int j = lane; j < kept; j += 32) {
     double d = cd[j];
     uint32_t id = cid[j];
     int lo = 0, hi = K;
     while (lo < hi) {
       int mid = (lo + hi) >> 1;
-      if (dlt(rd[mid], rid[mid] & idmask, d, id)) lo = mid + 1; else hi = mid;
+      if (lt(rd[mid], rid[mid] & idmask, d, id)) lo = mid + 1; else hi = mid;
     }
     cpos[j] = j + lo;
   }
@@ -233,7 +252,7 @@ SB_DEV int warp_merge_topk(double* rd, uint32_t* rid, int K, double* cd, uint32_
       int lo = 0, hi = kept;
       while (lo < hi) {
         int mid = (lo + hi) >> 1;
-        if (dlt(cd[mid], cid[mid], d, id)) lo = mid + 1; else hi = mid;
+        if (lt(cd[mid], cid[mid], d, id)) lo = mid + 1; else hi = mid;
       }
       tgt = i + lo;
     }

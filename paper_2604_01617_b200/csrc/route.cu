@@ -33,6 +33,8 @@
 #include "rng.cuh"
 #include "sb_internal.h"
 
+#include <cub/device/device_radix_sort.cuh>
+
 namespace sb {
 
 constexpr uint32_t kChkR = 0x80000000u;   // phase-2 checked
@@ -339,6 +341,7 @@ __global__ void __launch_bounds__(256, ROUTE_MIN_CTAS) route_kernel(RouteArgs a)
   uint32_t* vlog = a.vlog + slot * (int64_t)a.logcap;
   const int K = a.K;
   const int Cap = a.Cpad;
+  const IdOrder ord{a.perm, (uint32_t)a.n};  // ties by original id in a relabeled layout
 
   for (;;) {
     int qi = 0;
@@ -417,6 +420,7 @@ __global__ void __launch_bounds__(256, ROUTE_MIN_CTAS) route_kernel(RouteArgs a)
         c = K - ent_pos < Cap ? K - ent_pos : Cap;
         for (int t = lane; t < c; t += 32) {
           uint32_t v = (uint32_t)ent[ent_pos + t];
+          if (a.inv) v = (uint32_t)__ldg(a.inv + v);  // original -> layout id
           atomicOr(vis + (v >> 5), 1u << (v & 31));
           if (ent_pos + t < a.logcap) vlog[ent_pos + t] = v;
           w.cid[t] = v;
@@ -511,19 +515,20 @@ __global__ void __launch_bounds__(256, ROUTE_MIN_CTAS) route_kernel(RouteArgs a)
             w.rid[t] = 0xFFFFFFFFu;
           }
           __syncwarp();
-          if (a.Kpad > 1) warp_bitonic_did(w.rd, w.rid, a.Kpad);
+          if (a.Kpad > 1) warp_bitonic_did(w.rd, w.rid, a.Kpad, ord);
           stage = a.use_coarse ? 1 : 2;
           lb = 0;
         }
         __syncwarp();
       } else if (c > 0) {
-        int ins = warp_merge_topk(w.rd, w.rid, K, w.cd, w.cid, w.cpos, c, kIdMask);
+        int ins = warp_merge_topk(w.rd, w.rid, K, w.cd, w.cid, w.cpos, c, kIdMask, ord);
         if (ins < lb) lb = ins;
       }
     }
     // results
     for (int t = lane; t < K; t += 32) {
-      a.out_ids[(int64_t)qi * K + t] = (int64_t)(w.rid[t] & kIdMask);
+      const uint32_t id = w.rid[t] & kIdMask;
+      a.out_ids[(int64_t)qi * K + t] = (int64_t)(a.perm ? (uint32_t)__ldg(a.perm + id) : id);
       a.out_dists[(int64_t)qi * K + t] = w.rd[t];
     }
     if (a.stats && lane == 0) {
@@ -629,6 +634,147 @@ __global__ void pack_u8_kernel(const float* F, int64_t n, int m, uint8_t* F8, in
 
 int launch_pack_u8(const float* F, int64_t n, int m, uint8_t* F8, int32_t* nx, cudaStream_t st) {
   pack_u8_kernel<<<(unsigned)((n + 7) / 8), 256, 0, st>>>(F, n, m, F8, nx);
+  return (int)cudaGetLastError();
+}
+
+// ---- routing layout: a locality order of the nodes ------------------------------------
+// Nodes are renumbered along a Z-order (Morton) curve over kOrdDims random +-1 projections of
+// their features, so the nodes one query visits sit close together: their visited bits share
+// words and sectors, and their rows, attributes and adjacency share DRAM pages.  Any order is
+// exact (ties still compare original ids); this one only changes speed.
+constexpr int kOrdDims = 6, kOrdBits = 10;
+
+SB_DEV float rademacher(int d, int p) {
+  uint32_t h = (uint32_t)(d * kOrdDims + p) * 0x9E3779B1u;
+  h ^= h >> 15;
+  h *= 0x85EBCA77u;
+  h ^= h >> 13;
+  return (h & 1u) ? 1.f : -1.f;
+}
+
+__global__ void order_project_kernel(const float* F, int64_t n, int m, float* proj, unsigned* lohi) {
+  const int64_t v = (int64_t)blockIdx.x * (blockDim.x >> 5) + warp_id();
+  if (v >= n) return;
+  float acc[kOrdDims];
+#pragma unroll
+  for (int p = 0; p < kOrdDims; ++p) acc[p] = 0.f;
+  for (int t = lane_id(); t < m; t += 32) {
+    const float x = F[v * m + t];
+#pragma unroll
+    for (int p = 0; p < kOrdDims; ++p) acc[p] += rademacher(t, p) * x;
+  }
+#pragma unroll
+  for (int p = 0; p < kOrdDims; ++p) {
+    const float r = warp_sum(acc[p]);
+    if (lane_id() == 0) {
+      proj[v * kOrdDims + p] = r;
+      atomicMin(lohi + 2 * p, fkey(r));
+      atomicMax(lohi + 2 * p + 1, fkey(r));
+    }
+  }
+}
+
+__global__ void order_morton_kernel(const float* proj, int64_t n, const unsigned* lohi,
+                                    uint64_t* key, int32_t* val) {
+  const int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (v >= n) return;
+  uint32_t qv[kOrdDims];
+#pragma unroll
+  for (int p = 0; p < kOrdDims; ++p) {
+    const float lo = fkey_inv(lohi[2 * p]), hi = fkey_inv(lohi[2 * p + 1]);
+    const float t = hi > lo ? (proj[v * kOrdDims + p] - lo) / (hi - lo) : 0.f;
+    qv[p] = (uint32_t)fminf(fmaxf(t * (float)((1 << kOrdBits) - 1), 0.f), (float)((1 << kOrdBits) - 1));
+  }
+  uint64_t k = 0;
+  for (int b = kOrdBits - 1; b >= 0; --b)
+#pragma unroll
+    for (int p = 0; p < kOrdDims; ++p) k = (k << 1) | ((qv[p] >> b) & 1u);
+  key[v] = k;
+  val[v] = (int32_t)v;
+}
+
+__global__ void order_inverse_kernel(const int32_t* perm, int64_t n, int32_t* inv) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) inv[perm[i]] = (int32_t)i;
+}
+
+size_t route_order_scratch_bytes(int64_t n) {
+  size_t temp = 0;
+  cub::DeviceRadixSort::SortPairs(nullptr, temp, (const uint64_t*)nullptr, (uint64_t*)nullptr,
+                                  (const int32_t*)nullptr, (int32_t*)nullptr, (int)n);
+  return (size_t)n * (2 * sizeof(uint64_t) + sizeof(int32_t) + sizeof(float) * kOrdDims) + temp +
+         64 * sizeof(unsigned) + 1024;
+}
+
+int launch_route_order(const float* F, int64_t n, int m, int32_t* perm, int32_t* inv,
+                       void* scratch, size_t scratch_bytes, cudaStream_t st) {
+  char* p = static_cast<char*>(scratch);
+  auto take = [&](size_t b) { char* r = p; p += (b + 255) & ~(size_t)255; return r; };
+  uint64_t* k_in = reinterpret_cast<uint64_t*>(take(sizeof(uint64_t) * n));
+  uint64_t* k_out = reinterpret_cast<uint64_t*>(take(sizeof(uint64_t) * n));
+  int32_t* v_in = reinterpret_cast<int32_t*>(take(sizeof(int32_t) * n));
+  float* proj = reinterpret_cast<float*>(take(sizeof(float) * n * kOrdDims));
+  unsigned* lohi = reinterpret_cast<unsigned*>(take(64 * sizeof(unsigned)));
+  size_t temp = 0;
+  cub::DeviceRadixSort::SortPairs(nullptr, temp, k_in, k_out, v_in, perm, (int)n);
+  void* d_temp = take(temp);
+  if ((size_t)(p - static_cast<char*>(scratch)) > scratch_bytes) return (int)cudaErrorInvalidValue;
+  unsigned init[2 * kOrdDims];
+  for (int i = 0; i < kOrdDims; ++i) { init[2 * i] = 0xFFFFFFFFu; init[2 * i + 1] = 0u; }
+  cudaMemcpyAsync(lohi, init, sizeof(init), cudaMemcpyHostToDevice, st);
+  order_project_kernel<<<(unsigned)((n + 7) / 8), 256, 0, st>>>(F, n, m, proj, lohi);
+  order_morton_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(proj, n, lohi, k_in, v_in);
+  cudaError_t e = cub::DeviceRadixSort::SortPairs(d_temp, temp, k_in, k_out, v_in, perm, (int)n,
+                                                  0, kOrdDims * kOrdBits, st);
+  if (e != cudaSuccess) return (int)e;
+  order_inverse_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(perm, n, inv);
+  // the init copy above must complete before `init` leaves scope
+  cudaStreamSynchronize(st);
+  return (int)cudaGetLastError();
+}
+
+__global__ void permute_rows_f32_kernel(const float* src, int64_t n, int m, const int32_t* perm,
+                                        float* dst) {
+  const int64_t v = (int64_t)blockIdx.x * (blockDim.x >> 5) + warp_id();
+  if (v >= n) return;
+  const float* s = src + (int64_t)perm[v] * m;
+  for (int t = lane_id(); t < m; t += 32) dst[v * m + t] = s[t];
+}
+
+__global__ void permute_rows_i32_kernel(const int32_t* src, int64_t n, int w, const int32_t* perm,
+                                        int32_t* dst) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n * w) return;
+  const int64_t v = i / w;
+  dst[i] = src[(int64_t)perm[v] * w + (i - v * w)];
+}
+
+__global__ void relabel_adjacency_kernel(const int32_t* ids, const int32_t* counts, int64_t n, int g,
+                                         const int32_t* perm, const int32_t* inv, int32_t* ids_r,
+                                         int32_t* counts_r) {
+  const int64_t v = (int64_t)blockIdx.x * (blockDim.x >> 5) + warp_id();
+  if (v >= n) return;
+  const int64_t o = perm[v];
+  const int c = counts[o];
+  for (int t = lane_id(); t < g; t += 32) ids_r[v * g + t] = t < c ? inv[ids[o * g + t]] : 0;
+  if (lane_id() == 0) counts_r[v] = c;
+}
+
+int launch_permute_rows_f32(const float* src, int64_t n, int m, const int32_t* perm, float* dst,
+                            cudaStream_t st) {
+  permute_rows_f32_kernel<<<(unsigned)((n + 7) / 8), 256, 0, st>>>(src, n, m, perm, dst);
+  return (int)cudaGetLastError();
+}
+int launch_permute_rows_i32(const int32_t* src, int64_t n, int w, const int32_t* perm,
+                            int32_t* dst, cudaStream_t st) {
+  permute_rows_i32_kernel<<<(unsigned)((n * w + 255) / 256), 256, 0, st>>>(src, n, w, perm, dst);
+  return (int)cudaGetLastError();
+}
+int launch_relabel_adjacency(const int32_t* ids, const int32_t* counts, int64_t n, int g,
+                             const int32_t* perm, const int32_t* inv, int32_t* ids_r,
+                             int32_t* counts_r, cudaStream_t st) {
+  relabel_adjacency_kernel<<<(unsigned)((n + 7) / 8), 256, 0, st>>>(ids, counts, n, g, perm, inv,
+                                                                   ids_r, counts_r);
   return (int)cudaGetLastError();
 }
 

@@ -38,7 +38,23 @@ struct RouteArgs {
   // u8 copy of integer features in [0, 255] (null: not available) and exact |x|^2
   const uint8_t* F8;
   const int32_t* nx8;
+  // relabeled layout (route_layout): every id the kernel sees is a new id; entries arrive as
+  // original ids (mapped through inv), results leave as original ids (through perm), and
+  // exact distance ties compare original ids.  Null: identity.
+  const int32_t* perm;  // new -> original
+  const int32_t* inv;   // original -> new
 };
+// locality order of the nodes for routing: Z-order of random projections (route.cu)
+int launch_route_order(const float* F, int64_t n, int m, int32_t* perm, int32_t* inv,
+                       void* scratch, size_t scratch_bytes, cudaStream_t st);
+size_t route_order_scratch_bytes(int64_t n);
+int launch_permute_rows_f32(const float* src, int64_t n, int m, const int32_t* perm, float* dst,
+                            cudaStream_t st);
+int launch_permute_rows_i32(const int32_t* src, int64_t n, int w, const int32_t* perm,
+                            int32_t* dst, cudaStream_t st);
+int launch_relabel_adjacency(const int32_t* ids, const int32_t* counts, int64_t n, int g,
+                             const int32_t* perm, const int32_t* inv, int32_t* ids_r,
+                             int32_t* counts_r, cudaStream_t st);
 
 size_t route_smem_per_warp(const RouteArgs& a);
 int launch_feature_scan(const float* F, int64_t count, unsigned* out3, cudaStream_t st);

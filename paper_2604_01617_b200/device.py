@@ -87,6 +87,10 @@ class DeviceIndex:
         names = {0: "fp64", 1: "fp32", 2: "fp32-groups", 3: "fp64-generic", 4: "u8-dp4a"}
         return {"path": names.get(path.value, "none"), "row_bytes": rb.value}
 
+    def route_prepare(self):
+        """Build the routing layout (locality order, u8 copy) now; see sb_route_prepare."""
+        _lib.call("sb_route_prepare", self._h)
+
     def set_distance_mode(self, sequential: bool):
         _lib.call("sb_set_distance_mode", self._h, 1 if sequential else 0)
 

@@ -296,6 +296,10 @@ def build(features, attrs, schema, params: BuildParams, metric: MetricConfig) ->
     graph = run_descent(features, attrs, schema, params, metric)
     semantic_prune(graph, params)
     graph.frozen = True
+    # the search-ready layout (locality order, u8 copy) is part of the build
+    t1 = time.perf_counter()
+    graph.device().route_prepare()
+    graph.build_log["seconds_route_layout"] = time.perf_counter() - t1
     graph.build_log["seconds_total"] = time.perf_counter() - t0
     return graph
 

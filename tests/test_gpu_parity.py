@@ -359,3 +359,32 @@ def test_config_recipes_end_to_end(cfg, n, q):
         wi, wd = O.oracle_auto_topk(X, A, QX[i], QA[i], 10, cfg_m.alpha, return_dists=True)
         np.testing.assert_array_equal(ti[i], wi)
         np.testing.assert_array_equal(td[i], wd)
+
+
+@pytest.mark.gpu
+def test_route_layout_follows_adjacency_changes():
+    """The relabeled routing layout is rebuilt when the adjacency changes, and routing with
+    and without it (SB_ROUTE_RELABEL=0) equals the oracle."""
+    import os
+    rng = np.random.default_rng(11)
+    n, m, l, g = 3000, 16, 2, 12
+    f = rng.integers(0, 4, (n, m)).astype(np.float32)
+    a = rng.integers(1, 3, (n, l)).astype(np.int32)
+    qf = rng.integers(0, 4, (20, m)).astype(np.float32)
+    qa = rng.integers(1, 3, (20, l)).astype(np.int32)
+    dev = DeviceIndex(f, a, g)
+    for trial in range(2):
+        ids = np.stack([rng.choice(n, g, replace=False) for _ in range(n)]).astype(np.int32)
+        cnt = rng.integers(1, g + 1, n).astype(np.int32)
+        dev.upload(ids, np.zeros((n, g), np.float32), cnt)
+        want = O.search_batch(f, a, ids, cnt, 0.9, qf, qa, 24, seed=1)
+        ent = O.all_entry_points(n, 24, 1, qf.shape[0])
+        for relabel in ("1", "0"):
+            os.environ["SB_ROUTE_RELABEL"] = relabel
+            try:
+                got = dev.route(qf, qa, 24, 12, 1.0 / 0.9, entries=ent)
+            finally:
+                del os.environ["SB_ROUTE_RELABEL"]
+            np.testing.assert_array_equal(got[0], want[0], err_msg=f"trial {trial} relabel {relabel}")
+            np.testing.assert_array_equal(got[1], want[1])
+            np.testing.assert_array_equal(got[2][:, :4], want[2])
