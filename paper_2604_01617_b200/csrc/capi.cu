@@ -99,7 +99,7 @@ struct sb_index {
   bool have_indeg = false;
   int64_t last_overflow_rows = 0;
   // exact reinforce (overflow rows)
-  DBuf rf_n8, rf_nb, rf_n32, rf_n64, rf_o32, rf_o64, rf_ulist, rf_bits, rf_rec, rf_sim;
+  DBuf rf_n8, rf_nb, rf_n32, rf_n64, rf_o32, rf_o64, rf_ulist, rf_bits, rf_rec, rf_sim, rf_eo;
   // routing / brute force
   DBuf qf, qa, qm, entries, ent_scratch, out_ids, out_dists, stats, visited, vlog, counter;
   DBuf bf_part_d, bf_part_i, bf_self, bf_qa, bf_qm, bf_out32, fb, fb_norm, fb_tmp, qb, f8;
@@ -119,7 +119,7 @@ struct sb_index {
                    &qa, &qm, &entries, &ent_scratch, &out_ids, &out_dists, &stats, &visited,
                    &vlog, &counter, &bf_part_d, &bf_part_i, &bf_self, &bf_qa, &bf_qm,
                    &bf_out32, &rf_n8, &rf_nb, &rf_n32, &rf_n64, &rf_o32, &rf_o64,
-                   &rf_ulist, &rf_bits, &rf_rec, &rf_sim};
+                   &rf_ulist, &rf_bits, &rf_rec, &rf_sim, &rf_eo};
     for (DBuf* b : all) b->release();
     if (own) cudaStreamDestroy(own);
   }
@@ -615,10 +615,12 @@ static int reinforce_overflow(sb_index* idx, double sigma) {
   a.ids = idx->ids.as<int32_t>(); a.dists = idx->dists.as<float>();
   a.counts = idx->counts.as<int32_t>(); a.in_deg = idx->in_deg.as<int32_t>(); a.sigma = sigma;
   CK(idx->rf_n8.ensure((size_t)n * g));            // mutual flags
+  CK(idx->rf_eo.ensure(sizeof(int32_t) * (size_t)n * g));  // per-edge O index of the target
   CK(idx->rf_nb.ensure((size_t)n * 2));            // is_o, relevant
   CK(idx->rf_n32.ensure(sizeof(int32_t) * n * 2)); // o_idx, static_ins
   CK(idx->rf_n64.ensure(sizeof(int64_t) * n * 8)); // rev_extra, oflag, oscan, orev, apply x3, rec_head
   a.mutual = idx->rf_n8.as<uint8_t>();
+  a.eo = idx->rf_eo.as<int32_t>();
   a.is_o = idx->rf_nb.as<uint8_t>();
   a.relevant = a.is_o + n;
   a.o_idx = idx->rf_n32.as<int32_t>();

@@ -93,6 +93,15 @@ __global__ void rf_classify_kernel(RfArgs a, const int64_t* oscan) {
   a.relevant[s] = rel ? 1 : 0;
 }
 
+// K3b: per-edge O index of the target (post-prune rows; static for rows outside O)
+__global__ void rf_eo_kernel(RfArgs a) {
+  int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= a.n * a.g) return;
+  const int64_t s = e / a.g;
+  const int t = (int)(e - s * a.g);
+  a.eo[e] = t < a.counts[s] ? a.o_idx[a.ids[e]] : -2;
+}
+
 // K4a: scatter reverse sources of O targets into their U lists (after the row's own ids)
 __global__ void rf_u_scatter_kernel(RfArgs a) {
   int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -494,30 +503,65 @@ __global__ void rf_simulate_kernel(RfArgs a) {
     const int32_t jd = (int32_t)key_id(kd);
     warp_try_insert(a, S, jd, a.o_idx[jd], (int32_t)s, key_dist(kd), s, err);
   };
+  // Per source: count, O index, the row (gamma wide, masked by the count), the head of its
+  // recorded mirrors and the targets' O indices.  Rows outside O never change during the
+  // simulation and their targets' O indices are precomputed (eo), so all of it is one round
+  // of independent loads, issued for the NEXT relevant source of the chunk before the current
+  // one is processed.  O rows may change, so an O source is always (re)loaded when reached.
+  struct Src {
+    int64_t s;
+    int cs, osrc;
+    int64_t rh;
+    int32_t vi[8];
+    float vd[8];
+    int oj[8];
+  };
+  auto load_src = [&](int64_t s, Src& D) {
+    D.s = s;
+    D.cs = a.counts[s];
+    D.osrc = a.o_idx[s];
+    D.rh = a.rec_head[s];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const int t = lane + 32 * k;
+      if (t < g) {
+        D.vi[k] = a.ids[s * g + t];
+        D.vd[k] = a.dists[s * g + t];
+        D.oj[k] = a.eo[s * g + t];
+      } else {
+        D.oj[k] = -2;
+      }
+    }
+  };
   for (int64_t base = 0; base < a.n; base += 32) {
     const int64_t idx = base + lane;
     unsigned bal = __ballot_sync(kFull, idx < a.n && relevant[idx]);
+    Src nxt;
+    nxt.s = -1;
     while (bal) {
       const int64_t s = base + __ffs(bal) - 1;
       bal &= bal - 1u;
       if (kRfProf && lane == 0) atomicAdd(&g_rf_prof[7], 1ull);
-      // one round of loads for the source: count, O index, the row (gamma wide, masked by
-      // the count), the head of its recorded mirrors; then the targets' O indices
-      const int cs = a.counts[s];
-      const int osrc = a.o_idx[s];
+      Src D;
+      if (nxt.s == s && nxt.osrc < 0) {
+        D = nxt;  // valid: only O sources record mirrors, and they discard the prefetch
+      } else {
+        load_src(s, D);
+      }
+      nxt.s = -1;
+      if (bal) load_src(base + __ffs(bal) - 1, nxt);
+      const int cs = D.cs;
+      const int osrc = D.osrc;
+      const int64_t rh = D.rh;
       int32_t vi[8];
       float vd[8];
-#pragma unroll
-      for (int k = 0; k < 8; ++k) {
-        const int t = lane + 32 * k;
-        if (t < g) { vi[k] = a.ids[s * g + t]; vd[k] = a.dists[s * g + t]; }
-      }
-      const int64_t rh = a.rec_head[s];
       int oj[8];
 #pragma unroll
       for (int k = 0; k < 8; ++k) {
-        const int t = lane + 32 * k;
-        oj[k] = t < cs ? a.o_idx[vi[k]] : -2;
+        vi[k] = D.vi[k];
+        vd[k] = D.vd[k];
+        // an O row's entries may have changed since eo was computed: look their O index up
+        oj[k] = osrc >= 0 ? ((lane + 32 * k) < cs ? a.o_idx[vi[k]] : -2) : D.oj[k];
       }
       if (osrc >= 0) {
         // mirrors into rows that cannot overflow: record each one not already present
@@ -561,6 +605,7 @@ __global__ void rf_simulate_kernel(RfArgs a) {
         }
         // recorded mirrors may have made later sources of this chunk relevant
         bal = __ballot_sync(kFull, idx > s && idx < a.n && relevant[idx]);
+        nxt.s = -1;
       } else {
         // O-target events of a non-O row in key order: static entries j in O, plus entries
         // mirrored in by O sources processed earlier (linked list, sorted here)
@@ -650,6 +695,7 @@ int rf_launch_stage2(RfArgs& a, const int64_t* oscan, cudaStream_t st) {
   cudaMemsetAsync(a.orev_cnt, 0, sizeof(int64_t) * a.n, st);
   cudaMemsetAsync(a.apply_cnt, 0, sizeof(int64_t) * a.n, st);
   rf_classify_kernel<<<nblk(a.n, 256), 256, 0, st>>>(a, oscan);
+  rf_eo_kernel<<<nblk(a.n * a.g, 256), 256, 0, st>>>(a);
   return (int)cudaGetLastError();
 }
 

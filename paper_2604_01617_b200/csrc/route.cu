@@ -642,7 +642,13 @@ int launch_pack_u8(const float* F, int64_t n, int m, uint8_t* F8, int32_t* nx, c
 // their features, so the nodes one query visits sit close together: their visited bits share
 // words and sectors, and their rows, attributes and adjacency share DRAM pages.  Any order is
 // exact (ties still compare original ids); this one only changes speed.
-constexpr int kOrdDims = 6, kOrdBits = 10;
+#ifndef ROUTE_ORD_DIMS
+#define ROUTE_ORD_DIMS 6
+#endif
+#ifndef ROUTE_ORD_BITS
+#define ROUTE_ORD_BITS 10
+#endif
+constexpr int kOrdDims = ROUTE_ORD_DIMS, kOrdBits = ROUTE_ORD_BITS;
 
 SB_DEV float rademacher(int d, int p) {
   uint32_t h = (uint32_t)(d * kOrdDims + p) * 0x9E3779B1u;

@@ -217,6 +217,7 @@ struct RfArgs {
   int32_t* in_deg;
   double sigma;
   uint8_t* mutual;      // n x g
+  int32_t* eo;          // n x g: O index of each edge's target (-1 not in O, -2 past count)
   int64_t* rev_extra;   // n
   uint8_t* is_o;        // n
   int32_t* o_idx;       // n
