@@ -104,16 +104,30 @@ SB_DEV void bulk_g2s(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar
 }
 
 // ---- prep kernels ----------------------------------------------------------------------
-// queries -> bf16 in the row-group layout (rows up to qpad, zero past q) + exact |q|^2
-__global__ void tc_prep_queries_kernel(const double* qf, int64_t q, int64_t qpad, int m,
+// queries -> bf16 in the row-group layout of K = mk columns (rows up to qpad, zero past q)
+// + exact |q|^2.  Folded operands (mk = m + 16): columns 0..m-1 hold 2q, columns m..m+2 hold
+// -2^16, -2^8, -1 (all exact in bf16), so that against a node row ending in the three bytes
+// of |x|^2 the tensor core produces y = 2 x.q - |x|^2 directly.
+__global__ void tc_prep_queries_kernel(const double* qf, int64_t q, int64_t qpad, int m, int mk,
                                        char* Qb, int32_t* nq) {
   int64_t i = (int64_t)blockIdx.x * (blockDim.x >> 5) + warp_id();
   if (i >= qpad) return;
+  const bool fold = mk > m;
   int acc = 0;
-  for (int t = lane_id(); t < m; t += 32) {
-    double x = i < q ? qf[i * m + t] : 0.0;
-    reinterpret_cast<__nv_bfloat16*>(Qb + rg_off(i, t >> 3, m))[t & 7] = __float2bfloat16_rn((float)x);
-    acc += (int)x * (int)x;
+  for (int t = lane_id(); t < mk; t += 32) {
+    float x = 0.f;
+    if (t < m) {
+      const double v = i < q ? qf[i * m + t] : 0.0;
+      acc += (int)v * (int)v;
+      x = fold ? 2.0f * (float)v : (float)v;
+    } else if (t == m) {
+      x = -65536.f;
+    } else if (t == m + 1) {
+      x = -256.f;
+    } else if (t == m + 2) {
+      x = -1.f;
+    }
+    reinterpret_cast<__nv_bfloat16*>(Qb + rg_off(i, t >> 3, mk))[t & 7] = __float2bfloat16_rn(x);
   }
   acc = warp_sum(acc);
   if (lane_id() == 0 && i < q) nq[i] = acc;
@@ -134,7 +148,7 @@ struct TcArgs {
   const int64_t* qa;        // q x l
   const int64_t* qmask;     // q x l or null
   int64_t n, q;
-  int m, l, kk, splits, N;
+  int m, l, kk, splits, N;  // m = operand K (features, plus 16 folded columns when folded)
   double alpha;
   double* part_d;           // q x (2 splits) x kk
   uint32_t* part_i;
@@ -151,6 +165,7 @@ struct TcArgs {
 // accumulator ready and B stage free again), empty (all 256 epilogue threads finished the
 // tile: accumulator and metadata free).  Rows for tile i + 1 load while MMA i runs; MMA i + 1
 // starts as soon as the epilogue leaves tile i - 1.
+template <bool FOLD>
 __global__ void __launch_bounds__(kTcThreads + 32, 1) bf_tc_kernel(TcArgs a) {
   extern __shared__ __align__(1024) char smem[];
   const int tid = threadIdx.x;
@@ -309,13 +324,19 @@ __global__ void __launch_bounds__(kTcThreads + 32, 1) bf_tc_kernel(TcArgs a) {
         const int c0 = half * cols + c * 16;
         float y[16];
         float mx = -3.4e38f;
+        if (FOLD) {
+          // the accumulator already holds y = 2 x.q - |x|^2 (exact integers below 2^24)
 #pragma unroll
-        for (int q4 = 0; q4 < 4; ++q4) {
-          const float4 v = *reinterpret_cast<const float4*>(s_nx + c0 + 4 * q4);
-          y[4 * q4 + 0] = fmaf(2.0f, __uint_as_float(r[4 * q4 + 0]), -v.x);
-          y[4 * q4 + 1] = fmaf(2.0f, __uint_as_float(r[4 * q4 + 1]), -v.y);
-          y[4 * q4 + 2] = fmaf(2.0f, __uint_as_float(r[4 * q4 + 2]), -v.z);
-          y[4 * q4 + 3] = fmaf(2.0f, __uint_as_float(r[4 * q4 + 3]), -v.w);
+          for (int j = 0; j < 16; ++j) y[j] = __uint_as_float(r[j]);
+        } else {
+#pragma unroll
+          for (int q4 = 0; q4 < 4; ++q4) {
+            const float4 v = *reinterpret_cast<const float4*>(s_nx + c0 + 4 * q4);
+            y[4 * q4 + 0] = fmaf(2.0f, __uint_as_float(r[4 * q4 + 0]), -v.x);
+            y[4 * q4 + 1] = fmaf(2.0f, __uint_as_float(r[4 * q4 + 1]), -v.y);
+            y[4 * q4 + 2] = fmaf(2.0f, __uint_as_float(r[4 * q4 + 2]), -v.z);
+            y[4 * q4 + 3] = fmaf(2.0f, __uint_as_float(r[4 * q4 + 3]), -v.w);
+          }
         }
 #pragma unroll
         for (int j = 0; j < 16; ++j) mx = fmaxf(mx, y[j]);
@@ -352,8 +373,9 @@ __global__ void __launch_bounds__(kTcThreads + 32, 1) bf_tc_kernel(TcArgs a) {
 #pragma unroll
           for (int jj = 0; jj < 16; ++jj)
             if (jj == j) rj = __uint_as_float(r[jj]);
-          // exact: x.q is an integer below 2^24 held exactly by the fp32 accumulator
-          const int S = (int)s_nx[col] + my_nq - 2 * (int)rj;
+          // exact: x.q (or y when folded) is an integer below 2^24 held exactly by the fp32
+          // accumulator
+          const int S = FOLD ? my_nq - (int)rj : (int)s_nx[col] + my_nq - 2 * (int)rj;
           if ((float)S * f2 > t2_eff) continue;
           // exact fp64 decision (evaluate.py:48-53), ties by original id
           const double dist = dmul(sqrt((double)S), dadd(1.0, __ddiv_rn((double)sa, a.alpha)));
@@ -466,10 +488,11 @@ __global__ void tc_scatter_kernel(const int32_t* code, int64_t n, const int64_t*
   orig[off[c] + (int64_t)p] = (int32_t)i;
 }
 
-// sorted copies: bf16 rows (row-group layout), exact squared norms, codes, attributes
-// (warp per node)
+// sorted copies: bf16 rows (row-group layout, K = mk columns), exact squared norms, codes,
+// attributes (warp per node).  Folded rows (mk = m + 16) end in the bytes of |x|^2
+// (|x|^2 < 2^24: h * 2^16 + m * 2^8 + l, each byte exact in bf16).
 __global__ void tc_gather_kernel(const float* F, const int32_t* A, const int32_t* code_in,
-                                 const int32_t* orig, int64_t n, int m, int l, char* Fb,
+                                 const int32_t* orig, int64_t n, int m, int mk, int l, char* Fb,
                                  int32_t* nx, int32_t* code, int32_t* As) {
   int64_t p = (int64_t)blockIdx.x * (blockDim.x >> 5) + warp_id();
   if (p >= n) return;
@@ -477,10 +500,16 @@ __global__ void tc_gather_kernel(const float* F, const int32_t* A, const int32_t
   int acc = 0;
   for (int t = lane_id(); t < m; t += 32) {
     float x = F[v * m + t];
-    reinterpret_cast<__nv_bfloat16*>(Fb + rg_off(p, t >> 3, m))[t & 7] = __float2bfloat16_rn(x);
+    reinterpret_cast<__nv_bfloat16*>(Fb + rg_off(p, t >> 3, mk))[t & 7] = __float2bfloat16_rn(x);
     acc += (int)x * (int)x;
   }
   acc = warp_sum(acc);
+  for (int t = m + lane_id(); t < mk; t += 32) {
+    const int b = t - m;
+    const float x = b == 0 ? (float)((acc >> 16) & 255) : b == 1 ? (float)((acc >> 8) & 255)
+                  : b == 2 ? (float)(acc & 255) : 0.f;
+    reinterpret_cast<__nv_bfloat16*>(Fb + rg_off(p, t >> 3, mk))[t & 7] = __float2bfloat16_rn(x);
+  }
   if (lane_id() == 0) {
     nx[p] = __float_as_int((float)acc);  // |x|^2 as fp32 (exact: below 2^24)
     code[p] = code_in[v];
@@ -504,24 +533,25 @@ int launch_tc_scatter(const int32_t* code, int64_t n, const int64_t* off, unsign
   return (int)cudaGetLastError();
 }
 int launch_tc_gather(const float* F, const int32_t* A, const int32_t* code_in, const int32_t* orig,
-                     int64_t n, int m, int l, void* Fb, int32_t* nx, int32_t* code, int32_t* As,
-                     cudaStream_t st) {
-  tc_gather_kernel<<<(unsigned)((n + 7) / 8), 256, 0, st>>>(F, A, code_in, orig, n, m, l,
+                     int64_t n, int m, int mk, int l, void* Fb, int32_t* nx, int32_t* code,
+                     int32_t* As, cudaStream_t st) {
+  tc_gather_kernel<<<(unsigned)((n + 7) / 8), 256, 0, st>>>(F, A, code_in, orig, n, m, mk, l,
                                                              (char*)Fb, nx, code, As);
   return (int)cudaGetLastError();
 }
 
-int launch_bf_tc_prep_queries(const double* qf, int64_t q, int m, void* Qb, int32_t* nq,
+int launch_bf_tc_prep_queries(const double* qf, int64_t q, int m, int mk, void* Qb, int32_t* nq,
                               cudaStream_t st) {
   const int64_t qpad = (q + kTcM - 1) / kTcM * kTcM;
-  tc_prep_queries_kernel<<<(unsigned)((qpad + 7) / 8), 256, 0, st>>>(qf, q, qpad, m, (char*)Qb, nq);
+  tc_prep_queries_kernel<<<(unsigned)((qpad + 7) / 8), 256, 0, st>>>(qf, q, qpad, m, mk, (char*)Qb, nq);
   return (int)cudaGetLastError();
 }
 
 int launch_bf_tc(const void* Fb, const int32_t* nx, const int32_t* A, const int32_t* code,
                  const int32_t* orig, const void* Qb, const int32_t* nq, const int64_t* qa,
                  const int64_t* qmask, int64_t n, int64_t q, int m, int l, int kk, int splits,
-                 double alpha, double* part_d, uint32_t* part_i, int* gthr, cudaStream_t st) {
+                 double alpha, double* part_d, uint32_t* part_i, int* gthr, int fold,
+                 cudaStream_t st) {
   TcArgs a;
   a.gthr = gthr;
   a.Fb = (const char*)Fb; a.nx = nx; a.A = A; a.code = code; a.orig = orig;
@@ -531,10 +561,11 @@ int launch_bf_tc(const void* Fb, const int32_t* nx, const int32_t* A, const int3
   a.N = bf_tc_tile(m, l, kk);
   if (a.N == 0) return (int)cudaErrorInvalidValue;
   size_t smem = bf_tc_smem_n(m, l, kk, a.N);
-  cudaError_t e = cudaFuncSetAttribute(bf_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  auto kern = fold ? bf_tc_kernel<true> : bf_tc_kernel<false>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return (int)e;
   dim3 grid((unsigned)((q + kTcM - 1) / kTcM), (unsigned)splits);
-  bf_tc_kernel<<<grid, kTcThreads + 32, smem, st>>>(a);
+  kern<<<grid, kTcThreads + 32, smem, st>>>(a);
   return (int)cudaGetLastError();
 }
 

@@ -76,6 +76,7 @@ struct sb_index {
   float flo = 0.f, fhi = 0.f;
   bool force_sequential = false;  // testing: always use the sequential-order distance path
   bool have_fb = false;           // bf16 feature copy + norms for the tensor-core top-k
+  int fb_mk = 0;                  // its operand K (features, + 16 when |x|^2 is folded in)
   bool last_bf_tc = false;        // the last sb_bf_topk_queries ran on tensor cores
   bool have_f8 = false;           // u8 feature copy for routing (integer data in [0, 255])
   // routing layout: nodes renumbered in a locality order (route_layout); valid while
@@ -875,22 +876,39 @@ int sb_bf_topk_queries(sb_index* idx, const double* qf, const int64_t* qa, const
   bool tc = idx->int_exact && idx->fmax <= 256.0 && idx->m <= 255 && !idx->force_sequential &&
             sb::bf_tc_supported(idx->m, idx->l, k);
   if (const char* e = getenv("SB_BF_TC")) tc = tc && atoi(e) != 0;
+  double qmin = 0.0, qmax = 0.0;
   for (int64_t i = 0; tc && i < q * idx->m; ++i) {
     double v = qf[i];
     tc = v == std::rint(v) && std::fabs(v) <= 256.0;
+    qmin = std::min(qmin, v);
+    qmax = std::max(qmax, v);
   }
+  // Fold |x|^2 into the MMA (16 more K columns) when y = 2 x.q - |x|^2 and all its partial
+  // sums stay exact integers below 2^24: non-negative data bounds every partial sum by
+  // max(sum 2qx, |x|^2); mixed signs by 3 m f^2.
+  bool fold = false;
+  if (tc) {
+    const double m = idx->m, fx = idx->fmax, fq = std::max(std::fabs(qmin), std::fabs(qmax));
+    const bool nonneg = idx->flo >= 0.f && qmin >= 0.0;
+    const double bound = nonneg ? std::max(2.0 * m * fx * fq, m * fx * fx)
+                                : 3.0 * m * std::max(fx, fq) * std::max(fx, fq);
+    fold = bound < 16777216.0;
+    if (const char* e = getenv("SB_BF_FOLD")) fold = fold && atoi(e) != 0;
+    if (fold && !sb::bf_tc_supported(idx->m + 16, idx->l, k)) fold = false;
+  }
+  const int mk = fold ? idx->m + 16 : idx->m;
   if (tc) {
     kk = k;
     a.k = kk;
     const int64_t n = idx->n;
     const int64_t npad = (n + sb::kTcNodePad - 1) / sb::kTcNodePad * sb::kTcNodePad;
-    if (!idx->have_fb) {
+    if (!idx->have_fb || idx->fb_mk != mk) {
       // attribute-grouped node order: counting sort by the attribute tuple
       const int l = idx->l;
       // padded, zero-filled: every tile the kernel copies lies inside the buffers
-      CK(idx->fb.ensure(sizeof(uint16_t) * npad * idx->m));
+      CK(idx->fb.ensure(sizeof(uint16_t) * npad * mk));
       CK(idx->fb_norm.ensure(sizeof(int32_t) * npad * (3 + l)));  // nx | code | orig | attrs
-      CK(cudaMemsetAsync(idx->fb.p, 0, sizeof(uint16_t) * npad * idx->m, idx->st));
+      CK(cudaMemsetAsync(idx->fb.p, 0, sizeof(uint16_t) * npad * mk, idx->st));
       CK(cudaMemsetAsync(idx->fb_norm.p, 0, sizeof(int32_t) * npad * (3 + l), idx->st));
       int32_t* s_nx = idx->fb_norm.as<int32_t>();
       int32_t* s_code = s_nx + npad;
@@ -932,17 +950,18 @@ int sb_bf_topk_queries(sb_index* idx, const double* qf, const int64_t* qa, const
       CKL(sb::launch_tc_scatter(d_code, n, idx->rev_off.as<int64_t>(),
                                 idx->rev_cur.as<unsigned long long>(), s_orig, idx->st));
       CKL(sb::launch_tc_gather(idx->F.as<float>(), idx->A.as<int32_t>(), d_code, s_orig, n,
-                               idx->m, l, idx->fb.p, s_nx, s_code, s_attr, idx->st));
+                               idx->m, mk, l, idx->fb.p, s_nx, s_code, s_attr, idx->st));
       idx->have_fb = true;
+      idx->fb_mk = mk;
       idx->have_cand = false;  // rev_* scratch was reused
       idx->launches += 6;
     }
     const int64_t qpad = (q + 127) / 128 * 128;
-    CK(idx->qb.ensure(sizeof(uint16_t) * qpad * idx->m + 2 * sizeof(int32_t) * q + 64));
-    int32_t* d_nq = reinterpret_cast<int32_t*>(idx->qb.as<char>() + sizeof(uint16_t) * qpad * idx->m);
+    CK(idx->qb.ensure(sizeof(uint16_t) * qpad * mk + 2 * sizeof(int32_t) * q + 64));
+    int32_t* d_nq = reinterpret_cast<int32_t*>(idx->qb.as<char>() + sizeof(uint16_t) * qpad * mk);
     int32_t* d_gthr = d_nq + q;  // per-query shared bound, 0x7F7F7F7F = 3.39e38f
     CK(cudaMemsetAsync(d_gthr, 0x7F, sizeof(int32_t) * q, idx->st));
-    CKL(sb::launch_bf_tc_prep_queries(idx->qf.as<double>(), q, idx->m, idx->qb.p, d_nq, idx->st));
+    CKL(sb::launch_bf_tc_prep_queries(idx->qf.as<double>(), q, idx->m, mk, idx->qb.p, d_nq, idx->st));
     // split the node range so that whole waves of CTAs are busy: minimise waves / splits
     const int groups = (int)((q + 127) / 128);
     int splits = 1;
@@ -963,8 +982,8 @@ int sb_bf_topk_queries(sb_index* idx, const double* qf, const int64_t* qa, const
     {
       int32_t* s_nx = idx->fb_norm.as<int32_t>();
       CKL(sb::launch_bf_tc(idx->fb.p, s_nx, s_nx + 3 * npad, s_nx + npad, s_nx + 2 * npad, idx->qb.p,
-                           d_nq, a.qa, a.qmask, n, q, idx->m, idx->l, kk, splits, alpha, a.part_d,
-                           a.part_i, d_gthr, idx->st));
+                           d_nq, a.qa, a.qmask, n, q, mk, idx->l, kk, splits, alpha, a.part_d,
+                           a.part_i, d_gthr, fold ? 1 : 0, idx->st));
     }
     CKL(sb::launch_bf_merge_k(a, k, idx->out_ids.as<int64_t>(), nullptr, idx->out_dists.as<double>(),
                               d_unc, idx->st));

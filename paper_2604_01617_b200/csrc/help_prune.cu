@@ -522,6 +522,199 @@ __global__ void reconnect_kernel(SeqCtx c, int64_t n) {
   }
 }
 
+// ---- reconnect_islands by one CTA ------------------------------------------------------
+// The sweep is sequential over v (_kernels.py:455-487), but the costly part of each
+// _try_insert_edge on a full row, the redundancy of every pair of the merged list
+// (attrs_equal && cos > sigma, _kernels.py:356-366), is independent per pair: 256 threads
+// compute the norms |p - j|^2 and the pair dots in the reference's dimension order (separate
+// accumulation chains, same values) into a bit matrix, and thread 0 runs the greedy keep pass
+// over it.  In-degrees of the merged entries are loaded up front: within one insertion an
+// entry's in-degree changes only when that entry is dropped, and it is not read again.
+constexpr int kRcThreads = 256;
+constexpr int kRcMaxG = 256;
+
+struct RcShared {
+  int64_t mi[kRcMaxG + 1];
+  double md[kRcMaxG + 1];
+  double nrm[kRcMaxG + 1];
+  int32_t midg[kRcMaxG + 1];
+  uint8_t keep[kRcMaxG + 1];
+  int result, total, pos, flag;
+};
+
+// returns 1 if cand ends up in row j (all threads get the value)
+SB_DEV int cta_try_insert(SeqCtx& c, RcShared& S, uint32_t* bits, int64_t j, int64_t cand, double dd) {
+  const int tid = threadIdx.x;
+  const float d = __double2float_rn(dd);
+  int32_t* ri = c.ids + j * c.g;
+  float* rd = c.dists + j * c.g;
+  if (tid == 0) {
+    S.result = -1;
+    const int cj = c.counts[j];
+    bool dup = false;
+    for (int t = 0; t < cj && !dup; ++t) dup = ri[t] == cand;
+    if (dup) {
+      S.result = 0;
+    } else if (cj < c.g) {
+      int pos = cj;
+      while (pos > 0 && (rd[pos - 1] > d || (rd[pos - 1] == d && ri[pos - 1] > cand))) {
+        ri[pos] = ri[pos - 1];
+        rd[pos] = rd[pos - 1];
+        --pos;
+      }
+      ri[pos] = (int32_t)cand;
+      rd[pos] = d;
+      c.counts[j] = cj + 1;
+      c.in_deg[cand] += 1;
+      S.result = 1;
+    } else {
+      int pos = cj;
+      for (int t = 0; t < cj; ++t) { S.mi[t] = ri[t]; S.md[t] = (double)rd[t]; }
+      while (pos > 0 && (S.md[pos - 1] > (double)d ||
+                         (S.md[pos - 1] == (double)d && S.mi[pos - 1] > cand))) {
+        S.mi[pos] = S.mi[pos - 1];
+        S.md[pos] = S.md[pos - 1];
+        --pos;
+      }
+      S.mi[pos] = cand;
+      S.md[pos] = (double)d;
+      S.total = cj + 1;
+    }
+  }
+  __syncthreads();
+  if (S.result >= 0) {
+    const int r = S.result;
+    __syncthreads();
+    return r;
+  }
+  const int total = S.total;
+  const int W = (total + 31) >> 5;
+  const float* xj = c.F + j * c.m;
+  for (int t = tid; t < total; t += kRcThreads) {
+    const int64_t p = S.mi[t];
+    const float* xp = c.F + p * c.m;
+    double np2 = 0.0;
+    for (int u = 0; u < c.m; ++u) {
+      const double dp = dsub((double)xp[u], (double)xj[u]);
+      np2 = dadd(np2, dmul(dp, dp));
+    }
+    S.nrm[t] = np2;
+    S.midg[t] = p == cand ? 0 : c.in_deg[p];
+    S.keep[t] = 1;
+  }
+  for (int w = tid; w < total * W; w += kRcThreads) bits[w] = 0u;
+  __syncthreads();
+  // pair (t, u), u < t, enumerated over the lower triangle
+  const int pairs = total * (total - 1) / 2;
+  for (int e = tid; e < pairs; e += kRcThreads) {
+    int t = (int)((sqrt(8.0 * e + 1.0) + 1.0) * 0.5);
+    while (t * (t - 1) / 2 > e) --t;
+    while ((t + 1) * t / 2 <= e) ++t;
+    const int u = e - t * (t - 1) / 2;
+    const int64_t p = S.mi[t], k = S.mi[u];
+    if (!seq_attrs_equal(c, p, k)) continue;
+    double cs;
+    if (S.nrm[t] == 0.0 || S.nrm[u] == 0.0) {
+      cs = 1.0;
+    } else {
+      const float* xp = c.F + p * c.m;
+      const float* xk = c.F + k * c.m;
+      double dot = 0.0;
+      for (int q = 0; q < c.m; ++q) {
+        const double dp = dsub((double)xp[q], (double)xj[q]);
+        const double dk = dsub((double)xk[q], (double)xj[q]);
+        dot = dadd(dot, dmul(dp, dk));
+      }
+      cs = __ddiv_rn(dot, sqrt(dmul(S.nrm[t], S.nrm[u])));
+    }
+    if (cs > c.sigma) atomicOr(bits + t * W + (u >> 5), 1u << (u & 31));
+  }
+  __syncthreads();
+  if (tid == 0) {
+    // kept mask over list positions; at step t it holds exactly the kept u < t
+    uint32_t km[(kRcMaxG + 32) / 32];
+    for (int w = 0; w < W; ++w) km[w] = 0u;
+    km[0] = 1u;
+    int kept = 1;
+    for (int t = 1; t < total; ++t) {
+      bool red = false;
+      for (int w = 0; w <= (t >> 5) && !red; ++w) red = (bits[t * W + w] & km[w]) != 0u;
+      const int64_t p = S.mi[t];
+      if (red && (p == cand || S.midg[t] >= 2)) {
+        S.keep[t] = 0;
+      } else {
+        ++kept;
+        km[t >> 5] |= 1u << (t & 31);
+      }
+    }
+    if (kept > c.g) {
+      for (int t = total - 1; t >= 0; --t) {
+        if (!S.keep[t]) continue;
+        const int64_t p = S.mi[t];
+        if (p == cand) { S.keep[t] = 0; break; }
+        if (S.midg[t] >= 2) { S.keep[t] = 0; break; }
+      }
+    }
+    int w = 0, inserted = 0;
+    for (int t = 0; t < total; ++t) {
+      if (!S.keep[t]) {
+        if (S.mi[t] != cand) c.in_deg[S.mi[t]] -= 1;
+        continue;
+      }
+      ri[w] = (int32_t)S.mi[t];
+      rd[w] = __double2float_rn(S.md[t]);
+      if (S.mi[t] == cand) inserted = 1;
+      ++w;
+    }
+    c.counts[j] = w;
+    if (inserted) c.in_deg[cand] += 1;
+    S.result = inserted;
+  }
+  __syncthreads();
+  const int r = S.result;
+  __syncthreads();
+  return r;
+}
+
+__global__ void __launch_bounds__(kRcThreads) reconnect_cta_kernel(SeqCtx c, int64_t n) {
+  extern __shared__ __align__(16) uint32_t rc_bits[];
+  __shared__ RcShared S;
+  const int tid = threadIdx.x;
+  const volatile int32_t* indeg = c.in_deg;
+  for (int64_t base = 0; base < n; base += kRcThreads) {
+    int64_t from = base;
+    for (;;) {
+      // first node of this chunk at or after `from` with in-degree 0 (re-read after every
+      // node: an insertion can drop a later node's in-degree to 0)
+      if (tid == 0) S.flag = 0x7FFFFFFF;
+      __syncthreads();
+      const int64_t v0 = base + tid;
+      if (v0 >= from && v0 < n && indeg[v0] <= 0) atomicMin(&S.flag, tid);
+      __syncthreads();
+      const int first = S.flag;
+      __syncthreads();
+      if (first == 0x7FFFFFFF) break;
+      const int64_t v = base + first;
+      from = v + 1;
+      bool done = false;
+      const int cv = c.counts[v];
+      for (int t = 0; t < cv && !done; ++t) {
+        const int64_t u = c.ids[v * c.g + t];
+        done = cta_try_insert(c, S, rc_bits, u, v, (double)c.dists[v * c.g + t]) != 0;
+      }
+      if (tid == 0 && !done) {
+        for (int t = 0; t < c.counts[v] && !done; ++t) {
+          const int64_t u = c.ids[v * c.g + t];
+          done = seq_force_insert(c, u, v, (double)c.dists[v * c.g + t], false) != 0;
+        }
+        if (!done && c.counts[v] > 0)
+          seq_force_insert(c, c.ids[v * c.g], v, (double)c.dists[v * c.g], true);
+      }
+      __syncthreads();
+    }
+  }
+}
+
 __global__ void min_kernel(const int32_t* x, int64_t n, int* out) {
   int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i < n) atomicMin(out, x[i]);
@@ -537,8 +730,16 @@ int launch_seq_reinforce(const float* F, const int32_t* A, int m, int l, int g, 
   c.tmp_ids = reinterpret_cast<int64_t*>(p); p += sizeof(int64_t) * (g + 1);
   c.tmp_d = reinterpret_cast<double*>(p); p += sizeof(double) * (g + 1);
   c.keep = reinterpret_cast<uint8_t*>(p);
-  if (reconnect) reconnect_kernel<<<1, 1, 0, st>>>(c, n);
-  else reinforce_exact_kernel<<<1, 1, 0, st>>>(c, n);
+  if (reconnect) {
+    if (g > kRcMaxG) return (int)cudaErrorInvalidValue;
+    const size_t bits = sizeof(uint32_t) * (size_t)(g + 1) * ((g + 32) / 32);
+    cudaError_t e = cudaFuncSetAttribute(reconnect_cta_kernel,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bits);
+    if (e != cudaSuccess) return (int)e;
+    reconnect_cta_kernel<<<1, kRcThreads, bits, st>>>(c, n);
+  } else {
+    reinforce_exact_kernel<<<1, 1, 0, st>>>(c, n);
+  }
   return (int)cudaGetLastError();
 }
 

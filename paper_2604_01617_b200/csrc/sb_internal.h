@@ -100,14 +100,16 @@ int launch_tc_code(const int32_t* A, int64_t n, int l, const int32_t* lo, const 
 int launch_tc_scatter(const int32_t* code, int64_t n, const int64_t* off, unsigned long long* cur,
                       int32_t* orig, cudaStream_t st);
 int launch_tc_gather(const float* F, const int32_t* A, const int32_t* code_in, const int32_t* orig,
-                     int64_t n, int m, int l, void* Fb, int32_t* nx, int32_t* code, int32_t* As,
-                     cudaStream_t st);
-int launch_bf_tc_prep_queries(const double* qf, int64_t q, int m, void* Qb, int32_t* nq,
+                     int64_t n, int m, int mk, int l, void* Fb, int32_t* nx, int32_t* code,
+                     int32_t* As, cudaStream_t st);
+int launch_bf_tc_prep_queries(const double* qf, int64_t q, int m, int mk, void* Qb, int32_t* nq,
                               cudaStream_t st);
+// m below is the operand K: the feature count, plus 16 when fold (|x|^2 folded into the MMA)
 int launch_bf_tc(const void* Fb, const int32_t* nx, const int32_t* A, const int32_t* code,
                  const int32_t* orig, const void* Qb, const int32_t* nq, const int64_t* qa,
                  const int64_t* qmask, int64_t n, int64_t q, int m, int l, int kk, int splits,
-                 double alpha, double* part_d, uint32_t* part_i, int* gthr, cudaStream_t st);
+                 double alpha, double* part_d, uint32_t* part_i, int* gthr, int fold,
+                 cudaStream_t st);
 
 // ---- HELP build ---------------------------------------------------------------
 // random initial rows (help_init.cu): device ids, consumed PCG64 outputs, rows with repeats

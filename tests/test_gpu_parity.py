@@ -259,17 +259,21 @@ def test_order_free_mode_is_bit_exact():
                                 nbr_counts=cnt, frozen=True).device().info()["int_exact"]
 
 
-@pytest.mark.parametrize("n,m,l,q,k", [(5000, 128, 3, 300, 10), (3001, 64, 2, 129, 16),
-                                       (777, 32, 1, 5, 1), (20000, 128, 3, 1000, 10)])
-def test_tensor_core_topk_exact(n, m, l, q, k):
-    """tcgen05 path (integer data): identical ids and fp64 distances to the fp64 SIMT path and
-    to the oracle, including ragged tiles (n % 256, q % 128), masks and duplicate points."""
+@pytest.mark.parametrize("n,m,l,q,k,lo", [(5000, 128, 3, 300, 10, 0), (3001, 64, 2, 129, 16, 0),
+                                          (777, 32, 1, 5, 1, 0), (20000, 128, 3, 1000, 10, 0),
+                                          (4000, 48, 2, 200, 10, -255)])
+@pytest.mark.parametrize("fold", ["1", "0"])
+def test_tensor_core_topk_exact(n, m, l, q, k, lo, fold):
+    """tcgen05 path (integer data, with and without |x|^2 folded into the MMA): identical ids
+    and fp64 distances to the fp64 SIMT path and to the oracle, including ragged tiles
+    (n % 256, q % 128), masks, duplicate points and signed values."""
     import os
+    os.environ["SB_BF_FOLD"] = fold
     rng = np.random.default_rng(n + m)
-    f = np.clip(np.rint(rng.normal(128, 50, (n, m))), 0, 255).astype(np.float32)
+    f = np.clip(np.rint(rng.normal(128 + lo, 50 - lo / 3, (n, m))), lo, 255).astype(np.float32)
     f[10:20] = f[5]                      # exact duplicates: ties broken by id
     a = rng.integers(1, 6, (n, l)).astype(np.int32)
-    qf = np.clip(np.rint(rng.normal(128, 50, (q, m))), 0, 255)
+    qf = np.clip(np.rint(rng.normal(128 + lo, 50 - lo / 3, (q, m))), lo, 255)
     qf[0] = f[5]
     qa = rng.integers(1, 6, (q, l))
     masks = rng.integers(0, 2, (q, l))
@@ -291,6 +295,7 @@ def test_tensor_core_topk_exact(n, m, l, q, k):
                                         None if mk is None else mk[qi], return_dists=True)
             np.testing.assert_array_equal(ids_tc[qi], wi)
             np.testing.assert_array_equal(dd_tc[qi], wd)
+    del os.environ["SB_BF_FOLD"]
 
 
 @pytest.mark.slow
