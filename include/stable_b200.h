@@ -149,6 +149,11 @@ int sb_route_batch_dev(sb_index* idx, const double* qf, const double* qa, const 
                        const int64_t* entries, uint64_t seed, int64_t qi0, double inv_alpha,
                        int64_t* out_ids, double* out_dists, int64_t* out_stats);
 
+/* page-locked host memory (cudaHostAlloc) for inputs and results: copies to and from it run
+ * at full link speed, asynchronously */
+int sb_host_alloc(size_t bytes, void** out);
+int sb_host_free(void* p);
+
 /* number of kernel launches this handle issued since creation (instrumentation) */
 int64_t sb_launch_count(sb_index* idx);
 

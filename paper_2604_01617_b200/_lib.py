@@ -59,6 +59,8 @@ _SIGS = {
     "sb_set_distance_mode": [_vp, _i32],
     "sb_route_info": [_vp, _vp, _vp],
     "sb_route_prepare": [_vp],
+    "sb_host_alloc": [ctypes.c_size_t, _pp],
+    "sb_host_free": [_vp],
 }
 _RESTYPE = {"sb_last_error": ctypes.c_char_p, "sb_launch_count": ctypes.c_int64}
 
@@ -112,6 +114,35 @@ def device_count() -> int:
 def require_gpu() -> None:
     if device_count() < 1:
         raise RuntimeError("no CUDA device visible: the B200 path has no CPU fallback")
+
+
+# ---- page-locked result buffers ----------------------------------------------------------
+# Results come back through pinned memory (full-speed, asynchronous D2H).  Blocks are recycled:
+# a returned array owns its block until it (and every view of it) is garbage collected.
+_POOL: dict[int, list[int]] = {}
+
+
+def _release(nbytes: int, addr: int) -> None:
+    _POOL.setdefault(nbytes, []).append(addr)
+
+
+def pinned_empty(shape, dtype) -> np.ndarray:
+    """np.empty in page-locked host memory."""
+    import weakref
+    dt = np.dtype(dtype)
+    count = int(np.prod(shape))
+    nbytes = max(64, ((count * dt.itemsize + 4095) // 4096) * 4096)
+    free = _POOL.get(nbytes)
+    if free:
+        addr = free.pop()
+    else:
+        p = ctypes.c_void_p(0)
+        check(load().sb_host_alloc(nbytes, ctypes.byref(p)))
+        addr = p.value
+    buf = (ctypes.c_char * nbytes).from_address(addr)
+    arr = np.frombuffer(buf, dtype=dt, count=count).reshape(shape)
+    weakref.finalize(arr, _release, nbytes, addr)
+    return arr
 
 
 def ptr(a: np.ndarray | None):

@@ -216,6 +216,19 @@ int sb_index_info(sb_index* idx, int32_t* int_exact, double* fmax_abs, int32_t* 
   return SB_OK;
 }
 
+int sb_host_alloc(size_t bytes, void** out) {
+  if (!out) return fail(SB_EARG, "NULL argument");
+  *out = nullptr;
+  if (bytes == 0) return SB_OK;
+  CK(cudaHostAlloc(out, bytes, cudaHostAllocDefault));
+  return SB_OK;
+}
+
+int sb_host_free(void* p) {
+  if (p) CK(cudaFreeHost(p));
+  return SB_OK;
+}
+
 int sb_route_info(sb_index* idx, int32_t* path, int32_t* row_bytes) {
   if (!idx) return fail(SB_EARG, "idx is NULL");
   if (path) *path = idx->last_route_path;
@@ -893,7 +906,9 @@ int sb_bf_topk_queries(sb_index* idx, const double* qf, const int64_t* qa, const
     const double bound = nonneg ? std::max(2.0 * m * fx * fq, m * fx * fx)
                                 : 3.0 * m * std::max(fx, fq) * std::max(fx, fq);
     fold = bound < 16777216.0;
-    if (const char* e = getenv("SB_BF_FOLD")) fold = fold && atoi(e) != 0;
+    // measured neutral on cfg 2 (the epilogue is bound by barrier waits, not the filter):
+    // opt in with SB_BF_FOLD=1
+    { const char* e = getenv("SB_BF_FOLD"); fold = fold && e && atoi(e) != 0; }
     if (fold && !sb::bf_tc_supported(idx->m + 16, idx->l, k)) fold = false;
   }
   const int mk = fold ? idx->m + 16 : idx->m;
@@ -1190,6 +1205,17 @@ int sb_route_batch_dev(sb_index* idx, const double* qf, const double* qa, const 
                    out_ids, out_dists, out_stats);
 }
 
+// device address of page-locked host memory (cudaHostAlloc / registered), or null
+static void* mapped_host(const void* p) {
+  if (!p) return nullptr;
+  cudaPointerAttributes at;
+  if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
+    cudaGetLastError();
+    return nullptr;
+  }
+  return at.type == cudaMemoryTypeHost ? at.devicePointer : nullptr;
+}
+
 int sb_route_batch(sb_index* idx, const double* qf, const double* qa, const double* qmask,
                    int64_t q, int32_t k, int32_t pioneer, int32_t use_coarse,
                    const int64_t* entries, uint64_t seed, int64_t qi0, double inv_alpha,
@@ -1197,27 +1223,39 @@ int sb_route_batch(sb_index* idx, const double* qf, const double* qa, const doub
   if (!idx || !qf || !qa || !out_ids || !out_dists) return fail(SB_EARG, "NULL argument");
   if (q <= 0) return SB_OK;
   const int m = idx->m, l = idx->l;
+  // Results go through device memory and one copy at the end (page-locked result buffers
+  // make it a full-speed copy).  Writing page-locked results from the kernel itself over the
+  // link (SB_ROUTE_DIRECT=1) measured slower on cfg 2 (933k vs 983k e2e QPS).
+  const char* de = getenv("SB_ROUTE_DIRECT");
+  const bool want_direct = de && atoi(de) != 0;
+  int64_t* d_ids_h = want_direct ? static_cast<int64_t*>(mapped_host(out_ids)) : nullptr;
+  double* d_dists_h = want_direct ? static_cast<double*>(mapped_host(out_dists)) : nullptr;
+  int64_t* d_st_h = want_direct && out_stats ? static_cast<int64_t*>(mapped_host(out_stats)) : nullptr;
+  const bool direct = d_ids_h && d_dists_h && (!out_stats || d_st_h);
   // one device block for all per-call inputs/outputs
   size_t o_qf = 0, o_qa = o_qf + sizeof(double) * q * m, o_qm = o_qa + sizeof(double) * q * l;
   size_t o_en = o_qm + sizeof(double) * q * l, o_ids = o_en + (entries ? sizeof(int64_t) * q * k : 0);
   size_t o_d = o_ids + sizeof(int64_t) * q * k, o_st = o_d + sizeof(double) * q * k;
-  size_t total = o_st + sizeof(int64_t) * q * 5;
+  size_t total = direct ? o_ids : o_st + sizeof(int64_t) * q * 5;
   CK(idx->qf.ensure(total));
   char* base = idx->qf.as<char>();
   CK(cudaMemcpyAsync(base + o_qf, qf, sizeof(double) * q * m, cudaMemcpyHostToDevice, idx->st));
   CK(cudaMemcpyAsync(base + o_qa, qa, sizeof(double) * q * l, cudaMemcpyHostToDevice, idx->st));
   if (qmask) CK(cudaMemcpyAsync(base + o_qm, qmask, sizeof(double) * q * l, cudaMemcpyHostToDevice, idx->st));
   if (entries) CK(cudaMemcpyAsync(base + o_en, entries, sizeof(int64_t) * q * k, cudaMemcpyHostToDevice, idx->st));
+  int64_t* r_ids = direct ? d_ids_h : reinterpret_cast<int64_t*>(base + o_ids);
+  double* r_d = direct ? d_dists_h : reinterpret_cast<double*>(base + o_d);
+  int64_t* r_st = direct ? d_st_h : (out_stats ? reinterpret_cast<int64_t*>(base + o_st) : nullptr);
   int r = route_dev(idx, reinterpret_cast<double*>(base + o_qf), reinterpret_cast<double*>(base + o_qa),
                     qmask ? reinterpret_cast<double*>(base + o_qm) : nullptr, q, k, pioneer,
                     use_coarse, entries ? reinterpret_cast<int64_t*>(base + o_en) : nullptr, seed,
-                    qi0, inv_alpha, reinterpret_cast<int64_t*>(base + o_ids),
-                    reinterpret_cast<double*>(base + o_d),
-                    out_stats ? reinterpret_cast<int64_t*>(base + o_st) : nullptr);
+                    qi0, inv_alpha, r_ids, r_d, r_st);
   if (r) return r;
-  CK(cudaMemcpyAsync(out_ids, base + o_ids, sizeof(int64_t) * q * k, cudaMemcpyDeviceToHost, idx->st));
-  CK(cudaMemcpyAsync(out_dists, base + o_d, sizeof(double) * q * k, cudaMemcpyDeviceToHost, idx->st));
-  if (out_stats) CK(cudaMemcpyAsync(out_stats, base + o_st, sizeof(int64_t) * q * 5, cudaMemcpyDeviceToHost, idx->st));
+  if (!direct) {
+    CK(cudaMemcpyAsync(out_ids, base + o_ids, sizeof(int64_t) * q * k, cudaMemcpyDeviceToHost, idx->st));
+    CK(cudaMemcpyAsync(out_dists, base + o_d, sizeof(double) * q * k, cudaMemcpyDeviceToHost, idx->st));
+    if (out_stats) CK(cudaMemcpyAsync(out_stats, base + o_st, sizeof(int64_t) * q * 5, cudaMemcpyDeviceToHost, idx->st));
+  }
   CK(cudaStreamSynchronize(idx->st));
   return SB_OK;
 }

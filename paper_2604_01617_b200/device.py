@@ -204,9 +204,9 @@ class DeviceIndex:
         qm = None if qmask is None else c64(np.atleast_2d(qmask), np.float64)
         ent = None if entries is None else c64(np.atleast_2d(entries), np.int64)
         q = qf.shape[0]
-        ids = np.empty((q, k), np.int64)
-        dists = np.empty((q, k), np.float64)
-        st = np.empty((q, 5), np.int64) if stats else None
+        ids = _lib.pinned_empty((q, k), np.int64)
+        dists = _lib.pinned_empty((q, k), np.float64)
+        st = _lib.pinned_empty((q, 5), np.int64) if stats else None
         _lib.call("sb_route_batch", self._h, ptr(qf), ptr(qa), ptr(qm), q, int(k), int(pioneer),
                   1 if use_coarse else 0, ptr(ent), int(seed), int(qi0), float(inv_alpha),
                   ptr(ids), ptr(dists), ptr(st))
