@@ -102,7 +102,8 @@ struct IdOrder {
   uint32_t n;
   SB_DEV uint32_t key(uint32_t i) const { return (perm && i < n) ? (uint32_t)__ldg(perm + i) : i; }
   SB_DEV bool operator()(double da, uint32_t ia, double db, uint32_t ib) const {
-    return da < db || (da == db && key(ia) < key(ib));
+    if (__builtin_expect(da != db, 1)) return da < db;
+    return key(ia) < key(ib);
   }
 };
 struct PlainOrder {

@@ -642,6 +642,9 @@ int launch_pack_u8(const float* F, int64_t n, int m, uint8_t* F8, int32_t* nx, c
 // their features, so the nodes one query visits sit close together: their visited bits share
 // words and sectors, and their rows, attributes and adjacency share DRAM pages.  Any order is
 // exact (ties still compare original ids); this one only changes speed.
+#ifndef ROUTE_ORD_RADEMACHER
+#define ROUTE_ORD_RADEMACHER 1  // +-1 projections (measured equal to Gaussian ones)
+#endif
 #ifndef ROUTE_ORD_DIMS
 #define ROUTE_ORD_DIMS 6
 #endif
@@ -650,12 +653,26 @@ int launch_pack_u8(const float* F, int64_t n, int m, uint8_t* F8, int32_t* nx, c
 #endif
 constexpr int kOrdDims = ROUTE_ORD_DIMS, kOrdBits = ROUTE_ORD_BITS;
 
-SB_DEV float rademacher(int d, int p) {
-  uint32_t h = (uint32_t)(d * kOrdDims + p) * 0x9E3779B1u;
-  h ^= h >> 15;
-  h *= 0x85EBCA77u;
-  h ^= h >> 13;
-  return (h & 1u) ? 1.f : -1.f;
+SB_DEV uint32_t ord_hash(uint32_t x) {
+  x *= 0x9E3779B1u;
+  x ^= x >> 15;
+  x *= 0x85EBCA77u;
+  x ^= x >> 13;
+  x *= 0xC2B2AE3Du;
+  x ^= x >> 16;
+  return x;
+}
+
+// fixed Gaussian projection matrix entry (Box-Muller from two hashed uniforms)
+SB_DEV float proj_coef(int d, int p) {
+#if ROUTE_ORD_RADEMACHER
+  return (ord_hash((uint32_t)(d * kOrdDims + p)) & 1u) ? 1.f : -1.f;
+#else
+  const uint32_t k = (uint32_t)(d * kOrdDims + p);
+  const float u1 = ((ord_hash(2 * k) >> 8) + 1) * (1.0f / 16777217.0f);
+  const float u2 = (ord_hash(2 * k + 1) >> 8) * (1.0f / 16777216.0f);
+  return sqrtf(-2.0f * __logf(u1)) * __cosf(6.28318531f * u2);
+#endif
 }
 
 __global__ void order_project_kernel(const float* F, int64_t n, int m, float* proj, unsigned* lohi) {
@@ -667,7 +684,7 @@ __global__ void order_project_kernel(const float* F, int64_t n, int m, float* pr
   for (int t = lane_id(); t < m; t += 32) {
     const float x = F[v * m + t];
 #pragma unroll
-    for (int p = 0; p < kOrdDims; ++p) acc[p] += rademacher(t, p) * x;
+    for (int p = 0; p < kOrdDims; ++p) acc[p] += proj_coef(t, p) * x;
   }
 #pragma unroll
   for (int p = 0; p < kOrdDims; ++p) {
