@@ -150,3 +150,21 @@ def test_index_format_round_trip_host(small_golden, tmp_path):
     p1.write_bytes(p1.read_bytes()[:-3])
     with pytest.raises(sb.FormatError, match="truncated"):
         sb.read_index(p1)
+
+
+def test_no_cpu_fallback(tmp_path):
+    """The product path has no CPU fallback: without a GPU every device entry point raises,
+    and a missing shared library raises at load time."""
+    import subprocess
+    import sys
+    from paper_2604_01617_b200 import _lib
+    from paper_2604_01617_b200.device import DeviceIndex
+    if _lib.device_count() == 0:
+        with pytest.raises(RuntimeError, match="no CUDA device"):
+            DeviceIndex(np.zeros((10, 4), np.float32), np.ones((10, 1), np.int32), 4)
+    code = ("import paper_2604_01617_b200._lib as L\n"
+            "try:\n    L.load()\nexcept RuntimeError as e:\n    print('raised', e)\n")
+    env = dict(os.environ, STABLE_B200_LIB=str(tmp_path / "missing.so"))
+    out = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, env=env,
+                         cwd=os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    assert "raised" in out.stdout and "missing" in out.stdout
