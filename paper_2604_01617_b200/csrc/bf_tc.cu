@@ -20,6 +20,7 @@
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <stdlib.h>
 
 #include "common.cuh"
 #include "sb_internal.h"
@@ -165,8 +166,10 @@ struct TcArgs {
 // accumulator ready and B stage free again), empty (all 256 epilogue threads finished the
 // tile: accumulator and metadata free).  Rows for tile i + 1 load while MMA i runs; MMA i + 1
 // starts as soon as the epilogue leaves tile i - 1.
-template <bool FOLD>
-__global__ void __launch_bounds__(kTcThreads + 32, 1) bf_tc_kernel(TcArgs a) {
+// NBS = shared-memory stages for node rows: 2 (one CTA per SM, N = 256) or 1 (two CTAs per SM,
+// N = 128: the other CTA's epilogue covers this one's row load)
+template <bool FOLD, int NBS>
+__global__ void __launch_bounds__(kTcThreads + 32, NBS == 1 ? 2 : 1) bf_tc_kernel(TcArgs a) {
   extern __shared__ __align__(1024) char smem[];
   const int tid = threadIdx.x;
   const int m = a.m, N = a.N, l = a.l;
@@ -175,7 +178,7 @@ __global__ void __launch_bounds__(kTcThreads + 32, 1) bf_tc_kernel(TcArgs a) {
   // shared layout: A tile | 2 x B tile | 2 x (nx | code | orig | attrs) | lists | t2 | barriers
   char* p = smem;
   char* sA = p; p += (size_t)kTcM * m * 2;
-  char* sB = p; p += 2 * b_bytes;
+  char* sB = p; p += NBS * b_bytes;
   char* sM = p; p += 2 * meta_bytes;
   double* ld = reinterpret_cast<double*>(p); p += sizeof(double) * (size_t)a.kk * kTcThreads;
   uint32_t* li = reinterpret_cast<uint32_t*>(p); p += sizeof(uint32_t) * (size_t)a.kk * kTcThreads;
@@ -228,7 +231,7 @@ __global__ void __launch_bounds__(kTcThreads + 32, 1) bf_tc_kernel(TcArgs a) {
       mbar_expect_tx(bar_a, a_bytes);
       bulk_g2s(smem_u32(sA), a.Qb + (size_t)q0 * m * 2, a_bytes, bar_a);
       auto load_rows = [&](int i) {
-        const int s = i & 1;
+        const int s = NBS == 1 ? 0 : (i & 1);
         const int64_t v0 = (t_begin + i) * (int64_t)N;
         mbar_expect_tx(bar_fullB + 8 * s, (uint32_t)b_bytes);
         bulk_g2s(smem_u32(sB + s * b_bytes), a.Fb + (size_t)v0 * m * 2, (uint32_t)b_bytes,
@@ -252,9 +255,10 @@ __global__ void __launch_bounds__(kTcThreads + 32, 1) bf_tc_kernel(TcArgs a) {
         bulk_g2s(smem_u32(meta + N * 4), a.code + v0, (uint32_t)(N * 4), fm);
         bulk_g2s(smem_u32(meta + N * 8), a.orig + v0, (uint32_t)(N * 4), fm);
         bulk_g2s(smem_u32(meta + N * 12), a.A + v0 * l, (uint32_t)(N * l * 4), fm);
-        mbar_wait(bar_fullB + 8 * s, ph);
+        const int sb = NBS == 1 ? 0 : s;
+        mbar_wait(bar_fullB + 8 * sb, NBS == 1 ? (uint32_t)(i & 1) : ph);
         tc_fence_after();
-        const uint32_t a0 = smem_u32(sA), b0 = smem_u32(sB + s * b_bytes);
+        const uint32_t a0 = smem_u32(sA), b0 = smem_u32(sB + sb * b_bytes);
         for (int k = 0; k < m / 16; ++k) {
           uint64_t ad = umma_desc(a0 + (uint32_t)k * 256, 128, sbo);
           uint64_t bd = umma_desc(b0 + (uint32_t)k * 256, 128, sbo);
@@ -265,9 +269,11 @@ __global__ void __launch_bounds__(kTcThreads + 32, 1) bf_tc_kernel(TcArgs a) {
               "l"(ad), "l"(bd), "r"(idesc), "r"(k > 0 ? 1u : 0u));
         }
         mma_commit(bar_done + 8 * s);
-        // rows of tile i + 1 go to B stage s ^ 1, free once MMA i - 1 has completed
+        // rows of tile i + 1 go to B stage s ^ 1, free once MMA i - 1 has completed (one
+        // stage: once MMA i has)
         if (i + 1 < ntl) {
-          if (i >= 1) mbar_wait(bar_done + 8 * (s ^ 1), (uint32_t)(((i - 1) >> 1) & 1));
+          if (NBS == 1) mbar_wait(bar_done + 8 * s, ph);
+          else if (i >= 1) mbar_wait(bar_done + 8 * (s ^ 1), (uint32_t)(((i - 1) >> 1) & 1));
           load_rows(i + 1);
         }
       }
@@ -437,18 +443,33 @@ __global__ void __launch_bounds__(kTcThreads + 32, 1) bf_tc_kernel(TcArgs a) {
   }
 }
 
-size_t bf_tc_smem_n(int m, int l, int kk, int N) {
-  return (size_t)kTcM * m * 2 + 2 * ((size_t)N * m * 2 + (size_t)N * (3 + l) * 4) +
+size_t bf_tc_smem_n(int m, int l, int kk, int N, int nbs) {
+  return (size_t)kTcM * m * 2 + (size_t)nbs * N * m * 2 + 2 * (size_t)N * (3 + l) * 4 +
          (sizeof(double) + sizeof(uint32_t)) * (size_t)kk * kTcThreads + sizeof(float) * kTcThreads +
          8 + 80 + 16;
 }
 
-// widest tile (N = 256 or 128 nodes) whose double-buffered stages fit in shared memory; 0 if none
-int bf_tc_tile(int m, int l, int kk) {
+// Tile shape.  Two CTAs per SM (N = 128, one row stage, <= 113 KB each) when they fit and
+// SB_BF_PAIR is not 0; else one CTA with N = 256 (or 128) and two row stages.  Returns N.
+int bf_tc_tile(int m, int l, int kk, int* nbs = nullptr) {
   if (m % 16 != 0 || m > 256 || l > 8 || kk > kTcMaxKK) return 0;
+  const char* e = getenv("SB_BF_PAIR");
+  const bool pair = e ? atoi(e) != 0 : true;
+  if (pair && bf_tc_smem_n(m, l, kk, 128, 1) <= 113 * 1024) {
+    if (nbs) *nbs = 1;
+    return 128;
+  }
   for (int N = 256; N >= 128; N >>= 1)
-    if (bf_tc_smem_n(m, l, kk, N) <= 227 * 1024) return N;
+    if (bf_tc_smem_n(m, l, kk, N, 2) <= 227 * 1024) {
+      if (nbs) *nbs = 2;
+      return N;
+    }
   return 0;
+}
+
+int bf_tc_ctas_per_sm(int m, int l, int kk) {
+  int nbs = 2;
+  return bf_tc_tile(m, l, kk, &nbs) != 0 && nbs == 1 ? 2 : 1;
 }
 
 int bf_tc_supported(int m, int l, int kk) { return bf_tc_tile(m, l, kk) != 0; }
@@ -558,10 +579,12 @@ int launch_bf_tc(const void* Fb, const int32_t* nx, const int32_t* A, const int3
   a.Qb = (const char*)Qb;
   a.nq = nq; a.qa = qa; a.qmask = qmask; a.n = n; a.q = q; a.m = m; a.l = l; a.kk = kk;
   a.splits = splits; a.alpha = alpha; a.part_d = part_d; a.part_i = part_i;
-  a.N = bf_tc_tile(m, l, kk);
+  int nbs = 2;
+  a.N = bf_tc_tile(m, l, kk, &nbs);
   if (a.N == 0) return (int)cudaErrorInvalidValue;
-  size_t smem = bf_tc_smem_n(m, l, kk, a.N);
-  auto kern = fold ? bf_tc_kernel<true> : bf_tc_kernel<false>;
+  size_t smem = bf_tc_smem_n(m, l, kk, a.N, nbs);
+  auto kern = nbs == 1 ? (fold ? bf_tc_kernel<true, 1> : bf_tc_kernel<false, 1>)
+                       : (fold ? bf_tc_kernel<true, 2> : bf_tc_kernel<false, 2>);
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return (int)e;
   dim3 grid((unsigned)((q + kTcM - 1) / kTcM), (unsigned)splits);

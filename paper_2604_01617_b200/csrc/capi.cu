@@ -981,8 +981,9 @@ int sb_bf_topk_queries(sb_index* idx, const double* qf, const int64_t* qa, const
     const int groups = (int)((q + 127) / 128);
     int splits = 1;
     double best = 1e30;
+    const int slots = idx->sms * sb::bf_tc_ctas_per_sm(mk, idx->l, kk);
     for (int s2 = 1; s2 <= 8 && (int64_t)s2 * 256 <= n; ++s2) {
-      double waves = (double)((groups * s2 + idx->sms - 1) / idx->sms);
+      double waves = (double)((groups * s2 + slots - 1) / slots);
       double cost = waves / s2;
       if (cost < best - 1e-9) { best = cost; splits = s2; }
     }

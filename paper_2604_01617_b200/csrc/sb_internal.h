@@ -92,6 +92,7 @@ int launch_bf_merge_k(const BfArgs& a, int kout, int64_t* out_ids64, int32_t* ou
 
 // tensor-core query-mode top-k for integer data (bf_tc.cu)
 int bf_tc_supported(int m, int l, int kk);
+int bf_tc_ctas_per_sm(int m, int l, int kk);
 constexpr int kTcNodePad = 256;  // node arrays of the tensor-core path are padded to this
 int launch_tc_attr_range(const int32_t* A, int64_t n, int l, int32_t* lo, int32_t* hi,
                          cudaStream_t st);
