@@ -20,6 +20,7 @@
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <stdio.h>
 #include <stdlib.h>
 
 #include "common.cuh"
@@ -166,10 +167,10 @@ struct TcArgs {
 // accumulator ready and B stage free again), empty (all 256 epilogue threads finished the
 // tile: accumulator and metadata free).  Rows for tile i + 1 load while MMA i runs; MMA i + 1
 // starts as soon as the epilogue leaves tile i - 1.
-// NBS = shared-memory stages for node rows: 2 (one CTA per SM, N = 256) or 1 (two CTAs per SM,
-// N = 128: the other CTA's epilogue covers this one's row load)
-template <bool FOLD, int NBS>
-__global__ void __launch_bounds__(kTcThreads + 32, NBS == 1 ? 2 : 1) bf_tc_kernel(TcArgs a) {
+// NBS = shared-memory stages for node rows (1 or 2), CTAS = CTAs per SM the shape is sized
+// for (the other CTA's epilogue covers this one's waits)
+template <bool FOLD, int NBS, int CTAS>
+__global__ void __launch_bounds__(kTcThreads + 32, CTAS) bf_tc_kernel(TcArgs a) {
   extern __shared__ __align__(1024) char smem[];
   const int tid = threadIdx.x;
   const int m = a.m, N = a.N, l = a.l;
@@ -449,30 +450,39 @@ size_t bf_tc_smem_n(int m, int l, int kk, int N, int nbs) {
          8 + 80 + 16;
 }
 
-// Tile shape.  Two CTAs per SM (N = 128, one row stage, <= 113 KB each) when they fit and
-// SB_BF_PAIR is not 0; else one CTA with N = 256 (or 128) and two row stages.  Returns N.
-int bf_tc_tile(int m, int l, int kk, int* nbs = nullptr) {
-  if (m % 16 != 0 || m > 256 || l > 8 || kk > kTcMaxKK) return 0;
-  const char* e = getenv("SB_BF_PAIR");
-  const bool pair = e ? atoi(e) != 0 : true;
-  if (pair && bf_tc_smem_n(m, l, kk, 128, 1) <= 113 * 1024) {
-    if (nbs) *nbs = 1;
-    return 128;
-  }
-  for (int N = 256; N >= 128; N >>= 1)
-    if (bf_tc_smem_n(m, l, kk, N, 2) <= 227 * 1024) {
-      if (nbs) *nbs = 2;
-      return N;
-    }
-  return 0;
+// Tile shapes (N nodes per tile, row stages, CTAs per SM), in order of preference; the first
+// that fits shared memory is used.  SB_BF_TILE = "N,stages,ctas" forces one (testing).
+struct TcShape { int N, nbs, ctas; };
+static const TcShape kTcShapes[] = {{128, 1, 2}, {64, 2, 2}, {256, 2, 1}, {128, 2, 1}};
+
+static bool tc_shape_fits(int m, int l, int kk, const TcShape& t) {
+  const size_t limit = t.ctas == 2 ? 113 * 1024 : 227 * 1024;
+  return bf_tc_smem_n(m, l, kk, t.N, t.nbs) <= limit;
 }
 
-int bf_tc_ctas_per_sm(int m, int l, int kk) {
-  int nbs = 2;
-  return bf_tc_tile(m, l, kk, &nbs) != 0 && nbs == 1 ? 2 : 1;
+static TcShape tc_shape(int m, int l, int kk) {
+  if (m % 16 != 0 || m > 256 || l > 8 || kk > kTcMaxKK) return {0, 0, 0};
+  if (const char* e = getenv("SB_BF_TILE")) {
+    TcShape t{0, 0, 0};
+    if (sscanf(e, "%d,%d,%d", &t.N, &t.nbs, &t.ctas) == 3 && tc_shape_fits(m, l, kk, t)) return t;
+  }
+  for (const TcShape& t : kTcShapes)
+    if (tc_shape_fits(m, l, kk, t)) return t;
+  return {0, 0, 0};
+}
+
+int bf_tc_tile(int m, int l, int kk, int* nbs = nullptr) {
+  const TcShape t = tc_shape(m, l, kk);
+  if (nbs) *nbs = t.nbs;
+  return t.N;
 }
 
 int bf_tc_supported(int m, int l, int kk) { return bf_tc_tile(m, l, kk) != 0; }
+
+int bf_tc_ctas_per_sm(int m, int l, int kk) {
+  const TcShape t = tc_shape(m, l, kk);
+  return t.N ? t.ctas : 1;
+}
 
 // ---- attribute-grouped node order ---------------------------------------------------
 __global__ void tc_attr_range_kernel(const int32_t* A, int64_t n, int l, int32_t* lo, int32_t* hi) {
@@ -579,12 +589,14 @@ int launch_bf_tc(const void* Fb, const int32_t* nx, const int32_t* A, const int3
   a.Qb = (const char*)Qb;
   a.nq = nq; a.qa = qa; a.qmask = qmask; a.n = n; a.q = q; a.m = m; a.l = l; a.kk = kk;
   a.splits = splits; a.alpha = alpha; a.part_d = part_d; a.part_i = part_i;
-  int nbs = 2;
-  a.N = bf_tc_tile(m, l, kk, &nbs);
+  const TcShape sh = tc_shape(m, l, kk);
+  a.N = sh.N;
   if (a.N == 0) return (int)cudaErrorInvalidValue;
-  size_t smem = bf_tc_smem_n(m, l, kk, a.N, nbs);
-  auto kern = nbs == 1 ? (fold ? bf_tc_kernel<true, 1> : bf_tc_kernel<false, 1>)
-                       : (fold ? bf_tc_kernel<true, 2> : bf_tc_kernel<false, 2>);
+  size_t smem = bf_tc_smem_n(m, l, kk, a.N, sh.nbs);
+  void (*kern)(TcArgs);
+  if (sh.nbs == 1) kern = fold ? bf_tc_kernel<true, 1, 2> : bf_tc_kernel<false, 1, 2>;
+  else if (sh.ctas == 2) kern = fold ? bf_tc_kernel<true, 2, 2> : bf_tc_kernel<false, 2, 2>;
+  else kern = fold ? bf_tc_kernel<true, 2, 1> : bf_tc_kernel<false, 2, 1>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return (int)e;
   dim3 grid((unsigned)((q + kTcM - 1) / kTcM), (unsigned)splits);
