@@ -19,6 +19,7 @@
 // epilogue mostly costs one fp32 compare per (query, node).
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
+#include <limits.h>
 #include <stdint.h>
 #include <stdio.h>
 #include <stdlib.h>
@@ -90,6 +91,11 @@ SB_DEV void tmem_ld16(uint32_t taddr, uint32_t (&r)[16]) {
 SB_DEV size_t rg_off(int64_t row, int kc, int m) {
   return (size_t)(row >> 3) * (size_t)(8 * m * 2) + (size_t)kc * 128 + (size_t)(row & 7) * 16;
 }
+// the same layout for 8-bit operands: a 16-byte chunk holds 16 elements, rows are m bytes
+SB_DEV size_t rg_off8(int64_t row, int t, int m) {
+  return (size_t)(row >> 3) * (size_t)(8 * m) + (size_t)(t >> 4) * 128 + (size_t)(row & 7) * 16 +
+         (size_t)(t & 15);
+}
 
 SB_DEV void mbar_arrive(uint32_t bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
@@ -135,6 +141,21 @@ __global__ void tc_prep_queries_kernel(const double* qf, int64_t q, int64_t qpad
   if (lane_id() == 0 && i < q) nq[i] = acc;
 }
 
+// u8 operands: queries and node rows as bytes in the row-group layout (m-byte rows)
+__global__ void tc_prep_queries_u8_kernel(const double* qf, int64_t q, int64_t qpad, int m,
+                                          uint8_t* Qb, int32_t* nq) {
+  int64_t i = (int64_t)blockIdx.x * (blockDim.x >> 5) + warp_id();
+  if (i >= qpad) return;
+  int acc = 0;
+  for (int t = lane_id(); t < m; t += 32) {
+    const int x = i < q ? (int)qf[i * m + t] : 0;
+    Qb[rg_off8(i, t, m)] = (uint8_t)x;
+    acc += x * x;
+  }
+  acc = warp_sum(acc);
+  if (lane_id() == 0 && i < q) nq[i] = acc;
+}
+
 // ---- main kernel -------------------------------------------------------------------------
 struct TcArgs {
   // node arrays in attribute-grouped order (tc_prepare): nodes with one attribute tuple are
@@ -169,16 +190,22 @@ struct TcArgs {
 // starts as soon as the epilogue leaves tile i - 1.
 // NBS = shared-memory stages for node rows (1 or 2), CTAS = CTAs per SM the shape is sized
 // for (the other CTA's epilogue covers this one's waits)
-template <bool FOLD, int NBS, int CTAS>
+// KIND: 0 = bf16 operands, 1 = bf16 with |x|^2 folded into the MMA, 2 = u8 operands
+// (tcgen05 kind::i8, exact int32 accumulation; integer data in [0, 255])
+template <int KIND, int NBS, int CTAS>
 __global__ void __launch_bounds__(kTcThreads + 32, CTAS) bf_tc_kernel(TcArgs a) {
+  constexpr bool FOLD = KIND == 1;
+  constexpr bool U8 = KIND == 2;
+  constexpr int ESZ = U8 ? 1 : 2;  // operand bytes per element
   extern __shared__ __align__(1024) char smem[];
   const int tid = threadIdx.x;
   const int m = a.m, N = a.N, l = a.l;
-  const size_t b_bytes = (size_t)N * m * 2;
+  const int rowb = m * ESZ;        // operand bytes per row
+  const size_t b_bytes = (size_t)N * rowb;
   const size_t meta_bytes = (size_t)N * (3 + l) * 4;
   // shared layout: A tile | 2 x B tile | 2 x (nx | code | orig | attrs) | lists | t2 | barriers
   char* p = smem;
-  char* sA = p; p += (size_t)kTcM * m * 2;
+  char* sA = p; p += (size_t)kTcM * rowb;
   char* sB = p; p += NBS * b_bytes;
   char* sM = p; p += 2 * meta_bytes;
   double* ld = reinterpret_cast<double*>(p); p += sizeof(double) * (size_t)a.kk * kTcThreads;
@@ -228,21 +255,22 @@ __global__ void __launch_bounds__(kTcThreads + 32, CTAS) bf_tc_kernel(TcArgs a) 
   if (warp_id() == kTcThreads / 32) {
     // ---------------- producer / MMA issuer ----------------
     if (lane_id() == 0) {
-      const uint32_t a_bytes = (uint32_t)(kTcM * m * 2);
+      const uint32_t a_bytes = (uint32_t)(kTcM * rowb);
       mbar_expect_tx(bar_a, a_bytes);
-      bulk_g2s(smem_u32(sA), a.Qb + (size_t)q0 * m * 2, a_bytes, bar_a);
+      bulk_g2s(smem_u32(sA), a.Qb + (size_t)q0 * rowb, a_bytes, bar_a);
       auto load_rows = [&](int i) {
         const int s = NBS == 1 ? 0 : (i & 1);
         const int64_t v0 = (t_begin + i) * (int64_t)N;
         mbar_expect_tx(bar_fullB + 8 * s, (uint32_t)b_bytes);
-        bulk_g2s(smem_u32(sB + s * b_bytes), a.Fb + (size_t)v0 * m * 2, (uint32_t)b_bytes,
+        bulk_g2s(smem_u32(sB + s * b_bytes), a.Fb + (size_t)v0 * rowb, (uint32_t)b_bytes,
                  bar_fullB + 8 * s);
       };
       if (ntl > 0) load_rows(0);
       mbar_wait(bar_a, 0);
-      const uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(N >> 3) << 17) |
-                             ((uint32_t)(kTcM >> 4) << 24);
-      const uint32_t sbo = (uint32_t)(m / 8) * 128;
+      // BF16 x BF16 -> F32, or U8 x U8 -> S32 (c_format bits [4,6), a/b formats [7,13))
+      const uint32_t idesc = (U8 ? (2u << 4) : ((1u << 4) | (1u << 7) | (1u << 10))) |
+                             ((uint32_t)(N >> 3) << 17) | ((uint32_t)(kTcM >> 4) << 24);
+      const uint32_t sbo = (uint32_t)(rowb / 16) * 128;
       for (int i = 0; i < ntl; ++i) {
         const int s = i & 1;
         const uint32_t ph = (uint32_t)((i >> 1) & 1);
@@ -260,14 +288,22 @@ __global__ void __launch_bounds__(kTcThreads + 32, CTAS) bf_tc_kernel(TcArgs a) 
         mbar_wait(bar_fullB + 8 * sb, NBS == 1 ? (uint32_t)(i & 1) : ph);
         tc_fence_after();
         const uint32_t a0 = smem_u32(sA), b0 = smem_u32(sB + sb * b_bytes);
-        for (int k = 0; k < m / 16; ++k) {
+        // one MMA per 32 bytes of K (16 bf16 or 32 u8 elements)
+        for (int k = 0; k < rowb / 32; ++k) {
           uint64_t ad = umma_desc(a0 + (uint32_t)k * 256, 128, sbo);
           uint64_t bd = umma_desc(b0 + (uint32_t)k * 256, 128, sbo);
-          asm volatile(
-              "{\n\t.reg .pred p;\n\t"
-              "setp.ne.b32 p, %4, 0;\n\t"
-              "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(tmem + (uint32_t)(s * N)),
-              "l"(ad), "l"(bd), "r"(idesc), "r"(k > 0 ? 1u : 0u));
+          if (U8)
+            asm volatile(
+                "{\n\t.reg .pred p;\n\t"
+                "setp.ne.b32 p, %4, 0;\n\t"
+                "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(tmem + (uint32_t)(s * N)),
+                "l"(ad), "l"(bd), "r"(idesc), "r"(k > 0 ? 1u : 0u));
+          else
+            asm volatile(
+                "{\n\t.reg .pred p;\n\t"
+                "setp.ne.b32 p, %4, 0;\n\t"
+                "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(tmem + (uint32_t)(s * N)),
+                "l"(ad), "l"(bd), "r"(idesc), "r"(k > 0 ? 1u : 0u));
         }
         mma_commit(bar_done + 8 * s);
         // rows of tile i + 1 go to B stage s ^ 1, free once MMA i - 1 has completed (one
@@ -329,34 +365,60 @@ __global__ void __launch_bounds__(kTcThreads + 32, CTAS) bf_tc_kernel(TcArgs a) 
         tmem_ld16(lane_base + (uint32_t)(s * N + c * 16), r);
         if (!qok) continue;
         const int c0 = half * cols + c * 16;
-        float y[16];
-        float mx = -3.4e38f;
-        if (FOLD) {
-          // the accumulator already holds y = 2 x.q - |x|^2 (exact integers below 2^24)
-#pragma unroll
-          for (int j = 0; j < 16; ++j) y[j] = __uint_as_float(r[j]);
-        } else {
-#pragma unroll
-          for (int q4 = 0; q4 < 4; ++q4) {
-            const float4 v = *reinterpret_cast<const float4*>(s_nx + c0 + 4 * q4);
-            y[4 * q4 + 0] = fmaf(2.0f, __uint_as_float(r[4 * q4 + 0]), -v.x);
-            y[4 * q4 + 1] = fmaf(2.0f, __uint_as_float(r[4 * q4 + 1]), -v.y);
-            y[4 * q4 + 2] = fmaf(2.0f, __uint_as_float(r[4 * q4 + 2]), -v.z);
-            y[4 * q4 + 3] = fmaf(2.0f, __uint_as_float(r[4 * q4 + 3]), -v.w);
-          }
-        }
-#pragma unroll
-        for (int j = 0; j < 16; ++j) mx = fmaxf(mx, y[j]);
         // columns are in attribute-grouped order: if both ends of the chunk carry the current
         // tuple, the whole chunk does, and one threshold covers all 16 columns
         const bool uniform = s_code[c0] == last_code && s_code[c0 + 15] == last_code;
-        if (uniform && mx < thr) continue;
         unsigned cand = 0;
-        if (uniform) {
+        if (U8) {
+          // int32 dot products and |x|^2: y = 2 x.q - |x|^2 and the test stay integer
+          // (y >= thr  <=>  y >= floor(thr) for integer y, conservatively)
+          const int32_t* s_nxi = reinterpret_cast<const int32_t*>(s_nx);
+          int yi[16];
+          int mxi = INT_MIN;
 #pragma unroll
-          for (int j = 0; j < 16; ++j) cand |= (y[j] >= thr ? 1u : 0u) << j;
+          for (int q4 = 0; q4 < 4; ++q4) {
+            const int4 v = *reinterpret_cast<const int4*>(s_nxi + c0 + 4 * q4);
+            yi[4 * q4 + 0] = 2 * (int)r[4 * q4 + 0] - v.x;
+            yi[4 * q4 + 1] = 2 * (int)r[4 * q4 + 1] - v.y;
+            yi[4 * q4 + 2] = 2 * (int)r[4 * q4 + 2] - v.z;
+            yi[4 * q4 + 3] = 2 * (int)r[4 * q4 + 3] - v.w;
+          }
+#pragma unroll
+          for (int j = 0; j < 16; ++j) mxi = max(mxi, yi[j]);
+          const int thri = thr < -2.0e9f ? INT_MIN : (thr > 2.0e9f ? INT_MAX : __float2int_rd(thr));
+          if (uniform && mxi < thri) continue;
+          if (uniform) {
+#pragma unroll
+            for (int j = 0; j < 16; ++j) cand |= (yi[j] >= thri ? 1u : 0u) << j;
+          } else {
+            cand = 0xFFFFu;  // mixed chunk: decide column by column below
+          }
         } else {
-          cand = 0xFFFFu;  // mixed chunk: decide column by column below
+          float y[16];
+          float mx = -3.4e38f;
+          if (FOLD) {
+            // the accumulator already holds y = 2 x.q - |x|^2 (exact integers below 2^24)
+#pragma unroll
+            for (int j = 0; j < 16; ++j) y[j] = __uint_as_float(r[j]);
+          } else {
+#pragma unroll
+            for (int q4 = 0; q4 < 4; ++q4) {
+              const float4 v = *reinterpret_cast<const float4*>(s_nx + c0 + 4 * q4);
+              y[4 * q4 + 0] = fmaf(2.0f, __uint_as_float(r[4 * q4 + 0]), -v.x);
+              y[4 * q4 + 1] = fmaf(2.0f, __uint_as_float(r[4 * q4 + 1]), -v.y);
+              y[4 * q4 + 2] = fmaf(2.0f, __uint_as_float(r[4 * q4 + 2]), -v.z);
+              y[4 * q4 + 3] = fmaf(2.0f, __uint_as_float(r[4 * q4 + 3]), -v.w);
+            }
+          }
+#pragma unroll
+          for (int j = 0; j < 16; ++j) mx = fmaxf(mx, y[j]);
+          if (uniform && mx < thr) continue;
+          if (uniform) {
+#pragma unroll
+            for (int j = 0; j < 16; ++j) cand |= (y[j] >= thr ? 1u : 0u) << j;
+          } else {
+            cand = 0xFFFFu;  // mixed chunk: decide column by column below
+          }
         }
         if (c0 + 16 > nvalid) cand &= (nvalid > c0) ? ((1u << (nvalid - c0)) - 1u) : 0u;
         while (cand) {
@@ -376,13 +438,15 @@ __global__ void __launch_bounds__(kTcThreads + 32, CTAS) bf_tc_kernel(TcArgs a) 
             inv_f2 = __frcp_ru(f2);
             thr = nqf - t2_eff * inv_f2 - 8.0f;
           }
-          float rj = 0.f;
+          uint32_t rr = 0u;
 #pragma unroll
           for (int jj = 0; jj < 16; ++jj)
-            if (jj == j) rj = __uint_as_float(r[jj]);
+            if (jj == j) rr = r[jj];
           // exact: x.q (or y when folded) is an integer below 2^24 held exactly by the fp32
-          // accumulator
-          const int S = FOLD ? my_nq - (int)rj : (int)s_nx[col] + my_nq - 2 * (int)rj;
+          // accumulator, or an int32 (u8 operands)
+          const int S = U8 ? reinterpret_cast<const int32_t*>(s_nx)[col] + my_nq - 2 * (int)rr
+                      : FOLD ? my_nq - (int)__uint_as_float(rr)
+                             : (int)s_nx[col] + my_nq - 2 * (int)__uint_as_float(rr);
           if ((float)S * f2 > t2_eff) continue;
           // exact fp64 decision (evaluate.py:48-53), ties by original id
           const double dist = dmul(sqrt((double)S), dadd(1.0, __ddiv_rn((double)sa, a.alpha)));
@@ -444,8 +508,9 @@ __global__ void __launch_bounds__(kTcThreads + 32, CTAS) bf_tc_kernel(TcArgs a) 
   }
 }
 
-size_t bf_tc_smem_n(int m, int l, int kk, int N, int nbs) {
-  return (size_t)kTcM * m * 2 + (size_t)nbs * N * m * 2 + 2 * (size_t)N * (3 + l) * 4 +
+// rowb = operand bytes per row (2 m for bf16, m for u8)
+size_t bf_tc_smem_n(int rowb, int l, int kk, int N, int nbs) {
+  return (size_t)kTcM * rowb + (size_t)nbs * N * rowb + 2 * (size_t)N * (3 + l) * 4 +
          (sizeof(double) + sizeof(uint32_t)) * (size_t)kk * kTcThreads + sizeof(float) * kTcThreads +
          8 + 80 + 16;
 }
@@ -453,15 +518,17 @@ size_t bf_tc_smem_n(int m, int l, int kk, int N, int nbs) {
 // Tile shapes (N nodes per tile, row stages, CTAs per SM), in order of preference; the first
 // that fits shared memory is used.  SB_BF_TILE = "N,stages,ctas" forces one (testing).
 struct TcShape { int N, nbs, ctas; };
-static const TcShape kTcShapes[] = {{128, 1, 2}, {64, 2, 2}, {256, 2, 1}, {128, 2, 1}};
+static const TcShape kTcShapes[] = {{128, 2, 2}, {256, 1, 2}, {128, 1, 2}, {64, 2, 2},
+                                    {256, 2, 1}, {128, 2, 1}};
 
-static bool tc_shape_fits(int m, int l, int kk, const TcShape& t) {
+static bool tc_shape_fits(int rowb, int l, int kk, const TcShape& t) {
   const size_t limit = t.ctas == 2 ? 113 * 1024 : 227 * 1024;
-  return bf_tc_smem_n(m, l, kk, t.N, t.nbs) <= limit;
+  return bf_tc_smem_n(rowb, l, kk, t.N, t.nbs) <= limit;
 }
 
+// m = operand bytes per row here (2 x features for bf16, features for u8)
 static TcShape tc_shape(int m, int l, int kk) {
-  if (m % 16 != 0 || m > 256 || l > 8 || kk > kTcMaxKK) return {0, 0, 0};
+  if (m % 32 != 0 || m > 512 || l > 8 || kk > kTcMaxKK) return {0, 0, 0};
   if (const char* e = getenv("SB_BF_TILE")) {
     TcShape t{0, 0, 0};
     if (sscanf(e, "%d,%d,%d", &t.N, &t.nbs, &t.ctas) == 3 && tc_shape_fits(m, l, kk, t)) return t;
@@ -471,16 +538,16 @@ static TcShape tc_shape(int m, int l, int kk) {
   return {0, 0, 0};
 }
 
-int bf_tc_tile(int m, int l, int kk, int* nbs = nullptr) {
-  const TcShape t = tc_shape(m, l, kk);
+int bf_tc_tile(int rowb, int l, int kk, int* nbs = nullptr) {
+  const TcShape t = tc_shape(rowb, l, kk);
   if (nbs) *nbs = t.nbs;
   return t.N;
 }
 
-int bf_tc_supported(int m, int l, int kk) { return bf_tc_tile(m, l, kk) != 0; }
+int bf_tc_supported(int rowb, int l, int kk) { return bf_tc_tile(rowb, l, kk) != 0; }
 
-int bf_tc_ctas_per_sm(int m, int l, int kk) {
-  const TcShape t = tc_shape(m, l, kk);
+int bf_tc_ctas_per_sm(int rowb, int l, int kk) {
+  const TcShape t = tc_shape(rowb, l, kk);
   return t.N ? t.ctas : 1;
 }
 
@@ -548,6 +615,43 @@ __global__ void tc_gather_kernel(const float* F, const int32_t* A, const int32_t
   for (int u = lane_id(); u < l; u += 32) As[p * l + u] = A[v * l + u];
 }
 
+// sorted u8 copies (row-group layout), exact squared norms as int32, codes, attributes
+__global__ void tc_gather_u8_kernel(const float* F, const int32_t* A, const int32_t* code_in,
+                                    const int32_t* orig, int64_t n, int m, int l, uint8_t* Fb,
+                                    int32_t* nx, int32_t* code, int32_t* As) {
+  int64_t p = (int64_t)blockIdx.x * (blockDim.x >> 5) + warp_id();
+  if (p >= n) return;
+  const int64_t v = orig[p];
+  int acc = 0;
+  for (int t = lane_id(); t < m; t += 32) {
+    const int x = (int)F[v * m + t];
+    Fb[rg_off8(p, t, m)] = (uint8_t)x;
+    acc += x * x;
+  }
+  acc = warp_sum(acc);
+  if (lane_id() == 0) {
+    nx[p] = acc;
+    code[p] = code_in[v];
+  }
+  for (int u = lane_id(); u < l; u += 32) As[p * l + u] = A[v * l + u];
+}
+
+int launch_tc_gather_u8(const float* F, const int32_t* A, const int32_t* code_in,
+                        const int32_t* orig, int64_t n, int m, int l, void* Fb, int32_t* nx,
+                        int32_t* code, int32_t* As, cudaStream_t st) {
+  tc_gather_u8_kernel<<<(unsigned)((n + 7) / 8), 256, 0, st>>>(F, A, code_in, orig, n, m, l,
+                                                                (uint8_t*)Fb, nx, code, As);
+  return (int)cudaGetLastError();
+}
+
+int launch_bf_tc_prep_queries_u8(const double* qf, int64_t q, int m, void* Qb, int32_t* nq,
+                                 cudaStream_t st) {
+  const int64_t qpad = (q + kTcM - 1) / kTcM * kTcM;
+  tc_prep_queries_u8_kernel<<<(unsigned)((qpad + 7) / 8), 256, 0, st>>>(qf, q, qpad, m,
+                                                                        (uint8_t*)Qb, nq);
+  return (int)cudaGetLastError();
+}
+
 int launch_tc_attr_range(const int32_t* A, int64_t n, int l, int32_t* lo, int32_t* hi,
                          cudaStream_t st) {
   tc_attr_range_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(A, n, l, lo, hi);
@@ -582,21 +686,25 @@ int launch_bf_tc(const void* Fb, const int32_t* nx, const int32_t* A, const int3
                  const int32_t* orig, const void* Qb, const int32_t* nq, const int64_t* qa,
                  const int64_t* qmask, int64_t n, int64_t q, int m, int l, int kk, int splits,
                  double alpha, double* part_d, uint32_t* part_i, int* gthr, int fold,
-                 cudaStream_t st) {
+                 int u8, cudaStream_t st) {
   TcArgs a;
   a.gthr = gthr;
   a.Fb = (const char*)Fb; a.nx = nx; a.A = A; a.code = code; a.orig = orig;
   a.Qb = (const char*)Qb;
   a.nq = nq; a.qa = qa; a.qmask = qmask; a.n = n; a.q = q; a.m = m; a.l = l; a.kk = kk;
   a.splits = splits; a.alpha = alpha; a.part_d = part_d; a.part_i = part_i;
-  const TcShape sh = tc_shape(m, l, kk);
+  const int kind = u8 ? 2 : (fold ? 1 : 0);
+  const TcShape sh = tc_shape(m * (u8 ? 1 : 2), l, kk);
   a.N = sh.N;
   if (a.N == 0) return (int)cudaErrorInvalidValue;
-  size_t smem = bf_tc_smem_n(m, l, kk, a.N, sh.nbs);
+  size_t smem = bf_tc_smem_n(m * (u8 ? 1 : 2), l, kk, a.N, sh.nbs);
   void (*kern)(TcArgs);
-  if (sh.nbs == 1) kern = fold ? bf_tc_kernel<true, 1, 2> : bf_tc_kernel<false, 1, 2>;
-  else if (sh.ctas == 2) kern = fold ? bf_tc_kernel<true, 2, 2> : bf_tc_kernel<false, 2, 2>;
-  else kern = fold ? bf_tc_kernel<true, 2, 1> : bf_tc_kernel<false, 2, 1>;
+#define SB_TC_PICK(NB, CT) \
+  (kind == 2 ? bf_tc_kernel<2, NB, CT> : kind == 1 ? bf_tc_kernel<1, NB, CT> : bf_tc_kernel<0, NB, CT>)
+  if (sh.nbs == 1) kern = SB_TC_PICK(1, 2);
+  else if (sh.ctas == 2) kern = SB_TC_PICK(2, 2);
+  else kern = SB_TC_PICK(2, 1);
+#undef SB_TC_PICK
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return (int)e;
   dim3 grid((unsigned)((q + kTcM - 1) / kTcM), (unsigned)splits);

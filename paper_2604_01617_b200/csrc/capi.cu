@@ -887,7 +887,7 @@ int sb_bf_topk_queries(sb_index* idx, const double* qf, const int64_t* qa, const
   // partial dot product below 2^24 (exact in the fp32 accumulator)
   // (integer data: U is exact whatever the summation order, so lists of exactly k suffice)
   bool tc = idx->int_exact && idx->fmax <= 256.0 && idx->m <= 255 && !idx->force_sequential &&
-            sb::bf_tc_supported(idx->m, idx->l, k);
+            sb::bf_tc_supported(2 * idx->m, idx->l, k);
   if (const char* e = getenv("SB_BF_TC")) tc = tc && atoi(e) != 0;
   double qmin = 0.0, qmax = 0.0;
   for (int64_t i = 0; tc && i < q * idx->m; ++i) {
@@ -909,21 +909,27 @@ int sb_bf_topk_queries(sb_index* idx, const double* qf, const int64_t* qa, const
     // measured neutral on cfg 2 (the epilogue is bound by barrier waits, not the filter):
     // opt in with SB_BF_FOLD=1
     { const char* e = getenv("SB_BF_FOLD"); fold = fold && e && atoi(e) != 0; }
-    if (fold && !sb::bf_tc_supported(idx->m + 16, idx->l, k)) fold = false;
+    if (fold && !sb::bf_tc_supported(2 * (idx->m + 16), idx->l, k)) fold = false;
   }
+  // u8 operands (tcgen05 kind::i8, exact int32 dot products) for data and queries in [0, 255]
+  bool u8 = tc && idx->flo >= 0.f && idx->fhi <= 255.f && qmin >= 0.0 && qmax <= 255.0 &&
+            idx->m % 32 == 0 && sb::bf_tc_supported(idx->m, idx->l, k);
+  if (const char* e = getenv("SB_BF_U8")) u8 = u8 && atoi(e) != 0;
+  if (u8) fold = false;
   const int mk = fold ? idx->m + 16 : idx->m;
+  const int esz = u8 ? 1 : 2;  // operand bytes per element
   if (tc) {
     kk = k;
     a.k = kk;
     const int64_t n = idx->n;
     const int64_t npad = (n + sb::kTcNodePad - 1) / sb::kTcNodePad * sb::kTcNodePad;
-    if (!idx->have_fb || idx->fb_mk != mk) {
+    if (!idx->have_fb || idx->fb_mk != mk * esz) {
       // attribute-grouped node order: counting sort by the attribute tuple
       const int l = idx->l;
       // padded, zero-filled: every tile the kernel copies lies inside the buffers
-      CK(idx->fb.ensure(sizeof(uint16_t) * npad * mk));
+      CK(idx->fb.ensure((size_t)esz * npad * mk));
       CK(idx->fb_norm.ensure(sizeof(int32_t) * npad * (3 + l)));  // nx | code | orig | attrs
-      CK(cudaMemsetAsync(idx->fb.p, 0, sizeof(uint16_t) * npad * mk, idx->st));
+      CK(cudaMemsetAsync(idx->fb.p, 0, (size_t)esz * npad * mk, idx->st));
       CK(cudaMemsetAsync(idx->fb_norm.p, 0, sizeof(int32_t) * npad * (3 + l), idx->st));
       int32_t* s_nx = idx->fb_norm.as<int32_t>();
       int32_t* s_code = s_nx + npad;
@@ -964,24 +970,31 @@ int sb_bf_topk_queries(sb_index* idx, const double* qf, const int64_t* qa, const
                              idx->scan_tmp.as<int64_t>(), idx->st));
       CKL(sb::launch_tc_scatter(d_code, n, idx->rev_off.as<int64_t>(),
                                 idx->rev_cur.as<unsigned long long>(), s_orig, idx->st));
-      CKL(sb::launch_tc_gather(idx->F.as<float>(), idx->A.as<int32_t>(), d_code, s_orig, n,
-                               idx->m, mk, l, idx->fb.p, s_nx, s_code, s_attr, idx->st));
+      if (u8)
+        CKL(sb::launch_tc_gather_u8(idx->F.as<float>(), idx->A.as<int32_t>(), d_code, s_orig, n,
+                                    idx->m, l, idx->fb.p, s_nx, s_code, s_attr, idx->st));
+      else
+        CKL(sb::launch_tc_gather(idx->F.as<float>(), idx->A.as<int32_t>(), d_code, s_orig, n,
+                                 idx->m, mk, l, idx->fb.p, s_nx, s_code, s_attr, idx->st));
       idx->have_fb = true;
-      idx->fb_mk = mk;
+      idx->fb_mk = mk * esz;
       idx->have_cand = false;  // rev_* scratch was reused
       idx->launches += 6;
     }
     const int64_t qpad = (q + 127) / 128 * 128;
-    CK(idx->qb.ensure(sizeof(uint16_t) * qpad * mk + 2 * sizeof(int32_t) * q + 64));
-    int32_t* d_nq = reinterpret_cast<int32_t*>(idx->qb.as<char>() + sizeof(uint16_t) * qpad * mk);
+    CK(idx->qb.ensure((size_t)esz * qpad * mk + 2 * sizeof(int32_t) * q + 64));
+    int32_t* d_nq = reinterpret_cast<int32_t*>(idx->qb.as<char>() + (size_t)esz * qpad * mk);
     int32_t* d_gthr = d_nq + q;  // per-query shared bound, 0x7F7F7F7F = 3.39e38f
     CK(cudaMemsetAsync(d_gthr, 0x7F, sizeof(int32_t) * q, idx->st));
-    CKL(sb::launch_bf_tc_prep_queries(idx->qf.as<double>(), q, idx->m, mk, idx->qb.p, d_nq, idx->st));
+    if (u8)
+      CKL(sb::launch_bf_tc_prep_queries_u8(idx->qf.as<double>(), q, idx->m, idx->qb.p, d_nq, idx->st));
+    else
+      CKL(sb::launch_bf_tc_prep_queries(idx->qf.as<double>(), q, idx->m, mk, idx->qb.p, d_nq, idx->st));
     // split the node range so that whole waves of CTAs are busy: minimise waves / splits
     const int groups = (int)((q + 127) / 128);
     int splits = 1;
     double best = 1e30;
-    const int slots = idx->sms * sb::bf_tc_ctas_per_sm(mk, idx->l, kk);
+    const int slots = idx->sms * sb::bf_tc_ctas_per_sm(mk * esz, idx->l, kk);
     for (int s2 = 1; s2 <= 8 && (int64_t)s2 * 256 <= n; ++s2) {
       double waves = (double)((groups * s2 + slots - 1) / slots);
       double cost = waves / s2;
@@ -999,7 +1012,7 @@ int sb_bf_topk_queries(sb_index* idx, const double* qf, const int64_t* qa, const
       int32_t* s_nx = idx->fb_norm.as<int32_t>();
       CKL(sb::launch_bf_tc(idx->fb.p, s_nx, s_nx + 3 * npad, s_nx + npad, s_nx + 2 * npad, idx->qb.p,
                            d_nq, a.qa, a.qmask, n, q, mk, idx->l, kk, splits, alpha, a.part_d,
-                           a.part_i, d_gthr, fold ? 1 : 0, idx->st));
+                           a.part_i, d_gthr, fold ? 1 : 0, u8 ? 1 : 0, idx->st));
     }
     CKL(sb::launch_bf_merge_k(a, k, idx->out_ids.as<int64_t>(), nullptr, idx->out_dists.as<double>(),
                               d_unc, idx->st));

@@ -91,8 +91,14 @@ int launch_bf_merge_k(const BfArgs& a, int kout, int64_t* out_ids64, int32_t* ou
                       double* out_dists, int* uncertain, cudaStream_t st);
 
 // tensor-core query-mode top-k for integer data (bf_tc.cu)
-int bf_tc_supported(int m, int l, int kk);
-int bf_tc_ctas_per_sm(int m, int l, int kk);
+// rowb = operand bytes per row: 2 x features (bf16) or features (u8)
+int bf_tc_supported(int rowb, int l, int kk);
+int bf_tc_ctas_per_sm(int rowb, int l, int kk);
+int launch_tc_gather_u8(const float* F, const int32_t* A, const int32_t* code_in,
+                        const int32_t* orig, int64_t n, int m, int l, void* Fb, int32_t* nx,
+                        int32_t* code, int32_t* As, cudaStream_t st);
+int launch_bf_tc_prep_queries_u8(const double* qf, int64_t q, int m, void* Qb, int32_t* nq,
+                                 cudaStream_t st);
 constexpr int kTcNodePad = 256;  // node arrays of the tensor-core path are padded to this
 int launch_tc_attr_range(const int32_t* A, int64_t n, int l, int32_t* lo, int32_t* hi,
                          cudaStream_t st);
@@ -109,7 +115,7 @@ int launch_bf_tc_prep_queries(const double* qf, int64_t q, int m, int mk, void* 
 int launch_bf_tc(const void* Fb, const int32_t* nx, const int32_t* A, const int32_t* code,
                  const int32_t* orig, const void* Qb, const int32_t* nq, const int64_t* qa,
                  const int64_t* qmask, int64_t n, int64_t q, int m, int l, int kk, int splits,
-                 double alpha, double* part_d, uint32_t* part_i, int* gthr, int fold,
+                 double alpha, double* part_d, uint32_t* part_i, int* gthr, int fold, int u8,
                  cudaStream_t st);
 
 // ---- HELP build ---------------------------------------------------------------

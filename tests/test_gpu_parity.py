@@ -262,13 +262,15 @@ def test_order_free_mode_is_bit_exact():
 @pytest.mark.parametrize("n,m,l,q,k,lo", [(5000, 128, 3, 300, 10, 0), (3001, 64, 2, 129, 16, 0),
                                           (777, 32, 1, 5, 1, 0), (20000, 128, 3, 1000, 10, 0),
                                           (4000, 48, 2, 200, 10, -255)])
-@pytest.mark.parametrize("fold", ["1", "0"])
-def test_tensor_core_topk_exact(n, m, l, q, k, lo, fold):
-    """tcgen05 path (integer data, with and without |x|^2 folded into the MMA): identical ids
-    and fp64 distances to the fp64 SIMT path and to the oracle, including ragged tiles
-    (n % 256, q % 128), masks, duplicate points and signed values."""
+@pytest.mark.parametrize("path", ["u8", "bf16", "fold"])
+def test_tensor_core_topk_exact(n, m, l, q, k, lo, path):
+    """tcgen05 paths (integer data: u8 operands with kind::i8, bf16 operands, bf16 with |x|^2
+    folded into the MMA): identical ids and fp64 distances to the fp64 SIMT path and to the
+    oracle, including ragged tiles (n % 256, q % 128), masks, duplicate points and signed
+    values (which take the bf16 path)."""
     import os
-    os.environ["SB_BF_FOLD"] = fold
+    os.environ["SB_BF_U8"] = "1" if path == "u8" else "0"
+    os.environ["SB_BF_FOLD"] = "1" if path == "fold" else "0"
     rng = np.random.default_rng(n + m)
     f = np.clip(np.rint(rng.normal(128 + lo, 50 - lo / 3, (n, m))), lo, 255).astype(np.float32)
     f[10:20] = f[5]                      # exact duplicates: ties broken by id
@@ -296,6 +298,7 @@ def test_tensor_core_topk_exact(n, m, l, q, k, lo, fold):
             np.testing.assert_array_equal(ids_tc[qi], wi)
             np.testing.assert_array_equal(dd_tc[qi], wd)
     del os.environ["SB_BF_FOLD"]
+    del os.environ["SB_BF_U8"]
 
 
 @pytest.mark.slow
