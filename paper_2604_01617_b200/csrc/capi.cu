@@ -406,6 +406,8 @@ int sb_set_candidates(sb_index* idx, int32_t gamma_new, const int32_t* new_cand,
   return SB_OK;
 }
 
+static int ensure_u8(sb_index* idx, const float* F, DBuf& buf, bool& have);
+
 int sb_local_join(sb_index* idx, double inv_alpha, int64_t* inserted_out, int64_t* pairs_out) {
   if (idx) idx->graph_version++;
   if (!idx) return fail(SB_EARG, "idx is NULL");
@@ -438,6 +440,15 @@ int sb_local_join(sb_index* idx, double inv_alpha, int64_t* inserted_out, int64_
   CK(idx->scan_tmp.ensure(sizeof(int64_t) * sb::scan_tmp_slots(n)));
   CKL(sb::launch_thr_init(idx->ids.as<int32_t>(), idx->dists.as<float>(), n, g,
                           idx->thr.as<uint64_t>(), idx->st));
+  // integer features in [0, 255]: pair distances from u8 rows with dp4a (exact), unless
+  // SB_JOIN_U8=0
+  bool join_u8 = idx->int_exact && idx->flo >= 0.f && idx->fhi <= 255.f && idx->m % 4 == 0 &&
+                 !idx->force_sequential;
+  if (const char* e = getenv("SB_JOIN_U8")) join_u8 = join_u8 && atoi(e) != 0;
+  if (join_u8) {
+    int r = ensure_u8(idx, idx->F.as<float>(), idx->f8, idx->have_f8);
+    if (r) return r;
+  }
   // emit kernel geometry
   const int spad = (max_ns + 3) & ~3;
   const int ntiles_max = ((max_na + 3) / 4) * ((max_ns + 3) / 4);
@@ -488,6 +499,9 @@ int sb_local_join(sb_index* idx, double inv_alpha, int64_t* inserted_out, int64_
     a.node_counter = d_nodectr; a.push_tgt = idx->push_tgt.as<uint32_t>();
     a.push_key = idx->push_key.as<uint64_t>(); a.push_cap = cap; a.push_count = d_count;
     a.row_cnt = idx->row_cnt.as<int64_t>(); a.overflow = d_overflow; a.spad = spad; a.dc = dc;
+    a.ntiles_max = ntiles_max;
+    a.F8 = join_u8 ? idx->f8.as<uint8_t>() : nullptr;
+    a.nx8 = join_u8 ? reinterpret_cast<const int32_t*>(idx->f8.as<uint8_t>() + (((size_t)n * idx->m + 255) & ~(size_t)255)) : nullptr;
     int nctas = (int)std::min<int64_t>(ctas, end - begin);
     CKL(sb::launch_join_emit(a, nctas, smem, idx->st));
     unsigned long long used = 0;

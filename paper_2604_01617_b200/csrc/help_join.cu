@@ -32,8 +32,9 @@ constexpr int kEmitBlock = 1024;  // push slots a warp reserves at a time (<= 6%
 struct JoinCta {
   int32_t* slot_id;   // [spad]
   int32_t* slot_attr; // [spad * l]
-  float* xs;          // [dc][spad]
+  float* xs;          // [dc][spad] (u8 path: uint32 words [m / 4][spad])
   int* tiles;         // tile list
+  int32_t* nrm;       // [spad] |x|^2 (u8 path)
 };
 
 // warp-aggregated append of up to two pushes per lane into the global push buffer
@@ -84,6 +85,10 @@ SB_DEV void emit2(const JoinArgs& a, Emitter& em, bool p1, uint32_t t1, uint64_t
   em.used += total;
 }
 
+// U8: integer features in [0, 255]: the slots' rows are staged as u8 words and each pair's
+// S = |x|^2 + |y|^2 - 2 x.y comes from byte dot products (dp4a), exact in int32 and equal to
+// the reference's fp64 sum of squares.
+template <bool U8>
 __global__ void __launch_bounds__(kJoinThreads, 2) join_emit_kernel(JoinArgs a) {
   extern __shared__ __align__(16) char smem_raw[];
   const int spad = a.spad;
@@ -93,7 +98,8 @@ __global__ void __launch_bounds__(kJoinThreads, 2) join_emit_kernel(JoinArgs a) 
     s.xs = reinterpret_cast<float*>(p); p += sizeof(float) * (size_t)a.dc * spad;
     s.slot_id = reinterpret_cast<int32_t*>(p); p += sizeof(int32_t) * spad;
     s.slot_attr = reinterpret_cast<int32_t*>(p); p += sizeof(int32_t) * (size_t)spad * a.l;
-    s.tiles = reinterpret_cast<int*>(p);
+    s.tiles = reinterpret_cast<int*>(p); p += sizeof(int) * (size_t)a.ntiles_max;
+    s.nrm = reinterpret_cast<int32_t*>(p);
   }
   __shared__ int sh_node, sh_ntiles, sh_na, sh_nb;
   const int tid = threadIdx.x;
@@ -136,7 +142,16 @@ __global__ void __launch_bounds__(kJoinThreads, 2) join_emit_kernel(JoinArgs a) 
     }
     __syncthreads();
     const int ntiles = sh_ntiles;
-    if (whole) {
+    if (U8) {
+      const int nw = a.m >> 2;
+      uint32_t* xw = reinterpret_cast<uint32_t*>(s.xs);
+      for (int e = tid; e < ns * nw; e += blockDim.x) {
+        const int t = e / nw, dw = e % nw;
+        xw[dw * spad + t] = __ldg(reinterpret_cast<const uint32_t*>(a.F8 + (int64_t)s.slot_id[t] * a.m) + dw);
+      }
+      for (int t = tid; t < ns; t += blockDim.x) s.nrm[t] = __ldg(a.nx8 + s.slot_id[t]);
+      __syncthreads();
+    } else if (whole) {
       for (int e = tid; e < ns * a.m; e += blockDim.x) {
         int t = e / a.m, dd = e % a.m;
         s.xs[dd * spad + t] = __ldg(a.F + (int64_t)s.slot_id[t] * a.m + dd);
@@ -153,7 +168,35 @@ __global__ void __launch_bounds__(kJoinThreads, 2) join_emit_kernel(JoinArgs a) 
       for (int u = 0; u < kJT; ++u)
 #pragma unroll
         for (int w = 0; w < kJT; ++w) acc[u][w] = 0.0;
-      for (int d0 = 0; d0 < a.m; d0 += a.dc) {
+      if (U8) {
+        unsigned dot[kJT][kJT];
+#pragma unroll
+        for (int u = 0; u < kJT; ++u)
+#pragma unroll
+          for (int w = 0; w < kJT; ++w) dot[u][w] = 0u;
+        if (have) {
+          const uint32_t* xw = reinterpret_cast<const uint32_t*>(s.xs);
+          for (int dw = 0; dw < (a.m >> 2); ++dw) {
+            const uint4 xv = *reinterpret_cast<const uint4*>(xw + dw * spad + rb * kJT);
+            const uint4 yv = *reinterpret_cast<const uint4*>(xw + dw * spad + cb * kJT);
+            const uint32_t xx[4] = {xv.x, xv.y, xv.z, xv.w};
+            const uint32_t yy[4] = {yv.x, yv.y, yv.z, yv.w};
+#pragma unroll
+            for (int u = 0; u < kJT; ++u)
+#pragma unroll
+              for (int w = 0; w < kJT; ++w) dot[u][w] = __dp4a(xx[u], yy[w], dot[u][w]);
+          }
+#pragma unroll
+          for (int u = 0; u < kJT; ++u)
+#pragma unroll
+            for (int w = 0; w < kJT; ++w) {
+              const int x = rb * kJT + u, y = cb * kJT + w;
+              const int nx_ = x < ns ? s.nrm[x] : 0, ny_ = y < ns ? s.nrm[y] : 0;
+              acc[u][w] = (double)(nx_ + ny_ - 2 * (int)dot[u][w]);
+            }
+        }
+      }
+      for (int d0 = 0; !U8 && d0 < a.m; d0 += a.dc) {
         const int dc = a.m - d0 < a.dc ? a.m - d0 : a.dc;
         if (!whole) {
           __syncthreads();
@@ -341,7 +384,8 @@ __global__ void thr_init_kernel(const int32_t* ids, const float* dists, int64_t 
 
 size_t join_emit_smem(int spad, int dc, int l, int ntiles_max) {
   return sizeof(float) * (size_t)dc * spad + sizeof(int32_t) * spad +
-         sizeof(int32_t) * (size_t)spad * l + sizeof(int) * (size_t)ntiles_max + 64;
+         sizeof(int32_t) * (size_t)spad * l + sizeof(int) * (size_t)ntiles_max +
+         sizeof(int32_t) * spad + 64;
 }
 
 int launch_thr_init(const int32_t* ids, const float* dists, int64_t n, int g, uint64_t* thr,
@@ -351,17 +395,23 @@ int launch_thr_init(const int32_t* ids, const float* dists, int64_t n, int g, ui
 }
 
 int launch_join_emit(const JoinArgs& a, int ctas, size_t smem, cudaStream_t st) {
-  cudaError_t e = cudaFuncSetAttribute(join_emit_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       (int)smem);
+  auto kern = a.F8 ? join_emit_kernel<true> : join_emit_kernel<false>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return (int)e;
-  join_emit_kernel<<<ctas, kJoinThreads, smem, st>>>(a);
+  kern<<<ctas, kJoinThreads, smem, st>>>(a);
   return (int)cudaGetLastError();
 }
 
 int join_emit_occupancy(size_t smem, int* ctas_per_sm) {
-  cudaFuncSetAttribute(join_emit_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  return (int)cudaOccupancyMaxActiveBlocksPerMultiprocessor(ctas_per_sm, join_emit_kernel,
-                                                            kJoinThreads, smem);
+  cudaFuncSetAttribute(join_emit_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaFuncSetAttribute(join_emit_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  int a = 0, b = 0;
+  cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&a, join_emit_kernel<false>,
+                                                                kJoinThreads, smem);
+  if (e == cudaSuccess)
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, join_emit_kernel<true>, kJoinThreads, smem);
+  *ctas_per_sm = a < b ? a : b;
+  return (int)e;
 }
 
 int launch_push_scatter(const uint32_t* tgt, const uint64_t* key, uint64_t total,

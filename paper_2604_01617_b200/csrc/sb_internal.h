@@ -164,7 +164,9 @@ struct JoinArgs {
   unsigned long long* push_count;
   int64_t* row_cnt;
   int* overflow;
-  int spad, dc;
+  int spad, dc, ntiles_max;
+  const uint8_t* F8;      // u8 rows (integer data in [0, 255]) or null: fp64 path
+  const int32_t* nx8;     // exact |x|^2 of the u8 rows
 };
 size_t join_emit_smem(int spad, int dc, int l, int ntiles_max);
 int join_emit_occupancy(size_t smem, int* ctas_per_sm);
