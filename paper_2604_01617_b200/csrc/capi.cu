@@ -643,12 +643,13 @@ static int reinforce_overflow(sb_index* idx, double sigma) {
   a.ids = idx->ids.as<int32_t>(); a.dists = idx->dists.as<float>();
   a.counts = idx->counts.as<int32_t>(); a.in_deg = idx->in_deg.as<int32_t>(); a.sigma = sigma;
   CK(idx->rf_n8.ensure((size_t)n * g));            // mutual flags
-  CK(idx->rf_eo.ensure(sizeof(int32_t) * (size_t)n * g));  // per-edge O index of the target
+  CK(idx->rf_eo.ensure(sizeof(int32_t) * (size_t)n * g * 2));  // per-edge O index, U position
   CK(idx->rf_nb.ensure((size_t)n * 2));            // is_o, relevant
   CK(idx->rf_n32.ensure(sizeof(int32_t) * n * 2)); // o_idx, static_ins
   CK(idx->rf_n64.ensure(sizeof(int64_t) * n * 8)); // rev_extra, oflag, oscan, orev, apply x3, rec_head
   a.mutual = idx->rf_n8.as<uint8_t>();
   a.eo = idx->rf_eo.as<int32_t>();
+  a.ecu = a.eo + (size_t)n * g;
   a.is_o = idx->rf_nb.as<uint8_t>();
   a.relevant = a.is_o + n;
   a.o_idx = idx->rf_n32.as<int32_t>();
@@ -701,20 +702,22 @@ static int reinforce_overflow(sb_index* idx, double sigma) {
   CKL(sb::rf_launch_stage3(a, upad_max, dc_max, upad4, bits_smem, idx->st));
   // sequential simulation over events touching overflow rows
   a.rec_cap = std::max<int64_t>(1, no * g);
-  CK(idx->rf_rec.ensure((sizeof(int32_t) + sizeof(uint64_t) + sizeof(int64_t)) * a.rec_cap + 64));
+  CK(idx->rf_rec.ensure((2 * sizeof(int32_t) + sizeof(uint64_t) + sizeof(int64_t)) * a.rec_cap + 64));
   a.rec_key = idx->rf_rec.as<uint64_t>();
   a.rec_next = reinterpret_cast<int64_t*>(a.rec_key + a.rec_cap);
   a.rec_tgt = reinterpret_cast<int32_t*>(a.rec_next + a.rec_cap);
+  a.rec_cu = a.rec_tgt + a.rec_cap;
   CK(cudaMemsetAsync(a.rec_head, 0xFF, sizeof(int64_t) * n, idx->st));
   a.dyn_cap = 1 << 16;
   a.sim_wmax = (int)wmax;
   if (g > 255) return fail(SB_EARG, "reinforce: gamma must be below 256");
   if (sb::rf_simulate_smem(g, (int)wmax) > 227 * 1024)
     return fail(SB_ECUDA, "reinforce: simulation scratch exceeds shared memory");
-  size_t sim_bytes = sizeof(uint64_t) * a.dyn_cap + 64;
+  size_t sim_bytes = (sizeof(uint64_t) + sizeof(int32_t)) * a.dyn_cap + 64;
   CK(idx->rf_sim.ensure(sim_bytes));
   char* sp = idx->rf_sim.as<char>();
   a.dyn = reinterpret_cast<uint64_t*>(sp); sp += sizeof(uint64_t) * a.dyn_cap;
+  a.dyn_cu = reinterpret_cast<int32_t*>(sp); sp += sizeof(int32_t) * a.dyn_cap;
   a.result = reinterpret_cast<int64_t*>(sp);
   CKL(sb::rf_launch_simulate(a, idx->st));
   int64_t res[2] = {0, 0};

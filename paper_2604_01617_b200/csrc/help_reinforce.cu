@@ -321,8 +321,10 @@ size_t rf_simulate_smem(int g, int wmax) {
 constexpr bool kRfProf = SB_RF_PROF != 0;
 __device__ unsigned long long g_rf_prof[8];
 
+// cu_hint: cand's position in U_j when known (precomputed for static edges, recorded for
+// mirrors), or -1 to search U_j
 SB_DEV int warp_try_insert(RfArgs& a, const SimSmem& S, int32_t j, int o, int32_t cand,
-                           float d, int64_t s, int& err) {
+                           float d, int64_t s, int& err, int cu_hint = -1) {
   const int lane = lane_id();
   const long long t_start = clock64();
   const int g = a.g;
@@ -358,7 +360,7 @@ SB_DEV int warp_try_insert(RfArgs& a, const SimSmem& S, int32_t j, int o, int32_
     if (kRfProf && lane == 0) { atomicAdd(&g_rf_prof[4], (unsigned long long)(clock64() - t_start)); atomicAdd(&g_rf_prof[5], 1ull); }
     return 0;
   }
-  const int cu = warp_u_index(a.u_list + uoff, usz, cand);
+  const int cu = cu_hint >= 0 ? cu_hint : warp_u_index(a.u_list + uoff, usz, cand);
   if (cu < 0) {
     err = 1;
     return 0;
@@ -499,9 +501,10 @@ __global__ void rf_simulate_kernel(RfArgs a) {
   int64_t nrec = 0;
   const long long t_kernel = clock64();
   const volatile uint8_t* relevant = a.relevant;
-  auto dyn_insert = [&](uint64_t kd, int64_t s) {
+  auto dyn_insert = [&](int q, int64_t s) {
+    const uint64_t kd = a.dyn[q];
     const int32_t jd = (int32_t)key_id(kd);
-    warp_try_insert(a, S, jd, a.o_idx[jd], (int32_t)s, key_dist(kd), s, err);
+    warp_try_insert(a, S, jd, a.o_idx[jd], (int32_t)s, key_dist(kd), s, err, a.dyn_cu[q]);
   };
   // Per source: count, O index, the row (gamma wide, masked by the count), the head of its
   // recorded mirrors and the targets' O indices.  Rows outside O never change during the
@@ -515,6 +518,7 @@ __global__ void rf_simulate_kernel(RfArgs a) {
     int32_t vi[8];
     float vd[8];
     int oj[8];
+    int cu[8];  // s's position in U_j of each static O-target edge (rows outside O)
   };
   auto load_src = [&](int64_t s, Src& D) {
     D.s = s;
@@ -528,8 +532,10 @@ __global__ void rf_simulate_kernel(RfArgs a) {
         D.vi[k] = a.ids[s * g + t];
         D.vd[k] = a.dists[s * g + t];
         D.oj[k] = a.eo[s * g + t];
+        D.cu[k] = a.ecu[s * g + t];
       } else {
         D.oj[k] = -2;
+        D.cu[k] = -1;
       }
     }
   };
@@ -556,10 +562,14 @@ __global__ void rf_simulate_kernel(RfArgs a) {
       int32_t vi[8];
       float vd[8];
       int oj[8];
+      int cuh[8];
 #pragma unroll
       for (int k = 0; k < 8; ++k) {
         vi[k] = D.vi[k];
         vd[k] = D.vd[k];
+        // an O row's entries are live: its U positions come from u_pos, its events search
+        cuh[k] = osrc >= 0 ? ((lane + 32 * k) < cs ? a.u_pos[(int64_t)osrc * g + lane + 32 * k] : -1)
+                           : D.cu[k];
         // an O row's entries may have changed since eo was computed: look their O index up
         oj[k] = osrc >= 0 ? ((lane + 32 * k) < cs ? a.o_idx[vi[k]] : -2) : D.oj[k];
       }
@@ -579,6 +589,7 @@ __global__ void rf_simulate_kernel(RfArgs a) {
               const int32_t j = vi[k];
               a.rec_tgt[r] = j;
               a.rec_key[r] = row_key(vd[k], (uint32_t)s);
+              a.rec_cu[r] = cuh[k];  // j's position in U_s: the hint of the later event
               a.rec_next[r] = a.rec_head[j];
               a.rec_head[j] = r;
               if (j > s) a.relevant[j] = 1;
@@ -614,9 +625,15 @@ __global__ void rf_simulate_kernel(RfArgs a) {
           for (int64_t r = rh; r >= 0; r = a.rec_next[r]) {
             if (nd < a.dyn_cap) {
               uint64_t kk = row_key(key_dist(a.rec_key[r]), key_id(a.rec_key[r]));
+              const int cr = a.rec_cu[r];
               int pos = nd;
-              while (pos > 0 && a.dyn[pos - 1] > kk) { a.dyn[pos] = a.dyn[pos - 1]; --pos; }
+              while (pos > 0 && a.dyn[pos - 1] > kk) {
+                a.dyn[pos] = a.dyn[pos - 1];
+                a.dyn_cu[pos] = a.dyn_cu[pos - 1];
+                --pos;
+              }
               a.dyn[pos] = kk;
+              a.dyn_cu[pos] = cr;
               ++nd;
             } else {
               err = 3;
@@ -636,12 +653,13 @@ __global__ void rf_simulate_kernel(RfArgs a) {
             const int32_t jj = __shfl_sync(kFull, vi[k], src);
             const float dd = __shfl_sync(kFull, vd[k], src);
             const int oo = __shfl_sync(kFull, oj[k], src);
+            const int ch = __shfl_sync(kFull, cuh[k], src);
             const uint64_t ks = row_key(dd, (uint32_t)jj);
-            while (q < nd && a.dyn[q] < ks) dyn_insert(a.dyn[q++], s);
-            warp_try_insert(a, S, jj, oo, (int32_t)s, dd, s, err);
+            while (q < nd && a.dyn[q] < ks) dyn_insert(q++, s);
+            warp_try_insert(a, S, jj, oo, (int32_t)s, dd, s, err, ch);
           }
         }
-        while (q < nd) dyn_insert(a.dyn[q++], s);
+        while (q < nd) dyn_insert(q++, s);
       }
     }
   }
@@ -699,6 +717,14 @@ int rf_launch_stage2(RfArgs& a, const int64_t* oscan, cudaStream_t st) {
   return (int)cudaGetLastError();
 }
 
+// K6b: for every edge s -> j with j in O: s's position in U_j (static for rows outside O)
+__global__ void rf_ecu_kernel(RfArgs a) {
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= a.n * a.g) return;
+  const int o = a.eo[e];
+  a.ecu[e] = o >= 0 ? u_index(a, o, (int32_t)(e / a.g)) : -1;
+}
+
 int rf_launch_stage3(RfArgs& a, int upad_max, int dc_max, int upad4_max, size_t bits_smem,
                      cudaStream_t st) {
   cudaMemsetAsync(a.u_cur, 0, sizeof(int64_t) * a.no, st);
@@ -710,6 +736,7 @@ int rf_launch_stage3(RfArgs& a, int upad_max, int dc_max, int upad4_max, size_t 
   cudaFuncSetAttribute(rf_bits_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bits_smem);
   rf_bits_kernel<<<(unsigned)a.no, kRfThreads, bits_smem, st>>>(a, dc_max, upad4_max);
   rf_init_upos_kernel<<<nblk(a.no * a.g, 256), 256, 0, st>>>(a);
+  rf_ecu_kernel<<<nblk(a.n * a.g, 256), 256, 0, st>>>(a);
   return (int)cudaGetLastError();
 }
 

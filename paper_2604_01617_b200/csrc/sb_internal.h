@@ -229,6 +229,7 @@ struct RfArgs {
   double sigma;
   uint8_t* mutual;      // n x g
   int32_t* eo;          // n x g: O index of each edge's target (-1 not in O, -2 past count)
+  int32_t* ecu;         // n x g: the source's position in U_target for edges into O, else -1
   int64_t* rev_extra;   // n
   uint8_t* is_o;        // n
   int32_t* o_idx;       // n
@@ -251,9 +252,11 @@ struct RfArgs {
   int32_t* rec_tgt;
   uint64_t* rec_key;
   int64_t* rec_next;
+  int32_t* rec_cu;      // per record: the mirrored node's position in U_source
   int64_t* rec_head;    // n
   int64_t rec_cap;
   uint64_t* dyn;
+  int32_t* dyn_cu;      // U position of each dynamic event's candidate
   int dyn_cap;
   int sim_wmax;         // max redundancy-row words over O rows (simulation scratch size)
   int64_t* result;      // [nrec, err]
