@@ -781,7 +781,6 @@ static int reconnect_sweep(sb_index* idx, double sigma, int* ran) {
   const int g = idx->g;
   CK(idx->in_deg.ensure(sizeof(int32_t) * n));
   CK(idx->small.ensure(64));
-  CK(idx->seqtmp.ensure((sizeof(int64_t) + sizeof(double) + 1) * (g + 1) + 64));
   int* d_min = reinterpret_cast<int*>(idx->small.as<unsigned long long>() + 5);
   CKL(sb::launch_count_in_degrees(idx->ids.as<int32_t>(), idx->counts.as<int32_t>(), n, g,
                                   idx->in_deg.as<int32_t>(), nullptr, idx->st));
@@ -794,10 +793,9 @@ static int reconnect_sweep(sb_index* idx, double sigma, int* ran) {
   idx->launches += 2;
   *ran = 0;
   if (mn >= 1) return SB_OK;
-  CKL(sb::launch_seq_reinforce(idx->F.as<float>(), idx->A.as<int32_t>(), idx->m, idx->l, g,
-                               idx->ids.as<int32_t>(), idx->dists.as<float>(),
-                               idx->counts.as<int32_t>(), idx->in_deg.as<int32_t>(), sigma, n,
-                               idx->seqtmp.p, 1, idx->st));
+  CKL(sb::launch_reconnect(idx->F.as<float>(), idx->A.as<int32_t>(), idx->m, idx->l, g,
+                           idx->ids.as<int32_t>(), idx->dists.as<float>(), idx->counts.as<int32_t>(),
+                           idx->in_deg.as<int32_t>(), sigma, n, idx->st));
   idx->launches += 1;
   CK(cudaStreamSynchronize(idx->st));
   *ran = 1;

@@ -19,8 +19,8 @@
 // reinforce_pass (_kernels.py:398-409) equals symmetrisation when no row j would exceed
 // capacity, |row_j ∪ {s : j in row_s}| <= gamma — checked exactly first.  Rows
 // then get their missing reverse entries merged in by (f32 dist, id).  Otherwise the exact
-// sequential semantics (_try_insert_edge re-prune, reconnect_islands) run in a single-thread
-// device kernel over the same device arrays (reinforce_exact_kernel / reconnect_kernel).
+// overflow path of help_reinforce.cu runs.  reconnect_islands keeps its sequential order over
+// nodes and runs in one CTA (reconnect_cta_kernel below).
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -362,100 +362,12 @@ struct SeqCtx {
   int32_t* counts;
   int32_t* in_deg;
   double sigma;
-  int64_t* tmp_ids;   // g + 1
-  double* tmp_d;      // g + 1
-  uint8_t* keep;      // g + 1
 };
 
 SB_DEV bool seq_attrs_equal(const SeqCtx& c, int64_t a, int64_t b) {
   for (int t = 0; t < c.l; ++t)
     if (c.A[a * c.l + t] != c.A[b * c.l + t]) return false;
   return true;
-}
-
-SB_DEV double seq_cos(const SeqCtx& c, int64_t s, int64_t p, int64_t k) {
-  const float* xs = c.F + s * c.m;
-  const float* xp = c.F + p * c.m;
-  const float* xk = c.F + k * c.m;
-  double dot = 0.0, np2 = 0.0, nk2 = 0.0;
-  for (int t = 0; t < c.m; ++t) {
-    double dp = dsub((double)xp[t], (double)xs[t]);
-    double dk = dsub((double)xk[t], (double)xs[t]);
-    dot = dadd(dot, dmul(dp, dk));
-    np2 = dadd(np2, dmul(dp, dp));
-    nk2 = dadd(nk2, dmul(dk, dk));
-  }
-  if (np2 == 0.0 || nk2 == 0.0) return 1.0;
-  return __ddiv_rn(dot, sqrt(dmul(np2, nk2)));
-}
-
-SB_DEV int seq_try_insert(SeqCtx& c, int64_t j, int64_t cand, double dd) {
-  const float d = __double2float_rn(dd);
-  int32_t* ri = c.ids + j * c.g;
-  float* rd = c.dists + j * c.g;
-  const int cj = c.counts[j];
-  for (int t = 0; t < cj; ++t)
-    if (ri[t] == cand) return 0;
-  if (cj < c.g) {
-    int pos = cj;
-    while (pos > 0 && (rd[pos - 1] > d || (rd[pos - 1] == d && ri[pos - 1] > cand))) {
-      ri[pos] = ri[pos - 1];
-      rd[pos] = rd[pos - 1];
-      --pos;
-    }
-    ri[pos] = (int32_t)cand;
-    rd[pos] = d;
-    c.counts[j] = cj + 1;
-    c.in_deg[cand] += 1;
-    return 1;
-  }
-  int pos = cj;
-  for (int t = 0; t < cj; ++t) { c.tmp_ids[t] = ri[t]; c.tmp_d[t] = (double)rd[t]; }
-  while (pos > 0 && (c.tmp_d[pos - 1] > (double)d ||
-                     (c.tmp_d[pos - 1] == (double)d && c.tmp_ids[pos - 1] > cand))) {
-    c.tmp_ids[pos] = c.tmp_ids[pos - 1];
-    c.tmp_d[pos] = c.tmp_d[pos - 1];
-    --pos;
-  }
-  c.tmp_ids[pos] = cand;
-  c.tmp_d[pos] = (double)d;
-  const int total = cj + 1;
-  for (int t = 0; t < total; ++t) c.keep[t] = 1;
-  int kept = 1;
-  for (int t = 1; t < total; ++t) {
-    int64_t p = c.tmp_ids[t];
-    bool red = false;
-    for (int u = 0; u < t; ++u) {
-      if (!c.keep[u]) continue;
-      int64_t k = c.tmp_ids[u];
-      if (seq_attrs_equal(c, p, k) && seq_cos(c, j, p, k) > c.sigma) { red = true; break; }
-    }
-    if (red && (p == cand || c.in_deg[p] >= 2)) {
-      c.keep[t] = 0;
-      if (p != cand) c.in_deg[p] -= 1;
-    } else {
-      ++kept;
-    }
-  }
-  if (kept > c.g) {
-    for (int t = total - 1; t >= 0; --t) {
-      if (!c.keep[t]) continue;
-      int64_t p = c.tmp_ids[t];
-      if (p == cand) { c.keep[t] = 0; break; }
-      if (c.in_deg[p] >= 2) { c.keep[t] = 0; c.in_deg[p] -= 1; break; }
-    }
-  }
-  int w = 0, inserted = 0;
-  for (int t = 0; t < total; ++t) {
-    if (!c.keep[t]) continue;
-    ri[w] = (int32_t)c.tmp_ids[t];
-    rd[w] = __double2float_rn(c.tmp_d[t]);
-    if (c.tmp_ids[t] == cand) inserted = 1;
-    ++w;
-  }
-  c.counts[j] = w;
-  if (inserted) c.in_deg[cand] += 1;
-  return inserted;
 }
 
 SB_DEV int seq_force_insert(SeqCtx& c, int64_t j, int64_t cand, double dd, bool unsafe) {
@@ -488,38 +400,6 @@ SB_DEV int seq_force_insert(SeqCtx& c, int64_t j, int64_t cand, double dd, bool 
   c.counts[j] = cj + 1;
   c.in_deg[cand] += 1;
   return 1;
-}
-
-__global__ void reinforce_exact_kernel(SeqCtx c, int64_t n) {
-  if (blockIdx.x != 0 || threadIdx.x != 0) return;
-  for (int64_t s = 0; s < n; ++s) {
-    const int cs = c.counts[s];
-    for (int t = 0; t < cs; ++t) {
-      if (t >= c.counts[s]) break;
-      int64_t j = c.ids[s * c.g + t];
-      double d = (double)c.dists[s * c.g + t];
-      seq_try_insert(c, j, s, d);
-    }
-  }
-}
-
-__global__ void reconnect_kernel(SeqCtx c, int64_t n) {
-  if (blockIdx.x != 0 || threadIdx.x != 0) return;
-  for (int64_t v = 0; v < n; ++v) {
-    if (c.in_deg[v] > 0) continue;
-    bool done = false;
-    for (int t = 0; t < c.counts[v]; ++t) {
-      int64_t u = c.ids[v * c.g + t];
-      if (seq_try_insert(c, u, v, (double)c.dists[v * c.g + t])) { done = true; break; }
-    }
-    if (done) continue;
-    for (int t = 0; t < c.counts[v]; ++t) {
-      int64_t u = c.ids[v * c.g + t];
-      if (seq_force_insert(c, u, v, (double)c.dists[v * c.g + t], false)) { done = true; break; }
-    }
-    if (!done && c.counts[v] > 0)
-      seq_force_insert(c, c.ids[v * c.g], v, (double)c.dists[v * c.g], true);
-  }
 }
 
 // ---- reconnect_islands by one CTA ------------------------------------------------------
@@ -720,26 +600,18 @@ __global__ void min_kernel(const int32_t* x, int64_t n, int* out) {
   if (i < n) atomicMin(out, x[i]);
 }
 
-int launch_seq_reinforce(const float* F, const int32_t* A, int m, int l, int g, int32_t* ids,
-                         float* dists, int32_t* counts, int32_t* in_deg, double sigma,
-                         int64_t n, void* scratch, int reconnect, cudaStream_t st) {
+int launch_reconnect(const float* F, const int32_t* A, int m, int l, int g, int32_t* ids,
+                     float* dists, int32_t* counts, int32_t* in_deg, double sigma, int64_t n,
+                     cudaStream_t st) {
   SeqCtx c;
   c.F = F; c.A = A; c.m = m; c.l = l; c.g = g;
   c.ids = ids; c.dists = dists; c.counts = counts; c.in_deg = in_deg; c.sigma = sigma;
-  char* p = reinterpret_cast<char*>(scratch);
-  c.tmp_ids = reinterpret_cast<int64_t*>(p); p += sizeof(int64_t) * (g + 1);
-  c.tmp_d = reinterpret_cast<double*>(p); p += sizeof(double) * (g + 1);
-  c.keep = reinterpret_cast<uint8_t*>(p);
-  if (reconnect) {
-    if (g > kRcMaxG) return (int)cudaErrorInvalidValue;
-    const size_t bits = sizeof(uint32_t) * (size_t)(g + 1) * ((g + 32) / 32);
-    cudaError_t e = cudaFuncSetAttribute(reconnect_cta_kernel,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bits);
-    if (e != cudaSuccess) return (int)e;
-    reconnect_cta_kernel<<<1, kRcThreads, bits, st>>>(c, n);
-  } else {
-    reinforce_exact_kernel<<<1, 1, 0, st>>>(c, n);
-  }
+  if (g > kRcMaxG) return (int)cudaErrorInvalidValue;
+  const size_t bits = sizeof(uint32_t) * (size_t)(g + 1) * ((g + 32) / 32);
+  cudaError_t e = cudaFuncSetAttribute(reconnect_cta_kernel,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bits);
+  if (e != cudaSuccess) return (int)e;
+  reconnect_cta_kernel<<<1, kRcThreads, bits, st>>>(c, n);
   return (int)cudaGetLastError();
 }
 

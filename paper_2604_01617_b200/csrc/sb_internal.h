@@ -208,9 +208,10 @@ int launch_reinforce_check(const int32_t* ids, const float* dists, const int32_t
 int launch_symmetrize(int32_t* ids, float* dists, int32_t* counts, int64_t n, int g,
                       const int64_t* rev_extra, int64_t* off, int64_t* cur, uint64_t* seg,
                       int64_t* scan_tmp, cudaStream_t st);
-int launch_seq_reinforce(const float* F, const int32_t* A, int m, int l, int g, int32_t* ids,
-                         float* dists, int32_t* counts, int32_t* in_deg, double sigma,
-                         int64_t n, void* scratch, int reconnect, cudaStream_t st);
+// one reconnect_islands sweep (_kernels.py:455-487), exact, by one CTA (help_prune.cu)
+int launch_reconnect(const float* F, const int32_t* A, int m, int l, int g, int32_t* ids,
+                     float* dists, int32_t* counts, int32_t* in_deg, double sigma, int64_t n,
+                     cudaStream_t st);
 int launch_min_i32(const int32_t* x, int64_t n, int* out, cudaStream_t st);
 int launch_row_union_merge(int32_t* ids, float* dists, int32_t* counts, int64_t n, int g,
                            const int64_t* off, const int64_t* extra, const uint64_t* seg,
