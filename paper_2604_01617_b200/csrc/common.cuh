@@ -164,6 +164,16 @@ SB_DEV void cta_bitonic_u64(uint64_t* s, int n) {
   }
 }
 
+// an order on id words that carry flag bits outside `mask`
+template <class Less>
+struct MaskedOrder {
+  Less lt;
+  uint32_t mask;
+  SB_DEV bool operator()(double da, uint32_t ia, double db, uint32_t ib) const {
+    return lt(da, ia & mask, db, ib & mask);
+  }
+};
+
 // Bitonic sort of (fp64 dist, u32 id) pairs held in two shared arrays, one warp.
 template <class Less = PlainOrder>
 SB_DEV void warp_bitonic_did(double* d, uint32_t* id, int n, Less lt = Less()) {
@@ -190,10 +200,12 @@ SB_DEV void warp_bitonic_did(double* d, uint32_t* id, int n, Less lt = Less()) {
 // candidates one by one with a bounded insertion sort (_kernels.py:490-501): candidates that
 // do not beat the tail are dropped, the rest land at j + #{R < C[j]} and R[i] moves to
 // i + #{C < R[i]}.  cpos is scratch of >= c ints; cd/cid must hold next_pow2(c) slots.
-// Returns the lowest position that received a new entry, or K if none did.
+// Returns the lowest position that received a new entry, or K if none did.  `presorted`:
+// the candidates already come in list order (the filter keeps their order).
 template <class Less = PlainOrder>
 SB_DEV int warp_merge_topk(double* rd, uint32_t* rid, int K, double* cd, uint32_t* cid,
-                           int* cpos, int c, uint32_t idmask, Less lt = Less()) {
+                           int* cpos, int c, uint32_t idmask, Less lt = Less(),
+                           bool presorted = false) {
   const int lane = lane_id();
   const double wd = rd[K - 1];
   const uint32_t wi = rid[K - 1] & idmask;
@@ -206,7 +218,7 @@ SB_DEV int warp_merge_topk(double* rd, uint32_t* rid, int K, double* cd, uint32_
     if (i < c) {
       d = cd[i];
       id = cid[i];
-      ok = lt(d, id, wd, wi);
+      ok = lt(d, id & idmask, wd, wi);
     }
     unsigned bal = __ballot_sync(0xffffffffu, ok);
     __syncwarp();
@@ -219,16 +231,18 @@ SB_DEV int warp_merge_topk(double* rd, uint32_t* rid, int K, double* cd, uint32_
     __syncwarp();
   }
   if (kept == 0) return K;
-  int np = next_pow2(kept);
-  for (int i = kept + lane; i < np; i += 32) {
-    cd[i] = __longlong_as_double(0x7FF0000000000000ll);
-    cid[i] = 0xFFFFFFFFu;
+  if (!presorted) {
+    int np = next_pow2(kept);
+    for (int i = kept + lane; i < np; i += 32) {
+      cd[i] = __longlong_as_double(0x7FF0000000000000ll);
+      cid[i] = 0xFFFFFFFFu;
+    }
+    __syncwarp();
+    warp_bitonic_did(cd, cid, np, MaskedOrder<Less>{lt, idmask});
   }
-  __syncwarp();
-  if (np > 1) warp_bitonic_did(cd, cid, np, lt);
   for (int j = lane; j < kept; j += 32) {
     double d = cd[j];
-    uint32_t id = cid[j];
+    uint32_t id = cid[j] & idmask;
     int lo = 0, hi = K;
     while (lo < hi) {
       int mid = (lo + hi) >> 1;
@@ -253,7 +267,7 @@ SB_DEV int warp_merge_topk(double* rd, uint32_t* rid, int K, double* cd, uint32_
       int lo = 0, hi = kept;
       while (lo < hi) {
         int mid = (lo + hi) >> 1;
-        if (lt(cd[mid], cid[mid], d, id)) lo = mid + 1; else hi = mid;
+        if (lt(cd[mid], cid[mid] & idmask, d, id)) lo = mid + 1; else hi = mid;
       }
       tgt = i + lo;
     }

@@ -28,6 +28,7 @@
 //   (a full clear when the log overflows).
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <stdlib.h>
 
 #include "common.cuh"
 #include "rng.cuh"
@@ -45,7 +46,12 @@ constexpr int kRows = 8;                   // rows per lane group in flight (fp3
 #define ROUTE_F32_CHUNK 8                  // float4 loads in flight per lane (fp32 lane path)
 #endif
 
+constexpr int kLazyB = 64;  // insertion buffer of the large-K kernel instances
+constexpr int kLazyK = 1024; // K from which routing uses the insertion buffer
+
 struct WarpSmem {
+  double* bd;     // kLazyB (large-K instances)
+  uint32_t* bid;  // kLazyB
   double* rd;     // Kpad
   double* cd;     // Cpad
   double* qs;     // m
@@ -57,17 +63,27 @@ struct WarpSmem {
   int* cpos;      // Cpad
 };
 
-SB_HD size_t route_warp_smem_bytes_full(int Kpad, int Cpad, int m, int l) {
+SB_HD size_t route_warp_smem_bytes_full(int Kpad, int Cpad, int m, int l, bool lazy) {
   size_t b = (size_t)((m + 3) & ~3) * 4;  // fp32 query first: 16-byte aligned float4 reads
+  if (lazy) b += (size_t)kLazyB * 12;
   b += (size_t)Kpad * 8 + (size_t)Cpad * 8 + (size_t)m * 8 + (size_t)l * 16;
   b += (size_t)Kpad * 4 + (size_t)Cpad * 8;
   return (b + 15) & ~(size_t)15;
 }
 
+template <bool LAZY>
 SB_DEV WarpSmem carve(char* base, const RouteArgs& a) {
   WarpSmem w;
   w.qs32 = reinterpret_cast<float*>(base);
   double* dp = reinterpret_cast<double*>(base + (size_t)((a.m + 3) & ~3) * 4);
+  w.bd = nullptr;
+  w.bid = nullptr;
+  if (LAZY) {
+    w.bd = dp;
+    dp += kLazyB;
+    w.bid = reinterpret_cast<uint32_t*>(dp);
+    dp = reinterpret_cast<double*>(w.bid + kLazyB);
+  }
   w.rd = dp; dp += a.Kpad;
   w.cd = dp; dp += a.Cpad;
   w.qs = dp; dp += a.m;
@@ -328,14 +344,31 @@ SB_HD float fkey_inv(uint32_t k) {
 #ifndef ROUTE_MIN_CTAS
 #define ROUTE_MIN_CTAS 3
 #endif
-template <int MODE>
+// entries of the sorted (d, id) list x[0..n) ordered before (d, id); ids compared without flags
+SB_DEV int count_before(const double* xd, const uint32_t* xi, int n, double d, uint32_t id,
+                        const IdOrder& ord) {
+  int lo = 0, hi = n;
+  while (lo < hi) {
+    const int mid = (lo + hi) >> 1;
+    if (ord(xd[mid], xi[mid] & kIdMask, d, id)) lo = mid + 1; else hi = mid;
+  }
+  return lo;
+}
+
+// LAZY (K >= kLazyK): new candidates collect in a small sorted buffer B next to the result
+// list R and are merged into R only when B fills, so the O(K) list shift is paid once per
+// ~kLazyB candidates instead of once per expansion.  R ∪ B holds the walk's results; an entry
+// whose rank in R ∪ B is >= K is evicted in the reference and can never return (ranks only
+// grow), so it simply stays unselectable until the next merge drops it.  Selection takes the
+// first unchecked entry of R ∪ B by rank; the admission tail is the union's K-th entry.
+template <int MODE, bool LAZY>
 __global__ void __launch_bounds__(256, ROUTE_MIN_CTAS) route_kernel(RouteArgs a) {
   extern __shared__ __align__(16) char smem_raw[];
   const int lane = lane_id();
   const int wid = warp_id();
   const int nw = blockDim.x >> 5;
-  const size_t wbytes = route_warp_smem_bytes_full(a.Kpad, a.Cpad, a.m, a.l);
-  WarpSmem w = carve(smem_raw + wbytes * wid, a);
+  const size_t wbytes = route_warp_smem_bytes_full(a.Kpad, a.Cpad, a.m, a.l, LAZY);
+  WarpSmem w = carve<LAZY>(smem_raw + wbytes * wid, a);
   const int64_t slot = (int64_t)blockIdx.x * nw + wid;
   uint32_t* vis = a.visited + slot * a.vwords;
   uint32_t* vlog = a.vlog + slot * (int64_t)a.logcap;
@@ -407,10 +440,96 @@ __global__ void __launch_bounds__(256, ROUTE_MIN_CTAS) route_kernel(RouteArgs a)
 
     int64_t evals = 0, p1_evals = 0, p1_exp = 0, hops = 0, scanned = 0;
     int logn = 0;
+    int lb = 0;    // first position of R that may hold an unchecked entry
+    int nbuf = 0;  // LAZY: entries in the insertion buffer B
+    const int bcap = Cap < kLazyB ? Cap : kLazyB;
+    // LAZY: merge B into R (drops whatever leaves the top K)
+    auto flush_b = [&]() {
+      if (nbuf > 0) {
+        const int ins = warp_merge_topk(w.rd, w.rid, K, w.bd, w.bid, w.cpos, nbuf, kIdMask, ord, true);
+        if (ins < lb) lb = ins;
+        nbuf = 0;
+      }
+    };
+    // LAZY: admit the batch cd/cid[0..c) against the K-th entry of R ∪ B, then add it to B
+    // (or, when it does not fit, flush B and merge the batch into R directly)
+    auto lazy_merge = [&](int c) {
+      // the union's K-th entry: j = number of B entries within the first K of R ∪ B
+      int lo = 0, hi2 = nbuf;
+      while (lo < hi2) {  // largest j with B[j-1] before R[K-j]
+        const int j = (lo + hi2 + 1) >> 1;
+        if (ord(w.bd[j - 1], w.bid[j - 1] & kIdMask, w.rd[K - j], w.rid[K - j] & kIdMask)) lo = j;
+        else hi2 = j - 1;
+      }
+      const int jt = lo;
+      double td = w.rd[K - 1 - jt];
+      uint32_t ti = w.rid[K - 1 - jt] & kIdMask;
+      if (jt > 0 && ord(td, ti, w.bd[jt - 1], w.bid[jt - 1] & kIdMask)) {
+        td = w.bd[jt - 1];
+        ti = w.bid[jt - 1] & kIdMask;
+      }
+      int kept = 0;
+      for (int base = 0; base < c; base += 32) {
+        const int i = base + lane;
+        double d = 0.0;
+        uint32_t id = 0;
+        bool ok = false;
+        if (i < c) {
+          d = w.cd[i];
+          id = w.cid[i];
+          ok = ord(d, id, td, ti);
+        }
+        const unsigned bal = __ballot_sync(0xffffffffu, ok);
+        __syncwarp();
+        if (ok) {
+          const int pos = kept + __popc(bal & ((1u << lane) - 1u));
+          w.cd[pos] = d;
+          w.cid[pos] = id;
+        }
+        kept += __popc(bal);
+        __syncwarp();
+      }
+      if (kept == 0) return;
+      if (nbuf + kept > bcap) flush_b();
+      if (kept > bcap) {
+        const int ins = warp_merge_topk(w.rd, w.rid, K, w.cd, w.cid, w.cpos, kept, kIdMask, ord);
+        if (ins < lb) lb = ins;
+        return;
+      }
+      // B <- B ∪ batch by ranks (distinct ids): B[j] goes to j + #{batch < B[j]}, batch entry
+      // x to #{batch < x} + #{B < x}; kept + nbuf <= bcap <= 64 entries, two per lane at most
+      double xd[4];
+      uint32_t xw[4];
+      int xp[4];
+#pragma unroll
+      for (int h = 0; h < 4; ++h) {
+        const int t = lane + 32 * (h & 1);
+        const bool fromb = h < 2;
+        xp[h] = -1;
+        if (t < (fromb ? nbuf : kept)) {
+          xd[h] = fromb ? w.bd[t] : w.cd[t];
+          xw[h] = fromb ? w.bid[t] : w.cid[t];
+          const uint32_t id = xw[h] & kIdMask;
+          int r = fromb ? t : count_before(w.bd, w.bid, nbuf, xd[h], id, ord);
+          for (int i = 0; i < kept; ++i) r += ord(w.cd[i], w.cid[i], xd[h], id);
+          xp[h] = r;
+        }
+      }
+      __syncwarp();
+#pragma unroll
+      for (int h = 0; h < 4; ++h)
+        if (xp[h] >= 0) {
+          w.bd[xp[h]] = xd[h];
+          w.bid[xp[h]] = xw[h];
+        }
+      const int tot = kept + nbuf;
+      __syncwarp();
+      nbuf = tot;
+      __syncwarp();
+    };
     // walk state: stage 0 = evaluating entries, 1 = phase 1, 2 = phase 2
     int stage = 0;
     int ent_pos = 0;
-    int lb = 0;
     const int64_t* ent = a.entries + (int64_t)qi * K;
     for (;;) {
       int c = 0;
@@ -430,22 +549,62 @@ __global__ void __launch_bounds__(256, ROUTE_MIN_CTAS) route_kernel(RouteArgs a)
         const int hi = p1 ? a.P : K;
         const uint32_t bit = p1 ? kChkP : kChkR;
         int nxt;
-        int sel = first_unchecked(w.rid, lb, hi, bit, &nxt);
-        if (sel < 0) {
-          if (!p1) break;
-          stage = 2;  // phase 2 starts with all checked flags cleared (_kernels.py:587-588)
-          lb = 0;
-          for (int t = lane; t < K; t += 32) w.rid[t] &= ~kChkR;
+        int sel;
+        uint32_t node;
+        if (LAZY) {
+          // first unchecked of R (by position) and of B, each admitted only if its rank in
+          // R ∪ B is below hi; the smaller of the two is the reference's selection
+          int iR = first_unchecked(w.rid, lb, hi, bit, &nxt);  // rank >= position
+          if (iR >= 0 && iR + count_before(w.bd, w.bid, nbuf, w.rd[iR], w.rid[iR] & kIdMask, ord) >= hi)
+            iR = -1;
+          int jB = -1;
+          for (int base = 0; base < nbuf && jB < 0; base += 32) {
+            const int j = base + lane;
+            const unsigned bal = __ballot_sync(0xffffffffu, j < nbuf && !(w.bid[j] & bit));
+            if (bal) jB = base + __ffs(bal) - 1;
+          }
+          if (jB >= 0 && jB + count_before(w.rd, w.rid, K, w.bd[jB], w.bid[jB] & kIdMask, ord) >= hi)
+            jB = -1;
+          if (iR >= 0 && jB >= 0) {
+            if (ord(w.bd[jB], w.bid[jB] & kIdMask, w.rd[iR], w.rid[iR] & kIdMask)) iR = -1;
+            else jB = -1;
+          }
+          if (iR < 0 && jB < 0) {
+            if (!p1) break;
+            stage = 2;  // phase 2 starts with all checked flags cleared (_kernels.py:587-588)
+            lb = 0;
+            for (int t = lane; t < K; t += 32) w.rid[t] &= ~kChkR;
+            for (int t = lane; t < nbuf; t += 32) w.bid[t] &= ~kChkR;
+            __syncwarp();
+            continue;
+          }
+          sel = iR;
+          node = iR >= 0 ? (w.rid[iR] & kIdMask) : (w.bid[jB] & kIdMask);
           __syncwarp();
-          continue;
+          if (lane == 0) {
+            if (iR >= 0) w.rid[iR] |= bit;
+            else w.bid[jB] |= bit;
+          }
+          __syncwarp();
+          if (iR >= 0) lb = iR + 1;
+        } else {
+          sel = first_unchecked(w.rid, lb, hi, bit, &nxt);
+          if (sel < 0) {
+            if (!p1) break;
+            stage = 2;  // phase 2 starts with all checked flags cleared (_kernels.py:587-588)
+            lb = 0;
+            for (int t = lane; t < K; t += 32) w.rid[t] &= ~kChkR;
+            __syncwarp();
+            continue;
+          }
+          node = w.rid[sel] & kIdMask;
+          if (nxt >= 0) prefetch_row(a, w.rid[nxt] & kIdMask);
+          __syncwarp();
+          if (lane == 0) w.rid[sel] |= bit;
+          __syncwarp();
+          lb = sel + 1;
         }
-        const uint32_t node = w.rid[sel] & kIdMask;
-        if (nxt >= 0) prefetch_row(a, w.rid[nxt] & kIdMask);
-        __syncwarp();
-        if (lane == 0) w.rid[sel] |= bit;
-        __syncwarp();
         if (p1) ++p1_exp; else ++hops;
-        lb = sel + 1;
         half = p1;
         // expand: count and id row load together; visited test-and-set of the first cnt
         const int32_t* nb = a.nbr_ids + (int64_t)node * a.g;
@@ -521,10 +680,15 @@ __global__ void __launch_bounds__(256, ROUTE_MIN_CTAS) route_kernel(RouteArgs a)
         }
         __syncwarp();
       } else if (c > 0) {
-        int ins = warp_merge_topk(w.rd, w.rid, K, w.cd, w.cid, w.cpos, c, kIdMask, ord);
-        if (ins < lb) lb = ins;
+        if (LAZY) {
+          lazy_merge(c);
+        } else {
+          int ins = warp_merge_topk(w.rd, w.rid, K, w.cd, w.cid, w.cpos, c, kIdMask, ord);
+          if (ins < lb) lb = ins;
+        }
       }
     }
+    if (LAZY) flush_b();
     // results
     for (int t = lane; t < K; t += 32) {
       const uint32_t id = w.rid[t] & kIdMask;
@@ -566,17 +730,26 @@ int launch_entry_points(int64_t n, int K, uint64_t seed, int64_t qi0, int64_t q,
   return (int)cudaGetLastError();
 }
 
+// the insertion-buffer instance for large K (SB_ROUTE_LAZY=0 disables it, for A/B runs)
+static bool route_lazy(const RouteArgs& a) {
+  static const bool on = [] {
+    const char* e = getenv("SB_ROUTE_LAZY");
+    return !(e && e[0] == '0');
+  }();
+  return on && a.Kpad >= kLazyK && a.Cpad >= 16;
+}
+
 size_t route_smem_per_warp(const RouteArgs& a) {
-  return route_warp_smem_bytes_full(a.Kpad, a.Cpad, a.m, a.l);
+  return route_warp_smem_bytes_full(a.Kpad, a.Cpad, a.m, a.l, route_lazy(a));
 }
 
 template <int MODE>
 static int launch_route_t(const RouteArgs& a, int warps_per_cta, int ctas, size_t smem,
                           cudaStream_t st) {
-  cudaError_t e = cudaFuncSetAttribute(route_kernel<MODE>,
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  auto kern = route_lazy(a) ? route_kernel<MODE, true> : route_kernel<MODE, false>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return (int)e;
-  route_kernel<MODE><<<ctas, warps_per_cta * 32, smem, st>>>(a);
+  kern<<<ctas, warps_per_cta * 32, smem, st>>>(a);
   return (int)cudaGetLastError();
 }
 
@@ -600,21 +773,22 @@ int launch_route(const RouteArgs& a, int warps_per_cta, int ctas, cudaStream_t s
 }
 
 template <int MODE>
-static int route_occupancy_t(int warps_per_cta, size_t smem, int* ctas_per_sm) {
-  cudaError_t e = cudaFuncSetAttribute(route_kernel<MODE>,
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+static int route_occupancy_t(int warps_per_cta, size_t smem, int* ctas_per_sm, bool lazy) {
+  auto kern = lazy ? route_kernel<MODE, true> : route_kernel<MODE, false>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return (int)e;
-  return (int)cudaOccupancyMaxActiveBlocksPerMultiprocessor(ctas_per_sm, route_kernel<MODE>,
-                                                            warps_per_cta * 32, smem);
+  return (int)cudaOccupancyMaxActiveBlocksPerMultiprocessor(ctas_per_sm, kern, warps_per_cta * 32,
+                                                            smem);
 }
 
 int route_occupancy(const RouteArgs& a, int warps_per_cta, size_t smem, int* ctas_per_sm) {
+  const bool lz = route_lazy(a);
   switch (route_mode(a)) {
-    case kModeF64x4: return route_occupancy_t<kModeF64x4>(warps_per_cta, smem, ctas_per_sm);
-    case kModeF32Lane: return route_occupancy_t<kModeF32Lane>(warps_per_cta, smem, ctas_per_sm);
-    case kModeF32Split: return route_occupancy_t<kModeF32Split>(warps_per_cta, smem, ctas_per_sm);
-    case kModeU8: return route_occupancy_t<kModeU8>(warps_per_cta, smem, ctas_per_sm);
-    default: return route_occupancy_t<kModeGeneric>(warps_per_cta, smem, ctas_per_sm);
+    case kModeF64x4: return route_occupancy_t<kModeF64x4>(warps_per_cta, smem, ctas_per_sm, lz);
+    case kModeF32Lane: return route_occupancy_t<kModeF32Lane>(warps_per_cta, smem, ctas_per_sm, lz);
+    case kModeF32Split: return route_occupancy_t<kModeF32Split>(warps_per_cta, smem, ctas_per_sm, lz);
+    case kModeU8: return route_occupancy_t<kModeU8>(warps_per_cta, smem, ctas_per_sm, lz);
+    default: return route_occupancy_t<kModeGeneric>(warps_per_cta, smem, ctas_per_sm, lz);
   }
 }
 

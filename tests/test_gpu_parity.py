@@ -199,6 +199,45 @@ def test_route_random_graph_vs_oracle():
         np.testing.assert_array_equal(got[2][:, :4], want[2], err_msg=f"k={k}")
 
 
+@pytest.mark.parametrize("relabel", ["1", "0"])
+@pytest.mark.parametrize("g,path", [(32, "u8"), (24, "fp32"), (16, "fp64")])
+def test_route_large_k_insertion_buffer(relabel, g, path, monkeypatch):
+    """K >= 512 routes through the insertion-buffer kernel instance (new candidates wait in a
+    small sorted buffer next to the K-list); every result must equal the oracle bit for bit:
+    ties everywhere (features in {0..3}), both phases, masks, relabeled layout or not, and the
+    same answers as the plain instance (SB_ROUTE_LAZY=0)."""
+    monkeypatch.setenv("SB_ROUTE_RELABEL", relabel)
+    rng = np.random.default_rng(11 + g)
+    n, m, l = 9000, 32, 2
+    f = rng.integers(0, 4, (n, m)).astype(np.float32)
+    if path == "fp64":
+        f = f + np.float32(0.5) * rng.integers(0, 2, (n, m)).astype(np.float32) * np.float32(0.001)
+    if path == "fp32":
+        monkeypatch.setenv("SB_ROUTE_U8", "0")
+    a = rng.integers(1, 4, (n, l)).astype(np.int32)
+    ids = np.stack([rng.choice(n, g, replace=False) for _ in range(n)]).astype(np.int32)
+    cnt = rng.integers(g // 2, g + 1, n).astype(np.int32)
+
+    def graph():
+        return sb.RelationGraph(features=f, attrs=a, schema=sb.AttributeSchema((("x",),) * l),
+                                metric=sb.MetricConfig.manual(0.9, l), sigma=0.44, nbr_ids=ids,
+                                nbr_dists=np.zeros((n, g), np.float32), nbr_counts=cnt, frozen=True)
+    q = 24
+    qf = rng.integers(0, 4, (q, m)).astype(np.float32)
+    qa = rng.integers(1, 4, (q, l)).astype(np.int32)
+    masks = rng.integers(0, 2, (q, l)).astype(np.float64)
+    gr = graph()
+    for k, coarse in ((600, True), (1000, False), (2500, True)):
+        p = sb.SearchParams(k=k, seed=7, use_coarse=coarse)
+        got = sb.search_batch_arrays(gr, qf, qa, p, masks=masks)
+        want = O.search_batch(f, a, ids, cnt, 0.9, qf, qa, k, seed=7, masks=masks, use_coarse=coarse)
+        np.testing.assert_array_equal(got[0], want[0], err_msg=f"k={k}")
+        np.testing.assert_array_equal(got[1], want[1], err_msg=f"k={k}")
+        np.testing.assert_array_equal(got[2][:, :4], want[2], err_msg=f"k={k}")
+    want_path = {"u8": "u8-dp4a", "fp32": "fp32", "fp64": "fp64"}[path]
+    assert gr.device().route_info()["path"].startswith(want_path)
+
+
 def test_order_free_mode_is_bit_exact():
     """Integer-valued data in [0, 255] routes through the u8/dp4a path by default; the fp32
     order-free paths (one row per lane, lane groups), the fp64 lane path and the sequential
