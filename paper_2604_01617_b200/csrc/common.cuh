@@ -253,23 +253,27 @@ SB_DEV int warp_merge_topk(double* rd, uint32_t* rid, int K, double* cd, uint32_
   __syncwarp();
   const int first_ins = cpos[0];
   if (first_ins >= K) return K;
-  // move list entries at or after first_ins back to front; targets never precede sources
+  // move list entries at or after first_ins back to front; targets never precede sources.
+  // R[i] moves by #{j : lo_j <= i}, lo_j = cpos[j] - j (nondecreasing): jc counts the
+  // candidates with lo_j <= top, and the few with lo_j inside the chunk are subtracted per lane
+  int jc = kept;
   for (int top = K - 1; top >= first_ins; top -= 32) {
     int i = top - lane;
     bool act = i >= first_ins;
+    while (jc > 0 && cpos[jc - 1] - (jc - 1) > top) --jc;
     double d = 0.0;
     uint32_t idw = 0;
     int tgt = K;
     if (act) {
       d = rd[i];
       idw = rid[i];
-      uint32_t id = idw & idmask;
-      int lo = 0, hi = kept;
-      while (lo < hi) {
-        int mid = (lo + hi) >> 1;
-        if (lt(cd[mid], cid[mid] & idmask, d, id)) lo = mid + 1; else hi = mid;
+      int sh = jc;
+      for (int j = jc - 1; j >= 0; --j) {
+        const int loj = cpos[j] - j;
+        if (loj <= top - 32) break;
+        sh -= loj > i;
       }
-      tgt = i + lo;
+      tgt = i + sh;
     }
     __syncwarp();
     if (act && tgt < K) {
