@@ -193,44 +193,6 @@ __global__ void __launch_bounds__(kBfThreads) bf_partial_kernel(BfArgs a, int kk
   }
 }
 
-// NumPy's pairwise sum of squared differences (x_v - q)^2 for one pair (the order
-// evaluate.py:48's (diff*diff).sum(axis=1) uses): 8-way unrolled blocks of <= 128 elements,
-// halves (rounded down to a multiple of 8) above that.
-__device__ __noinline__ double np_pairwise_sq(const float* x, const double* q, int n) {
-  if (n > 128) {
-    int n2 = n / 2;
-    n2 -= n2 % 8;
-    return dadd(np_pairwise_sq(x, q, n2), np_pairwise_sq(x + n2, q + n2, n - n2));
-  }
-  if (n < 8) {
-    double res = 0.0;
-    for (int i = 0; i < n; ++i) {
-      double d = dsub((double)x[i], q[i]);
-      res = dadd(res, dmul(d, d));
-    }
-    return res;
-  }
-  double r[8];
-#pragma unroll
-  for (int j = 0; j < 8; ++j) {
-    double d = dsub((double)x[j], q[j]);
-    r[j] = dmul(d, d);
-  }
-  int i = 8;
-  for (; i < n - (n % 8); i += 8)
-#pragma unroll
-    for (int j = 0; j < 8; ++j) {
-      double d = dsub((double)x[i + j], q[i + j]);
-      r[j] = dadd(r[j], dmul(d, d));
-    }
-  double res = dadd(dadd(dadd(r[0], r[1]), dadd(r[2], r[3])), dadd(dadd(r[4], r[5]), dadd(r[6], r[7])));
-  for (; i < n; ++i) {
-    double d = dsub((double)x[i], q[i]);
-    res = dadd(res, dmul(d, d));
-  }
-  return res;
-}
-
 // merge the splits of each query (warp per query), then (query mode) exact re-rank
 __global__ void bf_merge_kernel(BfArgs a, int kk, int kpad, int kout, int64_t* out_ids64,
                                 int32_t* out_ids32, double* out_dists, int* uncertain) {

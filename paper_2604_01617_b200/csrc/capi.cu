@@ -78,6 +78,10 @@ struct sb_index {
   bool have_fb = false;           // bf16 feature copy + norms for the tensor-core top-k
   int fb_mk = 0;                  // its operand K (features, + 16 when |x|^2 is folded in)
   bool last_bf_tc = false;        // the last sb_bf_topk_queries ran on tensor cores
+  int last_bf_path = 0;           // 0 fp64 SIMT, 1 tcgen05 integer-exact, 2 tcgen05 TF32 filter
+  int64_t last_bf_fallback = 0;   // queries of the last TF32 call recomputed on the fp64 path
+  int64_t last_bf_cands = 0;      // candidates the last TF32 call emitted (all queries)
+  bool have_ft = false;           // TF32 operand copy + metadata (bf_tf.cu)
   bool have_f8 = false;           // u8 feature copy for routing (integer data in [0, 255])
   // routing layout: nodes renumbered in a locality order (route_layout); valid while
   // rl_version == graph_version (every call that changes the adjacency bumps graph_version)
@@ -105,9 +109,12 @@ struct sb_index {
   DBuf qf, qa, qm, entries, ent_scratch, out_ids, out_dists, stats, visited, vlog, counter;
   DBuf bf_part_d, bf_part_i, bf_self, bf_qa, bf_qm, bf_out32, fb, fb_norm, fb_tmp, qb, f8;
   DBuf rl_F, rl_A, rl_ids, rl_counts, rl_perm, rl_f8, rl_tmp;
+  DBuf ft, ft_meta, tq, tcand, tovf;
   ~sb_index() {
     fb.release();
     f8.release();
+    DBuf* tfb[] = {&ft, &ft_meta, &tq, &tcand, &tovf};
+    for (DBuf* b : tfb) b->release();
     DBuf* rl[] = {&rl_F, &rl_A, &rl_ids, &rl_counts, &rl_perm, &rl_f8, &rl_tmp};
     for (DBuf* b : rl) b->release();
     fb_tmp.release();
@@ -213,6 +220,14 @@ int sb_index_info(sb_index* idx, int32_t* int_exact, double* fmax_abs, int32_t* 
   if (last_bf_tc) *last_bf_tc = idx->last_bf_tc ? 1 : 0;
   if (int_exact) *int_exact = idx->int_exact ? 1 : 0;
   if (fmax_abs) *fmax_abs = idx->fmax;
+  return SB_OK;
+}
+
+int sb_bf_info(sb_index* idx, int32_t* path, int64_t* candidates, int64_t* fallback) {
+  if (!idx) return fail(SB_EARG, "idx is NULL");
+  if (path) *path = idx->last_bf_path;
+  if (candidates) *candidates = idx->last_bf_cands;
+  if (fallback) *fallback = idx->last_bf_fallback;
   return SB_OK;
 }
 
@@ -835,6 +850,51 @@ int sb_reinforce(sb_index* idx, double sigma, int64_t* overflow_rows, int32_t* s
   return SB_OK;
 }
 
+// Attribute-grouped node order for the tensor-core top-k paths: a counting sort of the nodes by
+// their attribute tuple (mixed-radix code; the node id when tuples are too many to group).
+// Writes the sorted order to s_orig (n) and leaves each node's code in *d_code_out (fb_tmp).
+static int node_order(sb_index* idx, int32_t* s_orig, int32_t** d_code_out) {
+  const int64_t n = idx->n;
+  const int l = idx->l;
+  CK(idx->small.ensure(64));
+  CK(idx->fb_tmp.ensure(sizeof(int32_t) * (2 * 8 + n + 2) + sizeof(int64_t) * 8));
+  int32_t* d_lo = idx->fb_tmp.as<int32_t>();
+  int32_t* d_hi = d_lo + 8;
+  int32_t* d_code = d_hi + 8;
+  int64_t* d_stride = reinterpret_cast<int64_t*>(d_code + n + (n & 1));
+  std::vector<int32_t> hlo(8, 0x7FFFFFFF), hhi(8, (int32_t)0x80000000);
+  CK(cudaMemcpyAsync(d_lo, hlo.data(), sizeof(int32_t) * 8, cudaMemcpyHostToDevice, idx->st));
+  CK(cudaMemcpyAsync(d_hi, hhi.data(), sizeof(int32_t) * 8, cudaMemcpyHostToDevice, idx->st));
+  CKL(sb::launch_tc_attr_range(idx->A.as<int32_t>(), n, l, d_lo, d_hi, idx->st));
+  CK(cudaMemcpyAsync(hlo.data(), d_lo, sizeof(int32_t) * 8, cudaMemcpyDeviceToHost, idx->st));
+  CK(cudaMemcpyAsync(hhi.data(), d_hi, sizeof(int32_t) * 8, cudaMemcpyDeviceToHost, idx->st));
+  CK(cudaStreamSynchronize(idx->st));
+  std::vector<int64_t> stride(8, 0);
+  int64_t combos = 1;
+  for (int u = l - 1; u >= 0; --u) {
+    stride[u] = combos;
+    combos *= (int64_t)hhi[u] - hlo[u] + 1;
+    if (combos > ((int64_t)1 << 24)) break;
+  }
+  const int grouped = combos <= ((int64_t)1 << 24) ? 1 : 0;
+  const int64_t bins = grouped ? combos : n;
+  CK(cudaMemcpyAsync(d_stride, stride.data(), sizeof(int64_t) * 8, cudaMemcpyHostToDevice, idx->st));
+  CK(idx->rev_cnt.ensure(sizeof(int64_t) * std::max<int64_t>(bins, n)));
+  CK(idx->rev_off.ensure(sizeof(int64_t) * std::max<int64_t>(bins, n)));
+  CK(idx->rev_cur.ensure(sizeof(int64_t) * std::max<int64_t>(bins, n)));
+  CK(idx->scan_tmp.ensure(sizeof(int64_t) * sb::scan_tmp_slots(std::max<int64_t>(bins, n))));
+  CK(cudaMemsetAsync(idx->rev_cnt.p, 0, sizeof(int64_t) * bins, idx->st));
+  CK(cudaMemsetAsync(idx->rev_cur.p, 0, sizeof(int64_t) * bins, idx->st));
+  CKL(sb::launch_tc_code(idx->A.as<int32_t>(), n, l, d_lo, d_stride, grouped, d_code,
+             idx->rev_cnt.as<unsigned long long>(), idx->st));
+  CKL(sb::exclusive_scan(idx->rev_cnt.as<int64_t>(), idx->rev_off.as<int64_t>(), bins,
+             idx->scan_tmp.as<int64_t>(), idx->st));
+  CKL(sb::launch_tc_scatter(d_code, n, idx->rev_off.as<int64_t>(),
+            idx->rev_cur.as<unsigned long long>(), s_orig, idx->st));
+  *d_code_out = d_code;
+  return SB_OK;
+}
+
 // ---------------------------------------------------------------------------
 static int bf_run(sb_index* idx, sb::BfArgs& a, int kout, int64_t* out64, int32_t* out32,
                   double* outd, int* uncertain_host) {
@@ -855,6 +915,166 @@ static int bf_run(sb_index* idx, sb::BfArgs& a, int kout, int64_t* out64, int32_
   CKL(sb::launch_bf_merge_k(a, kout, out64, out32, outd, d_unc, idx->st));
   idx->launches += 2;
   if (uncertain_host) CK(cudaMemcpyAsync(uncertain_host, d_unc, sizeof(int), cudaMemcpyDeviceToHost, idx->st));
+  return SB_OK;
+}
+
+// TF32 filter + exact re-rank (bf_tf.cu).  Queries whose candidates overflow the buffers are
+// recomputed on the exact fp64 kernel (bf_run); the count is reported by sb_bf_info.
+static int bf_tf_run(sb_index* idx, const double* qf, const int64_t* qa, const int64_t* qmask,
+                     int64_t q, int k, double alpha, double qmax_abs, int64_t* out_ids,
+                     double* out_dists, int* unc_out) {
+  const int64_t n = idx->n;
+  const int m = idx->m, l = idx->l;
+  const int dpad = sb::bf_tf_dpad(m);
+  const double cE = sb::tf_margin(dpad);
+  const int64_t npad = (n + sb::kTcNodePad - 1) / sb::kTcNodePad * sb::kTcNodePad;
+  if (!idx->have_ft) {
+    CK(idx->ft.ensure((size_t)4 * npad * dpad));
+    CK(idx->ft_meta.ensure((size_t)4 * npad * (4 + l)));
+    CK(cudaMemsetAsync(idx->ft.p, 0, (size_t)4 * npad * dpad, idx->st));
+    CK(cudaMemsetAsync(idx->ft_meta.p, 0, (size_t)4 * npad * (4 + l), idx->st));
+  }
+  float* nxd = idx->ft_meta.as<float>();
+  int32_t* s_code = reinterpret_cast<int32_t*>(nxd + npad);
+  int32_t* s_orig = s_code + npad;
+  int32_t* s_run = s_orig + npad;
+  int32_t* s_attr = s_run + npad;
+  if (!idx->have_ft) {
+    int32_t* d_code = nullptr;
+    int r = node_order(idx, s_orig, &d_code);
+    if (r) return r;
+    CKL(sb::launch_tf_gather(idx->F.as<float>(), idx->A.as<int32_t>(), d_code, s_orig, n, m, l, cE,
+                             idx->ft.as<float>(), nxd, s_code, s_attr, idx->st));
+    CKL(sb::launch_tf_runend(s_code, n, s_run, idx->st));
+    idx->have_ft = true;
+    idx->have_cand = false;  // rev_* scratch was reused
+    idx->launches += 5;
+  }
+  int qblock = 128, hsegs = 2;
+  sb::bf_tf_layout(m, l, k, &qblock, &hsegs);
+  const int64_t qpad = (q + qblock - 1) / qblock * qblock;
+  // node-range splits: whole waves of one CTA per SM, fewest splits within 3% of the best
+  const int groups = (int)(qpad / qblock);
+  const int64_t tiles = npad / 256;
+  int splits = 1;
+  {
+    double best = 1e30;
+    std::vector<double> cost(65, 1e30);
+    // each epilogue thread should see many more than k nodes, or its list bound stays loose
+    // and nearly every node is emitted: (tiles / splits) * 128 >= 16 k
+    const int64_t smax = std::max<int64_t>(1, std::min<int64_t>(64, tiles * 128 / (16 * (int64_t)k)));
+    for (int s2 = 1; s2 <= smax; ++s2) {
+      const double waves = (double)((groups * s2 + idx->sms - 1) / idx->sms);
+      cost[s2] = waves / s2;
+      best = std::min(best, cost[s2]);
+    }
+    for (int s2 = 1; s2 <= 64; ++s2)
+      if (cost[s2] <= best * 1.03) { splits = s2; break; }
+    if (const char* e = getenv("SB_TF_SPLITS")) splits = std::max(1, atoi(e));
+  }
+  // one candidate segment per epilogue thread of a query (two per CTA); a thread emits about
+  // k (1 + ln(its nodes / k)) candidates at most once its own list is full
+  const int segs = hsegs * splits;
+  int cap = std::max(512, 16 * k);
+  while (cap > 64 && (double)q * segs * cap * 8.0 > 8e9) cap /= 2;
+  if (const char* e = getenv("SB_TF_CAP")) cap = std::max(1, atoi(e));
+  const int scap = 2048;
+  const int ocap = 4096;  // per-query overflow area behind full segments
+  // tq: Qt (qpad x dpad f32) | nqs | nqu | gthr | ovf | ovf_count | emitted total | ocnt (q) |
+  //     cnt (q x segs)
+  const size_t qt_bytes = (size_t)4 * qpad * dpad;
+  CK(idx->tq.ensure(qt_bytes + (size_t)4 * 5 * q + 80 + (size_t)4 * q * segs));
+  float* Qt = idx->tq.as<float>();
+  float* nqs = reinterpret_cast<float*>(idx->tq.as<char>() + qt_bytes);
+  float* nqu = nqs + q;
+  int* gthr = reinterpret_cast<int*>(nqu + q);
+  int* ovf = gthr + q;
+  int* ovf_count = ovf + q;
+  unsigned long long* emitted_total =
+      reinterpret_cast<unsigned long long*>(reinterpret_cast<uintptr_t>(ovf_count + 2) & ~(uintptr_t)7);
+  uint32_t* ocnt = reinterpret_cast<uint32_t*>(emitted_total + 2);
+  uint32_t* cnt = ocnt + q;
+  CK(idx->tcand.ensure(sizeof(uint64_t) * ((size_t)q * segs * cap + (size_t)q * ocap)));
+  uint64_t* ocand = idx->tcand.as<uint64_t>() + (size_t)q * segs * cap;
+  CK(cudaMemsetAsync(gthr, 0x7F, sizeof(int) * q, idx->st));  // 0x7F7F7F7F = 3.39e38f
+  CK(cudaMemsetAsync(ovf, 0, reinterpret_cast<char*>(cnt) - reinterpret_cast<char*>(ovf), idx->st));
+  CK(cudaMemsetAsync(cnt + (size_t)q * segs, 0, 16, idx->st));  // SB_TF_DEBUG & 8 counters
+  // absolute slack for tf32 subnormal rounding and fp32 product underflow (negligible otherwise)
+  const double tiny = dpad * std::ldexp(1.0, -120) * (1.0 + idx->fmax) * (1.0 + qmax_abs);
+  CKL(sb::launch_tf_prep_queries(idx->qf.as<double>(), q, qpad, m, cE, tiny, Qt, nqs, nqu, idx->st));
+  // seed pass (first tile of every range, bound only), then the full pass
+  for (int seed = 1; seed >= 0; --seed)
+    CKL(sb::launch_bf_tf(idx->ft.as<float>(), nxd, s_code, s_orig, s_run, s_attr, Qt, nqs, nqu,
+                         idx->bf_qa.as<int64_t>(), qmask ? idx->bf_qm.as<int64_t>() : nullptr, n, q,
+                         m, l, k, splits, alpha, gthr, cnt, idx->tcand.as<uint64_t>(), cap, ocnt,
+                         ocand, ocap, seed, idx->st));
+  CKL(sb::launch_tf_refine(idx->F.as<float>(), idx->A.as<int32_t>(), m, l, idx->qf.as<double>(),
+                           idx->bf_qa.as<int64_t>(), qmask ? idx->bf_qm.as<int64_t>() : nullptr, q,
+                           k, alpha, cnt, idx->tcand.as<uint64_t>(), segs, cap, ocnt, ocand, ocap, gthr, scap,
+                           idx->out_ids.as<int64_t>(), idx->out_dists.as<double>(), ovf, ovf_count,
+                           emitted_total, idx->st));
+  idx->launches += 4;
+  if (getenv("SB_TF_DEBUG") && (atoi(getenv("SB_TF_DEBUG")) & 8)) {
+    uint32_t h[4];
+    CK(cudaMemcpy(h, cnt + (size_t)q * segs, sizeof(h), cudaMemcpyDeviceToHost));
+    fprintf(stderr, "tf debug: chunks past the max test %u, filter survivors %u, emitted %u, "
+            "list inserts %u\n", h[0], h[1], h[2], h[3]);
+  }
+  int novf = 0;
+  CK(cudaMemcpyAsync(&novf, ovf_count, sizeof(int), cudaMemcpyDeviceToHost, idx->st));
+  CK(cudaMemcpyAsync(out_ids, idx->out_ids.p, sizeof(int64_t) * q * k, cudaMemcpyDeviceToHost, idx->st));
+  if (out_dists) CK(cudaMemcpyAsync(out_dists, idx->out_dists.p, sizeof(double) * q * k, cudaMemcpyDeviceToHost, idx->st));
+  unsigned long long total = 0;
+  CK(cudaMemcpyAsync(&total, emitted_total, sizeof(total), cudaMemcpyDeviceToHost, idx->st));
+  CK(cudaStreamSynchronize(idx->st));
+  idx->last_bf_cands = (int64_t)total;
+  idx->last_bf_fallback = novf;
+  idx->last_bf_tc = true;
+  idx->last_bf_path = 2;
+  *unc_out = 0;
+  if (novf > 0) {
+    // exact fp64 path for the flagged queries
+    std::vector<int> hovf(q);
+    CK(cudaMemcpy(hovf.data(), ovf, sizeof(int) * q, cudaMemcpyDeviceToHost));
+    std::vector<int64_t> sel;
+    for (int64_t i = 0; i < q; ++i)
+      if (hovf[i]) sel.push_back(i);
+    const int64_t s = (int64_t)sel.size();
+    std::vector<double> sqf((size_t)s * m);
+    std::vector<int64_t> sqa((size_t)s * l), sqm((size_t)s * l);
+    for (int64_t j = 0; j < s; ++j) {
+      memcpy(&sqf[j * m], qf + sel[j] * m, sizeof(double) * m);
+      memcpy(&sqa[j * l], qa + sel[j] * l, sizeof(int64_t) * l);
+      if (qmask) memcpy(&sqm[j * l], qmask + sel[j] * l, sizeof(int64_t) * l);
+    }
+    const size_t sub = sizeof(double) * s * m + 2 * sizeof(int64_t) * s * l + (sizeof(int64_t) + sizeof(double)) * s * k;
+    CK(idx->tovf.ensure(sub + 64));
+    double* d_qf = idx->tovf.as<double>();
+    int64_t* d_qa = reinterpret_cast<int64_t*>(d_qf + s * m);
+    int64_t* d_qm = d_qa + s * l;
+    int64_t* d_ids = d_qm + s * l;
+    double* d_d = reinterpret_cast<double*>(d_ids + s * k);
+    CK(cudaMemcpyAsync(d_qf, sqf.data(), sizeof(double) * s * m, cudaMemcpyHostToDevice, idx->st));
+    CK(cudaMemcpyAsync(d_qa, sqa.data(), sizeof(int64_t) * s * l, cudaMemcpyHostToDevice, idx->st));
+    if (qmask) CK(cudaMemcpyAsync(d_qm, sqm.data(), sizeof(int64_t) * s * l, cudaMemcpyHostToDevice, idx->st));
+    sb::BfArgs a{};
+    a.F = idx->F.as<float>(); a.A = idx->A.as<int32_t>(); a.n = n; a.m = m; a.l = l;
+    a.qf = d_qf; a.qa = d_qa; a.qmask = qmask ? d_qm : nullptr; a.q = s;
+    a.k = (int)std::min<int64_t>(n, k + 16); a.alpha = alpha;
+    int unc = 0;
+    int r = bf_run(idx, a, k, d_ids, nullptr, d_d, &unc);
+    if (r) return r;
+    std::vector<int64_t> hi((size_t)s * k);
+    std::vector<double> hd((size_t)s * k);
+    CK(cudaMemcpyAsync(hi.data(), d_ids, sizeof(int64_t) * s * k, cudaMemcpyDeviceToHost, idx->st));
+    CK(cudaMemcpyAsync(hd.data(), d_d, sizeof(double) * s * k, cudaMemcpyDeviceToHost, idx->st));
+    CK(cudaStreamSynchronize(idx->st));
+    for (int64_t j = 0; j < s; ++j) {
+      memcpy(out_ids + sel[j] * k, &hi[j * k], sizeof(int64_t) * k);
+      if (out_dists) memcpy(out_dists + sel[j] * k, &hd[j * k], sizeof(double) * k);
+    }
+    *unc_out = unc;
+  }
   return SB_OK;
 }
 
@@ -933,6 +1153,17 @@ int sb_bf_topk_queries(sb_index* idx, const double* qf, const int64_t* qa, const
   if (u8) fold = false;
   const int mk = fold ? idx->m + 16 : idx->m;
   const int esz = u8 ? 1 : 2;  // operand bytes per element
+  // other data: TF32 tensor-core filter with a certified bound + exact fp64 re-rank (bf_tf.cu)
+  double qmax_abs = 0.0;
+  bool tf = !tc && !idx->force_sequential && sb::bf_tf_supported(idx->m, idx->l, k) &&
+            idx->fmax < 1e15;
+  for (int64_t i = 0; tf && i < q * idx->m; ++i) {
+    const double v = std::fabs(qf[i]);
+    tf = v < 1e15;  // also rejects NaN
+    qmax_abs = std::max(qmax_abs, v);
+  }
+  if (const char* e = getenv("SB_BF_TF")) tf = tf && atoi(e) != 0;
+  if (const char* e = getenv("SB_BF_TC")) tf = tf && atoi(e) != 0;  // no tensor cores at all
   if (tc) {
     kk = k;
     a.k = kk;
@@ -950,41 +1181,8 @@ int sb_bf_topk_queries(sb_index* idx, const double* qf, const int64_t* qa, const
       int32_t* s_code = s_nx + npad;
       int32_t* s_orig = s_code + npad;
       int32_t* s_attr = s_orig + npad;
-      CK(idx->small.ensure(64));
-      CK(idx->fb_tmp.ensure(sizeof(int32_t) * (2 * 8 + n + 2) + sizeof(int64_t) * 8));
-      int32_t* d_lo = idx->fb_tmp.as<int32_t>();
-      int32_t* d_hi = d_lo + 8;
-      int32_t* d_code = d_hi + 8;
-      int64_t* d_stride = reinterpret_cast<int64_t*>(d_code + n + (n & 1));
-      std::vector<int32_t> hlo(8, 0x7FFFFFFF), hhi(8, (int32_t)0x80000000);
-      CK(cudaMemcpyAsync(d_lo, hlo.data(), sizeof(int32_t) * 8, cudaMemcpyHostToDevice, idx->st));
-      CK(cudaMemcpyAsync(d_hi, hhi.data(), sizeof(int32_t) * 8, cudaMemcpyHostToDevice, idx->st));
-      CKL(sb::launch_tc_attr_range(idx->A.as<int32_t>(), n, l, d_lo, d_hi, idx->st));
-      CK(cudaMemcpyAsync(hlo.data(), d_lo, sizeof(int32_t) * 8, cudaMemcpyDeviceToHost, idx->st));
-      CK(cudaMemcpyAsync(hhi.data(), d_hi, sizeof(int32_t) * 8, cudaMemcpyDeviceToHost, idx->st));
-      CK(cudaStreamSynchronize(idx->st));
-      std::vector<int64_t> stride(8, 0);
-      int64_t combos = 1;
-      for (int u = l - 1; u >= 0; --u) {
-        stride[u] = combos;
-        combos *= (int64_t)hhi[u] - hlo[u] + 1;
-        if (combos > ((int64_t)1 << 24)) break;
-      }
-      const int grouped = combos <= ((int64_t)1 << 24) ? 1 : 0;
-      const int64_t bins = grouped ? combos : n;
-      CK(cudaMemcpyAsync(d_stride, stride.data(), sizeof(int64_t) * 8, cudaMemcpyHostToDevice, idx->st));
-      CK(idx->rev_cnt.ensure(sizeof(int64_t) * std::max<int64_t>(bins, n)));
-      CK(idx->rev_off.ensure(sizeof(int64_t) * std::max<int64_t>(bins, n)));
-      CK(idx->rev_cur.ensure(sizeof(int64_t) * std::max<int64_t>(bins, n)));
-      CK(idx->scan_tmp.ensure(sizeof(int64_t) * sb::scan_tmp_slots(std::max<int64_t>(bins, n))));
-      CK(cudaMemsetAsync(idx->rev_cnt.p, 0, sizeof(int64_t) * bins, idx->st));
-      CK(cudaMemsetAsync(idx->rev_cur.p, 0, sizeof(int64_t) * bins, idx->st));
-      CKL(sb::launch_tc_code(idx->A.as<int32_t>(), n, l, d_lo, d_stride, grouped, d_code,
-                             idx->rev_cnt.as<unsigned long long>(), idx->st));
-      CKL(sb::exclusive_scan(idx->rev_cnt.as<int64_t>(), idx->rev_off.as<int64_t>(), bins,
-                             idx->scan_tmp.as<int64_t>(), idx->st));
-      CKL(sb::launch_tc_scatter(d_code, n, idx->rev_off.as<int64_t>(),
-                                idx->rev_cur.as<unsigned long long>(), s_orig, idx->st));
+      int32_t* d_code = nullptr;
+      { int r = node_order(idx, s_orig, &d_code); if (r) return r; }
       if (u8)
         CKL(sb::launch_tc_gather_u8(idx->F.as<float>(), idx->A.as<int32_t>(), d_code, s_orig, n,
                                     idx->m, l, idx->fb.p, s_nx, s_code, s_attr, idx->st));
@@ -1034,10 +1232,17 @@ int sb_bf_topk_queries(sb_index* idx, const double* qf, const int64_t* qa, const
     CK(cudaMemcpyAsync(&unc, d_unc, sizeof(int), cudaMemcpyDeviceToHost, idx->st));
     idx->launches += 3;
     idx->last_bf_tc = true;
+    idx->last_bf_path = 1;
+  } else if (tf) {
+    int r = bf_tf_run(idx, qf, qa, qmask, q, k, alpha, qmax_abs, out_ids, out_dists, &unc);
+    if (r) return r;
+    if (uncertain) *uncertain = unc;
+    return SB_OK;
   } else {
     int r = bf_run(idx, a, k, idx->out_ids.as<int64_t>(), nullptr, idx->out_dists.as<double>(), &unc);
     if (r) return r;
     idx->last_bf_tc = false;
+    idx->last_bf_path = 0;
   }
   CK(cudaMemcpyAsync(out_ids, idx->out_ids.p, sizeof(int64_t) * q * k, cudaMemcpyDeviceToHost, idx->st));
   if (out_dists) CK(cudaMemcpyAsync(out_dists, idx->out_dists.p, sizeof(double) * q * k, cudaMemcpyDeviceToHost, idx->st));

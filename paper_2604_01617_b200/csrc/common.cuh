@@ -303,4 +303,42 @@ SB_DEV int lower_bound_u64(const uint64_t* s, int n, uint64_t x) {
   return lo;
 }
 
+// NumPy's pairwise sum of squared differences (x_v - q)^2 for one pair (the order
+// evaluate.py:48's (diff*diff).sum(axis=1) uses): 8-way unrolled blocks of <= 128 elements,
+// halves (rounded down to a multiple of 8) above that.
+static __device__ __noinline__ double np_pairwise_sq(const float* x, const double* q, int n) {
+  if (n > 128) {
+    int n2 = n / 2;
+    n2 -= n2 % 8;
+    return dadd(np_pairwise_sq(x, q, n2), np_pairwise_sq(x + n2, q + n2, n - n2));
+  }
+  if (n < 8) {
+    double res = 0.0;
+    for (int i = 0; i < n; ++i) {
+      double d = dsub((double)x[i], q[i]);
+      res = dadd(res, dmul(d, d));
+    }
+    return res;
+  }
+  double r[8];
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    double d = dsub((double)x[j], q[j]);
+    r[j] = dmul(d, d);
+  }
+  int i = 8;
+  for (; i < n - (n % 8); i += 8)
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      double d = dsub((double)x[i + j], q[i + j]);
+      r[j] = dadd(r[j], dmul(d, d));
+    }
+  double res = dadd(dadd(dadd(r[0], r[1]), dadd(r[2], r[3])), dadd(dadd(r[4], r[5]), dadd(r[6], r[7])));
+  for (; i < n; ++i) {
+    double d = dsub((double)x[i], q[i]);
+    res = dadd(res, dmul(d, d));
+  }
+  return res;
+}
+
 }  // namespace sb

@@ -118,6 +118,29 @@ int launch_bf_tc(const void* Fb, const int32_t* nx, const int32_t* A, const int3
                  double alpha, double* part_d, uint32_t* part_i, int* gthr, int fold, int u8,
                  cudaStream_t st);
 
+// tensor-core query-mode top-k for real-valued data (bf_tf.cu): TF32 filter, exact re-rank
+double tf_margin(int dpad);
+int bf_tf_supported(int m, int l, int kk);
+int bf_tf_dpad(int m);
+void bf_tf_layout(int m, int l, int kk, int* qblock, int* hsegs);
+int launch_tf_gather(const float* F, const int32_t* A, const int32_t* code_in, const int32_t* orig,
+                     int64_t n, int m, int l, double cE, float* Ft, float* nxd, int32_t* code,
+                     int32_t* As, cudaStream_t st);
+int launch_tf_runend(const int32_t* code, int64_t n, int32_t* runend, cudaStream_t st);
+int launch_tf_prep_queries(const double* qf, int64_t q, int64_t qpad, int m, double cE, double tiny,
+                           float* Qt, float* nqs, float* nqu, cudaStream_t st);
+int launch_bf_tf(const float* Ft, const float* nxd, const int32_t* code,
+                 const int32_t* orig, const int32_t* runend, const int32_t* As, const float* Qt, const float* nqs,
+                 const float* nqu, const int64_t* qa, const int64_t* qmask, int64_t n, int64_t q,
+                 int m, int l, int kk, int splits, double alpha, int* gthr, uint32_t* cnt,
+                 uint64_t* cand, int cap, uint32_t* ocnt, uint64_t* ocand, int ocap, int seed,
+                 cudaStream_t st);
+int launch_tf_refine(const float* F, const int32_t* A, int m, int l, const double* qf,
+                     const int64_t* qa, const int64_t* qmask, int64_t q, int k, double alpha,
+                     const uint32_t* cnt, const uint64_t* cand, int segs, int cap,
+                     const uint32_t* ocnt, const uint64_t* ocand, int ocap, const int* gthr, int scap, int64_t* out_ids, double* out_d, int* ovf, int* ovf_count,
+                     unsigned long long* emitted_total, cudaStream_t st);
+
 // ---- HELP build ---------------------------------------------------------------
 // random initial rows (help_init.cu): device ids, consumed PCG64 outputs, rows with repeats
 int launch_init_random_ids(uint64_t seed, int64_t n, int g, int32_t* ids, int64_t* scratch,

@@ -87,6 +87,18 @@ class DeviceIndex:
         names = {0: "fp64", 1: "fp32", 2: "fp32-groups", 3: "fp64-generic", 4: "u8-dp4a"}
         return {"path": names.get(path.value, "none"), "row_bytes": rb.value}
 
+    def bf_info(self) -> dict:
+        """Path of the last exhaustive top-k call, TF32 candidates passed to the re-rank and
+        queries recomputed on the fp64 kernel (sb_bf_info)."""
+        path = ctypes.c_int32(-1)
+        cands = ctypes.c_int64(0)
+        fb = ctypes.c_int64(0)
+        _lib.call("sb_bf_info", self._h, ctypes.addressof(path), ctypes.addressof(cands),
+                  ctypes.addressof(fb))
+        names = {0: "fp64", 1: "tc-int-exact", 2: "tc-tf32-filter"}
+        return {"path": names.get(path.value, "none"), "candidates": cands.value,
+                "fallback_queries": fb.value}
+
     def route_prepare(self):
         """Build the routing layout (locality order, u8 copy) now; see sb_route_prepare."""
         _lib.call("sb_route_prepare", self._h)

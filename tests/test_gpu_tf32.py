@@ -1,0 +1,158 @@
+"""Exhaustive AUTO top-k for real-valued data on the tensor cores (bf_tf.cu): the TF32 filter
+with a certified error bound must hand the exact re-rank every true member, so ids and fp64
+distances equal the exact fp64 SIMT kernel and the CPU oracle (oracle_auto_topk,
+evaluate.py:32-55) bit for bit — ragged K chunks, streamed and resident query tiles, masks,
+duplicate points (ties by id), k up to 100, and queries whose candidates overflow the buffers
+(recomputed on the fp64 kernel)."""
+
+import os
+
+import numpy as np
+import pytest
+
+import paper_2604_01617_b200 as sb
+from oracle import oracle as O
+from paper_2604_01617_b200.device import DeviceIndex
+
+pytestmark = pytest.mark.gpu
+
+
+def _data(kind, n, m, q, rng):
+    if kind == "normal":
+        f = rng.standard_normal((n, m)).astype(np.float32)
+        qf = rng.standard_normal((q, m))
+    elif kind == "gauss_w":  # cfg 5's recipe: N(0, I) W
+        w = rng.standard_normal((m, m))
+        f = (rng.standard_normal((n, m)) @ w).astype(np.float32)
+        qf = (rng.standard_normal((q, m)) @ w).astype(np.float32).astype(np.float64)
+    elif kind == "unit":  # cfg 3's recipe: clustered unit vectors
+        mu = rng.standard_normal((16, m))
+        mu /= np.linalg.norm(mu, axis=1, keepdims=True)
+        x = 8.0 * mu[rng.integers(0, 16, n + q)] + rng.standard_normal((n + q, m))
+        x = (x / np.linalg.norm(x, axis=1, keepdims=True)).astype(np.float32)
+        f, qf = x[:n], x[n:].astype(np.float64)
+    elif kind == "gamma":  # cfg 4's recipe: Gamma(2, 1) with a per-dimension scale
+        s = np.exp(rng.uniform(-1, 1, m))
+        f = (rng.gamma(2.0, 1.0, (n, m)) * s).astype(np.float32)
+        qf = (rng.gamma(2.0, 1.0, (q, m)) * s).astype(np.float32).astype(np.float64)
+    elif kind == "dup":  # duplicates and near-duplicates
+        f = rng.standard_normal((n, m)).astype(np.float32)
+        f[10:40] = f[3]
+        f[50:60] = f[3] + np.float32(1e-6)
+        qf = rng.standard_normal((q, m))
+        qf[0] = f[3]
+        qf[1] = f[3] + 1e-7
+    else:
+        raise ValueError(kind)
+    return f, np.ascontiguousarray(qf, np.float64)
+
+
+def _fp64_path(d, qf, qa, k, alpha, mk):
+    os.environ["SB_BF_TF"] = "0"
+    try:
+        out = d.bf_topk_queries(qf, qa, k, alpha, mk)
+        assert d.bf_info()["path"] == "fp64"
+        return out
+    finally:
+        del os.environ["SB_BF_TF"]
+
+
+@pytest.mark.parametrize("kind,n,m,l,q,k", [
+    ("normal", 10000, 32, 1, 200, 10),     # cfg 1 shape
+    ("gauss_w", 6000, 100, 1, 130, 10),    # d = 100: ragged last K chunk (104)
+    ("unit", 3001, 96, 2, 129, 100),       # k = 100, ragged node and query tiles
+    ("gamma", 2500, 960, 2, 70, 10),       # d = 960: streamed query tile
+    ("normal", 777, 7, 3, 5, 1),           # d = 7, k = 1
+    ("dup", 5000, 33, 2, 300, 32),         # ties by id
+])
+def test_tf32_topk_exact(kind, n, m, l, q, k):
+    rng = np.random.default_rng(n + m + k)
+    f, qf = _data(kind, n, m, q, rng)
+    a = rng.integers(1, 5, (n, l)).astype(np.int32)
+    qa = rng.integers(1, 5, (q, l))
+    masks = rng.integers(0, 2, (q, l))
+    alpha = 0.37 if kind != "unit" else 0.05
+    d = DeviceIndex(f, a, 2)
+    assert not d.info()["int_exact"]
+    for mk in (None, masks):
+        ids, dd = d.bf_topk_queries(qf, qa, k, alpha, mk)
+        info = d.bf_info()
+        assert info["path"] == "tc-tf32-filter", info
+        assert info["fallback_queries"] == 0, info
+        ids_s, dd_s = _fp64_path(d, qf, qa, k, alpha, mk)
+        np.testing.assert_array_equal(ids, ids_s)
+        np.testing.assert_array_equal(dd, dd_s)
+        for qi in sorted(set(list(range(0, q, max(1, q // 6))) + [0, 1, q - 1])):
+            wi, wd = O.oracle_auto_topk(f, a, qf[qi], qa[qi], k, alpha,
+                                        None if mk is None else mk[qi], return_dists=True)
+            np.testing.assert_array_equal(ids[qi], wi, err_msg=f"query {qi}")
+            np.testing.assert_array_equal(dd[qi], wd, err_msg=f"query {qi}")
+
+
+def test_tf32_filter_is_selective():
+    """The certified window passes few candidates per query to the exact re-rank."""
+    rng = np.random.default_rng(5)
+    n, m, q, k = 20000, 96, 256, 10
+    f, qf = _data("unit", n, m, q, rng)
+    a = rng.integers(1, 4, (n, 1)).astype(np.int32)
+    qa = rng.integers(1, 4, (q, 1))
+    d = DeviceIndex(f, a, 2)
+    d.bf_topk_queries(qf, qa, k, 0.2)
+    info = d.bf_info()
+    assert info["path"] == "tc-tf32-filter"
+    assert info["candidates"] / q < 0.1 * n, info
+
+
+@pytest.mark.parametrize("n", [3000, 12000])
+def test_tf32_overflow_falls_back_exactly(n):
+    """Points closer together than the TF32 window (steps of 1e-7 along one dimension): every
+    node is a candidate, so the survivors overflow the re-rank (more than 2048); those queries
+    are recomputed on the exact fp64 kernel and the answer is still the oracle's."""
+    rng = np.random.default_rng(n)
+    f = np.tile(rng.standard_normal((1, 40)).astype(np.float32), (n, 1))
+    f[:, 0] += (np.arange(n) * 1e-7).astype(np.float32)
+    a = np.ones((n, 1), np.int32)
+    qf = rng.standard_normal((3, 40))
+    qa = np.ones((3, 1), np.int64)
+    d = DeviceIndex(f, a, 2)
+    ids, dd = d.bf_topk_queries(qf, qa, 10, 0.5)
+    info = d.bf_info()
+    assert info["path"] == "tc-tf32-filter" and info["fallback_queries"] == 3, info
+    for qi in range(3):
+        wi, wd = O.oracle_auto_topk(f, a, qf[qi], qa[qi], 10, 0.5, return_dists=True)
+        np.testing.assert_array_equal(ids[qi], wi)
+        np.testing.assert_array_equal(dd[qi], wd)
+
+
+def test_tf32_public_api_and_config_cfg1():
+    """oracle_auto_topk_batch (the public API) on the cfg 1 recipe takes the TF32 path."""
+    rng = np.random.default_rng(0)
+    X = rng.standard_normal((10000, 32), dtype=np.float32)
+    A = rng.integers(1, 5, (10000, 1), dtype=np.int32)
+    QX = rng.standard_normal((200, 32), dtype=np.float32)
+    QA = rng.integers(1, 5, (200, 1), dtype=np.int32)
+    cfg = sb.compute_alpha(sb.sample_statistics(X, A, 1000, seed=0), 10000, 1)
+    gt, gd = sb.oracle_auto_topk_batch(X, A, QX, QA, 10, cfg, return_dists=True)
+    for qi in range(0, 200, 9):
+        wi, wd = O.oracle_auto_topk(X, A, QX[qi], QA[qi], 10, cfg.alpha, return_dists=True)
+        np.testing.assert_array_equal(gt[qi], wi)
+        np.testing.assert_array_equal(gd[qi], wd)
+
+
+@pytest.mark.parametrize("tile", ["128,4,1,2", "256,3,1,1", "128,3,1,1", "256,2,0,1", "128,4,0,1"])
+def test_tf32_every_tile_shape(tile, monkeypatch):
+    """Every kernel instance (two resident query tiles x 128 nodes; one query tile x 256 or 128
+    nodes, resident or streamed) gives the exact answer, seed pass included."""
+    monkeypatch.setenv("SB_TF_TILE", tile)
+    rng = np.random.default_rng(7)
+    n, m, l, q, k = 7000, 100, 2, 300, 16
+    f, qf = _data("gauss_w", n, m, q, rng)
+    a = rng.integers(1, 4, (n, l)).astype(np.int32)
+    qa = rng.integers(1, 4, (q, l))
+    masks = rng.integers(0, 2, (q, l))
+    d = DeviceIndex(f, a, 2)
+    ids, dd = d.bf_topk_queries(qf, qa, k, 0.6, masks)
+    assert d.bf_info()["path"] == "tc-tf32-filter" and d.bf_info()["fallback_queries"] == 0
+    ids_s, dd_s = _fp64_path(d, qf, qa, k, 0.6, masks)
+    np.testing.assert_array_equal(ids, ids_s)
+    np.testing.assert_array_equal(dd, dd_s)

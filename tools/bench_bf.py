@@ -22,7 +22,7 @@ for mode in os.environ.get("MODES", "1,0").split(","):
     res[mode] = (ids, dd)
     q, n, m = QX.shape[0], X.shape[0], X.shape[1]
     flops = 2.0 * q * n * m
-    print(f"SB_BF_TC={mode} tc={d.info()['last_bf_tc']} {dt*1e3:.1f} ms  {q*n/dt/1e9:.1f} G scores/s  "
+    print(f"SB_BF_TC={mode} {d.bf_info()} {dt*1e3:.1f} ms  {q*n/dt/1e9:.1f} G scores/s  "
           f"{flops/dt/1e12:.1f} TFLOP/s useful", flush=True)
 if len(res) == 2:
     print("identical:", np.array_equal(res["1"][0], res["0"][0]) and np.array_equal(res["1"][1], res["0"][1]))
