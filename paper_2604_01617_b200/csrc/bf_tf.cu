@@ -41,8 +41,6 @@
 namespace sb {
 
 constexpr int kTfM = 128;                 // queries per CTA (UMMA M, TMEM lanes)
-constexpr int kTfEpi = 256;               // epilogue threads: two per query
-constexpr int kTfThreads = kTfEpi + 96;   // + operand loader, MMA and metadata warps
 constexpr int kTfKC = 32;                 // K elements per streamed chunk
 constexpr int kTfChunkBytes = kTfM * kTfKC * 4;  // one full 128-row chunk block
 
@@ -152,37 +150,42 @@ struct TfArgs {
   int dpad, l, kk, splits, stages;
   double alpha;
   int* gthr;               // q: best upper bound of U_k^2 over all threads (fp32 bits)
-  uint32_t* cnt;           // q x segs: candidates each epilogue thread emitted
-  uint64_t* cand;          // q x segs x cap: (lower key bits << 32) | original id
-  int cap;                 // per segment; segs = splits x (epilogue threads per query per CTA)
+  uint32_t* cnt;           // one per epilogue thread of the grid: candidates it emitted
+  uint64_t* cand;          // (CTA, thread) segments of cap: (lower key bits << 32) | original id;
+                           // a CTA's segments are contiguous (its stores stay within a few pages)
+  int cap;
   uint32_t* ocnt;          // q: entries in the query's shared overflow area (full segments)
   uint64_t* ocand;         // q x ocap
   int ocap;
-  int seed;                // 1: bound-only pass over the first tile of each range (no emission)
-  int dbg;                 // timing experiments (SB_TF_DEBUG): 1 = no epilogue work, 2 = no MMAs
+  int seed;                // > 0: bound-only pass over `seed` evenly spread tiles per split
+  int strided;             // 1: split s walks tiles s, s + splits, ...; 0: contiguous ranges
 };
 
 constexpr int kTfMetaStages = 4;
-constexpr int kTfQueue = 8;  // per-thread queue of one tile's filter survivors
 
 SB_HD size_t tf_meta_bytes(int N, int l) { return (size_t)N * (4 + l) * 4; }
 
-// shared layout: [A resident | A stages] | B stages | meta ring | lists | t2 | barriers
-SB_HD size_t tf_smem_bytes(int dpad, int l, int kk, int N, int stages, bool ares, int qt) {
+// shared layout: [A resident | A stages] | B stages | meta ring | smem lists (KR = 0) | bounds |
+// query attributes | barriers
+SB_HD size_t tf_smem_bytes(int dpad, int l, int kk, int N, int stages, bool ares, int qt, int ew, int kr) {
+  const int epi = 32 * ew;
   const size_t a = ares ? (size_t)qt * kTfM * dpad * 4 : (size_t)stages * qt * kTfChunkBytes;
-  return 1024 + a + (size_t)stages * N * kTfKC * 4 + kTfMetaStages * tf_meta_bytes(N, l) +
-         sizeof(float) * (size_t)kk * kTfEpi + sizeof(float) * kTfEpi +
-         sizeof(uint64_t) * kTfQueue * kTfEpi + 8 * 32 + 16;
+  return a + (size_t)stages * N * kTfKC * 4 + kTfMetaStages * tf_meta_bytes(N, l) +
+         (kr == 0 ? sizeof(float) * (size_t)kk * epi : 0) + sizeof(float) * epi +
+         2 * sizeof(int32_t) * (size_t)l * qt * kTfM + 8 * 32 + 16;
 }
 
 // N = nodes per tile, ARES = query tiles resident in shared memory, QT = query tiles (of 128)
-// per CTA.  TMEM: 2 buffers x QT x N fp32 columns.  Epilogue warp w reads TMEM lane group w % 4;
-// with QT = 2 warps 0..3 own query tile 0 and warps 4..7 tile 1 (all N columns each); with
-// QT = 1 they own the two column halves of the one query tile.
-template <int N, bool ARES, int QT>
-__global__ void __launch_bounds__(kTfThreads, 1) bf_tf_kernel(TfArgs a) {
-  constexpr int H = QT == 1 ? 2 : 1;       // epilogue threads per query
-  constexpr int cols = N / H;              // columns per epilogue thread and tile
+// per CTA, EW = epilogue warps (8 or 16), KR = register list length (16, 32; 0 = list in shared
+// memory).  TMEM: 2 buffers x QT x N fp32 columns.  Epilogue warp w reads TMEM lane group w % 4;
+// the EW / 4 warps of a lane group split the QT query tiles and their columns: PPQ = EW / 4 / QT
+// threads per query, N / PPQ columns each.
+template <int N, bool ARES, int QT, int EW, int KR>
+__global__ void __launch_bounds__(32 * EW + 64, 1) bf_tf_kernel(TfArgs a) {
+  constexpr int EPI = 32 * EW;              // epilogue threads
+  constexpr int PPQ = EW / 4 / QT;          // epilogue threads per query
+  constexpr int cols = N / PPQ;             // columns per epilogue thread and tile
+  static_assert(cols % 32 == 0, "32-column TMEM loads");
   // (pointer arithmetic on the shared array itself keeps every access an LDS/STS)
   extern __shared__ __align__(1024) char smem[];
   const int tid = threadIdx.x;
@@ -194,9 +197,11 @@ __global__ void __launch_bounds__(kTfThreads, 1) bf_tf_kernel(TfArgs a) {
   char* sA = p; p += ARES ? QT * qblk_bytes : (size_t)S * QT * kTfChunkBytes;
   char* sB = p; p += (size_t)S * N * kTfKC * 4;
   char* sM = p; p += kTfMetaStages * meta_bytes;
-  float* ul = reinterpret_cast<float*>(p); p += sizeof(float) * (size_t)a.kk * kTfEpi;
-  volatile float* s_t2 = reinterpret_cast<float*>(p); p += sizeof(float) * kTfEpi;
-  uint64_t* s_q = reinterpret_cast<uint64_t*>(p); p += sizeof(uint64_t) * kTfQueue * kTfEpi;
+  float* ul = reinterpret_cast<float*>(p); p += KR == 0 ? sizeof(float) * (size_t)a.kk * EPI : 0;
+  volatile float* s_t2 = reinterpret_cast<float*>(p); p += sizeof(float) * EPI;
+  int32_t* s_qa = reinterpret_cast<int32_t*>(p); p += sizeof(int32_t) * (size_t)l * QT * kTfM;
+  int32_t* s_qm = reinterpret_cast<int32_t*>(p); p += sizeof(int32_t) * (size_t)l * QT * kTfM;
+  p += (8 - ((p - smem) & 7)) & 7;
   uint64_t* bars = reinterpret_cast<uint64_t*>(p);
   uint32_t* tslot = reinterpret_cast<uint32_t*>(bars + 31);
   // barriers: full[0..7] sfree[8..15] fullM[16..19] emptyM[20..23] accf[24,25] empty[26,27]
@@ -210,37 +215,60 @@ __global__ void __launch_bounds__(kTfThreads, 1) bf_tf_kernel(TfArgs a) {
   auto bar_empty = [&](int s) { return b0 + 8u * (uint32_t)(26 + s); };
   const uint32_t bar_aready = b0 + 8u * 28;
 
+  // tiles of this CTA: i -> tile0 + i * tstride
   const int64_t tiles = (a.n + N - 1) / N;
-  const int64_t per = (tiles + a.splits - 1) / a.splits;
-  const int64_t t_begin = per * blockIdx.y;
-  const int64_t t_end = t_begin + per < tiles ? t_begin + per : tiles;
-  int ntl = t_end > t_begin ? (int)(t_end - t_begin) : 0;
-  if (a.seed && ntl > 1) ntl = 1;
+  int ntl;
+  int64_t tile0, tstride;
+  if (a.seed) {  // bound-only pass: a.seed tiles per split, spread evenly over the sorted order
+    const int64_t total = (int64_t)a.seed * a.splits < tiles ? (int64_t)a.seed * a.splits : tiles;
+    ntl = blockIdx.y < total ? (int)((total - blockIdx.y + a.splits - 1) / a.splits) : 0;
+    tile0 = (int64_t)blockIdx.y * (tiles / total);
+    tstride = tiles / total * a.splits;
+  } else if (a.strided) {
+    // split s walks tiles s, s + splits, ...: every split sees the same mix of attribute codes,
+    // so the survivors of queries with popular codes do not pile up in a few CTAs
+    ntl = tiles > blockIdx.y ? (int)((tiles - blockIdx.y + a.splits - 1) / a.splits) : 0;
+    tile0 = blockIdx.y;
+    tstride = a.splits;
+  } else {  // contiguous ranges
+    const int64_t per = (tiles + a.splits - 1) / a.splits;
+    tile0 = per * blockIdx.y;
+    tstride = 1;
+    ntl = tile0 < tiles ? (int)(tile0 + per < tiles ? per : tiles - tile0) : 0;
+  }
 
   if (warp_id() == 0) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tslot)),
                  "r"(2 * QT * N));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
-  if (tid == kTfEpi) {
+  if (tid == EPI) {
     for (int s = 0; s < S; ++s) {
       mbar_init(bar_full(s), 1);
       mbar_init(bar_sfree(s), 1);
     }
     for (int s = 0; s < kTfMetaStages; ++s) {
       mbar_init(bar_fullM(s), 1);
-      mbar_init(bar_emptyM(s), kTfEpi);
+      mbar_init(bar_emptyM(s), EPI);
     }
     for (int s = 0; s < 2; ++s) {
       mbar_init(bar_accf(s), 1);
-      mbar_init(bar_empty(s), kTfEpi);
+      mbar_init(bar_empty(s), EPI);
     }
     mbar_init(bar_aready, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  if (tid < kTfEpi) {
-    for (int i = 0; i < a.kk; ++i) ul[i * kTfEpi + tid] = FLT_MAX;
+  if (tid < EPI) {
+    if (KR == 0)
+      for (int i = 0; i < a.kk; ++i) ul[i * EPI + tid] = FLT_MAX;
     s_t2[tid] = FLT_MAX;
+  }
+  // query attributes and masks of the CTA's queries
+  for (int i = tid; i < QT * kTfM * l; i += blockDim.x) {
+    const int64_t g = (int64_t)blockIdx.x * QT * kTfM + i / l;
+    const bool ok = g < a.q;
+    s_qa[i] = ok ? (int32_t)a.qa[g * l + i % l] : 0;
+    s_qm[i] = ok ? (int32_t)(a.qmask ? a.qmask[g * l + i % l] : 1) : 0;
   }
   tc_fence_before();
   __syncthreads();
@@ -248,8 +276,8 @@ __global__ void __launch_bounds__(kTfThreads, 1) bf_tf_kernel(TfArgs a) {
   const uint32_t tmem = *tslot;
   const char* qblk = a.Qt + (size_t)blockIdx.x * QT * qblk_bytes;
 
-  if (warp_id() == kTfEpi / 32) {
-    // ---------------- operand loader ----------------
+  if (warp_id() == EW) {
+    // ---------------- loaders: lane 0 operands, lane 1 node metadata (its own ring) --------
     if (lane_id() == 0 && ntl > 0) {
       if (ARES) {
         const uint32_t ab = (uint32_t)(QT * qblk_bytes);
@@ -258,7 +286,7 @@ __global__ void __launch_bounds__(kTfThreads, 1) bf_tf_kernel(TfArgs a) {
       }
       int it = 0;
       for (int i = 0; i < ntl; ++i) {
-        const int64_t v0 = (t_begin + i) * (int64_t)N;
+        const int64_t v0 = ((int64_t)i * tstride + tile0) * (int64_t)N;
         for (int c = 0; c < nch; ++c, ++it) {
           const int st = it % S;
           const int use = it / S;
@@ -281,16 +309,12 @@ __global__ void __launch_bounds__(kTfThreads, 1) bf_tf_kernel(TfArgs a) {
           }
         }
       }
-    }
-    __syncwarp();
-  } else if (warp_id() == kTfEpi / 32 + 2) {
-    // ---------------- metadata loader (its own ring, ahead of the accumulators) -------------
-    if (lane_id() == 0) {
+    } else if (lane_id() == 1) {
       for (int i = 0; i < ntl; ++i) {
         const int ms = i % kTfMetaStages;
         const int use = i / kTfMetaStages;
         if (use >= 1) mbar_wait(bar_emptyM(ms), (uint32_t)((use - 1) & 1));
-        const int64_t v0 = (t_begin + i) * (int64_t)N;
+        const int64_t v0 = ((int64_t)i * tstride + tile0) * (int64_t)N;
         char* meta = sM + ms * meta_bytes;
         const uint32_t fm = bar_fullM(ms);
         mbar_expect_tx(fm, (uint32_t)meta_bytes);
@@ -302,7 +326,7 @@ __global__ void __launch_bounds__(kTfThreads, 1) bf_tf_kernel(TfArgs a) {
       }
     }
     __syncwarp();
-  } else if (warp_id() == kTfEpi / 32 + 1) {
+  } else if (warp_id() == EW + 1) {
     // ---------------- MMA issuer ----------------
     if (lane_id() == 0 && ntl > 0) {
       // TF32 x TF32 -> F32: c_format = 1 [4,6), a/b format = 2 [7,10) [10,13), N >> 3 [17,23),
@@ -327,7 +351,7 @@ __global__ void __launch_bounds__(kTfThreads, 1) bf_tf_kernel(TfArgs a) {
             const uint32_t ab = ARES ? smem_u32(sA + t * qblk_bytes + (size_t)c * kTfChunkBytes)
                                      : smem_u32(sA + ((size_t)st * QT + t) * kTfChunkBytes);
             const uint32_t dt = tmem + (uint32_t)((acc * QT + t) * N);
-            for (int s = 0; s < cw / 8 && !(a.dbg & 2); ++s) {
+            for (int s = 0; s < cw / 8; ++s) {
               const uint64_t ad = umma_desc(ab + (uint32_t)s * 256, 128, sbo);
               const uint64_t bd = umma_desc(bb + (uint32_t)s * 256, 128, sbo);
               asm volatile(
@@ -346,25 +370,23 @@ __global__ void __launch_bounds__(kTfThreads, 1) bf_tf_kernel(TfArgs a) {
   } else {
     // ---------------- epilogue ----------------
     const int lg = warp_id() & 3;                 // TMEM lane group
-    const int slot = warp_id() >> 2;
-    const int qt = QT == 2 ? slot : 0;            // query tile
-    const int half = QT == 1 ? slot : 0;          // column half (QT == 1)
+    const int u = warp_id() >> 2;
+    const int qt = u / PPQ;                       // query tile
+    const int part = u % PPQ;                     // column part
     const int row = lg * 32 + lane_id();
-    const int64_t my_q = ((int64_t)blockIdx.x * QT + qt) * kTfM + row;
+    const int qrow = qt * kTfM + row;             // query within the CTA's block
+    const int64_t my_q = (int64_t)blockIdx.x * QT * kTfM + qrow;
     const bool qok = my_q < a.q;
     const float nq_s = qok ? a.nqs[my_q] : 0.f;
     const float nq_u = qok ? a.nqu[my_q] : 0.f;
-    int32_t qa_row[8];
-    int32_t qm_row[8];
-#pragma unroll
-    for (int u = 0; u < 8; ++u) {
-      qa_row[u] = (qok && u < l) ? (int32_t)a.qa[my_q * l + u] : 0;
-      qm_row[u] = (qok && u < l) ? (int32_t)(a.qmask ? a.qmask[my_q * l + u] : 1) : 0;
-    }
     const float ia = __double2float_ru(1.0 / a.alpha);
     const int kk = a.kk;
-    // min(own list tail, partner's, global); starts from the seed pass's bound
+    // min(own list tail, partners', global); starts from the seed pass's bound
     float t2_eff = qok ? fminf(FLT_MAX, __int_as_float(a.gthr[my_q])) : FLT_MAX;
+    float own_t2 = FLT_MAX;     // this thread's kk-th smallest upper key
+    float rl[KR > 0 ? KR : 1];  // KR > 0: the list in registers, -FLT_MAX in its first KR - kk
+#pragma unroll
+    for (int j = 0; j < (KR > 0 ? KR : 1); ++j) rl[j] = j < (KR > 0 ? KR : 1) - kk ? -FLT_MAX : FLT_MAX;
     int last_code = -2;
     float f2 = 1.f, inv_f2 = 1.f, thr_h = -FLT_MAX;
     // y = 2 z >= thr  <=>  lo = nqs - y <= T2 / f^2 (conservatively rounded); thr_h = thr / 2
@@ -372,84 +394,81 @@ __global__ void __launch_bounds__(kTfThreads, 1) bf_tf_kernel(TfArgs a) {
       const float t = t2_eff * inv_f2 * 1.00002f;
       thr_h = t >= FLT_MAX ? -FLT_MAX : 0.5f * (nq_s - t);
     };
+    const int32_t* s_at = nullptr;  // the current tile's node attributes
     // f^2 of a node's attribute tuple for this query (f = 1 + s_a / alpha, fp32, rounded up)
-    const int32_t* s_at_cur = nullptr;
     auto attr_f2 = [&](int col) {
       int sa = 0;
-#pragma unroll
-      for (int u = 0; u < 8; ++u)
-        if (u < l) sa += abs(s_at_cur[col * l + u] - qa_row[u]) * qm_row[u];
+      for (int w = 0; w < l; ++w) sa += abs(s_at[col * l + w] - s_qa[qrow * l + w]) * s_qm[qrow * l + w];
       const float f = fmaf((float)sa, ia, 1.0f);
       return f * f;
     };
-    int p_code = -2;   // factor state of the queue processing
-    float p_f2 = 1.f;
-    const uint32_t lane_base = tmem + ((uint32_t)(lg * 32) << 16) + (uint32_t)(qt * N + half * cols);
-    // this thread's private candidate segment: no atomics on the emission path
-    const int segs = H * a.splits;
-    const size_t seg = (size_t)my_q * segs + H * blockIdx.y + half;
+    const uint32_t lane_base = tmem + ((uint32_t)(lg * 32) << 16) + (uint32_t)(qt * N + part * cols);
+    // this thread's private candidate segment (no atomics on the emission path)
+    const size_t seg = ((size_t)blockIdx.y * gridDim.x + blockIdx.x) * EPI + tid;
     uint64_t* my_cand = qok ? a.cand + seg * a.cap : nullptr;
     uint32_t emitted = 0;
     for (int i = 0; i < ntl; ++i) {
       const int s = i & 1;
-      const uint32_t ph = (uint32_t)((i >> 1) & 1);
       const int ms = i % kTfMetaStages;
       const char* meta = sM + ms * meta_bytes;
       const float* s_nxd = reinterpret_cast<const float*>(meta);
       const int32_t* s_code = reinterpret_cast<const int32_t*>(meta + N * 4);
       const int32_t* s_orig = reinterpret_cast<const int32_t*>(meta + N * 8);
       const int32_t* s_run = reinterpret_cast<const int32_t*>(meta + N * 12);
-      s_at_cur = reinterpret_cast<const int32_t*>(meta + N * 16);
-      const int64_t vb = (t_begin + i) * (int64_t)N;
+      s_at = reinterpret_cast<const int32_t*>(meta + N * 16);
+      const int64_t vb = ((int64_t)i * tstride + tile0) * (int64_t)N;
       const int nvalid = (int)(a.n - vb < N ? a.n - vb : N);
       const float gpre = qok ? __int_as_float(*reinterpret_cast<volatile int*>(a.gthr + my_q)) : FLT_MAX;
       mbar_wait(bar_fullM(ms), (uint32_t)((i / kTfMetaStages) & 1));
-      mbar_wait(bar_accf(s), ph);
+      mbar_wait(bar_accf(s), (uint32_t)((i >> 1) & 1));
       tc_fence_after();
-      // one filter survivor: exact-order keys, emission, this thread's upper-key list
+      // one filter survivor: emission (lower key), this thread's upper-key list
       auto process = [&](int col, float zj, float fsq) {
         const float yj = 2.0f * zj;
         const float lo = fmaxf(nq_s - yj, 0.f) * fsq * 0.99998f;
         if (lo > t2_eff) return;
-        if (a.dbg & 8) atomicAdd(a.cnt + (size_t)a.q * H * a.splits + 2, 1u);
-        // emit: a possible member of the exact top k
-        if (!a.seed && !(a.dbg & 16)) {
+        if (!a.seed) {  // a possible member of the exact top k
           const uint64_t e = ((uint64_t)__float_as_uint(lo) << 32) | (uint32_t)s_orig[col];
           if (emitted < (uint32_t)a.cap) {
             my_cand[emitted++] = e;
           } else {  // segment full: the query's shared overflow area
-            const uint32_t slot2 = atomicAdd(a.ocnt + my_q, 1u);
-            if (slot2 < (uint32_t)a.ocap) a.ocand[(size_t)my_q * a.ocap + slot2] = e;
+            const uint32_t slot = atomicAdd(a.ocnt + my_q, 1u);
+            if (slot < (uint32_t)a.ocap) a.ocand[(size_t)my_q * a.ocap + slot] = e;
           }
         }
-        // upper key (nqu + nxu - 2 dot = nq_u - y + nxd) into this thread's k smallest
+        // upper key (nqu + nxu - 2 dot = nq_u - y + nxd) into this thread's kk smallest
         const float hi = fmaxf(nq_u - yj + s_nxd[col], 0.f) * fsq * 1.00002f;
-        if ((a.dbg & 32) || !(hi < ul[(kk - 1) * kTfEpi + tid])) return;
-        int pos = kk - 1;
-        while (pos > 0) {
-          const float pv = ul[(pos - 1) * kTfEpi + tid];
-          if (!(hi < pv)) break;
-          ul[pos * kTfEpi + tid] = pv;
-          --pos;
+        if (!(hi < own_t2)) return;
+        if (KR > 0) {  // sorted register list: one branch-free pass, no memory chain
+#pragma unroll
+          for (int j = KR - 1; j > 0; --j) rl[j] = hi < rl[j - 1] ? rl[j - 1] : fminf(hi, rl[j]);
+          rl[0] = fminf(rl[0], hi);
+          own_t2 = rl[KR - 1];
+        } else {
+          int pos = kk - 1;
+          while (pos > 0) {
+            const float pv = ul[(pos - 1) * EPI + tid];
+            if (!(hi < pv)) break;
+            ul[pos * EPI + tid] = pv;
+            --pos;
+          }
+          ul[pos * EPI + tid] = hi;
+          own_t2 = ul[(kk - 1) * EPI + tid];
         }
-        ul[pos * kTfEpi + tid] = hi;
-        if (a.dbg & 8) atomicAdd(a.cnt + (size_t)a.q * H * a.splits + 3, 1u);
-        const float t2 = ul[(kk - 1) * kTfEpi + tid];
-        if (t2 < t2_eff) {
-          t2_eff = t2;
+        if (own_t2 < t2_eff) {
+          t2_eff = own_t2;
           set_thr();
-          if (!(a.dbg & 64)) atomicMin(a.gthr + my_q, __float_as_int(t2));  // floats >= 0 order as ints
+          atomicMin(a.gthr + my_q, __float_as_int(own_t2));  // non-negative floats order as ints
         }
       };
-      // scan: the fast filter over the accumulator; survivors wait in a small queue so that
-      // the accumulator goes back to the MMA warp as soon as the scan ends
-      int qn = 0;
+      // scan: the fast filter over the accumulator.  All lanes of a warp see the same columns
+      // (nodes) for different queries, so the chunk / run structure is warp-uniform; survivors
+      // are processed in rounds, one per lane per round, so lanes with work run in parallel.
 #pragma unroll 1
       for (int c = 0; c < cols / 32; ++c) {
         uint32_t r[32];
         tmem_ld32(lane_base + (uint32_t)(s * QT * N + c * 32), r);
-        if (!qok || (a.dbg & 1)) continue;
-        const int c0 = half * cols + c * 32;
+        const int c0 = part * cols + c * 32;
         // the accumulator holds z = y / 2 with y = 2 x.q - nxs: one max decides the chunk
         float m0 = fmaxf(__uint_as_float(r[0]), __uint_as_float(r[1]));
         float m1 = fmaxf(__uint_as_float(r[2]), __uint_as_float(r[3]));
@@ -459,9 +478,9 @@ __global__ void __launch_bounds__(kTfThreads, 1) bf_tf_kernel(TfArgs a) {
           m1 = fmaxf(m1, __uint_as_float(r[j + 1]));
         }
         const float mx = fmaxf(m0, m1);
-        const bool uniform = s_code[c0] == last_code && s_code[c0 + 31] == last_code;
-        if (uniform && mx < thr_h) continue;
-        if (a.dbg & 8) atomicAdd(a.cnt + (size_t)a.q * H * a.splits, 1u);
+        const bool uniform = s_code[c0] == last_code && s_code[c0 + 31] == last_code;  // warp-uniform
+        const bool act = qok && !(uniform && mx < thr_h);
+        if (!__any_sync(0xffffffffu, act)) continue;
         const int jend = nvalid - c0 < 32 ? nvalid - c0 : 32;
         // runs of equal codes inside the chunk: one factor (and threshold) per run
         for (int j0 = 0; j0 < jend;) {
@@ -482,44 +501,31 @@ __global__ void __launch_bounds__(kTfThreads, 1) bf_tf_kernel(TfArgs a) {
 #pragma unroll
           for (int j = 0; j < 32; ++j)
             cand |= (j >= j0 && j < j1 && __uint_as_float(r[j]) >= thr_h ? 1u : 0u) << j;
+          if (!act) cand = 0;
           j0 = j1;
-          if (a.dbg & 8) atomicAdd(a.cnt + (size_t)a.q * H * a.splits + 1, (unsigned)__popc(cand));
-          if (a.dbg & 4) continue;
-          while (cand) {
-            const int j = __ffs(cand) - 1;
-            cand &= cand - 1u;
-            float zj = 0.f;
+          while (__any_sync(0xffffffffu, cand != 0)) {
+            if (cand) {
+              const int j = __ffs(cand) - 1;
+              cand &= cand - 1u;
+              float zj = 0.f;
 #pragma unroll
-            for (int jj = 0; jj < 32; ++jj)
-              if (jj == j) zj = __uint_as_float(r[jj]);
-            if (qn < kTfQueue) {
-              s_q[qn * kTfEpi + tid] = ((uint64_t)__float_as_uint(zj) << 32) | (uint32_t)(c0 + j);
-              ++qn;
-            } else {
-              process(c0 + j, zj, f2);  // queue full: now (the scan's factor is this column's)
+              for (int jj = 0; jj < 32; ++jj)
+                if (jj == j) zj = __uint_as_float(r[jj]);
+              process(c0 + j, zj, f2);
             }
           }
         }
       }
       tc_fence_before();
       mbar_arrive(bar_empty(s));
-      // the queued survivors, in column order (their codes ascend)
-      for (int e = 0; e < qn; ++e) {
-        const uint64_t v = s_q[e * kTfEpi + tid];
-        const int col = (int)(uint32_t)v;
-        const int code = s_code[col];
-        if (code != p_code) {
-          p_code = code;
-          p_f2 = attr_f2(col);
-        }
-        process(col, __uint_as_float((uint32_t)(v >> 32)), p_f2);
-      }
       mbar_arrive(bar_emptyM(ms));
-      // share bounds with the other column half (QT == 1) and with the other CTAs
+      // share bounds with the query's other epilogue threads and with the other CTAs
       float pt = gpre;
-      if (H == 2) {
+      if (PPQ > 1) {
         s_t2[tid] = t2_eff;
-        pt = fminf(pt, s_t2[tid ^ kTfM]);
+#pragma unroll
+        for (int q2 = 0; q2 < PPQ; ++q2)
+          pt = fminf(pt, s_t2[(lg + 4 * (qt * PPQ + q2)) * 32 + lane_id()]);
       }
       if (pt < t2_eff) {
         t2_eff = pt;
@@ -536,12 +542,25 @@ __global__ void __launch_bounds__(kTfThreads, 1) bf_tf_kernel(TfArgs a) {
   }
 }
 
+// segment of query g's sg-th epilogue thread (sg = split * ppq + column part); matches the
+// kernel's (CTA, thread) numbering
+SB_DEV size_t tf_seg(int64_t g, int sg, int splits, int ppq, int qblock, int ew, int64_t q) {
+  const int64_t G = (q + qblock - 1) / qblock;
+  const int64_t qb = g / qblock;
+  const int w = (int)(g % qblock);
+  const int sp = sg / ppq, part = sg % ppq;
+  const int qt = w / kTfM, row = w % kTfM;
+  const int t = ((row >> 5) + 4 * (qt * ppq + part)) * 32 + (row & 31);
+  return ((size_t)sp * G + qb) * (32 * ew) + t;
+}
+
 // ---- refine: exact top k of each query's survivors (warp per query) -----------------------
 __global__ void tf_refine_kernel(const float* __restrict__ F, const int32_t* __restrict__ A, int m, int l,
                                  const double* __restrict__ qf, const int64_t* __restrict__ qa,
                                  const int64_t* __restrict__ qmask, int64_t q, int k, double alpha,
                                  const uint32_t* __restrict__ cnt, const uint64_t* __restrict__ cand,
-                                 int segs, int cap, const uint32_t* __restrict__ ocnt,
+                                 int splits, int hsegs, int qblock, int ew, int cap,
+                                 const uint32_t* __restrict__ ocnt,
                                  const uint64_t* __restrict__ ocand, int ocap, const int* __restrict__ gthr, int scap, int64_t* out_ids,
                                  double* out_d, int* ovf, int* ovf_count,
                                  unsigned long long* emitted_total) {
@@ -558,15 +577,17 @@ __global__ void tf_refine_kernel(const float* __restrict__ F, const int32_t* __r
   bool bad = false;
   if (lane == 0) {
     unsigned long long tot = 0;
-    for (int sg = 0; sg < segs; ++sg) tot += cnt[(size_t)g * segs + sg];
+    for (int sg = 0; sg < splits * hsegs; ++sg) tot += cnt[tf_seg(g, sg, splits, hsegs, qblock, ew, q)];
     tot += ocnt[g];
     atomicAdd(emitted_total, tot);
   }
-  // segments 0..segs-1, then the overflow area
+  // the query's segments (one per split and epilogue thread), then its overflow area
+  const int segs = splits * hsegs;
   for (int sg = 0; sg <= segs && !bad; ++sg) {
-    const uint32_t c = sg < segs ? cnt[(size_t)g * segs + sg] : ocnt[g];
+    const size_t sid = sg < segs ? tf_seg(g, sg, splits, hsegs, qblock, ew, q) : 0;
+    const uint32_t c = sg < segs ? cnt[sid] : ocnt[g];
     if (sg == segs && c > (uint32_t)ocap) { bad = true; break; }
-    const uint64_t* cg = sg < segs ? cand + ((size_t)g * segs + sg) * cap : ocand + (size_t)g * ocap;
+    const uint64_t* cg = sg < segs ? cand + sid * cap : ocand + (size_t)g * ocap;
     for (uint32_t base = 0; base < c; base += 32) {
       const uint32_t i = base + lane;
       bool ok = false;
@@ -632,40 +653,47 @@ double tf_margin(int dpad) {
   return 1.25 * (c1 + std::ldexp(1.0, -21) + std::ldexp(1.0, -20)) + std::ldexp(1.0, -19);
 }
 
-struct TfShape { int N, stages; bool ares; int qt; };
+struct TfShape { int N, stages; bool ares; int qt, ew, kr; };
 
 // Tile shape: the first that fits shared memory, in order of preference.  Two resident query
-// tiles against 128-node tiles halve the node-operand traffic per MMA (L2 -> SM bandwidth is
-// the limit of one 128 x 256 TF32 tile per SM); wide rows stream both operands.
+// tiles against 128-node tiles halve the node-operand traffic per MMA; wide rows stream both
+// operands.  k <= 32 keeps the per-thread lists in registers and runs 16 epilogue warps; larger
+// k keeps them in shared memory with 8.
 static TfShape tf_shape(int dpad, int l, int kk) {
-  if (l > 8 || kk > 256 || dpad > 4096) return {0, 0, false, 0};
+  if (l > 8 || kk > 256 || dpad > 4096) return {0, 0, false, 0, 0, 0};
   const size_t limit = 227 * 1024;
+  int kr = kk <= 16 ? 16 : kk <= 32 ? 32 : 0;
+  if (const char* e = getenv("SB_TF_KR")) kr = atoi(e) == 0 ? 0 : kr;  // testing: the smem list
+  const int ew = kr > 0 ? 16 : 8;
   if (const char* e = getenv("SB_TF_TILE")) {  // "N,stages,ares,qt" (testing)
     int Nn = 0, st = 0, ar = 0, qt = 1;
     if (sscanf(e, "%d,%d,%d,%d", &Nn, &st, &ar, &qt) == 4 && (Nn == 128 || Nn == 256) && st >= 2 &&
         st <= 8 && (qt == 1 || qt == 2) && 2 * qt * Nn <= 512 &&
-        tf_smem_bytes(dpad, l, kk, Nn, st, ar != 0, qt) <= limit)
-      return {Nn, st, ar != 0, qt};
+        tf_smem_bytes(dpad, l, kk, Nn, st, ar != 0, qt, ew, kr) <= limit)
+      return {Nn, st, ar != 0, qt, ew, kr};
   }
   const int pref[][4] = {// N, max stages, min stages, qt (resident query tiles)
                          {128, 8, 4, 2}, {256, 6, 3, 1}, {128, 8, 3, 1}};
   for (auto& pr : pref)
     for (int st = pr[1]; st >= pr[2]; --st)
-      if (tf_smem_bytes(dpad, l, kk, pr[0], st, true, pr[3]) <= limit) return {pr[0], st, true, pr[3]};
+      if (tf_smem_bytes(dpad, l, kk, pr[0], st, true, pr[3], ew, kr) <= limit)
+        return {pr[0], st, true, pr[3], ew, kr};
   const int spref[][2] = {{256, 4}, {256, 3}, {256, 2}, {128, 6}, {128, 4}, {128, 2}};
   for (auto& pr : spref)
-    if (tf_smem_bytes(dpad, l, kk, pr[0], pr[1], false, 1) <= limit) return {pr[0], pr[1], false, 1};
-  return {0, 0, false, 0};
+    if (tf_smem_bytes(dpad, l, kk, pr[0], pr[1], false, 1, ew, kr) <= limit)
+      return {pr[0], pr[1], false, 1, ew, kr};
+  return {0, 0, false, 0, 0, 0};
 }
 
 int bf_tf_supported(int m, int l, int kk) { return tf_shape(tf_dpad(m), l, kk).N != 0; }
 int bf_tf_dpad(int m) { return tf_dpad(m); }
 
-// queries per CTA (query block) and epilogue threads per query of the chosen shape
-void bf_tf_layout(int m, int l, int kk, int* qblock, int* hsegs) {
+// queries per CTA (query block), epilogue threads per query and epilogue warps of the shape
+void bf_tf_layout(int m, int l, int kk, int* qblock, int* ppq, int* ew) {
   const TfShape sh = tf_shape(tf_dpad(m), l, kk);
   *qblock = sh.qt * kTfM;
-  *hsegs = sh.qt == 1 ? 2 : 1;
+  *ppq = sh.ew / 4 / sh.qt;
+  *ew = sh.ew;
 }
 
 int launch_tf_gather(const float* F, const int32_t* A, const int32_t* code_in, const int32_t* orig,
@@ -695,7 +723,7 @@ int launch_bf_tf(const float* Ft, const float* nxd, const int32_t* code,
                  const float* nqu, const int64_t* qa, const int64_t* qmask, int64_t n, int64_t q,
                  int m, int l, int kk, int splits, double alpha, int* gthr, uint32_t* cnt,
                  uint64_t* cand, int cap, uint32_t* ocnt, uint64_t* ocand, int ocap, int seed,
-                 cudaStream_t st) {
+                 int strided, cudaStream_t st) {
   const int dpad = tf_dpad(m);
   const TfShape sh = tf_shape(dpad, l, kk);
   if (sh.N == 0) return (int)cudaErrorInvalidValue;
@@ -705,23 +733,29 @@ int launch_bf_tf(const float* Ft, const float* nxd, const int32_t* code,
   a.qmask = qmask; a.n = n; a.q = q; a.dpad = dpad; a.l = l; a.kk = kk; a.splits = splits;
   a.stages = sh.stages; a.alpha = alpha; a.gthr = gthr; a.cnt = cnt; a.cand = cand;
   a.cap = cap; a.ocnt = ocnt; a.ocand = ocand; a.ocap = ocap; a.seed = seed;
-  a.dbg = 0;
-  if (const char* e = getenv("SB_TF_DEBUG")) a.dbg = atoi(e);
-  const size_t smem = tf_smem_bytes(dpad, l, kk, sh.N, sh.stages, sh.ares, sh.qt);
-  void (*kern)(TfArgs) = sh.qt == 2 ? bf_tf_kernel<128, true, 2>
-                       : sh.N == 256 ? (sh.ares ? bf_tf_kernel<256, true, 1> : bf_tf_kernel<256, false, 1>)
-                                     : (sh.ares ? bf_tf_kernel<128, true, 1> : bf_tf_kernel<128, false, 1>);
+  a.strided = strided;
+  const size_t smem = tf_smem_bytes(dpad, l, kk, sh.N, sh.stages, sh.ares, sh.qt, sh.ew, sh.kr);
+  void (*kern)(TfArgs) = nullptr;
+#define SB_TF_PICK(EW, KR)                                                                          \
+  kern = sh.qt == 2 ? bf_tf_kernel<128, true, 2, EW, KR>                                            \
+       : sh.N == 256 ? (sh.ares ? bf_tf_kernel<256, true, 1, EW, KR> : bf_tf_kernel<256, false, 1, EW, KR>) \
+                     : (sh.ares ? bf_tf_kernel<128, true, 1, EW, KR> : bf_tf_kernel<128, false, 1, EW, KR>)
+  if (sh.kr == 16) SB_TF_PICK(16, 16);
+  else if (sh.kr == 32) SB_TF_PICK(16, 32);
+  else SB_TF_PICK(8, 0);
+#undef SB_TF_PICK
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return (int)e;
   const int qb = sh.qt * kTfM;
   dim3 grid((unsigned)((q + qb - 1) / qb), (unsigned)splits);
-  kern<<<grid, kTfThreads, smem, st>>>(a);
+  kern<<<grid, 32 * sh.ew + 64, smem, st>>>(a);
   return (int)cudaGetLastError();
 }
 
 int launch_tf_refine(const float* F, const int32_t* A, int m, int l, const double* qf,
                      const int64_t* qa, const int64_t* qmask, int64_t q, int k, double alpha,
-                     const uint32_t* cnt, const uint64_t* cand, int segs, int cap,
+                     const uint32_t* cnt, const uint64_t* cand, int splits, int hsegs, int qblock,
+                     int ew, int cap,
                      const uint32_t* ocnt, const uint64_t* ocand, int ocap, const int* gthr, int scap, int64_t* out_ids, double* out_d, int* ovf, int* ovf_count,
                      unsigned long long* emitted_total, cudaStream_t st) {
   const int wpb = 4;
@@ -729,7 +763,7 @@ int launch_tf_refine(const float* F, const int32_t* A, int m, int l, const doubl
   cudaError_t e = cudaFuncSetAttribute(tf_refine_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return (int)e;
   tf_refine_kernel<<<(unsigned)((q + wpb - 1) / wpb), wpb * 32, smem, st>>>(
-      F, A, m, l, qf, qa, qmask, q, k, alpha, cnt, cand, segs, cap, ocnt, ocand, ocap, gthr, scap, out_ids, out_d, ovf,
+      F, A, m, l, qf, qa, qmask, q, k, alpha, cnt, cand, splits, hsegs, qblock, ew, cap, ocnt, ocand, ocap, gthr, scap, out_ids, out_d, ovf,
       ovf_count, emitted_total);
   return (int)cudaGetLastError();
 }

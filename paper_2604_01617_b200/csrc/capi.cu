@@ -82,6 +82,7 @@ struct sb_index {
   int64_t last_bf_fallback = 0;   // queries of the last TF32 call recomputed on the fp64 path
   int64_t last_bf_cands = 0;      // candidates the last TF32 call emitted (all queries)
   bool have_ft = false;           // TF32 operand copy + metadata (bf_tf.cu)
+  int tf_strided = 1;             // walk the node tiles strided (skewed attribute codes)
   bool have_f8 = false;           // u8 feature copy for routing (integer data in [0, 255])
   // routing layout: nodes renumbered in a locality order (route_layout); valid while
   // rl_version == graph_version (every call that changes the adjacency bumps graph_version)
@@ -891,6 +892,21 @@ static int node_order(sb_index* idx, int32_t* s_orig, int32_t** d_code_out) {
              idx->scan_tmp.as<int64_t>(), idx->st));
   CKL(sb::launch_tc_scatter(d_code, n, idx->rev_off.as<int64_t>(),
             idx->rev_cur.as<unsigned long long>(), s_orig, idx->st));
+  // skewed code sizes (one tuple far above the mean, e.g. Zipf codes) make the exhaustive
+  // top-k walk node tiles strided across the splits (bf_tf.cu), so no CTA owns a hot region
+  idx->tf_strided = 0;
+  if (grouped && bins <= ((int64_t)1 << 22)) {
+    std::vector<int64_t> hist(bins);
+    CK(cudaMemcpyAsync(hist.data(), idx->rev_cnt.p, sizeof(int64_t) * bins, cudaMemcpyDeviceToHost, idx->st));
+    CK(cudaStreamSynchronize(idx->st));
+    int64_t mx = 0, used = 0;
+    for (int64_t b = 0; b < bins; ++b) {
+      mx = std::max(mx, hist[b]);
+      used += hist[b] > 0;
+    }
+    idx->tf_strided = used > 1 && mx * used > 4 * n ? 1 : 0;
+  }
+  if (const char* e = getenv("SB_TF_STRIDE")) idx->tf_strided = atoi(e) != 0;
   *d_code_out = d_code;
   return SB_OK;
 }
@@ -950,8 +966,8 @@ static int bf_tf_run(sb_index* idx, const double* qf, const int64_t* qa, const i
     idx->have_cand = false;  // rev_* scratch was reused
     idx->launches += 5;
   }
-  int qblock = 128, hsegs = 2;
-  sb::bf_tf_layout(m, l, k, &qblock, &hsegs);
+  int qblock = 128, hsegs = 2, ew = 8;
+  sb::bf_tf_layout(m, l, k, &qblock, &hsegs, &ew);
   const int64_t qpad = (q + qblock - 1) / qblock * qblock;
   // node-range splits: whole waves of one CTA per SM, fewest splits within 3% of the best
   const int groups = (int)(qpad / qblock);
@@ -972,18 +988,18 @@ static int bf_tf_run(sb_index* idx, const double* qf, const int64_t* qa, const i
       if (cost[s2] <= best * 1.03) { splits = s2; break; }
     if (const char* e = getenv("SB_TF_SPLITS")) splits = std::max(1, atoi(e));
   }
-  // one candidate segment per epilogue thread of a query (two per CTA); a thread emits about
-  // k (1 + ln(its nodes / k)) candidates at most once its own list is full
-  const int segs = hsegs * splits;
-  int cap = std::max(512, 16 * k);
-  while (cap > 64 && (double)q * segs * cap * 8.0 > 8e9) cap /= 2;
+  // one candidate segment per epilogue thread of the grid; after the seed pass a thread emits
+  // a few dozen candidates (full segments spill into the query's overflow area)
+  const int64_t nthreads = (int64_t)groups * splits * 32 * ew;
+  int cap = std::max(256, 32 * k);
+  while (cap > 64 && (double)nthreads * cap * 8.0 > 8e9) cap /= 2;
   if (const char* e = getenv("SB_TF_CAP")) cap = std::max(1, atoi(e));
-  const int scap = 2048;
-  const int ocap = 4096;  // per-query overflow area behind full segments
+  const int scap = k > 32 ? 4096 : 2048;  // survivors of the final bound the re-rank takes
+  const int ocap = std::max(4096, 64 * k);  // per-query overflow area behind full segments
   // tq: Qt (qpad x dpad f32) | nqs | nqu | gthr | ovf | ovf_count | emitted total | ocnt (q) |
   //     cnt (q x segs)
   const size_t qt_bytes = (size_t)4 * qpad * dpad;
-  CK(idx->tq.ensure(qt_bytes + (size_t)4 * 5 * q + 80 + (size_t)4 * q * segs));
+  CK(idx->tq.ensure(qt_bytes + (size_t)4 * 5 * q + 64 + (size_t)4 * nthreads));
   float* Qt = idx->tq.as<float>();
   float* nqs = reinterpret_cast<float*>(idx->tq.as<char>() + qt_bytes);
   float* nqu = nqs + q;
@@ -994,32 +1010,29 @@ static int bf_tf_run(sb_index* idx, const double* qf, const int64_t* qa, const i
       reinterpret_cast<unsigned long long*>(reinterpret_cast<uintptr_t>(ovf_count + 2) & ~(uintptr_t)7);
   uint32_t* ocnt = reinterpret_cast<uint32_t*>(emitted_total + 2);
   uint32_t* cnt = ocnt + q;
-  CK(idx->tcand.ensure(sizeof(uint64_t) * ((size_t)q * segs * cap + (size_t)q * ocap)));
-  uint64_t* ocand = idx->tcand.as<uint64_t>() + (size_t)q * segs * cap;
+  CK(idx->tcand.ensure(sizeof(uint64_t) * ((size_t)nthreads * cap + (size_t)q * ocap)));
+  uint64_t* ocand = idx->tcand.as<uint64_t>() + (size_t)nthreads * cap;
   CK(cudaMemsetAsync(gthr, 0x7F, sizeof(int) * q, idx->st));  // 0x7F7F7F7F = 3.39e38f
   CK(cudaMemsetAsync(ovf, 0, reinterpret_cast<char*>(cnt) - reinterpret_cast<char*>(ovf), idx->st));
-  CK(cudaMemsetAsync(cnt + (size_t)q * segs, 0, 16, idx->st));  // SB_TF_DEBUG & 8 counters
   // absolute slack for tf32 subnormal rounding and fp32 product underflow (negligible otherwise)
   const double tiny = dpad * std::ldexp(1.0, -120) * (1.0 + idx->fmax) * (1.0 + qmax_abs);
   CKL(sb::launch_tf_prep_queries(idx->qf.as<double>(), q, qpad, m, cE, tiny, Qt, nqs, nqu, idx->st));
   // seed pass (first tile of every range, bound only), then the full pass
-  for (int seed = 1; seed >= 0; --seed)
+  // seed pass: enough evenly spread tiles that every thread's list of k fills several times
+  int seed_tiles = std::min(64, std::max(4, k / 2));
+  if (const char* e = getenv("SB_TF_SEED")) seed_tiles = std::max(0, atoi(e));
+  for (int seed = seed_tiles; seed >= 0; seed = seed > 0 ? 0 : -1)
     CKL(sb::launch_bf_tf(idx->ft.as<float>(), nxd, s_code, s_orig, s_run, s_attr, Qt, nqs, nqu,
                          idx->bf_qa.as<int64_t>(), qmask ? idx->bf_qm.as<int64_t>() : nullptr, n, q,
                          m, l, k, splits, alpha, gthr, cnt, idx->tcand.as<uint64_t>(), cap, ocnt,
-                         ocand, ocap, seed, idx->st));
+                         ocand, ocap, seed, idx->tf_strided, idx->st));
   CKL(sb::launch_tf_refine(idx->F.as<float>(), idx->A.as<int32_t>(), m, l, idx->qf.as<double>(),
                            idx->bf_qa.as<int64_t>(), qmask ? idx->bf_qm.as<int64_t>() : nullptr, q,
-                           k, alpha, cnt, idx->tcand.as<uint64_t>(), segs, cap, ocnt, ocand, ocap, gthr, scap,
+                           k, alpha, cnt, idx->tcand.as<uint64_t>(), splits, hsegs, qblock, ew, cap, ocnt, ocand,
+                           ocap, gthr, scap,
                            idx->out_ids.as<int64_t>(), idx->out_dists.as<double>(), ovf, ovf_count,
                            emitted_total, idx->st));
   idx->launches += 4;
-  if (getenv("SB_TF_DEBUG") && (atoi(getenv("SB_TF_DEBUG")) & 8)) {
-    uint32_t h[4];
-    CK(cudaMemcpy(h, cnt + (size_t)q * segs, sizeof(h), cudaMemcpyDeviceToHost));
-    fprintf(stderr, "tf debug: chunks past the max test %u, filter survivors %u, emitted %u, "
-            "list inserts %u\n", h[0], h[1], h[2], h[3]);
-  }
   int novf = 0;
   CK(cudaMemcpyAsync(&novf, ovf_count, sizeof(int), cudaMemcpyDeviceToHost, idx->st));
   CK(cudaMemcpyAsync(out_ids, idx->out_ids.p, sizeof(int64_t) * q * k, cudaMemcpyDeviceToHost, idx->st));

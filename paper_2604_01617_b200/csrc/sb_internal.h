@@ -122,7 +122,7 @@ int launch_bf_tc(const void* Fb, const int32_t* nx, const int32_t* A, const int3
 double tf_margin(int dpad);
 int bf_tf_supported(int m, int l, int kk);
 int bf_tf_dpad(int m);
-void bf_tf_layout(int m, int l, int kk, int* qblock, int* hsegs);
+void bf_tf_layout(int m, int l, int kk, int* qblock, int* ppq, int* ew);
 int launch_tf_gather(const float* F, const int32_t* A, const int32_t* code_in, const int32_t* orig,
                      int64_t n, int m, int l, double cE, float* Ft, float* nxd, int32_t* code,
                      int32_t* As, cudaStream_t st);
@@ -134,10 +134,11 @@ int launch_bf_tf(const float* Ft, const float* nxd, const int32_t* code,
                  const float* nqu, const int64_t* qa, const int64_t* qmask, int64_t n, int64_t q,
                  int m, int l, int kk, int splits, double alpha, int* gthr, uint32_t* cnt,
                  uint64_t* cand, int cap, uint32_t* ocnt, uint64_t* ocand, int ocap, int seed,
-                 cudaStream_t st);
+                 int strided, cudaStream_t st);
 int launch_tf_refine(const float* F, const int32_t* A, int m, int l, const double* qf,
                      const int64_t* qa, const int64_t* qmask, int64_t q, int k, double alpha,
-                     const uint32_t* cnt, const uint64_t* cand, int segs, int cap,
+                     const uint32_t* cnt, const uint64_t* cand, int splits, int hsegs, int qblock,
+                     int ew, int cap,
                      const uint32_t* ocnt, const uint64_t* ocand, int ocap, const int* gthr, int scap, int64_t* out_ids, double* out_d, int* ovf, int* ovf_count,
                      unsigned long long* emitted_total, cudaStream_t st);
 
