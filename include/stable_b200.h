@@ -172,9 +172,12 @@ int sb_route_info(sb_index* idx, int32_t* path, int32_t* row_bytes);
 /* the last sb_bf_topk_queries on this handle: *path = 0 exact fp64 kernel, 1 tcgen05 with exact
  * integer products (integer data), 2 tcgen05 TF32 filter with a certified error bound + exact
  * fp64 re-rank (other data); *candidates = pairs the TF32 filter passed to the re-rank (all
- * queries); *fallback = queries whose candidates overflowed and were recomputed on path 0.
- * Replaces nothing in the reference (instrumentation of evaluate.py:32-55's replacement). */
-int sb_bf_info(sb_index* idx, int32_t* path, int64_t* candidates, int64_t* fallback);
+ * queries); *fallback = queries whose candidates overflowed and were recomputed on path 0;
+ * *kernel_ms = duration of the tensor-core pass over all nodes (CUDA events on the handle's
+ * stream; 0 on path 0).  Any pointer may be NULL.  Replaces nothing in the reference
+ * (instrumentation of evaluate.py:32-55's replacement). */
+int sb_bf_info(sb_index* idx, int32_t* path, int64_t* candidates, int64_t* fallback,
+               double* kernel_ms);
 /* Prepare the routing layout now instead of at the first routing call: the nodes renumbered
  * along a locality order (features, attributes and adjacency permuted; results, entries and
  * distance ties still use the original ids, so routing output is unchanged) and, for

@@ -58,7 +58,7 @@ _SIGS = {
     "sb_index_info": [_vp, _vp, _vp, _vp],
     "sb_set_distance_mode": [_vp, _i32],
     "sb_route_info": [_vp, _vp, _vp],
-    "sb_bf_info": [_vp, _vp, _vp, _vp],
+    "sb_bf_info": [_vp, _vp, _vp, _vp, _vp],
     "sb_route_prepare": [_vp],
     "sb_host_alloc": [ctypes.c_size_t, _pp],
     "sb_host_free": [_vp],

@@ -83,6 +83,8 @@ struct sb_index {
   int64_t last_bf_cands = 0;      // candidates the last TF32 call emitted (all queries)
   bool have_ft = false;           // TF32 operand copy + metadata (bf_tf.cu)
   int tf_strided = 1;             // walk the node tiles strided (skewed attribute codes)
+  cudaEvent_t bf_ev[2] = {nullptr, nullptr};  // around the last tensor-core top-k pass
+  bool bf_ev_valid = false;
   bool have_f8 = false;           // u8 feature copy for routing (integer data in [0, 255])
   // routing layout: nodes renumbered in a locality order (route_layout); valid while
   // rl_version == graph_version (every call that changes the adjacency bumps graph_version)
@@ -130,7 +132,16 @@ struct sb_index {
                    &bf_out32, &rf_n8, &rf_nb, &rf_n32, &rf_n64, &rf_o32, &rf_o64,
                    &rf_ulist, &rf_bits, &rf_rec, &rf_sim, &rf_eo};
     for (DBuf* b : all) b->release();
+    if (bf_ev[0]) cudaEventDestroy(bf_ev[0]);
+    if (bf_ev[1]) cudaEventDestroy(bf_ev[1]);
     if (own) cudaStreamDestroy(own);
+  }
+  cudaError_t bf_event(int i) {
+    if (!bf_ev[i]) {
+      cudaError_t e = cudaEventCreate(&bf_ev[i]);
+      if (e != cudaSuccess) return e;
+    }
+    return cudaEventRecord(bf_ev[i], st);
   }
 };
 
@@ -224,8 +235,17 @@ int sb_index_info(sb_index* idx, int32_t* int_exact, double* fmax_abs, int32_t* 
   return SB_OK;
 }
 
-int sb_bf_info(sb_index* idx, int32_t* path, int64_t* candidates, int64_t* fallback) {
+int sb_bf_info(sb_index* idx, int32_t* path, int64_t* candidates, int64_t* fallback,
+               double* kernel_ms) {
   if (!idx) return fail(SB_EARG, "idx is NULL");
+  if (kernel_ms) {
+    *kernel_ms = 0.0;
+    if (idx->bf_ev_valid) {
+      float ms = 0.f;
+      CK(cudaEventElapsedTime(&ms, idx->bf_ev[0], idx->bf_ev[1]));
+      *kernel_ms = ms;
+    }
+  }
   if (path) *path = idx->last_bf_path;
   if (candidates) *candidates = idx->last_bf_cands;
   if (fallback) *fallback = idx->last_bf_fallback;
@@ -1021,11 +1041,15 @@ static int bf_tf_run(sb_index* idx, const double* qf, const int64_t* qa, const i
   // seed pass: enough evenly spread tiles that every thread's list of k fills several times
   int seed_tiles = std::min(64, std::max(4, k / 2));
   if (const char* e = getenv("SB_TF_SEED")) seed_tiles = std::max(0, atoi(e));
-  for (int seed = seed_tiles; seed >= 0; seed = seed > 0 ? 0 : -1)
+  CK(idx->bf_event(0));  // the tensor-core pass = seed + full launch
+  for (int seed = seed_tiles; seed >= 0; seed = seed > 0 ? 0 : -1) {
     CKL(sb::launch_bf_tf(idx->ft.as<float>(), nxd, s_code, s_orig, s_run, s_attr, Qt, nqs, nqu,
                          idx->bf_qa.as<int64_t>(), qmask ? idx->bf_qm.as<int64_t>() : nullptr, n, q,
                          m, l, k, splits, alpha, gthr, cnt, idx->tcand.as<uint64_t>(), cap, ocnt,
                          ocand, ocap, seed, idx->tf_strided, idx->st));
+  }
+  CK(idx->bf_event(1));
+  idx->bf_ev_valid = true;
   CKL(sb::launch_tf_refine(idx->F.as<float>(), idx->A.as<int32_t>(), m, l, idx->qf.as<double>(),
                            idx->bf_qa.as<int64_t>(), qmask ? idx->bf_qm.as<int64_t>() : nullptr, q,
                            k, alpha, cnt, idx->tcand.as<uint64_t>(), splits, hsegs, qblock, ew, cap, ocnt, ocand,
@@ -1236,9 +1260,12 @@ int sb_bf_topk_queries(sb_index* idx, const double* qf, const int64_t* qa, const
     CK(cudaMemsetAsync(d_unc, 0, sizeof(int), idx->st));
     {
       int32_t* s_nx = idx->fb_norm.as<int32_t>();
+      CK(idx->bf_event(0));
       CKL(sb::launch_bf_tc(idx->fb.p, s_nx, s_nx + 3 * npad, s_nx + npad, s_nx + 2 * npad, idx->qb.p,
                            d_nq, a.qa, a.qmask, n, q, mk, idx->l, kk, splits, alpha, a.part_d,
                            a.part_i, d_gthr, fold ? 1 : 0, u8 ? 1 : 0, idx->st));
+      CK(idx->bf_event(1));
+      idx->bf_ev_valid = true;
     }
     CKL(sb::launch_bf_merge_k(a, k, idx->out_ids.as<int64_t>(), nullptr, idx->out_dists.as<double>(),
                               d_unc, idx->st));
@@ -1254,6 +1281,7 @@ int sb_bf_topk_queries(sb_index* idx, const double* qf, const int64_t* qa, const
   } else {
     int r = bf_run(idx, a, k, idx->out_ids.as<int64_t>(), nullptr, idx->out_dists.as<double>(), &unc);
     if (r) return r;
+    idx->bf_ev_valid = false;
     idx->last_bf_tc = false;
     idx->last_bf_path = 0;
   }

@@ -93,11 +93,12 @@ class DeviceIndex:
         path = ctypes.c_int32(-1)
         cands = ctypes.c_int64(0)
         fb = ctypes.c_int64(0)
+        ms = ctypes.c_double(0.0)
         _lib.call("sb_bf_info", self._h, ctypes.addressof(path), ctypes.addressof(cands),
-                  ctypes.addressof(fb))
+                  ctypes.addressof(fb), ctypes.addressof(ms))
         names = {0: "fp64", 1: "tc-int-exact", 2: "tc-tf32-filter"}
         return {"path": names.get(path.value, "none"), "candidates": cands.value,
-                "fallback_queries": fb.value}
+                "fallback_queries": fb.value, "kernel_ms": ms.value}
 
     def route_prepare(self):
         """Build the routing layout (locality order, u8 copy) now; see sb_route_prepare."""
