@@ -643,8 +643,22 @@ int sb_prune(sb_index* idx, double sigma, int32_t* rounds_out) {
   a.cpad = (g + 3) & ~3;
   const size_t stage_budget = 96 * 1024;
   a.dc = (int)std::min<int64_t>(idx->m, (int64_t)(stage_budget / (sizeof(float) * a.cpad)));
-  size_t smem = sb::prune_bits_smem(a.cpad, a.dc, idx->m, idx->l, W);
-  CKL(sb::launch_prune_bits(a, smem, idx->st));
+  // integer features in [0, 255]: exact integer cosine terms from u8 rows (dp4a), unless
+  // SB_PRUNE_U8=0
+  bool prune_u8 = idx->int_exact && idx->flo >= 0.f && idx->fhi <= 255.f && idx->m % 4 == 0 &&
+                  idx->m <= 4096 && !idx->force_sequential;
+  if (const char* e = getenv("SB_PRUNE_U8")) prune_u8 = prune_u8 && atoi(e) != 0;
+  if (prune_u8) {
+    int r = ensure_u8(idx, idx->F.as<float>(), idx->f8, idx->have_f8);
+    if (r) return r;
+    const int32_t* nx8 = reinterpret_cast<const int32_t*>(idx->f8.as<uint8_t>() +
+                                                          (((size_t)n * idx->m + 255) & ~(size_t)255));
+    CKL(sb::launch_prune_bits_u8(a, idx->f8.as<uint8_t>(), nx8,
+                                 sb::prune_bits_u8_smem(a.cpad, idx->m, idx->l, W), idx->st));
+  } else {
+    size_t smem = sb::prune_bits_smem(a.cpad, a.dc, idx->m, idx->l, W);
+    CKL(sb::launch_prune_bits(a, smem, idx->st));
+  }
   int* d_changed = reinterpret_cast<int*>(idx->small.p);
   int rounds = 0;
   for (;;) {

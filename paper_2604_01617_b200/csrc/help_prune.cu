@@ -145,6 +145,93 @@ __global__ void __launch_bounds__(kPruneThreads) prune_bits_kernel(PruneArgs a) 
   for (int t = tid; t < cnt * a.W; t += blockDim.x) out[t] = bits[t];
 }
 
+// Integer features in [0, 255] (the u8 copy F8 with exact squared norms nx8): every product and
+// partial sum of _diff_cosine's fp64 loops (_kernels.py:236-253) is an integer below 2^53, so
+// dot, np2 and nk2 are exact in any order; from the u8 rows
+//   dot(p, k) = x_p.x_k - x_p.x_s - x_k.x_s + |x_s|^2,  np2 = |x_p|^2 - 2 x_p.x_s + |x_s|^2
+// with dp4a, and the cosine is then formed exactly as the reference forms it.  Same bits as
+// prune_bits_kernel.  Rows are staged with a 33-word stride (no bank conflicts between rows).
+__global__ void __launch_bounds__(kPruneThreads) prune_bits_u8_kernel(PruneArgs a, const uint8_t* __restrict__ F8,
+                                                                     const int32_t* __restrict__ nx8) {
+  extern __shared__ __align__(16) char smem_raw[];
+  const int cpad = a.cpad;
+  const int mw = a.m >> 2;       // 32-bit words per row
+  const int rs = mw | 1;         // odd word stride
+  char* p = smem_raw;
+  uint32_t* xr = reinterpret_cast<uint32_t*>(p); p += sizeof(uint32_t) * (size_t)cpad * rs;
+  uint32_t* xs = reinterpret_cast<uint32_t*>(p); p += sizeof(uint32_t) * (size_t)rs;
+  int32_t* ax = reinterpret_cast<int32_t*>(p); p += sizeof(int32_t) * cpad;   // x_p . x_s
+  int32_t* nr = reinterpret_cast<int32_t*>(p); p += sizeof(int32_t) * cpad;   // |x_p|^2
+  int32_t* eid = reinterpret_cast<int32_t*>(p); p += sizeof(int32_t) * cpad;
+  int32_t* eat = reinterpret_cast<int32_t*>(p); p += sizeof(int32_t) * (size_t)cpad * a.l;
+  uint32_t* bits = reinterpret_cast<uint32_t*>(p); p += sizeof(uint32_t) * (size_t)cpad * a.W;
+  const int64_t s = blockIdx.x;
+  const int cnt = a.counts[s];
+  if (cnt <= 1) return;
+  const int tid = threadIdx.x;
+  const uint32_t* F8w = reinterpret_cast<const uint32_t*>(F8);
+  for (int t = tid; t < mw; t += blockDim.x) xs[t] = __ldg(F8w + s * mw + t);
+  for (int t = tid; t < cpad; t += blockDim.x) {
+    const int32_t v = t < cnt ? a.ids[s * a.g + t] : 0;
+    eid[t] = v;
+    nr[t] = t < cnt ? __ldg(nx8 + v) : 0;
+    for (int u = 0; u < a.l; ++u) eat[t * a.l + u] = t < cnt ? __ldg(a.A + (int64_t)v * a.l + u) : 0;
+  }
+  for (int t = tid; t < cpad * a.W; t += blockDim.x) bits[t] = 0u;
+  __syncthreads();
+  for (int e = tid; e < cnt * mw; e += blockDim.x) {
+    const int t = e / mw, w = e - t * mw;
+    xr[t * rs + w] = __ldg(F8w + (int64_t)eid[t] * mw + w);
+  }
+  __syncthreads();
+  for (int t = tid; t < cnt; t += blockDim.x) {
+    uint32_t acc = 0u;  // u8 x u8 products: unsigned dp4a
+    for (int w = 0; w < mw; ++w) acc = __dp4a(xr[t * rs + w], xs[w], acc);
+    ax[t] = (int32_t)acc;
+  }
+  __syncthreads();
+  const int64_t c0 = __ldg(nx8 + s);
+  const int npairs = cnt * (cnt - 1) / 2;
+  for (int pi = tid; pi < npairs; pi += blockDim.x) {
+    // pi -> (t, v), v < t, row-major over the strict lower triangle
+    int t = (int)((1.0 + sqrt(1.0 + 8.0 * pi)) * 0.5);
+    while (t * (t - 1) / 2 > pi) --t;
+    while ((t + 1) * t / 2 <= pi) ++t;
+    const int v = pi - t * (t - 1) / 2;
+    bool eq = true;
+    for (int z = 0; z < a.l; ++z) eq = eq && eat[t * a.l + z] == eat[v * a.l + z];
+    if (!eq) continue;
+    uint32_t g = 0u;
+    const uint32_t* rt = xr + t * rs;
+    const uint32_t* rv = xr + v * rs;
+    for (int w = 0; w < mw; ++w) g = __dp4a(rt[w], rv[w], g);
+    const int64_t dot = (int64_t)g - ax[t] - ax[v] + c0;
+    const int64_t np2 = (int64_t)nr[t] - 2 * (int64_t)ax[t] + c0;
+    const int64_t nk2 = (int64_t)nr[v] - 2 * (int64_t)ax[v] + c0;
+    const double cs = (np2 == 0 || nk2 == 0) ? 1.0
+                    : __ddiv_rn((double)dot, sqrt(dmul((double)np2, (double)nk2)));
+    if (cs > a.sigma) atomicOr(bits + t * a.W + (v >> 5), 1u << (v & 31));
+  }
+  __syncthreads();
+  uint32_t* out = a.rbits + s * (int64_t)a.g * a.W;
+  for (int t = tid; t < cnt * a.W; t += blockDim.x) out[t] = bits[t];
+}
+
+size_t prune_bits_u8_smem(int cpad, int m, int l, int W) {
+  const int rs = (m >> 2) | 1;
+  return sizeof(uint32_t) * ((size_t)cpad + 1) * rs + sizeof(int32_t) * (size_t)cpad * (3 + l) +
+         sizeof(uint32_t) * (size_t)cpad * W + 64;
+}
+
+int launch_prune_bits_u8(const PruneArgs& a, const uint8_t* F8, const int32_t* nx8, size_t smem,
+                         cudaStream_t st) {
+  cudaError_t e = cudaFuncSetAttribute(prune_bits_u8_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)smem);
+  if (e != cudaSuccess) return (int)e;
+  prune_bits_u8_kernel<<<(unsigned)a.n, kPruneThreads, smem, st>>>(a, F8, nx8);
+  return (int)cudaGetLastError();
+}
+
 __global__ void prune_scan_kernel(PruneArgs a) {
   int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (s >= a.n) return;

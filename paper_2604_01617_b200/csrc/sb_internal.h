@@ -223,6 +223,9 @@ struct PruneArgs {
 };
 size_t prune_bits_smem(int cpad, int dc, int m, int l, int W);
 int launch_prune_bits(const PruneArgs& a, size_t smem, cudaStream_t st);
+size_t prune_bits_u8_smem(int cpad, int m, int l, int W);
+int launch_prune_bits_u8(const PruneArgs& a, const uint8_t* F8, const int32_t* nx8, size_t smem,
+                         cudaStream_t st);
 int launch_prune_scan(const PruneArgs& a, cudaStream_t st);
 int launch_prune_guard(const PruneArgs& a, int* changed, cudaStream_t st);
 int launch_prune_compact(const PruneArgs& a, cudaStream_t st);

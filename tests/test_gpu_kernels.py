@@ -163,3 +163,36 @@ def test_device_random_init_equals_numpy(n, g, seed):
     ref_dev.init_graph(host, 1.0)
     for x, y in zip(dev.download(), ref_dev.download()):
         np.testing.assert_array_equal(x, y)
+
+
+@pytest.mark.parametrize("u8", ["1", "0"])
+@pytest.mark.parametrize("n,d,card,gamma,sigma,seed", [
+    (3000, 32, 3, 24, 0.44, 3),     # integer data in [0, 255], clustered: many redundant pairs
+    (2000, 64, 1, 16, 0.6, 9),      # one attribute value: every pair is tested
+])
+def test_prune_integer_rows_u8_path(u8, n, d, card, gamma, sigma, seed, monkeypatch):
+    """Integer features in [0, 255]: semantic_prune's cosines from u8 rows (dp4a, exact integer
+    dot products and norms) equal the reference's fp64 _diff_cosine decisions bit for bit,
+    exact duplicate points (zero-length offsets, cosine 1) included; SB_PRUNE_U8=0 runs the
+    fp64 kernel on the same data."""
+    monkeypatch.setenv("SB_PRUNE_U8", u8)
+    rng = np.random.default_rng(seed)
+    centres = rng.uniform(0, 255, (40, d))
+    f = np.clip(np.rint(centres[rng.integers(0, 40, n)] + rng.normal(0, 12, (n, d))), 0, 255)
+    f = f.astype(np.float32)
+    f[100:110] = f[7]  # exact duplicates
+    a = rng.integers(1, card + 1, (n, 1)).astype(np.int32)
+    alpha = 0.8
+    g = O.run_descent(f, a, alpha, gamma=gamma, gamma_new=gamma, seed=seed)
+    base = (g.nbr_ids.copy(), g.nbr_dists.copy(), g.nbr_counts.copy())
+    O.semantic_prune(g, sigma)
+    from paper_2604_01617_b200.device import DeviceIndex
+    dev = DeviceIndex(f, a, gamma)
+    assert dev.info()["int_exact"]
+    dev.upload(*base)
+    dev.prune(sigma)
+    dev.reinforce(sigma)
+    ids, dists, counts, _ = dev.download(with_flags=False)
+    np.testing.assert_array_equal(counts, g.nbr_counts)
+    np.testing.assert_array_equal(ids, g.nbr_ids)
+    np.testing.assert_array_equal(dists, g.nbr_dists)
