@@ -159,6 +159,7 @@ struct TfArgs {
   int ocap;
   int seed;                // > 0: bound-only pass over `seed` evenly spread tiles per split
   int strided;             // 1: split s walks tiles s, s + splits, ...; 0: contiguous ranges
+  uint32_t wait_ns;        // > 0: barrier waits sleep (suspend-time hint) instead of polling
 };
 
 constexpr int kTfMetaStages = 4;
@@ -214,6 +215,10 @@ __global__ void __launch_bounds__(32 * EW + 64, 1) bf_tf_kernel(TfArgs a) {
   auto bar_accf = [&](int s) { return b0 + 8u * (uint32_t)(24 + s); };
   auto bar_empty = [&](int s) { return b0 + 8u * (uint32_t)(26 + s); };
   const uint32_t bar_aready = b0 + 8u * 28;
+  auto wait = [&](uint32_t bar, uint32_t parity) {
+    if (a.wait_ns) mbar_wait_sleep(bar, parity, a.wait_ns);
+    else mbar_wait(bar, parity);
+  };
 
   // tiles of this CTA: i -> tile0 + i * tstride
   const int64_t tiles = (a.n + N - 1) / N;
@@ -290,7 +295,7 @@ __global__ void __launch_bounds__(32 * EW + 64, 1) bf_tf_kernel(TfArgs a) {
         for (int c = 0; c < nch; ++c, ++it) {
           const int st = it % S;
           const int use = it / S;
-          if (use >= 1) mbar_wait(bar_sfree(st), (uint32_t)((use - 1) & 1));
+          if (use >= 1) wait(bar_sfree(st), (uint32_t)((use - 1) & 1));
           const int cw = dpad - 32 * c < 32 ? dpad - 32 * c : 32;
           const uint32_t blk = (uint32_t)(kTfM * cw * 4);  // one 128-row chunk block
           const uint32_t fb = bar_full(st);
@@ -313,7 +318,7 @@ __global__ void __launch_bounds__(32 * EW + 64, 1) bf_tf_kernel(TfArgs a) {
       for (int i = 0; i < ntl; ++i) {
         const int ms = i % kTfMetaStages;
         const int use = i / kTfMetaStages;
-        if (use >= 1) mbar_wait(bar_emptyM(ms), (uint32_t)((use - 1) & 1));
+        if (use >= 1) wait(bar_emptyM(ms), (uint32_t)((use - 1) & 1));
         const int64_t v0 = ((int64_t)i * tstride + tile0) * (int64_t)N;
         char* meta = sM + ms * meta_bytes;
         const uint32_t fm = bar_fullM(ms);
@@ -333,15 +338,15 @@ __global__ void __launch_bounds__(32 * EW + 64, 1) bf_tf_kernel(TfArgs a) {
       // M >> 4 [24,29), both K-major
       const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(N >> 3) << 17) |
                              ((uint32_t)(kTfM >> 4) << 24);
-      if (ARES) mbar_wait(bar_aready, 0);
+      if (ARES) wait(bar_aready, 0);
       int it = 0;
       for (int i = 0; i < ntl; ++i) {
         const int acc = i & 1;
-        if (i >= 2) mbar_wait(bar_empty(acc), (uint32_t)(((i >> 1) - 1) & 1));
+        if (i >= 2) wait(bar_empty(acc), (uint32_t)(((i >> 1) - 1) & 1));
         tc_fence_after();
         for (int c = 0; c < nch; ++c, ++it) {
           const int st = it % S;
-          mbar_wait(bar_full(st), (uint32_t)((it / S) & 1));
+          wait(bar_full(st), (uint32_t)((it / S) & 1));
           tc_fence_after();
           const int cw = dpad - 32 * c < 32 ? dpad - 32 * c : 32;
           const uint32_t sbo = (uint32_t)(32 * cw);
@@ -419,8 +424,8 @@ __global__ void __launch_bounds__(32 * EW + 64, 1) bf_tf_kernel(TfArgs a) {
       const int64_t vb = ((int64_t)i * tstride + tile0) * (int64_t)N;
       const int nvalid = (int)(a.n - vb < N ? a.n - vb : N);
       const float gpre = qok ? __int_as_float(*reinterpret_cast<volatile int*>(a.gthr + my_q)) : FLT_MAX;
-      mbar_wait(bar_fullM(ms), (uint32_t)((i / kTfMetaStages) & 1));
-      mbar_wait(bar_accf(s), (uint32_t)((i >> 1) & 1));
+      wait(bar_fullM(ms), (uint32_t)((i / kTfMetaStages) & 1));
+      wait(bar_accf(s), (uint32_t)((i >> 1) & 1));
       tc_fence_after();
       // one filter survivor: emission (lower key), this thread's upper-key list
       auto process = [&](int col, float zj, float fsq) {
@@ -734,6 +739,8 @@ int launch_bf_tf(const float* Ft, const float* nxd, const int32_t* code,
   a.stages = sh.stages; a.alpha = alpha; a.gthr = gthr; a.cnt = cnt; a.cand = cand;
   a.cap = cap; a.ocnt = ocnt; a.ocand = ocand; a.ocap = ocap; a.seed = seed;
   a.strided = strided;
+  a.wait_ns = 0;
+  if (const char* e = getenv("SB_TF_WAIT_NS")) a.wait_ns = (uint32_t)atoi(e);
   const size_t smem = tf_smem_bytes(dpad, l, kk, sh.N, sh.stages, sh.ares, sh.qt, sh.ew, sh.kr);
   void (*kern)(TfArgs) = nullptr;
 #define SB_TF_PICK(EW, KR)                                                                          \

@@ -1,0 +1,102 @@
+"""Full-scale runs of BASELINE.json's configs on one B200: HELP build seconds, exact AUTO ground
+truth (tensor cores) and the QPS-vs-recall curve over the K sweep, written as JSON lines.
+
+  python tools/config_report.py cfg3 cfg4 cfg5c1 cfg5c10 cfg5c100 cfg5c1000 cfg5c10000 \
+      [--kcap 4000] [--out profiles/configs_r1.jsonl] [--k100]
+
+QPS is end to end through the public API (search_batch_arrays: host query arrays in, host
+results out), best of two runs per K.  Recall@10 is against oracle_auto_topk's exact top 10;
+with --k100 (cfg 3's "k=100") also Recall@100 against the exact top 100 for K >= 100.
+Data: the seeded generators of tools/configs.py (synthetic stand-ins).
+"""
+import argparse
+import json
+import os
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+K_SWEEP = [10, 20, 25, 30, 50, 100, 200, 300, 500, 750, 1000, 1500, 2000, 3000, 4000]
+
+
+def recall(ids, gt, k):
+    hit = 0
+    for a, b in zip(ids[:, :k], gt[:, :k]):
+        hit += len(np.intersect1d(a, b, assume_unique=False))
+    return hit / (gt.shape[0] * k)
+
+
+def run(name, kcap, k100, out):
+    import paper_2604_01617_b200 as sb
+    from tools.configs import make_config
+    t0 = time.perf_counter()
+    X, A, QX, QA, card = make_config(name)
+    gen_s = time.perf_counter() - t0
+    n, m = X.shape
+    cfg = sb.compute_alpha(sb.sample_statistics(X, A, min(1000, n), seed=0), n, A.shape[1])
+    schema = sb.AttributeSchema(tuple(tuple(str(i) for i in range(c)) for c in card))
+    t0 = time.perf_counter()
+    g = sb.build(X, A, schema, sb.BuildParams(), cfg)
+    build_s = time.perf_counter() - t0
+    log = {k: v for k, v in g.build_log.items() if k != "psi_history"}
+    kk = 100 if k100 else 10
+    sb.oracle_auto_topk_batch(X, A, QX[:256], QA[:256], kk, cfg)  # warm the operand layout
+    t0 = time.perf_counter()
+    gt = sb.oracle_auto_topk_batch(X, A, QX, QA, kk, cfg)
+    gt_s = time.perf_counter() - t0
+    info = g.device().info()
+    bf = None
+    try:
+        from paper_2604_01617_b200.evaluate import _device_for
+        bf = _device_for(g.features, g.attrs).bf_info()
+    except Exception:
+        pass
+    sweep = []
+    kstar = None
+    for k in K_SWEEP:
+        if k > min(kcap, n):
+            break
+        p = sb.SearchParams(k=k)
+        best = 1e30
+        for _ in range(2):
+            t0 = time.perf_counter()
+            ids, _, st = sb.search_batch_arrays(g, QX, QA, p)
+            best = min(best, time.perf_counter() - t0)
+        row = {"k": k, "recall_at_10": round(recall(ids, gt, 10), 5), "qps": round(QX.shape[0] / best, 1),
+               "mean_dist_evals": round(float(st[:, 0].mean()), 1)}
+        if k100 and k >= 100:
+            row["recall_at_100"] = round(recall(ids, gt, 100), 5)
+        sweep.append(row)
+        print(name, row, flush=True)
+        target = row.get("recall_at_100", row["recall_at_10"]) if k100 else row["recall_at_10"]
+        if target >= 0.95 and (not k100 or k >= 100):
+            kstar = k
+            break
+    rec = {"config": name, "N": n, "d": m, "cards": list(card), "queries": int(QX.shape[0]),
+           "gt_k": kk, "data_gen_s": round(gen_s, 1), "build_s": round(build_s, 3), "build_log": log,
+           "edges": int(g.nbr_counts.sum()), "gt_s": round(gt_s, 3), "gt_path": bf,
+           "int_exact": info["int_exact"], "operating_K": kstar,
+           "recall_metric": "recall@100" if k100 else "recall@10", "sweep": sweep,
+           "note": None if kstar else f"recall@{kk} below 0.95 at the K cap {kcap}"}
+    with open(out, "a") as f:
+        f.write(json.dumps(rec, default=str) + "\n")
+    print(json.dumps({k: rec[k] for k in ("config", "build_s", "gt_s", "operating_K")}), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("configs", nargs="+")
+    ap.add_argument("--kcap", type=int, default=4000)
+    ap.add_argument("--k100", action="store_true")
+    ap.add_argument("--out", default=os.path.join(ROOT, "profiles", "configs_r1.jsonl"))
+    a = ap.parse_args()
+    for name in a.configs:
+        run(name, a.kcap, a.k100, a.out)
+
+
+if __name__ == "__main__":
+    main()
