@@ -106,6 +106,7 @@ struct sb_index {
   DBuf rbits, smax, indeg0, guard, drop_other, keep, in_deg, seqtmp;
   bool have_indeg = false;
   int64_t last_overflow_rows = 0;
+  int64_t last_rf_groups = 0, last_rf_components = 0;  // overflow replay parallelism
   // exact reinforce (overflow rows)
   DBuf rf_n8, rf_nb, rf_n32, rf_n64, rf_o32, rf_o64, rf_ulist, rf_bits, rf_rec, rf_sim, rf_eo;
   // routing / brute force
@@ -758,21 +759,103 @@ static int reinforce_overflow(sb_index* idx, double sigma) {
   a.rec_tgt = reinterpret_cast<int32_t*>(a.rec_next + a.rec_cap);
   a.rec_cu = a.rec_tgt + a.rec_cap;
   CK(cudaMemsetAsync(a.rec_head, 0xFF, sizeof(int64_t) * n, idx->st));
-  a.dyn_cap = 1 << 16;
   a.sim_wmax = (int)wmax;
   if (g > 255) return fail(SB_EARG, "reinforce: gamma must be below 256");
   if (sb::rf_simulate_smem(g, (int)wmax) > 227 * 1024)
     return fail(SB_ECUDA, "reinforce: simulation scratch exceeds shared memory");
-  size_t sim_bytes = (sizeof(uint64_t) + sizeof(int32_t)) * a.dyn_cap + 64;
-  CK(idx->rf_sim.ensure(sim_bytes));
-  char* sp = idx->rf_sim.as<char>();
-  a.dyn = reinterpret_cast<uint64_t*>(sp); sp += sizeof(uint64_t) * a.dyn_cap;
-  a.dyn_cu = reinterpret_cast<int32_t*>(sp); sp += sizeof(int32_t) * a.dyn_cap;
-  a.result = reinterpret_cast<int64_t*>(sp);
+  // Independent groups of O rows.  Two O rows interact only (a) when one is in the other's U
+  // (an event between them, or a source row that changes), or (b) through the in-degree of a
+  // node p both can hold, when p's in-degree can reach the safeguard: each O row lowers it at
+  // most twice (p dropped, re-inserted by its own event, dropped again), so p with
+  // in_deg0[p] - 2 * exposure[p] >= 2 passes every `in_deg >= 2` test in any order.  Unsafe
+  // nodes tie every O row whose U holds them (and their own row) into one component.  The
+  // components, packed into at most kMaxGroups groups by work, are simulated in parallel.
+  {
+    std::vector<int32_t> ul((size_t)uoff[no]), onodes(no), indeg(n), oidx(n);
+    CK(cudaMemcpyAsync(ul.data(), a.u_list, sizeof(int32_t) * uoff[no], cudaMemcpyDeviceToHost, idx->st));
+    CK(cudaMemcpyAsync(onodes.data(), a.o_nodes, sizeof(int32_t) * no, cudaMemcpyDeviceToHost, idx->st));
+    CK(cudaMemcpyAsync(indeg.data(), a.in_deg, sizeof(int32_t) * n, cudaMemcpyDeviceToHost, idx->st));
+    CK(cudaMemcpyAsync(oidx.data(), a.o_idx, sizeof(int32_t) * n, cudaMemcpyDeviceToHost, idx->st));
+    CK(cudaStreamSynchronize(idx->st));
+    std::vector<int32_t> expo(n, 0), first(n, -1), par(no);
+    for (int64_t o = 0; o < no; ++o)
+      for (int64_t t = uoff[o]; t < uoff[o + 1]; ++t) ++expo[ul[t]];
+    for (int64_t o = 0; o < no; ++o) par[o] = (int32_t)o;
+    auto find = [&](int32_t x) {
+      while (par[x] != x) { par[x] = par[par[x]]; x = par[x]; }
+      return x;
+    };
+    auto unite = [&](int32_t x, int32_t y) {
+      x = find(x); y = find(y);
+      if (x != y) par[std::max(x, y)] = std::min(x, y);
+    };
+    for (int64_t o = 0; o < no; ++o)
+      for (int64_t t = uoff[o]; t < uoff[o + 1]; ++t) {
+        const int32_t p = ul[t];
+        if (oidx[p] >= 0) unite((int32_t)o, oidx[p]);
+        if ((int64_t)indeg[p] - 2 * (int64_t)expo[p] < 2) {  // unsafe
+          if (first[p] < 0) {
+            first[p] = (int32_t)o;
+            if (oidx[p] >= 0) unite((int32_t)o, oidx[p]);
+          } else {
+            unite((int32_t)o, first[p]);
+          }
+        }
+      }
+    std::vector<int64_t> cwork(no, 0);
+    std::vector<int32_t> croot;
+    for (int64_t o = 0; o < no; ++o) {
+      const int32_t r = find((int32_t)o);
+      if (cwork[r] == 0) croot.push_back(r);
+      cwork[r] += usz[o] + 1;
+    }
+    constexpr int kMaxGroups = 1024;
+    int ng = (int)std::min<size_t>(croot.size(), kMaxGroups);
+    if (const char* e = getenv("SB_RF_GROUPS")) ng = std::max(1, std::min(ng, atoi(e)));
+    // longest-processing-time packing of components into groups
+    std::sort(croot.begin(), croot.end(), [&](int32_t x, int32_t y) { return cwork[x] > cwork[y]; });
+    std::vector<int32_t> cgrp(no, 0);
+    std::vector<std::pair<int64_t, int32_t>> heap;
+    for (int32_t q = 0; q < ng; ++q) heap.push_back({0, q});
+    auto cmp = [](const std::pair<int64_t, int32_t>& x, const std::pair<int64_t, int32_t>& y) {
+      return x.first > y.first;
+    };
+    std::make_heap(heap.begin(), heap.end(), cmp);
+    for (int32_t r : croot) {
+      std::pop_heap(heap.begin(), heap.end(), cmp);
+      cgrp[r] = heap.back().second;
+      heap.back().first += cwork[r];
+      std::push_heap(heap.begin(), heap.end(), cmp);
+    }
+    std::vector<int32_t> gofo(no);
+    for (int64_t o = 0; o < no; ++o) gofo[o] = cgrp[find((int32_t)o)];
+    a.ngroups = ng;
+    a.bm_words = (n + 31) / 32;
+    idx->last_rf_groups = ng;
+    idx->last_rf_components = (int64_t)croot.size();
+    // a group's dynamic events at one source are mirrors recorded into that (non-O) row, at
+    // most |rev_j| <= gamma of them
+    a.dyn_cap = g + 1;
+    const size_t gb = sizeof(uint32_t) * (size_t)ng * a.bm_words;
+    const size_t sim_bytes = (sizeof(uint64_t) + sizeof(int32_t)) * (size_t)ng * a.dyn_cap +
+                             sizeof(int32_t) * (size_t)no + gb + 128;
+    CK(idx->rf_sim.ensure(sim_bytes));
+    char* sp = idx->rf_sim.as<char>();
+    a.result = reinterpret_cast<int64_t*>(sp); sp += 4 * sizeof(int64_t);
+    a.rec_count = a.result + 2;
+    a.dyn = reinterpret_cast<uint64_t*>(sp); sp += sizeof(uint64_t) * (size_t)ng * a.dyn_cap;
+    a.grp_bits = reinterpret_cast<uint32_t*>(sp); sp += gb;
+    a.dyn_cu = reinterpret_cast<int32_t*>(sp); sp += sizeof(int32_t) * (size_t)ng * a.dyn_cap;
+    a.grp_of_o = reinterpret_cast<int32_t*>(sp);
+    CK(cudaMemsetAsync(a.result, 0, 4 * sizeof(int64_t), idx->st));
+    CK(cudaMemcpyAsync(a.grp_of_o, gofo.data(), sizeof(int32_t) * no, cudaMemcpyHostToDevice, idx->st));
+    CKL(sb::rf_launch_group_bits(a, idx->st));
+  }
   CKL(sb::rf_launch_simulate(a, idx->st));
-  int64_t res[2] = {0, 0};
+  int64_t res[3] = {0, 0, 0};
   CK(cudaMemcpyAsync(res, a.result, sizeof(res), cudaMemcpyDeviceToHost, idx->st));
   CK(cudaStreamSynchronize(idx->st));
+  res[0] = std::min(res[2], a.rec_cap);  // records allocated
   if (res[1]) return fail(SB_ECUDA, "reinforce simulation invariant violated (code " + std::to_string(res[1]) + ")");
   // parallel part: insertions into rows that cannot overflow
   CK(idx->seg.ensure(sizeof(uint64_t) * n * g));

@@ -293,7 +293,7 @@ SB_DEV int warp_u_index(const int32_t* U, int u, int32_t node) {
 }
 
 SB_DEV int32_t indeg_read(const RfArgs& a, int32_t p, int64_t s) {
-  int32_t v = a.in_deg[p];
+  int32_t v = __ldcg(a.in_deg + p);  // other groups update in-degrees with L2 atomics
   if (p < s && !a.is_o[p]) v += a.static_ins[p];
   return v;
 }
@@ -309,8 +309,9 @@ struct SimSmem {
   uint32_t* Rs;
 };
 
-size_t rf_simulate_smem(int g, int wmax) {
-  return (size_t)(g + 1) * (4 * 4 + 1) + 16 + sizeof(uint32_t) * (size_t)(g + 1) * wmax + 64;
+__host__ __device__ size_t rf_simulate_smem(int g, int wmax) {
+  const size_t b = (size_t)(g + 1) * (4 * 4 + 1) + 16 + sizeof(uint32_t) * (size_t)(g + 1) * wmax + 64;
+  return (b + 15) & ~(size_t)15;  // per-warp slices stay 16-byte aligned
 }
 
 // exact _try_insert_edge on O row j (_kernels.py:306-395); returns 1 if inserted
@@ -376,7 +377,7 @@ SB_DEV int warp_try_insert(RfArgs& a, const SimSmem& S, int32_t j, int o, int32_
     if (lane == 0) {
       ri[pos] = cand; rd[pos] = d; ru[pos] = cu;
       a.counts[j] = cj + 1;
-      a.in_deg[cand] += 1;
+      atomicAdd(a.in_deg + cand, 1);
       if (kRfProf) { atomicAdd(&g_rf_prof[0], (unsigned long long)(clock64() - t_start)); atomicAdd(&g_rf_prof[1], 1ull); }
     }
     __syncwarp();
@@ -449,7 +450,7 @@ SB_DEV int warp_try_insert(RfArgs& a, const SimSmem& S, int32_t j, int o, int32_
   __syncwarp();
   // every dropped entry other than the candidate loses one in-degree
   for (int t = lane; t < total; t += 32)
-    if (!S.mkeep[t] && S.mi[t] != cand) a.in_deg[S.mi[t]] -= 1;
+    if (!S.mkeep[t] && S.mi[t] != cand) atomicSub(a.in_deg + S.mi[t], 1);
   int w0 = 0, inserted = 0;
   for (int t0 = 0; t0 < total; t0 += 32) {
     const int t = t0 + lane;
@@ -465,7 +466,7 @@ SB_DEV int warp_try_insert(RfArgs& a, const SimSmem& S, int32_t j, int o, int32_
   inserted = __any_sync(kFull, inserted) ? 1 : 0;
   if (lane == 0) {
     a.counts[j] = w0;
-    if (inserted) a.in_deg[cand] += 1;
+    if (inserted) atomicAdd(a.in_deg + cand, 1);
     if (kRfProf) { atomicAdd(&g_rf_prof[2], (unsigned long long)(clock64() - t_start)); atomicAdd(&g_rf_prof[3], 1ull); }
   }
   __syncwarp();
@@ -482,14 +483,19 @@ __global__ void rf_init_upos_kernel(RfArgs a) {
   a.u_pos[e] = u_index(a, (int)o, a.ids[(int64_t)j * a.g + t]);
 }
 
+// One warp per group of O-row components (components do not interact: see rf_groups in
+// capi.cu), each walking the sources its group's rows see, in ascending order, through the
+// group's source bitmap.
 __global__ void rf_simulate_kernel(RfArgs a) {
   extern __shared__ __align__(16) char smem_raw[];
-  if (blockIdx.x != 0) return;
   const int lane = lane_id();
   const int g = a.g;
+  const int grp = blockIdx.x * (blockDim.x >> 5) + warp_id();
+  if (grp >= a.ngroups) return;
+  uint32_t* bm = a.grp_bits + (size_t)grp * a.bm_words;
   SimSmem S;
   {
-    char* p = smem_raw;
+    char* p = smem_raw + (size_t)warp_id() * rf_simulate_smem(g, a.sim_wmax);
     S.Rs = reinterpret_cast<uint32_t*>(p); p += sizeof(uint32_t) * (size_t)(g + 1) * a.sim_wmax;
     S.mi = reinterpret_cast<int32_t*>(p); p += sizeof(int32_t) * (g + 1);
     S.mu = reinterpret_cast<int32_t*>(p); p += sizeof(int32_t) * (g + 1);
@@ -497,14 +503,15 @@ __global__ void rf_simulate_kernel(RfArgs a) {
     S.md = reinterpret_cast<float*>(p); p += sizeof(float) * (g + 1);
     S.mkeep = reinterpret_cast<uint8_t*>(p);
   }
+  uint64_t* dyn = a.dyn + (size_t)grp * a.dyn_cap;
+  int32_t* dyn_cu = a.dyn_cu + (size_t)grp * a.dyn_cap;
+  auto in_grp = [&](int o) { return a.grp_of_o[o] == grp; };
   int err = 0;
-  int64_t nrec = 0;
   const long long t_kernel = clock64();
-  const volatile uint8_t* relevant = a.relevant;
   auto dyn_insert = [&](int q, int64_t s) {
-    const uint64_t kd = a.dyn[q];
+    const uint64_t kd = dyn[q];
     const int32_t jd = (int32_t)key_id(kd);
-    warp_try_insert(a, S, jd, a.o_idx[jd], (int32_t)s, key_dist(kd), s, err, a.dyn_cu[q]);
+    warp_try_insert(a, S, jd, a.o_idx[jd], (int32_t)s, key_dist(kd), s, err, dyn_cu[q]);
   };
   // Per source: count, O index, the row (gamma wide, masked by the count), the head of its
   // recorded mirrors and the targets' O indices.  Rows outside O never change during the
@@ -524,7 +531,7 @@ __global__ void rf_simulate_kernel(RfArgs a) {
     D.s = s;
     D.cs = a.counts[s];
     D.osrc = a.o_idx[s];
-    D.rh = a.rec_head[s];
+    D.rh = *reinterpret_cast<const volatile int64_t*>(a.rec_head + s);
 #pragma unroll
     for (int k = 0; k < 8; ++k) {
       const int t = lane + 32 * k;
@@ -539,9 +546,10 @@ __global__ void rf_simulate_kernel(RfArgs a) {
       }
     }
   };
-  for (int64_t base = 0; base < a.n; base += 32) {
-    const int64_t idx = base + lane;
-    unsigned bal = __ballot_sync(kFull, idx < a.n && relevant[idx]);
+  const volatile uint32_t* vbm = bm;
+  for (int64_t wi = 0; wi < a.bm_words; ++wi) {
+    const int64_t base = wi * 32;
+    unsigned bal = vbm[wi];
     Src nxt;
     nxt.s = -1;
     while (bal) {
@@ -583,24 +591,35 @@ __global__ void rf_simulate_kernel(RfArgs a) {
                            row_find_key(a.ids + (int64_t)vi[k] * g, a.dists + (int64_t)vi[k] * g,
                                         a.counts[vi[k]], row_key(vd[k], (uint32_t)s)) < 0;
           const unsigned rb = __ballot_sync(kFull, rec);
+          int64_t rbase = 0;
+          if (lane == 0 && rb) rbase = (int64_t)atomicAdd(reinterpret_cast<unsigned long long*>(a.rec_count),
+                                                          (unsigned long long)__popc(rb));
+          rbase = __shfl_sync(kFull, rbase, 0);
           if (rec) {
-            const int64_t r = nrec + __popc(rb & ((1u << lane) - 1u));
+            const int64_t r = rbase + __popc(rb & ((1u << lane) - 1u));
             if (r < a.rec_cap) {
               const int32_t j = vi[k];
               a.rec_tgt[r] = j;
               a.rec_key[r] = row_key(vd[k], (uint32_t)s);
               a.rec_cu[r] = cuh[k];  // j's position in U_s: the hint of the later event
-              a.rec_next[r] = a.rec_head[j];
-              a.rec_head[j] = r;
-              if (j > s) a.relevant[j] = 1;
+              // lock-free push: other groups read j's list concurrently (and skip this record)
+              unsigned long long* head = reinterpret_cast<unsigned long long*>(a.rec_head + j);
+              unsigned long long old = *reinterpret_cast<volatile unsigned long long*>(head);
+              for (;;) {
+                a.rec_next[r] = (int64_t)old;
+                __threadfence();
+                const unsigned long long prev = atomicCAS(head, old, (unsigned long long)r);
+                if (prev == old) break;
+                old = prev;
+              }
+              if (j > s) atomicOr(bm + (j >> 5), 1u << (j & 31));
             } else {
               err = 2;
             }
           }
-          const int64_t room = a.rec_cap - nrec;
+          const int64_t room = a.rec_cap - rbase;
           const int64_t ok = (int64_t)__popc(rb) < room ? (int64_t)__popc(rb) : (room > 0 ? room : 0);
-          nrec += ok;
-          if (lane == 0) a.in_deg[s] += (int32_t)ok;
+          if (lane == 0 && ok) atomicAdd(a.in_deg + s, (int32_t)ok);
         }
         __syncwarp();
 #pragma unroll
@@ -614,26 +633,30 @@ __global__ void rf_simulate_kernel(RfArgs a) {
                             (int32_t)s, __shfl_sync(kFull, vd[k], src), s, err);
           }
         }
-        // recorded mirrors may have made later sources of this chunk relevant
-        bal = __ballot_sync(kFull, idx > s && idx < a.n && relevant[idx]);
+        // recorded mirrors may have made later sources of this word relevant
+        __syncwarp();
+        bal = vbm[wi] & (s - base == 31 ? 0u : (0xFFFFFFFFu << (s - base + 1)));
         nxt.s = -1;
       } else {
         // O-target events of a non-O row in key order: static entries j in O, plus entries
         // mirrored in by O sources processed earlier (linked list, sorted here)
         int nd = 0;
         if (lane == 0) {
-          for (int64_t r = rh; r >= 0; r = a.rec_next[r]) {
+          const volatile int64_t* vnext = a.rec_next;
+          for (int64_t r = rh; r >= 0; r = vnext[r]) {
+            const uint64_t rk = a.rec_key[r];
+            if (!in_grp(a.o_idx[key_id(rk)])) continue;  // another group's mirror
             if (nd < a.dyn_cap) {
-              uint64_t kk = row_key(key_dist(a.rec_key[r]), key_id(a.rec_key[r]));
+              uint64_t kk = row_key(key_dist(rk), key_id(rk));
               const int cr = a.rec_cu[r];
               int pos = nd;
-              while (pos > 0 && a.dyn[pos - 1] > kk) {
-                a.dyn[pos] = a.dyn[pos - 1];
-                a.dyn_cu[pos] = a.dyn_cu[pos - 1];
+              while (pos > 0 && dyn[pos - 1] > kk) {
+                dyn[pos] = dyn[pos - 1];
+                dyn_cu[pos] = dyn_cu[pos - 1];
                 --pos;
               }
-              a.dyn[pos] = kk;
-              a.dyn_cu[pos] = cr;
+              dyn[pos] = kk;
+              dyn_cu[pos] = cr;
               ++nd;
             } else {
               err = 3;
@@ -646,7 +669,7 @@ __global__ void rf_simulate_kernel(RfArgs a) {
 #pragma unroll
         for (int k = 0; k < 8; ++k) {
           if (32 * k >= cs) break;
-          unsigned ob = __ballot_sync(kFull, oj[k] >= 0);
+          unsigned ob = __ballot_sync(kFull, oj[k] >= 0 && in_grp(oj[k]));
           while (ob) {
             const int src = __ffs(ob) - 1;
             ob &= ob - 1u;
@@ -655,7 +678,7 @@ __global__ void rf_simulate_kernel(RfArgs a) {
             const int oo = __shfl_sync(kFull, oj[k], src);
             const int ch = __shfl_sync(kFull, cuh[k], src);
             const uint64_t ks = row_key(dd, (uint32_t)jj);
-            while (q < nd && a.dyn[q] < ks) dyn_insert(q++, s);
+            while (q < nd && dyn[q] < ks) dyn_insert(q++, s);
             warp_try_insert(a, S, jj, oo, (int32_t)s, dd, s, err, ch);
           }
         }
@@ -665,8 +688,7 @@ __global__ void rf_simulate_kernel(RfArgs a) {
   }
   err = __reduce_max_sync(kFull, err);
   if (lane == 0) {
-    a.result[0] = nrec;
-    a.result[1] = err;
+    if (err) atomicMax(reinterpret_cast<unsigned long long*>(a.result + 1), (unsigned long long)err);
     if (kRfProf) g_rf_prof[6] = clock64() - t_kernel;
   }
 }
@@ -696,6 +718,28 @@ __global__ void rf_apply_count_rec_kernel(RfArgs a, int64_t nrec) {
   int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (r >= nrec) return;
   atomicAdd(reinterpret_cast<unsigned long long*>(a.apply_cnt + a.rec_tgt[r]), 1ull);
+}
+
+// per-group source bitmaps: a non-O source is relevant to the groups of its O-target rows, an O
+// source to its own row's group (rf_simulate_kernel walks these)
+__global__ void rf_group_bits_kernel(RfArgs a) {
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= a.n * a.g) return;
+  const int64_t s = e / a.g;
+  const int t = (int)(e - s * a.g);
+  const int os = a.o_idx[s];
+  if (os >= 0) {
+    if (t == 0) atomicOr(a.grp_bits + (size_t)a.grp_of_o[os] * a.bm_words + (s >> 5), 1u << (s & 31));
+    return;
+  }
+  const int o = a.eo[e];  // -1 target outside O, -2 past the count
+  if (o >= 0) atomicOr(a.grp_bits + (size_t)a.grp_of_o[o] * a.bm_words + (s >> 5), 1u << (s & 31));
+}
+
+int rf_launch_group_bits(RfArgs& a, cudaStream_t st) {
+  cudaMemsetAsync(a.grp_bits, 0, sizeof(uint32_t) * (size_t)a.ngroups * a.bm_words, st);
+  rf_group_bits_kernel<<<(unsigned)((a.n * a.g + 255) / 256), 256, 0, st>>>(a);
+  return (int)cudaGetLastError();
 }
 
 // ---------------------------------------------------------------------------------------
@@ -742,14 +786,17 @@ int rf_launch_stage3(RfArgs& a, int upad_max, int dc_max, int upad4_max, size_t 
 
 int rf_launch_simulate(RfArgs& a, cudaStream_t st) {
   const size_t smem = rf_simulate_smem(a.g, a.sim_wmax);
-  cudaError_t e = cudaFuncSetAttribute(rf_simulate_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  const int kSimWarps = smem * 4 <= 200 * 1024 ? 4 : 1;
+  cudaError_t e = cudaFuncSetAttribute(rf_simulate_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)(smem * kSimWarps));
   if (e != cudaSuccess) return (int)e;
   static const bool prof = kRfProf && getenv("SB_RF_PROF") != nullptr;
   if (prof) {
     unsigned long long z[8] = {0};
     cudaMemcpyToSymbol(g_rf_prof, z, sizeof(z));
   }
-  rf_simulate_kernel<<<1, 32, smem, st>>>(a);
+  rf_simulate_kernel<<<(unsigned)((a.ngroups + kSimWarps - 1) / kSimWarps), 32 * kSimWarps,
+                       smem * kSimWarps, st>>>(a);
   if (prof) {
     unsigned long long z[8];
     cudaDeviceSynchronize();

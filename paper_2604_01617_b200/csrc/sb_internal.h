@@ -288,13 +288,20 @@ struct RfArgs {
   int dyn_cap;
   int sim_wmax;         // max redundancy-row words over O rows (simulation scratch size)
   int64_t* result;      // [nrec, err]
+  int64_t* rec_count;   // records allocated (all groups)
+  // groups of O-row components simulated in parallel (one warp each)
+  int ngroups;
+  int32_t* grp_of_o;    // no
+  uint32_t* grp_bits;   // ngroups x bm_words source bitmaps
+  int64_t bm_words;
 };
-size_t rf_simulate_smem(int g, int wmax);
+__host__ __device__ size_t rf_simulate_smem(int g, int wmax);
 int rf_launch_stage1(RfArgs& a, int64_t* oflag, int64_t* oscan, int64_t* scan_tmp, cudaStream_t st);
 int rf_launch_stage2(RfArgs& a, const int64_t* oscan, cudaStream_t st);
 int rf_launch_stage3(RfArgs& a, int upad_max, int dc_max, int upad4_max, size_t bits_smem,
                      cudaStream_t st);
 int rf_launch_simulate(RfArgs& a, cudaStream_t st);
+int rf_launch_group_bits(RfArgs& a, cudaStream_t st);
 int rf_launch_apply(RfArgs& a, int64_t nrec, int64_t* scan_tmp, cudaStream_t st);
 
 }  // namespace sb
