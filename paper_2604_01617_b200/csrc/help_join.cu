@@ -35,6 +35,7 @@ struct JoinCta {
   float* xs;          // [dc][spad] (u8 path: uint32 words [m / 4][spad])
   int* tiles;         // tile list
   int32_t* nrm;       // [spad] |x|^2 (u8 path)
+  uint64_t* thr;      // [spad] the slots' row tails (push filter)
 };
 
 // warp-aggregated append of up to two pushes per lane into the global push buffer
@@ -95,6 +96,7 @@ __global__ void __launch_bounds__(kJoinThreads, 2) join_emit_kernel(JoinArgs a) 
   JoinCta s;
   {
     char* p = smem_raw;
+    s.thr = reinterpret_cast<uint64_t*>(p); p += sizeof(uint64_t) * (size_t)spad;
     s.xs = reinterpret_cast<float*>(p); p += sizeof(float) * (size_t)a.dc * spad;
     s.slot_id = reinterpret_cast<int32_t*>(p); p += sizeof(int32_t) * spad;
     s.slot_attr = reinterpret_cast<int32_t*>(p); p += sizeof(int32_t) * (size_t)spad * a.l;
@@ -128,6 +130,7 @@ __global__ void __launch_bounds__(kJoinThreads, 2) join_emit_kernel(JoinArgs a) 
     for (int t = tid; t < ns; t += blockDim.x) {
       int32_t v = t < na ? a.new_cand[(int64_t)node * a.gn + t] : a.old_cand[(int64_t)node * a.g + (t - na)];
       s.slot_id[t] = v;
+      s.thr[t] = a.thr[v];
       for (int u = 0; u < a.l; ++u) s.slot_attr[t * a.l + u] = __ldg(a.A + (int64_t)v * a.l + u);
     }
     for (int t = ns + tid; t < spad; t += blockDim.x) s.slot_id[t] = -1;
@@ -240,8 +243,8 @@ __global__ void __launch_bounds__(kJoinThreads, 2) join_emit_kernel(JoinArgs a) 
             float d = __double2float_rn(auto_finish(acc[u][w], sa, a.inv_alpha));
             k1 = row_key(d, (uint32_t)k);  // into row j
             k2 = row_key(d, (uint32_t)j);  // into row k
-            p1 = k1 < a.thr[j];
-            p2 = k2 < a.thr[k];
+            p1 = k1 < s.thr[x];
+            p2 = k2 < s.thr[y];
           }
           emit2(a, em, p1, (uint32_t)j, k1, p2, (uint32_t)k, k2);
         }
@@ -383,7 +386,7 @@ __global__ void thr_init_kernel(const int32_t* ids, const float* dists, int64_t 
 }
 
 size_t join_emit_smem(int spad, int dc, int l, int ntiles_max) {
-  return sizeof(float) * (size_t)dc * spad + sizeof(int32_t) * spad +
+  return sizeof(uint64_t) * (size_t)spad + sizeof(float) * (size_t)dc * spad + sizeof(int32_t) * spad +
          sizeof(int32_t) * (size_t)spad * l + sizeof(int) * (size_t)ntiles_max +
          sizeof(int32_t) * spad + 64;
 }
