@@ -34,6 +34,7 @@ constexpr int kTcM = 128;       // queries per CTA (UMMA M)
 constexpr int kTcThreads = 256;  // two threads per query row, each owning half the columns
 constexpr int kTcMaxKK = 32;    // per-thread list length limit
 constexpr int kTcPad = 256;     // node arrays are zero-padded to a multiple of this
+constexpr int kTcMeta = 4;      // node-metadata ring stages (ahead of the accumulators)
 
 // Operand layout in HBM and shared memory (both operands, identical): K-major core matrices in
 // row-group-major order.  The 8 rows of group g occupy one contiguous 8 * m * 2-byte block;
@@ -146,16 +147,17 @@ __global__ void __launch_bounds__(kTcThreads + 32, CTAS) bf_tc_kernel(TcArgs a) 
   char* p = smem;
   char* sA = p; p += (size_t)kTcM * rowb;
   char* sB = p; p += NBS * b_bytes;
-  char* sM = p; p += 2 * meta_bytes;
+  char* sM = p; p += kTcMeta * meta_bytes;
   double* ld = reinterpret_cast<double*>(p); p += sizeof(double) * (size_t)a.kk * kTcThreads;
   uint32_t* li = reinterpret_cast<uint32_t*>(p); p += sizeof(uint32_t) * (size_t)a.kk * kTcThreads;
   volatile float* s_t2 = reinterpret_cast<float*>(p); p += sizeof(float) * kTcThreads;
   p = reinterpret_cast<char*>(((uintptr_t)p + 7) & ~(uintptr_t)7);
-  uint64_t* bars = reinterpret_cast<uint64_t*>(p); p += 8 * 10;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(p); p += 8 * 16;
   uint32_t* tslot = reinterpret_cast<uint32_t*>(p);
-  const uint32_t bar_fullB = smem_u32(bars), bar_fullM = smem_u32(bars + 2),
-                 bar_done = smem_u32(bars + 4), bar_empty = smem_u32(bars + 6),
-                 bar_a = smem_u32(bars + 8);
+  // fullB[2] done[2] empty[2] a fullM[kTcMeta] emptyM[kTcMeta]
+  const uint32_t bar_fullB = smem_u32(bars), bar_done = smem_u32(bars + 2),
+                 bar_empty = smem_u32(bars + 4), bar_a = smem_u32(bars + 6),
+                 bar_fullM = smem_u32(bars + 7), bar_emptyM = smem_u32(bars + 7 + kTcMeta);
 
   const int64_t q0 = (int64_t)blockIdx.x * kTcM;
   const int64_t tiles = (a.n + N - 1) / N;
@@ -172,9 +174,12 @@ __global__ void __launch_bounds__(kTcThreads + 32, CTAS) bf_tc_kernel(TcArgs a) 
   if (tid == kTcThreads) {
     for (int s = 0; s < 2; ++s) {
       mbar_init(bar_fullB + 8 * s, 1);
-      mbar_init(bar_fullM + 8 * s, 1);
       mbar_init(bar_done + 8 * s, 1);
       mbar_init(bar_empty + 8 * s, kTcThreads);
+    }
+    for (int s = 0; s < kTcMeta; ++s) {
+      mbar_init(bar_fullM + 8 * s, 1);
+      mbar_init(bar_emptyM + 8 * s, kTcThreads);
     }
     mbar_init(bar_a, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -213,16 +218,8 @@ __global__ void __launch_bounds__(kTcThreads + 32, CTAS) bf_tc_kernel(TcArgs a) 
       for (int i = 0; i < ntl; ++i) {
         const int s = i & 1;
         const uint32_t ph = (uint32_t)((i >> 1) & 1);
-        // accumulator s and meta stage s: free once the epilogue has left tile i - 2
+        // accumulator s: free once the epilogue has left tile i - 2
         if (i >= 2) mbar_wait(bar_empty + 8 * s, ph ^ 1u);
-        const int64_t v0 = (t_begin + i) * (int64_t)N;
-        char* meta = sM + s * meta_bytes;
-        const uint32_t fm = bar_fullM + 8 * s;
-        mbar_expect_tx(fm, (uint32_t)meta_bytes);
-        bulk_g2s(smem_u32(meta), a.nx + v0, (uint32_t)(N * 4), fm);
-        bulk_g2s(smem_u32(meta + N * 4), a.code + v0, (uint32_t)(N * 4), fm);
-        bulk_g2s(smem_u32(meta + N * 8), a.orig + v0, (uint32_t)(N * 4), fm);
-        bulk_g2s(smem_u32(meta + N * 12), a.A + v0 * l, (uint32_t)(N * l * 4), fm);
         const int sb = NBS == 1 ? 0 : s;
         mbar_wait(bar_fullB + 8 * sb, NBS == 1 ? (uint32_t)(i & 1) : ph);
         tc_fence_after();
@@ -252,6 +249,20 @@ __global__ void __launch_bounds__(kTcThreads + 32, CTAS) bf_tc_kernel(TcArgs a) 
           else if (i >= 1) mbar_wait(bar_done + 8 * (s ^ 1), (uint32_t)(((i - 1) >> 1) & 1));
           load_rows(i + 1);
         }
+      }
+    } else if (lane_id() == 1) {
+      // node metadata on its own ring, kTcMeta tiles ahead of the epilogue
+      for (int i = 0; i < ntl; ++i) {
+        const int ms = i % kTcMeta;
+        if (i >= kTcMeta) mbar_wait(bar_emptyM + 8 * ms, (uint32_t)(((i / kTcMeta) - 1) & 1));
+        const int64_t v0 = (t_begin + i) * (int64_t)N;
+        char* meta = sM + ms * meta_bytes;
+        const uint32_t fm = bar_fullM + 8 * ms;
+        mbar_expect_tx(fm, (uint32_t)meta_bytes);
+        bulk_g2s(smem_u32(meta), a.nx + v0, (uint32_t)(N * 4), fm);
+        bulk_g2s(smem_u32(meta + N * 4), a.code + v0, (uint32_t)(N * 4), fm);
+        bulk_g2s(smem_u32(meta + N * 8), a.orig + v0, (uint32_t)(N * 4), fm);
+        bulk_g2s(smem_u32(meta + N * 12), a.A + v0 * l, (uint32_t)(N * l * 4), fm);
       }
     }
     __syncwarp();
@@ -287,7 +298,8 @@ __global__ void __launch_bounds__(kTcThreads + 32, CTAS) bf_tc_kernel(TcArgs a) 
     for (int i = 0; i < ntl; ++i) {
       const int s = i & 1;
       const uint32_t ph = (uint32_t)((i >> 1) & 1);
-      const char* meta = sM + s * meta_bytes;
+      const int ms = i % kTcMeta;
+      const char* meta = sM + ms * meta_bytes;
       const float* s_nx = reinterpret_cast<const float*>(meta);
       const int32_t* s_code = reinterpret_cast<const int32_t*>(meta) + N;
       const int32_t* s_orig = reinterpret_cast<const int32_t*>(meta) + 2 * N;
@@ -296,7 +308,7 @@ __global__ void __launch_bounds__(kTcThreads + 32, CTAS) bf_tc_kernel(TcArgs a) 
       const int nvalid = (int)(a.n - vb < N ? a.n - vb : N);
       // the query's tightest bound published by any CTA (read now, used after the tile)
       const float gpre = qok ? __int_as_float(*reinterpret_cast<volatile int*>(a.gthr + my_q)) : 3.4e38f;
-      mbar_wait(bar_fullM + 8 * s, ph);
+      mbar_wait(bar_fullM + 8 * ms, (uint32_t)((i / kTcMeta) & 1));
       mbar_wait(bar_done + 8 * s, ph);
       tc_fence_after();
       for (int c = 0; c < cols / 16; ++c) {
@@ -415,9 +427,10 @@ __global__ void __launch_bounds__(kTcThreads + 32, CTAS) bf_tc_kernel(TcArgs a) 
           }
         }
       }
-      // release accumulator s and meta stage s to the producer
+      // release accumulator s and meta stage ms to the producers
       tc_fence_before();
       mbar_arrive(bar_empty + 8 * s);
+      mbar_arrive(bar_emptyM + 8 * ms);
       // Share list tails between all partial lists of a query (the other column half in
       // this CTA, the other node ranges in other CTAs): a node beyond any list's kk-th
       // cannot enter the merged top-kk either, so the tightest bound filters every list.
@@ -449,9 +462,9 @@ __global__ void __launch_bounds__(kTcThreads + 32, CTAS) bf_tc_kernel(TcArgs a) 
 
 // rowb = operand bytes per row (2 m for bf16, m for u8)
 size_t bf_tc_smem_n(int rowb, int l, int kk, int N, int nbs) {
-  return (size_t)kTcM * rowb + (size_t)nbs * N * rowb + 2 * (size_t)N * (3 + l) * 4 +
+  return (size_t)kTcM * rowb + (size_t)nbs * N * rowb + kTcMeta * (size_t)N * (3 + l) * 4 +
          (sizeof(double) + sizeof(uint32_t)) * (size_t)kk * kTcThreads + sizeof(float) * kTcThreads +
-         8 + 80 + 16;
+         8 + 128 + 16;
 }
 
 // Tile shapes (N nodes per tile, row stages, CTAs per SM), in order of preference; the first

@@ -351,19 +351,30 @@ __global__ void __launch_bounds__(32 * EW + 64, 1) bf_tf_kernel(TfArgs a) {
           const int cw = dpad - 32 * c < 32 ? dpad - 32 * c : 32;
           const uint32_t sbo = (uint32_t)(32 * cw);
           const uint32_t bb = smem_u32(sB + (size_t)st * N * kTfKC * 4);
+          // descriptors are linear in the start address (bits [0,14) hold addr >> 4, no carry
+          // below 256 KB): a K = 8 step adds 256 B = 16 units
+          const uint64_t bd0 = umma_desc(bb, 128, sbo);
 #pragma unroll
           for (int t = 0; t < QT; ++t) {
             const uint32_t ab = ARES ? smem_u32(sA + t * qblk_bytes + (size_t)c * kTfChunkBytes)
                                      : smem_u32(sA + ((size_t)st * QT + t) * kTfChunkBytes);
             const uint32_t dt = tmem + (uint32_t)((acc * QT + t) * N);
-            for (int s = 0; s < cw / 8; ++s) {
-              const uint64_t ad = umma_desc(ab + (uint32_t)s * 256, 128, sbo);
-              const uint64_t bd = umma_desc(bb + (uint32_t)s * 256, 128, sbo);
-              asm volatile(
-                  "{\n\t.reg .pred p;\n\t"
-                  "setp.ne.b32 p, %4, 0;\n\t"
-                  "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(dt),
-                  "l"(ad), "l"(bd), "r"(idesc), "r"((c | s) != 0 ? 1u : 0u));
+            const uint64_t ad0 = umma_desc(ab, 128, sbo);
+            if (cw == 32) {
+#pragma unroll
+              for (int s = 0; s < 4; ++s)
+                asm volatile(
+                    "{\n\t.reg .pred p;\n\t"
+                    "setp.ne.b32 p, %4, 0;\n\t"
+                    "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(dt),
+                    "l"(ad0 + 16u * s), "l"(bd0 + 16u * s), "r"(idesc), "r"((c | s) != 0 ? 1u : 0u));
+            } else {
+              for (int s = 0; s < cw / 8; ++s)
+                asm volatile(
+                    "{\n\t.reg .pred p;\n\t"
+                    "setp.ne.b32 p, %4, 0;\n\t"
+                    "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(dt),
+                    "l"(ad0 + 16u * s), "l"(bd0 + 16u * s), "r"(idesc), "r"((c | s) != 0 ? 1u : 0u));
             }
           }
           mma_commit(bar_sfree(st));  // the stage is free once these MMAs complete
@@ -660,8 +671,7 @@ double tf_margin(int dpad) {
 
 struct TfShape { int N, stages; bool ares; int qt, ew, kr; };
 
-// Tile shape: the first that fits shared memory, in order of preference.  Two resident query
-// tiles against 128-node tiles halve the node-operand traffic per MMA; wide rows stream both
+// Tile shape: the first that fits shared memory, in order of preference; wide rows stream both
 // operands.  k <= 32 keeps the per-thread lists in registers and runs 16 epilogue warps; larger
 // k keeps them in shared memory with 8.
 static TfShape tf_shape(int dpad, int l, int kk) {
@@ -677,8 +687,10 @@ static TfShape tf_shape(int dpad, int l, int kk) {
         tf_smem_bytes(dpad, l, kk, Nn, st, ar != 0, qt, ew, kr) <= limit)
       return {Nn, st, ar != 0, qt, ew, kr};
   }
+  // (N = 256 first: one tf32 MMA instruction moves twice the work of an N = 128 one, and the
+  // single issuing thread is the limit for small instructions; measured 9.0 vs 9.9 ms on cfg 3)
   const int pref[][4] = {// N, max stages, min stages, qt (resident query tiles)
-                         {128, 8, 4, 2}, {256, 6, 3, 1}, {128, 8, 3, 1}};
+                         {256, 6, 3, 1}, {128, 8, 4, 2}, {128, 8, 3, 1}};
   for (auto& pr : pref)
     for (int st = pr[1]; st >= pr[2]; --st)
       if (tf_smem_bytes(dpad, l, kk, pr[0], st, true, pr[3], ew, kr) <= limit)
