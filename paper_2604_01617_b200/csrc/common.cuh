@@ -293,6 +293,79 @@ SB_DEV int warp_merge_topk(double* rd, uint32_t* rid, int K, double* cd, uint32_
   return first_ins;
 }
 
+// warp_merge_topk for at most 32 candidates, without sorting them in shared memory: each
+// candidate stays in a lane, finds its insertion index lo into R by binary search and its rank
+// among the candidates by one round of shuffles (keys are distinct: ids are), so it lands at
+// lo + rank; R[i] moves by #{candidates with lo <= i}, a 5-step search over the candidates' lo
+// values sorted by rank.  Same result as warp_merge_topk.  `ok`, (d, id): this lane's
+// candidate (ok = beats R's tail); slo: 32 ints of scratch.  Returns the lowest position that
+// received a new entry, or K.
+template <class Less>
+SB_DEV int warp_merge_lanes(double* rd, uint32_t* rid, int K, bool ok, double d, uint32_t id,
+                            uint32_t idmask, int* slo, Less lt) {
+  const int lane = lane_id();
+  const unsigned bal = __ballot_sync(0xffffffffu, ok);
+  if (!bal) return K;
+  const int kept = __popc(bal);
+  const uint32_t idk = id & idmask;
+  int lo = 0;
+  if (ok) {
+    int hi = K;
+    while (lo < hi) {
+      const int mid = (lo + hi) >> 1;
+      if (lt(rd[mid], rid[mid] & idmask, d, idk)) lo = mid + 1; else hi = mid;
+    }
+  }
+  // rank among the candidates: lo_k < lo_j orders k first; equal lo compares keys
+  int rank = 0;
+  unsigned rem = bal;
+  while (rem) {
+    const int src = __ffs(rem) - 1;
+    rem &= rem - 1u;
+    const double dk = __shfl_sync(0xffffffffu, d, src);
+    const uint32_t ik = __shfl_sync(0xffffffffu, idk, src);
+    const int lk = __shfl_sync(0xffffffffu, lo, src);
+    if (ok && src != lane) rank += (lk < lo) || (lk == lo && lt(dk, ik, d, idk));
+  }
+  if (ok) slo[rank] = lo;
+  int first = ok ? lo : K;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) first = min(first, __shfl_xor_sync(0xffffffffu, first, o));
+  __syncwarp();
+  if (first >= K) return K;
+  // move R entries at or after `first`, highest first (targets never precede sources)
+  for (int top = K - 1; top >= first; top -= 32) {
+    const int i = top - lane;
+    const bool act = i >= first;
+    double di = 0.0;
+    uint32_t wi = 0;
+    int tgt = K;
+    if (act) {
+      di = rd[i];
+      wi = rid[i];
+      int a = 0, b = kept;  // #{j : slo[j] <= i}
+      while (a < b) {
+        const int mid = (a + b) >> 1;
+        if (slo[mid] <= i) a = mid + 1; else b = mid;
+      }
+      tgt = i + a;
+    }
+    __syncwarp();
+    if (act && tgt < K) {
+      rd[tgt] = di;
+      rid[tgt] = wi;
+    }
+    __syncwarp();
+  }
+  const int pos = lo + rank;
+  if (ok && pos < K) {
+    rd[pos] = d;
+    rid[pos] = id;
+  }
+  __syncwarp();
+  return first;
+}
+
 // number of elements of sorted u64 array s[0..n) strictly less than x
 SB_DEV int lower_bound_u64(const uint64_t* s, int n, uint64_t x) {
   int lo = 0, hi = n;

@@ -48,6 +48,10 @@ constexpr int kRows = 8;                   // rows per lane group in flight (fp3
 
 constexpr int kLazyB = 64;  // insertion buffer of the large-K kernel instances
 constexpr int kLazyK = 1024; // K from which routing uses the insertion buffer
+#ifndef ROUTE_FAST_MERGE
+#define ROUTE_FAST_MERGE 1
+#endif
+constexpr bool kFastMerge = ROUTE_FAST_MERGE != 0;  // warp_merge_lanes for batches of <= 32
 
 struct WarpSmem {
   double* bd;     // kLazyB (large-K instances)
@@ -705,7 +709,19 @@ __global__ void __launch_bounds__(256, ROUTE_MIN_CTAS) route_kernel(RouteArgs a)
         if (LAZY) {
           lazy_merge(c);
         } else {
-          int ins = warp_merge_topk(w.rd, w.rid, K, w.cd, w.cid, w.cpos, c, kIdMask, ord);
+          int ins;
+          if (c <= 32 && kFastMerge) {
+            // one candidate per lane: filter against the tail, then the shuffle-ranked merge
+            const double wd = w.rd[K - 1];
+            const uint32_t wi = w.rid[K - 1] & kIdMask;
+            const bool have = lane < c;
+            const double d = have ? w.cd[lane] : 0.0;
+            const uint32_t id = have ? w.cid[lane] : 0u;
+            const bool ok = have && ord(d, id, wd, wi);
+            ins = warp_merge_lanes(w.rd, w.rid, K, ok, d, id, kIdMask, w.cpos, ord);
+          } else {
+            ins = warp_merge_topk(w.rd, w.rid, K, w.cd, w.cid, w.cpos, c, kIdMask, ord);
+          }
           if (ins < lb) lb = ins;
         }
       }
@@ -758,7 +774,11 @@ static bool route_lazy(const RouteArgs& a) {
     const char* e = getenv("SB_ROUTE_LAZY");
     return !(e && e[0] == '0');
   }();
-  return on && a.Kpad >= kLazyK && a.Cpad >= 16;
+  static const int kmin = [] {
+    const char* e = getenv("SB_ROUTE_LAZYK");
+    return e ? atoi(e) : kLazyK;
+  }();
+  return on && a.Kpad >= kmin && a.Cpad >= 16;
 }
 
 size_t route_smem_per_warp(const RouteArgs& a) {
