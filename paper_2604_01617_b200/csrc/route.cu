@@ -321,6 +321,8 @@ SB_DEV void prefetch_row(const RouteArgs& a, uint32_t node) {
   const int lane = lane_id();
   const char* p = reinterpret_cast<const char*>(a.nbr_ids + (int64_t)node * a.g);
   if (lane * 128 < a.g * 4) asm volatile("prefetch.global.L2 [%0];" ::"l"(p + lane * 128));
+  // and its count (loaded beside the ids: the slower of the two sets the pace)
+  if (lane == 31) asm volatile("prefetch.global.L2 [%0];" ::"l"(a.nbr_counts + node));
 }
 
 // float ordering key usable with integer atomics (monotone in the float value)
@@ -673,7 +675,7 @@ __global__ void __launch_bounds__(256, ROUTE_MIN_CTAS) route_kernel(RouteArgs a)
         if (half) p1_evals += c;
       }
       __syncwarp();
-      if (c > 0 && a.pf_rows) {
+      if (c > 32 && a.pf_rows) {  // (a batch of <= 32 rows is one load per lane already)
         // request every line of the batch's rows at once (L2), so the per-lane row loads
         // below wait for one memory latency instead of one per 128-byte chunk
         const int lines = MODE == kModeU8 && f32 ? (a.m + 127) >> 7 : (a.m * 4 + 127) >> 7;
