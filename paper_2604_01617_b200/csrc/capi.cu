@@ -113,13 +113,16 @@ struct sb_index {
   DBuf qf, qa, qm, entries, ent_scratch, out_ids, out_dists, stats, visited, vlog, counter;
   DBuf bf_part_d, bf_part_i, bf_self, bf_qa, bf_qm, bf_out32, fb, fb_norm, fb_tmp, qb, f8;
   DBuf rl_F, rl_A, rl_ids, rl_counts, rl_perm, rl_f8, rl_tmp;
+  DBuf meta16;                       // {|x|^2, attrs} per node for u8 routing (l <= 3)
+  int64_t meta_version = -1;         // graph_version / layout it was built for
+  int meta_relabel = -1;
   DBuf ft, ft_meta, tq, tcand, tovf;
   ~sb_index() {
     fb.release();
     f8.release();
     DBuf* tfb[] = {&ft, &ft_meta, &tq, &tcand, &tovf};
     for (DBuf* b : tfb) b->release();
-    DBuf* rl[] = {&rl_F, &rl_A, &rl_ids, &rl_counts, &rl_perm, &rl_f8, &rl_tmp};
+    DBuf* rl[] = {&rl_F, &rl_A, &rl_ids, &rl_counts, &rl_perm, &rl_f8, &rl_tmp, &meta16};
     for (DBuf* b : rl) b->release();
     fb_tmp.release();
     fb_norm.release();
@@ -1539,6 +1542,19 @@ static int route_dev(sb_index* idx, const double* qf, const double* qa, const do
     if (r) return r;
     a.F8 = buf.as<uint8_t>();
     a.nx8 = reinterpret_cast<const int32_t*>(buf.as<uint8_t>() + (((size_t)n * idx->m + 255) & ~(size_t)255));
+  }
+  a.meta16 = nullptr;
+  if (a.F8 && idx->l <= 3) {
+    const int rl = relabel ? 1 : 0;
+    const int64_t ver = relabel ? idx->rl_version : 0;
+    if (idx->meta_version != ver || idx->meta_relabel != rl || !idx->meta16.p) {
+      CK(idx->meta16.ensure(16 * (size_t)n));
+      CKL(sb::launch_pack_meta16(a.nx8, a.A, n, idx->l, idx->meta16.p, idx->st));
+      idx->meta_version = ver;
+      idx->meta_relabel = rl;
+      idx->launches += 1;
+    }
+    a.meta16 = reinterpret_cast<const uint4*>(idx->meta16.p);
   }
   idx->last_route_path = sb::route_path(a);
   size_t per_warp = sb::route_smem_per_warp(a);

@@ -148,8 +148,15 @@ SB_DEV void eval_rows(const RouteArgs& a, WarpSmem& w, int c, bool f32, int nq8)
       const uint32_t v = w.cid[j];
       const uint4* xr = reinterpret_cast<const uint4*>(a.F8 + (int64_t)v * a.m);
       AttrPre pre;
-      attr_preload(a, v, pre);
-      const int nxv = __ldg(a.nx8 + v);
+      int nxv;
+      if (a.meta16) {  // |x|^2 and up to three attributes in one 16-byte load
+        const uint4 mt = __ldg(a.meta16 + v);
+        nxv = (int)mt.x;
+        pre.v[0] = (int32_t)mt.y; pre.v[1] = (int32_t)mt.z; pre.v[2] = (int32_t)mt.w; pre.v[3] = 0;
+      } else {
+        attr_preload(a, v, pre);
+        nxv = __ldg(a.nx8 + v);
+      }
       unsigned acc0 = 0u, acc1 = 0u;
       int k = 0;
       for (; k + 8 <= n16; k += 8) {
@@ -848,6 +855,23 @@ __global__ void pack_u8_kernel(const float* F, int64_t n, int m, uint8_t* F8, in
   }
   acc = warp_sum(acc);
   if (lane_id() == 0) nx[v] = acc;
+}
+
+// {|x|^2, attrs[0..2]} per node for the u8 routing rows (l <= 3)
+__global__ void pack_meta16_kernel(const int32_t* nx, const int32_t* A, int64_t n, int l, uint4* out) {
+  const int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (v >= n) return;
+  uint4 r;
+  r.x = (uint32_t)nx[v];
+  r.y = l > 0 ? (uint32_t)A[v * l] : 0u;
+  r.z = l > 1 ? (uint32_t)A[v * l + 1] : 0u;
+  r.w = l > 2 ? (uint32_t)A[v * l + 2] : 0u;
+  out[v] = r;
+}
+
+int launch_pack_meta16(const int32_t* nx, const int32_t* A, int64_t n, int l, void* out, cudaStream_t st) {
+  pack_meta16_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(nx, A, n, l, reinterpret_cast<uint4*>(out));
+  return (int)cudaGetLastError();
 }
 
 int launch_pack_u8(const float* F, int64_t n, int m, uint8_t* F8, int32_t* nx, cudaStream_t st) {

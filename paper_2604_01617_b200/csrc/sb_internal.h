@@ -43,7 +43,10 @@ struct RouteArgs {
   // exact distance ties compare original ids.  Null: identity.
   const int32_t* perm;  // new -> original
   const int32_t* inv;   // original -> new
+  // u8 path, l <= 3: {|x|^2, attrs} per node in one 16-byte record (null: separate arrays)
+  const uint4* meta16;
 };
+int launch_pack_meta16(const int32_t* nx, const int32_t* A, int64_t n, int l, void* out, cudaStream_t st);
 // locality order of the nodes for routing: Z-order of random projections (route.cu)
 int launch_route_order(const float* F, int64_t n, int m, int32_t* perm, int32_t* inv,
                        void* scratch, size_t scratch_bytes, cudaStream_t st);
