@@ -576,7 +576,7 @@ __global__ void __launch_bounds__(256, ROUTE_MIN_CTAS) route_kernel(RouteArgs a)
           uint32_t v = (uint32_t)ent[ent_pos + t];
           if (a.inv) v = (uint32_t)__ldg(a.inv + v);  // original -> layout id
           atomicOr(vis + (v >> 5), 1u << (v & 31));
-          if (ent_pos + t < a.logcap) vlog[ent_pos + t] = v;
+          if (ent_pos + t < a.logcap) vlog[ent_pos + t] = v >> 5;  // the log holds bitset words
           w.cid[t] = v;
         }
       } else {
@@ -671,7 +671,7 @@ __global__ void __launch_bounds__(256, ROUTE_MIN_CTAS) route_kernel(RouteArgs a)
               int pos = c + __popc(bal & ((1u << lane) - 1u));
               w.cid[pos] = v[k];
               int lp = logn + pos;
-              if (lp < a.logcap) vlog[lp] = v[k];
+              if (lp < a.logcap) vlog[lp] = v[k] >> 5;
             }
             c += __popc(bal);
           }
@@ -686,12 +686,17 @@ __global__ void __launch_bounds__(256, ROUTE_MIN_CTAS) route_kernel(RouteArgs a)
         // request every line of the batch's rows at once (L2), so the per-lane row loads
         // below wait for one memory latency instead of one per 128-byte chunk
         const int lines = MODE == kModeU8 && f32 ? (a.m + 127) >> 7 : (a.m * 4 + 127) >> 7;
-        for (int t = lane; t < c * lines; t += 32) {
-          const uint32_t v = w.cid[t / lines];
-          const char* p = (MODE == kModeU8 && f32)
-                              ? reinterpret_cast<const char*>(a.F8 + (int64_t)v * a.m) + (t % lines) * 128
-                              : reinterpret_cast<const char*>(a.F + (int64_t)v * a.m) + (t % lines) * 128;
-          asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
+        const char* fb = (MODE == kModeU8 && f32) ? reinterpret_cast<const char*>(a.F8)
+                                                  : reinterpret_cast<const char*>(a.F);
+        const int64_t rowb = (MODE == kModeU8 && f32) ? a.m : 4 * (int64_t)a.m;
+        if (lines == 1) {  // one 128-byte line per row: no division
+          for (int t = lane; t < c; t += 32)
+            asm volatile("prefetch.global.L2 [%0];" ::"l"(fb + (int64_t)w.cid[t] * rowb));
+        } else {
+          for (int t = lane; t < c * lines; t += 32) {
+            const int r = t / lines;
+            asm volatile("prefetch.global.L2 [%0];" ::"l"(fb + (int64_t)w.cid[r] * rowb + (t - r * lines) * 128));
+          }
         }
       }
       if (c > 0) eval_rows<MODE>(a, w, c, f32, nq8);
@@ -752,7 +757,7 @@ __global__ void __launch_bounds__(256, ROUTE_MIN_CTAS) route_kernel(RouteArgs a)
     }
     // clear the visited bits this query set
     if (logn <= a.logcap) {
-      for (int t = lane; t < logn; t += 32) vis[vlog[t] >> 5] = 0u;
+      for (int t = lane; t < logn; t += 32) vis[vlog[t]] = 0u;
     } else {
       for (int64_t t = lane; t < a.vwords; t += 32) vis[t] = 0u;
     }
