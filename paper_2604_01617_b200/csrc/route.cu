@@ -396,7 +396,7 @@ SB_DEV int warp_count_before(const double* xd, const uint32_t* xi, int n, double
 // grow), so it simply stays unselectable until the next merge drops it.  Selection takes the
 // first unchecked entry of R ∪ B by rank; the admission tail is the union's K-th entry.
 template <int MODE, bool LAZY>
-__global__ void __launch_bounds__(256, ROUTE_MIN_CTAS) route_kernel(RouteArgs a) {
+__global__ void __launch_bounds__(256, LAZY ? 2 : ROUTE_MIN_CTAS) route_kernel(RouteArgs a) {
   extern __shared__ __align__(16) char smem_raw[];
   const int lane = lane_id();
   const int wid = warp_id();
