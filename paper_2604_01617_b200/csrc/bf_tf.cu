@@ -159,7 +159,6 @@ struct TfArgs {
   int ocap;
   int seed;                // > 0: bound-only pass over `seed` evenly spread tiles per split
   int strided;             // 1: split s walks tiles s, s + splits, ...; 0: contiguous ranges
-  uint32_t wait_ns;        // > 0: barrier waits sleep (suspend-time hint) instead of polling
 };
 
 constexpr int kTfMetaStages = 4;
@@ -215,10 +214,7 @@ __global__ void __launch_bounds__(32 * EW + 64, 1) bf_tf_kernel(TfArgs a) {
   auto bar_accf = [&](int s) { return b0 + 8u * (uint32_t)(24 + s); };
   auto bar_empty = [&](int s) { return b0 + 8u * (uint32_t)(26 + s); };
   const uint32_t bar_aready = b0 + 8u * 28;
-  auto wait = [&](uint32_t bar, uint32_t parity) {
-    if (a.wait_ns) mbar_wait_sleep(bar, parity, a.wait_ns);
-    else mbar_wait(bar, parity);
-  };
+  auto wait = [&](uint32_t bar, uint32_t parity) { mbar_wait(bar, parity); };
 
   // tiles of this CTA: i -> tile0 + i * tstride
   const int64_t tiles = (a.n + N - 1) / N;
@@ -751,8 +747,6 @@ int launch_bf_tf(const float* Ft, const float* nxd, const int32_t* code,
   a.stages = sh.stages; a.alpha = alpha; a.gthr = gthr; a.cnt = cnt; a.cand = cand;
   a.cap = cap; a.ocnt = ocnt; a.ocand = ocand; a.ocap = ocap; a.seed = seed;
   a.strided = strided;
-  a.wait_ns = 0;
-  if (const char* e = getenv("SB_TF_WAIT_NS")) a.wait_ns = (uint32_t)atoi(e);
   const size_t smem = tf_smem_bytes(dpad, l, kk, sh.N, sh.stages, sh.ares, sh.qt, sh.ew, sh.kr);
   void (*kern)(TfArgs) = nullptr;
 #define SB_TF_PICK(EW, KR)                                                                          \

@@ -39,18 +39,6 @@ SB_DEV void mbar_wait(uint32_t bar, uint32_t parity) {
       : "memory");
 }
 
-// the same wait with a suspend-time hint (ns): the thread sleeps in the barrier instead of
-// re-polling, leaving the issue slots to the warps that do work
-SB_DEV void mbar_wait_sleep(uint32_t bar, uint32_t parity, uint32_t ns) {
-  asm volatile(
-      "{\n\t.reg .pred P1;\n\t"
-      "WAIT_%=:\n\t"
-      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1, %2;\n\t"
-      "@!P1 bra WAIT_%=;\n\t}\n" ::"r"(bar),
-      "r"(parity), "r"(ns)
-      : "memory");
-}
-
 SB_DEV void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 SB_DEV void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
 SB_DEV void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
