@@ -324,7 +324,7 @@ __global__ void __launch_bounds__(kTcThreads + 32, CTAS) bf_tc_kernel(TcArgs a) 
           // int32 dot products and |x|^2: y = 2 x.q - |x|^2 and the test stay integer
           // (y >= thr  <=>  y >= floor(thr) for integer y, conservatively)
           const int32_t* s_nxi = reinterpret_cast<const int32_t*>(s_nx);
-          int yi[16];
+          int yi[21];  // 16 values + 5 partial maxima
           int mxi = INT_MIN;
 #pragma unroll
           for (int q4 = 0; q4 < 4; ++q4) {
@@ -335,7 +335,9 @@ __global__ void __launch_bounds__(kTcThreads + 32, CTAS) bf_tc_kernel(TcArgs a) 
             yi[4 * q4 + 3] = 2 * (int)r[4 * q4 + 3] - v.w;
           }
 #pragma unroll
-          for (int j = 0; j < 16; ++j) mxi = max(mxi, yi[j]);
+          for (int j = 0; j < 5; ++j)  // tree of 3-input maxima: depth 3, not a 16-long chain
+            yi[16 + j] = max(max(yi[3 * j], yi[3 * j + 1]), yi[3 * j + 2]);
+          mxi = max(max(max(yi[16], yi[17]), yi[18]), max(max(yi[19], yi[20]), yi[15]));
           const int thri = thr < -2.0e9f ? INT_MIN : (thr > 2.0e9f ? INT_MAX : __float2int_rd(thr));
           if (uniform && mxi < thri) continue;
           if (uniform) {
@@ -362,7 +364,7 @@ __global__ void __launch_bounds__(kTcThreads + 32, CTAS) bf_tc_kernel(TcArgs a) 
             }
           }
 #pragma unroll
-          for (int j = 0; j < 16; ++j) mx = fmaxf(mx, y[j]);
+          for (int j = 0; j < 16; ++j) mx = fmaxf(mx, y[j]);  // (bf16 path)
           if (uniform && mx < thr) continue;
           if (uniform) {
 #pragma unroll

@@ -482,14 +482,15 @@ __global__ void __launch_bounds__(32 * EW + 64, 1) bf_tf_kernel(TfArgs a) {
         tmem_ld32(lane_base + (uint32_t)(s * QT * N + c * 32), r);
         const int c0 = part * cols + c * 32;
         // the accumulator holds z = y / 2 with y = 2 x.q - nxs: one max decides the chunk
-        float m0 = fmaxf(__uint_as_float(r[0]), __uint_as_float(r[1]));
-        float m1 = fmaxf(__uint_as_float(r[2]), __uint_as_float(r[3]));
+        // tree of 3-input maxima: depth 4 instead of a 16-long chain
+        float t9[11];
 #pragma unroll
-        for (int j = 4; j < 32; j += 2) {
-          m0 = fmaxf(m0, __uint_as_float(r[j]));
-          m1 = fmaxf(m1, __uint_as_float(r[j + 1]));
-        }
-        const float mx = fmaxf(m0, m1);
+        for (int j = 0; j < 10; ++j)
+          t9[j] = fmaxf(fmaxf(__uint_as_float(r[3 * j]), __uint_as_float(r[3 * j + 1])), __uint_as_float(r[3 * j + 2]));
+        t9[10] = fmaxf(__uint_as_float(r[30]), __uint_as_float(r[31]));
+        const float u0 = fmaxf(fmaxf(t9[0], t9[1]), t9[2]), u1 = fmaxf(fmaxf(t9[3], t9[4]), t9[5]);
+        const float u2 = fmaxf(fmaxf(t9[6], t9[7]), t9[8]), u3 = fmaxf(t9[9], t9[10]);
+        const float mx = fmaxf(fmaxf(u0, u1), fmaxf(u2, u3));
         const bool uniform = s_code[c0] == last_code && s_code[c0 + 31] == last_code;  // warp-uniform
         const bool act = qok && !(uniform && mx < thr_h);
         if (!__any_sync(0xffffffffu, act)) continue;
