@@ -295,6 +295,7 @@ __global__ void __launch_bounds__(kTcThreads + 32, CTAS) bf_tc_kernel(TcArgs a) 
     float thr = -3.4e38f;    // y threshold for the current tuple and t2_eff
     const int cols = N >> 1;
     const uint32_t lane_base = tmem + ((uint32_t)((warp_id() & 3) * 32) << 16) + (uint32_t)(half * cols);
+    float gnext = 3.4e38f;
     for (int i = 0; i < ntl; ++i) {
       const int s = i & 1;
       const uint32_t ph = (uint32_t)((i >> 1) & 1);
@@ -306,8 +307,10 @@ __global__ void __launch_bounds__(kTcThreads + 32, CTAS) bf_tc_kernel(TcArgs a) 
       const int32_t* s_at = reinterpret_cast<const int32_t*>(meta) + 3 * N;
       const int64_t vb = (t_begin + i) * (int64_t)N;
       const int nvalid = (int)(a.n - vb < N ? a.n - vb : N);
-      // the query's tightest bound published by any CTA (read now, used after the tile)
-      const float gpre = qok ? __int_as_float(*reinterpret_cast<volatile int*>(a.gthr + my_q)) : 3.4e38f;
+      // the query's tightest bound published by any CTA: the value loaded one tile ago (its
+      // latency hides behind a whole tile), and the load for the next tile issued now
+      const float gpre = gnext;
+      gnext = qok ? __int_as_float(*reinterpret_cast<volatile int*>(a.gthr + my_q)) : 3.4e38f;
       mbar_wait(bar_fullM + 8 * ms, (uint32_t)((i / kTcMeta) & 1));
       mbar_wait(bar_done + 8 * s, ph);
       tc_fence_after();

@@ -419,6 +419,7 @@ __global__ void __launch_bounds__(32 * EW + 64, 1) bf_tf_kernel(TfArgs a) {
     const size_t seg = ((size_t)blockIdx.y * gridDim.x + blockIdx.x) * EPI + tid;
     uint64_t* my_cand = qok ? a.cand + seg * a.cap : nullptr;
     uint32_t emitted = 0;
+    float gnext = FLT_MAX;
     for (int i = 0; i < ntl; ++i) {
       const int s = i & 1;
       const int ms = i % kTfMetaStages;
@@ -430,7 +431,10 @@ __global__ void __launch_bounds__(32 * EW + 64, 1) bf_tf_kernel(TfArgs a) {
       s_at = reinterpret_cast<const int32_t*>(meta + N * 16);
       const int64_t vb = ((int64_t)i * tstride + tile0) * (int64_t)N;
       const int nvalid = (int)(a.n - vb < N ? a.n - vb : N);
-      const float gpre = qok ? __int_as_float(*reinterpret_cast<volatile int*>(a.gthr + my_q)) : FLT_MAX;
+      // the query's tightest bound published by any CTA: the value loaded one tile ago (its
+      // latency hides behind a whole tile), and the load for the next tile issued now
+      const float gpre = gnext;
+      gnext = qok ? __int_as_float(*reinterpret_cast<volatile int*>(a.gthr + my_q)) : FLT_MAX;
       wait(bar_fullM(ms), (uint32_t)((i / kTfMetaStages) & 1));
       wait(bar_accf(s), (uint32_t)((i >> 1) & 1));
       tc_fence_after();
