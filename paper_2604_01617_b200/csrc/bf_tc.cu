@@ -152,12 +152,13 @@ __global__ void __launch_bounds__(kTcThreads + 32, CTAS) bf_tc_kernel(TcArgs a) 
   uint32_t* li = reinterpret_cast<uint32_t*>(p); p += sizeof(uint32_t) * (size_t)a.kk * kTcThreads;
   volatile float* s_t2 = reinterpret_cast<float*>(p); p += sizeof(float) * kTcThreads;
   p = reinterpret_cast<char*>(((uintptr_t)p + 7) & ~(uintptr_t)7);
-  uint64_t* bars = reinterpret_cast<uint64_t*>(p); p += 8 * 16;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(p); p += 8 * 24;
   uint32_t* tslot = reinterpret_cast<uint32_t*>(p);
-  // fullB[2] done[2] empty[2] a fullM[kTcMeta] emptyM[kTcMeta]
-  const uint32_t bar_fullB = smem_u32(bars), bar_done = smem_u32(bars + 2),
-                 bar_empty = smem_u32(bars + 4), bar_a = smem_u32(bars + 6),
-                 bar_fullM = smem_u32(bars + 7), bar_emptyM = smem_u32(bars + 7 + kTcMeta);
+  // fullB[4] done[2] empty[2] a fullM[kTcMeta] emptyM[kTcMeta] freeB[4]
+  const uint32_t bar_fullB = smem_u32(bars), bar_done = smem_u32(bars + 4),
+                 bar_empty = smem_u32(bars + 6), bar_a = smem_u32(bars + 8),
+                 bar_fullM = smem_u32(bars + 9), bar_emptyM = smem_u32(bars + 9 + kTcMeta),
+                 bar_freeB = smem_u32(bars + 9 + 2 * kTcMeta);
 
   const int64_t q0 = (int64_t)blockIdx.x * kTcM;
   const int64_t tiles = (a.n + N - 1) / N;
@@ -173,9 +174,12 @@ __global__ void __launch_bounds__(kTcThreads + 32, CTAS) bf_tc_kernel(TcArgs a) 
   }
   if (tid == kTcThreads) {
     for (int s = 0; s < 2; ++s) {
-      mbar_init(bar_fullB + 8 * s, 1);
       mbar_init(bar_done + 8 * s, 1);
       mbar_init(bar_empty + 8 * s, kTcThreads);
+    }
+    for (int s = 0; s < 4; ++s) {
+      mbar_init(bar_fullB + 8 * s, 1);
+      mbar_init(bar_freeB + 8 * s, 1);
     }
     for (int s = 0; s < kTcMeta; ++s) {
       mbar_init(bar_fullM + 8 * s, 1);
@@ -203,13 +207,14 @@ __global__ void __launch_bounds__(kTcThreads + 32, CTAS) bf_tc_kernel(TcArgs a) 
       mbar_expect_tx(bar_a, a_bytes);
       bulk_g2s(smem_u32(sA), a.Qb + (size_t)q0 * rowb, a_bytes, bar_a);
       auto load_rows = [&](int i) {
-        const int s = NBS == 1 ? 0 : (i & 1);
+        const int s = NBS == 1 ? 0 : (i % NBS);
         const int64_t v0 = (t_begin + i) * (int64_t)N;
         mbar_expect_tx(bar_fullB + 8 * s, (uint32_t)b_bytes);
         bulk_g2s(smem_u32(sB + s * b_bytes), a.Fb + (size_t)v0 * rowb, (uint32_t)b_bytes,
                  bar_fullB + 8 * s);
       };
-      if (ntl > 0) load_rows(0);
+      // NBS >= 2: a ring of row stages, the first NBS tiles in flight before any MMA
+      for (int j = 0; j < (NBS == 1 ? 1 : NBS) && j < ntl; ++j) load_rows(j);
       mbar_wait(bar_a, 0);
       // BF16 x BF16 -> F32, or U8 x U8 -> S32 (c_format bits [4,6), a/b formats [7,13))
       const uint32_t idesc = (U8 ? (2u << 4) : ((1u << 4) | (1u << 7) | (1u << 10))) |
@@ -220,8 +225,8 @@ __global__ void __launch_bounds__(kTcThreads + 32, CTAS) bf_tc_kernel(TcArgs a) 
         const uint32_t ph = (uint32_t)((i >> 1) & 1);
         // accumulator s: free once the epilogue has left tile i - 2
         if (i >= 2) mbar_wait(bar_empty + 8 * s, ph ^ 1u);
-        const int sb = NBS == 1 ? 0 : s;
-        mbar_wait(bar_fullB + 8 * sb, NBS == 1 ? (uint32_t)(i & 1) : ph);
+        const int sb = NBS == 1 ? 0 : i % NBS;
+        mbar_wait(bar_fullB + 8 * sb, NBS == 1 ? (uint32_t)(i & 1) : (uint32_t)((i / NBS) & 1));
         tc_fence_after();
         const uint32_t a0 = smem_u32(sA), b0 = smem_u32(sB + sb * b_bytes);
         // one MMA per 32 bytes of K (16 bf16 or 32 u8 elements)
@@ -242,12 +247,21 @@ __global__ void __launch_bounds__(kTcThreads + 32, CTAS) bf_tc_kernel(TcArgs a) 
                 "l"(ad), "l"(bd), "r"(idesc), "r"(k > 0 ? 1u : 0u));
         }
         mma_commit(bar_done + 8 * s);
-        // rows of tile i + 1 go to B stage s ^ 1, free once MMA i - 1 has completed (one
-        // stage: once MMA i has)
-        if (i + 1 < ntl) {
-          if (NBS == 1) mbar_wait(bar_done + 8 * s, ph);
-          else if (i >= 1) mbar_wait(bar_done + 8 * (s ^ 1), (uint32_t)(((i - 1) >> 1) & 1));
-          load_rows(i + 1);
+        if (NBS == 1) {
+          // one stage: rows of tile i + 1 once MMA i has completed
+          if (i + 1 < ntl) {
+            mbar_wait(bar_done + 8 * s, ph);
+            load_rows(i + 1);
+          }
+        } else {
+          mma_commit(bar_freeB + 8 * sb);
+          // refill the stage of tile i - 1 (its MMAs have had a tile's time to finish) with
+          // tile i - 1 + NBS
+          if (i >= 1 && i - 1 + NBS < ntl) {
+            const int s1 = (i - 1) % NBS;
+            mbar_wait(bar_freeB + 8 * s1, (uint32_t)(((i - 1) / NBS) & 1));
+            load_rows(i - 1 + NBS);
+          }
         }
       }
     } else if (lane_id() == 1) {
@@ -469,14 +483,14 @@ __global__ void __launch_bounds__(kTcThreads + 32, CTAS) bf_tc_kernel(TcArgs a) 
 size_t bf_tc_smem_n(int rowb, int l, int kk, int N, int nbs) {
   return (size_t)kTcM * rowb + (size_t)nbs * N * rowb + kTcMeta * (size_t)N * (3 + l) * 4 +
          (sizeof(double) + sizeof(uint32_t)) * (size_t)kk * kTcThreads + sizeof(float) * kTcThreads +
-         8 + 128 + 16;
+         8 + 8 * 24 + 16;
 }
 
 // Tile shapes (N nodes per tile, row stages, CTAs per SM), in order of preference; the first
 // that fits shared memory is used.  SB_BF_TILE = "N,stages,ctas" forces one (testing).
 struct TcShape { int N, nbs, ctas; };
-static const TcShape kTcShapes[] = {{128, 2, 2}, {256, 1, 2}, {128, 1, 2}, {64, 2, 2},
-                                    {256, 2, 1}, {128, 2, 1}};
+static const TcShape kTcShapes[] = {{128, 3, 2}, {128, 2, 2}, {256, 1, 2}, {128, 1, 2}, {64, 2, 2},
+                                    {128, 4, 1}, {256, 2, 1}, {128, 2, 1}};
 
 static bool tc_shape_fits(int rowb, int l, int kk, const TcShape& t) {
   const size_t limit = t.ctas == 2 ? 113 * 1024 : 227 * 1024;
@@ -659,6 +673,8 @@ int launch_bf_tc(const void* Fb, const int32_t* nx, const int32_t* A, const int3
 #define SB_TC_PICK(NB, CT) \
   (kind == 2 ? bf_tc_kernel<2, NB, CT> : kind == 1 ? bf_tc_kernel<1, NB, CT> : bf_tc_kernel<0, NB, CT>)
   if (sh.nbs == 1) kern = SB_TC_PICK(1, 2);
+  else if (sh.nbs == 3) kern = SB_TC_PICK(3, 2);
+  else if (sh.nbs == 4) kern = SB_TC_PICK(4, 1);
   else if (sh.ctas == 2) kern = SB_TC_PICK(2, 2);
   else kern = SB_TC_PICK(2, 1);
 #undef SB_TC_PICK
