@@ -156,3 +156,38 @@ def test_tf32_every_tile_shape(tile, monkeypatch):
     ids_s, dd_s = _fp64_path(d, qf, qa, k, 0.6, masks)
     np.testing.assert_array_equal(ids, ids_s)
     np.testing.assert_array_equal(dd, dd_s)
+
+
+@pytest.mark.parametrize("case", ["one_query", "zero_mask", "large_scale", "tiny_scale", "k_equals_n"])
+def test_tf32_edge_cases(case):
+    """Edge cases of the TF32 path: a single query, all-zero masks (no attribute term),
+    values at 1e6 and 1e-6 scale (the certified margin scales with |x|^2 + |q|^2), and
+    k = n (beyond the tensor-core list sizes: the exact fp64 kernel answers)."""
+    rng = np.random.default_rng(["one_query", "zero_mask", "large_scale", "tiny_scale", "k_equals_n"].index(case))
+    n, m, l, q, k = 3000, 24, 2, 40, 10
+    f = rng.standard_normal((n, m)).astype(np.float32)
+    qf = rng.standard_normal((q, m))
+    if case == "large_scale":
+        f *= np.float32(1e6)
+        qf *= 1e6
+    if case == "tiny_scale":
+        f *= np.float32(1e-6)
+        qf *= 1e-6
+    if case == "one_query":
+        qf = qf[:1]
+        q = 1
+    if case == "k_equals_n":
+        n, k = 200, 200
+        f = f[:n]
+    a = rng.integers(1, 4, (n, l)).astype(np.int32)
+    qa = rng.integers(1, 4, (q, l))
+    mk = np.zeros((q, l), np.int64) if case == "zero_mask" else None
+    d = DeviceIndex(f, a, 2)
+    ids, dd = d.bf_topk_queries(qf, qa, k, 0.7, mk)
+    if case != "k_equals_n":
+        assert d.bf_info()["path"] == "tc-tf32-filter"
+    for qi in range(q):
+        wi, wd = O.oracle_auto_topk(f, a, qf[qi], qa[qi], k, 0.7, None if mk is None else mk[qi],
+                                    return_dists=True)
+        np.testing.assert_array_equal(ids[qi], wi, err_msg=f"{case} query {qi}")
+        np.testing.assert_array_equal(dd[qi], wd, err_msg=f"{case} query {qi}")
