@@ -495,6 +495,8 @@ int sb_local_join(sb_index* idx, double inv_alpha, int64_t* inserted_out, int64_
   const size_t stage_budget = 96 * 1024;
   int dc = (int)std::min<int64_t>(idx->m, (int64_t)(stage_budget / (sizeof(float) * spad)));
   if (dc < idx->m) dc = std::max(4, dc & ~3);
+  // the u8 path stages m / 4 words per slot (the stage is sized by dc): room for more CTAs
+  if (join_u8) dc = idx->m / 4;
   size_t smem = sb::join_emit_smem(spad, dc, idx->l, ntiles_max);
   int per_sm = 0;
   CKL(sb::join_emit_occupancy(smem, &per_sm));

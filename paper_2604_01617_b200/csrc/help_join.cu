@@ -90,7 +90,7 @@ SB_DEV void emit2(const JoinArgs& a, Emitter& em, bool p1, uint32_t t1, uint64_t
 // S = |x|^2 + |y|^2 - 2 x.y comes from byte dot products (dp4a), exact in int32 and equal to
 // the reference's fp64 sum of squares.
 template <bool U8>
-__global__ void __launch_bounds__(kJoinThreads, 2) join_emit_kernel(JoinArgs a) {
+__global__ void __launch_bounds__(kJoinThreads, U8 ? 3 : 2) join_emit_kernel(JoinArgs a) {
   extern __shared__ __align__(16) char smem_raw[];
   const int spad = a.spad;
   JoinCta s;
