@@ -67,7 +67,9 @@ struct WarpSmem {
   int* cpos;      // Cpad
 };
 
-SB_HD size_t route_warp_smem_bytes_full(int Kpad, int Cpad, int m, int l, bool lazy) {
+SB_HD size_t route_warp_smem_bytes_full(int Kpad, int Cpad, int m, int l, bool lazy,
+                                         bool rglobal = false) {
+  if (rglobal) Kpad = 0;  // R lives in global memory
   size_t b = (size_t)((m + 3) & ~3) * 4;  // fp32 query first: 16-byte aligned float4 reads
   if (lazy) b += (size_t)kLazyB * 12;
   b += (size_t)Kpad * 8 + (size_t)Cpad * 8 + (size_t)m * 8 + (size_t)l * 16;
@@ -76,7 +78,8 @@ SB_HD size_t route_warp_smem_bytes_full(int Kpad, int Cpad, int m, int l, bool l
 }
 
 template <bool LAZY>
-SB_DEV WarpSmem carve(char* base, const RouteArgs& a) {
+SB_DEV WarpSmem carve(char* base, const RouteArgs& a, int64_t slot) {
+  const bool rg = a.gr_d != nullptr;
   WarpSmem w;
   w.qs32 = reinterpret_cast<float*>(base);
   double* dp = reinterpret_cast<double*>(base + (size_t)((a.m + 3) & ~3) * 4);
@@ -88,13 +91,23 @@ SB_DEV WarpSmem carve(char* base, const RouteArgs& a) {
     w.bid = reinterpret_cast<uint32_t*>(dp);
     dp = reinterpret_cast<double*>(w.bid + kLazyB);
   }
-  w.rd = dp; dp += a.Kpad;
+  if (rg) {
+    w.rd = a.gr_d + slot * a.Kpad;
+  } else {
+    w.rd = dp;
+    dp += a.Kpad;
+  }
   w.cd = dp; dp += a.Cpad;
   w.qs = dp; dp += a.m;
   w.qas = dp; dp += a.l;
   w.qms = dp; dp += a.l;
   uint32_t* up = reinterpret_cast<uint32_t*>(dp);
-  w.rid = up; up += a.Kpad;
+  if (rg) {
+    w.rid = a.gr_i + slot * a.Kpad;
+  } else {
+    w.rid = up;
+    up += a.Kpad;
+  }
   w.cid = up; up += a.Cpad;
   w.cpos = reinterpret_cast<int*>(up);
   return w;
@@ -401,9 +414,9 @@ __global__ void __launch_bounds__(256, LAZY ? 2 : ROUTE_MIN_CTAS) route_kernel(R
   const int lane = lane_id();
   const int wid = warp_id();
   const int nw = blockDim.x >> 5;
-  const size_t wbytes = route_warp_smem_bytes_full(a.Kpad, a.Cpad, a.m, a.l, LAZY);
-  WarpSmem w = carve<LAZY>(smem_raw + wbytes * wid, a);
+  const size_t wbytes = route_warp_smem_bytes_full(a.Kpad, a.Cpad, a.m, a.l, LAZY, a.gr_d != nullptr);
   const int64_t slot = (int64_t)blockIdx.x * nw + wid;
+  WarpSmem w = carve<LAZY>(smem_raw + wbytes * wid, a, slot);
   uint32_t* vis = a.visited + slot * a.vwords;
   uint32_t* vlog = a.vlog + slot * (int64_t)a.logcap;
   const int K = a.K;
@@ -796,7 +809,7 @@ static bool route_lazy(const RouteArgs& a) {
 }
 
 size_t route_smem_per_warp(const RouteArgs& a) {
-  return route_warp_smem_bytes_full(a.Kpad, a.Cpad, a.m, a.l, route_lazy(a));
+  return route_warp_smem_bytes_full(a.Kpad, a.Cpad, a.m, a.l, route_lazy(a), a.gr_d != nullptr);
 }
 
 template <int MODE>

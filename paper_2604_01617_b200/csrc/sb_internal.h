@@ -45,6 +45,10 @@ struct RouteArgs {
   const int32_t* inv;   // original -> new
   // u8 path, l <= 3: {|x|^2, attrs} per node in one 16-byte record (null: separate arrays)
   const uint4* meta16;
+  // very large K: the result list R of each slot in global memory (slots x Kpad dists and
+  // ids) instead of shared memory; null: R in shared memory
+  double* gr_d;
+  uint32_t* gr_i;
 };
 int launch_pack_meta16(const int32_t* nx, const int32_t* A, int64_t n, int l, void* out, cudaStream_t st);
 // locality order of the nodes for routing: Z-order of random projections (route.cu)

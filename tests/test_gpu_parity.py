@@ -238,6 +238,34 @@ def test_route_large_k_insertion_buffer(relabel, g, path, monkeypatch):
     assert gr.device().route_info()["path"].startswith(want_path)
 
 
+@pytest.mark.parametrize("k,force", [(40, True), (700, True), (17000, False)])
+def test_route_result_list_in_global_memory(k, force, monkeypatch):
+    """K beyond shared memory (cfg 5 at cardinality 10^4 needs K near 3·Θ):
+    each slot's result list lives in global memory (automatic once it outgrows shared memory;
+    SB_ROUTE_RGLOBAL=1 forces it at small K).  Results equal the oracle bit for bit."""
+    if force:
+        monkeypatch.setenv("SB_ROUTE_RGLOBAL", "1")
+    rng = np.random.default_rng(k)
+    n, m, l, g = 24000 if k > 1000 else 6000, 24, 1, 20
+    f = rng.integers(0, 5, (n, m)).astype(np.float32)
+    a = rng.integers(1, 30, (n, l)).astype(np.int32)
+    ids = np.stack([rng.choice(n, g, replace=False) for _ in range(n)]).astype(np.int32)
+    cnt = rng.integers(g // 2, g + 1, n).astype(np.int32)
+    gr = sb.RelationGraph(features=f, attrs=a, schema=sb.AttributeSchema((("x",),) * l),
+                          metric=sb.MetricConfig.manual(0.7, l), sigma=0.44, nbr_ids=ids,
+                          nbr_dists=np.zeros((n, g), np.float32), nbr_counts=cnt, frozen=True)
+    q = 3 if k > 1000 else 20
+    qf = rng.integers(0, 5, (q, m)).astype(np.float32)
+    qa = rng.integers(1, 30, (q, l)).astype(np.int32)
+    masks = rng.integers(0, 2, (q, l)).astype(np.float64)
+    p = sb.SearchParams(k=k, seed=3, use_coarse=True)
+    got = sb.search_batch_arrays(gr, qf, qa, p, masks=masks)
+    want = O.search_batch(f, a, ids, cnt, 0.7, qf, qa, k, seed=3, masks=masks, use_coarse=True)
+    np.testing.assert_array_equal(got[0], want[0])
+    np.testing.assert_array_equal(got[1], want[1])
+    np.testing.assert_array_equal(got[2][:, :4], want[2])
+
+
 def test_order_free_mode_is_bit_exact():
     """Integer-valued data in [0, 255] routes through the u8/dp4a path by default; the fp32
     order-free paths (one row per lane, lane groups), the fp64 lane path and the sequential

@@ -11,6 +11,7 @@ from tools.configs import make_config
 cfgname = os.environ.get("CFG", "cfg2")
 K = int(os.environ.get("K", "200"))
 X, A, QX, QA, card = make_config(cfgname)
+QREP = int(os.environ.get("QREP", "1"))  # repeat the query batch: per-query cost without the launch tail
 cache = f"/tmp/sb_graph_{cfgname}.npz"
 if os.path.exists(cache):
     z = np.load(cache); ids, dists, counts, alpha = z["ids"], z["dists"], z["counts"], float(z["alpha"])
@@ -22,8 +23,10 @@ else:
 dev = DeviceIndex(X, A, ids.shape[1])
 dev.upload(ids, dists, counts)
 if os.environ.get("SEQ"): dev.set_distance_mode(True)
-q, m = QX.shape
 P = max(1, K // 2)
+if QREP > 1:
+    QX, QA = np.tile(QX, (QREP, 1)), np.tile(QA, (QREP, 1))
+q, m = QX.shape
 s = torch.cuda.Stream(); torch.cuda.set_stream(s); dev.set_stream(s.cuda_stream)
 qf = torch.from_numpy(QX.astype(np.float64)).cuda(); qa = torch.from_numpy(QA.astype(np.float64)).cuda()
 ent = torch.from_numpy(entry_points_host(X.shape[0], K, 0, 0, q)).cuda()
@@ -42,3 +45,6 @@ stn = st.cpu().numpy().astype(np.float64)
 byt = (stn[:, 0] * (4 * m + 4 * A.shape[1]) + 4 * (stn[:, 2] + stn[:, 3] + stn[:, 4])).sum()
 print(f"lib={os.path.basename(os.environ.get('STABLE_B200_LIB','default'))} K={K} route {ms:.3f} ms  {q/ms*1e3:,.0f} QPS  {byt/ms/1e6:,.1f} GB/s  "
       f"evals={stn[:,0].mean():.0f} p1_exp={stn[:,2].mean():.1f} hops={stn[:,3].mean():.1f} scanned={stn[:,4].mean():.0f}  ids_sum={int(out_i.sum())}", flush=True)
+ev = stn[:, 0]
+print(f"  per 10k queries {ms * 1e4 / q:.3f} ms; evals p50 {np.percentile(ev, 50):.0f} p90 {np.percentile(ev, 90):.0f} "
+      f"p99 {np.percentile(ev, 99):.0f} max {ev.max():.0f}", flush=True)

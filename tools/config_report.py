@@ -2,7 +2,7 @@
 truth (tensor cores) and the QPS-vs-recall curve over the K sweep, written as JSON lines.
 
   python tools/config_report.py cfg3 cfg4 cfg5c1 cfg5c10 cfg5c100 cfg5c1000 cfg5c10000 \
-      [--kcap 4000] [--out profiles/configs_r1.jsonl] [--k100]
+      [--kcap 48000] [--out profiles/configs_r1.jsonl] [--k100]
 
 QPS is end to end through the public API (search_batch_arrays: host query arrays in, host
 results out), best of two runs per K.  Recall@10 is against oracle_auto_topk's exact top 10;
@@ -20,7 +20,8 @@ import numpy as np
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 
-K_SWEEP = [10, 20, 25, 30, 50, 100, 200, 300, 500, 750, 1000, 1500, 2000, 3000, 4000]
+K_SWEEP = [10, 20, 25, 30, 50, 100, 200, 300, 500, 750, 1000, 1500, 2000, 3000, 4000, 6000, 8000,
+           12000, 16000, 24000, 32000, 48000]
 
 
 def recall(ids, gt, k):
@@ -90,7 +91,7 @@ def run(name, kcap, k100, out):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("configs", nargs="+")
-    ap.add_argument("--kcap", type=int, default=4000)
+    ap.add_argument("--kcap", type=int, default=48000)
     ap.add_argument("--k100", action="store_true")
     ap.add_argument("--out", default=os.path.join(ROOT, "profiles", "configs_r1.jsonl"))
     a = ap.parse_args()
