@@ -1581,6 +1581,8 @@ static int route_dev(sb_index* idx, const double* qf, const double* qa, const do
   int per_sm = 0;
   CKL(sb::route_occupancy(a, wpc, per_warp * wpc, &per_sm));
   if (per_sm < 1) return fail(SB_EARG, "routing kernel does not fit on an SM for this k");
+  if (const char* e = getenv("SB_ROUTE_QPSM"))  // resident queries per SM cap (experiments)
+    per_sm = std::max(1, std::min(per_sm, atoi(e) / wpc));
   int ctas = (int)std::min<int64_t>((int64_t)idx->sms * per_sm, (q + wpc - 1) / wpc);
   int64_t slots = (int64_t)ctas * wpc;
   a.vwords = (n + 31) / 32;

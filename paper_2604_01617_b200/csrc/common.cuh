@@ -194,6 +194,51 @@ SB_DEV void warp_bitonic_did(double* d, uint32_t* id, int n, Less lt = Less()) {
   }
 }
 
+// warp_bitonic_did for a list in global memory: each stage walks the n/2 disjoint pairs
+// (i, i | j) directly, U pairs per lane loaded before any is stored (pairs of a stage are
+// disjoint), so the sort costs one L1/L2 round trip per U pairs rather than per pair.
+template <class Less = PlainOrder, int U = 4>
+SB_DEV void warp_bitonic_did_batched(double* d, uint32_t* id, int n, Less lt = Less()) {
+  const int half = n >> 1;
+  for (int k = 2; k <= n; k <<= 1) {
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      const int lj = __ffs(j) - 1;
+      for (int t0 = lane_id(); t0 < half; t0 += 32 * U) {
+        double da[U], db[U];
+        uint32_t ia[U], ib[U];
+        int ii[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const int t = t0 + 32 * u;
+          ii[u] = -1;
+          if (t < half) {
+            const int i = ((t >> lj) << (lj + 1)) | (t & (j - 1));
+            ii[u] = i;
+            da[u] = d[i];
+            db[u] = d[i | j];
+            ia[u] = id[i];
+            ib[u] = id[i | j];
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const int i = ii[u];
+          if (i < 0) continue;
+          const bool up = (i & k) == 0;
+          const bool gt = lt(db[u], ib[u], da[u], ia[u]);
+          if (gt == up) {
+            d[i] = db[u];
+            d[i | j] = da[u];
+            id[i] = ib[u];
+            id[i | j] = ia[u];
+          }
+        }
+      }
+      __syncwarp();
+    }
+  }
+}
+
 // Merge c unsorted candidates (cd, cid) into the sorted top list (rd, rid) of size K, by one
 // warp, in shared memory.  The list's id words may carry flag bits outside `idmask`; flags
 // travel with their entries, inserted entries carry none.  Equivalent to inserting the
@@ -202,7 +247,10 @@ SB_DEV void warp_bitonic_did(double* d, uint32_t* id, int n, Less lt = Less()) {
 // i + #{C < R[i]}.  cpos is scratch of >= c ints; cd/cid must hold next_pow2(c) slots.
 // Returns the lowest position that received a new entry, or K if none did.  `presorted`:
 // the candidates already come in list order (the filter keeps their order).
-template <class Less = PlainOrder>
+// U: list chunks of 32 moved per round trip (all loaded before any is stored: targets never
+// precede sources, so a store cannot clobber an entry not yet loaded); U > 1 for lists in
+// global memory, where each round trip is an L1/L2 latency.
+template <class Less = PlainOrder, int U = 1>
 SB_DEV int warp_merge_topk(double* rd, uint32_t* rid, int K, double* cd, uint32_t* cid,
                            int* cpos, int c, uint32_t idmask, Less lt = Less(),
                            bool presorted = false) {
@@ -257,29 +305,38 @@ SB_DEV int warp_merge_topk(double* rd, uint32_t* rid, int K, double* cd, uint32_
   // R[i] moves by #{j : lo_j <= i}, lo_j = cpos[j] - j (nondecreasing): jc counts the
   // candidates with lo_j <= top, and the few with lo_j inside the chunk are subtracted per lane
   int jc = kept;
-  for (int top = K - 1; top >= first_ins; top -= 32) {
-    int i = top - lane;
-    bool act = i >= first_ins;
-    while (jc > 0 && cpos[jc - 1] - (jc - 1) > top) --jc;
-    double d = 0.0;
-    uint32_t idw = 0;
-    int tgt = K;
-    if (act) {
-      d = rd[i];
-      idw = rid[i];
-      int sh = jc;
-      for (int j = jc - 1; j >= 0; --j) {
-        const int loj = cpos[j] - j;
-        if (loj <= top - 32) break;
-        sh -= loj > i;
+  for (int top0 = K - 1; top0 >= first_ins; top0 -= 32 * U) {
+    double d[U];
+    uint32_t idw[U];
+    int tgt[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int top = top0 - 32 * u;
+      const int i = top - lane;
+      tgt[u] = K;
+      d[u] = 0.0;
+      idw[u] = 0;
+      if (top < first_ins) continue;
+      while (jc > 0 && cpos[jc - 1] - (jc - 1) > top) --jc;
+      if (i >= first_ins) {
+        d[u] = rd[i];
+        idw[u] = rid[i];
+        int sh = jc;
+        for (int j = jc - 1; j >= 0; --j) {
+          const int loj = cpos[j] - j;
+          if (loj <= top - 32) break;
+          sh -= loj > i;
+        }
+        tgt[u] = i + sh;
       }
-      tgt = i + sh;
     }
     __syncwarp();
-    if (act && tgt < K) {
-      rd[tgt] = d;
-      rid[tgt] = idw;
-    }
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+      if (tgt[u] < K) {
+        rd[tgt[u]] = d[u];
+        rid[tgt[u]] = idw[u];
+      }
     __syncwarp();
   }
   for (int j = lane; j < kept; j += 32) {

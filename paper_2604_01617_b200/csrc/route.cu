@@ -408,6 +408,15 @@ SB_DEV int warp_count_before(const double* xd, const uint32_t* xi, int n, double
 // whose rank in R ∪ B is >= K is evicted in the reference and can never return (ranks only
 // grow), so it simply stays unselectable until the next merge drops it.  Selection takes the
 // first unchecked entry of R ∪ B by rank; the admission tail is the union's K-th entry.
+// warp_merge_topk into R: lists in global memory (large-K instance) move 8 chunks per round
+// trip; the small-K instance keeps one code path (its hot loop must stay compact)
+template <bool LAZY, class L>
+SB_DEV int merge_into_r(const RouteArgs& a, double* rd, uint32_t* rid, int K, double* cd,
+                        uint32_t* cid, int* cpos, int c, L lt, bool presorted = false) {
+  if (LAZY && a.gr_d) return warp_merge_topk<L, 8>(rd, rid, K, cd, cid, cpos, c, kIdMask, lt, presorted);
+  return warp_merge_topk<L, 1>(rd, rid, K, cd, cid, cpos, c, kIdMask, lt, presorted);
+}
+
 template <int MODE, bool LAZY>
 __global__ void __launch_bounds__(256, LAZY ? 2 : ROUTE_MIN_CTAS) route_kernel(RouteArgs a) {
   extern __shared__ __align__(16) char smem_raw[];
@@ -493,7 +502,7 @@ __global__ void __launch_bounds__(256, LAZY ? 2 : ROUTE_MIN_CTAS) route_kernel(R
     // LAZY: merge B into R (drops whatever leaves the top K)
     auto flush_b = [&]() {
       if (nbuf > 0) {
-        const int ins = warp_merge_topk(w.rd, w.rid, K, w.bd, w.bid, w.cpos, nbuf, kIdMask, ord, true);
+        const int ins = merge_into_r<LAZY>(a, w.rd, w.rid, K, w.bd, w.bid, w.cpos, nbuf, ord, true);
         if (ins < lb) lb = ins;
         nbuf = 0;
       }
@@ -540,7 +549,7 @@ __global__ void __launch_bounds__(256, LAZY ? 2 : ROUTE_MIN_CTAS) route_kernel(R
       if (kept == 0) return;
       if (nbuf + kept > bcap) flush_b();
       if (kept > bcap) {
-        const int ins = warp_merge_topk(w.rd, w.rid, K, w.cd, w.cid, w.cpos, kept, kIdMask, ord);
+        const int ins = merge_into_r<LAZY>(a, w.rd, w.rid, K, w.cd, w.cid, w.cpos, kept, ord);
         if (ins < lb) lb = ins;
         return;
       }
@@ -727,7 +736,10 @@ __global__ void __launch_bounds__(256, LAZY ? 2 : ROUTE_MIN_CTAS) route_kernel(R
             w.rid[t] = 0xFFFFFFFFu;
           }
           __syncwarp();
-          if (a.Kpad > 1) warp_bitonic_did(w.rd, w.rid, a.Kpad, ord);
+          if (a.Kpad > 1) {
+            if (LAZY && a.gr_d) warp_bitonic_did_batched(w.rd, w.rid, a.Kpad, ord);
+            else warp_bitonic_did(w.rd, w.rid, a.Kpad, ord);
+          }
           stage = a.use_coarse ? 1 : 2;
           lb = 0;
         }
@@ -747,7 +759,7 @@ __global__ void __launch_bounds__(256, LAZY ? 2 : ROUTE_MIN_CTAS) route_kernel(R
             const bool ok = have && ord(d, id, wd, wi);
             ins = warp_merge_lanes(w.rd, w.rid, K, ok, d, id, kIdMask, w.cpos, ord);
           } else {
-            ins = warp_merge_topk(w.rd, w.rid, K, w.cd, w.cid, w.cpos, c, kIdMask, ord);
+            ins = merge_into_r<LAZY>(a, w.rd, w.rid, K, w.cd, w.cid, w.cpos, c, ord);
           }
           if (ins < lb) lb = ins;
         }
