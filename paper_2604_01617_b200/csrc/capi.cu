@@ -1570,6 +1570,7 @@ static int route_dev(sb_index* idx, const double* qf, const double* qa, const do
   // SB_ROUTE_RGLOBAL=1 forces it, 0 disables it (unless R cannot fit shared memory at all).
   bool rglobal = per_warp * 16 > (size_t)227 * 1024;
   if (const char* e = getenv("SB_ROUTE_RGLOBAL")) rglobal = atoi(e) != 0 || per_warp > (size_t)200 * 1024;
+  rglobal = rglobal && sb::route_large_k(a);  // the small-K instance keeps R in shared memory
   if (rglobal) {
     a.gr_d = reinterpret_cast<double*>(16);  // placeholder until the slots are known
     per_warp = sb::route_smem_per_warp(a);

@@ -79,7 +79,7 @@ SB_HD size_t route_warp_smem_bytes_full(int Kpad, int Cpad, int m, int l, bool l
 
 template <bool LAZY>
 SB_DEV WarpSmem carve(char* base, const RouteArgs& a, int64_t slot) {
-  const bool rg = a.gr_d != nullptr;
+  const bool rg = LAZY && a.gr_d != nullptr;  // global lists only in the large-K instance
   WarpSmem w;
   w.qs32 = reinterpret_cast<float*>(base);
   double* dp = reinterpret_cast<double*>(base + (size_t)((a.m + 3) & ~3) * 4);
@@ -423,7 +423,7 @@ __global__ void __launch_bounds__(256, LAZY ? 2 : ROUTE_MIN_CTAS) route_kernel(R
   const int lane = lane_id();
   const int wid = warp_id();
   const int nw = blockDim.x >> 5;
-  const size_t wbytes = route_warp_smem_bytes_full(a.Kpad, a.Cpad, a.m, a.l, LAZY, a.gr_d != nullptr);
+  const size_t wbytes = route_warp_smem_bytes_full(a.Kpad, a.Cpad, a.m, a.l, LAZY, LAZY && a.gr_d != nullptr);
   const int64_t slot = (int64_t)blockIdx.x * nw + wid;
   WarpSmem w = carve<LAZY>(smem_raw + wbytes * wid, a, slot);
   uint32_t* vis = a.visited + slot * a.vwords;
@@ -820,8 +820,11 @@ static bool route_lazy(const RouteArgs& a) {
   return on && a.Kpad >= kmin && a.Cpad >= 16;
 }
 
+bool route_large_k(const RouteArgs& a) { return route_lazy(a); }
+
 size_t route_smem_per_warp(const RouteArgs& a) {
-  return route_warp_smem_bytes_full(a.Kpad, a.Cpad, a.m, a.l, route_lazy(a), a.gr_d != nullptr);
+  const bool lz = route_lazy(a);
+  return route_warp_smem_bytes_full(a.Kpad, a.Cpad, a.m, a.l, lz, lz && a.gr_d != nullptr);
 }
 
 template <int MODE>

@@ -64,6 +64,8 @@ int launch_relabel_adjacency(const int32_t* ids, const int32_t* counts, int64_t 
                              int32_t* counts_r, cudaStream_t st);
 
 size_t route_smem_per_warp(const RouteArgs& a);
+// the insertion-buffer (large-K) kernel instance serves this launch
+bool route_large_k(const RouteArgs& a);
 int launch_feature_scan(const float* F, int64_t count, unsigned* out3, cudaStream_t st);
 int launch_pack_u8(const float* F, int64_t n, int m, uint8_t* F8, int32_t* nx, cudaStream_t st);
 float feature_key_to_float(unsigned k);
