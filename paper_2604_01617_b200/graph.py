@@ -240,7 +240,10 @@ def descent_iteration(graph: RelationGraph, params: BuildParams, _pull: bool = T
     return int(inserted)
 
 
-def run_descent(features, attrs, schema, params: BuildParams, metric: MetricConfig) -> RelationGraph:
+def run_descent(features, attrs, schema, params: BuildParams, metric: MetricConfig,
+                _pull: bool = True) -> RelationGraph:
+    """_pull=False (build()): the rows stay on the device for semantic_prune; the host arrays
+    are refreshed by its download."""
     t0 = time.perf_counter()
     graph = init_random_graph(features, attrs, schema, params, metric, _pull=False)
     t_init = time.perf_counter() - t0
@@ -263,7 +266,8 @@ def run_descent(features, attrs, schema, params: BuildParams, metric: MetricConf
             if psi_history[-1] < params.psi_target:
                 termination = "converged_below_target"
             break
-    graph._pull()
+    if _pull:
+        graph._pull()
     graph.build_log.update({
         "iterations": iterations,
         "psi_history": psi_history,
@@ -293,7 +297,7 @@ def semantic_prune(graph: RelationGraph, params: BuildParams) -> RelationGraph:
 
 def build(features, attrs, schema, params: BuildParams, metric: MetricConfig) -> RelationGraph:
     t0 = time.perf_counter()
-    graph = run_descent(features, attrs, schema, params, metric)
+    graph = run_descent(features, attrs, schema, params, metric, _pull=False)
     semantic_prune(graph, params)
     graph.frozen = True
     # the search-ready layout (locality order, u8 copy) is part of the build
