@@ -69,6 +69,68 @@ struct DBuf {
 
 }  // namespace
 
+// Large copies between the device and pageable host memory, through two page-locked bounce
+// buffers: the DMA of one chunk overlaps the host-side copy of the other, and the host copy
+// (with the first touch of fresh destination pages) is split over host threads.  A direct
+// cudaMemcpy to or from pageable memory runs at a few GB/s (≈0.18 s for cfg 2's adjacency).
+static cudaError_t transfer_large(cudaStream_t st, void* dst, const void* src, size_t bytes,
+                                  bool d2h) {
+  constexpr size_t kChunk = 32u << 20;
+  if (bytes < (8u << 20))
+    return cudaMemcpyAsync(dst, src, bytes, d2h ? cudaMemcpyDeviceToHost : cudaMemcpyHostToDevice, st);
+  static std::mutex mu;  // the bounce buffers are shared by every index of the process
+  std::lock_guard<std::mutex> lock(mu);
+  static char* bounce[2] = {nullptr, nullptr};
+  static cudaEvent_t ev[2] = {nullptr, nullptr};
+  cudaError_t e = cudaSuccess;
+  if (!bounce[0]) {
+    for (int b = 0; b < 2 && e == cudaSuccess; ++b) {
+      e = cudaHostAlloc(reinterpret_cast<void**>(&bounce[b]), kChunk, cudaHostAllocDefault);
+      if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ev[b], cudaEventDisableTiming);
+    }
+    if (e != cudaSuccess) return e;
+  }
+  const size_t nch = (bytes + kChunk - 1) / kChunk;
+  const unsigned hw = std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
+  auto host_copy = [&](char* to, const char* from, size_t len) {
+    const size_t per = (len / hw + 4095) & ~(size_t)4095;
+    std::vector<std::thread> th;
+    for (unsigned t = 0; t < hw && (size_t)t * per < len; ++t) {
+      const size_t o = (size_t)t * per, l = std::min(per, len - o);
+      th.emplace_back([=] { memcpy(to + o, from + o, l); });
+    }
+    for (auto& x : th) x.join();
+  };
+  auto dma = [&](size_t c) {
+    const size_t off = c * kChunk, len = std::min(kChunk, bytes - off);
+    cudaError_t r = d2h ? cudaMemcpyAsync(bounce[c & 1], static_cast<const char*>(src) + off, len,
+                                          cudaMemcpyDeviceToHost, st)
+                        : cudaMemcpyAsync(static_cast<char*>(dst) + off, bounce[c & 1], len,
+                                          cudaMemcpyHostToDevice, st);
+    if (r == cudaSuccess) r = cudaEventRecord(ev[c & 1], st);
+    return r;
+  };
+  if (d2h) {
+    if ((e = dma(0)) != cudaSuccess) return e;
+    for (size_t c = 0; c < nch; ++c) {
+      if (c + 1 < nch && (e = dma(c + 1)) != cudaSuccess) return e;
+      if ((e = cudaEventSynchronize(ev[c & 1])) != cudaSuccess) return e;
+      const size_t off = c * kChunk;
+      host_copy(static_cast<char*>(dst) + off, bounce[c & 1], std::min(kChunk, bytes - off));
+    }
+  } else {
+    for (size_t c = 0; c < nch; ++c) {
+      if (c >= 2 && (e = cudaEventSynchronize(ev[c & 1])) != cudaSuccess) return e;  // buffer free
+      const size_t off = c * kChunk;
+      host_copy(bounce[c & 1], static_cast<const char*>(src) + off, std::min(kChunk, bytes - off));
+      if ((e = dma(c)) != cudaSuccess) return e;
+    }
+    // the caller's later host writes may not race the last DMAs out of the bounce buffers
+    e = cudaStreamSynchronize(st);
+  }
+  return e;
+}
+
 struct sb_index {
   int64_t n = 0;
   int m = 0, l = 0, g = 0;
@@ -193,7 +255,7 @@ int sb_index_create(const float* features, const int32_t* attrs, int64_t n, int3
     delete x;
     return cuda_fail(e, "cudaMalloc(index)");
   }
-  e = cudaMemcpyAsync(x->F.p, features, fb, cudaMemcpyHostToDevice, x->st);
+  e = transfer_large(x->st, x->F.p, features, fb, false);
   if (e == cudaSuccess) e = cudaMemcpyAsync(x->A.p, attrs, ab, cudaMemcpyHostToDevice, x->st);
   if (e == cudaSuccess) e = cudaMemsetAsync(x->counts.p, 0, (size_t)n * 4, x->st);
   if (e == cudaSuccess) e = cudaMemsetAsync(x->flags.p, 0, adj, x->st);
@@ -291,8 +353,8 @@ int sb_adj_upload(sb_index* idx, const int32_t* ids, const float* dists, const i
   if (idx) idx->graph_version++;
   if (!idx || !ids || !dists || !counts) return fail(SB_EARG, "NULL argument");
   size_t adj = (size_t)idx->n * idx->g;
-  CK(cudaMemcpyAsync(idx->ids.p, ids, adj * 4, cudaMemcpyHostToDevice, idx->st));
-  CK(cudaMemcpyAsync(idx->dists.p, dists, adj * 4, cudaMemcpyHostToDevice, idx->st));
+  CK(transfer_large(idx->st, idx->ids.p, ids, adj * 4, false));
+  CK(transfer_large(idx->st, idx->dists.p, dists, adj * 4, false));
   CK(cudaMemcpyAsync(idx->counts.p, counts, (size_t)idx->n * 4, cudaMemcpyHostToDevice, idx->st));
   if (flags) CK(cudaMemcpyAsync(idx->flags.p, flags, adj, cudaMemcpyHostToDevice, idx->st));
   idx->have_cand = false;
@@ -301,60 +363,13 @@ int sb_adj_upload(sb_index* idx, const int32_t* ids, const float* dists, const i
   return SB_OK;
 }
 
-// device -> pageable host copy of a large array through two page-locked bounce buffers: the
-// DMA of chunk i+1 overlaps the host copy-out of chunk i, and the copy-out (with the first
-// touch of freshly allocated destination pages) is split over host threads.  A direct
-// cudaMemcpy into pageable memory runs at a few GB/s (≈0.18 s for cfg 2's adjacency).
-static int download_large(sb_index* idx, void* dst, const void* src, size_t bytes) {
-  constexpr size_t kChunk = 32u << 20;
-  if (bytes < (8u << 20)) {
-    CK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, idx->st));
-    return SB_OK;
-  }
-  static std::mutex mu;  // the bounce buffers are shared by every index of the process
-  std::lock_guard<std::mutex> lock(mu);
-  static char* bounce[2] = {nullptr, nullptr};
-  static cudaEvent_t ev[2] = {nullptr, nullptr};
-  if (!bounce[0]) {
-    for (int b = 0; b < 2; ++b) {
-      CK(cudaHostAlloc(reinterpret_cast<void**>(&bounce[b]), kChunk, cudaHostAllocDefault));
-      CK(cudaEventCreateWithFlags(&ev[b], cudaEventDisableTiming));
-    }
-  }
-  const size_t nch = (bytes + kChunk - 1) / kChunk;
-  const unsigned hw = std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
-  auto issue = [&](size_t c) -> int {
-    const size_t off = c * kChunk, len = std::min(kChunk, bytes - off);
-    CK(cudaMemcpyAsync(bounce[c & 1], static_cast<const char*>(src) + off, len,
-                       cudaMemcpyDeviceToHost, idx->st));
-    CK(cudaEventRecord(ev[c & 1], idx->st));
-    return SB_OK;
-  };
-  int r = issue(0);
-  if (r) return r;
-  for (size_t c = 0; c < nch; ++c) {
-    if (c + 1 < nch && (r = issue(c + 1))) return r;
-    CK(cudaEventSynchronize(ev[c & 1]));
-    const size_t off = c * kChunk, len = std::min(kChunk, bytes - off);
-    const size_t per = (len / hw + 4095) & ~(size_t)4095;
-    std::vector<std::thread> th;
-    for (unsigned t = 0; t < hw && (size_t)t * per < len; ++t) {
-      const size_t o = (size_t)t * per, l = std::min(per, len - o);
-      th.emplace_back([=] { memcpy(static_cast<char*>(dst) + off + o, bounce[c & 1] + o, l); });
-    }
-    for (auto& x : th) x.join();
-  }
-  return SB_OK;
-}
-
 int sb_adj_download(sb_index* idx, int32_t* ids, float* dists, int32_t* counts, uint8_t* flags) {
   if (!idx) return fail(SB_EARG, "idx is NULL");
   size_t adj = (size_t)idx->n * idx->g;
-  int r = 0;
-  if (ids && (r = download_large(idx, ids, idx->ids.p, adj * 4))) return r;
-  if (dists && (r = download_large(idx, dists, idx->dists.p, adj * 4))) return r;
+  if (ids) CK(transfer_large(idx->st, ids, idx->ids.p, adj * 4, true));
+  if (dists) CK(transfer_large(idx->st, dists, idx->dists.p, adj * 4, true));
   if (counts) CK(cudaMemcpyAsync(counts, idx->counts.p, (size_t)idx->n * 4, cudaMemcpyDeviceToHost, idx->st));
-  if (flags && (r = download_large(idx, flags, idx->flags.p, adj))) return r;
+  if (flags) CK(transfer_large(idx->st, flags, idx->flags.p, adj, true));
   CK(cudaStreamSynchronize(idx->st));
   return SB_OK;
 }
