@@ -80,12 +80,19 @@ static cudaError_t transfer_large(cudaStream_t st, void* dst, const void* src, s
     return cudaMemcpyAsync(dst, src, bytes, d2h ? cudaMemcpyDeviceToHost : cudaMemcpyHostToDevice, st);
   static std::mutex mu;  // the bounce buffers are shared by every index of the process
   std::lock_guard<std::mutex> lock(mu);
-  static char* bounce[2] = {nullptr, nullptr};
-  static cudaEvent_t ev[2] = {nullptr, nullptr};
-  cudaError_t e = cudaSuccess;
+  constexpr int kMaxDev = 64;  // events belong to a device: one pair of buffers per device
+  static char* bounce_d[kMaxDev][2] = {};
+  static cudaEvent_t ev_d[kMaxDev][2] = {};
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  if (dev < 0 || dev >= kMaxDev)
+    return cudaMemcpyAsync(dst, src, bytes, d2h ? cudaMemcpyDeviceToHost : cudaMemcpyHostToDevice, st);
+  char** bounce = bounce_d[dev];
+  cudaEvent_t* ev = ev_d[dev];
   if (!bounce[0]) {
     for (int b = 0; b < 2 && e == cudaSuccess; ++b) {
-      e = cudaHostAlloc(reinterpret_cast<void**>(&bounce[b]), kChunk, cudaHostAllocDefault);
+      e = cudaHostAlloc(reinterpret_cast<void**>(&bounce[b]), kChunk, cudaHostAllocPortable);
       if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ev[b], cudaEventDisableTiming);
     }
     if (e != cudaSuccess) return e;
