@@ -137,7 +137,8 @@ int sb_entry_points(int64_t n, int32_t k, uint64_t seed, int64_t qi0, int64_t q,
  * queries with query_index = qi0 + row.  qf f64[q*m], qa f64[q*l], qmask f64[q*l] or NULL
  * (router.py:62-73 widens to f64); entries i64[q*k] or NULL (drawn on the device with the
  * reference's stream).  out_stats i64[q*5] or NULL: dist_evals, phase1_evals,
- * phase1_expansions, hops (SearchStats, router.py:34-39) + neighbours scanned. */
+ * phase1_expansions, hops (SearchStats, router.py:34-39) + neighbours scanned.
+ * 1 <= k <= min(n, 262144); 1 <= pioneer <= k (SB_EARG otherwise). */
 int sb_route_batch(sb_index* idx, const double* qf, const double* qa, const double* qmask,
                    int64_t q, int32_t k, int32_t pioneer, int32_t use_coarse,
                    const int64_t* entries, uint64_t seed, int64_t qi0, double inv_alpha,
