@@ -116,16 +116,26 @@ int sb_reconnect_islands(sb_index* idx, double sigma, int32_t* ran);
 
 /* ---- exhaustive AUTO top-k ------------------------------------------------------ */
 
-/* brute_force_topk (_kernels.py:176-204): exact top-k over all v != u, ids padded -1. */
+/* brute_force_topk (_kernels.py:176-204): exact top-k over all v != u, ids padded -1.
+ * Any k >= 1 (k > 1024 takes the full-sort kernel, bf_sort.cu). */
 int sb_bf_topk_nodes(sb_index* idx, const int64_t* sample_ids, int64_t s, int32_t k,
                      double inv_alpha, int32_t* out_ids);
 
 /* oracle_auto_topk (evaluate.py:32-55) for q queries at once: qf f64[q*m], qa i64[q*l],
  * qmask i64[q*l] or NULL; fused = sqrt(s_v) * (1 + s_a / alpha), ties by id.
- * *uncertain counts queries whose exact re-rank could not be certified (0 expected). */
+ * *uncertain counts queries whose exact re-rank could not be certified (0 expected).
+ * Any 1 <= k <= n (k > 1000 takes the full-sort kernel, bf_sort.cu). */
 int sb_bf_topk_queries(sb_index* idx, const double* qf, const int64_t* qa, const int64_t* qmask,
                        int64_t q, int32_t k, double alpha, int64_t* out_ids, double* out_dists,
                        int32_t* uncertain);
+
+/* oracle_hybrid_groundtruth (evaluate.py:58-77) for q queries: the nodes whose (masked)
+ * attribute Manhattan distance to the query is 0, ranked by pure feature distance
+ * (sqrt of NumPy's pairwise sum, evaluate.py:73-74), ties by id.  out_ids i64[q*k] padded
+ * with -1, out_dists f64[q*k] (+inf padding) or NULL, out_counts i64[q] = min(k, matches). */
+int sb_hybrid_groundtruth(sb_index* idx, const double* qf, const int64_t* qa, const int64_t* qmask,
+                          int64_t q, int32_t k, int64_t* out_ids, double* out_dists,
+                          int64_t* out_counts);
 
 /* ---- Dynamic Heterogeneity Routing --------------------------------------------- */
 
@@ -138,7 +148,10 @@ int sb_entry_points(int64_t n, int32_t k, uint64_t seed, int64_t qi0, int64_t q,
  * (router.py:62-73 widens to f64); entries i64[q*k] or NULL (drawn on the device with the
  * reference's stream).  out_stats i64[q*5] or NULL: dist_evals, phase1_evals,
  * phase1_expansions, hops (SearchStats, router.py:34-39) + neighbours scanned.
- * 1 <= k <= min(n, 262144); 1 <= pioneer <= k (SB_EARG otherwise). */
+ * 1 <= k <= min(n, 262144); 1 <= pioneer <= k (SB_EARG otherwise).  k above ~16,000 keeps
+ * its result lists in global memory, which only the large-K kernel instance supports: that
+ * instance needs gamma > 8 and SB_ROUTE_LAZY != 0; otherwise such k fails with SB_EARG
+ * "k too large for the routing kernel". */
 int sb_route_batch(sb_index* idx, const double* qf, const double* qa, const double* qmask,
                    int64_t q, int32_t k, int32_t pioneer, int32_t use_coarse,
                    const int64_t* entries, uint64_t seed, int64_t qi0, double inv_alpha,

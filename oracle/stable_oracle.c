@@ -16,6 +16,17 @@
  * Layouts (C-contiguous, as the reference passes them, _kernels.py:1-6):
  *   features f32[n*m]   attrs i32[n*l]
  *   nbr_ids i32[n*g]    nbr_dists f32[n*g]   nbr_flags u8[n*g]   nbr_counts i32[n]
+ *
+ * Two ways to run the build:
+ *  - the or_* functions below the metric: the reference's loops one for one, sequential
+ *    (what tests/test_oracle_golden.py pins against the reference's own outputs);
+ *  - the or_*_x functions: the same results computed in parallel on the host cores (OpenMP),
+ *    so the oracle can build 100k-2M node graphs in seconds to minutes.  Each one states why
+ *    its order of work cannot change the result, and the tests pin
+ *    every _x function bit-exact against its sequential twin.  The _x functions also accept
+ *    an optional u8 copy of the features (F8, NULL = none) for data whose features are all
+ *    integers in [0, 255]: then every partial sum of _pair_dist / _diff_cosine is an integer
+ *    below 2^53, so an int32 sum converted to double IS the sequential fp64 sum, bit for bit.
  */
 #include <math.h>
 #include <stdint.h>
@@ -24,8 +35,19 @@
 #ifdef _OPENMP
 #include <omp.h>
 #endif
+#ifdef __AVX2__
+#include <immintrin.h>
+#endif
 
 /* ---- metric (_kernels.py:14-35) -------------------------------------- */
+
+/* the data a distance needs: fp32 features, optional exact u8 copy, attributes */
+typedef struct {
+    const float *F;
+    const uint8_t *F8; /* NULL unless every feature is an integer in [0, 255] */
+    const int32_t *A;
+    int64_t m, l;
+} feat_t;
 
 /* _pair_dist (_kernels.py:14-23): sequential fp64 sums, then sqrt(s_v)*(1+s_a*inv_alpha). */
 static inline double pair_dist(const float *F, const int32_t *A, int64_t m, int64_t l,
@@ -254,6 +276,141 @@ static inline double diff_cosine(const float *F, int64_t m, int64_t s, int64_t p
     return dot / sqrt(np2 * nk2);
 }
 
+/* _pair_dist over feat_t: the u8 path sums exact integers (equal to the sequential fp64 sum,
+ * see the header), the fp32 path is pair_dist above. */
+/* exact integer sums over u8 rows: sum (a-b)^2, and the three sums of _diff_cosine */
+static inline int32_t u8_l2(const uint8_t *a, const uint8_t *b, int64_t m) {
+    int64_t t = 0;
+    int32_t s = 0;
+#ifdef __AVX2__
+    __m256i acc = _mm256_setzero_si256();
+    for (; t + 16 <= m; t += 16) {
+        __m256i x = _mm256_cvtepu8_epi16(_mm_loadu_si128((const __m128i *)(a + t)));
+        __m256i y = _mm256_cvtepu8_epi16(_mm_loadu_si128((const __m128i *)(b + t)));
+        __m256i d = _mm256_sub_epi16(x, y);
+        acc = _mm256_add_epi32(acc, _mm256_madd_epi16(d, d));
+    }
+    __m128i h = _mm_add_epi32(_mm256_castsi256_si128(acc), _mm256_extracti128_si256(acc, 1));
+    h = _mm_add_epi32(h, _mm_shuffle_epi32(h, 0x4E));
+    h = _mm_add_epi32(h, _mm_shuffle_epi32(h, 0xB1));
+    s = _mm_cvtsi128_si32(h);
+#endif
+    for (; t < m; ++t) {
+        int32_t d = (int32_t)a[t] - (int32_t)b[t];
+        s += d * d;
+    }
+    return s;
+}
+
+static inline void u8_cos3(const uint8_t *xs, const uint8_t *xp, const uint8_t *xk, int64_t m,
+                           int32_t *dot, int32_t *np2, int32_t *nk2) {
+    int64_t t = 0;
+    int32_t sd = 0, sp = 0, sk = 0;
+#ifdef __AVX2__
+    __m256i ad = _mm256_setzero_si256(), ap = ad, ak = ad;
+    for (; t + 16 <= m; t += 16) {
+        __m256i s0 = _mm256_cvtepu8_epi16(_mm_loadu_si128((const __m128i *)(xs + t)));
+        __m256i dp = _mm256_sub_epi16(_mm256_cvtepu8_epi16(_mm_loadu_si128((const __m128i *)(xp + t))), s0);
+        __m256i dk = _mm256_sub_epi16(_mm256_cvtepu8_epi16(_mm_loadu_si128((const __m128i *)(xk + t))), s0);
+        ad = _mm256_add_epi32(ad, _mm256_madd_epi16(dp, dk));
+        ap = _mm256_add_epi32(ap, _mm256_madd_epi16(dp, dp));
+        ak = _mm256_add_epi32(ak, _mm256_madd_epi16(dk, dk));
+    }
+    int32_t buf[8];
+    _mm256_storeu_si256((__m256i *)buf, ad);
+    for (int i = 0; i < 8; ++i) sd += buf[i];
+    _mm256_storeu_si256((__m256i *)buf, ap);
+    for (int i = 0; i < 8; ++i) sp += buf[i];
+    _mm256_storeu_si256((__m256i *)buf, ak);
+    for (int i = 0; i < 8; ++i) sk += buf[i];
+#endif
+    for (; t < m; ++t) {
+        int32_t dp = (int32_t)xp[t] - (int32_t)xs[t];
+        int32_t dk = (int32_t)xk[t] - (int32_t)xs[t];
+        sd += dp * dk;
+        sp += dp * dp;
+        sk += dk * dk;
+    }
+    *dot = sd;
+    *np2 = sp;
+    *nk2 = sk;
+}
+
+static inline double fpair_dist(const feat_t *f, int64_t i, int64_t j, double inv_alpha) {
+    if (!f->F8) return pair_dist(f->F, f->A, f->m, f->l, i, j, inv_alpha);
+    int32_t s = u8_l2(f->F8 + i * f->m, f->F8 + j * f->m, f->m);
+    const int32_t *ai = f->A + i * f->l, *aj = f->A + j * f->l;
+    double s_a = 0.0;
+    for (int64_t t = 0; t < f->l; ++t) s_a += fabs((double)ai[t] - (double)aj[t]);
+    return sqrt((double)s) * (1.0 + s_a * inv_alpha);
+}
+
+/* _pair_dist of row j against four rows k[0..3] at once (fp32 features): each AVX2 lane
+ * carries one pair's own sequential fp64 chain, t ascending, multiply and add separately
+ * rounded (no FMA), so every lane equals pair_dist bit for bit. */
+static inline void fpair_dist4(const feat_t *f, int64_t j, const int32_t *k, double inv_alpha,
+                               double out[4]) {
+    if (f->F8) {
+        for (int u = 0; u < 4; ++u) out[u] = fpair_dist(f, j, k[u], inv_alpha);
+        return;
+    }
+    const int64_t m = f->m;
+    const float *xj = f->F + j * m;
+    const float *x0 = f->F + (int64_t)k[0] * m, *x1 = f->F + (int64_t)k[1] * m;
+    const float *x2 = f->F + (int64_t)k[2] * m, *x3 = f->F + (int64_t)k[3] * m;
+    double acc[4];
+    int64_t t = 0;
+#ifdef __AVX2__
+    __m256d s = _mm256_setzero_pd();
+    for (; t + 4 <= m; t += 4) {
+        __m256d r0 = _mm256_cvtps_pd(_mm_loadu_ps(x0 + t));
+        __m256d r1 = _mm256_cvtps_pd(_mm_loadu_ps(x1 + t));
+        __m256d r2 = _mm256_cvtps_pd(_mm_loadu_ps(x2 + t));
+        __m256d r3 = _mm256_cvtps_pd(_mm_loadu_ps(x3 + t));
+        /* transpose: c_u = (x0[t+u], x1[t+u], x2[t+u], x3[t+u]) */
+        __m256d a01l = _mm256_unpacklo_pd(r0, r1), a01h = _mm256_unpackhi_pd(r0, r1);
+        __m256d a23l = _mm256_unpacklo_pd(r2, r3), a23h = _mm256_unpackhi_pd(r2, r3);
+        __m256d c0 = _mm256_permute2f128_pd(a01l, a23l, 0x20);
+        __m256d c1 = _mm256_permute2f128_pd(a01h, a23h, 0x20);
+        __m256d c2 = _mm256_permute2f128_pd(a01l, a23l, 0x31);
+        __m256d c3 = _mm256_permute2f128_pd(a01h, a23h, 0x31);
+        __m256d d;
+        d = _mm256_sub_pd(_mm256_set1_pd((double)xj[t]), c0);
+        s = _mm256_add_pd(s, _mm256_mul_pd(d, d));
+        d = _mm256_sub_pd(_mm256_set1_pd((double)xj[t + 1]), c1);
+        s = _mm256_add_pd(s, _mm256_mul_pd(d, d));
+        d = _mm256_sub_pd(_mm256_set1_pd((double)xj[t + 2]), c2);
+        s = _mm256_add_pd(s, _mm256_mul_pd(d, d));
+        d = _mm256_sub_pd(_mm256_set1_pd((double)xj[t + 3]), c3);
+        s = _mm256_add_pd(s, _mm256_mul_pd(d, d));
+    }
+    _mm256_storeu_pd(acc, s);
+#else
+    acc[0] = acc[1] = acc[2] = acc[3] = 0.0;
+#endif
+    const float *xs[4] = {x0, x1, x2, x3};
+    for (int u = 0; u < 4; ++u) {
+        double a = acc[u];
+        for (int64_t tt = t; tt < m; ++tt) {
+            double d = (double)xj[tt] - (double)xs[u][tt];
+            a += d * d;
+        }
+        const int32_t *ai = f->A + j * f->l, *ak = f->A + (int64_t)k[u] * f->l;
+        double s_a = 0.0;
+        for (int64_t q = 0; q < f->l; ++q) s_a += fabs((double)ai[q] - (double)ak[q]);
+        out[u] = sqrt(a) * (1.0 + s_a * inv_alpha);
+    }
+}
+
+/* _diff_cosine over feat_t (u8 path: exact integer dot products, then the same fp64 finish) */
+static inline double fdiff_cosine(const feat_t *f, int64_t s, int64_t p, int64_t k) {
+    if (!f->F8) return diff_cosine(f->F, f->m, s, p, k);
+    int32_t dot, np2, nk2;
+    u8_cos3(f->F8 + s * f->m, f->F8 + p * f->m, f->F8 + k * f->m, f->m, &dot, &np2, &nk2);
+    if (np2 == 0 || nk2 == 0) return 1.0;
+    return (double)dot / sqrt((double)np2 * (double)nk2);
+}
+
 /* count_in_degrees (_kernels.py:256-263). */
 void or_count_in_degrees(const int32_t *ids, const int32_t *counts, int64_t n, int64_t g,
                          int64_t *in_deg) {
@@ -298,7 +455,7 @@ void or_prune_pass(const float *F, const int32_t *A, int64_t n, int64_t m, int64
 
 /* _try_insert_edge (_kernels.py:306-395): insert j->cand; full rows merge + re-prune
  * under the safeguard, then drop the farthest safe entry.  Returns 1 if inserted. */
-static int try_insert_edge(const float *F, const int32_t *A, int64_t m, int64_t l, int32_t *ids,
+static int try_insert_edge(const feat_t *f, int32_t *ids,
                            float *dists, int32_t *counts, int64_t g, int64_t *in_deg, int64_t j,
                            int64_t cand, double dd, double sigma, int64_t *tmp_ids,
                            double *tmp_dists, uint8_t *keep) {
@@ -341,7 +498,7 @@ static int try_insert_edge(const float *F, const int32_t *A, int64_t m, int64_t 
         for (int32_t u = 0; u < t; ++u) {
             if (!keep[u]) continue;
             int64_t kk = tmp_ids[u];
-            if (attrs_equal(A, l, p, kk) && diff_cosine(F, m, j, p, kk) > sigma) {
+            if (attrs_equal(f->A, f->l, p, kk) && fdiff_cosine(f, j, p, kk) > sigma) {
                 redundant = 1;
                 break;
             }
@@ -377,9 +534,8 @@ static int try_insert_edge(const float *F, const int32_t *A, int64_t m, int64_t 
 
 /* reinforce_pass (_kernels.py:398-409).  Returns the number of full-row merges
  * (instrumentation: 0 means reinforce acted as plain symmetrisation). */
-int64_t or_reinforce_pass(const float *F, const int32_t *A, int64_t n, int64_t m, int64_t l,
-                          int32_t *ids, float *dists, int32_t *counts, int64_t g, int64_t *in_deg,
-                          double sigma) {
+static int64_t reinforce_pass(const feat_t *f, int64_t n, int32_t *ids, float *dists,
+                              int32_t *counts, int64_t g, int64_t *in_deg, double sigma) {
     int64_t *tmp_ids = (int64_t *)malloc(sizeof(int64_t) * (size_t)(g + 1));
     double *tmp_dists = (double *)malloc(sizeof(double) * (size_t)(g + 1));
     uint8_t *keep = (uint8_t *)malloc((size_t)(g + 1));
@@ -396,7 +552,7 @@ int64_t or_reinforce_pass(const float *F, const int32_t *A, int64_t n, int64_t m
                     if (ids[(int64_t)j * g + u] == s) { present = 1; break; }
                 if (!present) ++full_merges;
             }
-            try_insert_edge(F, A, m, l, ids, dists, counts, g, in_deg, j, s, d, sigma, tmp_ids,
+            try_insert_edge(f, ids, dists, counts, g, in_deg, j, s, d, sigma, tmp_ids,
                             tmp_dists, keep);
         }
     }
@@ -404,6 +560,22 @@ int64_t or_reinforce_pass(const float *F, const int32_t *A, int64_t n, int64_t m
     free(tmp_dists);
     free(keep);
     return full_merges;
+}
+
+int64_t or_reinforce_pass(const float *F, const int32_t *A, int64_t n, int64_t m, int64_t l,
+                          int32_t *ids, float *dists, int32_t *counts, int64_t g, int64_t *in_deg,
+                          double sigma) {
+    feat_t f = {F, NULL, A, m, l};
+    return reinforce_pass(&f, n, ids, dists, counts, g, in_deg, sigma);
+}
+
+/* reinforce_pass with the optional exact u8 features (sequential: the overflow re-prune makes
+ * the order of mirrored edges matter, _kernels.py:336-395). */
+int64_t or_reinforce_pass_x(const float *F, const uint8_t *F8, const int32_t *A, int64_t n,
+                            int64_t m, int64_t l, int32_t *ids, float *dists, int32_t *counts,
+                            int64_t g, int64_t *in_deg, double sigma) {
+    feat_t f = {F, F8, A, m, l};
+    return reinforce_pass(&f, n, ids, dists, counts, g, in_deg, sigma);
 }
 
 /* _force_insert_edge (_kernels.py:412-452). */
@@ -442,9 +614,8 @@ static int force_insert_edge(int32_t *ids, float *dists, int32_t *counts, int64_
 }
 
 /* reconnect_islands (_kernels.py:455-487). */
-void or_reconnect_islands(const float *F, const int32_t *A, int64_t n, int64_t m, int64_t l,
-                          int32_t *ids, float *dists, int32_t *counts, int64_t g,
-                          int64_t *in_deg, double sigma) {
+static void reconnect_islands(const feat_t *f, int64_t n, int32_t *ids, float *dists,
+                              int32_t *counts, int64_t g, int64_t *in_deg, double sigma) {
     int64_t *tmp_ids = (int64_t *)malloc(sizeof(int64_t) * (size_t)(g + 1));
     double *tmp_dists = (double *)malloc(sizeof(double) * (size_t)(g + 1));
     uint8_t *keep = (uint8_t *)malloc((size_t)(g + 1));
@@ -454,7 +625,7 @@ void or_reconnect_islands(const float *F, const int32_t *A, int64_t n, int64_t m
         for (int32_t t = 0; t < counts[v]; ++t) {
             int64_t u = ids[v * g + t];
             double d = (double)dists[v * g + t];
-            if (try_insert_edge(F, A, m, l, ids, dists, counts, g, in_deg, u, v, d, sigma,
+            if (try_insert_edge(f, ids, dists, counts, g, in_deg, u, v, d, sigma,
                                 tmp_ids, tmp_dists, keep)) { done = 1; break; }
         }
         if (done) continue;
@@ -470,6 +641,20 @@ void or_reconnect_islands(const float *F, const int32_t *A, int64_t n, int64_t m
     free(tmp_ids);
     free(tmp_dists);
     free(keep);
+}
+
+void or_reconnect_islands(const float *F, const int32_t *A, int64_t n, int64_t m, int64_t l,
+                          int32_t *ids, float *dists, int32_t *counts, int64_t g,
+                          int64_t *in_deg, double sigma) {
+    feat_t f = {F, NULL, A, m, l};
+    reconnect_islands(&f, n, ids, dists, counts, g, in_deg, sigma);
+}
+
+void or_reconnect_islands_x(const float *F, const uint8_t *F8, const int32_t *A, int64_t n,
+                            int64_t m, int64_t l, int32_t *ids, float *dists, int32_t *counts,
+                            int64_t g, int64_t *in_deg, double sigma) {
+    feat_t f = {F, F8, A, m, l};
+    reconnect_islands(&f, n, ids, dists, counts, g, in_deg, sigma);
 }
 
 /* _list_insert (_kernels.py:490-501). */
@@ -661,4 +846,328 @@ void or_fused_all(const float *F, const int32_t *A, int64_t n, int64_t m, int64_
         }
         free(sq);
     }
+}
+
+/* =====================================================================================
+ * Parallel restatements of the build (OpenMP, all host cores).  Each _x function returns
+ * exactly what its sequential twin above returns; tests/test_oracle_golden.py pins that.
+ * nthreads <= 0 means all cores.  F8 may be NULL (see the header).
+ * ===================================================================================== */
+
+static int omp_threads(int nthreads) {
+#ifdef _OPENMP
+    return nthreads > 0 ? nthreads : omp_get_max_threads();
+#else
+    (void)nthreads;
+    return 1;
+#endif
+}
+
+/* compute_row_distances (_kernels.py:71-78): every (i, t) entry is independent. */
+void or_compute_row_distances_x(const float *F, const uint8_t *F8, const int32_t *A, int64_t n,
+                                int64_t m, int64_t l, const int32_t *ids, int64_t g,
+                                double inv_alpha, float *out, int nthreads) {
+    feat_t f = {F, F8, A, m, l};
+#pragma omp parallel for schedule(static) num_threads(omp_threads(nthreads))
+    for (int64_t i = 0; i < n; ++i)
+        for (int64_t t = 0; t < g; ++t)
+            out[i * g + t] = (float)fpair_dist(&f, i, ids[i * g + t], inv_alpha);
+}
+
+/* reverse union of build_candidates for one list kind: row j gains sources i (ascending) while
+ * it has room and i is not already in it.  Row j changes only through its own appends (row i is
+ * read only in its forward prefix, which appends never touch), so targets are independent. */
+static void reverse_union(const int32_t *fwd, int64_t n, int64_t cap, int32_t *cand,
+                          int32_t *counts, int nthreads) {
+    int64_t *off = (int64_t *)calloc((size_t)n + 1, sizeof(int64_t));
+    for (int64_t i = 0; i < n; ++i)
+        for (int32_t x = 0; x < fwd[i]; ++x) off[cand[i * cap + x] + 1] += 1;
+    for (int64_t j = 0; j < n; ++j) off[j + 1] += off[j];
+    int32_t *src = (int32_t *)malloc(sizeof(int32_t) * (size_t)(off[n] > 0 ? off[n] : 1));
+    int64_t *pos = (int64_t *)malloc(sizeof(int64_t) * (size_t)n);
+    memcpy(pos, off, sizeof(int64_t) * (size_t)n);
+    for (int64_t i = 0; i < n; ++i) /* ascending source order within every target */
+        for (int32_t x = 0; x < fwd[i]; ++x) src[pos[cand[i * cap + x]]++] = (int32_t)i;
+#pragma omp parallel for schedule(dynamic, 1024) num_threads(omp_threads(nthreads))
+    for (int64_t j = 0; j < n; ++j) {
+        int32_t *row = cand + j * cap;
+        for (int64_t e = off[j]; e < off[j + 1] && counts[j] < cap; ++e) {
+            int32_t i = src[e];
+            int dup = 0;
+            for (int32_t t = 0; t < counts[j]; ++t)
+                if (row[t] == i) { dup = 1; break; }
+            if (!dup) row[counts[j]++] = i;
+        }
+    }
+    free(src);
+    free(pos);
+    free(off);
+}
+
+/* build_candidates (_kernels.py:81-135): the forward split is per row, then the two reverse
+ * unions (lines 110-134 interleave them per source, but they write disjoint arrays). */
+void or_build_candidates_x(const int32_t *ids, uint8_t *flags, int64_t n, int64_t g, int64_t gn,
+                           int32_t *new_cand, int32_t *new_counts, int32_t *old_cand,
+                           int32_t *old_counts, int nthreads) {
+#pragma omp parallel for schedule(static) num_threads(omp_threads(nthreads))
+    for (int64_t i = 0; i < n; ++i) {
+        int32_t *nc = new_cand + i * gn, *oc = old_cand + i * g;
+        for (int64_t t = 0; t < gn; ++t) nc[t] = -1;
+        for (int64_t t = 0; t < g; ++t) oc[t] = -1;
+        int32_t c = 0, o = 0;
+        for (int64_t t = 0; t < g; ++t) {
+            int32_t j = ids[i * g + t];
+            if (flags[i * g + t] == 1) {
+                nc[c++] = j;
+                flags[i * g + t] = 0;
+                if (c >= gn) break;
+            } else if (o < g) {
+                oc[o++] = j;
+            }
+        }
+        new_counts[i] = c;
+        old_counts[i] = o;
+    }
+    int32_t *fwd = (int32_t *)malloc(sizeof(int32_t) * (size_t)n);
+    memcpy(fwd, new_counts, sizeof(int32_t) * (size_t)n);
+    reverse_union(fwd, n, gn, new_cand, new_counts, nthreads);
+    memcpy(fwd, old_counts, sizeof(int32_t) * (size_t)n);
+    reverse_union(fwd, n, g, old_cand, old_counts, nthreads);
+    free(fwd);
+}
+
+/* _heap_push under row j's spinlock.  The row's tail key only ever decreases, so a candidate
+ * whose distance exceeds a (possibly stale) unlocked read of the tail distance would be
+ * rejected by the locked test too; everything else takes the lock and runs heap_push. */
+static inline int heap_push_locked(int32_t *ids, float *dists, uint8_t *flags, int64_t g,
+                                   int64_t row, int32_t cand, double dd, uint8_t *lk) {
+    if (cand == row) return 0;
+    const float d = (float)dd;
+    uint32_t tb = __atomic_load_n((const uint32_t *)(dists + row * g + g - 1), __ATOMIC_RELAXED);
+    float tail;
+    memcpy(&tail, &tb, sizeof tail);
+    if (d > tail) return 0;
+    while (__atomic_test_and_set(lk + row, __ATOMIC_ACQUIRE))
+        ;
+    int32_t *ri = ids + row * g;
+    float *rd = dists + row * g;
+    uint8_t *rf = flags + row * g;
+    int r = 0;
+    float wd = rd[g - 1];
+    if (!(d > wd || (d == wd && cand >= ri[g - 1]))) {
+        int dup = 0;
+        for (int64_t t = 0; t < g; ++t)
+            if (ri[t] == cand) { dup = 1; break; }
+        if (!dup) {
+            int64_t pos = g - 1;
+            while (pos > 0 && (rd[pos - 1] > d || (rd[pos - 1] == d && ri[pos - 1] > cand))) --pos;
+            /* shift [pos, g-2] up by one; the tail slot is the one read without the lock */
+            uint32_t nb;
+            memcpy(&nb, pos == g - 1 ? &d : &rd[g - 2], sizeof nb);
+            for (int64_t t = g - 1; t > pos; --t) {
+                ri[t] = ri[t - 1];
+                rf[t] = rf[t - 1];
+                if (t < g - 1) rd[t] = rd[t - 1];
+            }
+            __atomic_store_n((uint32_t *)(rd + g - 1), nb, __ATOMIC_RELAXED);
+            ri[pos] = cand;
+            if (pos < g - 1) rd[pos] = d;
+            rf[pos] = 1;
+            r = 1;
+        }
+    }
+    __atomic_clear(lk + row, __ATOMIC_RELEASE);
+    return r;
+}
+
+/* local_join (_kernels.py:138-173) in parallel over i.  Every pushed candidate has a fixed key
+ * (f32 of its pair distance, id), rows reject duplicates, and a row's tail only improves, so
+ * after all pushes each row is the top-g of (its old entries U everything pushed to it) in any
+ * order; old entries that survive keep their flags, new ones get 1.  The
+ * returned count of successful pushes depends on the order, but it is 0 exactly when no row
+ * changed, which is all graph.py:256 tests. */
+int64_t or_local_join_x(const float *F, const uint8_t *F8, const int32_t *A, int64_t n, int64_t m,
+                        int64_t l, double inv_alpha, const int32_t *new_cand,
+                        const int32_t *new_counts, int64_t gn, const int32_t *old_cand,
+                        const int32_t *old_counts, int32_t *ids, float *dists, uint8_t *flags,
+                        int64_t g, int64_t *pairs_out, int nthreads) {
+    feat_t f = {F, F8, A, m, l};
+    uint8_t *lk = (uint8_t *)calloc((size_t)n, 1);
+    int64_t changes = 0, pairs = 0;
+#pragma omp parallel for schedule(dynamic, 256) reduction(+ : changes, pairs) \
+    num_threads(omp_threads(nthreads))
+    for (int64_t i = 0; i < n; ++i) {
+        int32_t na = new_counts[i], nb = old_counts[i];
+        const int32_t *nw = new_cand + i * gn, *od = old_cand + i * g;
+        for (int32_t x = 0; x < na; ++x) {
+            int32_t j = nw[x];
+            /* the partners of j in the reference's order: new[y > x], then old[0..nb) (j == k
+             * skipped); distances four at a time, pushes in that same order per j (the order
+             * is immaterial anyway, see above) */
+            int32_t blk[4];
+            int nblk = 0;
+            for (int32_t y = x + 1; y < na + nb; ++y) {
+                int32_t k = y < na ? nw[y] : od[y - na];
+                if (j == k) continue;
+                blk[nblk++] = k;
+                if (nblk == 4) {
+                    double dd[4];
+                    fpair_dist4(&f, j, blk, inv_alpha, dd);
+                    for (int u = 0; u < 4; ++u) {
+                        ++pairs;
+                        changes += heap_push_locked(ids, dists, flags, g, j, blk[u], dd[u], lk);
+                        changes += heap_push_locked(ids, dists, flags, g, blk[u], j, dd[u], lk);
+                    }
+                    nblk = 0;
+                }
+            }
+            if (nblk) {
+                for (int u = 0; u < nblk; ++u) {
+                    double d = fpair_dist(&f, j, blk[u], inv_alpha);
+                    ++pairs;
+                    changes += heap_push_locked(ids, dists, flags, g, j, blk[u], d, lk);
+                    changes += heap_push_locked(ids, dists, flags, g, blk[u], j, d, lk);
+                }
+            }
+        }
+    }
+    free(lk);
+    if (pairs_out) *pairs_out = pairs;
+    return changes;
+}
+
+/* brute_force_topk (_kernels.py:176-204) with the optional u8 features. */
+void or_brute_force_topk_x(const float *F, const uint8_t *F8, const int32_t *A, int64_t n,
+                           int64_t m, int64_t l, double inv_alpha, const int64_t *sample_ids,
+                           int64_t s, int64_t k, int32_t *out_ids, int nthreads) {
+    feat_t f = {F, F8, A, m, l};
+#pragma omp parallel for schedule(dynamic, 1) num_threads(omp_threads(nthreads))
+    for (int64_t si = 0; si < s; ++si) {
+        int64_t u = sample_ids[si];
+        double *bd = (double *)malloc(sizeof(double) * (size_t)k);
+        int64_t *bi = (int64_t *)malloc(sizeof(int64_t) * (size_t)k);
+        for (int64_t t = 0; t < k; ++t) { bd[t] = INFINITY; bi[t] = n; }
+        for (int64_t v = 0; v < n; ++v) {
+            if (v == u) continue;
+            double d = fpair_dist(&f, u, v, inv_alpha);
+            double wd = bd[k - 1];
+            if (d > wd || (d == wd && v >= bi[k - 1])) continue;
+            int64_t pos = k - 1;
+            while (pos > 0 && (bd[pos - 1] > d || (bd[pos - 1] == d && bi[pos - 1] > v))) {
+                bd[pos] = bd[pos - 1];
+                bi[pos] = bi[pos - 1];
+                --pos;
+            }
+            bd[pos] = d;
+            bi[pos] = v;
+        }
+        for (int64_t t = 0; t < k; ++t) out_ids[si * k + t] = bi[t] < n ? (int32_t)bi[t] : -1;
+        free(bd);
+        free(bi);
+    }
+}
+
+/* One row of prune_pass given the guard decisions: entry p is dropped iff it is redundant and
+ * the in-degree safeguard allows it.  For a row s that is NOT p's highest-id in-neighbour,
+ * in_deg[p] >= 2 when s is processed (s itself and the higher in-neighbour still hold p), so
+ * the safeguard never blocks; for s = maxin[p] it blocks exactly when every other in-neighbour
+ * has already dropped p, which is fire[p].  keep[] receives the row's decisions. */
+static void prune_row(const feat_t *f, const int32_t *ids, const int32_t *counts, int64_t g,
+                      const int32_t *maxin, const uint8_t *fire, double sigma, int64_t s,
+                      uint8_t *keep) {
+    int32_t cnt = counts[s];
+    const int32_t *ri = ids + s * g;
+    if (cnt <= 1) {
+        for (int32_t t = 0; t < cnt; ++t) keep[t] = 1;
+        return;
+    }
+    memset(keep, 0, (size_t)cnt);
+    keep[0] = 1;
+    for (int32_t t = 1; t < cnt; ++t) {
+        int32_t p = ri[t];
+        int redundant = 0;
+        for (int32_t u = 0; u < t; ++u) {
+            if (!keep[u]) continue;
+            int32_t kk = ri[u];
+            if (attrs_equal(f->A, f->l, p, kk) && fdiff_cosine(f, s, p, kk) > sigma) {
+                redundant = 1;
+                break;
+            }
+        }
+        int blocked = maxin[p] == s && fire[p];
+        keep[t] = !(redundant && !blocked);
+    }
+}
+
+/* prune_pass (_kernels.py:266-303) in parallel.  in_deg[p] when row s is
+ * processed = 1 + (rows s' < s that still hold p); it can fall below 2 only at p's highest-id
+ * in-neighbour maxin[p], and there exactly when all other in-neighbours dropped p.  Let
+ * fire[p] be that event.  Rows are evaluated in parallel given fire[], then fire[] is
+ * recomputed from the drops; rows whose maxin entries changed are re-evaluated until nothing
+ * changes.  fire[p] depends only on rows below maxin[p], whose decisions depend only on fire[]
+ * of entries with an even lower maxin, so the iteration reaches the sequential result.
+ * in_deg: in = count_in_degrees (graph.py:212), out = as the sequential pass leaves it. */
+int32_t or_prune_pass_x(const float *F, const uint8_t *F8, const int32_t *A, int64_t n, int64_t m,
+                        int64_t l, int32_t *ids, float *dists, int32_t *counts, int64_t g,
+                        int64_t *in_deg, double sigma, int nthreads) {
+    feat_t f = {F, F8, A, m, l};
+    const int nt = omp_threads(nthreads);
+    int32_t *maxin = (int32_t *)malloc(sizeof(int32_t) * (size_t)n);
+    uint8_t *fire = (uint8_t *)calloc((size_t)n, 1);
+    uint8_t *keep = (uint8_t *)malloc((size_t)(n * g));
+    uint8_t *dirty = (uint8_t *)malloc((size_t)n);
+    int64_t *drops = (int64_t *)malloc(sizeof(int64_t) * (size_t)n);
+    for (int64_t p = 0; p < n; ++p) maxin[p] = -1;
+    for (int64_t s = 0; s < n; ++s) /* ascending s: the last writer is the highest id */
+        for (int32_t t = 0; t < counts[s]; ++t) maxin[ids[s * g + t]] = (int32_t)s;
+    memset(dirty, 1, (size_t)n);
+    int32_t rounds = 0;
+    for (;;) {
+        ++rounds;
+#pragma omp parallel for schedule(dynamic, 256) num_threads(nt)
+        for (int64_t s = 0; s < n; ++s)
+            if (dirty[s]) prune_row(&f, ids, counts, g, maxin, fire, sigma, s, keep + s * g);
+        /* drops of p by rows other than maxin[p] */
+        memset(drops, 0, sizeof(int64_t) * (size_t)n);
+        for (int64_t s = 0; s < n; ++s)
+            for (int32_t t = 0; t < counts[s]; ++t) {
+                int32_t p = ids[s * g + t];
+                if (!keep[s * g + t] && maxin[p] != s) drops[p] += 1;
+            }
+        memset(dirty, 0, (size_t)n);
+        int changed = 0;
+        for (int64_t p = 0; p < n; ++p) {
+            uint8_t nf = maxin[p] >= 0 && drops[p] == in_deg[p] - 1;
+            if (nf != fire[p]) {
+                fire[p] = nf;
+                dirty[maxin[p]] = 1;
+                changed = 1;
+            }
+        }
+        if (!changed) break;
+    }
+    /* compact rows, final in-degrees */
+    for (int64_t s = 0; s < n; ++s) {
+        int32_t cnt = counts[s];
+        if (cnt <= 1) continue;
+        int32_t *ri = ids + s * g;
+        float *rd = dists + s * g;
+        int32_t w = 0;
+        for (int32_t t = 0; t < cnt; ++t) {
+            if (keep[s * g + t]) {
+                ri[w] = ri[t];
+                rd[w] = rd[t];
+                ++w;
+            } else {
+                in_deg[ri[t]] -= 1;
+            }
+        }
+        counts[s] = w;
+    }
+    free(maxin);
+    free(fire);
+    free(keep);
+    free(dirty);
+    free(drops);
+    return rounds;
 }

@@ -11,9 +11,9 @@ __version__ = "0.1.0"
 
 from .errors import (CalibrationError, ConstraintError, FormatError, HybridAnnError,
                      MappingError)
-from .evaluate import (SweepRow, bench_sweep, mean_recall, oracle_auto_topk,
-                       oracle_auto_topk_batch, oracle_hybrid_groundtruth, recall_at_k,
-                       write_sweep_csv)
+from .evaluate import (CSV_FIELDS, ROOFLINE_FIELDS, SweepRow, bench_sweep, mean_recall,
+                       oracle_auto_topk, oracle_auto_topk_batch, oracle_hybrid_groundtruth,
+                       oracle_hybrid_groundtruth_batch, recall_at_k, write_sweep_csv)
 from .graph import (BuildParams, QualityEstimate, RelationGraph, build, descent_iteration,
                     estimate_graph_quality, init_random_graph, init_random_ids,
                     prepare_quality_estimate, read_index, run_descent, semantic_prune,
@@ -30,6 +30,7 @@ __all__ = [
     "compute_alpha", "descent_iteration", "entry_points", "estimate_graph_quality",
     "fused_distance", "init_random_graph", "init_random_ids", "mean_recall", "norm_scale",
     "oracle_auto_topk", "oracle_auto_topk_batch", "oracle_hybrid_groundtruth",
+    "oracle_hybrid_groundtruth_batch", "CSV_FIELDS", "ROOFLINE_FIELDS",
     "prepare_quality_estimate", "read_index", "recall_at_k", "run_descent",
     "sample_statistics", "search", "search_batch", "search_batch_arrays", "semantic_prune",
     "write_index", "write_sweep_csv",

@@ -7,9 +7,9 @@ the adjacency / in-degree arrays, so the reference's own orchestration can drive
 
 (the reference resolves ``_kernels.<fn>`` at call time, graph.py:13, router.py:15).
 
-Device indexes are cached per (features, attrs) buffer; ``route`` additionally caches the
-uploaded adjacency per (nbr_ids, nbr_counts) buffer, i.e. it assumes a frozen graph, as the
-reference's search does (router.py:56-57).
+Device indexes are cached per (features, attrs) CONTENTS (``_lib.fingerprint``), and
+``route`` caches the uploaded adjacency per (nbr_ids, nbr_counts) contents: a new graph whose
+arrays land on a freed address, or arrays written in place, are re-uploaded.
 """
 
 from __future__ import annotations
@@ -19,7 +19,7 @@ import ctypes
 import numpy as np
 
 from . import _lib
-from ._lib import c64, ptr
+from ._lib import c64, fingerprint, ptr
 from .device import DeviceIndex
 
 __all__ = ["compute_row_distances", "build_candidates", "local_join", "brute_force_topk",
@@ -30,12 +30,8 @@ _IDX: dict = {}
 _ROUTE_ADJ: dict = {}
 
 
-def _addr(a: np.ndarray) -> int:
-    return a.__array_interface__["data"][0]
-
-
 def _index(features, attrs, gamma) -> DeviceIndex:
-    key = (_addr(features), features.shape, _addr(attrs), attrs.shape, int(gamma))
+    key = (fingerprint(features), fingerprint(attrs), int(gamma))
     d = _IDX.get(key)
     if d is None:
         if len(_IDX) > 4:
@@ -51,6 +47,12 @@ def _adjacency_only(n, gamma) -> DeviceIndex:
     return _index(np.zeros((n, 1), np.float32), np.zeros((n, 1), np.int32), gamma)
 
 
+def _upload(d: DeviceIndex, *adj):
+    """Replace the device adjacency; the routing cache no longer describes it."""
+    _ROUTE_ADJ.pop(id(d), None)
+    d.upload(*adj)
+
+
 def _write_back(dst: np.ndarray, src: np.ndarray):
     dst[...] = src
 
@@ -58,6 +60,7 @@ def _write_back(dst: np.ndarray, src: np.ndarray):
 def compute_row_distances(features, attrs, nbr_ids, inv_alpha):  # _kernels.py:71-78
     n, g = nbr_ids.shape
     d = _index(features, attrs, g)
+    _ROUTE_ADJ.pop(id(d), None)
     d.init_graph(nbr_ids, inv_alpha)   # computes and sorts each row on the device
     ids_s, dists_s, _, _ = d.download(with_flags=False)
     # back to the caller's column order
@@ -71,7 +74,7 @@ def compute_row_distances(features, attrs, nbr_ids, inv_alpha):  # _kernels.py:7
 def build_candidates(nbr_ids, nbr_flags, gamma_new):  # _kernels.py:81-135
     n, g = nbr_ids.shape
     d = _adjacency_only(n, g)
-    d.upload(nbr_ids, np.zeros((n, g), np.float32), np.full(n, g, np.int32), nbr_flags)
+    _upload(d, nbr_ids, np.zeros((n, g), np.float32), np.full(n, g, np.int32), nbr_flags)
     nc, ncnt, oc, ocnt = d.build_candidates(int(gamma_new), download=True)
     _, _, _, flags = d.download(with_flags=True)
     _write_back(nbr_flags, flags)
@@ -82,7 +85,7 @@ def local_join(features, attrs, inv_alpha, new_cand, new_counts, old_cand, old_c
                nbr_ids, nbr_dists, nbr_flags):  # _kernels.py:138-173
     n, g = nbr_ids.shape
     d = _index(features, attrs, g)
-    d.upload(nbr_ids, nbr_dists, np.full(n, g, np.int32), nbr_flags)
+    _upload(d, nbr_ids, nbr_dists, np.full(n, g, np.int32), nbr_flags)
     nc, ncnt = c64(new_cand, np.int32), c64(new_counts, np.int32)
     oc, ocnt = c64(old_cand, np.int32), c64(old_counts, np.int32)
     _lib.call("sb_set_candidates", d.handle, nc.shape[1], ptr(nc), ptr(ncnt), ptr(oc), ptr(ocnt))
@@ -111,7 +114,7 @@ def graph_quality(nbr_ids, nbr_counts, sample_ids, gt_ids):  # _kernels.py:207-2
 def count_in_degrees(nbr_ids, nbr_counts):  # _kernels.py:256-263
     n, g = nbr_ids.shape
     d = _adjacency_only(n, g)
-    d.upload(nbr_ids, np.zeros((n, g), np.float32), nbr_counts)
+    _upload(d, nbr_ids, np.zeros((n, g), np.float32), nbr_counts)
     return d.count_in_degrees()
 
 
@@ -124,7 +127,7 @@ def _check_indeg(d: DeviceIndex, in_deg):
 def prune_pass(features, attrs, nbr_ids, nbr_dists, nbr_counts, in_deg, sigma):  # 266-303
     n, g = nbr_ids.shape
     d = _index(features, attrs, g)
-    d.upload(nbr_ids, nbr_dists, nbr_counts)
+    _upload(d, nbr_ids, nbr_dists, nbr_counts)
     _check_indeg(d, in_deg)
     d.prune(sigma)
     ids, dists, counts, _ = d.download(with_flags=False)
@@ -137,7 +140,7 @@ def prune_pass(features, attrs, nbr_ids, nbr_dists, nbr_counts, in_deg, sigma): 
 def reinforce_pass(features, attrs, nbr_ids, nbr_dists, nbr_counts, in_deg, sigma):  # 398-409
     n, g = nbr_ids.shape
     d = _index(features, attrs, g)
-    d.upload(nbr_ids, nbr_dists, nbr_counts)
+    _upload(d, nbr_ids, nbr_dists, nbr_counts)
     _check_indeg(d, in_deg)
     over = ctypes.c_int64(0)
     _lib.call("sb_reinforce_pass", d.handle, float(sigma), ctypes.addressof(over))
@@ -151,7 +154,7 @@ def reinforce_pass(features, attrs, nbr_ids, nbr_dists, nbr_counts, in_deg, sigm
 def reconnect_islands(features, attrs, nbr_ids, nbr_dists, nbr_counts, in_deg, sigma):  # 455-487
     n, g = nbr_ids.shape
     d = _index(features, attrs, g)
-    d.upload(nbr_ids, nbr_dists, nbr_counts)
+    _upload(d, nbr_ids, nbr_dists, nbr_counts)
     _check_indeg(d, in_deg)
     ran = ctypes.c_int32(0)
     _lib.call("sb_reconnect_islands", d.handle, float(sigma), ctypes.addressof(ran))
@@ -166,10 +169,10 @@ def route(features, attrs, nbr_ids, nbr_counts, qfeat, qattr, qmask, inv_alpha, 
           pioneer_size, use_coarse):  # _kernels.py:504-610
     n, g = nbr_ids.shape
     d = _index(features, attrs, g)
-    key = (id(d), _addr(nbr_ids), _addr(nbr_counts))
+    key = (fingerprint(nbr_ids), fingerprint(nbr_counts))
     if _ROUTE_ADJ.get(id(d)) != key:
-        d.upload(nbr_ids, np.zeros((n, g), np.float32), nbr_counts)
-        _ROUTE_ADJ[id(d)] = key
+        _upload(d, nbr_ids, np.zeros((n, g), np.float32), nbr_counts)
+        _ROUTE_ADJ[id(d)] = key  # any other adjacency write clears it
     k = int(np.asarray(entries).shape[0])
     ids, dists, st = d.route(np.asarray(qfeat)[None], np.asarray(qattr)[None], k,
                              int(pioneer_size), inv_alpha, qmask=np.asarray(qmask)[None],

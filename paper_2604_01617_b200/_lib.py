@@ -49,6 +49,7 @@ _SIGS = {
     "sb_reconnect_islands": [_vp, _f64, _vp],
     "sb_bf_topk_nodes": [_vp, _vp, _i64, _i32, _f64, _vp],
     "sb_bf_topk_queries": [_vp, _vp, _vp, _vp, _i64, _i32, _f64, _vp, _vp, _vp],
+    "sb_hybrid_groundtruth": [_vp, _vp, _vp, _vp, _i64, _i32, _vp, _vp, _vp],
     "sb_entry_points": [_i64, _i32, _u64, _i64, _i64, _vp],
     "sb_route_batch": [_vp, _vp, _vp, _vp, _i64, _i32, _i32, _i32, _vp, _u64, _i64, _f64,
                        _vp, _vp, _vp],
@@ -141,9 +142,25 @@ def pinned_empty(shape, dtype) -> np.ndarray:
         check(load().sb_host_alloc(nbytes, ctypes.byref(p)))
         addr = p.value
     buf = (ctypes.c_char * nbytes).from_address(addr)
-    arr = np.frombuffer(buf, dtype=dt, count=count).reshape(shape)
-    weakref.finalize(arr, _release, nbytes, addr)
-    return arr
+    # The block goes back to the pool only when the ctypes buffer dies: every array that
+    # reads it (the frombuffer base, its reshape, any row view handed to a caller) holds a
+    # reference chain to `buf`, so a block is never recycled while a result still uses it.
+    weakref.finalize(buf, _release, nbytes, addr)
+    return np.frombuffer(buf, dtype=dt, count=count).reshape(shape)
+
+
+def fingerprint(a: np.ndarray) -> tuple:
+    """Content fingerprint of a host array (shape, dtype, xor and wrapping sum of its words).
+
+    The device caches key on it, so a cache hit needs the same contents, not just the same
+    buffer address: an array written in place, or a new array that lands on a freed address,
+    re-uploads.  Costs one read of the array (≈0.1 s for 512 MB)."""
+    a = np.ascontiguousarray(a)
+    raw = a.reshape(-1).view(np.uint8)
+    head = raw[: raw.size - raw.size % 8].view(np.uint64)
+    tail = bytes(raw[raw.size - raw.size % 8:])
+    return (a.shape, a.dtype.str, int(np.bitwise_xor.reduce(head)) if head.size else 0,
+            int(np.add.reduce(head)) if head.size else 0, tail)
 
 
 def ptr(a: np.ndarray | None):

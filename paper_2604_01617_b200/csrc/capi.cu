@@ -90,12 +90,23 @@ static cudaError_t transfer_large(cudaStream_t st, void* dst, const void* src, s
     return cudaMemcpyAsync(dst, src, bytes, d2h ? cudaMemcpyDeviceToHost : cudaMemcpyHostToDevice, st);
   char** bounce = bounce_d[dev];
   cudaEvent_t* ev = ev_d[dev];
-  if (!bounce[0]) {
+  if (!bounce[0] || !bounce[1] || !ev[0] || !ev[1]) {
+    // (re)initialise every slot; a partial failure frees what was allocated so the next
+    // call starts from a clean state instead of copying into a null buffer
     for (int b = 0; b < 2 && e == cudaSuccess; ++b) {
-      e = cudaHostAlloc(reinterpret_cast<void**>(&bounce[b]), kChunk, cudaHostAllocPortable);
-      if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ev[b], cudaEventDisableTiming);
+      if (!bounce[b])
+        e = cudaHostAlloc(reinterpret_cast<void**>(&bounce[b]), kChunk, cudaHostAllocPortable);
+      if (e == cudaSuccess && !ev[b]) e = cudaEventCreateWithFlags(&ev[b], cudaEventDisableTiming);
     }
-    if (e != cudaSuccess) return e;
+    if (e != cudaSuccess) {
+      for (int b = 0; b < 2; ++b) {
+        if (bounce[b]) cudaFreeHost(bounce[b]);
+        if (ev[b]) cudaEventDestroy(ev[b]);
+        bounce[b] = nullptr;
+        ev[b] = nullptr;
+      }
+      return e;
+    }
   }
   const size_t nch = (bytes + kChunk - 1) / kChunk;
   const unsigned hw = std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
@@ -189,7 +200,9 @@ struct sb_index {
   int64_t meta_version = -1;         // graph_version / layout it was built for
   int meta_relabel = -1;
   DBuf ft, ft_meta, tq, tcand, tovf;
+  DBuf bf_sort;                      // full-sort top-k scratch (bf_sort.cu: any k)
   ~sb_index() {
+    bf_sort.release();
     fb.release();
     f8.release();
     DBuf* tfb[] = {&ft, &ft_meta, &tq, &tcand, &tovf};
@@ -1289,11 +1302,40 @@ static int bf_tf_run(sb_index* idx, const double* qf, const int64_t* qa, const i
   return SB_OK;
 }
 
+// Any k: exact keys of every node, one segmented radix sort per chunk of queries
+// (bf_sort.cu).  a.q rows of a.self_ids / a.qf+a.qa(+a.qmask) are device-resident.
+static int bf_sorted_run(sb_index* idx, const sb::BfArgs& a, int mode, int kout, int64_t* out64,
+                         int32_t* out32, double* outd, int64_t* out_counts) {
+  const int64_t chunk = sb::bf_sort_chunk(idx->n, a.q);
+  const size_t bytes = sb::bf_sort_scratch_bytes(idx->n, chunk);
+  CK(idx->bf_sort.ensure(bytes));
+  for (int64_t q0 = 0; q0 < a.q; q0 += chunk) {
+    const int64_t b = std::min<int64_t>(chunk, a.q - q0);
+    CKL(sb::launch_bf_sorted(a, mode, q0, b, kout, idx->bf_sort.p, bytes, out64, out32, outd,
+                             out_counts, idx->st));
+    idx->launches += 4;
+  }
+  return SB_OK;
+}
+
 int sb_bf_topk_nodes(sb_index* idx, const int64_t* sample_ids, int64_t s, int32_t k,
                      double inv_alpha, int32_t* out_ids) {
   if (!idx || !sample_ids || !out_ids) return fail(SB_EARG, "NULL argument");
-  if (k < 1 || k > 1024) return fail(SB_EARG, "k must be in [1, 1024]");
+  if (k < 1) return fail(SB_EARG, "k must be >= 1");
   if (s <= 0) return SB_OK;
+  if (k > 1024) {  // beyond the tiled kernel's shared-memory lists: full sort per sample
+    CK(idx->bf_self.ensure(sizeof(int64_t) * s));
+    CK(idx->bf_out32.ensure(sizeof(int32_t) * s * k));
+    CK(cudaMemcpyAsync(idx->bf_self.p, sample_ids, sizeof(int64_t) * s, cudaMemcpyHostToDevice, idx->st));
+    sb::BfArgs a{};
+    a.F = idx->F.as<float>(); a.A = idx->A.as<int32_t>(); a.n = idx->n; a.m = idx->m; a.l = idx->l;
+    a.self_ids = idx->bf_self.as<int64_t>(); a.q = s; a.k = k; a.inv_alpha = inv_alpha;
+    int r = bf_sorted_run(idx, a, sb::kBfSortNode, k, nullptr, idx->bf_out32.as<int32_t>(), nullptr, nullptr);
+    if (r) return r;
+    CK(cudaMemcpyAsync(out_ids, idx->bf_out32.p, sizeof(int32_t) * s * k, cudaMemcpyDeviceToHost, idx->st));
+    CK(cudaStreamSynchronize(idx->st));
+    return SB_OK;
+  }
   CK(idx->bf_self.ensure(sizeof(int64_t) * s));
   CK(idx->bf_out32.ensure(sizeof(int32_t) * s * k));
   CK(cudaMemcpyAsync(idx->bf_self.p, sample_ids, sizeof(int64_t) * s, cudaMemcpyHostToDevice, idx->st));
@@ -1312,7 +1354,6 @@ int sb_bf_topk_queries(sb_index* idx, const double* qf, const int64_t* qa, const
                        int32_t* uncertain) {
   if (!idx || !qf || !qa || !out_ids) return fail(SB_EARG, "NULL argument");
   if (k < 1 || k > idx->n) return fail(SB_EARG, "k must be in [1, n]");
-  if (k > 1000) return fail(SB_EARG, "k must be <= 1000");
   if (q <= 0) return SB_OK;
   const int extra = 16;
   int kk = (int)std::min<int64_t>(idx->n, k + extra);
@@ -1329,6 +1370,19 @@ int sb_bf_topk_queries(sb_index* idx, const double* qf, const int64_t* qa, const
   a.qf = idx->qf.as<double>(); a.qa = idx->bf_qa.as<int64_t>();
   a.qmask = qmask ? idx->bf_qm.as<int64_t>() : nullptr; a.q = q; a.k = kk; a.alpha = alpha;
   int unc = 0;
+  if (k > 1000) {  // beyond every tiled kernel's lists: exact keys + full sort (bf_sort.cu)
+    int r = bf_sorted_run(idx, a, sb::kBfSortQuery, k, idx->out_ids.as<int64_t>(), nullptr,
+                          idx->out_dists.as<double>(), nullptr);
+    if (r) return r;
+    idx->bf_ev_valid = false;
+    idx->last_bf_tc = false;
+    idx->last_bf_path = 3;
+    CK(cudaMemcpyAsync(out_ids, idx->out_ids.p, sizeof(int64_t) * q * k, cudaMemcpyDeviceToHost, idx->st));
+    if (out_dists) CK(cudaMemcpyAsync(out_dists, idx->out_dists.p, sizeof(double) * q * k, cudaMemcpyDeviceToHost, idx->st));
+    CK(cudaStreamSynchronize(idx->st));
+    if (uncertain) *uncertain = 0;
+    return SB_OK;
+  }
   // tensor-core path: integer features and queries, |values| <= 256 (exact in bf16), every
   // partial dot product below 2^24 (exact in the fp32 accumulator)
   // (integer data: U is exact whatever the summation order, so lists of exactly k suffice)
@@ -1463,6 +1517,42 @@ int sb_bf_topk_queries(sb_index* idx, const double* qf, const int64_t* qa, const
   if (out_dists) CK(cudaMemcpyAsync(out_dists, idx->out_dists.p, sizeof(double) * q * k, cudaMemcpyDeviceToHost, idx->st));
   CK(cudaStreamSynchronize(idx->st));
   if (uncertain) *uncertain = unc;
+  return SB_OK;
+}
+
+// oracle_hybrid_groundtruth (evaluate.py:58-77) for q queries: nodes whose (masked) attribute
+// Manhattan distance to the query is 0, ranked by pure feature distance (NumPy pairwise order),
+// ties by id; out_ids q x k padded with -1, out_counts[i] = min(k, matches of query i).
+int sb_hybrid_groundtruth(sb_index* idx, const double* qf, const int64_t* qa, const int64_t* qmask,
+                          int64_t q, int32_t k, int64_t* out_ids, double* out_dists,
+                          int64_t* out_counts) {
+  if (!idx || !qf || !qa || !out_ids || !out_counts) return fail(SB_EARG, "NULL argument");
+  if (k < 1) return fail(SB_EARG, "k must be >= 1");
+  if (q <= 0) return SB_OK;
+  const int64_t kk = std::min<int64_t>(k, idx->n);
+  CK(idx->qf.ensure(sizeof(double) * q * idx->m));
+  CK(idx->bf_qa.ensure(sizeof(int64_t) * q * idx->l));
+  CK(idx->bf_qm.ensure(sizeof(int64_t) * q * idx->l));
+  CK(idx->out_ids.ensure(sizeof(int64_t) * q * k));
+  CK(idx->out_dists.ensure(sizeof(double) * q * k));
+  CK(idx->stats.ensure(sizeof(int64_t) * q));
+  CK(cudaMemcpyAsync(idx->qf.p, qf, sizeof(double) * q * idx->m, cudaMemcpyHostToDevice, idx->st));
+  CK(cudaMemcpyAsync(idx->bf_qa.p, qa, sizeof(int64_t) * q * idx->l, cudaMemcpyHostToDevice, idx->st));
+  if (qmask) CK(cudaMemcpyAsync(idx->bf_qm.p, qmask, sizeof(int64_t) * q * idx->l, cudaMemcpyHostToDevice, idx->st));
+  if (kk < k) {  // k > n: the tail past n stays -1 / +inf
+    CK(cudaMemsetAsync(idx->out_ids.p, 0xFF, sizeof(int64_t) * q * k, idx->st));
+  }
+  sb::BfArgs a{};
+  a.F = idx->F.as<float>(); a.A = idx->A.as<int32_t>(); a.n = idx->n; a.m = idx->m; a.l = idx->l;
+  a.qf = idx->qf.as<double>(); a.qa = idx->bf_qa.as<int64_t>();
+  a.qmask = qmask ? idx->bf_qm.as<int64_t>() : nullptr; a.q = q; a.k = (int)kk;
+  int r = bf_sorted_run(idx, a, sb::kBfSortHybrid, k, idx->out_ids.as<int64_t>(), nullptr,
+                        idx->out_dists.as<double>(), idx->stats.as<int64_t>());
+  if (r) return r;
+  CK(cudaMemcpyAsync(out_ids, idx->out_ids.p, sizeof(int64_t) * q * k, cudaMemcpyDeviceToHost, idx->st));
+  if (out_dists) CK(cudaMemcpyAsync(out_dists, idx->out_dists.p, sizeof(double) * q * k, cudaMemcpyDeviceToHost, idx->st));
+  CK(cudaMemcpyAsync(out_counts, idx->stats.p, sizeof(int64_t) * q, cudaMemcpyDeviceToHost, idx->st));
+  CK(cudaStreamSynchronize(idx->st));
   return SB_OK;
 }
 

@@ -99,6 +99,14 @@ int launch_bf_partial(const BfArgs& a, cudaStream_t st);
 int launch_bf_merge_k(const BfArgs& a, int kout, int64_t* out_ids64, int32_t* out_ids32,
                       double* out_dists, int* uncertain, cudaStream_t st);
 
+// exhaustive top-k of any k by a full segmented radix sort of exact keys (bf_sort.cu)
+enum { kBfSortNode = 0, kBfSortQuery = 1, kBfSortHybrid = 2 };
+int64_t bf_sort_chunk(int64_t n, int64_t q);               // queries per sort launch
+size_t bf_sort_scratch_bytes(int64_t n, int64_t b);
+int launch_bf_sorted(const BfArgs& a, int mode, int64_t q0, int64_t b, int kout, void* scratch,
+                     size_t scratch_bytes, int64_t* out_ids64, int32_t* out_ids32,
+                     double* out_dists, int64_t* out_counts, cudaStream_t st);
+
 // tensor-core query-mode top-k for integer data (bf_tc.cu)
 // rowb = operand bytes per row: 2 x features (bf16) or features (u8)
 int bf_tc_supported(int rowb, int l, int kk);

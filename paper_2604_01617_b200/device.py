@@ -209,6 +209,22 @@ class DeviceIndex:
                                "wider than the re-rank margin)")
         return ids, dists
 
+    def hybrid_groundtruth(self, qf, qa, k: int, qmask=None):
+        """oracle_hybrid_groundtruth (evaluate.py:58-77) for q queries: (ids q x k padded with
+        -1, pure feature distances q x k, per-query counts = min(k, matches))."""
+        qf = c64(np.atleast_2d(qf), np.float64)
+        qa = c64(np.atleast_2d(qa), np.int64)
+        qm = None if qmask is None else c64(np.atleast_2d(qmask), np.int64)
+        q = qf.shape[0]
+        if qf.shape[1] != self.m or qa.shape != (q, self.l):
+            raise ValueError("query shape mismatch")
+        ids = np.empty((q, k), np.int64)
+        dists = np.empty((q, k), np.float64)
+        counts = np.empty(q, np.int64)
+        _lib.call("sb_hybrid_groundtruth", self._h, ptr(qf), ptr(qa), ptr(qm), q, int(k),
+                  ptr(ids), ptr(dists), ptr(counts))
+        return ids, dists, counts
+
     # ---- routing -----------------------------------------------------------------------
     def route(self, qf, qa, k: int, pioneer: int, inv_alpha: float, qmask=None, entries=None,
               seed: int = 0, qi0: int = 0, use_coarse: bool = True, stats=True):

@@ -156,3 +156,87 @@ def test_cfg1_goldens(cfg1_golden):
     for qi in range(0, 200, 7):
         np.testing.assert_array_equal(O.oracle_auto_topk(X, A, QX[qi], QA[qi], 10, alpha),
                                       gd["oracle_top10"][qi])
+
+
+# ---- the parallel restatement (stable_oracle.c or_*_x, oracle.ParallelKernels) ---------------
+
+def _staged_par(gd, gamma, sigma, seed, nthreads, psi_target=0.8):
+    snaps, stages = [], {}
+    g = O.run_descent(gd["features"], gd["attrs"], float(gd["alpha"]), gamma=gamma,
+                      gamma_new=gamma, psi_target=psi_target, seed=seed, snapshots=snaps,
+                      nthreads=nthreads)
+    O.semantic_prune(g, sigma, stages, nthreads=nthreads)
+    return g, snaps, stages
+
+
+@pytest.mark.parametrize("nthreads", [0, 3])
+def test_parallel_build_small_every_stage(small_golden, nthreads):
+    gd = small_golden
+    g, snaps, stages = _staged_par(gd, 24, float(gd["sigma"]), 3, nthreads)
+    _check_stages(gd, g, snaps, stages)
+
+
+@pytest.mark.parametrize("nthreads", [0, 2])
+def test_parallel_build_overflow_every_stage(overflow_golden, nthreads):
+    gd = overflow_golden
+    g, snaps, stages = _staged_par(gd, 12, float(gd["sigma"]), 9, nthreads)
+    assert g.log["full_merges"] > 0
+    _check_stages(gd, g, snaps, stages)
+
+
+def _u8_or_real(kind, n, m, l, card, rng):
+    if kind == "u8":
+        centres = rng.uniform(0, 255, (20, m))
+        x = np.clip(np.rint(centres[rng.integers(0, 20, n)] + 25 * rng.standard_normal((n, m))), 0, 255)
+    elif kind == "dup":  # exact duplicate rows: zero-length offsets, cosine 1.0, ties by id
+        base = rng.integers(0, 4, (n // 3, m))
+        x = base[rng.integers(0, n // 3, n)]
+    else:
+        x = rng.standard_normal((n, m)) * np.exp(rng.uniform(-1, 1, m))
+    return x.astype(np.float32), rng.integers(1, card + 1, (n, l)).astype(np.int32)
+
+
+@pytest.mark.parametrize("kind,n,m,l,card,gamma,sigma", [
+    ("u8", 3000, 64, 2, 3, 24, 0.44), ("real", 3000, 37, 1, 5, 20, 0.3),
+    ("real", 2500, 13, 2, 2, 32, 0.6), ("dup", 1500, 8, 1, 2, 16, 0.44),
+    ("u8", 1200, 128, 3, 2, 40, 0.2)])
+def test_parallel_build_equals_sequential(kind, n, m, l, card, gamma, sigma):
+    """Every stage of the parallel build against the reference's loops on data the goldens do
+    not cover: exact u8 sums, d % 4 != 0 (the 4-lane fp64 tail), duplicates, heavy pruning."""
+    rng = np.random.default_rng(n + m)
+    X, A = _u8_or_real(kind, n, m, l, card, rng)
+    s_v, s_a = O.sample_statistics(X, A, min(500, n), seed=0)
+    alpha = O.compute_alpha(s_v, s_a, n, l)
+    seq_s, seq_st, par_s, par_st = [], {}, [], {}
+    g1 = O.run_descent(X, A, alpha, gamma=gamma, gamma_new=gamma, snapshots=seq_s, nthreads=1)
+    g2 = O.run_descent(X, A, alpha, gamma=gamma, gamma_new=gamma, snapshots=par_s, nthreads=0)
+    assert g1.log["psi_history"] == g2.log["psi_history"]
+    assert g1.log["pairs"] == g2.log["pairs"]
+    for a, b in zip(seq_s, par_s):
+        for x, y in zip(a, b):
+            np.testing.assert_array_equal(x, y)
+    O.semantic_prune(g1, sigma, seq_st, nthreads=1)
+    O.semantic_prune(g2, sigma, par_st, nthreads=0)
+    for key in seq_st:
+        np.testing.assert_array_equal(seq_st[key], par_st[key], err_msg=key)
+    np.testing.assert_array_equal(g1.nbr_counts, g2.nbr_counts)
+    np.testing.assert_array_equal(g1.nbr_ids, g2.nbr_ids)
+    np.testing.assert_array_equal(g1.nbr_dists, g2.nbr_dists)
+    assert g1.log["full_merges"] == g2.log["full_merges"]
+
+
+def test_u8_copy_only_for_exact_bytes():
+    assert O.u8_copy(np.array([[0, 255.0]], np.float32)) is not None
+    assert O.u8_copy(np.array([[0, 256.0]], np.float32)) is None
+    assert O.u8_copy(np.array([[-1, 2.0]], np.float32)) is None
+    assert O.u8_copy(np.array([[0.5, 2.0]], np.float32)) is None
+
+
+def test_hybrid_groundtruth_restatement():
+    # reference test_evaluate.py:40-49: exact-match filter, fewer than k when matches are scarce
+    f = np.array([[0, 0], [1, 0], [2, 0], [3, 0]], np.float32)
+    a = np.array([[1, 1], [1, 2], [1, 1], [2, 1]], np.int32)
+    np.testing.assert_array_equal(O.oracle_hybrid_groundtruth(f, a, [0, 0], [1, 1], 5), [0, 2])
+    np.testing.assert_array_equal(O.oracle_hybrid_groundtruth(f, a, [0, 0], [1, 1], 5, mask=[1, 0]),
+                                  [0, 1, 2])
+    assert O.oracle_hybrid_groundtruth(f, a, [0, 0], [9, 9], 5).size == 0
