@@ -102,7 +102,7 @@ __global__ void bf_sort_gather_kernel(int mode, int64_t n, int64_t q0, int64_t b
 
 int64_t bf_sort_chunk(int64_t n, int64_t q) {
   const int64_t cap = std::max<int64_t>(1, (int64_t(1) << 26) / std::max<int64_t>(1, n));
-  return std::min<int64_t>(q, cap);
+  return std::min<int64_t>(std::min<int64_t>(q, cap), 65535);  // grid.y limit
 }
 
 size_t bf_sort_scratch_bytes(int64_t n, int64_t b) {
@@ -113,7 +113,7 @@ size_t bf_sort_scratch_bytes(int64_t n, int64_t b) {
                                            (uint32_t*)nullptr, (int64_t)keys, (int64_t)b,
                                            (const int64_t*)nullptr, (const int64_t*)nullptr);
   return keys * 2 * (sizeof(uint64_t) + sizeof(uint32_t)) + sizeof(int64_t) * (b + 1) +
-         sizeof(unsigned long long) * b + temp + 1024;
+         sizeof(unsigned long long) * b + temp + 8192;  // + 256-byte alignment of six arrays
 }
 
 int launch_bf_sorted(const BfArgs& a, int mode, int64_t q0, int64_t b, int kout, void* scratch,

@@ -607,7 +607,9 @@ int sb_local_join(sb_index* idx, double inv_alpha, int64_t* inserted_out, int64_
   unsigned long long* d_inserted = d_count + 1;
   int* d_nodectr = reinterpret_cast<int*>(d_count + 2);
   int* d_overflow = d_nodectr + 1;
+  unsigned long long* d_same = d_count + 3;  // small: [count, inserted, nodectr|overflow, same]
   CK(cudaMemsetAsync(d_inserted, 0, sizeof(unsigned long long), idx->st));
+  CK(cudaMemsetAsync(d_same, 0, sizeof(unsigned long long), idx->st));
   int64_t begin = 0;
   while (begin < n) {
     uint64_t acc = slack;
@@ -626,6 +628,7 @@ int sb_local_join(sb_index* idx, double inv_alpha, int64_t* inserted_out, int64_
     a.node_counter = d_nodectr; a.push_tgt = idx->push_tgt.as<uint32_t>();
     a.push_key = idx->push_key.as<uint64_t>(); a.push_cap = cap; a.push_count = d_count;
     a.row_cnt = idx->row_cnt.as<int64_t>(); a.overflow = d_overflow; a.spad = spad; a.dc = dc;
+    a.same_pairs = d_same;
     a.ntiles_max = ntiles_max;
     a.F8 = join_u8 ? idx->f8.as<uint8_t>() : nullptr;
     a.nx8 = join_u8 ? reinterpret_cast<const int32_t*>(idx->f8.as<uint8_t>() + (((size_t)n * idx->m + 255) & ~(size_t)255)) : nullptr;
@@ -651,10 +654,14 @@ int sb_local_join(sb_index* idx, double inv_alpha, int64_t* inserted_out, int64_
     idx->launches += 5;
     begin = end;
   }
-  unsigned long long ins = 0;
+  unsigned long long ins = 0, same = 0;
   CK(cudaMemcpyAsync(&ins, d_inserted, sizeof(ins), cudaMemcpyDeviceToHost, idx->st));
+  CK(cudaMemcpyAsync(&same, d_same, sizeof(same), cudaMemcpyDeviceToHost, idx->st));
   CK(cudaStreamSynchronize(idx->st));
   if (inserted_out) *inserted_out = (int64_t)ins;
+  // pairs evaluated exactly as the reference's loop counts them (j == k pairs are skipped,
+  // _kernels.py:160,168)
+  if (pairs_out) *pairs_out = (int64_t)(total_pairs - same);
   idx->have_cand = false;
   return SB_OK;
 }

@@ -109,6 +109,7 @@ __global__ void __launch_bounds__(kJoinThreads, U8 ? 3 : 2) join_emit_kernel(Joi
   em.base = 0;
   em.used = kEmitBlock;  // forces a reservation on first use
   const bool whole = a.dc >= a.m;  // all dimensions staged at once
+  unsigned same = 0;  // (x, y) slots holding one id twice (in both the new and the old list)
 
   for (;;) {
     __syncthreads();
@@ -233,6 +234,7 @@ __global__ void __launch_bounds__(kJoinThreads, U8 ? 3 : 2) join_emit_kernel(Joi
           bool valid = have && x < na && y < ns && y > x;
           int32_t j = valid ? s.slot_id[x] : 0;
           int32_t k = valid ? s.slot_id[y] : 0;
+          same += (valid && j == k) ? 1u : 0u;
           valid = valid && j != k;
           bool p1 = false, p2 = false;
           uint64_t k1 = 0, k2 = 0;
@@ -250,6 +252,7 @@ __global__ void __launch_bounds__(kJoinThreads, U8 ? 3 : 2) join_emit_kernel(Joi
         }
     }
   }
+  if (same) atomicAdd(a.same_pairs, (unsigned long long)same);
   // pad this warp's unused reservation
   const int lane = lane_id();
   if (em.used < kEmitBlock)

@@ -205,6 +205,7 @@ struct JoinArgs {
   unsigned long long* push_count;
   int64_t* row_cnt;
   int* overflow;
+  unsigned long long* same_pairs;  // pairs skipped because new[x] == old[y] (j == k)
   int spad, dc, ntiles_max;
   const uint8_t* F8;      // u8 rows (integer data in [0, 255]) or null: fp64 path
   const int32_t* nx8;     // exact |x|^2 of the u8 rows

@@ -31,10 +31,12 @@ def _build_pair(cfg, n):
     return X, A, QX, QA, m, g, og
 
 
-@pytest.mark.parametrize("cfg,overflow", [("cfg2", False), ("cfg3", True), ("cfg4", True),
-                                          ("cfg5c1000", False), ("cfg5c10", False)])
-def test_config_recipes_at_100k(cfg, overflow):
-    n = 100_000
+@pytest.mark.parametrize("cfg,n,overflow", [
+    ("cfg2", 100_000, False), ("cfg3", 100_000, False), ("cfg3", 20_000, True),
+    ("cfg4", 100_000, True), ("cfg5c1000", 100_000, False), ("cfg5c10", 100_000, False),
+    ("cfg5c1", 100_000, True)])
+def test_config_recipes_at_100k(cfg, n, overflow):
+    """(cfg 3 overflows at 20k, not at 100k: both are run.)"""
     X, A, QX, QA, m, g, og = _build_pair(cfg, n)
     # the descent took the same path (psi history gates the iteration count)
     assert g.build_log["psi_history"] == og.log["psi_history"]
