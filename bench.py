@@ -9,10 +9,16 @@ AUTO ground truth is >= 0.95).  Data are seeded synthetic stand-ins (tools/confi
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl mine|reference] [--config cfg2]
 
+N > 1 (torchrun, one rank per GPU): every rank holds a replica of the index and the 10k-query
+batch is split across the ranks (sharding.search_batch_sharded_device: each rank routes its
+block, one NCCL all-gather per output assembles the results on every GPU) — strong scaling,
+max-over-ranks device time.  The node-sharded exact ground truth (one all-gather exchange) is
+timed beside it.
+
 --impl reference times the reference's CPU implementation of the path (the oracle port in
-oracle/, the reference being Python + Numba) on all host cores over bounded samples of the
-same workload.  N > 1: replicas only (routing does not shard); every rank searches the full
-query batch on its own copy of the index, timed with CUDA events, max over ranks.
+oracle/; the reference is Python + Numba with no native code to build) on all host cores:
+it builds the HELP index of the same data on the CPU (timed: the CPU "HELP build s"), then
+routes bounded samples of the same queries at the same K*.  It never loads the B200 library.
 """
 
 from __future__ import annotations
@@ -35,6 +41,7 @@ sys.path.insert(0, ROOT)
 METRIC = "hybrid QPS @ recall@10>=0.95 (1 B200); HELP build s; HBM GB/s vs peak"
 UNIT = "queries/s"
 K_SWEEP = [10, 20, 25, 30, 50, 100, 200, 300, 500, 750, 1000, 1500, 2000, 3000, 4000]
+GAMMA = 100  # BuildParams defaults (graph.py:26-33)
 
 
 def parse_args():
@@ -48,7 +55,9 @@ def parse_args():
     p.add_argument("--kcap", type=int, default=4000)
     p.add_argument("--cpu-seconds", type=float, default=12.0)
     p.add_argument("--no-topk", action="store_true",
-                   help="skip the exhaustive top-k tensor-core rooflines (cfg 2 exact u8, cfg 4 TF32)")
+                   help="skip the exhaustive top-k tensor-core rooflines")
+    p.add_argument("--no-cpu-build", action="store_true",
+                   help="skip the CPU oracle build + graph parity of the mine arm")
     return p.parse_args()
 
 
@@ -57,6 +66,16 @@ def dist_env():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     return rank, world, local
+
+
+def cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
 
 
 # ---------------------------------------------------------------------------------------
@@ -128,8 +147,18 @@ def ncu_traffic(config_name):
 # ---------------------------------------------------------------------------------------
 def load_workload(args):
     from tools.configs import make_config
-    X, A, QX, QA, card = make_config(args.config, args.n)
-    return X, A, QX, QA, card
+    return make_config(args.config, args.n)
+
+
+def bench_config(args, n, m, l, card, q, kstar, pioneer, features_bytes):
+    """The workload description both arms print (identical dicts: same config)."""
+    return {
+        "workload": f"{args.config}: N={n:,} d={m} L={l} cards={list(card)} Q={q} k=10",
+        "operating_K": int(kstar), "pioneer": int(pioneer),
+        "index": "HELP gamma=100 gamma_new=100 sigma=0.44 psi_target=0.8 (BuildParams defaults)",
+        "l2": "inputs larger than L2 (features %.0f MB + adjacency %.0f MB vs 126 MB L2)"
+              % (features_bytes / 1e6, n * GAMMA * 8 / 1e6),
+    }
 
 
 def build_index(X, A, card):
@@ -173,16 +202,50 @@ def algorithmic_bytes(st, m, l, row_bytes=None, norm_bytes=0):
     return float((evals * (rb + norm_bytes + 4 * l) + 4 * (exps + scanned)).sum())
 
 
+def build_summary(g, build_s, n, m, l, cpu=None):
+    """HELP build: seconds, distance evaluations (n*gamma init + join pairs +
+    the psi ground truth's sample*n) per second, and the local join against the HBM roofline
+    by §8(d)'s gather figure n*(gamma_new+gamma)*(4d+4L) bytes per descent iteration."""
+    log = g.build_log
+    pairs = [int(p) for p in log.get("pairs", [])]
+    sample = 100 if n > 100 else n
+    evals = n * GAMMA + sum(pairs) + sample * n
+    t_iter = float(sum(log.get("seconds_iterations", [])))
+    gath = len(pairs) * n * (2 * GAMMA) * (4 * m + 4 * l)
+    peak, src = measured_hbm_peak()
+    out = {"gpu_s": round(build_s, 3), "iterations": log.get("iterations"),
+           "psi_history": log.get("psi_history"), "termination": log.get("termination"),
+           "pairs": pairs, "dist_evals": int(evals),
+           "gpu_dist_evals_per_s": round(evals / build_s, 1),
+           "seconds_init": round(log.get("seconds_init", 0.0), 4),
+           "seconds_iterations": [round(x, 4) for x in log.get("seconds_iterations", [])],
+           "seconds_prune": round(log.get("seconds_prune", 0.0), 4),
+           "prune_guard_rounds": log.get("prune_guard_rounds"),
+           "reinforce_overflow_rows": log.get("reinforce_overflow_rows"),
+           "join_roofline": {"bound": "hbm", "unit": "GB/s",
+                             "achieved": round(gath / t_iter / 1e9, 1) if t_iter else None,
+                             "peak": peak, "frac": round(gath / t_iter / 1e9 / peak, 4) if t_iter else None,
+                             "bytes_def": "SURVEY 8(d): n*(gamma_new+gamma)*(4d+4L) per descent iteration",
+                             "seconds": round(t_iter, 4), "peak_source": src,
+                             "join_pairs_per_s": round(sum(pairs) / t_iter, 1) if t_iter else None}}
+    if cpu:
+        out.update(cpu)
+        out["cpu_dist_evals_per_s"] = round(evals / cpu["cpu_s"], 1)
+        out["speedup_vs_cpu"] = round(cpu["cpu_s"] / build_s, 1)
+    return out
+
+
 # ---------------------------------------------------------------------------------------
 def run_mine(args, rank, world, local):
     import torch
     import paper_2604_01617_b200 as sb
+    from paper_2604_01617_b200 import sharding
     from paper_2604_01617_b200.device import entry_points_host
 
     torch.cuda.set_device(local)
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl")
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
 
     def barrier():
         if world > 1:
@@ -219,17 +282,24 @@ def run_mine(args, rank, world, local):
     dists_d = torch.empty((q, kstar), dtype=torch.float64, device="cuda")
     st_d = torch.empty((q, 5), dtype=torch.int64, device="cuda")
 
-    def step_dev(entries_ptr=None):
+    def step_full(entries_ptr=None):
         dev.route_dev(qf_d.data_ptr(), qa_d.data_ptr(), None, q, kstar, P, inv_alpha,
                       ids_d.data_ptr(), dists_d.data_ptr(), st_d.data_ptr(),
                       entries_ptr=entries_ptr, seed=0, qi0=0)
 
+    def step():
+        if world == 1:
+            step_full()
+            return ids_d
+        return sharding.search_batch_sharded_device(dev, qf_d, qa_d, q, kstar, P, inv_alpha)[0]
+
     for _ in range(max(3, args.warmup)):
-        step_dev()
+        out_ids = step()
     torch.cuda.synchronize()
-    # parity of the device-resident path with the public API at K*
+    # parity of the device path (sharded at N > 1) with the public API at K*
     ids_api, _, st_api = sb.search_batch_arrays(g, QX, QA, params)
-    assert np.array_equal(ids_d.cpu().numpy(), ids_api), "device-resident path != public API"
+    dev.set_stream(stream.cuda_stream)
+    assert np.array_equal(out_ids.cpu().numpy(), ids_api), "device path != public API"
     gpu_index = int(os.environ.get("CUDA_VISIBLE_DEVICES", str(local)).split(",")[local]) \
         if os.environ.get("CUDA_VISIBLE_DEVICES") else local
     sampler = ClockSampler(gpu_index)
@@ -241,7 +311,7 @@ def run_mine(args, rank, world, local):
     e1 = torch.cuda.Event(enable_timing=True)
     e0.record(stream)
     for _ in range(args.steps):
-        step_dev()
+        step()
     e1.record(stream)
     torch.cuda.synchronize()
     barrier()
@@ -249,19 +319,19 @@ def run_mine(args, rank, world, local):
     launches = dev.launch_count() - l0
     ms = e0.elapsed_time(e1) / args.steps
     ms = max_over_ranks(ms)
-    value = world * q / (ms / 1000.0)
+    value = q / (ms / 1000.0)  # the whole batch per step, split over the ranks
 
-    # ---- roofline: the routing kernel alone (entries precomputed), CUDA events ----------
+    # ---- roofline: the routing kernel alone over the full batch (entries precomputed) ----
     ent = entry_points_host(n, kstar, 0, 0, q)
     ent_d = torch.from_numpy(ent).cuda()
-    step_dev(ent_d.data_ptr())
+    step_full(ent_d.data_ptr())
     torch.cuda.synchronize()
     reps = max(3, min(args.steps, 10))
     r0 = torch.cuda.Event(enable_timing=True)
     r1 = torch.cuda.Event(enable_timing=True)
     r0.record(stream)
     for _ in range(reps):
-        step_dev(ent_d.data_ptr())
+        step_full(ent_d.data_ptr())
     r1.record(stream)
     torch.cuda.synchronize()
     route_ms = r0.elapsed_time(r1) / reps
@@ -281,26 +351,47 @@ def run_mine(args, rank, world, local):
     qf_h[:] = QX
     qa_h[:] = QA
     dev.set_stream(None)
+
+    def e2e_call():
+        if world == 1:
+            return sb.search_batch_arrays(g, qf_h, qa_h, params)
+        return sharding.search_batch_sharded(g, qf_h, qa_h, params)
+
     # warm-up: two live result sets, so the page-locked result pool holds the two sets the
     # timed loop alternates between (no allocation inside the timed region)
-    warm = [sb.search_batch_arrays(g, qf_h, qa_h, params) for _ in range(2)]
+    warm = [e2e_call() for _ in range(2)]
     del warm
     barrier()
     t0 = time.perf_counter()
     for _ in range(args.steps):
-        ids_h, dists_h, st_h = sb.search_batch_arrays(g, qf_h, qa_h, params)
+        ids_h, dists_h, st_h = e2e_call()
     e2e_s = (time.perf_counter() - t0) / args.steps
     e2e_s = max_over_ranks(e2e_s)
-    e2e = world * q / e2e_s
+    e2e = q / e2e_s
     h2d = qf_h.nbytes + qa_h.nbytes
     d2h = ids_h.nbytes + dists_h.nbytes + st_h.nbytes
 
-    # ---- CPU baseline: the oracle port, one thread (the reference's search is
-    # single-threaded), bounded sample of the same queries -------------------
+    # ---- N > 1: the node-sharded exact ground truth (one all-gather exchange) -------------
+    sharded_gt = None
+    if world > 1:
+        sharding.oracle_auto_topk_sharded(X, A, QX[:256], QA[:256], 10, cfg)  # warm
+        barrier()
+        t0 = time.perf_counter()
+        si, _ = sharding.oracle_auto_topk_sharded(X, A, QX, QA, 10, cfg)
+        gs = max_over_ranks(time.perf_counter() - t0)
+        sharded_gt = {"seconds": round(gs, 4), "queries": q, "k": 10,
+                      "equal_to_single_gpu": bool(np.array_equal(si, gt))}
+
     cpu = None
     topk = None
+    cpu_build = None
+    parity = None
     if rank == 0 and world == 1:
+        # CPU baseline: the oracle port, one thread (the reference's search is single-threaded,
+        # SPEC.md:466), bounded sample of the same queries
         cpu = cpu_baseline(g, cfg, QX, QA, kstar, args.cpu_seconds, ids_api)
+        if not args.no_cpu_build:
+            cpu_build, parity = cpu_build_and_parity(g, cfg, X, A, QX, QA, gt)
         if not args.no_topk:
             topk = topk_rooflines(g, cfg, QX, QA)
 
@@ -308,21 +399,15 @@ def run_mine(args, rank, world, local):
         line = {
             "metric": METRIC, "value": round(value, 1), "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 4),
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "higher_is_better": True, "scaling": "strong" if world > 1 else "weak",
+            "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (seeded generator with the config's shapes; tools/configs.py)",
-            "config": {
-                "workload": f"{args.config}: N={n:,} d={m} L={l} cards={list(card)} Q={q} k=10",
-                "operating_K": kstar, "pioneer": P, "recall_at_10": table[-1]["recall_at_10"],
-                "index": "HELP gamma=100 sigma=0.44 psi_target=0.8 (BuildParams defaults)",
-                "parallelism": "replicas" if world > 1 else "single",
-                "l2": "inputs larger than L2 (features %.0f MB + adjacency %.0f MB vs 126 MB L2)"
-                      % (X.nbytes / 1e6, n * 100 * 8 / 1e6),
-            },
+            "config": bench_config(args, n, m, l, card, q, kstar, P, X.nbytes),
+            "parallelism": "queries split over %d replicas, NCCL all-gather of results" % world
+                           if world > 1 else "single GPU",
+            "recall_at_10": table[-1]["recall_at_10"],
             "build_s": round(build_s, 3),
-            "build_log": {k: v for k, v in g.build_log.items()
-                          if k in ("iterations", "psi_history", "termination", "seconds_init",
-                                   "seconds_iterations", "seconds_prune", "pairs",
-                                   "reinforce_overflow_rows", "prune_guard_rounds")},
+            "build": build_summary(g, build_s, n, m, l, cpu_build),
             "edges": int(g.nbr_counts.sum()),
             "gt_s": round(gt_s, 3),
             "sweep": table,
@@ -336,12 +421,14 @@ def run_mine(args, rank, world, local):
                          "frac_of_bytes_read": round(read_bytes / (route_ms / 1000.0) / 1e9 / peak, 4),
                          "kernel_ms": round(route_ms, 4),
                          "algorithmic_bytes_per_launch": abytes, "peak_source": peak_src,
-                         "share_of_step": round(route_ms / ms, 3)},
+                         "share_of_step": round(route_ms / ms, 3) if world == 1 else None},
             "e2e": {"value": round(e2e, 1), "unit": UNIT, "h2d_bytes_per_step": int(h2d),
                     "d2h_bytes_per_step": int(d2h)},
             "gpu_launches": int(launches),
             "clocks": clocks,
             "cpu_baseline": cpu,
+            "parity": parity,
+            "sharded_ground_truth": sharded_gt,
             "roofline_topk": topk,
         }
         print(json.dumps(line), flush=True)
@@ -350,9 +437,55 @@ def run_mine(args, rank, world, local):
         dist.destroy_process_group()
 
 
-def tf32_peak_tflops():
-    """cuBLAS dense TF32 throughput measured here (8192^3, best of 10): the roofline denominator
-    for the TF32 filter (MEASURED_PEAKS.json holds bf16 only)."""
+def cpu_build_and_parity(g, cfg, X, A, QX, QA, gt):
+    """The CPU oracle (parallel restatement of the reference's loops, all host cores) builds
+    the same index; its graph must equal the GPU's bit for bit.  The exact ground truth is
+    cross-checked on a 100-query sample."""
+    from oracle import oracle as O
+    t0 = time.perf_counter()
+    og = O.build(X, A, cfg.alpha, sigma=0.44, gamma=GAMMA, gamma_new=GAMMA, nthreads=0)
+    cpu_s = time.perf_counter() - t0
+    mask = np.arange(g.nbr_ids.shape[1])[None, :] < og.nbr_counts[:, None]
+    equal = bool(np.array_equal(g.nbr_counts, og.nbr_counts) and
+                 np.array_equal(np.where(mask, g.nbr_ids, -1), np.where(mask, og.nbr_ids, -1)) and
+                 np.array_equal(np.where(mask, g.nbr_dists, 0), np.where(mask, og.nbr_dists, 0)))
+    s = min(100, QX.shape[0])
+    t0 = time.perf_counter()
+    gt_ok = all(np.array_equal(O.oracle_auto_topk(X, A, QX[i], QA[i], 10, cfg.alpha), gt[i])
+                for i in range(s))
+    build = {"cpu_s": round(cpu_s, 2), "cpu_threads": os.cpu_count(), "cpu_model": cpu_model(),
+             "cpu_kind": "port (oracle/stable_oracle.c parallel restatement, exact)",
+             "graph_equal_to_cpu": equal}
+    parity = {"graph_equal_to_cpu_oracle": equal, "edges_cpu": int(og.nbr_counts.sum()),
+              "gt_parity_on_sample": bool(gt_ok), "gt_sample_queries": s,
+              "gt_check_s": round(time.perf_counter() - t0, 2)}
+    return build, parity
+
+
+def peak_int8_tops():
+    """Dense INT8 tensor throughput measured here: torch._int_mm 8192^3 (cuBLASLt, s8 x s8 ->
+    s32), best of 10 (2 N^3 ops)."""
+    import torch
+    n = 8192
+    a = torch.randint(-64, 64, (n, n), dtype=torch.int8, device="cuda")
+    b = torch.randint(-64, 64, (n, n), dtype=torch.int8, device="cuda")
+    for _ in range(3):
+        torch._int_mm(a, b)
+    best = 1e30
+    for _ in range(10):
+        s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s0.record()
+        torch._int_mm(a, b)
+        s1.record()
+        s1.synchronize()
+        best = min(best, s0.elapsed_time(s1) / 1e3)
+    del a, b
+    return 2 * n ** 3 / best / 1e12
+
+
+def peak_tf32_tflops():
+    """Dense TF32 tensor throughput measured here: cuBLAS fp32 8192^3 with TF32 allowed, best
+    of 10 (MEASURED_PEAKS.json holds bf16 only)."""
     import torch
     old = torch.backends.cuda.matmul.allow_tf32
     torch.backends.cuda.matmul.allow_tf32 = True
@@ -374,68 +507,51 @@ def tf32_peak_tflops():
     return 2 * n ** 3 / best / 1e12
 
 
-def topk_rooflines(g, cfg, QX, QA):
-    """Exhaustive AUTO top-k (oracle_auto_topk, evaluate.py:32-55) on the tensor cores:
-    (1) this config's ground truth (cfg 2: u8 operands, tcgen05 kind::i8, exact);
-    (2) a cfg 4-shaped workload (N=1M, d=960 Gamma(2,1) x exp(U[-1,1]) per dimension, 2
-    attributes 2/50, 1,000 queries, k=10; data drawn on the GPU with a seeded torch generator)
-    on the TF32 filter path.  achieved = 2 q n d useful ops / the tensor-core pass (CUDA events
-    inside the C ABI: seed + full launch); the exact re-rank is reported beside it."""
-    import torch
-    import paper_2604_01617_b200 as sb
-    from paper_2604_01617_b200.device import DeviceIndex
-    out = {}
-    dev = g.device()
-    q, n, m = QX.shape[0], g.features.shape[0], g.features.shape[1]
-    dev.bf_topk_queries(QX, QA, 10, cfg.alpha)
+def _topk_entry(dev, QX, QA, k, alpha, n, m, peak, unit, peak_src):
+    dev.bf_topk_queries(QX, QA, k, alpha)
     best = (1e30, 0.0)
     for _ in range(3):
         t0 = time.perf_counter()
-        dev.bf_topk_queries(QX, QA, 10, cfg.alpha)
+        dev.bf_topk_queries(QX, QA, k, alpha)
         call = time.perf_counter() - t0
         best = min(best, (dev.bf_info()["kernel_ms"], call))
     info = dev.bf_info()
-    tops = 2.0 * q * n * m / (best[0] / 1e3) / 1e12
-    out["bench_config"] = {"path": info["path"], "queries": q, "nodes": n, "d": m, "k": 10,
-                           "kernel_ms": round(best[0], 4), "call_ms": round(best[1] * 1e3, 3),
-                           "achieved": round(tops, 1), "unit": "TOP/s",
-                           "peak": 4500.0, "frac": round(tops / 4500.0, 4),
-                           "peak_source": "nominal B200 dense int8 (no measured int8 peak here)"}
-    # cfg 4 shape on the TF32 filter path
-    gen = torch.Generator(device="cuda").manual_seed(0)
-    n4, d4, q4 = 1_000_000, 960, 1000
-    scale = torch.exp(torch.rand(d4, device="cuda", generator=gen) * 2 - 1)
-    conc = torch.full((n4 + q4, d4), 2.0, device="cuda")
-    xg = torch._standard_gamma(conc, generator=gen) * scale
-    del conc
-    X4 = xg[:n4].float().cpu().numpy()
-    Q4 = xg[n4:].double().cpu().numpy()
-    del xg
-    A4 = np.stack([torch.randint(1, 3, (n4,), generator=gen, device="cuda").cpu().numpy(),
-                   torch.randint(1, 51, (n4,), generator=gen, device="cuda").cpu().numpy()],
-                  axis=1).astype(np.int32)
-    QA4 = np.stack([np.random.default_rng(4).integers(1, 3, q4), np.random.default_rng(5).integers(1, 51, q4)], axis=1)
-    cfg4 = sb.compute_alpha(sb.sample_statistics(X4, A4, 1000, seed=0), n4, 2)
-    d4i = DeviceIndex(X4, A4, 2)
-    d4i.bf_topk_queries(Q4, QA4, 10, cfg4.alpha)
-    best = (1e30, 0.0)
-    for _ in range(3):
-        t0 = time.perf_counter()
-        d4i.bf_topk_queries(Q4, QA4, 10, cfg4.alpha)
-        call = time.perf_counter() - t0
-        best = min(best, (d4i.bf_info()["kernel_ms"], call))
-    info = d4i.bf_info()
-    peak = tf32_peak_tflops()
-    tfl = 2.0 * q4 * n4 * d4 / (best[0] / 1e3) / 1e12
-    out["cfg4_tf32"] = {"path": info["path"], "queries": q4, "nodes": n4, "d": d4, "k": 10,
-                        "kernel_ms": round(best[0], 4), "call_ms": round(best[1] * 1e3, 3),
-                        "candidates_per_query": round(info["candidates"] / q4, 1),
-                        "fallback_queries": info["fallback_queries"],
-                        "achieved": round(tfl, 1), "unit": "TFLOP/s", "peak": round(peak, 1),
-                        "frac": round(tfl / peak, 4),
-                        "peak_source": "measured here: cuBLAS TF32 8192^3 best of 10",
-                        "frac_of_nominal_1100": round(tfl / 1100.0, 4)}
-    d4i.close()
+    q = QX.shape[0]
+    rate = 2.0 * q * n * m / (best[0] / 1e3) / 1e12
+    return {"path": info["path"], "queries": q, "nodes": n, "d": m, "k": k,
+            "kernel_ms": round(best[0], 4), "call_ms": round(best[1] * 1e3, 3),
+            "candidates_per_query": round(info["candidates"] / q, 1),
+            "fallback_queries": info["fallback_queries"],
+            "achieved": round(rate, 1), "unit": unit, "peak": round(peak, 1),
+            "frac": round(rate / peak, 4), "peak_source": peak_src}
+
+
+def topk_rooflines(g, cfg, QX, QA):
+    """Exhaustive AUTO top-k (oracle_auto_topk, evaluate.py:32-55) on the tensor cores, each
+    against the measured dense peak of its precision: this config's ground truth (cfg 2: u8
+    operands, tcgen05 kind::i8, exact; INT8 peak), cfg 3 at k = 10 and k = 100 and cfg 4 (both
+    from the tools/configs.py recipes) on the TF32 filter + exact re-rank (TF32 peak).
+    achieved = 2 q n d useful ops / the tensor-core pass (CUDA events inside the C ABI)."""
+    import paper_2604_01617_b200 as sb
+    from paper_2604_01617_b200.device import DeviceIndex
+    from tools.configs import make_config
+    i8 = peak_int8_tops()
+    tf = peak_tf32_tflops()
+    i8_src = "measured here: torch._int_mm s8 8192^3 best of 10"
+    tf_src = "measured here: cuBLAS TF32 8192^3 best of 10"
+    out = {"peaks": {"int8_tops": round(i8, 1), "tf32_tflops": round(tf, 1)}}
+    dev = g.device()
+    n, m = g.features.shape
+    out["bench_config"] = _topk_entry(dev, QX, QA, 10, cfg.alpha, n, m, i8, "TOP/s", i8_src)
+    for name, ks in (("cfg3", (10, 100)), ("cfg4", (10,))):
+        X, A, QXc, QAc, _ = make_config(name)
+        mc = sb.compute_alpha(sb.sample_statistics(X, A, 1000, seed=0), X.shape[0], A.shape[1])
+        d = DeviceIndex(X, A, 2)
+        for k in ks:
+            out[f"{name}_k{k}"] = _topk_entry(d, QXc, QAc, k, mc.alpha, X.shape[0], X.shape[1],
+                                              tf, "TFLOP/s", tf_src)
+        d.close()
+        del X, A
     return out
 
 
@@ -456,6 +572,7 @@ def cpu_baseline(g, cfg, QX, QA, kstar, seconds, ids_gpu):
     s = int(min(QX.shape[0], max(8, seconds / per)))
     dt, ids = run(0, s, 1)
     return {"value": round(s / dt, 2), "unit": UNIT, "cores": 1, "kind": "port",
+            "cpu_model": cpu_model(),
             "sample": f"first {s} of {QX.shape[0]} queries at K={kstar}, single thread "
                       f"(oracle/stable_oracle.c route + NumPy entry points, as search() does)",
             "parity_with_gpu_on_sample": bool(np.array_equal(ids, ids_gpu[:s]))}
@@ -463,26 +580,36 @@ def cpu_baseline(g, cfg, QX, QA, kstar, seconds, ids_gpu):
 
 # ---------------------------------------------------------------------------------------
 def run_reference(args, rank, world, local):
-    """The reference's CPU path (oracle port) on all host cores, bounded samples per step."""
+    """The reference's CPU path (oracle port) on all host cores: the HELP build of the same
+    data (timed), then bounded samples of the same queries routed at the same K*.  Nothing
+    here loads the B200 library."""
     if rank != 0:
         return
-    import paper_2604_01617_b200 as sb
     from oracle import oracle as O
+    from tools.configs import OPERATING_K
 
     X, A, QX, QA, card = load_workload(args)
-    # setup (untimed): the HELP index the CPU path searches.  Built on the GPU because the
-    # CPU build takes ~40 min at N=1M; the device build is bit-identical to the reference's
-    # (tests/test_gpu_parity.py), so the CPU search below runs on the reference's own graph.
-    g, cfg, _ = build_index(X, A, card)
-    kstar, table, _, _ = sweep_operating_point(g, cfg, X, A, QX, QA, args.kcap)
+    n, m = X.shape
+    l = A.shape[1]
     threads = os.cpu_count() or 1
-    n = X.shape[0]
+    s_v, s_a = O.sample_statistics(X, A, min(1000, n), seed=0)
+    alpha = O.compute_alpha(s_v, s_a, n, l)
+    t0 = time.perf_counter()
+    g = O.build(X, A, alpha, sigma=0.44, gamma=GAMMA, gamma_new=GAMMA, nthreads=0)
+    build_s = time.perf_counter() - t0
+    kstar = OPERATING_K.get(args.config, 100) if args.n is None else min(n, 200)
+    P = max(1, kstar // 2)
 
     def step(lo, hi):
         ent = np.stack([O.entry_points(n, kstar, 0, qi) for qi in range(lo, hi)])
-        O.search_batch(g.features, g.attrs, g.nbr_ids, g.nbr_counts, cfg.alpha, QX[lo:hi],
-                       QA[lo:hi], kstar, nthreads=threads, entries=ent)
+        return O.search_batch(X, A, g.nbr_ids, g.nbr_counts, alpha, QX[lo:hi], QA[lo:hi], kstar,
+                              nthreads=threads, entries=ent)
 
+    # recall at K* on a 100-query sample against the oracle's exact ground truth
+    s_rec = min(100, QX.shape[0])
+    ids_s, _, _ = step(0, s_rec)
+    rec = float(np.mean([O.recall_at_k(ids_s[i], O.oracle_auto_topk(X, A, QX[i], QA[i], 10, alpha), 10)
+                         for i in range(s_rec)]))
     t0 = time.perf_counter()
     step(0, min(QX.shape[0], 4 * threads))
     per = (time.perf_counter() - t0) / min(QX.shape[0], 4 * threads)
@@ -502,11 +629,18 @@ def run_reference(args, rank, world, local):
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": round(dt * 1000, 3), "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": f"{args.config}: N={n:,} d={X.shape[1]} L={A.shape[1]} "
-                               f"Q={QX.shape[0]} k=10", "operating_K": kstar},
+        "config": bench_config(args, n, m, l, card, QX.shape[0], kstar, P, X.nbytes),
+        "parallelism": f"{threads} host threads",
+        "recall_at_10_sample": round(rec, 4), "recall_sample_queries": s_rec,
+        "build_s": round(build_s, 2),
+        "build": {"cpu_s": round(build_s, 2), "cpu_threads": threads, "cpu_model": cpu_model(),
+                  "iterations": g.log["iterations"], "psi_history": g.log["psi_history"],
+                  "pairs": g.log["pairs"], "edges": int(g.nbr_counts.sum())},
         "cpu_baseline": {"value": round(value, 2), "unit": UNIT, "cores": threads, "kind": "port",
+                         "cpu_model": cpu_model(),
                          "sample": f"{s} queries per step at K={kstar}, {threads} threads "
-                                   "(oracle/stable_oracle.c route + NumPy entry points)"},
+                                   "(oracle/stable_oracle.c route + NumPy entry points) on the "
+                                   "HELP graph the CPU built"},
         "e2e": {"value": round(value, 2), "unit": UNIT, "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }

@@ -176,12 +176,14 @@ int64_t sb_launch_count(sb_index* idx);
  * sb_bf_topk_queries ran on the tensor cores (tcgen05). */
 int sb_index_info(sb_index* idx, int32_t* int_exact, double* fmax_abs, int32_t* last_bf_tc);
 /* distance evaluation order for routing and exhaustive top-k: 0 = automatic (order-free
- * exact paths for integer data: u8/dp4a or fp32 routing rows, tensor-core top-k), 1 = always
+ * exact paths for integer data: u8/dp4a or fp32 routing rows, tensor-core top-k; the
+ * certified fp32 routing filter for real-valued data), 1 = always
  * the sequential fp64 order of _query_dist (_kernels.py:26-35).  Both are bit-exact. */
 int sb_set_distance_mode(sb_index* idx, int32_t mode);
 /* the last sb_route_batch / sb_route_batch_dev on this handle: *path = 0 fp64 rows (d % 4 == 0),
  * 1 fp32 rows (integer data), 2 fp32 lane groups, 3 fp64 generic, 4 u8 rows with dp4a (integer
- * data in [0, 255]); *row_bytes = bytes read per feature row evaluated */
+ * data in [0, 255]), 5 certified fp32 filter + exact fp64 rows for the survivors (real-valued
+ * data, d % 4 == 0); *row_bytes = bytes read per feature row evaluated */
 int sb_route_info(sb_index* idx, int32_t* path, int32_t* row_bytes);
 /* the last sb_bf_topk_queries on this handle: *path = 0 exact fp64 kernel, 1 tcgen05 with exact
  * integer products (integer data), 2 tcgen05 TF32 filter with a certified error bound + exact

@@ -1702,6 +1702,16 @@ static int route_dev(sb_index* idx, const double* qf, const double* qa, const do
   if (const char* e = getenv("SB_ROUTE_LPR")) a.lpr = std::max(1, std::min(32, next_pow2(atoi(e))));
   a.pf_rows = 1;
   if (const char* e = getenv("SB_ROUTE_PF")) a.pf_rows = atoi(e);
+  // real-valued rows: certified fp32 filter (coalesced, lanes split each row) in front of the
+  // exact sequential fp64 evaluation of the rows that can still enter the result list
+  // (route.cu kModeF64Filt); SB_ROUTE_FILT=0 evaluates every row exactly
+  {
+    const int nq = idx->m / 4;
+    int lpr = 8;
+    while (lpr < 32 && lpr * 4 < nq) lpr *= 2;
+    a.flt_lpr = (idx->m % 4 == 0 && !idx->force_sequential) ? lpr : 0;
+    if (const char* e = getenv("SB_ROUTE_FILT")) a.flt_lpr = atoi(e) != 0 ? a.flt_lpr : 0;
+  }
   // integer features in [0, 255]: route over a u8 copy with dp4a dot products (exact), unless
   // SB_ROUTE_U8=0; built once per layout
   a.F8 = nullptr;

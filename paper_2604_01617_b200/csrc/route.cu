@@ -146,11 +146,24 @@ SB_DEV double finish_pre(const RouteArgs& a, const WarpSmem& w, uint32_t node, c
 
 // distance path of a route_kernel instance (each instance carries only its own path, plus the
 // generic fp64 path as the per-query fallback of the integer paths)
-enum RouteMode { kModeF64x4 = 0, kModeF32Lane = 1, kModeF32Split = 2, kModeGeneric = 3, kModeU8 = 4 };
+enum RouteMode { kModeF64x4 = 0, kModeF32Lane = 1, kModeF32Split = 2, kModeGeneric = 3, kModeU8 = 4,
+                 kModeF64Filt = 5 };
 
-// Exact distances of rows cid[0..c) -> cd[0..c).
+// attribute factor of _query_dist's finish: 1 + s_a * inv_alpha, computed exactly as
+// finish_row does (_kernels.py:32-35)
+SB_DEV double attr_factor(const RouteArgs& a, const WarpSmem& w, uint32_t v) {
+  const int32_t* av = a.A + (int64_t)v * a.l;
+  double sa = 0.0;
+  for (int u = 0; u < a.l; ++u)
+    sa = dadd(sa, dmul(w.qms[u], fabs(dsub((double)__ldg(av + u), w.qas[u]))));
+  return dadd(1.0, dmul(sa, a.inv_alpha));
+}
+
+// Exact distances of rows cid[0..c) -> cd[0..c).  tau: the admission tail of the result list
+// (+inf while the entries fill it); qn: |q| (fp64), both used only by the filtered path.
 template <int MODE>
-SB_DEV void eval_rows(const RouteArgs& a, WarpSmem& w, int c, bool f32, int nq8) {
+SB_DEV void eval_rows(const RouteArgs& a, WarpSmem& w, int c, bool f32, int nq8, double tau,
+                      double qn) {
   const int lane = lane_id();
   if (MODE == kModeU8 && f32) {
     // features and query are integers in [0, 255]: rows are read from the u8 copy and
@@ -281,10 +294,83 @@ SB_DEV void eval_rows(const RouteArgs& a, WarpSmem& w, int c, bool f32, int nq8)
           if (id[g] != 0xFFFFFFFFu) w.cd[base + grp + rpp * g] = finish_row(a, w, id[g], (double)acc[g]);
       }
     }
-  } else if (MODE == kModeF64x4) {
+  } else if (MODE == kModeF64x4 || MODE == kModeF64Filt) {
     const int nq = a.m >> 2;
-    for (int j = lane; j < c; j += 32) {
+    int ns = c;  // rows that need the exact value: all, or the filter's survivors (w.cpos)
+    const bool filt = MODE == kModeF64Filt && tau < __longlong_as_double(0x7FF0000000000000ll);
+    if (filt) {
+      // (1) Certified lower bound per row from fp32 arithmetic with coalesced loads: lpr lanes
+      // split each row (float4 k = sub, sub + lpr, ...), two rows per lane group in flight.
+      // With u = 2^-24, e_t = fl32(x_t - fl32(q_t)) and S~ = the fp32 sum of e_t^2:
+      //   |q - x| >= sqrt(S~ (1 - (m + 64) u)) (1 - u) - u |q|     (summation error of at most
+      //   m + 64 additions per chain, the rounding of x - q and of q to fp32),
+      // and the reference's fp64 value U = fl(sqrt(S_seq) * f) >= |q - x| f (1 - (m + 8) 2^-52)
+      // with the same attribute factor f.  A row whose bound exceeds tau cannot enter R (nor
+      // the pioneer list, a prefix of R), so its exact value is never needed; every other row
+      // gets the exact sequential fp64 value below.  Ids, distances and counters are unchanged.
+      const int lpr = a.flt_lpr;
+      const int G = 32 / lpr;
+      const int sub = lane & (lpr - 1), grp = lane / lpr;
+      const float4* F4 = reinterpret_cast<const float4*>(a.F);
+      const float4* Q4 = reinterpret_cast<const float4*>(w.qs32);
+      const double uu = 5.9604644775390625e-08;  // 2^-24
+      const double shrink = 1.0 - (a.m + 64) * uu;
+      const double fin = 1.0 - (a.m + 8) * 2.220446049250313e-16;
+      for (int base = 0; base < c; base += 2 * G) {
+        const int r0 = base + grp, r1 = base + G + grp;
+        const uint32_t v0 = r0 < c ? w.cid[r0] : 0u, v1 = r1 < c ? w.cid[r1] : 0u;
+        float s0a = 0.f, s0b = 0.f, s1a = 0.f, s1b = 0.f;
+        const float4* x0p = F4 + (int64_t)v0 * nq;
+        const float4* x1p = F4 + (int64_t)v1 * nq;
+#pragma unroll 4
+        for (int k = sub; k < nq; k += lpr) {
+          const float4 qv = Q4[k];
+          const float4 x0 = r0 < c ? __ldg(x0p + k) : qv;
+          const float4 x1 = r1 < c ? __ldg(x1p + k) : qv;
+          float d;
+          d = x0.x - qv.x; s0a = fmaf(d, d, s0a);
+          d = x0.y - qv.y; s0b = fmaf(d, d, s0b);
+          d = x0.z - qv.z; s0a = fmaf(d, d, s0a);
+          d = x0.w - qv.w; s0b = fmaf(d, d, s0b);
+          d = x1.x - qv.x; s1a = fmaf(d, d, s1a);
+          d = x1.y - qv.y; s1b = fmaf(d, d, s1b);
+          d = x1.z - qv.z; s1a = fmaf(d, d, s1a);
+          d = x1.w - qv.w; s1b = fmaf(d, d, s1b);
+        }
+        float t0 = s0a + s0b, t1 = s1a + s1b;
+        for (int o = lpr >> 1; o > 0; o >>= 1) {
+          t0 += __shfl_xor_sync(0xffffffffu, t0, o);
+          t1 += __shfl_xor_sync(0xffffffffu, t1, o);
+        }
+        if (sub == 0) {
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const int r = h ? r1 : r0;
+            if (r >= c) continue;
+            const double S = (double)(h ? t1 : t0);
+            double rl = sqrt(S * shrink) * (1.0 - uu) - uu * qn;
+            rl = rl > 0.0 ? rl : 0.0;
+            const double lo = rl * attr_factor(a, w, h ? v1 : v0) * fin;
+            w.cd[r] = lo > tau ? __longlong_as_double(0x7FF0000000000000ll) : -1.0;
+          }
+        }
+      }
+      __syncwarp();
+      // survivors -> w.cpos[0..ns)
+      ns = 0;
+      for (int b = 0; b < c; b += 32) {
+        const int j = b + lane;
+        const bool need = j < c && w.cd[j] < 0.0;
+        const unsigned bal = __ballot_sync(0xffffffffu, need);
+        if (need) w.cpos[ns + __popc(bal & ((1u << lane) - 1u))] = j;
+        ns += __popc(bal);
+      }
+      __syncwarp();
+    }
+    for (int t = lane; t < ns; t += 32) {
+      const int j = filt ? w.cpos[t] : t;
       const uint32_t v = w.cid[j];
+
       const float4* vx = reinterpret_cast<const float4*>(a.F) + (int64_t)v * nq;
       AttrPre pre;
       attr_preload(a, v, pre);
@@ -458,6 +544,11 @@ __global__ void __launch_bounds__(256, LAZY ? 2 : ROUTE_MIN_CTAS) route_kernel(R
       qhi = fmaxf(qhi, __shfl_xor_sync(0xffffffffu, qhi, o));
     }
     integral = __all_sync(0xffffffffu, integral);
+    double qn = 0.0;  // |q|, rounded up (the filtered fp64 path's bound)
+    if (MODE == kModeF64Filt) {
+      for (int t = lane; t < a.m; t += 32) qn += w.qs[t] * w.qs[t];
+      qn = sqrt(warp_sum(qn)) * (1.0 + 1e-12);
+    }
     bool f32 = false;
     int nq8 = 0;
     if ((MODE == kModeF32Lane || MODE == kModeF32Split) && integral) {
@@ -721,7 +812,9 @@ __global__ void __launch_bounds__(256, LAZY ? 2 : ROUTE_MIN_CTAS) route_kernel(R
           }
         }
       }
-      if (c > 0) eval_rows<MODE>(a, w, c, f32, nq8);
+      if (c > 0)
+        eval_rows<MODE>(a, w, c, f32, nq8,
+                        stage == 0 ? __longlong_as_double(0x7FF0000000000000ll) : w.rd[K - 1], qn);
       if (stage == 0) {
         for (int t = lane; t < c; t += 32) {
           w.rd[ent_pos + t] = w.cd[t];
@@ -840,7 +933,8 @@ static int launch_route_t(const RouteArgs& a, int warps_per_cta, int ctas, size_
 static int route_mode(const RouteArgs& a) {
   if (a.F8) return kModeU8;
   if (a.f32_ok) return a.lpr == 1 ? kModeF32Lane : kModeF32Split;
-  return (a.m & 3) == 0 ? kModeF64x4 : kModeGeneric;
+  if ((a.m & 3) == 0) return a.flt_lpr > 0 ? kModeF64Filt : kModeF64x4;
+  return kModeGeneric;
 }
 
 int route_path(const RouteArgs& a) { return route_mode(a); }
@@ -849,6 +943,7 @@ int launch_route(const RouteArgs& a, int warps_per_cta, int ctas, cudaStream_t s
   size_t smem = route_smem_per_warp(a) * warps_per_cta;
   switch (route_mode(a)) {
     case kModeF64x4: return launch_route_t<kModeF64x4>(a, warps_per_cta, ctas, smem, st);
+    case kModeF64Filt: return launch_route_t<kModeF64Filt>(a, warps_per_cta, ctas, smem, st);
     case kModeF32Lane: return launch_route_t<kModeF32Lane>(a, warps_per_cta, ctas, smem, st);
     case kModeF32Split: return launch_route_t<kModeF32Split>(a, warps_per_cta, ctas, smem, st);
     case kModeU8: return launch_route_t<kModeU8>(a, warps_per_cta, ctas, smem, st);
@@ -869,6 +964,7 @@ int route_occupancy(const RouteArgs& a, int warps_per_cta, size_t smem, int* cta
   const bool lz = route_lazy(a);
   switch (route_mode(a)) {
     case kModeF64x4: return route_occupancy_t<kModeF64x4>(warps_per_cta, smem, ctas_per_sm, lz);
+    case kModeF64Filt: return route_occupancy_t<kModeF64Filt>(warps_per_cta, smem, ctas_per_sm, lz);
     case kModeF32Lane: return route_occupancy_t<kModeF32Lane>(warps_per_cta, smem, ctas_per_sm, lz);
     case kModeF32Split: return route_occupancy_t<kModeF32Split>(warps_per_cta, smem, ctas_per_sm, lz);
     case kModeU8: return route_occupancy_t<kModeU8>(warps_per_cta, smem, ctas_per_sm, lz);

@@ -34,6 +34,9 @@ struct RouteArgs {
   int f32_ok;
   float flo, fhi;
   int lpr;
+  // real-valued data (m % 4 == 0): lanes per row of the certified fp32 filter in front of the
+  // exact fp64 rows (8, 16 or 32); 0 = every row exact (no filter)
+  int flt_lpr;
   int pf_rows;  // prefetch each batch's rows into L2 before evaluating
   // u8 copy of integer features in [0, 255] (null: not available) and exact |x|^2
   const uint8_t* F8;

@@ -1,9 +1,10 @@
 """Multi-GPU execution of the hot path: one process per GPU.
 
-* Routing shards QUERIES (replicas of the index, no collective on the data path): rank r
-  routes its contiguous block of queries with their global query indices (so entry points
-  are those of the single-GPU run, router.py:42-45), and the results are gathered in rank
-  order.  Output is identical to the single-GPU ``search_batch``.
+* Routing shards QUERIES over replicas of the index: rank r routes its contiguous block of
+  queries with their global query indices (so entry points are those of the single-GPU run,
+  router.py:42-45), and the results are gathered in rank order (``search_batch_sharded`` for
+  host arrays; ``search_batch_sharded_device`` keeps queries, results and the all-gather on
+  the GPUs).  Output is identical to the single-GPU ``search_batch``.
 * Exhaustive AUTO top-k shards the NODES: each rank keeps an exact local top-k over its node
   range (global ids), then ONE exchange step (all-gather of q x k (dist, id) lists) and a
   merge by (dist, id) give the exact global top-k of ``oracle_auto_topk``
@@ -82,6 +83,44 @@ def search_batch_sharded(graph, query_features, query_attrs, params, masks=None,
     ids, dists, stats = route_fn(qf[lo:hi], qa[lo:hi], mk, lo)
     parts = [all_gather_rows(np.asarray(x), group) for x in (ids, dists, stats)]
     return tuple(np.concatenate(p, axis=0) for p in parts)
+
+
+def search_batch_sharded_device(dev, qf_d, qa_d, q: int, k: int, pioneer: int, inv_alpha: float,
+                                qm_d=None, seed: int = 0, group=None, use_coarse: bool = True):
+    """search_batch with the queries split across ranks, everything on the device.
+
+    qf_d / qa_d (/ qm_d): the full q-row query batch as float64 CUDA tensors on every rank;
+    ``dev`` is this rank's DeviceIndex (a replica of the index), launching on the current torch
+    stream.  Rank r routes rows [r*cap, min(q, (r+1)*cap)) with cap = ceil(q / world) and their
+    global query indices (so entry points are the single-GPU run's, router.py:42-45); one
+    all_gather_into_tensor per output (NCCL over NVLink) assembles the results in rank order.
+    Returns CUDA tensors (ids int64 q x k, dists float64 q x k, stats int64 q x 5), identical to
+    the single-GPU call."""
+    import torch
+    import torch.distributed as dist
+    rank, world = comm(group)
+    cap = (q + world - 1) // world
+    lo = min(q, rank * cap)
+    hi = min(q, lo + cap)
+    dv = qf_d.device
+    ids = torch.empty((cap, k), dtype=torch.int64, device=dv)
+    dists = torch.empty((cap, k), dtype=torch.float64, device=dv)
+    st = torch.zeros((cap, 5), dtype=torch.int64, device=dv)
+    if hi > lo:
+        if dv.type == "cuda":
+            dev.set_stream(torch.cuda.current_stream(dv).cuda_stream)
+        dev.route_dev(qf_d[lo:hi].data_ptr(), qa_d[lo:hi].data_ptr(),
+                      None if qm_d is None else qm_d[lo:hi].data_ptr(), hi - lo, k, pioneer,
+                      inv_alpha, ids.data_ptr(), dists.data_ptr(), st.data_ptr(), seed=seed,
+                      qi0=lo, use_coarse=use_coarse)
+    if world == 1:
+        return ids[:q], dists[:q], st[:q]
+    out = []
+    for t in (ids, dists, st):
+        full = torch.empty((world * cap,) + tuple(t.shape[1:]), dtype=t.dtype, device=dv)
+        dist.all_gather_into_tensor(full, t, group=group)
+        out.append(full[:q])
+    return tuple(out)
 
 
 def merge_topk(dist_lists, id_lists, k: int):

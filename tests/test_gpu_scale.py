@@ -136,3 +136,46 @@ def test_search_results_survive_later_calls(small_golden):
     for ids, dists, ids0, dists0 in keep:
         np.testing.assert_array_equal(ids, ids0)
         np.testing.assert_array_equal(dists, dists0)
+
+
+@pytest.mark.parametrize("kind", ["shell", "offset", "wide"])
+def test_route_filter_near_ties_exact(kind, monkeypatch):
+    """The certified fp32 filter of real-valued routing (route.cu kModeF64Filt) must never drop
+    a row that can enter the result list: rows on a thin shell around the query (distances
+    equal to ~1e-9 relative, below fp32 resolution), rows far from the origin (the query's
+    rounding to fp32 dominates), and d = 960 (cfg 4's width).  Ids, fp64 distances and the
+    SearchStats counters equal the oracle's and the unfiltered path's."""
+    rng = np.random.default_rng({"shell": 1, "offset": 2, "wide": 3}[kind])
+    n, g, l = 3000, 16, 2
+    m = 960 if kind == "wide" else 36
+    q = 24
+    qf = rng.standard_normal((q, m))
+    if kind == "shell":
+        dirs = rng.standard_normal((n, m))
+        dirs /= np.linalg.norm(dirs, axis=1, keepdims=True)
+        f = (qf[0] + dirs * (1.0 + 1e-9 * rng.integers(0, 50, (n, 1)))).astype(np.float32)
+        qf = np.repeat(qf[:1], q, axis=0) + 1e-7 * rng.standard_normal((q, m))
+    elif kind == "offset":
+        f = (3e4 + rng.standard_normal((n, m))).astype(np.float32)
+        qf = 3e4 + rng.standard_normal((q, m))
+    else:
+        f = rng.gamma(2.0, 1.0, (n, m)).astype(np.float32)
+        qf = rng.gamma(2.0, 1.0, (q, m))
+    a = rng.integers(1, 3, (n, l)).astype(np.int32)
+    qa = rng.integers(1, 3, (q, l)).astype(np.int32)
+    ids = np.stack([rng.choice(n, g, replace=False) for _ in range(n)]).astype(np.int32)
+    cnt = rng.integers(g // 2, g + 1, n).astype(np.int32)
+    graph = sb.RelationGraph(features=f, attrs=a, schema=sb.AttributeSchema((("x", "y"),) * l),
+                             metric=sb.MetricConfig.manual(0.8, l), sigma=0.44, nbr_ids=ids,
+                             nbr_dists=np.zeros((n, g), np.float32), nbr_counts=cnt, frozen=True)
+    for k in (5, 64):
+        p = sb.SearchParams(k=k, seed=4)
+        got = sb.search_batch_arrays(graph, qf, qa, p)
+        assert graph.device().route_info()["path"] == "fp32-filter+fp64"
+        monkeypatch.setenv("SB_ROUTE_FILT", "0")
+        plain = sb.search_batch_arrays(graph, qf, qa, p)
+        monkeypatch.delenv("SB_ROUTE_FILT")
+        want = O.search_batch(f, a, ids, cnt, 0.8, qf, qa, k, seed=4)
+        for x, y, z in zip(got, plain, want):
+            np.testing.assert_array_equal(x[:, :z.shape[1]] if x.ndim == 2 else x, z, err_msg=f"{kind} k={k}")
+            np.testing.assert_array_equal(x, y)

@@ -50,6 +50,31 @@ def _oracle_local_topk(alpha):
     return local_fn
 
 
+class _OracleDevice:
+    """CPU stand-in for DeviceIndex.route_dev: same pointer-based contract (row block of the
+    query tensors in, results written through the output pointers), oracle compute."""
+
+    def __init__(self, f, a, ids, cnt, alpha, k, seed):
+        self.f, self.a, self.ids, self.cnt, self.alpha, self.k, self.seed = f, a, ids, cnt, alpha, k, seed
+
+    def set_stream(self, s):
+        raise AssertionError("CPU tensors need no stream")
+
+    def route_dev(self, qf_ptr, qa_ptr, qm_ptr, q, k, pioneer, inv_alpha, ids_ptr, dists_ptr,
+                  stats_ptr=None, entries_ptr=None, seed=0, qi0=0, use_coarse=True):
+        import ctypes
+        m, l = self.f.shape[1], self.a.shape[1]
+        view = lambda p, t, shape: np.ctypeslib.as_array(ctypes.cast(p, ctypes.POINTER(t)), shape)
+        qf = view(qf_ptr, ctypes.c_double, (q, m)).copy()
+        qa = view(qa_ptr, ctypes.c_double, (q, l)).copy()
+        ent = np.stack([O.entry_points(self.f.shape[0], k, seed, qi0 + i) for i in range(q)])
+        i, d, st = O.route_batch_raw(self.f, self.a, self.ids, self.cnt, qf, qa, None,
+                                     inv_alpha, ent, pioneer, use_coarse, 1)
+        view(ids_ptr, ctypes.c_int64, (q, k))[:] = i
+        view(dists_ptr, ctypes.c_double, (q, k))[:] = d
+        view(stats_ptr, ctypes.c_int64, (q, 5))[:, :4] = st
+
+
 def _worker(rank, world, port, out_dir):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
@@ -63,8 +88,15 @@ def _worker(rank, world, port, out_dir):
                                                                    alpha, k, seed))
         ti, td = sharding.oracle_auto_topk_sharded(f, a, qf, qa, 9, None,
                                                    local_fn=_oracle_local_topk(alpha))
+        import torch
+        dev = _OracleDevice(f, a, g.nbr_ids, g.nbr_counts, alpha, k, seed)
+        qf_t = torch.from_numpy(np.ascontiguousarray(qf, np.float64))
+        qa_t = torch.from_numpy(np.ascontiguousarray(qa, np.float64))
+        di, dd, ds = sharding.search_batch_sharded_device(dev, qf_t, qa_t, qf.shape[0], k,
+                                                          max(1, k // 2), 1.0 / alpha, seed=seed)
         np.savez(os.path.join(out_dir, f"r{rank}.npz"), ids=got[0], dists=got[1], stats=got[2],
-                 ti=ti, td=td)
+                 ti=ti, td=td, dev_ids=di.numpy(), dev_dists=dd.numpy(),
+                 dev_stats=ds.numpy()[:, :4])
     finally:
         dist.destroy_process_group()
 
@@ -118,6 +150,9 @@ def test_two_ranks_gloo_match_single_process(tmp_path):
         np.testing.assert_array_equal(z["stats"], want[2])
         np.testing.assert_array_equal(z["ti"], wi)
         np.testing.assert_array_equal(z["td"], wd)
+        np.testing.assert_array_equal(z["dev_ids"], want[0])
+        np.testing.assert_array_equal(z["dev_dists"], want[1])
+        np.testing.assert_array_equal(z["dev_stats"], want[2])
 
 
 @pytest.mark.gpu
@@ -137,3 +172,24 @@ def test_sharded_defaults_run_the_b200_path():
     want = sb.search_batch_arrays(g, qf, qa, p)
     for x, y in zip(got, want):
         np.testing.assert_array_equal(x, y)
+
+
+@pytest.mark.gpu
+def test_device_sharded_routing_single_process():
+    """search_batch_sharded_device on one GPU equals the public search_batch."""
+    import torch
+    import paper_2604_01617_b200 as sb
+    f, a, qf, qa = _data(n=3000, q=50)
+    cfg = sb.MetricConfig.manual(1.07, a.shape[1])
+    schema = sb.AttributeSchema(tuple(tuple(str(i) for i in range(4)) for _ in range(a.shape[1])))
+    g = sb.build(f, a, schema, sb.BuildParams(gamma=24, gamma_new=24), cfg)
+    p = sb.SearchParams(k=20, seed=2)
+    want = sb.search_batch_arrays(g, qf, qa, p)
+    qf_d = torch.from_numpy(np.ascontiguousarray(qf, np.float64)).cuda()
+    qa_d = torch.from_numpy(np.ascontiguousarray(qa, np.float64)).cuda()
+    got = sharding.search_batch_sharded_device(g.device(), qf_d, qa_d, qf.shape[0], 20, 10,
+                                               1.0 / 1.07, seed=2)
+    torch.cuda.synchronize()
+    g.device().set_stream(None)
+    for x, y in zip(got, want):
+        np.testing.assert_array_equal(x.cpu().numpy(), y)

@@ -95,3 +95,11 @@ def make_config(name: str, n_override=None):
         QA = rng.integers(1, card + 1, (q, 1)).astype(np.int32)
         return X, A, QX, QA, (card,)
     raise ValueError(name)
+
+
+# Operating pool size K* per config: the smallest K of bench.py's sweep whose mean Recall@10
+# against the exact AUTO ground truth of all queries is >= 0.95 (measured on the device build,
+# which is bit-identical to the oracle's: profiles/configs_r1.jsonl, profiles/parity_full_r2.jsonl).
+# The reference arm of bench.py routes at this K without recomputing the full ground truth.
+OPERATING_K = {"cfg2": 200, "cfg3": 6000, "cfg4": 500, "cfg5c1": 500, "cfg5c10": 200,
+               "cfg5c100": 500, "cfg5c1000": 4000, "cfg5c10000": 32000}
