@@ -158,6 +158,11 @@ struct TfArgs {
   uint64_t* ocand;         // q x ocap
   int ocap;
   int seed;                // > 0: bound-only pass over `seed` evenly spread tiles per split
+  // large k (two-pass scheme, see bf_tf_run): bound_only = a full pass that only builds the
+  // per-thread lists and writes them to `lists` (q x threads x KR); fixed = the emission pass
+  // under the bound the select kernel wrote to gthr (no list work, the bound never moves)
+  int bound_only, fixed;
+  float* lists;
   int strided;             // 1: split s walks tiles s, s + splits, ...; 0: contiguous ranges
 };
 
@@ -443,7 +448,7 @@ __global__ void __launch_bounds__(32 * EW + 64, 1) bf_tf_kernel(TfArgs a) {
         const float yj = 2.0f * zj;
         const float lo = fmaxf(nq_s - yj, 0.f) * fsq * 0.99998f;
         if (lo > t2_eff) return;
-        if (!a.seed) {  // a possible member of the exact top k
+        if (!a.seed && !a.bound_only) {  // a possible member of the exact top k
           const uint64_t e = ((uint64_t)__float_as_uint(lo) << 32) | (uint32_t)s_orig[col];
           if (emitted < (uint32_t)a.cap) {
             my_cand[emitted++] = e;
@@ -454,7 +459,7 @@ __global__ void __launch_bounds__(32 * EW + 64, 1) bf_tf_kernel(TfArgs a) {
         }
         // upper key (nqu + nxu - 2 dot = nq_u - y + nxd) into this thread's kk smallest
         const float hi = fmaxf(nq_u - yj + s_nxd[col], 0.f) * fsq * 1.00002f;
-        if (!(hi < own_t2)) return;
+        if (a.fixed || !(hi < own_t2)) return;
         if (KR > 0) {  // sorted register list: one branch-free pass, no memory chain
 #pragma unroll
           for (int j = KR - 1; j > 0; --j) rl[j] = hi < rl[j - 1] ? rl[j - 1] : fminf(hi, rl[j]);
@@ -549,7 +554,13 @@ __global__ void __launch_bounds__(32 * EW + 64, 1) bf_tf_kernel(TfArgs a) {
         set_thr();
       }
     }
-    if (qok && !a.seed) a.cnt[seg] = emitted;
+    if (qok && !a.seed && !a.bound_only) a.cnt[seg] = emitted;
+    if (KR > 0 && a.lists && qok) {  // this thread's KR smallest upper keys (FLT_MAX if unfilled)
+      const int tq = blockIdx.y * PPQ + part;  // thread index within the query: split, column part
+      float* dst = a.lists + ((size_t)my_q * gridDim.y * PPQ + tq) * KR;
+#pragma unroll
+      for (int j = 0; j < KR; ++j) dst[j] = rl[j];
+    }
   }
   tc_fence_before();
   __syncthreads();
@@ -654,6 +665,41 @@ __global__ void tf_refine_kernel(const float* __restrict__ F, const int32_t* __r
   }
 }
 
+// ---- large k: the bound from every thread's list ------------------------------------------
+// lists: q x nl upper keys (each a genuine upper key of a distinct node, or FLT_MAX).  Any k of
+// them bound U_k^2 from above, so the k-th smallest is a valid emission bound for the query
+// (and close to the exact k-th when the threads' lists cover the query's top k).  CTA per
+// query: bitonic sort of the (non-negative, int-ordered) keys in shared memory.
+__global__ void tf_select_kernel(const float* __restrict__ lists, int nl, int k, int* gthr) {
+  extern __shared__ int sk[];
+  const int64_t g = blockIdx.x;
+  const int np = next_pow2(nl);
+  for (int i = threadIdx.x; i < np; i += blockDim.x)
+    sk[i] = i < nl ? __float_as_int(lists[g * nl + i]) : __float_as_int(FLT_MAX);
+  __syncthreads();
+  for (int size = 2; size <= np; size <<= 1)
+    for (int stride = size >> 1; stride > 0; stride >>= 1) {
+      for (int i = threadIdx.x; i < np; i += blockDim.x) {
+        const int j = i ^ stride;
+        if (j > i) {
+          const bool up = (i & size) == 0;
+          const int x = sk[i], y = sk[j];
+          if ((x > y) == up) { sk[i] = y; sk[j] = x; }
+        }
+      }
+      __syncthreads();
+    }
+  if (threadIdx.x == 0) gthr[g] = sk[k - 1];
+}
+
+int launch_tf_select(const float* lists, int64_t q, int nl, int k, int* gthr, cudaStream_t st) {
+  const size_t smem = sizeof(int) * (size_t)next_pow2(nl);
+  cudaError_t e = cudaFuncSetAttribute(tf_select_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return (int)e;
+  tf_select_kernel<<<(unsigned)q, 256, smem, st>>>(lists, nl, k, gthr);
+  return (int)cudaGetLastError();
+}
+
 // ---- host side ------------------------------------------------------------------------------
 // cE of (1): |S~ - S| <= cE (|x|^2 + |q|^2) for d-dimensional rows (dpad = d rounded up to 8).
 //  * operands: |tf32(x) - x| <= 2^-11 |x| (round to nearest), so
@@ -741,7 +787,7 @@ int launch_bf_tf(const float* Ft, const float* nxd, const int32_t* code,
                  const float* nqu, const int64_t* qa, const int64_t* qmask, int64_t n, int64_t q,
                  int m, int l, int kk, int splits, double alpha, int* gthr, uint32_t* cnt,
                  uint64_t* cand, int cap, uint32_t* ocnt, uint64_t* ocand, int ocap, int seed,
-                 int strided, cudaStream_t st) {
+                 int strided, int bound_only, int fixed, float* lists, cudaStream_t st) {
   const int dpad = tf_dpad(m);
   const TfShape sh = tf_shape(dpad, l, kk);
   if (sh.N == 0) return (int)cudaErrorInvalidValue;
@@ -752,6 +798,7 @@ int launch_bf_tf(const float* Ft, const float* nxd, const int32_t* code,
   a.stages = sh.stages; a.alpha = alpha; a.gthr = gthr; a.cnt = cnt; a.cand = cand;
   a.cap = cap; a.ocnt = ocnt; a.ocand = ocand; a.ocap = ocap; a.seed = seed;
   a.strided = strided;
+  a.bound_only = bound_only; a.fixed = fixed; a.lists = lists;
   const size_t smem = tf_smem_bytes(dpad, l, kk, sh.N, sh.stages, sh.ares, sh.qt, sh.ew, sh.kr);
   void (*kern)(TfArgs) = nullptr;
 #define SB_TF_PICK(EW, KR)                                                                          \

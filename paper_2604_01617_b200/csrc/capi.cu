@@ -201,8 +201,10 @@ struct sb_index {
   int meta_relabel = -1;
   DBuf ft, ft_meta, tq, tcand, tovf;
   DBuf bf_sort;                      // full-sort top-k scratch (bf_sort.cu: any k)
+  DBuf tlists;                       // two-pass TF32 top-k: per-thread lists (q x threads x 32)
   ~sb_index() {
     bf_sort.release();
+    tlists.release();
     fb.release();
     f8.release();
     DBuf* tfb[] = {&ft, &ft_meta, &tq, &tcand, &tovf};
@@ -1148,6 +1150,9 @@ static int bf_run(sb_index* idx, sb::BfArgs& a, int kout, int64_t* out64, int32_
   return SB_OK;
 }
 
+static int bf_sorted_run(sb_index* idx, const sb::BfArgs& a, int mode, int kout, int64_t* out64,
+                         int32_t* out32, double* outd, int64_t* out_counts);
+
 // TF32 filter + exact re-rank (bf_tf.cu).  Queries whose candidates overflow the buffers are
 // recomputed on the exact fp64 kernel (bf_run); the count is reported by sb_bf_info.
 static int bf_tf_run(sb_index* idx, const double* qf, const int64_t* qa, const int64_t* qmask,
@@ -1180,8 +1185,17 @@ static int bf_tf_run(sb_index* idx, const double* qf, const int64_t* qa, const i
     idx->have_cand = false;  // rev_* scratch was reused
     idx->launches += 5;
   }
+  // k > 32: two full passes (bf_tf.cu "large k"): the first builds every epilogue thread's
+  // list of its 32 smallest upper keys, a select kernel takes the k-th smallest of all of a
+  // query's lists as its bound, the second emits the candidates under that bound.  Needs
+  // (threads per query) x 32 >= k; SB_TF_TWOPASS=0 keeps the single pass with shared-memory
+  // lists.
+  const int KRL = 32;
+  bool twopass = k > KRL && sb::bf_tf_supported(m, l, KRL);
+  if (const char* e = getenv("SB_TF_TWOPASS")) twopass = twopass && atoi(e) != 0;
+  const int kshape = twopass ? KRL : k;
   int qblock = 128, hsegs = 2, ew = 8;
-  sb::bf_tf_layout(m, l, k, &qblock, &hsegs, &ew);
+  sb::bf_tf_layout(m, l, kshape, &qblock, &hsegs, &ew);
   const int64_t qpad = (q + qblock - 1) / qblock * qblock;
   // node-range splits: whole waves of one CTA per SM, fewest splits within 3% of the best
   const int groups = (int)(qpad / qblock);
@@ -1192,7 +1206,7 @@ static int bf_tf_run(sb_index* idx, const double* qf, const int64_t* qa, const i
     std::vector<double> cost(65, 1e30);
     // each epilogue thread should see many more than k nodes, or its list bound stays loose
     // and nearly every node is emitted: (tiles / splits) * 128 >= 16 k
-    const int64_t smax = std::max<int64_t>(1, std::min<int64_t>(64, tiles * 128 / (16 * (int64_t)k)));
+    const int64_t smax = std::max<int64_t>(1, std::min<int64_t>(64, tiles * 128 / (16 * (int64_t)kshape)));
     for (int s2 = 1; s2 <= smax; ++s2) {
       const double waves = (double)((groups * s2 + idx->sms - 1) / idx->sms);
       cost[s2] = waves / s2;
@@ -1201,11 +1215,15 @@ static int bf_tf_run(sb_index* idx, const double* qf, const int64_t* qa, const i
     for (int s2 = 1; s2 <= 64; ++s2)
       if (cost[s2] <= best * 1.03) { splits = s2; break; }
     if (const char* e = getenv("SB_TF_SPLITS")) splits = std::max(1, atoi(e));
+    // the union of a query's thread lists must hold k keys
+    if (twopass) while (splits * hsegs * KRL < k && splits < 64) ++splits;
+    if (twopass && splits * hsegs * KRL < k)  // (64 splits x 2 x 32 >= 4096 > every k here)
+      return fail(SB_ECUDA, "two-pass top-k: too few thread lists for k");
   }
   // one candidate segment per epilogue thread of the grid; after the seed pass a thread emits
   // a few dozen candidates (full segments spill into the query's overflow area)
   const int64_t nthreads = (int64_t)groups * splits * 32 * ew;
-  int cap = std::max(256, 32 * k);
+  int cap = twopass ? 256 : std::max(256, 32 * k);
   while (cap > 64 && (double)nthreads * cap * 8.0 > 8e9) cap /= 2;
   if (const char* e = getenv("SB_TF_CAP")) cap = std::max(1, atoi(e));
   const int scap = k > 32 ? 4096 : 2048;  // survivors of the final bound the re-rank takes
@@ -1233,14 +1251,30 @@ static int bf_tf_run(sb_index* idx, const double* qf, const int64_t* qa, const i
   CKL(sb::launch_tf_prep_queries(idx->qf.as<double>(), q, qpad, m, cE, tiny, Qt, nqs, nqu, idx->st));
   // seed pass (first tile of every range, bound only), then the full pass
   // seed pass: enough evenly spread tiles that every thread's list of k fills several times
-  int seed_tiles = std::min(64, std::max(4, k / 2));
+  int seed_tiles = std::min(64, std::max(4, kshape / 2));
   if (const char* e = getenv("SB_TF_SEED")) seed_tiles = std::max(0, atoi(e));
-  CK(idx->bf_event(0));  // the tensor-core pass = seed + full launch
-  for (int seed = seed_tiles; seed >= 0; seed = seed > 0 ? 0 : -1) {
-    CKL(sb::launch_bf_tf(idx->ft.as<float>(), nxd, s_code, s_orig, s_run, s_attr, Qt, nqs, nqu,
-                         idx->bf_qa.as<int64_t>(), qmask ? idx->bf_qm.as<int64_t>() : nullptr, n, q,
-                         m, l, k, splits, alpha, gthr, cnt, idx->tcand.as<uint64_t>(), cap, ocnt,
-                         ocand, ocap, seed, idx->tf_strided, idx->st));
+  const int nl = splits * hsegs * KRL;  // list keys per query (two-pass)
+  float* lists = nullptr;
+  if (twopass) {
+    CK(idx->tlists.ensure(sizeof(float) * (size_t)q * nl));
+    lists = idx->tlists.as<float>();
+  }
+  CK(idx->bf_event(0));  // the tensor-core pass = seed + full launch(es)
+  auto pass = [&](int seed, int bound_only, int fixed) {
+    return sb::launch_bf_tf(idx->ft.as<float>(), nxd, s_code, s_orig, s_run, s_attr, Qt, nqs, nqu,
+                            idx->bf_qa.as<int64_t>(), qmask ? idx->bf_qm.as<int64_t>() : nullptr, n, q,
+                            m, l, kshape, splits, alpha, gthr, cnt, idx->tcand.as<uint64_t>(), cap,
+                            ocnt, ocand, ocap, seed, idx->tf_strided, bound_only, fixed,
+                            bound_only ? lists : nullptr, idx->st);
+  };
+  if (seed_tiles > 0) CKL(pass(seed_tiles, 0, 0));
+  if (twopass) {
+    CKL(pass(0, 1, 0));
+    CKL(sb::launch_tf_select(lists, q, nl, k, gthr, idx->st));
+    CKL(pass(0, 0, 1));
+    idx->launches += 2;
+  } else {
+    CKL(pass(0, 0, 0));
   }
   CK(idx->bf_event(1));
   idx->bf_ev_valid = true;
@@ -1293,7 +1327,10 @@ static int bf_tf_run(sb_index* idx, const double* qf, const int64_t* qa, const i
     a.qf = d_qf; a.qa = d_qa; a.qmask = qmask ? d_qm : nullptr; a.q = s;
     a.k = (int)std::min<int64_t>(n, k + 16); a.alpha = alpha;
     int unc = 0;
-    int r = bf_run(idx, a, k, d_ids, nullptr, d_d, &unc);
+    // the tiled fp64 kernel while its per-query lists fit shared memory, else the full sort
+    int r = sb::bf_partial_smem(a.k) <= (size_t)227 * 1024
+                ? bf_run(idx, a, k, d_ids, nullptr, d_d, &unc)
+                : bf_sorted_run(idx, a, sb::kBfSortQuery, k, d_ids, nullptr, d_d, nullptr);
     if (r) return r;
     std::vector<int64_t> hi((size_t)s * k);
     std::vector<double> hd((size_t)s * k);
@@ -1427,7 +1464,7 @@ int sb_bf_topk_queries(sb_index* idx, const double* qf, const int64_t* qa, const
   const int esz = u8 ? 1 : 2;  // operand bytes per element
   // other data: TF32 tensor-core filter with a certified bound + exact fp64 re-rank (bf_tf.cu)
   double qmax_abs = 0.0;
-  bool tf = !tc && !idx->force_sequential && sb::bf_tf_supported(idx->m, idx->l, k) &&
+  bool tf = !tc && !idx->force_sequential && sb::bf_tf_supported(idx->m, idx->l, std::min(k, 32)) &&
             idx->fmax < 1e15;
   for (int64_t i = 0; tf && i < q * idx->m; ++i) {
     const double v = std::fabs(qf[i]);
@@ -1514,7 +1551,10 @@ int sb_bf_topk_queries(sb_index* idx, const double* qf, const int64_t* qa, const
     if (uncertain) *uncertain = unc;
     return SB_OK;
   } else {
-    int r = bf_run(idx, a, k, idx->out_ids.as<int64_t>(), nullptr, idx->out_dists.as<double>(), &unc);
+    int r = sb::bf_partial_smem(a.k) <= (size_t)227 * 1024
+                ? bf_run(idx, a, k, idx->out_ids.as<int64_t>(), nullptr, idx->out_dists.as<double>(), &unc)
+                : bf_sorted_run(idx, a, sb::kBfSortQuery, k, idx->out_ids.as<int64_t>(), nullptr,
+                                idx->out_dists.as<double>(), nullptr);
     if (r) return r;
     idx->bf_ev_valid = false;
     idx->last_bf_tc = false;

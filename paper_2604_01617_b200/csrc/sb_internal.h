@@ -154,7 +154,9 @@ int launch_bf_tf(const float* Ft, const float* nxd, const int32_t* code,
                  const float* nqu, const int64_t* qa, const int64_t* qmask, int64_t n, int64_t q,
                  int m, int l, int kk, int splits, double alpha, int* gthr, uint32_t* cnt,
                  uint64_t* cand, int cap, uint32_t* ocnt, uint64_t* ocand, int ocap, int seed,
-                 int strided, cudaStream_t st);
+                 int strided, int bound_only, int fixed, float* lists, cudaStream_t st);
+// large k: gthr[g] = the k-th smallest of the q x nl per-thread list keys (bf_tf.cu)
+int launch_tf_select(const float* lists, int64_t q, int nl, int k, int* gthr, cudaStream_t st);
 int launch_tf_refine(const float* F, const int32_t* A, int m, int l, const double* qf,
                      const int64_t* qa, const int64_t* qmask, int64_t q, int k, double alpha,
                      const uint32_t* cnt, const uint64_t* cand, int splits, int hsegs, int qblock,

@@ -64,6 +64,9 @@ def _fp64_path(d, qf, qa, k, alpha, mk):
     ("gamma", 2500, 960, 2, 70, 10),       # d = 960: streamed query tile
     ("normal", 777, 7, 3, 5, 1),           # d = 7, k = 1
     ("dup", 5000, 33, 2, 300, 32),         # ties by id
+    ("unit", 20000, 96, 1, 300, 64),       # k > 32: two-pass bound (per-thread lists + select)
+    ("gauss_w", 8000, 100, 1, 150, 250),   # two-pass, k = 250
+    ("dup", 6000, 32, 2, 100, 600),        # two-pass with ties; fp64 check path = full sort
 ])
 def test_tf32_topk_exact(kind, n, m, l, q, k):
     rng = np.random.default_rng(n + m + k)
@@ -191,3 +194,22 @@ def test_tf32_edge_cases(case):
                                     return_dists=True)
         np.testing.assert_array_equal(ids[qi], wi, err_msg=f"{case} query {qi}")
         np.testing.assert_array_equal(dd[qi], wd, err_msg=f"{case} query {qi}")
+
+
+def test_tf32_two_pass_equals_single_pass(monkeypatch):
+    """k > 32: the two-pass bound (bf_tf.cu "large k") and the single pass with shared-memory
+    lists (SB_TF_TWOPASS=0) give the reference's answer; the two-pass bound emits fewer
+    candidates."""
+    rng = np.random.default_rng(9)
+    f, qf = _data("unit", 30000, 96, 400, rng)
+    a = rng.integers(1, 4, (30000, 1)).astype(np.int32)
+    qa = rng.integers(1, 4, (400, 1))
+    d = DeviceIndex(f, a, 2)
+    ids2, dd2 = d.bf_topk_queries(qf, qa, 100, 0.2)
+    c2 = d.bf_info()["candidates"]
+    monkeypatch.setenv("SB_TF_TWOPASS", "0")
+    ids1, dd1 = d.bf_topk_queries(qf, qa, 100, 0.2)
+    c1 = d.bf_info()["candidates"]
+    np.testing.assert_array_equal(ids1, ids2)
+    np.testing.assert_array_equal(dd1, dd2)
+    assert c2 < c1, (c2, c1)
