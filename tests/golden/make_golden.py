@@ -19,6 +19,8 @@ Cases
   cfg1      BASELINE config 1 (N=10k, d=32, card 4, 200 queries, seed 0, BuildParams()):
             alpha, psi history, edge counts, hashes of every stage, searches at
             K in {10, 25, 50} (ids, dists, stats) and the exact AUTO top-10 GT.
+  index     the small case's graph written by the reference's write_index (small_index.help)
+            and searched after the reference's read_index.
   rng       entry_points over an (n, K, seed, qi) grid covering NumPy's two
             choice() regimes; init_random_graph id matrices (pre-distance).
 """
@@ -224,6 +226,39 @@ def case_rng(ha):
     g = init_random_graph(f, a, schema, ha.BuildParams(gamma=24, gamma_new=24, seed=3),
                           ha.MetricConfig.manual(1.0, 1))
     assert set(map(tuple, np.sort(g.nbr_ids, 1))) == set(map(tuple, np.sort(out["init_300_24_3"], 1)))
+    return out
+
+
+def case_index(ha):
+    """The reference writes the small case's graph with its own write_index (graph.py:287-330)
+    -> small_index.help (kept beside the .npz); its read_index of that file, searched at two
+    pool sizes (ids, dists, stats), is pinned here."""
+    features = ha.generate_synthetic(600, 12, "gaussian", seed=11)
+    schema, attrs = ha.generate_attributes(600, 3, 3, seed=12)
+    stats = ha.sample_statistics(features, attrs, 300, seed=13)
+    config = ha.compute_alpha(stats, features.shape[0], schema.l)
+    graph = ha.build(features, attrs, schema, ha.BuildParams(gamma=24, gamma_new=24, seed=3), config)
+    path = os.path.join(OUT, "small_index.help")
+    ha.write_index(graph, path)
+    back = ha.read_index(path)
+    qf, qa, _ = ha.generate_queries(features, attrs, 20, 3, min_matches=5, seed=14)
+    out = searches(ha, back, qf, qa, [10, 30], coarse=(True,))
+    # the reference's bench_sweep over the read-back graph (evaluate.py:95-141): recall and
+    # distance evaluations are deterministic (QPS is not); and its CSV of fixed rows
+    gt = [ha.oracle_auto_topk(features, attrs, qf[i], qa[i], 10, config) for i in range(qf.shape[0])]
+    rows = ha.bench_sweep(back, qf, qa, gt, [5, 10, 30], timing_passes=1)
+    out["sweep"] = np.array([[r.k, r.pioneer, r.mean_recall_at_10, r.mean_dist_evals, r.n_queries]
+                             for r in rows], np.float64)
+    out["sweep_gt"] = np.stack(gt)
+    from hybridann.evaluate import SweepRow, write_sweep_csv
+    fixed = [SweepRow(k=10, pioneer=5, mean_recall_at_10=0.95123456, qps=1234.5678,
+                      mean_dist_evals=321.123, n_queries=20),
+             SweepRow(k=200, pioneer=100, mean_recall_at_10=1.0, qps=7.0, mean_dist_evals=4152.84, n_queries=10000)]
+    csv_path = os.path.join("/tmp", "ref_sweep.csv")
+    write_sweep_csv(csv_path, fixed)
+    out["sweep_csv"] = np.array(open(csv_path).read())
+    out.update(qf=qf, qa=qa, counts=back.nbr_counts.copy(), ids=back.nbr_ids.copy(),
+               dists=back.nbr_dists.copy(), file_sha=np.array(hashlib.sha256(open(path, "rb").read()).hexdigest()))
     return out
 
 

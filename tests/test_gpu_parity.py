@@ -234,8 +234,9 @@ def test_route_large_k_insertion_buffer(relabel, g, path, monkeypatch):
         np.testing.assert_array_equal(got[0], want[0], err_msg=f"k={k}")
         np.testing.assert_array_equal(got[1], want[1], err_msg=f"k={k}")
         np.testing.assert_array_equal(got[2][:, :4], want[2], err_msg=f"k={k}")
-    want_path = {"u8": "u8-dp4a", "fp32": "fp32", "fp64": "fp64"}[path]
-    assert gr.device().route_info()["path"].startswith(want_path)
+    # real-valued rows take the certified fp32 filter in front of the exact fp64 rows
+    want_path = {"u8": "u8-dp4a", "fp32": "fp32", "fp64": "fp32-filter+fp64"}[path]
+    assert gr.device().route_info()["path"] == want_path
 
 
 @pytest.mark.parametrize("k,force", [(600, True), (2000, True), (17000, False)])
@@ -304,12 +305,14 @@ def test_order_free_mode_is_bit_exact():
         assert dev.route_info()["path"] == "fp32"
         split = with_env({"SB_ROUTE_U8": "0", "SB_ROUTE_LPR": "8"}, run)
         f64 = with_env({"SB_ROUTE_F32": "0"}, run)
+        assert dev.route_info()["path"] == "fp32-filter+fp64"
+        f64u = with_env({"SB_ROUTE_F32": "0", "SB_ROUTE_FILT": "0"}, run)
         assert dev.route_info()["path"] == "fp64"
         dev.set_distance_mode(sequential=True)
         seq = sb.search_batch_arrays(graph, qf, qa, p)
         dev.set_distance_mode(sequential=False)
         want = O.search_batch(f, a, ids, cnt, 1.03, qf, qa, k, seed=2)
-        for got in (u8, lane, split, f64, seq):
+        for got in (u8, lane, split, f64, f64u, seq):
             np.testing.assert_array_equal(got[0], want[0])
             np.testing.assert_array_equal(got[1], want[1])
             np.testing.assert_array_equal(got[2][:, :4], want[2])
@@ -463,3 +466,38 @@ def test_route_layout_follows_adjacency_changes():
             np.testing.assert_array_equal(got[0], want[0], err_msg=f"trial {trial} relabel {relabel}")
             np.testing.assert_array_equal(got[1], want[1])
             np.testing.assert_array_equal(got[2][:, :4], want[2])
+
+
+def test_route_on_reference_written_index():
+    """Routing over the graph the reference wrote (write_index) and read back (read_index),
+    bit for bit against the reference's own searches of its read-back graph
+    (tests/golden/make_golden.py case_index; graph.py:287-415, _kernels.py:504-610)."""
+    import os
+    gd = np.load(os.path.join(os.path.dirname(__file__), "golden", "index.npz"))
+    g = sb.read_index(os.path.join(os.path.dirname(__file__), "golden", "small_index.help"))
+    for k in (10, 30):
+        ids, dists, st = sb.search_batch_arrays(g, gd["qf"], gd["qa"], sb.SearchParams(k=k))
+        np.testing.assert_array_equal(ids, gd[f"s_k{k}_c_ids"])
+        np.testing.assert_array_equal(dists, gd[f"s_k{k}_c_dists"])
+        np.testing.assert_array_equal(st[:, :4], gd[f"s_k{k}_c_stats"])
+
+
+def test_bench_sweep_matches_reference():
+    """bench_sweep (evaluate.py:95-141) through the device: pioneer sizes, mean Recall@10 and
+    mean distance evaluations equal the reference's own bench_sweep on the same graph and
+    ground truth; the roofline columns equal §8(d)'s bytes from the search stats."""
+    import os
+    gd = np.load(os.path.join(os.path.dirname(__file__), "golden", "index.npz"))
+    g = sb.read_index(os.path.join(os.path.dirname(__file__), "golden", "small_index.help"))
+    gt = list(gd["sweep_gt"])
+    rows = sb.evaluate.bench_sweep(g, gd["qf"], gd["qa"], gt, [5, 10, 30], timing_passes=2,
+                                   hbm_peak_gbs=6500.0)
+    for r, want in zip(rows, gd["sweep"]):
+        assert (r.k, r.pioneer, r.n_queries) == (int(want[0]), int(want[1]), int(want[4]))
+        assert r.mean_recall_at_10 == want[2] and r.mean_dist_evals == want[3]
+        assert r.qps > 0 and r.algorithmic_gbs > 0
+        assert abs(r.hbm_frac - r.algorithmic_gbs / 6500.0) < 1e-12
+    _, _, st = sb.search_batch_arrays(g, gd["qf"], gd["qa"], sb.SearchParams(k=30))
+    m, l = g.features.shape[1], g.attrs.shape[1]
+    assert sb.evaluate.routing_bytes(st, m, l) == \
+        float(st[:, 0].sum() * (4 * m + 4 * l) + 4 * (st[:, 2].sum() + st[:, 3].sum() + st[:, 4].sum()))

@@ -168,3 +168,44 @@ def test_no_cpu_fallback(tmp_path):
     out = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, env=env,
                          cwd=os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
     assert "raised" in out.stdout and "missing" in out.stdout
+
+
+def test_index_file_written_by_reference():
+    """tests/golden/small_index.help was written by the reference's own write_index
+    (graph.py:287-330; tests/golden/make_golden.py case_index).  read_index gives the arrays
+    the reference's read_index gave (stale tails as id 0 / +inf, graph.py:380-381), and
+    write_index of that graph reproduces the file byte for byte."""
+    import hashlib
+    import tempfile
+    path = os.path.join(os.path.dirname(__file__), "golden", "small_index.help")
+    gd = np.load(os.path.join(os.path.dirname(__file__), "golden", "index.npz"))
+    raw = open(path, "rb").read()
+    assert hashlib.sha256(raw).hexdigest() == str(gd["file_sha"])
+    g = sb.read_index(path)
+    np.testing.assert_array_equal(g.nbr_counts, gd["counts"])
+    np.testing.assert_array_equal(g.nbr_ids, gd["ids"])
+    np.testing.assert_array_equal(g.nbr_dists, gd["dists"])
+    assert g.frozen and g.gamma == 24 and g.n == 600
+    with tempfile.TemporaryDirectory() as td:
+        out = os.path.join(td, "again.help")
+        sb.write_index(g, out)
+        assert open(out, "rb").read() == raw
+
+
+def test_sweep_csv_matches_reference(tmp_path):
+    """write_sweep_csv writes the reference's CSV byte for byte (evaluate.py:144-158; the
+    reference's own output of the same rows is in tests/golden/index.npz); roofline=True
+    appends exactly the two roofline columns."""
+    gd = np.load(os.path.join(os.path.dirname(__file__), "golden", "index.npz"))
+    rows = [sb.evaluate.SweepRow(k=10, pioneer=5, mean_recall_at_10=0.95123456, qps=1234.5678,
+                                 mean_dist_evals=321.123, n_queries=20),
+            sb.evaluate.SweepRow(k=200, pioneer=100, mean_recall_at_10=1.0, qps=7.0,
+                                 mean_dist_evals=4152.84, n_queries=10000, algorithmic_gbs=3264.5,
+                                 hbm_frac=0.5051)]
+    p = tmp_path / "s.csv"
+    sb.evaluate.write_sweep_csv(p, rows)
+    assert p.read_text() == str(gd["sweep_csv"])
+    sb.evaluate.write_sweep_csv(p, rows, roofline=True)
+    lines = p.read_text().splitlines()
+    assert lines[0] == ",".join(sb.evaluate.CSV_FIELDS + ["algorithmic_gbs", "hbm_frac"])
+    assert lines[2].endswith(",3264.5,0.5051")
