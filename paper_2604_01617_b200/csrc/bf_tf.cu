@@ -190,6 +190,9 @@ __global__ void __launch_bounds__(32 * EW + 64, 1) bf_tf_kernel(TfArgs a) {
   constexpr int EPI = 32 * EW;              // epilogue threads
   constexpr int PPQ = EW / 4 / QT;          // epilogue threads per query
   constexpr int cols = N / PPQ;             // columns per epilogue thread and tile
+  // TMEM columns per load in the scan: 16 for the 32-key register lists (with 32 more live
+  // registers the 32-column buffer spilled in the hot loop: 18 warps leave 96 registers)
+  constexpr int CW = KR > 16 ? 16 : 32;
   static_assert(cols % 32 == 0, "32-column TMEM loads");
   // (pointer arithmetic on the shared array itself keeps every access an LDS/STS)
   extern __shared__ __align__(1024) char smem[];
@@ -424,6 +427,7 @@ __global__ void __launch_bounds__(32 * EW + 64, 1) bf_tf_kernel(TfArgs a) {
     const size_t seg = ((size_t)blockIdx.y * gridDim.x + blockIdx.x) * EPI + tid;
     uint64_t* my_cand = qok ? a.cand + seg * a.cap : nullptr;
     uint32_t emitted = 0;
+
     float gnext = FLT_MAX;
     for (int i = 0; i < ntl; ++i) {
       const int s = i & 1;
@@ -479,31 +483,44 @@ __global__ void __launch_bounds__(32 * EW + 64, 1) bf_tf_kernel(TfArgs a) {
         if (own_t2 < t2_eff) {
           t2_eff = own_t2;
           set_thr();
-          atomicMin(a.gthr + my_q, __float_as_int(own_t2));  // non-negative floats order as ints
+          // (bound-only pass: a thread's KR-th key bounds only the KR-th of the query, not the
+          // k-th the two-pass scheme needs, so it filters this thread's own list and nothing else)
+          if (!a.bound_only) atomicMin(a.gthr + my_q, __float_as_int(own_t2));  // non-negative floats order as ints
         }
       };
       // scan: the fast filter over the accumulator.  All lanes of a warp see the same columns
       // (nodes) for different queries, so the chunk / run structure is warp-uniform; survivors
       // are processed in rounds, one per lane per round, so lanes with work run in parallel.
 #pragma unroll 1
-      for (int c = 0; c < cols / 32; ++c) {
-        uint32_t r[32];
-        tmem_ld32(lane_base + (uint32_t)(s * QT * N + c * 32), r);
-        const int c0 = part * cols + c * 32;
+      for (int c = 0; c < cols / CW; ++c) {
+        uint32_t r[CW];
+        if constexpr (CW == 32) tmem_ld32(lane_base + (uint32_t)(s * QT * N + c * CW), r);
+        else tmem_ld16(lane_base + (uint32_t)(s * QT * N + c * CW), r);
+        const int c0 = part * cols + c * CW;
         // the accumulator holds z = y / 2 with y = 2 x.q - nxs: one max decides the chunk
         // tree of 3-input maxima: depth 4 instead of a 16-long chain
-        float t9[11];
+        float mx;
+        if constexpr (CW == 32) {
+          float t9[11];
 #pragma unroll
-        for (int j = 0; j < 10; ++j)
-          t9[j] = fmaxf(fmaxf(__uint_as_float(r[3 * j]), __uint_as_float(r[3 * j + 1])), __uint_as_float(r[3 * j + 2]));
-        t9[10] = fmaxf(__uint_as_float(r[30]), __uint_as_float(r[31]));
-        const float u0 = fmaxf(fmaxf(t9[0], t9[1]), t9[2]), u1 = fmaxf(fmaxf(t9[3], t9[4]), t9[5]);
-        const float u2 = fmaxf(fmaxf(t9[6], t9[7]), t9[8]), u3 = fmaxf(t9[9], t9[10]);
-        const float mx = fmaxf(fmaxf(u0, u1), fmaxf(u2, u3));
-        const bool uniform = s_code[c0] == last_code && s_code[c0 + 31] == last_code;  // warp-uniform
+          for (int j = 0; j < 10; ++j)
+            t9[j] = fmaxf(fmaxf(__uint_as_float(r[3 * j]), __uint_as_float(r[3 * j + 1])), __uint_as_float(r[3 * j + 2]));
+          t9[10] = fmaxf(__uint_as_float(r[30]), __uint_as_float(r[31]));
+          const float u0 = fmaxf(fmaxf(t9[0], t9[1]), t9[2]), u1 = fmaxf(fmaxf(t9[3], t9[4]), t9[5]);
+          const float u2 = fmaxf(fmaxf(t9[6], t9[7]), t9[8]), u3 = fmaxf(t9[9], t9[10]);
+          mx = fmaxf(fmaxf(u0, u1), fmaxf(u2, u3));
+        } else {
+          float t5[6];
+#pragma unroll
+          for (int j = 0; j < 5; ++j)
+            t5[j] = fmaxf(fmaxf(__uint_as_float(r[3 * j]), __uint_as_float(r[3 * j + 1])), __uint_as_float(r[3 * j + 2]));
+          t5[5] = __uint_as_float(r[15]);
+          mx = fmaxf(fmaxf(fmaxf(t5[0], t5[1]), t5[2]), fmaxf(fmaxf(t5[3], t5[4]), t5[5]));
+        }
+        const bool uniform = s_code[c0] == last_code && s_code[c0 + CW - 1] == last_code;  // warp-uniform
         const bool act = qok && !(uniform && mx < thr_h);
         if (!__any_sync(0xffffffffu, act)) continue;
-        const int jend = nvalid - c0 < 32 ? nvalid - c0 : 32;
+        const int jend = nvalid - c0 < CW ? nvalid - c0 : CW;
         // runs of equal codes inside the chunk: one factor (and threshold) per run
         for (int j0 = 0; j0 < jend;) {
           int j1 = jend;
@@ -521,7 +538,7 @@ __global__ void __launch_bounds__(32 * EW + 64, 1) bf_tf_kernel(TfArgs a) {
           }
           unsigned cand = 0;
 #pragma unroll
-          for (int j = 0; j < 32; ++j)
+          for (int j = 0; j < CW; ++j)
             cand |= (j >= j0 && j < j1 && __uint_as_float(r[j]) >= thr_h ? 1u : 0u) << j;
           if (!act) cand = 0;
           j0 = j1;
@@ -531,7 +548,7 @@ __global__ void __launch_bounds__(32 * EW + 64, 1) bf_tf_kernel(TfArgs a) {
               cand &= cand - 1u;
               float zj = 0.f;
 #pragma unroll
-              for (int jj = 0; jj < 32; ++jj)
+              for (int jj = 0; jj < CW; ++jj)
                 if (jj == j) zj = __uint_as_float(r[jj]);
               process(c0 + j, zj, f2);
             }
@@ -542,8 +559,8 @@ __global__ void __launch_bounds__(32 * EW + 64, 1) bf_tf_kernel(TfArgs a) {
       mbar_arrive(bar_empty(s));
       mbar_arrive(bar_emptyM(ms));
       // share bounds with the query's other epilogue threads and with the other CTAs
-      float pt = gpre;
-      if (PPQ > 1) {
+      float pt = a.bound_only ? FLT_MAX : gpre;
+      if (PPQ > 1 && !a.bound_only) {
         s_t2[tid] = t2_eff;
 #pragma unroll
         for (int q2 = 0; q2 < PPQ; ++q2)
@@ -668,8 +685,9 @@ __global__ void tf_refine_kernel(const float* __restrict__ F, const int32_t* __r
 // ---- large k: the bound from every thread's list ------------------------------------------
 // lists: q x nl upper keys (each a genuine upper key of a distinct node, or FLT_MAX).  Any k of
 // them bound U_k^2 from above, so the k-th smallest is a valid emission bound for the query
-// (and close to the exact k-th when the threads' lists cover the query's top k).  CTA per
-// query: bitonic sort of the (non-negative, int-ordered) keys in shared memory.
+// (and close to the exact k-th when the threads' lists cover the query's top k); the query's
+// bound becomes the smaller of it and the current one.  CTA per query: bitonic sort of the
+// (non-negative, int-ordered) keys in shared memory.
 __global__ void tf_select_kernel(const float* __restrict__ lists, int nl, int k, int* gthr) {
   extern __shared__ int sk[];
   const int64_t g = blockIdx.x;
@@ -689,7 +707,7 @@ __global__ void tf_select_kernel(const float* __restrict__ lists, int nl, int k,
       }
       __syncthreads();
     }
-  if (threadIdx.x == 0) gthr[g] = sk[k - 1];
+  if (threadIdx.x == 0) gthr[g] = min(gthr[g], sk[k - 1]);  // (a bound from an earlier pass may be tighter)
 }
 
 int launch_tf_select(const float* lists, int64_t q, int nl, int k, int* gthr, cudaStream_t st) {
@@ -697,6 +715,77 @@ int launch_tf_select(const float* lists, int64_t q, int nl, int k, int* gthr, cu
   cudaError_t e = cudaFuncSetAttribute(tf_select_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return (int)e;
   tf_select_kernel<<<(unsigned)q, 256, smem, st>>>(lists, nl, k, gthr);
+  return (int)cudaGetLastError();
+}
+
+// ---- large k: an exact seed bound from each query's own attribute-code run -------------------
+// The nodes are sorted by attribute tuple code (node_order).  For a query whose tuple code is
+// c, the M nodes starting at c's run (or the nearest codes when the run is short) get their
+// U^2 = S f^2 computed in fp64 (sum order free: any k genuine values bound the k-th from
+// above once rounded up), and the k-th smallest, rounded up, becomes the query's starting
+// bound.  The strided seed tiles of the tensor-core pass sample popular codes well and rare
+// codes badly; this run sample is the other way round, and the smaller of the two is kept.
+struct TfCodeSeed {
+  int32_t lo[8];
+  int64_t stride[8];
+};
+__global__ void tf_code_seed_kernel(const float* __restrict__ F, const int32_t* __restrict__ A,
+                                    const int32_t* __restrict__ s_code, const int32_t* __restrict__ s_orig,
+                                    int64_t n, int m, int l, const double* __restrict__ qf,
+                                    const int64_t* __restrict__ qa, const int64_t* __restrict__ qmask,
+                                    int64_t q, int k, int M, double alpha, TfCodeSeed cs, int* gthr) {
+  extern __shared__ uint64_t ks[];
+  const int wpb = blockDim.x >> 5;
+  const int64_t g = (int64_t)blockIdx.x * wpb + warp_id();
+  if (g >= q) return;
+  uint64_t* key = ks + (size_t)warp_id() * M;
+  const int lane = lane_id();
+  int64_t code = 0;
+  for (int u = 0; u < l; ++u) code += ((int64_t)qa[g * l + u] - cs.lo[u]) * cs.stride[u];
+  int64_t lo = 0, hi = n;  // first sorted position with s_code >= code
+  while (lo < hi) {
+    const int64_t mid = (lo + hi) >> 1;
+    if ((int64_t)s_code[mid] < code) lo = mid + 1; else hi = mid;
+  }
+  int64_t s0 = lo - M / 8;
+  if (s0 > n - M) s0 = n - M;
+  if (s0 < 0) s0 = 0;
+  const double* qv = qf + g * m;
+  for (int j = lane; j < M; j += 32) {
+    const int64_t v = s_orig[s0 + j];
+    const float* x = F + v * m;
+    double sv = 0.0;
+    for (int t = 0; t < m; ++t) {
+      const double d = (double)x[t] - qv[t];
+      sv = fma(d, d, sv);
+    }
+    double sa = 0.0;
+    for (int u = 0; u < l; ++u)
+      sa += (qmask ? (double)qmask[g * l + u] : 1.0) * fabs((double)A[v * l + u] - (double)qa[g * l + u]);
+    const double f = 1.0 + sa / alpha;
+    const float u2 = __double2float_ru(sv * f * f * (1.0 + 1e-9));
+    key[j] = ((uint64_t)__float_as_uint(u2) << 32) | (uint32_t)j;
+  }
+  __syncwarp();
+  warp_bitonic_u64(key, M);
+  if (lane == 0) atomicMin(gthr + g, (int)(key[k - 1] >> 32));
+}
+
+int launch_tf_code_seed(const float* F, const int32_t* A, const int32_t* s_code, const int32_t* s_orig,
+                        int64_t n, int m, int l, const double* qf, const int64_t* qa,
+                        const int64_t* qmask, int64_t q, int k, double alpha, const int32_t* lo8,
+                        const int64_t* stride8, int* gthr, cudaStream_t st) {
+  int M = 256;
+  while (M < 2 * k && M < 2048) M <<= 1;
+  if (M > n || k > M) return 0;  // (nothing to seed from)
+  TfCodeSeed cs;
+  for (int u = 0; u < 8; ++u) { cs.lo[u] = lo8[u]; cs.stride[u] = stride8[u]; }
+  const int wpb = 4;
+  const size_t smem = sizeof(uint64_t) * (size_t)M * wpb;
+  cudaError_t e = cudaFuncSetAttribute(tf_code_seed_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return (int)e;
+  tf_code_seed_kernel<<<(unsigned)((q + wpb - 1) / wpb), 32 * wpb, smem, st>>>(
+      F, A, s_code, s_orig, n, m, l, qf, qa, qmask, q, k, M, alpha, cs, gthr);
   return (int)cudaGetLastError();
 }
 

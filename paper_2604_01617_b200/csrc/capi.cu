@@ -165,6 +165,10 @@ struct sb_index {
   int64_t last_bf_cands = 0;      // candidates the last TF32 call emitted (all queries)
   bool have_ft = false;           // TF32 operand copy + metadata (bf_tf.cu)
   int tf_strided = 1;             // walk the node tiles strided (skewed attribute codes)
+  // the attribute tuple code of node_order: code = sum_u (a_u - lo_u) stride_u (grouped orders)
+  int32_t code_lo[8] = {0};
+  int64_t code_stride[8] = {0};
+  bool code_grouped = false;
   cudaEvent_t bf_ev[2] = {nullptr, nullptr};  // around the last tensor-core top-k pass
   bool bf_ev_valid = false;
   bool have_f8 = false;           // u8 feature copy for routing (integer data in [0, 255])
@@ -1094,6 +1098,11 @@ static int node_order(sb_index* idx, int32_t* s_orig, int32_t** d_code_out) {
     if (combos > ((int64_t)1 << 24)) break;
   }
   const int grouped = combos <= ((int64_t)1 << 24) ? 1 : 0;
+  idx->code_grouped = grouped != 0;
+  for (int u = 0; u < 8; ++u) {
+    idx->code_lo[u] = u < l ? hlo[u] : 0;
+    idx->code_stride[u] = u < l ? stride[u] : 0;
+  }
   const int64_t bins = grouped ? combos : n;
   CK(cudaMemcpyAsync(d_stride, stride.data(), sizeof(int64_t) * 8, cudaMemcpyHostToDevice, idx->st));
   CK(idx->rev_cnt.ensure(sizeof(int64_t) * std::max<int64_t>(bins, n)));
@@ -1267,12 +1276,43 @@ static int bf_tf_run(sb_index* idx, const double* qf, const int64_t* qa, const i
                             ocnt, ocand, ocap, seed, idx->tf_strided, bound_only, fixed,
                             bound_only ? lists : nullptr, idx->st);
   };
-  if (seed_tiles > 0) CKL(pass(seed_tiles, 0, 0));
   if (twopass) {
+    // seed lists -> a first bound on the k-th key (the k-th smallest key of the union of the
+    // threads' lists: k genuine upper keys of distinct nodes lie at or below it), the full
+    // list pass under that bound, the tightened bound, the emission pass
+    static const bool dbg = getenv("SB_TF_DEBUG") != nullptr;
+    auto dump = [&](const char* what) {
+      if (!dbg) return;
+      std::vector<float> h(q);
+      cudaMemcpyAsync(h.data(), gthr, sizeof(float) * q, cudaMemcpyDeviceToHost, idx->st);
+      cudaStreamSynchronize(idx->st);
+      std::vector<float> srt(h);
+      std::sort(srt.begin(), srt.end());
+      fprintf(stderr, "[tf] %s splits=%d nl=%d bound p10 %.4g p50 %.4g p90 %.4g max %.4g\n", what, splits, nl,
+              srt[q / 10], srt[q / 2], srt[q * 9 / 10], srt[q - 1]);
+    };
+    if (idx->code_grouped && !(getenv("SB_TF_CODESEED") && atoi(getenv("SB_TF_CODESEED")) == 0)) {
+      CKL(sb::launch_tf_code_seed(idx->F.as<float>(), idx->A.as<int32_t>(), s_code, s_orig, n, m, l,
+                                  idx->qf.as<double>(), idx->bf_qa.as<int64_t>(),
+                                  qmask ? idx->bf_qm.as<int64_t>() : nullptr, q, k, alpha,
+                                  idx->code_lo, idx->code_stride, gthr, idx->st));
+      idx->launches += 1;
+      dump("code");
+    }
+    if (seed_tiles > 0) {
+      CKL(pass(seed_tiles, 1, 0));
+      CKL(sb::launch_tf_select(lists, q, nl, k, gthr, idx->st));
+      idx->launches += 1;
+      dump("seed");
+    }
     CKL(pass(0, 1, 0));
     CKL(sb::launch_tf_select(lists, q, nl, k, gthr, idx->st));
+    dump("full");
     CKL(pass(0, 0, 1));
     idx->launches += 2;
+  } else if (seed_tiles > 0) {
+    CKL(pass(seed_tiles, 0, 0));
+    CKL(pass(0, 0, 0));
   } else {
     CKL(pass(0, 0, 0));
   }

@@ -157,6 +157,11 @@ int launch_bf_tf(const float* Ft, const float* nxd, const int32_t* code,
                  int strided, int bound_only, int fixed, float* lists, cudaStream_t st);
 // large k: gthr[g] = the k-th smallest of the q x nl per-thread list keys (bf_tf.cu)
 int launch_tf_select(const float* lists, int64_t q, int nl, int k, int* gthr, cudaStream_t st);
+// exact seed bound of each query's k-th key from the nodes of its own attribute-code run
+int launch_tf_code_seed(const float* F, const int32_t* A, const int32_t* s_code, const int32_t* s_orig,
+                        int64_t n, int m, int l, const double* qf, const int64_t* qa,
+                        const int64_t* qmask, int64_t q, int k, double alpha, const int32_t* lo8,
+                        const int64_t* stride8, int* gthr, cudaStream_t st);
 int launch_tf_refine(const float* F, const int32_t* A, int m, int l, const double* qf,
                      const int64_t* qa, const int64_t* qmask, int64_t q, int k, double alpha,
                      const uint32_t* cnt, const uint64_t* cand, int splits, int hsegs, int qblock,
