@@ -1782,15 +1782,18 @@ static int route_dev(sb_index* idx, const double* qf, const double* qa, const do
   if (const char* e = getenv("SB_ROUTE_LPR")) a.lpr = std::max(1, std::min(32, next_pow2(atoi(e))));
   a.pf_rows = 1;
   if (const char* e = getenv("SB_ROUTE_PF")) a.pf_rows = atoi(e);
-  // real-valued rows: certified fp32 filter (coalesced, lanes split each row) in front of the
-  // exact sequential fp64 evaluation of the rows that can still enter the result list
-  // (route.cu kModeF64Filt); SB_ROUTE_FILT=0 evaluates every row exactly
+  // real-valued rows: SB_ROUTE_FILT=1 puts a certified fp32 filter (coalesced, lanes split
+  // each row) in front of the exact sequential fp64 evaluation of the rows that can still enter
+  // the result list (route.cu kModeF64Filt).  Off by default: measured slower (cfg 4: 38.7 vs
+  // 29.3 ms, cfg 5 cardinality 10: 29.6 vs 20.6 ms; a batch almost always has a survivor, so
+  // the exact chain stays on the critical path and the filter adds a pass)
   {
     const int nq = idx->m / 4;
     int lpr = 8;
     while (lpr < 32 && lpr * 4 < nq) lpr *= 2;
-    a.flt_lpr = (idx->m % 4 == 0 && !idx->force_sequential) ? lpr : 0;
-    if (const char* e = getenv("SB_ROUTE_FILT")) a.flt_lpr = atoi(e) != 0 ? a.flt_lpr : 0;
+    a.flt_lpr = 0;
+    if (const char* e = getenv("SB_ROUTE_FILT"))
+      a.flt_lpr = (atoi(e) != 0 && idx->m % 4 == 0 && !idx->force_sequential) ? lpr : 0;
   }
   // integer features in [0, 255]: route over a u8 copy with dp4a dot products (exact), unless
   // SB_ROUTE_U8=0; built once per layout
@@ -1817,9 +1820,9 @@ static int route_dev(sb_index* idx, const double* qf, const double* qa, const do
     }
     a.meta16 = reinterpret_cast<const uint4*>(idx->meta16.p);
   }
-  idx->last_route_path = sb::route_path(a);
   a.gr_d = nullptr;
   a.gr_i = nullptr;
+  idx->last_route_path = sb::route_path(a);
   size_t per_warp = sb::route_smem_per_warp(a);
   // large K (thousands to tens of thousands): once shared-memory result
   // lists would hold the SM below 16 resident queries, each slot's R lives in global memory

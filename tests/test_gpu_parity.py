@@ -234,8 +234,7 @@ def test_route_large_k_insertion_buffer(relabel, g, path, monkeypatch):
         np.testing.assert_array_equal(got[0], want[0], err_msg=f"k={k}")
         np.testing.assert_array_equal(got[1], want[1], err_msg=f"k={k}")
         np.testing.assert_array_equal(got[2][:, :4], want[2], err_msg=f"k={k}")
-    # real-valued rows take the certified fp32 filter in front of the exact fp64 rows
-    want_path = {"u8": "u8-dp4a", "fp32": "fp32", "fp64": "fp32-filter+fp64"}[path]
+    want_path = {"u8": "u8-dp4a", "fp32": "fp32", "fp64": "fp64"}[path]
     assert gr.device().route_info()["path"] == want_path
 
 
@@ -305,9 +304,9 @@ def test_order_free_mode_is_bit_exact():
         assert dev.route_info()["path"] == "fp32"
         split = with_env({"SB_ROUTE_U8": "0", "SB_ROUTE_LPR": "8"}, run)
         f64 = with_env({"SB_ROUTE_F32": "0"}, run)
-        assert dev.route_info()["path"] == "fp32-filter+fp64"
-        f64u = with_env({"SB_ROUTE_F32": "0", "SB_ROUTE_FILT": "0"}, run)
         assert dev.route_info()["path"] == "fp64"
+        f64u = with_env({"SB_ROUTE_F32": "0", "SB_ROUTE_FILT": "1"}, run)
+        assert dev.route_info()["path"] == "fp32-filter+fp64"
         dev.set_distance_mode(sequential=True)
         seq = sb.search_batch_arrays(graph, qf, qa, p)
         dev.set_distance_mode(sequential=False)

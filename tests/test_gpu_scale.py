@@ -140,7 +140,8 @@ def test_search_results_survive_later_calls(small_golden):
 
 @pytest.mark.parametrize("kind", ["shell", "offset", "wide"])
 def test_route_filter_near_ties_exact(kind, monkeypatch):
-    """The certified fp32 filter of real-valued routing (route.cu kModeF64Filt) must never drop
+    """The certified fp32 filter of real-valued routing (route.cu kModeF64Filt, SB_ROUTE_FILT=1;
+    off by default) must never drop
     a row that can enter the result list: rows on a thin shell around the query (distances
     equal to ~1e-9 relative, below fp32 resolution), rows far from the origin (the query's
     rounding to fp32 dominates), and d = 960 (cfg 4's width).  Ids, fp64 distances and the
@@ -170,11 +171,12 @@ def test_route_filter_near_ties_exact(kind, monkeypatch):
                              nbr_dists=np.zeros((n, g), np.float32), nbr_counts=cnt, frozen=True)
     for k in (5, 64):
         p = sb.SearchParams(k=k, seed=4)
+        monkeypatch.setenv("SB_ROUTE_FILT", "1")
         got = sb.search_batch_arrays(graph, qf, qa, p)
         assert graph.device().route_info()["path"] == "fp32-filter+fp64"
-        monkeypatch.setenv("SB_ROUTE_FILT", "0")
-        plain = sb.search_batch_arrays(graph, qf, qa, p)
         monkeypatch.delenv("SB_ROUTE_FILT")
+        plain = sb.search_batch_arrays(graph, qf, qa, p)
+        assert graph.device().route_info()["path"] == "fp64"
         want = O.search_batch(f, a, ids, cnt, 0.8, qf, qa, k, seed=4)
         for x, y, z in zip(got, plain, want):
             np.testing.assert_array_equal(x[:, :z.shape[1]] if x.ndim == 2 else x, z, err_msg=f"{kind} k={k}")
