@@ -56,6 +56,8 @@ def parse_args():
     p.add_argument("--cpu-seconds", type=float, default=12.0)
     p.add_argument("--no-topk", action="store_true",
                    help="skip the exhaustive top-k tensor-core rooflines")
+    p.add_argument("--no-legs", action="store_true",
+                   help="skip the real-valued routing legs (cfg 4, cfg 5 cardinality 10)")
     p.add_argument("--no-cpu-build", action="store_true",
                    help="skip the CPU oracle build + graph parity of the mine arm")
     return p.parse_args()
@@ -384,6 +386,7 @@ def run_mine(args, rank, world, local):
 
     cpu = None
     topk = None
+    legs = None
     cpu_build = None
     parity = None
     if rank == 0 and world == 1:
@@ -393,7 +396,7 @@ def run_mine(args, rank, world, local):
         if not args.no_cpu_build:
             cpu_build, parity = cpu_build_and_parity(g, cfg, X, A, QX, QA, gt)
         if not args.no_topk:
-            topk = topk_rooflines(g, cfg, QX, QA)
+            topk, legs = topk_and_legs(g, cfg, QX, QA, legs=not args.no_legs)
 
     if rank == 0:
         line = {
@@ -430,6 +433,7 @@ def run_mine(args, rank, world, local):
             "parity": parity,
             "sharded_ground_truth": sharded_gt,
             "roofline_topk": topk,
+            "routing_legs": legs,
         }
         print(json.dumps(line), flush=True)
     if world > 1:
@@ -526,12 +530,75 @@ def _topk_entry(dev, QX, QA, k, alpha, n, m, peak, unit, peak_src):
             "frac": round(rate / peak, 4), "peak_source": peak_src}
 
 
-def topk_rooflines(g, cfg, QX, QA):
+def routing_leg(name, X, A, QX, QA, card, kcap=4000):
+    """A real-valued routing leg on another BASELINE config: HELP build, exact
+    ground truth, the K sweep to Recall@10 >= 0.95 through the public API, then the routing
+    kernel alone at K* over the full query batch (device-resident inputs, CUDA events) against
+    the HBM roofline by §8(d)'s bytes, and the public-API QPS (host arrays in and out)."""
+    import torch
+    import paper_2604_01617_b200 as sb
+    from paper_2604_01617_b200.device import entry_points_host
+    g, cfg, build_s = build_index(X, A, card)
+    kstar, table, _, gt_s = sweep_operating_point(g, cfg, X, A, QX, QA, kcap)
+    q, m = QX.shape
+    l = A.shape[1]
+    params = sb.SearchParams(k=kstar)
+    t0 = time.perf_counter()
+    sb.search_batch_arrays(g, QX, QA, params)
+    api_s = time.perf_counter() - t0
+    dev = g.device()
+    stream = torch.cuda.Stream()
+    dev.set_stream(stream.cuda_stream)
+    qf_d = torch.from_numpy(np.ascontiguousarray(QX, np.float64)).cuda()
+    qa_d = torch.from_numpy(np.ascontiguousarray(QA, np.float64)).cuda()
+    ent_d = torch.from_numpy(entry_points_host(X.shape[0], kstar, 0, 0, q)).cuda()
+    ids_d = torch.empty((q, kstar), dtype=torch.int64, device="cuda")
+    dists_d = torch.empty((q, kstar), dtype=torch.float64, device="cuda")
+    st_d = torch.empty((q, 5), dtype=torch.int64, device="cuda")
+
+    def run():
+        dev.route_dev(qf_d.data_ptr(), qa_d.data_ptr(), None, q, kstar, params.resolved_pioneer_size(),
+                      1.0 / cfg.alpha, ids_d.data_ptr(), dists_d.data_ptr(), st_d.data_ptr(),
+                      entries_ptr=ent_d.data_ptr())
+    run()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    reps = 3
+    e0.record(stream)
+    for _ in range(reps):
+        run()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / reps
+    dev.set_stream(None)
+    st = st_d.cpu().numpy()
+    abytes = algorithmic_bytes(st, m, l)
+    peak, src = measured_hbm_peak()
+    log = g.build_log
+    out = {"workload": f"{name}: N={X.shape[0]:,} d={m} L={l} cards={list(card)} Q={q} k=10",
+           "operating_K": int(kstar), "recall_at_10": table[-1]["recall_at_10"],
+           "distance_path": dev.route_info()["path"],
+           "build_s": round(build_s, 3), "build_seconds_prune": round(log.get("seconds_prune", 0.0), 3),
+           "build_iterations_s": [round(x, 3) for x in log.get("seconds_iterations", [])],
+           "reinforce_overflow_rows": log.get("reinforce_overflow_rows"),
+           "gt_s": round(gt_s, 3), "kernel_ms": round(ms, 3), "qps_kernel": round(q / ms * 1e3, 1),
+           "qps_public_api": round(q / api_s, 1), "mean_dist_evals": float(st[:, 0].mean()),
+           "roofline": {"bound": "hbm", "achieved": round(abytes / (ms / 1e3) / 1e9, 1), "peak": peak,
+                        "unit": "GB/s", "frac": round(abytes / (ms / 1e3) / 1e9 / peak, 4),
+                        "algorithmic_bytes_per_launch": abytes, "peak_source": src}}
+    dev.close()  # free the leg's device index before the next leg
+    g._device = None
+    return out
+
+
+def topk_and_legs(g, cfg, QX, QA, legs=True):
     """Exhaustive AUTO top-k (oracle_auto_topk, evaluate.py:32-55) on the tensor cores, each
     against the measured dense peak of its precision: this config's ground truth (cfg 2: u8
     operands, tcgen05 kind::i8, exact; INT8 peak), cfg 3 at k = 10 and k = 100 and cfg 4 (both
     from the tools/configs.py recipes) on the TF32 filter + exact re-rank (TF32 peak).
-    achieved = 2 q n d useful ops / the tensor-core pass (CUDA events inside the C ABI)."""
+    achieved = 2 q n d useful ops / the tensor-core pass (CUDA events inside the C ABI).
+    With `legs`, the real-valued routing legs of cfg 4 and cfg 5 (cardinality 10) on the same
+    generated data (routing_leg)."""
     import paper_2604_01617_b200 as sb
     from paper_2604_01617_b200.device import DeviceIndex
     from tools.configs import make_config
@@ -540,19 +607,25 @@ def topk_rooflines(g, cfg, QX, QA):
     i8_src = "measured here: torch._int_mm s8 8192^3 best of 10"
     tf_src = "measured here: cuBLAS TF32 8192^3 best of 10"
     out = {"peaks": {"int8_tops": round(i8, 1), "tf32_tflops": round(tf, 1)}}
+    route_legs = {}
     dev = g.device()
     n, m = g.features.shape
     out["bench_config"] = _topk_entry(dev, QX, QA, 10, cfg.alpha, n, m, i8, "TOP/s", i8_src)
-    for name, ks in (("cfg3", (10, 100)), ("cfg4", (10,))):
-        X, A, QXc, QAc, _ = make_config(name)
-        mc = sb.compute_alpha(sb.sample_statistics(X, A, 1000, seed=0), X.shape[0], A.shape[1])
-        d = DeviceIndex(X, A, 2)
-        for k in ks:
-            out[f"{name}_k{k}"] = _topk_entry(d, QXc, QAc, k, mc.alpha, X.shape[0], X.shape[1],
-                                              tf, "TFLOP/s", tf_src)
-        d.close()
+    for name, ks in (("cfg3", (10, 100)), ("cfg4", (10,)), ("cfg5c10", ())):
+        if not ks and not legs:
+            continue
+        X, A, QXc, QAc, card = make_config(name)
+        if ks:
+            mc = sb.compute_alpha(sb.sample_statistics(X, A, 1000, seed=0), X.shape[0], A.shape[1])
+            d = DeviceIndex(X, A, 2)
+            for k in ks:
+                out[f"{name}_k{k}"] = _topk_entry(d, QXc, QAc, k, mc.alpha, X.shape[0], X.shape[1],
+                                                  tf, "TFLOP/s", tf_src)
+            d.close()
+        if legs and name in ("cfg4", "cfg5c10"):
+            route_legs[name] = routing_leg(name, X, A, QXc, QAc, card)
         del X, A
-    return out
+    return out, route_legs
 
 
 def cpu_baseline(g, cfg, QX, QA, kstar, seconds, ids_gpu):
