@@ -1029,6 +1029,22 @@ static int reconnect_sweep(sb_index* idx, double sigma, int* ran) {
   idx->launches += 2;
   *ran = 0;
   if (mn >= 1) return SB_OK;
+  if (getenv("SB_RC_DEBUG")) {
+    std::vector<int32_t> deg(n), cnt(n), ids((size_t)n * g);
+    cudaMemcpy(deg.data(), idx->in_deg.p, 4 * n, cudaMemcpyDeviceToHost);
+    cudaMemcpy(cnt.data(), idx->counts.p, 4 * n, cudaMemcpyDeviceToHost);
+    cudaMemcpy(ids.data(), idx->ids.p, 4 * (size_t)n * g, cudaMemcpyDeviceToHost);
+    int64_t z = 0, zfull = 0, zdeg0 = 0, full = 0;
+    for (int64_t v = 0; v < n; ++v) {
+      full += cnt[v] >= g;
+      if (deg[v] > 0) continue;
+      ++z;
+      if (cnt[v] == 0) { ++zdeg0; continue; }
+      zfull += cnt[ids[(size_t)v * g]] >= g;
+    }
+    fprintf(stderr, "[rc] zero-in-degree %lld, first target full %lld, no out-edges %lld, full rows %lld\n",
+            (long long)z, (long long)zfull, (long long)zdeg0, (long long)full);
+  }
   CKL(sb::launch_reconnect(idx->F.as<float>(), idx->A.as<int32_t>(), idx->m, idx->l, g,
                            idx->ids.as<int32_t>(), idx->dists.as<float>(), idx->counts.as<int32_t>(),
                            idx->in_deg.as<int32_t>(), sigma, n, idx->st));

@@ -509,8 +509,113 @@ struct RcShared {
   int result, total, pos, flag;
 };
 
+// Redundancy bits of the merged list mi[0..total) relative to row owner j (bit u of row t,
+// u < t: attrs_equal && cos > sigma) and the norms |p - j|^2, by the whole CTA: dimension
+// chunks of every listed row are staged in shared memory (coalesced) and each thread owns up
+// to two 4 x 4 tiles of the lower triangle of pair dots in registers, so a row is read once
+// per chunk instead of once per pair.  Every dot, norm and cosine is accumulated in ascending
+// dimension order with separately rounded fp64 operations (_kernels.py:236-253): the same
+// values as the per-pair loops.
+constexpr int kRcDc = 32;  // dimensions per staged chunk
+SB_DEV void cta_pair_bits(const SeqCtx& c, const int64_t* mi, int total, int64_t j, double* nrm,
+                          uint32_t* bits, int W, float* xr, double* xs) {
+  const int tid = threadIdx.x;
+  const int cpad = (total + kPT - 1) / kPT * kPT;
+  const int nb = cpad / kPT;
+  const int ntiles = nb * (nb + 1) / 2;
+  for (int t = tid; t < c.m; t += kRcThreads) xs[t] = (double)__ldg(c.F + j * c.m + t);
+  for (int w = tid; w < total * W; w += kRcThreads) bits[w] = 0u;
+  // passes of two tiles per thread (one pass covers up to 123 list entries); the norms of list
+  // entries tid and tid + kRcThreads accumulate during the first pass
+  for (int pass = 0; pass * 2 * kRcThreads < ntiles; ++pass) {
+    int tbs[2], ubs[2];
+    bool have[2];
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int ti = pass * 2 * kRcThreads + h * kRcThreads + tid;
+      have[h] = ti < ntiles;
+      int tb = 0, ub = 0;
+      if (have[h]) {
+        tb = (int)((sqrt(8.0 * ti + 1.0) - 1.0) * 0.5);
+        while ((tb + 1) * (tb + 2) / 2 <= ti) ++tb;
+        while (tb * (tb + 1) / 2 > ti) --tb;
+        ub = ti - tb * (tb + 1) / 2;
+      }
+      tbs[h] = tb;
+      ubs[h] = ub;
+    }
+    double acc[2][kPT][kPT];
+#pragma unroll
+    for (int h = 0; h < 2; ++h)
+#pragma unroll
+      for (int u = 0; u < kPT; ++u)
+#pragma unroll
+        for (int w = 0; w < kPT; ++w) acc[h][u][w] = 0.0;
+    double nacc[2] = {0.0, 0.0};
+    for (int d0 = 0; d0 < c.m; d0 += kRcDc) {
+      const int dc = c.m - d0 < kRcDc ? c.m - d0 : kRcDc;
+      __syncthreads();
+      for (int e = tid; e < cpad * dc; e += kRcThreads) {
+        const int t = e / dc, dd = e - t * dc;
+        xr[dd * cpad + t] = t < total ? __ldg(c.F + mi[t] * c.m + d0 + dd) : 0.f;
+      }
+      __syncthreads();
+      if (pass == 0)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int t = tid + h * kRcThreads;
+          if (t < total)
+            for (int dd = 0; dd < dc; ++dd) {
+              const double dp = dsub((double)xr[dd * cpad + t], xs[d0 + dd]);
+              nacc[h] = dadd(nacc[h], dmul(dp, dp));
+            }
+        }
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        if (!have[h]) continue;
+        for (int dd = 0; dd < dc; ++dd) {
+          const float* row = xr + (size_t)dd * cpad;
+          const double xsd = xs[d0 + dd];
+          const float4 tv = *reinterpret_cast<const float4*>(row + tbs[h] * kPT);
+          const float4 uv = *reinterpret_cast<const float4*>(row + ubs[h] * kPT);
+          const double dt[4] = {dsub((double)tv.x, xsd), dsub((double)tv.y, xsd),
+                                dsub((double)tv.z, xsd), dsub((double)tv.w, xsd)};
+          const double du[4] = {dsub((double)uv.x, xsd), dsub((double)uv.y, xsd),
+                                dsub((double)uv.z, xsd), dsub((double)uv.w, xsd)};
+#pragma unroll
+          for (int u = 0; u < kPT; ++u)
+#pragma unroll
+            for (int w = 0; w < kPT; ++w) acc[h][u][w] = dadd(acc[h][u][w], dmul(dt[u], du[w]));
+        }
+      }
+    }
+    if (pass == 0)
+#pragma unroll
+      for (int h = 0; h < 2; ++h)
+        if (tid + h * kRcThreads < total) nrm[tid + h * kRcThreads] = nacc[h];
+    __syncthreads();
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      if (!have[h]) continue;
+#pragma unroll
+      for (int u = 0; u < kPT; ++u)
+#pragma unroll
+        for (int w = 0; w < kPT; ++w) {
+          const int t = tbs[h] * kPT + u, v = ubs[h] * kPT + w;
+          if (t >= total || v >= t) continue;
+          if (!seq_attrs_equal(c, mi[t], mi[v])) continue;
+          const double np2 = nrm[t], nk2 = nrm[v];
+          const double cs = (np2 == 0.0 || nk2 == 0.0) ? 1.0 : __ddiv_rn(acc[h][u][w], sqrt(dmul(np2, nk2)));
+          if (cs > c.sigma) atomicOr(bits + t * W + (v >> 5), 1u << (v & 31));
+        }
+    }
+  }
+  __syncthreads();
+}
+
 // returns 1 if cand ends up in row j (all threads get the value)
-SB_DEV int cta_try_insert(SeqCtx& c, RcShared& S, uint32_t* bits, int64_t j, int64_t cand, double dd) {
+SB_DEV int cta_try_insert(SeqCtx& c, RcShared& S, uint32_t* bits, int64_t j, int64_t cand, double dd,
+                          float* xr, double* xs) {
   const int tid = threadIdx.x;
   const float d = __double2float_rn(dd);
   int32_t* ri = c.ids + j * c.g;
@@ -556,47 +661,12 @@ SB_DEV int cta_try_insert(SeqCtx& c, RcShared& S, uint32_t* bits, int64_t j, int
   }
   const int total = S.total;
   const int W = (total + 31) >> 5;
-  const float* xj = c.F + j * c.m;
   for (int t = tid; t < total; t += kRcThreads) {
     const int64_t p = S.mi[t];
-    const float* xp = c.F + p * c.m;
-    double np2 = 0.0;
-    for (int u = 0; u < c.m; ++u) {
-      const double dp = dsub((double)xp[u], (double)xj[u]);
-      np2 = dadd(np2, dmul(dp, dp));
-    }
-    S.nrm[t] = np2;
     S.midg[t] = p == cand ? 0 : c.in_deg[p];
     S.keep[t] = 1;
   }
-  for (int w = tid; w < total * W; w += kRcThreads) bits[w] = 0u;
-  __syncthreads();
-  // pair (t, u), u < t, enumerated over the lower triangle
-  const int pairs = total * (total - 1) / 2;
-  for (int e = tid; e < pairs; e += kRcThreads) {
-    int t = (int)((sqrt(8.0 * e + 1.0) + 1.0) * 0.5);
-    while (t * (t - 1) / 2 > e) --t;
-    while ((t + 1) * t / 2 <= e) ++t;
-    const int u = e - t * (t - 1) / 2;
-    const int64_t p = S.mi[t], k = S.mi[u];
-    if (!seq_attrs_equal(c, p, k)) continue;
-    double cs;
-    if (S.nrm[t] == 0.0 || S.nrm[u] == 0.0) {
-      cs = 1.0;
-    } else {
-      const float* xp = c.F + p * c.m;
-      const float* xk = c.F + k * c.m;
-      double dot = 0.0;
-      for (int q = 0; q < c.m; ++q) {
-        const double dp = dsub((double)xp[q], (double)xj[q]);
-        const double dk = dsub((double)xk[q], (double)xj[q]);
-        dot = dadd(dot, dmul(dp, dk));
-      }
-      cs = __ddiv_rn(dot, sqrt(dmul(S.nrm[t], S.nrm[u])));
-    }
-    if (cs > c.sigma) atomicOr(bits + t * W + (u >> 5), 1u << (u & 31));
-  }
-  __syncthreads();
+  cta_pair_bits(c, S.mi, total, j, S.nrm, bits, W, xr, xs);
   if (tid == 0) {
     // kept mask over list positions; at step t it holds exactly the kept u < t
     uint32_t km[(kRcMaxG + 32) / 32];
@@ -645,6 +715,11 @@ SB_DEV int cta_try_insert(SeqCtx& c, RcShared& S, uint32_t* bits, int64_t j, int
 
 __global__ void __launch_bounds__(kRcThreads) reconnect_cta_kernel(SeqCtx c, int64_t n) {
   extern __shared__ __align__(16) uint32_t rc_bits[];
+  // dynamic shared memory: bits [(g + 1) x W words] | staged chunk [kRcDc x cpad floats] | owner row [m doubles]
+  const int cpad_max = (c.g + 1 + kPT - 1) / kPT * kPT;
+  const size_t bits_words = (size_t)(c.g + 1) * ((c.g + 32) / 32);
+  float* rc_xr = reinterpret_cast<float*>(rc_bits + ((bits_words + 3) & ~(size_t)3));
+  double* rc_xs = reinterpret_cast<double*>(rc_xr + (size_t)kRcDc * cpad_max);
   __shared__ RcShared S;
   const int tid = threadIdx.x;
   const volatile int32_t* indeg = c.in_deg;
@@ -667,7 +742,7 @@ __global__ void __launch_bounds__(kRcThreads) reconnect_cta_kernel(SeqCtx c, int
       const int cv = c.counts[v];
       for (int t = 0; t < cv && !done; ++t) {
         const int64_t u = c.ids[v * c.g + t];
-        done = cta_try_insert(c, S, rc_bits, u, v, (double)c.dists[v * c.g + t]) != 0;
+        done = cta_try_insert(c, S, rc_bits, u, v, (double)c.dists[v * c.g + t], rc_xr, rc_xs) != 0;
       }
       if (tid == 0 && !done) {
         for (int t = 0; t < c.counts[v] && !done; ++t) {
@@ -694,7 +769,10 @@ int launch_reconnect(const float* F, const int32_t* A, int m, int l, int g, int3
   c.F = F; c.A = A; c.m = m; c.l = l; c.g = g;
   c.ids = ids; c.dists = dists; c.counts = counts; c.in_deg = in_deg; c.sigma = sigma;
   if (g > kRcMaxG) return (int)cudaErrorInvalidValue;
-  const size_t bits = sizeof(uint32_t) * (size_t)(g + 1) * ((g + 32) / 32);
+  const int cpad_max = (g + 1 + kPT - 1) / kPT * kPT;
+  const size_t bits_words = (size_t)(g + 1) * ((g + 32) / 32);
+  const size_t bits = sizeof(uint32_t) * ((bits_words + 3) & ~(size_t)3) + sizeof(float) * (size_t)kRcDc * cpad_max +
+                      sizeof(double) * (size_t)m + 16;
   cudaError_t e = cudaFuncSetAttribute(reconnect_cta_kernel,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bits);
   if (e != cudaSuccess) return (int)e;
