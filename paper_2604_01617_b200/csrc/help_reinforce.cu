@@ -642,13 +642,18 @@ __global__ void rf_simulate_kernel(RfArgs a) {
         // mirrored in by O sources processed earlier (linked list, sorted here)
         int nd = 0;
         if (lane == 0) {
+          // records published by other groups' warps: read past L1 (a line cached before
+          // the record was written would hand back stale words; the writer's fence orders
+          // the record before its list link)
           const volatile int64_t* vnext = a.rec_next;
+          const volatile uint64_t* vkey = a.rec_key;
+          const volatile int32_t* vcu = a.rec_cu;
           for (int64_t r = rh; r >= 0; r = vnext[r]) {
-            const uint64_t rk = a.rec_key[r];
+            const uint64_t rk = vkey[r];
             if (!in_grp(a.o_idx[key_id(rk)])) continue;  // another group's mirror
             if (nd < a.dyn_cap) {
               uint64_t kk = row_key(key_dist(rk), key_id(rk));
-              const int cr = a.rec_cu[r];
+              const int cr = vcu[r];
               int pos = nd;
               while (pos > 0 && dyn[pos - 1] > kk) {
                 dyn[pos] = dyn[pos - 1];
