@@ -38,9 +38,15 @@ int cuda_fail(cudaError_t e, const char* what) {
     if (e_ != cudaSuccess) return cuda_fail(e_, #expr);       \
   } while (0)
 
+// SB_SYNC_CHECK=1 (debugging): synchronize after every launch so a fault names its kernel
+static bool sync_check() {
+  static const bool on = [] { const char* e = getenv("SB_SYNC_CHECK"); return e && atoi(e) != 0; }();
+  return on;
+}
 #define CKL(expr)                                                          \
   do {                                                                     \
     int r_ = (expr);                                                       \
+    if (r_ == 0 && sync_check()) r_ = (int)cudaDeviceSynchronize();        \
     if (r_ != 0) return cuda_fail((cudaError_t)r_, #expr);                 \
   } while (0)
 
