@@ -28,6 +28,8 @@
 #include "tc_ptx.cuh"
 #include "sb_internal.h"
 
+#include <cub/device/device_radix_sort.cuh>
+
 namespace sb {
 
 constexpr int kTcM = 128;       // queries per CTA (UMMA M)
@@ -116,6 +118,10 @@ struct TcArgs {
   double* part_d;           // q x (2 splits) x kk
   uint32_t* part_i;
   int* gthr;                // q: best list-tail bound of the query over all CTAs (fp32 bits)
+  // u8 path: per 16-node chunk {min |x|^2, the chunk's attribute code or -1 when mixed}; nodes
+  // are ordered by |x|^2 inside each attribute tuple, so 2 max(x.q) - min |x|^2 bounds the
+  // chunk's y tightly and skips it on raw accumulators
+  const int2* cmeta;
 };
 
 // One CTA = 128 queries x one node range, 9 warps:
@@ -142,7 +148,7 @@ __global__ void __launch_bounds__(kTcThreads + 32, CTAS) bf_tc_kernel(TcArgs a) 
   const int m = a.m, N = a.N, l = a.l;
   const int rowb = m * ESZ;        // operand bytes per row
   const size_t b_bytes = (size_t)N * rowb;
-  const size_t meta_bytes = (size_t)N * (3 + l) * 4;
+  const size_t meta_bytes = (size_t)N * (3 + l) * 4 + (U8 ? (size_t)(N / 16) * 8 : 0);
   // shared layout: A tile | 2 x B tile | 2 x (nx | code | orig | attrs) | lists | t2 | barriers
   char* p = smem;
   char* sA = p; p += (size_t)kTcM * rowb;
@@ -213,8 +219,9 @@ __global__ void __launch_bounds__(kTcThreads + 32, CTAS) bf_tc_kernel(TcArgs a) 
         bulk_g2s(smem_u32(sB + s * b_bytes), a.Fb + (size_t)v0 * rowb, (uint32_t)b_bytes,
                  bar_fullB + 8 * s);
       };
-      // NBS >= 2: a ring of row stages, the first NBS tiles in flight before any MMA
-      for (int j = 0; j < (NBS == 1 ? 1 : NBS) && j < ntl; ++j) load_rows(j);
+      // NBS == 1: this lane loads each tile's rows once the previous MMA is done; NBS >= 2:
+      // lane 2 keeps the ring of row stages full on its own (below)
+      if (NBS == 1 && ntl > 0) load_rows(0);
       mbar_wait(bar_a, 0);
       // BF16 x BF16 -> F32, or U8 x U8 -> S32 (c_format bits [4,6), a/b formats [7,13))
       const uint32_t idesc = (U8 ? (2u << 4) : ((1u << 4) | (1u << 7) | (1u << 10))) |
@@ -254,15 +261,19 @@ __global__ void __launch_bounds__(kTcThreads + 32, CTAS) bf_tc_kernel(TcArgs a) 
             load_rows(i + 1);
           }
         } else {
-          mma_commit(bar_freeB + 8 * sb);
-          // refill the stage of tile i - 1 (its MMAs have had a tile's time to finish) with
-          // tile i - 1 + NBS
-          if (i >= 1 && i - 1 + NBS < ntl) {
-            const int s1 = (i - 1) % NBS;
-            mbar_wait(bar_freeB + 8 * s1, (uint32_t)(((i - 1) / NBS) & 1));
-            load_rows(i - 1 + NBS);
-          }
+          mma_commit(bar_freeB + 8 * sb);  // the stage refills as soon as these MMAs complete
         }
+      }
+    } else if (NBS >= 2 && lane_id() == 2) {
+      // row loader: stage i % NBS gets tile i as soon as the MMAs of tile i - NBS are done, so
+      // up to NBS tiles are in flight whatever the epilogue does (issuing the refill from the
+      // MMA lane after MMA i - 1 left only NBS - 1 tiles of L2 latency covered)
+      for (int i = 0; i < ntl; ++i) {
+        const int sb = i % NBS;
+        if (i >= NBS) mbar_wait(bar_freeB + 8 * sb, (uint32_t)(((i / NBS) - 1) & 1));
+        const int64_t v0 = (t_begin + i) * (int64_t)N;
+        mbar_expect_tx(bar_fullB + 8 * sb, (uint32_t)b_bytes);
+        bulk_g2s(smem_u32(sB + sb * b_bytes), a.Fb + (size_t)v0 * rowb, (uint32_t)b_bytes, bar_fullB + 8 * sb);
       }
     } else if (lane_id() == 1) {
       // node metadata on its own ring, kTcMeta tiles ahead of the epilogue
@@ -277,6 +288,7 @@ __global__ void __launch_bounds__(kTcThreads + 32, CTAS) bf_tc_kernel(TcArgs a) 
         bulk_g2s(smem_u32(meta + N * 4), a.code + v0, (uint32_t)(N * 4), fm);
         bulk_g2s(smem_u32(meta + N * 8), a.orig + v0, (uint32_t)(N * 4), fm);
         bulk_g2s(smem_u32(meta + N * 12), a.A + v0 * l, (uint32_t)(N * l * 4), fm);
+        if (U8) bulk_g2s(smem_u32(meta + (size_t)N * (3 + l) * 4), a.cmeta + v0 / 16, (uint32_t)(N / 16 * 8), fm);
       }
     }
     __syncwarp();
@@ -319,6 +331,7 @@ __global__ void __launch_bounds__(kTcThreads + 32, CTAS) bf_tc_kernel(TcArgs a) 
       const int32_t* s_code = reinterpret_cast<const int32_t*>(meta) + N;
       const int32_t* s_orig = reinterpret_cast<const int32_t*>(meta) + 2 * N;
       const int32_t* s_at = reinterpret_cast<const int32_t*>(meta) + 3 * N;
+      const int2* s_cm = reinterpret_cast<const int2*>(meta + (size_t)N * (3 + l) * 4);
       const int64_t vb = (t_begin + i) * (int64_t)N;
       const int nvalid = (int)(a.n - vb < N ? a.n - vb : N);
       // the query's tightest bound published by any CTA: the value loaded one tile ago (its
@@ -335,9 +348,23 @@ __global__ void __launch_bounds__(kTcThreads + 32, CTAS) bf_tc_kernel(TcArgs a) 
         const int c0 = half * cols + c * 16;
         // columns are in attribute-grouped order: if both ends of the chunk carry the current
         // tuple, the whole chunk does, and one threshold covers all 16 columns
-        const bool uniform = s_code[c0] == last_code && s_code[c0 + 15] == last_code;
+        int2 cm = make_int2(0, -1);
+        if (U8) cm = s_cm[c0 >> 4];
+        const bool uniform = U8 ? cm.y == last_code : (s_code[c0] == last_code && s_code[c0 + 15] == last_code);
         unsigned cand = 0;
         if (U8) {
+          // the chunk test on raw dot products: y_j = 2 x_j.q - |x_j|^2 <= 2 max x.q - min |x|^2
+          // (exact int32; nodes sorted by |x|^2 inside a tuple keep the bound tight)
+          const int thri0 = thr < -2.0e9f ? INT_MIN : (thr > 2.0e9f ? INT_MAX : __float2int_rd(thr));
+          if (uniform) {
+            int t5[6];
+#pragma unroll
+            for (int j = 0; j < 5; ++j)
+              t5[j] = max(max((int)r[3 * j], (int)r[3 * j + 1]), (int)r[3 * j + 2]);
+            t5[5] = (int)r[15];
+            const int mr = max(max(max(t5[0], t5[1]), t5[2]), max(max(t5[3], t5[4]), t5[5]));
+            if (2 * mr - cm.x < thri0) continue;
+          }
           // int32 dot products and |x|^2: y = 2 x.q - |x|^2 and the test stay integer
           // (y >= thr  <=>  y >= floor(thr) for integer y, conservatively)
           const int32_t* s_nxi = reinterpret_cast<const int32_t*>(s_nx);
@@ -481,7 +508,7 @@ __global__ void __launch_bounds__(kTcThreads + 32, CTAS) bf_tc_kernel(TcArgs a) 
 
 // rowb = operand bytes per row (2 m for bf16, m for u8)
 size_t bf_tc_smem_n(int rowb, int l, int kk, int N, int nbs) {
-  return (size_t)kTcM * rowb + (size_t)nbs * N * rowb + kTcMeta * (size_t)N * (3 + l) * 4 +
+  return (size_t)kTcM * rowb + (size_t)nbs * N * rowb + kTcMeta * ((size_t)N * (3 + l) * 4 + (size_t)(N / 16) * 8) +
          (sizeof(double) + sizeof(uint32_t)) * (size_t)kk * kTcThreads + sizeof(float) * kTcThreads +
          8 + 8 * 24 + 16;
 }
@@ -607,6 +634,71 @@ __global__ void tc_gather_u8_kernel(const float* F, const int32_t* A, const int3
   for (int u = lane_id(); u < l; u += 32) As[p * l + u] = A[v * l + u];
 }
 
+// ---- |x|^2 order inside each attribute tuple, and the per-chunk records -----------------
+// key = (tuple code << 32) | |x|^2 of the node (integer data: exact); the node order keeps the
+// tuples contiguous and ascending, and within a tuple runs by |x|^2, so a 16-node chunk spans a
+// narrow |x|^2 range (the u8 epilogue's raw chunk test)
+__global__ void tc_norm_key_kernel(const float* F, int64_t n, int m, const int32_t* code_in,
+                                   const int32_t* orig, uint64_t* key, int32_t* val) {
+  const int64_t p = (int64_t)blockIdx.x * (blockDim.x >> 5) + warp_id();
+  if (p >= n) return;
+  const int64_t v = orig[p];
+  long long acc = 0;
+  for (int t = lane_id(); t < m; t += 32) {
+    const long long x = (long long)F[v * m + t];
+    acc += x * x;
+  }
+  acc = warp_sum(acc);
+  if (lane_id() == 0) {
+    key[p] = ((uint64_t)(uint32_t)code_in[v] << 32) | (uint64_t)(acc > 0xFFFFFFFFll ? 0xFFFFFFFFll : acc);
+    val[p] = (int32_t)v;
+  }
+}
+
+__global__ void tc_chunk_meta_kernel(const int32_t* nx, const int32_t* code, int64_t n, int64_t nchunks,
+                                     int2* cm) {
+  const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= nchunks) return;
+  int mn = INT_MAX, cd = -1;
+  bool mixed = false;
+  for (int j = 0; j < 16; ++j) {
+    const int64_t p = c * 16 + j;
+    if (p >= n) { mixed = true; break; }
+    mn = min(mn, nx[p]);
+    if (j == 0) cd = code[p]; else mixed = mixed || code[p] != cd;
+  }
+  cm[c] = make_int2(mn == INT_MAX ? 0 : mn, mixed ? -1 : cd);
+}
+
+size_t tc_norm_order_scratch(int64_t n) {
+  size_t temp = 0;
+  cub::DeviceRadixSort::SortPairs(nullptr, temp, (const uint64_t*)nullptr, (uint64_t*)nullptr,
+                                  (const int32_t*)nullptr, (int32_t*)nullptr, (int)n);
+  return (size_t)n * (2 * sizeof(uint64_t) + sizeof(int32_t)) + temp + 1024;
+}
+
+int launch_tc_norm_order(const float* F, int64_t n, int m, const int32_t* code_in, int32_t* orig,
+                         void* scratch, cudaStream_t st) {
+  char* p = static_cast<char*>(scratch);
+  auto take = [&](size_t b) { char* r = p; p += (b + 255) & ~(size_t)255; return r; };
+  uint64_t* k_in = reinterpret_cast<uint64_t*>(take(sizeof(uint64_t) * n));
+  uint64_t* k_out = reinterpret_cast<uint64_t*>(take(sizeof(uint64_t) * n));
+  int32_t* v_in = reinterpret_cast<int32_t*>(take(sizeof(int32_t) * n));
+  size_t temp = 0;
+  cub::DeviceRadixSort::SortPairs(nullptr, temp, k_in, k_out, v_in, orig, (int)n);
+  void* d_temp = take(temp);
+  tc_norm_key_kernel<<<(unsigned)((n + 7) / 8), 256, 0, st>>>(F, n, m, code_in, orig, k_in, v_in);
+  cudaError_t e = cub::DeviceRadixSort::SortPairs(d_temp, temp, k_in, k_out, v_in, orig, (int)n, 0, 64, st);
+  return e != cudaSuccess ? (int)e : (int)cudaGetLastError();
+}
+
+int launch_tc_chunk_meta(const int32_t* nx, const int32_t* code, int64_t n, int64_t npad, void* cm,
+                         cudaStream_t st) {
+  const int64_t nch = npad / 16;
+  tc_chunk_meta_kernel<<<(unsigned)((nch + 255) / 256), 256, 0, st>>>(nx, code, n, nch, reinterpret_cast<int2*>(cm));
+  return (int)cudaGetLastError();
+}
+
 int launch_tc_gather_u8(const float* F, const int32_t* A, const int32_t* code_in,
                         const int32_t* orig, int64_t n, int m, int l, void* Fb, int32_t* nx,
                         int32_t* code, int32_t* As, cudaStream_t st) {
@@ -657,9 +749,10 @@ int launch_bf_tc(const void* Fb, const int32_t* nx, const int32_t* A, const int3
                  const int32_t* orig, const void* Qb, const int32_t* nq, const int64_t* qa,
                  const int64_t* qmask, int64_t n, int64_t q, int m, int l, int kk, int splits,
                  double alpha, double* part_d, uint32_t* part_i, int* gthr, int fold,
-                 int u8, cudaStream_t st) {
+                 int u8, const void* cmeta, cudaStream_t st) {
   TcArgs a;
   a.gthr = gthr;
+  a.cmeta = reinterpret_cast<const int2*>(cmeta);
   a.Fb = (const char*)Fb; a.nx = nx; a.A = A; a.code = code; a.orig = orig;
   a.Qb = (const char*)Qb;
   a.nq = nq; a.qa = qa; a.qmask = qmask; a.n = n; a.q = q; a.m = m; a.l = l; a.kk = kk;

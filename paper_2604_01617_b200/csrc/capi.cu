@@ -212,9 +212,12 @@ struct sb_index {
   DBuf ft, ft_meta, tq, tcand, tovf;
   DBuf bf_sort;                      // full-sort top-k scratch (bf_sort.cu: any k)
   DBuf tlists;                       // two-pass TF32 top-k: per-thread lists (q x threads x 32)
+  DBuf fb_cmeta, fb_scratch;         // u8 top-k: per-16-node chunk records; sort scratch
   ~sb_index() {
     bf_sort.release();
     tlists.release();
+    fb_cmeta.release();
+    fb_scratch.release();
     fb.release();
     f8.release();
     DBuf* tfb[] = {&ft, &ft_meta, &tq, &tcand, &tovf};
@@ -1554,12 +1557,19 @@ int sb_bf_topk_queries(sb_index* idx, const double* qf, const int64_t* qa, const
       int32_t* s_attr = s_orig + npad;
       int32_t* d_code = nullptr;
       { int r = node_order(idx, s_orig, &d_code); if (r) return r; }
-      if (u8)
+      if (u8) {
+        // |x|^2 order inside each tuple + per-chunk {min |x|^2, code} records (bf_tc.cu)
+        CK(idx->fb_scratch.ensure(sb::tc_norm_order_scratch(n)));
+        CKL(sb::launch_tc_norm_order(idx->F.as<float>(), n, idx->m, d_code, s_orig, idx->fb_scratch.p, idx->st));
         CKL(sb::launch_tc_gather_u8(idx->F.as<float>(), idx->A.as<int32_t>(), d_code, s_orig, n,
                                     idx->m, l, idx->fb.p, s_nx, s_code, s_attr, idx->st));
-      else
+        CK(idx->fb_cmeta.ensure(sizeof(int32_t) * 2 * (size_t)(npad / 16)));
+        CKL(sb::launch_tc_chunk_meta(s_nx, s_code, n, npad, idx->fb_cmeta.p, idx->st));
+        idx->fb_scratch.release();
+      } else {
         CKL(sb::launch_tc_gather(idx->F.as<float>(), idx->A.as<int32_t>(), d_code, s_orig, n,
                                  idx->m, mk, l, idx->fb.p, s_nx, s_code, s_attr, idx->st));
+      }
       idx->have_fb = true;
       idx->fb_mk = mk * esz;
       idx->have_cand = false;  // rev_* scratch was reused
@@ -1597,7 +1607,7 @@ int sb_bf_topk_queries(sb_index* idx, const double* qf, const int64_t* qa, const
       CK(idx->bf_event(0));
       CKL(sb::launch_bf_tc(idx->fb.p, s_nx, s_nx + 3 * npad, s_nx + npad, s_nx + 2 * npad, idx->qb.p,
                            d_nq, a.qa, a.qmask, n, q, mk, idx->l, kk, splits, alpha, a.part_d,
-                           a.part_i, d_gthr, fold ? 1 : 0, u8 ? 1 : 0, idx->st));
+                           a.part_i, d_gthr, fold ? 1 : 0, u8 ? 1 : 0, idx->fb_cmeta.p, idx->st));
       CK(idx->bf_event(1));
       idx->bf_ev_valid = true;
     }

@@ -132,10 +132,16 @@ int launch_tc_gather(const float* F, const int32_t* A, const int32_t* code_in, c
 int launch_bf_tc_prep_queries(const double* qf, int64_t q, int m, int mk, void* Qb, int32_t* nq,
                               cudaStream_t st);
 // m below is the operand K: the feature count, plus 16 when fold (|x|^2 folded into the MMA)
+// |x|^2 order inside attribute tuples (u8 tensor-core top-k) and its per-16-node chunk records
+size_t tc_norm_order_scratch(int64_t n);
+int launch_tc_norm_order(const float* F, int64_t n, int m, const int32_t* code_in, int32_t* orig,
+                         void* scratch, cudaStream_t st);
+int launch_tc_chunk_meta(const int32_t* nx, const int32_t* code, int64_t n, int64_t npad, void* cm,
+                         cudaStream_t st);
 int launch_bf_tc(const void* Fb, const int32_t* nx, const int32_t* A, const int32_t* code,
                  const int32_t* orig, const void* Qb, const int32_t* nq, const int64_t* qa,
                  const int64_t* qmask, int64_t n, int64_t q, int m, int l, int kk, int splits,
-                 double alpha, double* part_d, uint32_t* part_i, int* gthr, int fold, int u8,
+                 double alpha, double* part_d, uint32_t* part_i, int* gthr, int fold, int u8, const void* cmeta,
                  cudaStream_t st);
 
 // tensor-core query-mode top-k for real-valued data (bf_tf.cu): TF32 filter, exact re-rank
