@@ -167,27 +167,28 @@ RNG_HD uint64_t bounded(Pcg64* g, uint64_t rng) {
 RNG_HD bool choice_uses_tail_shuffle(int64_t n, int64_t k) { return n > 10000 && k > n / 50; }
 
 // Floyd's algorithm + shuffle, writing k distinct ids of [0, n).  `table` is scratch of
-// `tmask + 1` int64 slots (power of two >= k, any contents); open addressing, linear probe.
-RNG_HD void choice_floyd(Pcg64* g, int64_t n, int64_t k, int64_t* out, int64_t* table,
-                         uint64_t tmask) {
+// `tmask + 1` slots (power of two >= k, any contents); open addressing, linear probe.  T is
+// int64_t, or int32_t when n < 2^31 (the shared-memory variant of the entry kernel).
+template <class T>
+RNG_HD void choice_floyd(Pcg64* g, int64_t n, int64_t k, T* out, T* table, uint64_t tmask) {
   for (uint64_t i = 0; i <= tmask; ++i) table[i] = -1;
   for (int64_t j = n - k; j < n; ++j) {
     int64_t v = (int64_t)bounded(g, (uint64_t)j);
     uint64_t loc = (uint64_t)v & tmask;
-    while (table[loc] != -1 && table[loc] != v) loc = (loc + 1) & tmask;
+    while (table[loc] != -1 && (int64_t)table[loc] != v) loc = (loc + 1) & tmask;
     if (table[loc] == -1) {
-      table[loc] = v;
-      out[j - n + k] = v;
+      table[loc] = (T)v;
+      out[j - n + k] = (T)v;
     } else {
       loc = (uint64_t)j & tmask;
       while (table[loc] != -1) loc = (loc + 1) & tmask;
-      table[loc] = j;
-      out[j - n + k] = j;
+      table[loc] = (T)j;
+      out[j - n + k] = (T)j;
     }
   }
   for (int64_t i = k - 1; i > 0; --i) {
     int64_t j = (int64_t)bounded(g, (uint64_t)i);
-    int64_t t = out[i]; out[i] = out[j]; out[j] = t;
+    T t = out[i]; out[i] = out[j]; out[j] = t;
   }
 }
 

@@ -895,8 +895,41 @@ __global__ void entry_points_kernel(int64_t n, int K, uint64_t seed, int64_t qi0
   sbrng::entry_points(n, K, seed, (uint64_t)(qi0 + i), out + i * K, scratch + i * scratch_slots);
 }
 
+// The Floyd regime (the usual one: k <= n / 50 or n <= 10,000) with the hash table and the
+// output in shared memory as int32 (n < 2^31): every probe and shuffle swap is a shared-memory
+// access instead of a dependent global one.  One thread per query, kEpThreads per block.
+constexpr int kEpThreads = 32;  // threads per block at most (fewer for large k)
+__global__ void entry_points_smem_kernel(int64_t n, int K, uint64_t seed, int64_t qi0, int64_t q,
+                                         int64_t* out, int tslots) {
+  extern __shared__ int32_t ep_smem[];
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= q) return;
+  int32_t* table = ep_smem + (size_t)threadIdx.x * (tslots + K);
+  int32_t* o = table + tslots;
+  sbrng::Pcg64 g;
+  sbrng::pcg_from_entropy2(&g, seed, (uint64_t)(qi0 + i));
+  sbrng::choice_floyd<int32_t>(&g, n, K, o, table, (uint64_t)tslots - 1);
+  int64_t* dst = out + i * K;
+  for (int t = 0; t < K; ++t) dst[t] = o[t];
+}
+
 int launch_entry_points(int64_t n, int K, uint64_t seed, int64_t qi0, int64_t q, int64_t* out,
                         int64_t* scratch, uint64_t scratch_slots, cudaStream_t st) {
+  const uint64_t ts = sbrng::choice_table_size(n, K);
+  const size_t per = sizeof(int32_t) * (size_t)(ts + K);
+  int tpb = kEpThreads;
+  while (tpb > 1 && per * tpb > (size_t)200 * 1024) tpb >>= 1;
+  if (!sbrng::choice_uses_tail_shuffle(n, K) && n < (int64_t)0x7FFFFFFF && per * tpb <= (size_t)200 * 1024) {
+    static bool attr = false;
+    if (!attr) {
+      cudaFuncSetAttribute(entry_points_smem_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+      attr = true;
+    }
+    const int64_t gb = (q + tpb - 1) / tpb;
+    if (gb > 0)
+      entry_points_smem_kernel<<<(unsigned)gb, tpb, per * tpb, st>>>(n, K, seed, qi0, q, out, (int)ts);
+    return (int)cudaGetLastError();
+  }
   int bs = 128;
   int64_t gb = (q + bs - 1) / bs;
   if (gb > 0) entry_points_kernel<<<(unsigned)gb, bs, 0, st>>>(n, K, seed, qi0, q, out, scratch,
