@@ -15,7 +15,9 @@ KEYS = ("Duration", "DRAM Throughput", "Compute (SM) Throughput", "Issue Slots B
         "L1/TEX Hit Rate", "Warp Cycles Per Issued Instruction", "Eligible Warps Per Scheduler",
         "Grid Size", "Block Size", "Dynamic Shared Memory Per Block")
 RAW = ("dram__bytes_read.sum", "dram__bytes_write.sum", "gpu__time_duration.sum",
-       "sm__inst_executed.sum", "lts__t_bytes.sum")
+       "sm__inst_executed.sum", "lts__t_bytes.sum",
+       "sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_elapsed",
+       "dram__sectors_read.sum", "dram__sectors_write.sum")
 
 
 def ncu(*args):
