@@ -122,6 +122,7 @@ struct TcArgs {
   // are ordered by |x|^2 inside each attribute tuple, so 2 max(x.q) - min |x|^2 bounds the
   // chunk's y tightly and skips it on raw accumulators
   const int2* cmeta;
+  int nacc;                 // TMEM accumulators (2, or 4 for 64-node tiles)
 };
 
 // One CTA = 128 queries x one node range, 9 warps:
@@ -158,13 +159,15 @@ __global__ void __launch_bounds__(kTcThreads + 32, CTAS) bf_tc_kernel(TcArgs a) 
   uint32_t* li = reinterpret_cast<uint32_t*>(p); p += sizeof(uint32_t) * (size_t)a.kk * kTcThreads;
   volatile float* s_t2 = reinterpret_cast<float*>(p); p += sizeof(float) * kTcThreads;
   p = reinterpret_cast<char*>(((uintptr_t)p + 7) & ~(uintptr_t)7);
-  uint64_t* bars = reinterpret_cast<uint64_t*>(p); p += 8 * 24;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(p); p += 8 * 32;
   uint32_t* tslot = reinterpret_cast<uint32_t*>(p);
   // fullB[4] done[2] empty[2] a fullM[kTcMeta] emptyM[kTcMeta] freeB[4]
+  // fullB[4] done[4] empty[4] a fullM[kTcMeta] emptyM[kTcMeta] freeB[4]
   const uint32_t bar_fullB = smem_u32(bars), bar_done = smem_u32(bars + 4),
-                 bar_empty = smem_u32(bars + 6), bar_a = smem_u32(bars + 8),
-                 bar_fullM = smem_u32(bars + 9), bar_emptyM = smem_u32(bars + 9 + kTcMeta),
-                 bar_freeB = smem_u32(bars + 9 + 2 * kTcMeta);
+                 bar_empty = smem_u32(bars + 8), bar_a = smem_u32(bars + 12),
+                 bar_fullM = smem_u32(bars + 13), bar_emptyM = smem_u32(bars + 13 + kTcMeta),
+                 bar_freeB = smem_u32(bars + 13 + 2 * kTcMeta);
+  const int nacc = a.nacc;  // TMEM accumulators in the MMA -> epilogue ring (2 or 4)
 
   const int64_t q0 = (int64_t)blockIdx.x * kTcM;
   const int64_t tiles = (a.n + N - 1) / N;
@@ -175,11 +178,11 @@ __global__ void __launch_bounds__(kTcThreads + 32, CTAS) bf_tc_kernel(TcArgs a) 
 
   if (warp_id() == 0) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tslot)),
-                 "r"(2 * N));
+                 "r"(nacc * N));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
   if (tid == kTcThreads) {
-    for (int s = 0; s < 2; ++s) {
+    for (int s = 0; s < nacc; ++s) {
       mbar_init(bar_done + 8 * s, 1);
       mbar_init(bar_empty + 8 * s, kTcThreads);
     }
@@ -228,10 +231,10 @@ __global__ void __launch_bounds__(kTcThreads + 32, CTAS) bf_tc_kernel(TcArgs a) 
                              ((uint32_t)(N >> 3) << 17) | ((uint32_t)(kTcM >> 4) << 24);
       const uint32_t sbo = (uint32_t)(rowb / 16) * 128;
       for (int i = 0; i < ntl; ++i) {
-        const int s = i & 1;
-        const uint32_t ph = (uint32_t)((i >> 1) & 1);
-        // accumulator s: free once the epilogue has left tile i - 2
-        if (i >= 2) mbar_wait(bar_empty + 8 * s, ph ^ 1u);
+        const int s = i % nacc;
+        const uint32_t ph = (uint32_t)((i / nacc) & 1);
+        // accumulator s: free once the epilogue has left tile i - nacc
+        if (i >= nacc) mbar_wait(bar_empty + 8 * s, ph ^ 1u);
         const int sb = NBS == 1 ? 0 : i % NBS;
         mbar_wait(bar_fullB + 8 * sb, NBS == 1 ? (uint32_t)(i & 1) : (uint32_t)((i / NBS) & 1));
         tc_fence_after();
@@ -323,8 +326,8 @@ __global__ void __launch_bounds__(kTcThreads + 32, CTAS) bf_tc_kernel(TcArgs a) 
     const uint32_t lane_base = tmem + ((uint32_t)((warp_id() & 3) * 32) << 16) + (uint32_t)(half * cols);
     float gnext = 3.4e38f;
     for (int i = 0; i < ntl; ++i) {
-      const int s = i & 1;
-      const uint32_t ph = (uint32_t)((i >> 1) & 1);
+      const int s = i % nacc;
+      const uint32_t ph = (uint32_t)((i / nacc) & 1);
       const int ms = i % kTcMeta;
       const char* meta = sM + ms * meta_bytes;
       const float* s_nx = reinterpret_cast<const float*>(meta);
@@ -502,7 +505,7 @@ __global__ void __launch_bounds__(kTcThreads + 32, CTAS) bf_tc_kernel(TcArgs a) 
   __syncthreads();
   if (warp_id() == 0) {
     tc_fence_after();
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(2 * N));
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(nacc * N));
   }
 }
 
@@ -510,7 +513,7 @@ __global__ void __launch_bounds__(kTcThreads + 32, CTAS) bf_tc_kernel(TcArgs a) 
 size_t bf_tc_smem_n(int rowb, int l, int kk, int N, int nbs) {
   return (size_t)kTcM * rowb + (size_t)nbs * N * rowb + kTcMeta * ((size_t)N * (3 + l) * 4 + (size_t)(N / 16) * 8) +
          (sizeof(double) + sizeof(uint32_t)) * (size_t)kk * kTcThreads + sizeof(float) * kTcThreads +
-         8 + 8 * 24 + 16;
+         8 + 8 * 32 + 16;
 }
 
 // Tile shapes (N nodes per tile, row stages, CTAs per SM), in order of preference; the first
@@ -518,6 +521,13 @@ size_t bf_tc_smem_n(int rowb, int l, int kk, int N, int nbs) {
 struct TcShape { int N, nbs, ctas; };
 static const TcShape kTcShapes[] = {{128, 3, 2}, {128, 2, 2}, {256, 1, 2}, {128, 1, 2}, {64, 2, 2},
                                     {128, 4, 1}, {256, 2, 1}, {128, 2, 1}};
+// TMEM accumulators of a shape: 2 x N columns, or 4 when 4 N fits the CTA's share of the 512
+// columns (SB_BF_NACC=2 forces two)
+static int tc_nacc(const TcShape& t) {
+  static const int force = [] { const char* e = getenv("SB_BF_NACC"); return e ? atoi(e) : 0; }();
+  if (force == 2 || force == 4) return (force * t.N <= 512 / t.ctas) ? force : 2;
+  return 4 * t.N <= 512 / t.ctas ? 4 : 2;
+}
 
 static bool tc_shape_fits(int rowb, int l, int kk, const TcShape& t) {
   const size_t limit = t.ctas == 2 ? 113 * 1024 : 227 * 1024;
@@ -761,6 +771,7 @@ int launch_bf_tc(const void* Fb, const int32_t* nx, const int32_t* A, const int3
   const TcShape sh = tc_shape(m * (u8 ? 1 : 2), l, kk);
   a.N = sh.N;
   if (a.N == 0) return (int)cudaErrorInvalidValue;
+  a.nacc = tc_nacc(sh);
   size_t smem = bf_tc_smem_n(m * (u8 ? 1 : 2), l, kk, a.N, sh.nbs);
   void (*kern)(TcArgs);
 #define SB_TC_PICK(NB, CT) \
