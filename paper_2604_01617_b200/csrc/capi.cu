@@ -213,7 +213,11 @@ struct sb_index {
   DBuf bf_sort;                      // full-sort top-k scratch (bf_sort.cu: any k)
   DBuf tlists;                       // two-pass TF32 top-k: per-thread lists (q x threads x 32)
   DBuf fb_cmeta, fb_scratch;         // u8 top-k: per-16-node chunk records; sort scratch
+  cudaStream_t st_up = nullptr;      // sb_route_batch: query upload beside the entry-point kernel
+  cudaEvent_t ev_up = nullptr;
   ~sb_index() {
+    if (st_up) cudaStreamDestroy(st_up);
+    if (ev_up) cudaEventDestroy(ev_up);
     bf_sort.release();
     tlists.release();
     fb_cmeta.release();
@@ -1758,6 +1762,24 @@ int sb_route_prepare(sb_index* idx) {
   return SB_OK;
 }
 
+// entry points (router.py:42-45) of queries qi0 .. qi0 + q - 1 into idx->entries, on the
+// device (one thread per query), on the handle's stream
+static int gen_entries(sb_index* idx, int64_t q, int32_t k, uint64_t seed, int64_t qi0) {
+  const int64_t n = idx->n;
+  uint64_t slots = sbrng::choice_scratch_slots(n, k);
+  CK(idx->entries.ensure(sizeof(int64_t) * q * k));
+  // bound the RNG scratch: draw in slices
+  int64_t slice = std::max<int64_t>(1, std::min<int64_t>(q, (int64_t)((1ull << 30) / (slots * 8))));
+  CK(idx->ent_scratch.ensure(sizeof(int64_t) * slots * slice));
+  for (int64_t b = 0; b < q; b += slice) {
+    int64_t c = std::min(slice, q - b);
+    CKL(sb::launch_entry_points(n, k, seed, qi0 + b, c, idx->entries.as<int64_t>() + b * k,
+                                idx->ent_scratch.as<int64_t>(), slots, idx->st));
+    idx->launches += 1;
+  }
+  return SB_OK;
+}
+
 static int route_dev(sb_index* idx, const double* qf, const double* qa, const double* qm, int64_t q,
                      int32_t k, int32_t p, int32_t use_coarse, const int64_t* entries,
                      uint64_t seed, int64_t qi0, double inv_alpha, int64_t* out_ids,
@@ -1768,17 +1790,8 @@ static int route_dev(sb_index* idx, const double* qf, const double* qa, const do
   if (q <= 0) return SB_OK;
   const int64_t n = idx->n;
   if (!entries) {
-    uint64_t slots = sbrng::choice_scratch_slots(n, k);
-    CK(idx->entries.ensure(sizeof(int64_t) * q * k));
-    // bound the RNG scratch: draw in slices
-    int64_t slice = std::max<int64_t>(1, std::min<int64_t>(q, (int64_t)((1ull << 30) / (slots * 8))));
-    CK(idx->ent_scratch.ensure(sizeof(int64_t) * slots * slice));
-    for (int64_t b = 0; b < q; b += slice) {
-      int64_t c = std::min(slice, q - b);
-      CKL(sb::launch_entry_points(n, k, seed, qi0 + b, c, idx->entries.as<int64_t>() + b * k,
-                                  idx->ent_scratch.as<int64_t>(), slots, idx->st));
-      idx->launches += 1;
-    }
+    int r = gen_entries(idx, q, k, seed, qi0);
+    if (r) return r;
     entries = idx->entries.as<int64_t>();
   }
   sb::RouteArgs a;
@@ -1944,16 +1957,34 @@ int sb_route_batch(sb_index* idx, const double* qf, const double* qa, const doub
   size_t total = direct ? o_ids : o_st + sizeof(int64_t) * q * 5;
   CK(idx->qf.ensure(total));
   char* base = idx->qf.as<char>();
-  CK(cudaMemcpyAsync(base + o_qf, qf, sizeof(double) * q * m, cudaMemcpyHostToDevice, idx->st));
-  CK(cudaMemcpyAsync(base + o_qa, qa, sizeof(double) * q * l, cudaMemcpyHostToDevice, idx->st));
-  if (qmask) CK(cudaMemcpyAsync(base + o_qm, qmask, sizeof(double) * q * l, cudaMemcpyHostToDevice, idx->st));
-  if (entries) CK(cudaMemcpyAsync(base + o_en, entries, sizeof(int64_t) * q * k, cudaMemcpyHostToDevice, idx->st));
+  // entry points drawn on the device need no query data: draw them first on the handle's
+  // stream while the queries upload on a side stream (the upload overlaps the RNG kernel)
+  const int64_t* dev_entries = nullptr;
+  cudaStream_t up = idx->st;
+  if (!entries && k >= 1 && k <= idx->n && k <= (1 << 18) && pioneer >= 1 && pioneer <= k) {
+    int r = gen_entries(idx, q, k, seed, qi0);
+    if (r) return r;
+    dev_entries = idx->entries.as<int64_t>();
+    if (!idx->st_up) {
+      CK(cudaStreamCreateWithFlags(&idx->st_up, cudaStreamNonBlocking));
+      CK(cudaEventCreateWithFlags(&idx->ev_up, cudaEventDisableTiming));
+    }
+    up = idx->st_up;
+  }
+  CK(cudaMemcpyAsync(base + o_qf, qf, sizeof(double) * q * m, cudaMemcpyHostToDevice, up));
+  CK(cudaMemcpyAsync(base + o_qa, qa, sizeof(double) * q * l, cudaMemcpyHostToDevice, up));
+  if (qmask) CK(cudaMemcpyAsync(base + o_qm, qmask, sizeof(double) * q * l, cudaMemcpyHostToDevice, up));
+  if (entries) CK(cudaMemcpyAsync(base + o_en, entries, sizeof(int64_t) * q * k, cudaMemcpyHostToDevice, up));
+  if (up != idx->st) {
+    CK(cudaEventRecord(idx->ev_up, up));
+    CK(cudaStreamWaitEvent(idx->st, idx->ev_up, 0));
+  }
   int64_t* r_ids = direct ? d_ids_h : reinterpret_cast<int64_t*>(base + o_ids);
   double* r_d = direct ? d_dists_h : reinterpret_cast<double*>(base + o_d);
   int64_t* r_st = direct ? d_st_h : (out_stats ? reinterpret_cast<int64_t*>(base + o_st) : nullptr);
   int r = route_dev(idx, reinterpret_cast<double*>(base + o_qf), reinterpret_cast<double*>(base + o_qa),
                     qmask ? reinterpret_cast<double*>(base + o_qm) : nullptr, q, k, pioneer,
-                    use_coarse, entries ? reinterpret_cast<int64_t*>(base + o_en) : nullptr, seed,
+                    use_coarse, entries ? reinterpret_cast<int64_t*>(base + o_en) : dev_entries, seed,
                     qi0, inv_alpha, r_ids, r_d, r_st);
   if (r) return r;
   if (!direct) {
