@@ -143,6 +143,10 @@ int sb_hybrid_groundtruth(sb_index* idx, const double* qf, const int64_t* qa, co
  * default_rng(SeedSequence((seed, qi))).choice(n, k, replace=False). out i64[q*k]. */
 int sb_entry_points(int64_t n, int32_t k, uint64_t seed, int64_t qi0, int64_t q, int64_t* out);
 
+/* the same on the device (the kernels sb_route_batch uses when entries is NULL), copied back to
+ * out i64[q*k]; for tests and comparisons */
+int sb_entry_points_device(int64_t n, int32_t k, uint64_t seed, int64_t qi0, int64_t q, int64_t* out);
+
 /* search_batch (router.py:98-124) as one device call: route (_kernels.py:504-610) for q
  * queries with query_index = qi0 + row.  qf f64[q*m], qa f64[q*l], qmask f64[q*l] or NULL
  * (router.py:62-73 widens to f64); entries i64[q*k] or NULL (drawn on the device with the

@@ -51,6 +51,7 @@ _SIGS = {
     "sb_bf_topk_queries": [_vp, _vp, _vp, _vp, _i64, _i32, _f64, _vp, _vp, _vp],
     "sb_hybrid_groundtruth": [_vp, _vp, _vp, _vp, _i64, _i32, _vp, _vp, _vp],
     "sb_entry_points": [_i64, _i32, _u64, _i64, _i64, _vp],
+    "sb_entry_points_device": [_i64, _i32, _u64, _i64, _i64, _vp],
     "sb_route_batch": [_vp, _vp, _vp, _vp, _i64, _i32, _i32, _i32, _vp, _u64, _i64, _f64,
                        _vp, _vp, _vp],
     "sb_route_batch_dev": [_vp, _vp, _vp, _vp, _i64, _i32, _i32, _i32, _vp, _u64, _i64, _f64,

@@ -1689,6 +1689,24 @@ int sb_entry_points(int64_t n, int32_t k, uint64_t seed, int64_t qi0, int64_t q,
   return SB_OK;
 }
 
+int sb_entry_points_device(int64_t n, int32_t k, uint64_t seed, int64_t qi0, int64_t q, int64_t* out) {
+  if (!out) return fail(SB_EARG, "out is NULL");
+  if (k < 1 || k > n) return fail(SB_EARG, "k must be in [1, n]");
+  if (q <= 0) return SB_OK;
+  const uint64_t slots = sbrng::choice_scratch_slots(n, k);
+  int64_t* d_out = nullptr;
+  int64_t* d_scr = nullptr;
+  CK(cudaMalloc(&d_out, sizeof(int64_t) * (size_t)q * k));
+  cudaError_t e = cudaMalloc(&d_scr, sizeof(int64_t) * slots * (size_t)q);
+  if (e != cudaSuccess) { cudaFree(d_out); return cuda_fail(e, "cudaMalloc(scratch)"); }
+  int r = sb::launch_entry_points(n, k, seed, qi0, q, d_out, d_scr, slots, 0);
+  if (r == 0) r = (int)cudaMemcpy(out, d_out, sizeof(int64_t) * (size_t)q * k, cudaMemcpyDeviceToHost);
+  cudaFree(d_out);
+  cudaFree(d_scr);
+  if (r) return cuda_fail((cudaError_t)r, "entry points on the device");
+  return SB_OK;
+}
+
 // The routing layout (route.cu "routing layout"): a locality order of the nodes and the
 // features, attributes and adjacency renumbered into it.  Rebuilt when the adjacency changed.
 static bool relabel_enabled() {

@@ -130,6 +130,31 @@ RNG_HD void pcg_from_entropy2(Pcg64* g, uint64_t a, uint64_t b) {
   pcg_seed_words(g, w);
 }
 
+// jump parameters of `delta` PCG64 steps: s' = mult * s + plus (squaring, O(log delta))
+RNG_HD void pcg_jump_params(U128 inc, uint64_t delta, U128* mult_out, U128* plus_out) {
+  U128 cur_mult = {0x2360ED051FC65DA4ull, 0x4385DF649FCCF645ull};
+  U128 cur_plus = inc;
+  U128 acc_mult = {0, 1}, acc_plus = {0, 0};
+  while (delta > 0) {
+    if (delta & 1) {
+      acc_mult = mul128(acc_mult, cur_mult);
+      acc_plus = add128(mul128(acc_plus, cur_mult), cur_plus);
+    }
+    cur_plus = mul128(add128(cur_mult, {0, 1}), cur_plus);
+    cur_mult = mul128(cur_mult, cur_mult);
+    delta >>= 1;
+  }
+  *mult_out = acc_mult;
+  *plus_out = acc_plus;
+}
+
+// 64-bit output of a PCG64 state (XSL-RR)
+RNG_HD uint64_t pcg_output(U128 s) {
+  uint64_t x = s.hi ^ s.lo;
+  unsigned rot = (unsigned)(s.hi >> 58);
+  return (x >> rot) | (x << ((64u - rot) & 63u));
+}
+
 RNG_HD uint64_t pcg_next64(Pcg64* g) {
   pcg_step(g);
   uint64_t x = g->s.hi ^ g->s.lo;

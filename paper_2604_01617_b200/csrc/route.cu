@@ -913,8 +913,96 @@ __global__ void entry_points_smem_kernel(int64_t n, int K, uint64_t seed, int64_
   for (int t = 0; t < K; ++t) dst[t] = o[t];
 }
 
+// Warp per query (Floyd regime, n < 2^31, n != K): every 32-bit draw of the query's choice()
+// comes from a PCG64 output reachable by jump-ahead — draw d is half d % 2 of output d / 2,
+// and with no Lemire rejection draw d serves bounded(n - K + d) (Floyd, d < K) or
+// bounded(2K - 1 - d) (the shuffle's i = 2K - 1 - d) — so the lanes compute all 2K - 1 bounded values in
+// parallel; lane 0 then resolves Floyd's collisions and applies the swaps in shared memory.
+// A rejection (probability ~ range / 2^32 per draw) shifts the stream: the warp then redoes
+// the query sequentially.  Same ids as NumPy (tests/test_gpu_kernels.py).
+__global__ void entry_points_warp_kernel(int64_t n, int K, uint64_t seed, int64_t qi0, int64_t q,
+                                         int64_t* out, int tslots) {
+  extern __shared__ int32_t ew_smem[];
+  const int lane = lane_id();
+  const int wpb = blockDim.x >> 5;
+  const int64_t i = (int64_t)blockIdx.x * wpb + warp_id();
+  if (i >= q) return;
+  int32_t* table = ew_smem + (size_t)warp_id() * (tslots + 2 * K);
+  int32_t* vals = table + tslots;  // [0, K): Floyd values, then the ids; [K, 2K - 1): swap partners
+  sbrng::Pcg64 g;
+  sbrng::pcg_from_entropy2(&g, seed, (uint64_t)(qi0 + i));
+  for (int t = lane; t < tslots; t += 32) table[t] = -1;
+  const int D = 2 * K - 1;
+  sbrng::U128 m1, p1, m16, p16;
+  sbrng::pcg_jump_params(g.inc, (uint64_t)(lane >> 1) + 1, &m1, &p1);
+  sbrng::pcg_jump_params(g.inc, 16, &m16, &p16);
+  sbrng::U128 stt = sbrng::add128(sbrng::mul128(m1, g.s), p1);
+  bool reject = false;
+  for (int d = lane; d < D; d += 32) {
+    const uint64_t o = sbrng::pcg_output(stt);
+    const uint32_t u = (lane & 1) ? (uint32_t)(o >> 32) : (uint32_t)o;
+    const uint32_t range = d < K ? (uint32_t)(n - K + d) : (uint32_t)(2 * K - 1 - d);
+    const uint32_t excl = range + 1u;
+    const uint64_t mm = (uint64_t)u * excl;
+    const uint32_t left = (uint32_t)mm;
+    if (left < excl && left < (0xFFFFFFFFu - range) % excl) reject = true;
+    vals[d] = (int32_t)(mm >> 32);
+    stt = sbrng::add128(sbrng::mul128(m16, stt), p16);
+  }
+  reject = __any_sync(0xffffffffu, reject);
+  __syncwarp();
+  if (lane == 0) {
+    if (reject) {
+      sbrng::choice_floyd<int32_t>(&g, n, K, vals, table, (uint64_t)tslots - 1);
+    } else {
+      const uint64_t tmask = (uint64_t)tslots - 1;
+      for (int t = 0; t < K; ++t) {  // Floyd: value v_j, or j itself when v_j was taken
+        const int32_t v = vals[t], j = (int32_t)(n - K + t);
+        uint64_t loc = (uint64_t)v & tmask;
+        while (table[loc] != -1 && table[loc] != v) loc = (loc + 1) & tmask;
+        if (table[loc] == -1) {
+          table[loc] = v;
+        } else {
+          loc = (uint64_t)j & tmask;
+          while (table[loc] != -1) loc = (loc + 1) & tmask;
+          table[loc] = j;
+          vals[t] = j;
+        }
+      }
+      for (int t = K - 1; t > 0; --t) {  // the shuffle
+        const int32_t jj = vals[K + (K - 1 - t)];
+        const int32_t x = vals[t];
+        vals[t] = vals[jj];
+        vals[jj] = x;
+      }
+    }
+  }
+  __syncwarp();
+  int64_t* dst = out + i * K;
+  for (int t = lane; t < K; t += 32) dst[t] = vals[t];
+}
+
 int launch_entry_points(int64_t n, int K, uint64_t seed, int64_t qi0, int64_t q, int64_t* out,
                         int64_t* scratch, uint64_t scratch_slots, cudaStream_t st) {
+  {
+    const uint64_t ts = sbrng::choice_table_size(n, K);
+    const size_t per = sizeof(int32_t) * (size_t)(ts + 2 * K);
+    int wpb = 8;
+    while (wpb > 1 && per * wpb > (size_t)100 * 1024) wpb >>= 1;
+    static const bool warp_on = [] { const char* e = getenv("SB_EP_WARP"); return !(e && e[0] == '0'); }();
+    if (warp_on && !sbrng::choice_uses_tail_shuffle(n, K) && n < (int64_t)0x7FFFFFFF && n != K && K >= 1 &&
+        per * wpb <= (size_t)100 * 1024) {
+      static bool attr = false;
+      if (!attr) {
+        cudaFuncSetAttribute(entry_points_warp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024);
+        attr = true;
+      }
+      const int64_t gb = (q + wpb - 1) / wpb;
+      if (gb > 0)
+        entry_points_warp_kernel<<<(unsigned)gb, 32 * wpb, per * wpb, st>>>(n, K, seed, qi0, q, out, (int)ts);
+      return (int)cudaGetLastError();
+    }
+  }
   const uint64_t ts = sbrng::choice_table_size(n, K);
   const size_t per = sizeof(int32_t) * (size_t)(ts + K);
   int tpb = kEpThreads;

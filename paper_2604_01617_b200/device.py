@@ -256,3 +256,11 @@ def entry_points_host(n: int, k: int, seed: int, qi0: int, q: int) -> np.ndarray
     out = np.empty((q, k), np.int64)
     _lib.call("sb_entry_points", int(n), int(k), int(seed), int(qi0), int(q), ptr(out))
     return out
+
+
+def entry_points_device(n: int, k: int, seed: int, qi0: int, q: int) -> np.ndarray:
+    """entry_points (router.py:42-45) for queries qi0 .. qi0 + q - 1 drawn by the device kernels
+    that routing uses (warp-parallel Floyd draws, shared-memory tables), copied back."""
+    out = np.empty((q, k), np.int64)
+    _lib.call("sb_entry_points_device", int(n), int(k), int(seed), int(qi0), int(q), ptr(out))
+    return out

@@ -196,3 +196,28 @@ def test_prune_integer_rows_u8_path(u8, n, d, card, gamma, sigma, seed, monkeypa
     np.testing.assert_array_equal(counts, g.nbr_counts)
     np.testing.assert_array_equal(ids, g.nbr_ids)
     np.testing.assert_array_equal(dists, g.nbr_dists)
+
+
+@pytest.mark.parametrize("warp", ["1", "0"])
+def test_device_entry_points_equal_reference(rng_golden, warp, monkeypatch):
+    """The device entry-point kernels (warp-parallel Floyd draws with jump-ahead, the
+    shared-memory and global-scratch per-thread kernels) reproduce the reference's
+    entry_points (router.py:42-45) on the golden (n, k, seed, qi) grid (NumPy's Floyd and
+    tail-shuffle regimes), and NumPy itself on query batches, including k = n and k = 1."""
+    from paper_2604_01617_b200.device import entry_points_device
+    monkeypatch.setenv("SB_EP_WARP", warp)
+    gd = rng_golden
+    for key in gd.files:
+        if key.startswith("ep_"):
+            _, n, k, seed, qi = key.split("_")
+            got = entry_points_device(int(n), int(k), int(seed), int(qi), 1)[0]
+            np.testing.assert_array_equal(got, gd[key], err_msg=key)
+        elif key.startswith("ephead_"):
+            _, n, k, seed, qi = key.split("_")
+            got = entry_points_device(int(n), int(k), int(seed), int(qi), 1)[0]
+            np.testing.assert_array_equal(got[:256], gd[key], err_msg=key)
+    for n, k in ((1000, 1000), (5000, 1), (1_000_000, 200), (9999, 4000), (2_000_000, 3000)):
+        got = entry_points_device(n, k, 7, 123, 300)
+        want = np.stack([np.random.default_rng(np.random.SeedSequence(entropy=(7, 123 + i))).choice(n, k, replace=False)
+                         for i in range(300)])
+        np.testing.assert_array_equal(got, want, err_msg=f"n={n} k={k}")
