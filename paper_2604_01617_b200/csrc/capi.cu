@@ -1858,6 +1858,14 @@ static int route_dev(sb_index* idx, const double* qf, const double* qa, const do
     if (const char* e = getenv("SB_ROUTE_FILT"))
       a.flt_lpr = (atoi(e) != 0 && idx->m % 4 == 0 && !idx->force_sequential) ? lpr : 0;
   }
+  // real-valued rows, register-pipelined instance (one 8-warp CTA per SM): when rows are longer
+  // than 1 KB (a lane walks its row in many dependent chunks) or the batch cannot fill more than
+  // one such CTA per SM anyway.  SB_ROUTE_DEEP=0/1 forces it off/on.
+  a.deep = (idx->m * 4 > 1024 || q <= (int64_t)idx->sms * 8) ? 1 : 0;
+  if (const char* e = getenv("SB_ROUTE_DEEP")) a.deep = atoi(e) != 0;
+  // its conversion-free fp32 -> fp64 step needs finite features (min/max of the upload scan)
+  if (!(idx->flo >= -3.4028234e38f && idx->fhi <= 3.4028234e38f)) a.deep = 0;
+  a.ring_slots = 0;
   // integer features in [0, 255]: route over a u8 copy with dp4a dot products (exact), unless
   // SB_ROUTE_U8=0; built once per layout
   a.F8 = nullptr;
@@ -1902,6 +1910,23 @@ static int route_dev(sb_index* idx, const double* qf, const double* qa, const do
   int wpc_max = 8;
   if (const char* e = getenv("SB_ROUTE_WPC")) wpc_max = std::max(1, std::min(8, atoi(e)));
   int wpc = (int)std::max<size_t>(1, std::min<size_t>(wpc_max, (size_t)(110 * 1024) / per_warp));
+  if (sb::route_path(a) == 6) {
+    // the staged instance runs one CTA per SM: just enough warps for the batch (at most 8), and
+    // what is left of the SM's shared memory becomes the warps' row-line rings
+    const size_t budget = (size_t)220 * 1024;
+    wpc = (int)std::max<int64_t>(1, std::min<int64_t>(wpc_max, (q + idx->sms - 1) / idx->sms));
+    while (wpc > 1 && budget / wpc < per_warp + 64 * 144 + 256) --wpc;
+    const size_t spare = budget / wpc > per_warp + 256 ? budget / wpc - per_warp - 256 : 0;
+    a.ring_slots = (int)std::min<size_t>(512, spare / 144);
+    if (a.ring_slots < 64) {  // no room for a useful ring: the three-CTA instance
+      a.deep = 0;
+      a.ring_slots = 0;
+      idx->last_route_path = sb::route_path(a);
+      wpc = (int)std::max<size_t>(1, std::min<size_t>(wpc_max, (size_t)(110 * 1024) / per_warp));
+    } else {
+      per_warp = sb::route_smem_per_warp(a);
+    }
+  }
   if (per_warp * wpc > 227 * 1024) return fail(SB_EARG, "k too large for the routing kernel");
   int per_sm = 0;
   CKL(sb::route_occupancy(a, wpc, per_warp * wpc, &per_sm));

@@ -33,6 +33,7 @@
 #include "common.cuh"
 #include "rng.cuh"
 #include "sb_internal.h"
+#include "tc_ptx.cuh"
 
 #include <cub/device/device_radix_sort.cuh>
 
@@ -46,6 +47,9 @@ constexpr int kRows = 8;                   // rows per lane group in flight (fp3
 #define ROUTE_F32_CHUNK 8                  // float4 loads in flight per lane (fp32 lane path)
 #endif
 
+#ifndef ROUTE_DEEP_SLOTS
+#define ROUTE_DEEP_SLOTS 8  // 4-float4 slots in flight per lane in the kModeF64Deep instance
+#endif
 constexpr int kLazyB = 64;  // insertion buffer of the large-K kernel instances
 constexpr int kLazyK = 1024; // K from which routing uses the insertion buffer
 #ifndef ROUTE_FAST_MERGE
@@ -65,16 +69,21 @@ struct WarpSmem {
   uint32_t* rid;  // Kpad
   uint32_t* cid;  // Cpad
   int* cpos;      // Cpad
+  char* ring;     // kModeF64Deep: ring_slots x kRingSlotB row-line staging
 };
 
+constexpr int kRingSlotB = 144;  // one 128-byte row line + 16 bytes: conflict-free lane-per-row reads
+constexpr int kRingStages = 4;   // cp.async groups in flight per round (kModeF64Deep)
 SB_HD size_t route_warp_smem_bytes_full(int Kpad, int Cpad, int m, int l, bool lazy,
-                                         bool rglobal = false) {
+                                         bool rglobal = false, int ring_slots = 0) {
   if (rglobal) Kpad = 0;  // R lives in global memory
   size_t b = (size_t)((m + 3) & ~3) * 4;  // fp32 query first: 16-byte aligned float4 reads
   if (lazy) b += (size_t)kLazyB * 12;
-  b += (size_t)Kpad * 8 + (size_t)Cpad * 8 + (size_t)m * 8 + (size_t)l * 16;
+  // the fp64 query is padded with zeros to whole 32-dimension lines (staged evaluation)
+  b += (size_t)Kpad * 8 + (size_t)Cpad * 8 + (size_t)((m + 31) & ~31) * 8 + (size_t)l * 16;
   b += (size_t)Kpad * 4 + (size_t)Cpad * 8;
-  return (b + 15) & ~(size_t)15;
+  b = (b + 15) & ~(size_t)15;
+  return b + (ring_slots ? (size_t)ring_slots * kRingSlotB + 256 : 0);  // + 32 row pointers
 }
 
 template <bool LAZY>
@@ -83,6 +92,7 @@ SB_DEV WarpSmem carve(char* base, const RouteArgs& a, int64_t slot) {
   WarpSmem w;
   w.qs32 = reinterpret_cast<float*>(base);
   double* dp = reinterpret_cast<double*>(base + (size_t)((a.m + 3) & ~3) * 4);
+  w.qs = dp; dp += (a.m + 31) & ~31;  // 16-byte aligned (double2 reads), zero-padded to lines
   w.bd = nullptr;
   w.bid = nullptr;
   if (LAZY) {
@@ -98,7 +108,6 @@ SB_DEV WarpSmem carve(char* base, const RouteArgs& a, int64_t slot) {
     dp += a.Kpad;
   }
   w.cd = dp; dp += a.Cpad;
-  w.qs = dp; dp += a.m;
   w.qas = dp; dp += a.l;
   w.qms = dp; dp += a.l;
   uint32_t* up = reinterpret_cast<uint32_t*>(dp);
@@ -110,6 +119,7 @@ SB_DEV WarpSmem carve(char* base, const RouteArgs& a, int64_t slot) {
   }
   w.cid = up; up += a.Cpad;
   w.cpos = reinterpret_cast<int*>(up);
+  w.ring = base + route_warp_smem_bytes_full(a.Kpad, a.Cpad, a.m, a.l, LAZY, rg, 0);
   return w;
 }
 
@@ -147,7 +157,191 @@ SB_DEV double finish_pre(const RouteArgs& a, const WarpSmem& w, uint32_t node, c
 // distance path of a route_kernel instance (each instance carries only its own path, plus the
 // generic fp64 path as the per-query fallback of the integer paths)
 enum RouteMode { kModeF64x4 = 0, kModeF32Lane = 1, kModeF32Split = 2, kModeGeneric = 3, kModeU8 = 4,
-                 kModeF64Filt = 5 };
+                 kModeF64Filt = 5, kModeF64Deep = 6 };
+
+// 16-byte read-only loads of a row with an L2 prefetch-size hint: a miss brings the whole
+// 128-byte line in one DRAM access instead of one access per 32-byte sector (ROUTE_L2PF: 0 = plain
+// __ldg, 128 / 256 = hint size)
+#ifndef ROUTE_L2PF
+#define ROUTE_L2PF 128
+#endif
+SB_DEV uint4 ldg_row(const uint4* p) {
+#if ROUTE_L2PF == 128
+  uint4 v;
+  asm("ld.global.nc.L2::128B.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(p));
+  return v;
+#elif ROUTE_L2PF == 256
+  uint4 v;
+  asm("ld.global.nc.L2::256B.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(p));
+  return v;
+#else
+  return __ldg(p);
+#endif
+}
+SB_DEV float4 ldg_row(const float4* p) {
+  const uint4 v = ldg_row(reinterpret_cast<const uint4*>(p));
+  return make_float4(__uint_as_float(v.x), __uint_as_float(v.y), __uint_as_float(v.z), __uint_as_float(v.w));
+}
+
+// fp32 -> fp64 without the conversion unit (F2F runs at a quarter of the fp64 rate and was the
+// busiest pipe of the real-valued walk): the float's fields dropped into a double's give
+// X = x * 2^-896 exactly (zero and subnormal floats land on subnormal doubles, which fp64
+// handles at full speed), so fma(X, 2^896, -q) is the correctly rounded x - q: the same value
+// as __dsub_rn((double)x, q) for every finite x.
+SB_DEV double f2d_scaled(float x) {
+  const int xi = __float_as_int(x);
+  return __hiloint2double((xi >> 3) & (int)0x8FFFFFFF, xi << 29);
+}
+SB_DEV double sq_diff(float x, double q) {
+  const double d = __fma_rn(f2d_scaled(x), 0x1p896, -q);
+  return dmul(d, d);
+}
+
+SB_DEV void cp_async16(uint32_t dst, const void* src, int src_bytes) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src), "r"(src_bytes) : "memory");
+}
+SB_DEV void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+SB_DEV void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
+// kModeF64Deep: exact distances of rows cid[0..c) -> cd[0..c), _query_dist's sequential fp64 sum
+// (bit-identical: the order of the additions is the reference's; padded dimensions add +0.0).
+//  * Loads: the warp copies the rows into a shared-memory ring one 128-byte line per row at a
+//    time with cp.async, 8 lanes per line (whole-line requests: one row per lane with 16-byte
+//    loads is bounded by the single-sector request rate, tools/probes/rowwalk_bw.cu), four
+//    groups of lines in flight, the ring as deep as its slots allow for the round's rows.
+//  * Chain: lane r walks row r out of the ring; the squares (x - q)^2 of the next 16
+//    dimensions are computed between the dependent adds of the current 16, so the chain
+//    advances at the latency of one fp64 add, and the loop body is small (no unrolled row).
+SB_DEV void eval_rows_staged(const RouteArgs& a, WarpSmem& w, int c) {
+  const int lane = lane_id();
+  const int rowb = a.m * 4;
+  const int nln = (rowb + 127) >> 7;  // 128-byte lines per row
+  const uint32_t ring = smem_u32(w.ring);
+  const int sub = lane & 7, grp = lane >> 3;
+  const double2* q2 = reinterpret_cast<const double2*>(w.qs);
+  // row pointers of the round, behind the ring (one per row: the copies read them back)
+  const char** rowptr = reinterpret_cast<const char**>(w.ring + (size_t)a.ring_slots * kRingSlotB);
+  const int cr_max = a.ring_slots / kRingStages < 32 ? a.ring_slots / kRingStages : 32;
+  for (int base = 0; base < c; base += cr_max) {
+    const int cr = c - base < cr_max ? c - base : cr_max;
+    int lps = a.ring_slots / (cr * kRingStages);  // lines per row per group
+    if (lps > 8) lps = 8;
+    const int nlr = lps * kRingStages;             // lines per row the ring holds
+    const int ngr = (cr + 3) >> 2;
+    const int my = lane < cr ? lane : cr - 1;      // idle lanes shadow the last row (no divergence)
+    const uint32_t v = w.cid[base + my];
+    if (lane < cr) rowptr[lane] = reinterpret_cast<const char*>(a.F) + (int64_t)v * rowb;
+    AttrPre pre;
+    attr_preload(a, v, pre);
+    __syncwarp();
+    int issue_ln = 0, issue_pos = 0;
+    // one group: the next `lps` lines of every row of the round; 8 lanes copy one line, so a
+    // warp instruction moves four rows' lines: rows grp, grp + 4, ... of this lane's group (the
+    // first four pointers in registers, any further row through the shared-memory table)
+    const char* rp[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) rp[i] = rowptr[grp + 4 * i < cr ? grp + 4 * i : my] + sub * 16;
+    const uint32_t dst0 = ring + (uint32_t)(grp * kRingSlotB + sub * 16);
+    const uint32_t line_b = (uint32_t)(cr * kRingSlotB);
+    auto issue_group = [&]() {
+      for (int k = 0; k < lps; ++k) {
+        if (issue_ln < nln) {
+          const int off = issue_ln * 128;
+          const int sz = off + sub * 16 < rowb ? 16 : 0;  // past the row's end: zero fill
+          const int so = sz ? off : 0;
+          const uint32_t dst = dst0 + (uint32_t)issue_pos * line_b;
+#pragma unroll
+          for (int i = 0; i < 4; ++i)
+            if (grp + 4 * i < cr) cp_async16(dst + (uint32_t)(4 * i * kRingSlotB), rp[i] + so, sz);
+          for (int r = grp + 16; r < cr; r += 4)
+            cp_async16(dst + (uint32_t)((r - grp) * kRingSlotB), rowptr[r] + sub * 16 + so, sz);
+        }
+        ++issue_ln;
+        issue_pos = issue_pos + 1 == nlr ? 0 : issue_pos + 1;
+      }
+      cp_async_commit();
+    };
+#pragma unroll
+    for (int g = 0; g < kRingStages; ++g) issue_group();
+    cp_async_wait<kRingStages - 1>();
+    __syncwarp();
+    // Software pipeline over half lines (16 dimensions): at the top of a step, t holds the
+    // squares of the current half line and (x, q) the raw inputs of the next one, read from
+    // shared memory a step ahead, so the squares never wait for their loads and can sit between
+    // the dependent adds.
+    double s = 0.0;
+    double t[16];
+    float4 x[4];
+    double2 q[8];
+    auto fetch = [&](int pos, int h, int e) {
+      const float4* x4 = reinterpret_cast<const float4*>(w.ring + (size_t)(pos * cr + my) * kRingSlotB + h * 64);
+#pragma unroll
+      for (int u = 0; u < 4; ++u) x[u] = x4[u];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) q[u] = q2[(e >> 1) + u];
+    };
+    auto square = [&](int u4, bool accumulate) {  // dimensions 4 u4 .. 4 u4 + 3 of the half line
+      if (accumulate) s = dadd(s, t[4 * u4 + 0]);
+      t[4 * u4 + 0] = sq_diff(x[u4].x, q[2 * u4].x);
+      if (accumulate) s = dadd(s, t[4 * u4 + 1]);
+      t[4 * u4 + 1] = sq_diff(x[u4].y, q[2 * u4].y);
+      if (accumulate) s = dadd(s, t[4 * u4 + 2]);
+      t[4 * u4 + 2] = sq_diff(x[u4].z, q[2 * u4 + 1].x);
+      if (accumulate) s = dadd(s, t[4 * u4 + 3]);
+      t[4 * u4 + 3] = sq_diff(x[u4].w, q[2 * u4 + 1].y);
+    };
+    // step: s += t; t <- squares of (x, q); (x, q) <- the half line at (pos, h) when `more`
+    auto step = [&](bool more, int pos, int h, int e) {
+      float4 xn[4];
+      double2 qn[8];
+      if (more) {
+        const float4* x4 = reinterpret_cast<const float4*>(w.ring + (size_t)(pos * cr + my) * kRingSlotB + h * 64);
+#pragma unroll
+        for (int u = 0; u < 4; ++u) xn[u] = x4[u];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) qn[u] = q2[(e >> 1) + u];
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) square(u, true);
+      if (more) {
+#pragma unroll
+        for (int u = 0; u < 4; ++u) x[u] = xn[u];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) q[u] = qn[u];
+      }
+    };
+    fetch(0, 0, 0);
+#pragma unroll
+    for (int u = 0; u < 4; ++u) square(u, false);
+    fetch(0, 1, 16);
+    int pos = 0, in_group = 0;
+    for (int ln = 0; ln < nln; ++ln) {
+      // t: squares of (ln, 0); (x, q): inputs of (ln, 1).  Line ln + 1 is read during this
+      // iteration: when it opens a new group that group must have landed, and the group before
+      // the current one (every lane has it in registers: the __syncwarp) is refilled.
+      if (++in_group == lps) {
+        in_group = 0;
+        cp_async_wait<kRingStages - 2>();
+        __syncwarp();
+        issue_group();
+      }
+      const int npos = pos + 1 == nlr ? 0 : pos + 1;
+      const bool more = ln + 1 < nln;
+      step(more, npos, 0, ln * 32 + 32);  // adds (ln, 0), squares (ln, 1), reads (ln + 1, 0)
+      if (more) {
+        step(true, npos, 1, ln * 32 + 48);  // adds (ln, 1), squares (ln + 1, 0), reads (ln + 1, 1)
+      } else {
+#pragma unroll
+        for (int u = 0; u < 16; ++u) s = dadd(s, t[u]);
+      }
+      pos = npos;
+    }
+    cp_async_wait<0>();
+    if (lane < cr) w.cd[base + lane] = finish_pre(a, w, v, pre, s);
+    __syncwarp();  // the ring and the row pointers are free for the next round
+  }
+}
 
 // attribute factor of _query_dist's finish: 1 + s_a * inv_alpha, computed exactly as
 // finish_row does (_kernels.py:32-35)
@@ -188,7 +382,7 @@ SB_DEV void eval_rows(const RouteArgs& a, WarpSmem& w, int c, bool f32, int nq8,
       for (; k + 8 <= n16; k += 8) {
         uint4 r[8];
 #pragma unroll
-        for (int u = 0; u < 8; ++u) r[u] = __ldg(xr + k + u);
+        for (int u = 0; u < 8; ++u) r[u] = ldg_row(xr + k + u);
 #pragma unroll
         for (int u = 0; u < 8; ++u) {
           const uint4 q = Q[k + u];
@@ -199,7 +393,7 @@ SB_DEV void eval_rows(const RouteArgs& a, WarpSmem& w, int c, bool f32, int nq8,
         }
       }
       for (; k < n16; ++k) {
-        const uint4 r = __ldg(xr + k);
+        const uint4 r = ldg_row(xr + k);
         const uint4 q = Q[k];
         acc0 = __dp4a(r.x, q.x, acc0);
         acc1 = __dp4a(r.y, q.y, acc1);
@@ -294,6 +488,8 @@ SB_DEV void eval_rows(const RouteArgs& a, WarpSmem& w, int c, bool f32, int nq8,
           if (id[g] != 0xFFFFFFFFu) w.cd[base + grp + rpp * g] = finish_row(a, w, id[g], (double)acc[g]);
       }
     }
+  } else if (MODE == kModeF64Deep) {
+    eval_rows_staged(a, w, c);
   } else if (MODE == kModeF64x4 || MODE == kModeF64Filt) {
     const int nq = a.m >> 2;
     int ns = c;  // rows that need the exact value: all, or the filter's survivors (w.cpos)
@@ -504,12 +700,14 @@ SB_DEV int merge_into_r(const RouteArgs& a, double* rd, uint32_t* rid, int K, do
 }
 
 template <int MODE, bool LAZY>
-__global__ void __launch_bounds__(256, LAZY ? 2 : ROUTE_MIN_CTAS) route_kernel(RouteArgs a) {
+__global__ void __launch_bounds__(256, MODE == kModeF64Deep ? 1 : LAZY ? 2 : ROUTE_MIN_CTAS)
+route_kernel(RouteArgs a) {
   extern __shared__ __align__(16) char smem_raw[];
   const int lane = lane_id();
   const int wid = warp_id();
   const int nw = blockDim.x >> 5;
-  const size_t wbytes = route_warp_smem_bytes_full(a.Kpad, a.Cpad, a.m, a.l, LAZY, LAZY && a.gr_d != nullptr);
+  const size_t wbytes = route_warp_smem_bytes_full(a.Kpad, a.Cpad, a.m, a.l, LAZY, LAZY && a.gr_d != nullptr,
+                                                   MODE == kModeF64Deep ? a.ring_slots : 0);
   const int64_t slot = (int64_t)blockIdx.x * nw + wid;
   WarpSmem w = carve<LAZY>(smem_raw + wbytes * wid, a, slot);
   uint32_t* vis = a.visited + slot * a.vwords;
@@ -535,6 +733,7 @@ __global__ void __launch_bounds__(256, LAZY ? 2 : ROUTE_MIN_CTAS) route_kernel(R
       qlo = fminf(qlo, (float)v);
       qhi = fmaxf(qhi, (float)v);
     }
+    for (int t = a.m + lane; t < ((a.m + 31) & ~31); t += 32) w.qs[t] = 0.0;
     for (int t = lane; t < a.l; t += 32) {
       w.qas[t] = a.qa[(int64_t)qi * a.l + t];
       w.qms[t] = a.qm ? a.qm[(int64_t)qi * a.l + t] : 1.0;
@@ -799,7 +998,7 @@ __global__ void __launch_bounds__(256, LAZY ? 2 : ROUTE_MIN_CTAS) route_kernel(R
       // many dependent chunks: cfg 4, d = 960: 28.9 -> 24.0 ms per 1k queries) whatever the batch
       // size, else when the batch exceeds one row per lane (cfg 5, d = 100: prefetching every
       // batch was 4% slower)
-      if ((c > 32 || (a.m * 4 > 1024 && !(MODE == kModeU8 && f32))) && a.pf_rows) {
+      if (MODE != kModeF64Deep && (c > 32 || (a.m * 4 > 1024 && !(MODE == kModeU8 && f32))) && a.pf_rows) {
         // request every line of the batch's rows at once (L2), so the per-lane row loads
         // below wait for one memory latency instead of one per 128-byte chunk
         const int lines = MODE == kModeU8 && f32 ? (a.m + 127) >> 7 : (a.m * 4 + 127) >> 7;
@@ -809,6 +1008,12 @@ __global__ void __launch_bounds__(256, LAZY ? 2 : ROUTE_MIN_CTAS) route_kernel(R
         if (lines == 1) {  // one 128-byte line per row: no division
           for (int t = lane; t < c; t += 32)
             asm volatile("prefetch.global.L2 [%0];" ::"l"(fb + (int64_t)w.cid[t] * rowb));
+        } else if (a.pf_rows == 2 && (rowb & 15) == 0) {
+          // one bulk prefetch per row: DRAM sees whole-row bursts instead of the lanes' single
+          // 32-byte sectors (the random-sector rate, not bandwidth, bounded the long rows)
+          for (int t = lane; t < c; t += 32)
+            asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(fb + (int64_t)w.cid[t] * rowb),
+                         "r"((uint32_t)rowb));
         } else {
           for (int t = lane; t < c * lines; t += 32) {
             const int r = t / lines;
@@ -1040,9 +1245,11 @@ static bool route_lazy(const RouteArgs& a) {
 
 bool route_large_k(const RouteArgs& a) { return route_lazy(a); }
 
+static int route_mode(const RouteArgs& a);
 size_t route_smem_per_warp(const RouteArgs& a) {
   const bool lz = route_lazy(a);
-  return route_warp_smem_bytes_full(a.Kpad, a.Cpad, a.m, a.l, lz, lz && a.gr_d != nullptr);
+  return route_warp_smem_bytes_full(a.Kpad, a.Cpad, a.m, a.l, lz, lz && a.gr_d != nullptr,
+                                    route_mode(a) == kModeF64Deep ? a.ring_slots : 0);
 }
 
 template <int MODE>
@@ -1058,7 +1265,7 @@ static int launch_route_t(const RouteArgs& a, int warps_per_cta, int ctas, size_
 static int route_mode(const RouteArgs& a) {
   if (a.F8) return kModeU8;
   if (a.f32_ok) return a.lpr == 1 ? kModeF32Lane : kModeF32Split;
-  if ((a.m & 3) == 0) return a.flt_lpr > 0 ? kModeF64Filt : kModeF64x4;
+  if ((a.m & 3) == 0) return a.flt_lpr > 0 ? kModeF64Filt : a.deep ? kModeF64Deep : kModeF64x4;
   return kModeGeneric;
 }
 
@@ -1069,6 +1276,7 @@ int launch_route(const RouteArgs& a, int warps_per_cta, int ctas, cudaStream_t s
   switch (route_mode(a)) {
     case kModeF64x4: return launch_route_t<kModeF64x4>(a, warps_per_cta, ctas, smem, st);
     case kModeF64Filt: return launch_route_t<kModeF64Filt>(a, warps_per_cta, ctas, smem, st);
+    case kModeF64Deep: return launch_route_t<kModeF64Deep>(a, warps_per_cta, ctas, smem, st);
     case kModeF32Lane: return launch_route_t<kModeF32Lane>(a, warps_per_cta, ctas, smem, st);
     case kModeF32Split: return launch_route_t<kModeF32Split>(a, warps_per_cta, ctas, smem, st);
     case kModeU8: return launch_route_t<kModeU8>(a, warps_per_cta, ctas, smem, st);
@@ -1090,6 +1298,7 @@ int route_occupancy(const RouteArgs& a, int warps_per_cta, size_t smem, int* cta
   switch (route_mode(a)) {
     case kModeF64x4: return route_occupancy_t<kModeF64x4>(warps_per_cta, smem, ctas_per_sm, lz);
     case kModeF64Filt: return route_occupancy_t<kModeF64Filt>(warps_per_cta, smem, ctas_per_sm, lz);
+    case kModeF64Deep: return route_occupancy_t<kModeF64Deep>(warps_per_cta, smem, ctas_per_sm, lz);
     case kModeF32Lane: return route_occupancy_t<kModeF32Lane>(warps_per_cta, smem, ctas_per_sm, lz);
     case kModeF32Split: return route_occupancy_t<kModeF32Split>(warps_per_cta, smem, ctas_per_sm, lz);
     case kModeU8: return route_occupancy_t<kModeU8>(warps_per_cta, smem, ctas_per_sm, lz);

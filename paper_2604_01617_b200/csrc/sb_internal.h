@@ -38,6 +38,10 @@ struct RouteArgs {
   // exact fp64 rows (8, 16 or 32); 0 = every row exact (no filter)
   int flt_lpr;
   int pf_rows;  // prefetch each batch's rows into L2 before evaluating
+  // real-valued rows: the register-pipelined instance (one CTA per SM, 128 registers of row
+  // loads in flight per lane) instead of the three-CTA one
+  int deep;
+  int ring_slots;  // its per-warp staging ring, in 144-byte row-line slots
   // u8 copy of integer features in [0, 255] (null: not available) and exact |x|^2
   const uint8_t* F8;
   const int32_t* nx8;

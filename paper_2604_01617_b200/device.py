@@ -85,8 +85,9 @@ class DeviceIndex:
         rb = ctypes.c_int32(0)
         _lib.call("sb_route_info", self._h, ctypes.addressof(path), ctypes.addressof(rb))
         names = {0: "fp64", 1: "fp32", 2: "fp32-groups", 3: "fp64-generic", 4: "u8-dp4a",
-                 5: "fp32-filter+fp64"}
-        return {"path": names.get(path.value, "none"), "row_bytes": rb.value}
+                 5: "fp32-filter+fp64", 6: "fp64"}
+        return {"path": names.get(path.value, "none"), "row_bytes": rb.value,
+                "pipelined": path.value == 6}
 
     def bf_info(self) -> dict:
         """Path of the last exhaustive top-k call, TF32 candidates passed to the re-rank and
