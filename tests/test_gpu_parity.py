@@ -500,3 +500,40 @@ def test_bench_sweep_matches_reference():
     m, l = g.features.shape[1], g.attrs.shape[1]
     assert sb.evaluate.routing_bytes(st, m, l) == \
         float(st[:, 0].sum() * (4 * m + 4 * l) + 4 * (st[:, 2].sum() + st[:, 3].sum() + st[:, 4].sum()))
+
+
+@pytest.mark.parametrize("deep", ["1", "0"])
+@pytest.mark.parametrize("m,g,k", [(4, 16, 9), (36, 8, 40), (100, 40, 64), (132, 100, 200),
+                                   (960, 24, 50), (64, 48, 1500)])
+def test_route_real_valued_both_instances(deep, m, g, k, monkeypatch):
+    """Real-valued rows (exact sequential fp64, _kernels.py:26-35) through both kernel instances:
+    the staged one (cp.async row lines in a shared-memory ring, conversion-free fp32 -> fp64:
+    small batches and long rows) and the three-CTA one (SB_ROUTE_DEEP=0).  Dimensions below,
+    at and off whole 128-byte lines, batches above the ring's rows per round (g = 100), K in
+    the insertion-buffer range, masks, subnormal / zero / huge features."""
+    monkeypatch.setenv("SB_ROUTE_DEEP", deep)
+    rng = np.random.default_rng(100 + m)
+    n, l, q = 3000, 2, 48
+    f = (rng.standard_normal((n, m)) * np.exp(rng.uniform(-3, 3, (1, m)))).astype(np.float32)
+    f[rng.integers(0, n, 40), rng.integers(0, m, 40)] = 0.0
+    f[rng.integers(0, n, 40), rng.integers(0, m, 40)] = np.float32(1e-41)   # subnormal
+    f[rng.integers(0, n, 40), rng.integers(0, m, 40)] = np.float32(-3e-39)  # subnormal
+    f[rng.integers(0, n, 10), rng.integers(0, m, 10)] = np.float32(1e18)
+    a = rng.integers(1, 5, (n, l)).astype(np.int32)
+    ids = np.stack([rng.choice(n, g, replace=False) for _ in range(n)]).astype(np.int32)
+    cnt = rng.integers(max(1, g // 2), g + 1, n).astype(np.int32)
+    graph = sb.RelationGraph(features=f, attrs=a, schema=sb.AttributeSchema((("x",),) * l),
+                             metric=sb.MetricConfig.manual(0.7, l), sigma=0.44, nbr_ids=ids,
+                             nbr_dists=np.zeros((n, g), np.float32), nbr_counts=cnt, frozen=True)
+    qf = (rng.standard_normal((q, m)) * 2).astype(np.float32)
+    qf[0] = f[7]          # a query equal to a node: zero differences
+    qa = rng.integers(1, 5, (q, l)).astype(np.int32)
+    masks = rng.integers(0, 2, (q, l)).astype(np.float64)
+    for mk in (None, masks):
+        got = sb.search_batch_arrays(graph, qf, qa, sb.SearchParams(k=k, seed=3), masks=mk)
+        info = graph.device().route_info()
+        assert info["path"] == "fp64" and info["pipelined"] == (deep == "1")
+        want = O.search_batch(f, a, ids, cnt, 0.7, qf, qa, k, seed=3, masks=mk)
+        np.testing.assert_array_equal(got[0], want[0])
+        np.testing.assert_array_equal(got[1], want[1])
+        np.testing.assert_array_equal(got[2][:, :4], want[2])
