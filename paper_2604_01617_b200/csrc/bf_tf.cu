@@ -802,7 +802,12 @@ double tf_margin(int dpad) {
   const double c_acc = (dpad / 8) * 16.0 * std::ldexp(1.0, -23);
   const double c1 = std::ldexp(1.0, -10) + std::ldexp(1.0, -22) + c_acc * (1.0 + std::ldexp(1.0, -10));
   // + the folded norm column: |hi + lo - (-(1 - cE)|x|^2 / 2)| <= 2^-21 |x|^2
-  return 1.25 * (c1 + std::ldexp(1.0, -21) + std::ldexp(1.0, -20)) + std::ldexp(1.0, -19);
+  const double cE = 1.25 * (c1 + std::ldexp(1.0, -21) + std::ldexp(1.0, -20)) + std::ldexp(1.0, -19);
+#ifdef SB_TF_MARGIN_SCALE  // tests only: a deliberately wrong margin (tests/test_gpu_tf32.py's
+  return cE * SB_TF_MARGIN_SCALE;  // adversarial case must fail with it, see profiles/README.md)
+#else
+  return cE;
+#endif
 }
 
 struct TfShape { int N, stages; bool ares; int qt, ew, kr; };

@@ -213,3 +213,39 @@ def test_tf32_two_pass_equals_single_pass(monkeypatch):
     np.testing.assert_array_equal(ids1, ids2)
     np.testing.assert_array_equal(dd1, dd2)
     assert c2 < c1, (c2, c1)
+
+
+@pytest.mark.parametrize("m,k,scale", [(96, 10, 1.0), (96, 50, 1024.0), (960, 10, 1.0), (960, 32, 2.0 ** -20)])
+def test_tf32_margin_adversarial(m, k, scale):
+    """Worst case for the certified TF32 margin (bf_tf.cu tf_margin): every coordinate of the
+    query and of its true neighbours sits just below a TF32 rounding midpoint
+    (1 + 2^-11 - 2^-19 (1 + r)), so each operand loses almost 2^-11 in the same direction, x is
+    parallel to q and |x| = |q| (both inequalities of the bound are tight): the filter sees
+    S~ ~ 2^-10 (|x|^2 + |q|^2) for neighbours whose true S is ~1e-9 d, about 0.8 of the margin.
+    The decoys are TF32-exact vectors (no operand error) that are truly farther but look four
+    times nearer to the filter.  The exact top-k must still be the true neighbours: a margin
+    below the real error would drop them silently."""
+    rng = np.random.default_rng(m + k)
+    n, l, q = 4000, 1, 8
+    base = np.float32(1.0 + 2.0 ** -11 - 2.0 ** -19)
+    qf32 = np.full((q, m), base, np.float32)
+    qf32 -= (np.float32(2.0 ** -19) * rng.integers(0, 4, (q, m))).astype(np.float32)
+    f = np.empty((n, m), np.float32)
+    n_true = 3 * k
+    f[:n_true] = base - (np.float32(2.0 ** -19) * rng.integers(0, 60, (n_true, m))).astype(np.float32)
+    f[n_true:] = (1.0 + 2.0 ** -10 * rng.integers(0, 2, (n - n_true, m)) *
+                  (rng.random((n - n_true, 1)) < 0.02)).astype(np.float32)  # sparse steps: near 1
+    perm = rng.permutation(n)
+    f = np.ascontiguousarray(f[perm] * np.float32(scale))
+    qf = (qf32 * np.float32(scale)).astype(np.float64)
+    a = np.ones((n, l), np.int32)
+    qa = np.ones((q, l), np.int32)
+    d = DeviceIndex(f, a, 2)
+    ids, dd = d.bf_topk_queries(qf, qa, k, 0.7, None)
+    assert d.bf_info()["path"] == "tc-tf32-filter"
+    true_ids = set(np.nonzero(perm < n_true)[0].tolist())
+    for qi in range(q):
+        wi, wd = O.oracle_auto_topk(f, a, qf[qi], qa[qi], k, 0.7, return_dists=True)
+        assert set(wi.tolist()) <= true_ids  # the construction: the exact answer is all true neighbours
+        np.testing.assert_array_equal(ids[qi], wi, err_msg=f"query {qi}")
+        np.testing.assert_array_equal(dd[qi], wd, err_msg=f"query {qi}")
