@@ -200,29 +200,58 @@ __global__ void __launch_bounds__(kJoinThreads, U8 ? 3 : 2) join_emit_kernel(Joi
             }
         }
       }
-      for (int d0 = 0; !U8 && d0 < a.m; d0 += a.dc) {
-        const int dc = a.m - d0 < a.dc ? a.m - d0 : a.dc;
-        if (!whole) {
-          __syncthreads();
-          for (int e = tid; e < ns * dc; e += blockDim.x) {
-            int t = e / dc, dd = e % dc;
-            s.xs[dd * spad + t] = __ldg(a.F + (int64_t)s.slot_id[t] * a.m + d0 + dd);
-          }
-          __syncthreads();
+      // one 4x4 tile's sums over the dimensions staged at xs_ (dc_ rows of spad floats)
+      auto tile_dims = [&](const float* xs_, int dc_) {
+        for (int dd = 0; dd < dc_; ++dd) {
+          const float* row = xs_ + (size_t)dd * spad;
+          float4 xv = *reinterpret_cast<const float4*>(row + rb * kJT);
+          float4 yv = *reinterpret_cast<const float4*>(row + cb * kJT);
+          const double xx[4] = {(double)xv.x, (double)xv.y, (double)xv.z, (double)xv.w};
+          const double yy[4] = {(double)yv.x, (double)yv.y, (double)yv.z, (double)yv.w};
+#pragma unroll
+          for (int u = 0; u < kJT; ++u)
+#pragma unroll
+            for (int w = 0; w < kJT; ++w) acc[u][w] = sq_step(acc[u][w], xx[u], yy[w]);
         }
-        if (have) {
-          const int off = whole ? d0 : 0;
-          for (int dd = 0; dd < dc; ++dd) {
-            const float* row = s.xs + (size_t)(off + dd) * spad;
-            float4 xv = *reinterpret_cast<const float4*>(row + rb * kJT);
-            float4 yv = *reinterpret_cast<const float4*>(row + cb * kJT);
-            const double xx[4] = {(double)xv.x, (double)xv.y, (double)xv.z, (double)xv.w};
-            const double yy[4] = {(double)yv.x, (double)yv.y, (double)yv.z, (double)yv.w};
-#pragma unroll
-            for (int u = 0; u < kJT; ++u)
-#pragma unroll
-              for (int w = 0; w < kJT; ++w) acc[u][w] = sq_step(acc[u][w], xx[u], yy[w]);
+      };
+      if (!U8 && whole) {
+        if (have) tile_dims(s.xs, a.m);
+      } else if (!U8) {
+        // Dimension chunks through two half stages: the 4-byte asynchronous copies of chunk
+        // c + 1 (a warp per slot, lanes along the dimensions: coalesced, transposed into
+        // [dimension][slot]) run under the pair sums of chunk c.  (A load -> store staging loop
+        // spent half of this kernel's stall samples waiting for one load per thread:
+        // profiles/README.md.)
+        const int dch = a.dc >> 1;
+        const int lane_ = tid & 31, nwarp = blockDim.x >> 5;
+        auto stage = [&](int c) {
+          const int d0 = c * dch;
+          const int dc_ = a.m - d0 < dch ? a.m - d0 : dch;
+          float* dst = s.xs + (size_t)(c & 1) * dch * spad;
+          for (int t = tid >> 5; t < ns; t += nwarp) {
+            const float* src = a.F + (int64_t)s.slot_id[t] * a.m + d0;
+            for (int dd = lane_; dd < dc_; dd += 32)
+              asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(
+                               (uint32_t)__cvta_generic_to_shared(dst + dd * spad + t)),
+                           "l"(src + dd)
+                           : "memory");
           }
+          asm volatile("cp.async.commit_group;" ::: "memory");
+        };
+        const int nchunk = (a.m + dch - 1) / dch;
+        __syncthreads();  // the previous pass is done with both half stages
+        stage(0);
+        for (int c = 0; c < nchunk; ++c) {
+          if (c + 1 < nchunk) {
+            stage(c + 1);
+            asm volatile("cp.async.wait_group 1;" ::: "memory");
+          } else {
+            asm volatile("cp.async.wait_group 0;" ::: "memory");
+          }
+          __syncthreads();  // chunk c has landed for every thread
+          const int d0 = c * dch;
+          if (have) tile_dims(s.xs + (size_t)(c & 1) * dch * spad, a.m - d0 < dch ? a.m - d0 : dch);
+          __syncthreads();  // its half stage may be overwritten (by chunk c + 2)
         }
       }
       // pushes (warp-uniform loop; lanes without a tile contribute nothing)

@@ -57,11 +57,21 @@ __global__ void __launch_bounds__(kPruneThreads) prune_bits_kernel(PruneArgs a) 
   for (int t = tid; t < cpad * a.W; t += blockDim.x) bits[t] = 0u;
   __syncthreads();
 
+  // dimensions [d0, d0 + dc) of every row entry, transposed into [dimension][entry], by 4-byte
+  // asynchronous copies: a warp per entry, lanes along the dimensions (coalesced), the whole
+  // chunk in flight at once (a load -> store loop waits for one load per thread at a time)
   auto stage = [&](int d0, int dc) {
-    for (int e = tid; e < cnt * dc; e += blockDim.x) {
-      int t = e / dc, dd = e % dc;
-      xr[dd * cpad + t] = __ldg(a.F + (int64_t)eid[t] * a.m + d0 + dd);
+    const int lane_ = tid & 31, nwarp = blockDim.x >> 5;
+    for (int t = tid >> 5; t < cnt; t += nwarp) {
+      const float* src = a.F + (int64_t)eid[t] * a.m + d0;
+      for (int dd = lane_; dd < dc; dd += 32)
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(
+                         (uint32_t)__cvta_generic_to_shared(xr + dd * cpad + t)),
+                     "l"(src + dd)
+                     : "memory");
     }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+    asm volatile("cp.async.wait_group 0;" ::: "memory");
   };
   // norms |p_t - s|^2, sequential over dimensions (np2 / nk2 of _diff_cosine)
   {
