@@ -146,20 +146,29 @@ __global__ void __launch_bounds__(kJoinThreads, U8 ? 3 : 2) join_emit_kernel(Joi
     }
     __syncthreads();
     const int ntiles = sh_ntiles;
-    if (U8) {
-      const int nw = a.m >> 2;
-      uint32_t* xw = reinterpret_cast<uint32_t*>(s.xs);
-      for (int e = tid; e < ns * nw; e += blockDim.x) {
-        const int t = e / nw, dw = e % nw;
-        xw[dw * spad + t] = __ldg(reinterpret_cast<const uint32_t*>(a.F8 + (int64_t)s.slot_id[t] * a.m) + dw);
+    // whole rows staged once per node, transposed into [word][slot], by 4-byte asynchronous
+    // copies (a warp per slot, lanes along the row: coalesced; every copy in flight at once)
+    auto stage_whole = [&](const void* base, int64_t row_bytes, int nwords) {
+      const int lane_ = tid & 31, nwarp = blockDim.x >> 5;
+      for (int t = tid >> 5; t < ns; t += nwarp) {
+        const uint32_t* src = reinterpret_cast<const uint32_t*>(
+            reinterpret_cast<const char*>(base) + (int64_t)s.slot_id[t] * row_bytes);
+        for (int dw = lane_; dw < nwords; dw += 32)
+          asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(
+                           (uint32_t)__cvta_generic_to_shared(s.xs + dw * spad + t)),
+                       "l"(src + dw)
+                       : "memory");
       }
+      asm volatile("cp.async.commit_group;" ::: "memory");
+    };
+    if (U8) {
+      stage_whole(a.F8, a.m, a.m >> 2);
       for (int t = tid; t < ns; t += blockDim.x) s.nrm[t] = __ldg(a.nx8 + s.slot_id[t]);
+      asm volatile("cp.async.wait_group 0;" ::: "memory");
       __syncthreads();
     } else if (whole) {
-      for (int e = tid; e < ns * a.m; e += blockDim.x) {
-        int t = e / a.m, dd = e % a.m;
-        s.xs[dd * spad + t] = __ldg(a.F + (int64_t)s.slot_id[t] * a.m + dd);
-      }
+      stage_whole(a.F, (int64_t)a.m * 4, a.m);
+      asm volatile("cp.async.wait_group 0;" ::: "memory");
       __syncthreads();
     }
     for (int pass = 0; pass * kJoinThreads < ntiles; ++pass) {

@@ -189,9 +189,18 @@ __global__ void __launch_bounds__(kPruneThreads) prune_bits_u8_kernel(PruneArgs 
   }
   for (int t = tid; t < cpad * a.W; t += blockDim.x) bits[t] = 0u;
   __syncthreads();
-  for (int e = tid; e < cnt * mw; e += blockDim.x) {
-    const int t = e / mw, w = e - t * mw;
-    xr[t * rs + w] = __ldg(F8w + (int64_t)eid[t] * mw + w);
+  {  // every row entry's u8 words, a warp per entry, by 4-byte asynchronous copies
+    const int lane_ = tid & 31, nwarp = blockDim.x >> 5;
+    for (int t = tid >> 5; t < cnt; t += nwarp) {
+      const uint32_t* src = F8w + (int64_t)eid[t] * mw;
+      for (int w = lane_; w < mw; w += 32)
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(
+                         (uint32_t)__cvta_generic_to_shared(xr + t * rs + w)),
+                     "l"(src + w)
+                     : "memory");
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+    asm volatile("cp.async.wait_group 0;" ::: "memory");
   }
   __syncthreads();
   for (int t = tid; t < cnt; t += blockDim.x) {
@@ -565,9 +574,22 @@ SB_DEV void cta_pair_bits(const SeqCtx& c, const int64_t* mi, int total, int64_t
     for (int d0 = 0; d0 < c.m; d0 += kRcDc) {
       const int dc = c.m - d0 < kRcDc ? c.m - d0 : kRcDc;
       __syncthreads();
-      for (int e = tid; e < cpad * dc; e += kRcThreads) {
-        const int t = e / dc, dd = e - t * dc;
-        xr[dd * cpad + t] = t < total ? __ldg(c.F + mi[t] * c.m + d0 + dd) : 0.f;
+      {  // a warp per entry, 4-byte asynchronous copies (zeros behind the merged list)
+        const int lane_ = tid & 31;
+        for (int t = tid >> 5; t < cpad; t += kRcThreads >> 5) {
+          if (t < total) {
+            const float* src = c.F + mi[t] * c.m + d0;
+            for (int dd = lane_; dd < dc; dd += 32)
+              asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(
+                               (uint32_t)__cvta_generic_to_shared(xr + dd * cpad + t)),
+                           "l"(src + dd)
+                           : "memory");
+          } else {
+            for (int dd = lane_; dd < dc; dd += 32) xr[dd * cpad + t] = 0.f;
+          }
+        }
+        asm volatile("cp.async.commit_group;" ::: "memory");
+        asm volatile("cp.async.wait_group 0;" ::: "memory");
       }
       __syncthreads();
       if (pass == 0)

@@ -157,6 +157,21 @@ __global__ void __launch_bounds__(kRfThreads) rf_bits_kernel(RfArgs a, int dc_ma
   double* nrm = reinterpret_cast<double*>(p);
   const int tid = threadIdx.x;
   const int up4 = (u + 3) & ~3;
+  // dimensions [d0, d0 + dc) of every member of U_j, transposed, by 4-byte asynchronous copies
+  // (a warp per member, lanes along the dimensions)
+  auto stage_rows = [&](int d0, int dc) {
+    const int lane_ = tid & 31, nwarp = blockDim.x >> 5;
+    for (int t = tid >> 5; t < u; t += nwarp) {
+      const float* src = a.F + (int64_t)U[t] * a.m + d0;
+      for (int dd = lane_; dd < dc; dd += 32)
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(
+                         (uint32_t)__cvta_generic_to_shared(xr + dd * up4 + t)),
+                     "l"(src + dd)
+                     : "memory");
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+    asm volatile("cp.async.wait_group 0;" ::: "memory");
+  };
   // norms |p - j|^2 in ascending dimension order; thread tid owns entries tid + 256 r
   constexpr int kMaxPer = 16;  // u <= 4096
   double myn[kMaxPer];
@@ -166,10 +181,7 @@ __global__ void __launch_bounds__(kRfThreads) rf_bits_kernel(RfArgs a, int dc_ma
     const int dc = a.m - d0 < dc_max ? a.m - d0 : dc_max;
     __syncthreads();
     for (int t = tid; t < dc; t += blockDim.x) xs[t] = (double)__ldg(a.F + (int64_t)j * a.m + d0 + t);
-    for (int e = tid; e < u * dc; e += blockDim.x) {
-      int t = e / dc, dd = e % dc;
-      xr[dd * up4 + t] = __ldg(a.F + (int64_t)U[t] * a.m + d0 + dd);
-    }
+    stage_rows(d0, dc);
     __syncthreads();
 #pragma unroll
     for (int r = 0; r < kMaxPer; ++r) {
@@ -207,10 +219,7 @@ __global__ void __launch_bounds__(kRfThreads) rf_bits_kernel(RfArgs a, int dc_ma
       const int dc = a.m - d0 < dc_max ? a.m - d0 : dc_max;
       __syncthreads();
       for (int t = tid; t < dc; t += blockDim.x) xs[t] = (double)__ldg(a.F + (int64_t)j * a.m + d0 + t);
-      for (int e = tid; e < u * dc; e += blockDim.x) {
-        int t = e / dc, dd = e % dc;
-        xr[dd * up4 + t] = __ldg(a.F + (int64_t)U[t] * a.m + d0 + dd);
-      }
+      stage_rows(d0, dc);
       __syncthreads();
       if (have) {
         for (int dd = 0; dd < dc; ++dd) {
