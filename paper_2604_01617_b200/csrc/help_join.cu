@@ -103,7 +103,7 @@ __global__ void __launch_bounds__(kJoinThreads, U8 ? 3 : 2) join_emit_kernel(Joi
     s.tiles = reinterpret_cast<int*>(p); p += sizeof(int) * (size_t)a.ntiles_max;
     s.nrm = reinterpret_cast<int32_t*>(p);
   }
-  __shared__ int sh_node, sh_ntiles, sh_na, sh_nb;
+  __shared__ int sh_node[2];
   const int tid = threadIdx.x;
   Emitter em;
   em.base = 0;
@@ -111,21 +111,19 @@ __global__ void __launch_bounds__(kJoinThreads, U8 ? 3 : 2) join_emit_kernel(Joi
   const bool whole = a.dc >= a.m;  // all dimensions staged at once
   unsigned same = 0;  // (x, y) slots holding one id twice (in both the new and the old list)
 
-  for (;;) {
-    __syncthreads();
-    if (tid == 0) {
-      int64_t i = a.node_begin + atomicAdd(a.node_counter, 1);
-      sh_node = i < a.node_end ? (int)i : -1;
-    }
-    __syncthreads();
-    const int node = sh_node;
+  // the node after the current one is claimed while the current one is processed (the counter's
+  // round trip and two barriers per node left the critical path)
+  auto claim = [&]() {
+    const int64_t i = a.node_begin + atomicAdd(a.node_counter, 1);
+    return i < a.node_end ? (int)i : -1;
+  };
+  if (tid == 0) sh_node[0] = claim();
+  for (int it = 0;; ++it) {
+    __syncthreads();  // the claim is visible; the previous node's shared-memory reads are done
+    const int node = sh_node[it & 1];
     if (node < 0) break;
-    if (tid == 0) {
-      sh_na = a.new_cnt[node];
-      sh_nb = a.old_cnt[node];
-    }
-    __syncthreads();
-    const int na = sh_na, nb = sh_nb;
+    if (tid == 0) sh_node[(it + 1) & 1] = claim();
+    const int na = __ldg(a.new_cnt + node), nb = __ldg(a.old_cnt + node);
     const int ns = na + nb;
     if (na == 0) continue;
     for (int t = tid; t < ns; t += blockDim.x) {
@@ -137,15 +135,15 @@ __global__ void __launch_bounds__(kJoinThreads, U8 ? 3 : 2) join_emit_kernel(Joi
     for (int t = ns + tid; t < spad; t += blockDim.x) s.slot_id[t] = -1;
     // tile list: row block rb (x in [4rb, 4rb+4) ⊂ new), col block cb (y in [4cb, 4cb+4)),
     // keep tiles holding at least one pair with y > x, y < ns
-    if (tid == 0) {
-      int nt = 0;
-      int nrb = (na + kJT - 1) / kJT, ncb = (ns + kJT - 1) / kJT;
-      for (int rb = 0; rb < nrb; ++rb)
-        for (int cb = rb; cb < ncb; ++cb) s.tiles[nt++] = (rb << 16) | cb;
-      sh_ntiles = nt;
+    // (row block rb owns the ncb - rb tiles from offset rb ncb - rb (rb - 1) / 2: the threads
+    // fill the list row block by row block, eight threads per row block)
+    const int nrb = (na + kJT - 1) / kJT, ncb = (ns + kJT - 1) / kJT;
+    for (int rb = tid >> 3; rb < nrb; rb += blockDim.x >> 3) {
+      const int off = rb * ncb - rb * (rb - 1) / 2 - rb;
+      for (int cb = rb + (tid & 7); cb < ncb; cb += 8) s.tiles[off + cb] = (rb << 16) | cb;
     }
     __syncthreads();
-    const int ntiles = sh_ntiles;
+    const int ntiles = nrb * ncb - nrb * (nrb - 1) / 2;
     // whole rows staged once per node, transposed into [word][slot], by 4-byte asynchronous
     // copies (a warp per slot, lanes along the row: coalesced; every copy in flight at once)
     auto stage_whole = [&](const void* base, int64_t row_bytes, int nwords) {
