@@ -52,6 +52,7 @@ constexpr int kRows = 8;                   // rows per lane group in flight (fp3
 #endif
 constexpr int kLazyB = 64;  // insertion buffer of the large-K kernel instances
 constexpr int kLazyK = 1024; // K from which routing uses the insertion buffer
+constexpr int kLazyW = kLazyB + 2;  // cached window of R below a rank bound (kLazyB + 1 entries used)
 #ifndef ROUTE_FAST_MERGE
 #define ROUTE_FAST_MERGE 1
 #endif
@@ -60,6 +61,8 @@ constexpr bool kFastMerge = ROUTE_FAST_MERGE != 0;  // warp_merge_lanes for batc
 struct WarpSmem {
   double* bd;     // kLazyB (large-K instances)
   uint32_t* bid;  // kLazyB
+  double* wd;     // 2 x kLazyW: R[hi - 1 - j], j = 0..kLazyB, for hi = K and hi = P (large-K instances)
+  uint32_t* wi;   // 2 x kLazyW
   double* rd;     // Kpad
   double* cd;     // Cpad
   double* qs;     // m
@@ -78,7 +81,7 @@ SB_HD size_t route_warp_smem_bytes_full(int Kpad, int Cpad, int m, int l, bool l
                                          bool rglobal = false, int ring_slots = 0) {
   if (rglobal) Kpad = 0;  // R lives in global memory
   size_t b = (size_t)((m + 3) & ~3) * 4;  // fp32 query first: 16-byte aligned float4 reads
-  if (lazy) b += (size_t)kLazyB * 12;
+  if (lazy) b += (size_t)(kLazyB + 2 * kLazyW) * 12;
   // the fp64 query is padded with zeros to whole 32-dimension lines (staged evaluation)
   b += (size_t)Kpad * 8 + (size_t)Cpad * 8 + (size_t)((m + 31) & ~31) * 8 + (size_t)l * 16;
   b += (size_t)Kpad * 4 + (size_t)Cpad * 8;
@@ -95,11 +98,16 @@ SB_DEV WarpSmem carve(char* base, const RouteArgs& a, int64_t slot) {
   w.qs = dp; dp += (a.m + 31) & ~31;  // 16-byte aligned (double2 reads), zero-padded to lines
   w.bd = nullptr;
   w.bid = nullptr;
+  w.wd = nullptr;
+  w.wi = nullptr;
   if (LAZY) {
     w.bd = dp;
     dp += kLazyB;
+    w.wd = dp;
+    dp += 2 * kLazyW;
     w.bid = reinterpret_cast<uint32_t*>(dp);
-    dp = reinterpret_cast<double*>(w.bid + kLazyB);
+    w.wi = w.bid + kLazyB;
+    dp = reinterpret_cast<double*>(w.wi + 2 * kLazyW);
   }
   if (rg) {
     w.rd = a.gr_d + slot * a.Kpad;
@@ -618,6 +626,25 @@ SB_DEV int first_unchecked(const uint32_t* rid, int lb, int hi, uint32_t bit, in
   return -1;
 }
 
+// first position in [lb, hi) whose id word lacks `bit`, with that entry's distance and id (the
+// distances ride along with the flag words: one memory round trip); -1 if none
+SB_DEV int first_unchecked_d(const double* rd, const uint32_t* rid, int lb, int hi, uint32_t bit,
+                             double* dsel, uint32_t* isel) {
+  for (int base = lb; base < hi; base += 32) {
+    const int i = base + lane_id();
+    const uint32_t wv = i < hi ? rid[i] : bit;
+    const double dv = i < hi ? rd[i] : 0.0;
+    const unsigned bal = __ballot_sync(0xffffffffu, !(wv & bit));
+    if (bal) {
+      const int f = __ffs(bal) - 1;
+      *dsel = __shfl_sync(0xffffffffu, dv, f);
+      *isel = __shfl_sync(0xffffffffu, wv, f);
+      return base + f;
+    }
+  }
+  return -1;
+}
+
 // warm L2 with the neighbour row of a node we will probably expand next
 SB_DEV void prefetch_row(const RouteArgs& a, uint32_t node) {
   const int lane = lane_id();
@@ -790,11 +817,42 @@ route_kernel(RouteArgs a) {
     int nbuf = 0;  // LAZY: entries in the insertion buffer B
     const int bcap = Cap < kLazyB ? Cap : kLazyB;
     // LAZY: merge B into R (drops whatever leaves the top K)
+    // LAZY: R changes only when B (or an oversized batch) is merged into it, so the entries just
+    // below the two rank bounds the walk uses (K: admission and phase-2 selection; P: phase-1
+    // selection) are cached in shared memory: window h holds R[hi - 1 - j], j = 0..kLazyB
+    // (-inf where R has no such entry).  With R in global memory this takes the admission tail
+    // and the rank tests of every expansion off the memory round trips.
+    auto refresh_windows = [&]() {
+      if (!LAZY) return;
+      __syncwarp();
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int hi_h = h ? a.P : K;
+        for (int j = lane; j <= kLazyB; j += 32) {
+          const int idx = hi_h - 1 - j;
+          w.wd[h * kLazyW + j] = idx >= 0 ? w.rd[idx] : -__longlong_as_double(0x7FF0000000000000ll);
+          w.wi[h * kLazyW + j] = idx >= 0 ? (w.rid[idx] & kIdMask) : 0u;
+        }
+      }
+      __syncwarp();
+    };
+    // entries of B within the first hi of R ∪ B (a prefix of B: B[j-1] before R[hi-j])
+    auto b_in_top = [&](int h) {
+      int jt = 0;
+      for (int base = 0; base < nbuf; base += 32) {
+        const int j = base + lane + 1;
+        const bool p = j <= nbuf && ord(w.bd[j - 1], w.bid[j - 1] & kIdMask, w.wd[h * kLazyW + j - 1],
+                                        w.wi[h * kLazyW + j - 1]);
+        jt += __popc(__ballot_sync(0xffffffffu, p));
+      }
+      return jt;
+    };
     auto flush_b = [&]() {
       if (nbuf > 0) {
         const int ins = merge_into_r<LAZY>(a, w.rd, w.rid, K, w.bd, w.bid, w.cpos, nbuf, ord, true);
         if (ins < lb) lb = ins;
         nbuf = 0;
+        refresh_windows();
       }
     };
     // LAZY: admit the batch cd/cid[0..c) against the K-th entry of R ∪ B, then add it to B
@@ -802,15 +860,9 @@ route_kernel(RouteArgs a) {
     auto lazy_merge = [&](int c) {
       // the union's K-th entry: j = number of B entries within the first K of R ∪ B
       // (B[j-1] before R[K-j] holds for a prefix of j = 1..nbuf: count it by ballots)
-      int jt = 0;
-      for (int base = 0; base < nbuf; base += 32) {
-        const int j = base + lane + 1;
-        const bool p = j <= nbuf && ord(w.bd[j - 1], w.bid[j - 1] & kIdMask, w.rd[K - j],
-                                        w.rid[K - j] & kIdMask);
-        jt += __popc(__ballot_sync(0xffffffffu, p));
-      }
-      double td = w.rd[K - 1 - jt];
-      uint32_t ti = w.rid[K - 1 - jt] & kIdMask;
+      const int jt = b_in_top(0);
+      double td = w.wd[jt];       // R[K - 1 - jt]
+      uint32_t ti = w.wi[jt];
       if (jt > 0 && ord(td, ti, w.bd[jt - 1], w.bid[jt - 1] & kIdMask)) {
         td = w.bd[jt - 1];
         ti = w.bid[jt - 1] & kIdMask;
@@ -841,6 +893,7 @@ route_kernel(RouteArgs a) {
       if (kept > bcap) {
         const int ins = merge_into_r<LAZY>(a, w.rd, w.rid, K, w.cd, w.cid, w.cpos, kept, ord);
         if (ins < lb) lb = ins;
+        refresh_windows();
         return;
       }
       // B <- B ∪ batch by ranks (distinct ids): B[j] goes to j + #{batch < B[j]}, batch entry
@@ -901,19 +954,21 @@ route_kernel(RouteArgs a) {
         if (LAZY) {
           // first unchecked of R (by position) and of B, each admitted only if its rank in
           // R ∪ B is below hi; the smaller of the two is the reference's selection
-          int iR = first_unchecked(w.rid, lb, hi, bit, &nxt);  // rank >= position
-          if (iR >= 0 && iR + warp_count_before(w.bd, w.bid, nbuf, w.rd[iR], w.rid[iR] & kIdMask, ord) >= hi)
-            iR = -1;
+          // The first hi of R ∪ B are B[0, jt) and R[0, hi - jt) (jt from the cached window, no
+          // access to R): the first unchecked entry of each, the smaller of the two.
+          nxt = -1;
+          const int jt = b_in_top(p1 ? 1 : 0);
+          double dR = 0.0;
+          uint32_t idR = 0u;
+          int iR = first_unchecked_d(w.rd, w.rid, lb, hi - jt, bit, &dR, &idR);
           int jB = -1;
-          for (int base = 0; base < nbuf && jB < 0; base += 32) {
+          for (int base = 0; base < jt && jB < 0; base += 32) {
             const int j = base + lane;
-            const unsigned bal = __ballot_sync(0xffffffffu, j < nbuf && !(w.bid[j] & bit));
+            const unsigned bal = __ballot_sync(0xffffffffu, j < jt && !(w.bid[j] & bit));
             if (bal) jB = base + __ffs(bal) - 1;
           }
-          if (jB >= 0 && jB + warp_count_before(w.rd, w.rid, K, w.bd[jB], w.bid[jB] & kIdMask, ord) >= hi)
-            jB = -1;
           if (iR >= 0 && jB >= 0) {
-            if (ord(w.bd[jB], w.bid[jB] & kIdMask, w.rd[iR], w.rid[iR] & kIdMask)) iR = -1;
+            if (ord(w.bd[jB], w.bid[jB] & kIdMask, dR, idR & kIdMask)) iR = -1;
             else jB = -1;
           }
           if (iR < 0 && jB < 0) {
@@ -926,7 +981,7 @@ route_kernel(RouteArgs a) {
             continue;
           }
           sel = iR;
-          node = iR >= 0 ? (w.rid[iR] & kIdMask) : (w.bid[jB] & kIdMask);
+          node = iR >= 0 ? (idR & kIdMask) : (w.bid[jB] & kIdMask);
           __syncwarp();
           if (lane == 0) {
             if (iR >= 0) w.rid[iR] |= bit;
@@ -1044,6 +1099,7 @@ route_kernel(RouteArgs a) {
           }
           stage = a.use_coarse ? 1 : 2;
           lb = 0;
+          refresh_windows();
         }
         __syncwarp();
       } else if (c > 0) {
