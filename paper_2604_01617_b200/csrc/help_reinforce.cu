@@ -329,7 +329,7 @@ __host__ __device__ size_t rf_simulate_smem(int g, int wmax) {
 #define SB_RF_PROF 0
 #endif
 constexpr bool kRfProf = SB_RF_PROF != 0;
-__device__ unsigned long long g_rf_prof[8];
+__device__ unsigned long long g_rf_prof[16];
 
 // cu_hint: cand's position in U_j when known (precomputed for static edges, recorded for
 // mirrors), or -1 to search U_j
@@ -370,7 +370,9 @@ SB_DEV int warp_try_insert(RfArgs& a, const SimSmem& S, int32_t j, int o, int32_
     if (kRfProf && lane == 0) { atomicAdd(&g_rf_prof[4], (unsigned long long)(clock64() - t_start)); atomicAdd(&g_rf_prof[5], 1ull); }
     return 0;
   }
+  const long long t_dup = clock64();
   const int cu = cu_hint >= 0 ? cu_hint : warp_u_index(a.u_list + uoff, usz, cand);
+  const long long t_uidx = clock64();
   if (cu < 0) {
     err = 1;
     return 0;
@@ -408,16 +410,90 @@ SB_DEV int warp_try_insert(RfArgs& a, const SimSmem& S, int32_t j, int o, int32_
   __syncwarp();
   // in-degrees: an entry's in-degree changes in this call only when that entry is dropped,
   // after which it is never read again, so loading them all up front is exact
-  for (int t = lane; t < total; t += 32) {
-    const int32_t p = S.mi[t];
-    S.midg[t] = p == cand ? 0 : indeg_read(a, p, s);
-    S.mkeep[t] = 1;
-  }
+  // the merged entries' redundancy rows: 4-byte asynchronous copies, all in flight at once (a
+  // load -> store loop paid one L2 round trip per 32 words: ~50 k cycles per re-prune, half of
+  // the replay's time on a single-attribute-value index)
   for (int e = lane; e < total * W; e += 32) {
     const int t = e / W, w = e - t * W;
-    S.Rs[e] = R[(int64_t)S.mu[t] * W + w];
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(
+                     (uint32_t)__cvta_generic_to_shared(S.Rs + e)),
+                 "l"(R + (int64_t)S.mu[t] * W + w)
+                 : "memory");
   }
+  asm volatile("cp.async.commit_group;" ::: "memory");
+  {  // in-degrees of up to 9 entries per lane (g + 1 <= 257): every load of a level issued before any is used
+    int32_t pp[9], vv[9];
+    bool st[9];
+#pragma unroll
+    for (int k = 0; k < 9; ++k) {
+      const int t = lane + 32 * k;
+      pp[k] = t < total ? S.mi[t] : cand;
+      vv[k] = pp[k] == cand ? 0 : __ldcg(a.in_deg + pp[k]);  // other groups update in-degrees with L2 atomics
+      st[k] = pp[k] != cand && pp[k] < s && !a.is_o[pp[k]];
+    }
+#pragma unroll
+    for (int k = 0; k < 9; ++k)
+      if (st[k]) vv[k] += a.static_ins[pp[k]];
+#pragma unroll
+    for (int k = 0; k < 9; ++k) {
+      const int t = lane + 32 * k;
+      if (t < total) {
+        S.midg[t] = vv[k];
+        S.mkeep[t] = 1;
+      }
+    }
+  }
+  asm volatile("cp.async.wait_group 0;" ::: "memory");
   __syncwarp();
+  const long long t_loads = clock64();
+  int kept = 1;
+  if (total <= 128) {
+    // Greedy re-prune in list order.  The kept-U mask lives in registers (word lane + 32 k);
+    // nothing on the loop-carried path but the row test, one vote and the mask update: the
+    // safeguard condition of every entry comes from ballots taken up front, the keep flags
+    // collect in register masks (no shared-memory store in the loop, so the rows and U
+    // positions of the next entries load ahead of the votes).
+    unsigned cond[4], keep[4] = {1u, 0u, 0u, 0u};
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      const int k = lane + 32 * c;
+      const bool cd = k < total && (S.mi[k] == cand || S.midg[k] >= 2);
+      cond[c] = __ballot_sync(kFull, cd);
+    }
+    uint32_t km[4] = {0u, 0u, 0u, 0u};
+    {
+      const int u0 = S.mu[0];
+#pragma unroll
+      for (int k = 0; k < 4; ++k)
+        if ((u0 >> 5) == lane + 32 * k) km[k] |= 1u << (u0 & 31);
+    }
+#pragma unroll
+    for (int c0 = 0; c0 < 4; ++c0) {  // (static indices: the masks stay in registers)
+      const int tend = total - 32 * c0 < 32 ? total - 32 * c0 : 32;
+#pragma unroll 4
+      for (int tb = c0 == 0 ? 1 : 0; tb < tend; ++tb) {
+        const int t = 32 * c0 + tb;
+        const int ut = S.mu[t];
+        const uint32_t* rr = S.Rs + t * W;
+        bool hit = false;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const int w = lane + 32 * k;
+          if (w < W) hit = hit || (rr[w] & km[k]) != 0u;
+        }
+        const bool red = __any_sync(kFull, hit);
+        if (!(red && ((cond[c0] >> tb) & 1u))) {
+          keep[c0] |= 1u << tb;
+#pragma unroll
+          for (int k = 0; k < 4; ++k)
+            if ((ut >> 5) == lane + 32 * k) km[k] |= 1u << (ut & 31);
+        }
+      }
+    }
+    kept = __popc(keep[0]) + __popc(keep[1]) + __popc(keep[2]) + __popc(keep[3]);
+    __syncwarp();
+    for (int t = lane; t < total; t += 32) S.mkeep[t] = (uint8_t)((keep[t >> 5] >> (t & 31)) & 1u);
+  } else {
   // greedy re-prune in list order; the kept-U mask lives in registers (word lane + 32 k)
   uint32_t km[4] = {0u, 0u, 0u, 0u};
   {
@@ -426,7 +502,6 @@ SB_DEV int warp_try_insert(RfArgs& a, const SimSmem& S, int32_t j, int o, int32_
     for (int k = 0; k < 4; ++k)
       if ((u0 >> 5) == lane + 32 * k) km[k] |= 1u << (u0 & 31);
   }
-  int kept = 1;
   for (int t = 1; t < total; ++t) {
     const uint32_t* rr = S.Rs + t * W;
     bool hit = false;
@@ -447,7 +522,9 @@ SB_DEV int warp_try_insert(RfArgs& a, const SimSmem& S, int32_t j, int o, int32_
         if ((ut >> 5) == lane + 32 * k) km[k] |= 1u << (ut & 31);
     }
   }
+  }
   __syncwarp();
+  const long long t_greedy = clock64();
   if (kept > g && lane == 0) {
     for (int t = total - 1; t >= 0; --t) {
       if (!S.mkeep[t]) continue;
@@ -476,7 +553,16 @@ SB_DEV int warp_try_insert(RfArgs& a, const SimSmem& S, int32_t j, int o, int32_
   if (lane == 0) {
     a.counts[j] = w0;
     if (inserted) atomicAdd(a.in_deg + cand, 1);
-    if (kRfProf) { atomicAdd(&g_rf_prof[2], (unsigned long long)(clock64() - t_start)); atomicAdd(&g_rf_prof[3], 1ull); }
+    if (kRfProf) {
+      const long long t_end = clock64();
+      atomicAdd(&g_rf_prof[2], (unsigned long long)(t_end - t_start)); atomicAdd(&g_rf_prof[3], 1ull);
+      atomicAdd(&g_rf_prof[8], (unsigned long long)(t_dup - t_start));
+      atomicAdd(&g_rf_prof[9], (unsigned long long)(t_uidx - t_dup));
+      atomicAdd(&g_rf_prof[10], (unsigned long long)(t_loads - t_uidx));
+      atomicAdd(&g_rf_prof[11], (unsigned long long)(t_greedy - t_loads));
+      atomicAdd(&g_rf_prof[12], (unsigned long long)(t_end - t_greedy));
+      atomicAdd(&g_rf_prof[13], (unsigned long long)W);
+    }
   }
   __syncwarp();
   return inserted;
@@ -806,15 +892,17 @@ int rf_launch_simulate(RfArgs& a, cudaStream_t st) {
   if (e != cudaSuccess) return (int)e;
   static const bool prof = kRfProf && getenv("SB_RF_PROF") != nullptr;
   if (prof) {
-    unsigned long long z[8] = {0};
+    unsigned long long z[16] = {0};
     cudaMemcpyToSymbol(g_rf_prof, z, sizeof(z));
   }
   rf_simulate_kernel<<<(unsigned)((a.ngroups + kSimWarps - 1) / kSimWarps), 32 * kSimWarps,
                        smem * kSimWarps, st>>>(a);
   if (prof) {
-    unsigned long long z[8];
+    unsigned long long z[16];
     cudaDeviceSynchronize();
     cudaMemcpyFromSymbol(z, g_rf_prof, sizeof(z));
+    fprintf(stderr, "rf_sim full-row phases (cycles): dup test %llu | U index %llu | loads %llu | greedy %llu | write back %llu | sum W %llu\n",
+            z[8], z[9], z[10], z[11], z[12], z[13]);
     fprintf(stderr, "rf_sim cycles: total %llu | nonfull %llu x%llu | full %llu x%llu | dup %llu x%llu | sources %llu\n",
             z[6], z[0], z[1], z[2], z[3], z[4], z[5], z[7]);
   }
