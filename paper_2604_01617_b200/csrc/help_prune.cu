@@ -30,9 +30,13 @@
 namespace sb {
 
 constexpr int kPruneThreads = 256;
+#ifndef PRUNE_F64_THREADS
+#define PRUNE_F64_THREADS 256
+#endif
+constexpr int kPruneThreadsF64 = PRUNE_F64_THREADS;  // fp64 kernel: tiles of a full row per pass
 constexpr int kPT = 4;
 
-__global__ void __launch_bounds__(kPruneThreads) prune_bits_kernel(PruneArgs a) {
+__global__ void __launch_bounds__(kPruneThreadsF64) prune_bits_kernel(PruneArgs a) {
   extern __shared__ __align__(16) char smem_raw[];
   const int cpad = a.cpad;
   // the float tile goes first: its float4 reads need 16-byte alignment
@@ -93,8 +97,8 @@ __global__ void __launch_bounds__(kPruneThreads) prune_bits_kernel(PruneArgs a) 
   // dot products on lower-triangle 4 x 4 tiles (row block tb >= column block ub)
   const int nb = (cnt + kPT - 1) / kPT;
   const int ntiles = nb * (nb + 1) / 2;
-  for (int pass = 0; pass * kPruneThreads < ntiles; ++pass) {
-    const int ti = pass * kPruneThreads + tid;
+  for (int pass = 0; pass * kPruneThreadsF64 < ntiles; ++pass) {
+    const int ti = pass * kPruneThreadsF64 + tid;
     const bool have = ti < ntiles;
     int tb = 0, ub = 0;
     if (have) {
@@ -315,7 +319,7 @@ int launch_prune_bits(const PruneArgs& a, size_t smem, cudaStream_t st) {
   cudaError_t e = cudaFuncSetAttribute(prune_bits_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)smem);
   if (e != cudaSuccess) return (int)e;
-  prune_bits_kernel<<<(unsigned)a.n, kPruneThreads, smem, st>>>(a);
+  prune_bits_kernel<<<(unsigned)a.n, kPruneThreadsF64, smem, st>>>(a);
   return (int)cudaGetLastError();
 }
 int launch_prune_scan(const PruneArgs& a, cudaStream_t st) {
