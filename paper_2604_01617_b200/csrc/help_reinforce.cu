@@ -475,13 +475,16 @@ SB_DEV int warp_try_insert(RfArgs& a, const SimSmem& S, int32_t j, int o, int32_
         const int t = 32 * c0 + tb;
         const int ut = S.mu[t];
         const uint32_t* rr = S.Rs + t * W;
-        bool hit = false;
+        // (all of the row's words loaded at once, no short circuit: a chain of conditional
+        // loads cost four shared-memory latencies per entry)
+        uint32_t hit = 0u;
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
           const int w = lane + 32 * k;
-          if (w < W) hit = hit || (rr[w] & km[k]) != 0u;
+          const uint32_t rv = w < W ? rr[w] : 0u;
+          hit |= rv & km[k];
         }
-        const bool red = __any_sync(kFull, hit);
+        const bool red = __any_sync(kFull, hit != 0u);
         if (!(red && ((cond[c0] >> tb) & 1u))) {
           keep[c0] |= 1u << tb;
 #pragma unroll
