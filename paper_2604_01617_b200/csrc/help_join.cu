@@ -261,9 +261,12 @@ __global__ void __launch_bounds__(kJoinThreads, U8 ? 3 : 2) join_emit_kernel(Joi
           __syncthreads();  // its half stage may be overwritten (by chunk c + 2)
         }
       }
-      // pushes (warp-uniform loop; lanes without a tile contribute nothing)
-#pragma unroll
-      for (int u = 0; u < kJT; ++u)
+      // pushes (warp-uniform loop; lanes without a tile contribute nothing).  The tile's rows
+      // go through one copy of the push code (the accumulator rows rotate through acc[0], so
+      // the indices stay static): a quarter of the instructions of the fully unrolled form,
+      // which stalled on instruction fetch (16% of the u8 kernel's samples).
+#pragma unroll 1
+      for (int u = 0; u < kJT; ++u) {
 #pragma unroll
         for (int w = 0; w < kJT; ++w) {
           const int x = rb * kJT + u, y = cb * kJT + w;
@@ -278,7 +281,7 @@ __global__ void __launch_bounds__(kJoinThreads, U8 ? 3 : 2) join_emit_kernel(Joi
             double sa = 0.0;
             for (int t = 0; t < a.l; ++t)
               sa = dadd(sa, fabs(dsub((double)s.slot_attr[x * a.l + t], (double)s.slot_attr[y * a.l + t])));
-            float d = __double2float_rn(auto_finish(acc[u][w], sa, a.inv_alpha));
+            float d = __double2float_rn(auto_finish(acc[0][w], sa, a.inv_alpha));
             k1 = row_key(d, (uint32_t)k);  // into row j
             k2 = row_key(d, (uint32_t)j);  // into row k
             p1 = k1 < s.thr[x];
@@ -286,6 +289,11 @@ __global__ void __launch_bounds__(kJoinThreads, U8 ? 3 : 2) join_emit_kernel(Joi
           }
           emit2(a, em, p1, (uint32_t)j, k1, p2, (uint32_t)k, k2);
         }
+#pragma unroll
+        for (int r = 0; r + 1 < kJT; ++r)
+#pragma unroll
+          for (int w = 0; w < kJT; ++w) acc[r][w] = acc[r + 1][w];
+      }
     }
   }
   if (same) atomicAdd(a.same_pairs, (unsigned long long)same);
